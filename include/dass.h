@@ -1,0 +1,316 @@
+/*
+ * dass.h — C-ABI of libdass.so, the B200 (sm_100a) hot path of DASS
+ * (arXiv 2411.14847): the per-timestep tile-based differentiable 3D Gaussian
+ * Splatting rasterizer every DASS stage optimises through, the masked
+ * per-Gaussian shift, and the error map of error-guided densification.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (with its section/eq.);
+ * "S:n" = SPEC.md line n; "A.." = a reading listed in DESIGN.md §Readings
+ * (SURVEY.md §8(c) table).  Paper passages defining the operations:
+ *   Eq. 5-8  (supplement §A.1): Gaussian, Σ = R S Sᵀ Rᵀ, EWA
+ *            Σ_2D = J W Σ Wᵀ Jᵀ, front-to-back blending C = Σ c_i α_i Π(1-α_j).
+ *   §3.3: shift p' = p + μ, q' = norm(q) × norm(σ).
+ *   §3.4 + Alg. 1: error maps E^c, D_err^c,
+ *            S_err; historical view-space positional gradient ∇p̄.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions shared by every export
+ * ---------------------------------------------------------------------------
+ *  - Every pointer argument named *_dev / every array argument is a DEVICE
+ *    pointer owned by the caller (normally a torch tensor's data_ptr()),
+ *    16-byte aligned where the element is float4.  `const dass_camera*` and
+ *    `const float bg[3]` are HOST pointers read during the call.
+ *  - `stream` is a cudaStream_t passed as void*; all work is enqueued on it
+ *    asynchronously.  Only dass_bin_sort in "host mode" synchronises.
+ *  - The library never allocates device memory, keeps no mutable global
+ *    state except a relaxed atomic launch counter (dass_kernel_launches) and
+ *    a thread-local last-error string; calls on distinct streams are
+ *    thread-safe.  Scratch memory is a caller-provided workspace whose size
+ *    the matching *_workspace query returns.
+ *  - Per-pixel outputs are OVERWRITTEN.  Per-Gaussian gradients and
+ *    statistics are ACCUMULATED (+=): the caller zeroes them once per step so
+ *    multi-view sums on one GPU cost nothing (A28).
+ *  - Return value: a dass_status.  On error nothing has been enqueued (argument
+ *    validation happens before any launch) unless the status is DASS_ERR_CUDA.
+ *
+ * Data layout in HBM (field-SoA of 16-byte records; one coalesced 128-bit load
+ * per field per thread):
+ *  Gaussian parameters, N = n:
+ *    pos_opa  float4[N]   x, y, z (world), opacity o ∈ (0,1) (activated, A16)
+ *    scale    float4[N]   sx, sy, sz > 0 (activated), w ignored
+ *    rot      float4[N]   quaternion w, x, y, z (real first, raw, A15)
+ *    sh       float4[K4][N]  coefficient PLANES: the 3·(d+1)² SH coefficients
+ *             of Gaussian i, ordered coefficient-major/channel-minor
+ *             (c[k*3+ch]), are split into K4 = ceil(3(d+1)²/4) float4 chunks;
+ *             chunk j of every Gaussian forms plane j (sh[j*N + i]).  Padding
+ *             floats are ignored on input and written 0 in gradients.
+ *    Gradients use the identical layout (g_pos_opa.w = dL/do).
+ *  Per-view projected records (outputs of dass_project):
+ *    xy_depth  float4[N]  u, v (pixels), z (camera-frame depth), 0
+ *    conic_opa float4[N]  A, B, C (inverse 2D covariance), o_eff
+ *    rgb       float4[N]  r, g, b (clamped ≥ 0), clamp bits (float 0..7,
+ *                         bit ch set when channel ch was clamped)
+ *    box       uint32[2N] per Gaussian {x0 | x1<<16, y0 | y1<<16}; a culled
+ *                         Gaussian has x0 = 1 > x1 = 0 (and y likewise)
+ *    tiles_touched uint32[N]
+ *  Images: float32 planar [3][H][W] (PyTorch CHW).  Pixel (X, Y) has its
+ *  centre at (X, Y) (A19); row-major pixel index Y·W + X.
+ *  Tiles: 16×16 pixels, tile id = ty·tiles_x + tx, tiles_x = ceil(W/16),
+ *  tiles_y = ceil(H/16) (A04).
+ */
+#ifndef DASS_H_
+#define DASS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DASS_TILE 16
+#define DASS_ABI_VERSION 1
+
+typedef enum dass_status {
+  DASS_OK = 0,
+  DASS_ERR_INVALID_ARG = 1, /* usage error: bad size, null required pointer */
+  DASS_ERR_DATA = 2,        /* data error: inputs inconsistent */
+  DASS_ERR_NUMERICAL = 3,   /* reserved: non-finite scan (validation mode) */
+  DASS_ERR_CAPACITY = 4,    /* pair capacity too small (bin_sort host mode) */
+  DASS_ERR_CUDA = 5         /* a CUDA runtime call failed */
+} dass_status;
+
+/*
+ * Camera (D03; Alg. 1 input).
+ *  - width, height ∈ [1, 65535]; fx, fy > 0.
+ *  - viewmat: world→camera [R|t], row-major 3×4: t_cam = R·p + t.  R must be
+ *    orthonormal (not checked).  Camera centre (SH direction origin) is −Rᵀt.
+ *  - Pinhole: u = fx·t_x/t_z + cx, v = fy·t_y/t_z + cy, pixel centres at
+ *    integers (A19): (W−1)/2 is the image centre.
+ *  - near_plane: Gaussians with !(t_z > near_plane) are culled (A09).
+ *  - full_proj: Alg. 1's "full projection matrix T", row-major 4×4 in
+ *    the row-vector convention P_hom = [p, 1]·T; column 3 is the
+ *    homogeneous coordinate.  Used only by dass_error_map.
+ */
+typedef struct dass_camera {
+  int32_t width;
+  int32_t height;
+  float fx, fy, cx, cy;
+  float viewmat[12];
+  float near_plane;
+  float full_proj[16];
+} dass_camera;
+
+/* Human-readable text for a status; never NULL. */
+const char* dass_status_string(int status);
+/* Thread-local message describing the last non-OK status of this thread. */
+const char* dass_last_error(void);
+/* DASS_ABI_VERSION of the loaded library. */
+int dass_abi_version(void);
+/* Total number of kernels this process has launched through libdass
+ * (relaxed atomic; diagnostic for bench.py's gpu_launches). */
+uint64_t dass_kernel_launches(void);
+
+/* ---------------------------------------------------------------------------
+ * dass_apply_shift — masked per-Gaussian shift (§3.3; A24, A25)
+ *   where dyn_mask[i] != 0:  p' = p + μ_i (xyz), o' = o,
+ *                            q' = n(q) ⊗ n(σ_i) (Hamilton product, q on the
+ *                            left; n(x) = x/‖x‖; ‖σ‖ < 1e-8 → σ := identity)
+ *   where dyn_mask[i] == 0:  p', q' = exact copy.
+ * mu, sigma: float4[n] (mu.w ignored; sigma = w,x,y,z).  dyn_mask: uint8[n],
+ * nullable = all ones.  In-place (pos_opa_out == pos_opa, rot_out == rot) OK.
+ * INVALID_ARG: n < 0, or n > 0 with a null required pointer.  n = 0 → OK.
+ * ------------------------------------------------------------------------- */
+int dass_apply_shift(int32_t n, const float* pos_opa, const float* rot,
+                     const float* mu, const float* sigma,
+                     const uint8_t* dyn_mask, float* pos_opa_out,
+                     float* rot_out, void* stream);
+
+/* dass_apply_shift_bwd — reverse of dass_apply_shift for the trained offsets
+ * (the shift stage trains only the deformation outputs):
+ *   g_mu    += mask · dL/dp'                         (xyz; w untouched)
+ *   g_sigma += mask · (dL/dn(σ) − n(σ)(n(σ)·dL/dn(σ)))/‖σ‖ with
+ *              dL/dn(σ) = L(n(q))ᵀ dL/dq' (L(a) = left-multiplication matrix);
+ *              zero when ‖σ‖ < 1e-8.
+ * rot is the PRE-shift quaternion.  g_pos_out/g_rot_out: gradients w.r.t. the
+ * shifted pos_opa'/rot' (float4[n]).  g_mu, g_sigma nullable. */
+int dass_apply_shift_bwd(int32_t n, const float* rot, const float* sigma,
+                         const uint8_t* dyn_mask, const float* g_pos_out,
+                         const float* g_rot_out, float* g_mu, float* g_sigma,
+                         void* stream);
+
+/* ---------------------------------------------------------------------------
+ * dass_project — EWA projection + SH colour, one view (Eqs. 5-7, P:336-347;
+ * colour P:351, A14).  Per Gaussian i:
+ *  o_eff = keep_mask ? (keep_mask[i] ? o : 0) : o;  s_eff likewise (Eq. 1,
+ *  P:94-95; a Quant = 0 Gaussian is culled by the opacity cull, A10).
+ *
+ *  KEY CHAIN — computed in IEEE fp32, every operation individually rounded
+ *  (no FMA contraction), IEEE division and square root, in EXACTLY this order
+ *  (a+b+c means ((a+b)+c); this is the bit-exact contract, hard part 1):
+ *   1. t_a = ((V[a][0]·x + V[a][1]·y) + V[a][2]·z) + V[a][3], a = 0..2.
+ *   2. cull unless t_z > near_plane.
+ *   3. nq = sqrt(((w·w + x·x) + y·y) + z·z) of rot; cull unless nq > 0 and
+ *      nq finite; q̂ = (w/nq, x/nq, y/nq, z/nq).
+ *   4. R(q̂): with products xx=x·x, yy, zz, xy, xz, yz, wx, wy, wz:
+ *      R00 = 1 − 2·(yy+zz), R01 = 2·(xy−wz), R02 = 2·(xz+wy),
+ *      R10 = 2·(xy+wz), R11 = 1 − 2·(xx+zz), R12 = 2·(yz−wx),
+ *      R20 = 2·(xz−wy), R21 = 2·(yz+wx), R22 = 1 − 2·(xx+yy).
+ *   5. m_ak = R_ak·s_k;  Σ_ab = (m_a0·m_b0 + m_a1·m_b1) + m_a2·m_b2 (a ≤ b).
+ *   6. lx = (1.3·W)/(2·fx), ly = (1.3·H)/(2·fy);
+ *      x̃ = min(lx, max(−lx, t_x/t_z))·t_z, ỹ likewise;
+ *      J00 = fx/t_z, J02 = −((fx·x̃)/(t_z·t_z)), J11 = fy/t_z,
+ *      J12 = −((fy·ỹ)/(t_z·t_z)).
+ *   7. M0k = J00·V[0][k] + J02·V[2][k];  M1k = J11·V[1][k] + J12·V[2][k].
+ *      P_ak = (M_a0·Σ_0k + M_a1·Σ_1k) + M_a2·Σ_2k.
+ *      a = ((P_00·M_00 + P_01·M_01) + P_02·M_02) + 0.3,
+ *      b =  (P_00·M_10 + P_01·M_11) + P_02·M_12,
+ *      c = ((P_10·M_10 + P_11·M_11) + P_12·M_12) + 0.3      (A07)
+ *   8. det = a·c − b·b; cull unless det > 0.
+ *   9. mid = 0.5·(a + c); λ = mid + sqrt(max(0.1, mid·mid − det));
+ *      r = ceil(3·sqrt(λ))                                    (A06)
+ *  10. u = (fx·t_x)/t_z + cx,  v = (fy·t_y)/t_z + cy  (unclamped);
+ *      cull unless u, v, λ finite.
+ *  11. x0 = max(0, ceil(u − r)), x1 = min(W − 1, floor(u + r)), y likewise
+ *      (clamped in float before conversion to int); visible iff x0 ≤ x1,
+ *      y0 ≤ y1 and o_eff ≥ 1/255 (A05, A10);
+ *      tiles_touched = (x1/16 − x0/16 + 1)·(y1/16 − y0/16 + 1).
+ *  The conic is (A, B, C) = (c/det, −b/det, a/det).  Colour (fast math
+ *  allowed): d = (p − c_cam)/‖p − c_cam‖, col = Σ_k Y_k(d)·sh_k + 0.5 with the
+ *  real SH basis of degree ≤ 3 listed in DESIGN.md (A14); a channel < 0 sets
+ *  its clamp bit and is clamped to 0.
+ * Culled Gaussians: tiles_touched = 0, box = {1, 1} (x0 > x1), other records
+ * zero.  Degenerate q is culled, not an error (A15).
+ * INVALID_ARG: bad camera, n < 0, sh_degree ∉ [0,3], null required pointer.
+ * ------------------------------------------------------------------------- */
+int dass_project(const dass_camera* cam, int32_t n, int32_t sh_degree,
+                 const float* pos_opa, const float* scale, const float* rot,
+                 const float* sh, const uint8_t* keep_mask, float* xy_depth,
+                 float* conic_opa, float* rgb, uint32_t* box,
+                 uint32_t* tiles_touched, void* stream);
+
+/* dass_project_views — the same as V calls of dass_project (one per camera),
+ * in one launch that reads the parameters once for all V views (a2, "multi-
+ * view batched").  Record arrays are [V][N] concatenations of the per-view
+ * layout above (view v's xy_depth at xy_depth + 4·v·N, etc.). */
+int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n,
+                       int32_t sh_degree, const float* pos_opa,
+                       const float* scale, const float* rot, const float* sh,
+                       const uint8_t* keep_mask, float* xy_depth,
+                       float* conic_opa, float* rgb, uint32_t* box,
+                       uint32_t* tiles_touched, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * dass_bin_sort — tile binning + sort + per-tile ranges (a3-a5; P:29
+ * "tile-based"; A03, A04).  For every visible Gaussian i and every tile
+ * (tx, ty) of its pixel box (tx = x>>4 over [x0>>4, x1>>4], same for y) emit
+ * the pair key = (tile_id << 32) | bits_u32(z_i), value = i.  Output: the
+ * pairs in ascending (key, i) order — i.e. lexicographic (tile, depth bits,
+ * Gaussian index) — and ranges[t] = [first, one-past-last) of tile t in that
+ * order, [0, 0) for an empty tile.  Integer work: bit-exact by contract.
+ *
+ *  ws, ws_bytes: workspace of at least dass_bin_sort_workspace(n, num_tiles,
+ *    pair_capacity) bytes.
+ *  sorted_keys: uint64[pair_capacity], nullable (skips writing the keys).
+ *  sorted_ids: uint32[pair_capacity].  tile_ranges: uint32[2·num_tiles].
+ *  num_pairs_dev: uint32[2] device: [0] = K (total pairs, even on overflow),
+ *    [1] = 1 if K > pair_capacity (then every range is [0,0)), else 0.
+ *  num_pairs_host: nullable.  Non-null = HOST MODE: the call synchronises the
+ *    stream once, stores K, and returns DASS_ERR_CAPACITY if K > capacity.
+ *    Null = GRAPH MODE: no synchronisation (capturable in a CUDA graph); the
+ *    caller reads num_pairs_dev later.
+ * Requires pair_capacity < 2^32 and n < 2^31.
+ * ------------------------------------------------------------------------- */
+int dass_bin_sort_workspace(int32_t n, int32_t num_tiles,
+                            int64_t pair_capacity, size_t* bytes);
+int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth,
+                  const uint32_t* box, const uint32_t* tiles_touched,
+                  void* ws, size_t ws_bytes, int64_t pair_capacity,
+                  uint64_t* sorted_keys, uint32_t* sorted_ids,
+                  uint32_t* tile_ranges, uint32_t* num_pairs_dev,
+                  int64_t* num_pairs_host, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * dass_render_fwd — front-to-back compositing (Eq. 8; A01, A05,
+ * A11-A13).  For pixel (X, Y), over the tile's sorted list, skipping entries
+ * whose box does not contain the pixel:
+ *   dx = u − X, dy = v − Y; power = −0.5·(A·dx² + C·dy²) − B·dx·dy;
+ *   skip if power > 0; α = min(0.99, o·exp(power)); skip if α < 1/255;
+ *   if T·(1 − α) < 1e-4 stop (the entry is NOT added);
+ *   otherwise C += rgb·α·T, T ← T·(1 − α).      (T starts at 1)
+ * out_img[ch] = C + T·bg[ch] (bg: host float[3], nullable = black);
+ * out_T = final T; out_last = one past the sorted-list index of the last
+ * accepted entry (the range start if none).  Both are needed by the backward.
+ * ------------------------------------------------------------------------- */
+int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges,
+                    const uint32_t* sorted_ids, const float* xy_depth,
+                    const float* conic_opa, const float* rgb,
+                    const uint32_t* box, const float* bg, float* out_img,
+                    float* out_T, uint32_t* out_last, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * dass_render_bwd — reverse-mode gradient of dass_project + dass_render_fwd
+ * for one view (a7, a8; reverse of Eqs. 5-8; P:159 for ∇p̄).  The exact
+ * derivative of the forward holding the accepted set and clamp states fixed
+ * (A17, A18): α clamped at 0.99 → ∂α/∂(o, G) = 0; clamped colour channels get
+ * no gradient; J's clamp differentiated exactly (A08).
+ * Gradients are w.r.t. the ACTIVATED scale and opacity and the RAW
+ * quaternion (A16), accumulated (+=) into g_* (nullable: a null output skips
+ * its work), summed over pixels and views (A27).
+ *   gradstat_sum[i] += ‖(dL/du·W/2, dL/dv·H/2)‖₂ and gradstat_cnt[i] += 1 for
+ *   every Gaussian visible in this view (A23).  Both nullable.
+ * The caller must pass the SAME records and fwd outputs; the ABI
+ * cannot check this.  dL_dimg: float [3][H][W].  ws: dass_render_bwd_workspace.
+ * ------------------------------------------------------------------------- */
+int dass_render_bwd_workspace(int32_t n, size_t* bytes);
+int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree,
+                    const float* pos_opa, const float* scale, const float* rot,
+                    const float* sh, const uint8_t* keep_mask,
+                    const uint32_t* tile_ranges, const uint32_t* sorted_ids,
+                    const float* xy_depth, const float* conic_opa,
+                    const float* rgb, const uint32_t* box, const float* bg,
+                    const float* out_T, const uint32_t* out_last,
+                    const float* dL_dimg, void* ws, size_t ws_bytes,
+                    float* g_pos_opa, float* g_scale, float* g_rot,
+                    float* g_sh, float* gradstat_sum, uint32_t* gradstat_cnt,
+                    void* stream);
+
+/* ---------------------------------------------------------------------------
+ * dass_error_map — error map, binarisation and Alg. 1 (§3.4 P:164-165, P:174;
+ * Alg. 1 P:403-415 with the garble fixed, A20-A22).
+ *   E(X,Y) = (1/3)·Σ_ch |rendered − gt|  → err (float [H][W], nullable)
+ *   D = E > gamma_err (strict)           → dmask (uint32[ceil(HW/32)],
+ *       bit (p & 31) of word p >> 5 for pixel p = Y·W + X; nullable)
+ *   For n < n_base (𝒢^base only): P_hom = [p_n, 1]·T (T = full_proj);
+ *   x_norm = P_hom.x/P_hom.w, y_norm = P_hom.y/P_hom.w;
+ *   x_n = round(0.5·((x_norm + 1)·W − 1)), y_n = round(0.5·((y_norm + 1)·H − 1))
+ *   (round half away from zero); skipped if P_hom.w ≤ near_plane or the pixel
+ *   is outside the image; otherwise s_err[n] |= D[y_n][x_n]  (uint8, nullable).
+ * INVALID_ARG: gamma_err ≤ 0, bad camera.  DATA: rendered or gt null.
+ * ------------------------------------------------------------------------- */
+int dass_error_map(const dass_camera* cam, const float* rendered,
+                   const float* gt, float gamma_err, float* err,
+                   uint32_t* dmask, int32_t n_base, const float* pos_opa,
+                   uint8_t* s_err, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * dass_render_stats — scene statistics of one rendered view,
+ * diagnostic, not on the timed path.  counters: uint64[8] device, overwritten:
+ *   [0] P_fwd   Σ_px entries whose box contains the pixel, visited by the
+ *               forward up to and including its terminating entry
+ *   [1] P_bwd   Σ_px entries with index < out_last whose box contains the pixel
+ *   [2] accepted Σ_px accepted (composited) entries
+ *   [3] pixels that terminated early (T·(1−α) < 1e-4 reached)
+ *   [4] Σ_tiles list length, [5] max list length, [6] non-empty tiles,
+ *   [7] Σ_px entries in the pixel's tile list up to out_last (box-unfiltered)
+ * ------------------------------------------------------------------------- */
+int dass_render_stats(const dass_camera* cam, const uint32_t* tile_ranges,
+                      const uint32_t* sorted_ids, const float* xy_depth,
+                      const float* conic_opa, const uint32_t* box,
+                      const float* out_T, const uint32_t* out_last,
+                      uint64_t* counters, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DASS_H_ */

@@ -1,0 +1,193 @@
+"""ctypes front end of the CPU oracle (oracle/oracle.cpp).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs — never by the product package
+`paper_2411_14847_b200`.  It shares no code with the CUDA path; its only shared
+dependency is the seeded input generator `paper_2411_14847_b200/synth.py`
+(random numbers and camera matrices, none of the method's arithmetic).
+
+All results are float64 NumPy arrays (the oracle computes in double; the only
+float arithmetic is the fp32 key replica of include/dass.h's KEY CHAIN).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain g++, -ffp-contract=off so the fp32 replica
+    rounds every operation once; OpenMP for the O(Σ box area) scatter form)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fopenmp", "-fPIC",
+               "-shared", _SRC, "-o", _LIB + ".tmp"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = C.CDLL(_LIB)
+        _lib.oracle_bin_sort.restype = C.c_int64
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def threads() -> int:
+    return lib().oracle_threads()
+
+
+def _cam(cam):
+    s = cam.to_struct() if hasattr(cam, "to_struct") else cam
+    return np.ascontiguousarray(s).reshape(1)
+
+
+def shift(pos_opa, rot, mu, sigma, mask=None):
+    n = pos_opa.shape[0]
+    po = np.zeros((n, 4)); ro = np.zeros((n, 4))
+    m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+    lib().oracle_shift(n, _p(_f32(pos_opa)), _p(_f32(rot)), _p(_f32(mu)), _p(_f32(sigma)),
+                       _p(m), _p(po), _p(ro))
+    return po, ro
+
+
+def shift_bwd(rot, sigma, mask, g_pos_out, g_rot_out):
+    n = rot.shape[0]
+    gm = np.zeros((n, 4)); gs = np.zeros((n, 4))
+    m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+    lib().oracle_shift_bwd(n, _p(_f32(rot)), _p(_f32(sigma)), _p(m),
+                           _p(np.ascontiguousarray(g_pos_out, np.float64)),
+                           _p(np.ascontiguousarray(g_rot_out, np.float64)), _p(gm), _p(gs))
+    return gm, gs
+
+
+def project(cam, scene, keep=None):
+    """O2 for one view.  Returns a dict of per-Gaussian arrays."""
+    n = scene.n
+    out = dict(uvz=np.zeros((n, 3)), conic=np.zeros((n, 3)), opa=np.zeros(n),
+               rgb=np.zeros((n, 3)), clampbits=np.zeros(n, np.int32), zf=np.zeros(n, np.float32),
+               zbits=np.zeros(n, np.uint32), box=np.zeros((n, 4), np.int32),
+               tiles=np.zeros(n, np.uint32), visible=np.zeros(n, np.uint8))
+    k = None if keep is None else np.ascontiguousarray(keep, np.uint8)
+    c = _cam(cam)
+    lib().oracle_project(_p(c), n, scene.sh_degree, _p(_f32(scene.pos_opa)), _p(_f32(scene.scale)),
+                         _p(_f32(scene.rot)), _p(_f32(scene.sh)), _p(k), _p(out["uvz"]),
+                         _p(out["conic"]), _p(out["opa"]), _p(out["rgb"]), _p(out["clampbits"]),
+                         _p(out["zf"]), _p(out["zbits"]), _p(out["box"]), _p(out["tiles"]),
+                         _p(out["visible"]))
+    return out
+
+
+def cov2d(cam, pos_opa, scale, rot):
+    n = pos_opa.shape[0]
+    out = np.zeros((n, 4))
+    c = _cam(cam)
+    lib().oracle_cov2d(_p(c), n, _p(_f32(pos_opa)), _p(_f32(scale)), _p(_f32(rot)), _p(out))
+    return out  # a, b, c, det
+
+
+def rotmat_cov(q, s):
+    R = np.zeros(9); S = np.zeros(9)
+    rc = lib().oracle_rotmat_cov(_p(_f32(q)), _p(_f32(s)), _p(R), _p(S))
+    if rc != 0:
+        raise ValueError("degenerate")
+    return R.reshape(3, 3), S.reshape(3, 3)
+
+
+def sh_basis(deg, dirs):
+    dirs = np.ascontiguousarray(dirs, np.float64)
+    Y = np.zeros((dirs.shape[0], 16))
+    lib().oracle_sh_basis(deg, dirs.shape[0], _p(dirs), _p(Y))
+    return Y
+
+
+def bin_sort(cam, proj):
+    """O3: brute-force pairs sorted by (key, id) and the per-tile ranges."""
+    n = proj["visible"].shape[0]
+    c = _cam(cam)
+    vis = np.ascontiguousarray(proj["visible"], np.uint8)
+    zb = np.ascontiguousarray(proj["zbits"], np.uint32)
+    box = np.ascontiguousarray(proj["box"], np.int32)
+    K = lib().oracle_bin_sort(_p(c), n, _p(vis), _p(zb), _p(box), C.c_int64(0), None, None, None)
+    ntiles = ((int(c["width"][0]) + 15) // 16) * ((int(c["height"][0]) + 15) // 16)
+    keys = np.zeros(max(K, 1), np.uint64); ids = np.zeros(max(K, 1), np.uint32)
+    ranges = np.zeros((ntiles, 2), np.uint32)
+    lib().oracle_bin_sort(_p(c), n, _p(vis), _p(zb), _p(box), C.c_int64(K), _p(keys), _p(ids),
+                          _p(ranges))
+    return keys[:K], ids[:K], ranges
+
+
+def _tie(tie_eps):
+    return None if tie_eps is None else np.ascontiguousarray(tie_eps, np.float64)
+
+
+def render(cam, scene, keep=None, bg=None, mode="scatter", tie_eps=None):
+    """O4: returns dict(img[3,H,W], T[H,W], nacc, last_id, tie, term, pfwd, pbwd)."""
+    c = _cam(cam)
+    H, W = int(c["height"][0]), int(c["width"][0])
+    o = dict(img=np.zeros((3, H, W)), T=np.zeros((H, W)), nacc=np.zeros((H, W), np.int32),
+             last_id=np.zeros((H, W), np.int32), tie=np.zeros((H, W), np.uint8),
+             term=np.zeros((H, W), np.uint8), pfwd=np.zeros((H, W), np.int64),
+             pbwd=np.zeros((H, W), np.int64))
+    k = None if keep is None else np.ascontiguousarray(keep, np.uint8)
+    b = None if bg is None else np.ascontiguousarray(bg, np.float32)
+    lib().oracle_render(_p(c), scene.n, scene.sh_degree, _p(_f32(scene.pos_opa)),
+                        _p(_f32(scene.scale)), _p(_f32(scene.rot)), _p(_f32(scene.sh)), _p(k),
+                        _p(b), 0 if mode == "literal" else 1, _p(_tie(tie_eps)), _p(o["img"]),
+                        _p(o["T"]), _p(o["nacc"]), _p(o["last_id"]), _p(o["tie"]), _p(o["term"]),
+                        _p(o["pfwd"]), _p(o["pbwd"]))
+    return o
+
+
+def render_bwd(cam, scene, dL_dimg, keep=None, bg=None, mode="scatter", tie_eps=None):
+    """O5+O6: gradients of sum(dL_dimg * render) w.r.t. all parameters."""
+    c = _cam(cam)
+    H, W = int(c["height"][0]), int(c["width"][0])
+    n = scene.n
+    nc = (scene.sh_degree + 1) ** 2
+    o = dict(g_pos_opa=np.zeros((n, 4)), g_scale=np.zeros((n, 4)), g_rot=np.zeros((n, 4)),
+             g_sh=np.zeros((n, nc, 3)), g2d=np.zeros((n, 9)), gradstat_sum=np.zeros(n),
+             gradstat_cnt=np.zeros(n, np.int32), gtie=np.zeros(n, np.uint8),
+             img=np.zeros((3, H, W)), T=np.zeros((H, W)))
+    k = None if keep is None else np.ascontiguousarray(keep, np.uint8)
+    b = None if bg is None else np.ascontiguousarray(bg, np.float32)
+    lib().oracle_render_bwd(_p(c), n, scene.sh_degree, _p(_f32(scene.pos_opa)),
+                            _p(_f32(scene.scale)), _p(_f32(scene.rot)), _p(_f32(scene.sh)), _p(k),
+                            _p(b), _p(_f32(dL_dimg)), 0 if mode == "literal" else 1,
+                            _p(_tie(tie_eps)), _p(o["g_pos_opa"]), _p(o["g_scale"]),
+                            _p(o["g_rot"]), _p(o["g_sh"]), _p(o["g2d"]), _p(o["gradstat_sum"]),
+                            _p(o["gradstat_cnt"]), _p(o["gtie"]), _p(o["img"]), _p(o["T"]))
+    return o
+
+
+def error_map(cam, rendered, gt, gamma, pos_opa, n_base=None, s_err=None):
+    c = _cam(cam)
+    H, W = int(c["height"][0]), int(c["width"][0])
+    n = pos_opa.shape[0]
+    nb = n if n_base is None else n_base
+    o = dict(err=np.zeros((H, W)), D=np.zeros((H, W), np.uint8),
+             s_err=np.zeros(n, np.uint8) if s_err is None else np.array(s_err, np.uint8),
+             xy=np.zeros((n, 2), np.int32), tie_g=np.zeros(n, np.uint8),
+             tie_px=np.zeros((H, W), np.uint8))
+    lib().oracle_error_map(_p(c), _p(_f32(rendered)), _p(_f32(gt)), C.c_double(gamma), nb,
+                           _p(_f32(pos_opa)), _p(o["err"]), _p(o["D"]), _p(o["s_err"]),
+                           _p(o["xy"]), _p(o["tie_g"]), _p(o["tie_px"]))
+    return o
