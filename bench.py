@@ -1,0 +1,419 @@
+"""bench.py — fwd+bwd throughput of the DASS hot path on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], the metric's "300k Gaussians, 1352x1014,
+1/2/4/8 B200"): an N3DV-shaped timestep — 20 views at 1352×1014, 300k
+Gaussians, SH degree 3, 30% dynamic.  One STEP = one shift-stage iteration
+over all 20 views:
+    dass_apply_shift → dass_project_views → per view (dass_bin_sort →
+    dass_render_fwd → dass_render_bwd) → dass_apply_shift_bwd
+    [N>1: one NCCL all_reduce(SUM) of the flat gradient buffer]
+with a fixed seeded dL/dC per view (the loss is outside the path).
+Views are sharded across ranks (strong scaling: the 20-view batch is fixed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd views/sec (Mpix/s) at 300k Gaussians, 1352x1014, 1/2/4/8 B200"
+WORKLOAD = ("C3: N3DV-shaped timestep, 20 views 1352x1014, 300k Gaussians SH3, 30% dynamic "
+            "masked shift; step = one shift iteration (shift + fwd+bwd over all views)")
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SM_COUNT = 148
+FP32_LANES = 128
+
+# Algorithmic FP32 work per unit of render_bwd raster:
+# an accepted (pixel, entry) evaluation and an in-box but rejected one.
+FLOP_BWD_ACCEPTED = 96
+FLOP_BWD_REJECTED = 19
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=300_000)
+    p.add_argument("--views", type=int, default=20)
+    p.add_argument("--capacity", type=int, default=1 << 24)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-sample-views", type=int, default=2)
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def shard(num_views, rank, world):
+    """Contiguous view blocks, sizes differ by at most one."""
+    base, extra = divmod(num_views, world)
+    start = rank * base + min(rank, extra)
+    return list(range(start, start + base + (1 if rank < extra else 0)))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = [r.split(",") for r in (self.out or "").strip().splitlines() if r.count(",") >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]),
+                "power_w_max": max(float(r[2]) for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def peaks():
+    try:
+        return json.load(open(PEAKS_PATH)), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# --------------------------------------------------------------- our arm ----
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_14847_b200 import dass, synth
+    from paper_2411_14847_b200.pipeline import DeviceScene, Grads, Raster, ViewRecords
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cams, scene = synth.c3(n=args.n, num_views=args.views)
+    mu, sigma = synth.shift_offsets(scene, seed=33)
+    mine = shard(len(cams), rank, world)
+    my_cams = [cams[v] for v in mine]
+    W, H = cams[0].width, cams[0].height
+    n = scene.n
+    deg = scene.sh_degree
+    K4 = synth.sh_planes(deg)
+
+    # ---- device state
+    base = DeviceScene.from_host(scene, dev)                 # 𝒢_{t−1}
+    shifted = DeviceScene(torch.empty_like(base.pos_opa), base.scale, torch.empty_like(base.rot),
+                          base.sh, deg, base.dynamic)       # 𝒢_t after the shift
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    mu_d, sigma_d = t(mu), t(sigma)
+    dLs = torch.stack([t(synth.grad_image(cams[v], 1000 + v, 1.0 / (3 * W * H))) for v in mine]) \
+        if mine else torch.empty(0, 3, H, W, device=dev)
+    # one flat gradient buffer (the all_reduce payload): pos_opa, scale, rot, sh,
+    # g_mu, g_sigma, gradstat_sum  (+ counts kept separately, int)
+    sizes = [n * 4, n * 4, n * 4, K4 * n * 4, n * 4, n * 4, n]
+    flat = torch.zeros(sum(sizes), dtype=torch.float32, device=dev)
+    parts = list(torch.split(flat, sizes))
+    grads = Grads(parts[0].view(n, 4), parts[1].view(n, 4), parts[2].view(n, 4),
+                  parts[3].view(K4, n, 4), parts[6], torch.zeros(n, dtype=torch.int32, device=dev))
+    g_mu, g_sigma = parts[4].view(n, 4), parts[5].view(n, 4)
+    records = ViewRecords(max(len(mine), 1), n, dev)
+    raster = Raster(W, H, n, args.capacity, dev)
+
+    def step():
+        flat.zero_()
+        grads.gradstat_cnt.zero_()
+        dass.dass_apply_shift(base.pos_opa, base.rot, mu_d, sigma_d, base.dynamic,
+                              shifted.pos_opa, shifted.rot)
+        if my_cams:
+            dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
+                                    shifted.sh, None, records.xy_depth, records.conic_opa,
+                                    records.rgb, records.box, records.tiles)
+        for k, cam in enumerate(my_cams):
+            rec = records.view(k)
+            raster.forward(cam, rec)
+            raster.backward(cam, shifted, rec, dLs[k], grads)
+        dass.dass_apply_shift_bwd(base.rot, sigma_d, base.dynamic, grads.pos_opa, grads.rot,
+                                  g_mu, g_sigma)
+        if world > 1:
+            dist.all_reduce(flat)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- scene statistics (not timed) and overflow check
+    stats = {"K": [], "P_fwd": [], "P_bwd": [], "accepted": [], "terminated_px": [],
+             "tile_list_mean": [], "tile_list_max": []}
+    step()
+    torch.cuda.synchronize()
+    cnt = torch.zeros(8, dtype=torch.int64, device=dev)
+    for k, cam in enumerate(my_cams):
+        rec = records.view(k)
+        K = raster.forward(cam, rec, host_mode=True)
+        dass.dass_render_stats(cam, raster.ranges, raster.sorted_ids, rec[0], rec[1], rec[3],
+                               raster.T, raster.last, cnt)
+        c = cnt.cpu().numpy()
+        stats["K"].append(int(K)); stats["P_fwd"].append(int(c[0])); stats["P_bwd"].append(int(c[1]))
+        stats["accepted"].append(int(c[2])); stats["terminated_px"].append(int(c[3]))
+        stats["tile_list_mean"].append(float(c[4]) / max(int(c[6]), 1))
+        stats["tile_list_max"].append(int(c[5]))
+
+    # ---- warm-up, then exactly K timed steps
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    l0 = dass.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        barrier()
+    launches = dass.kernel_launches() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_step = float(ms_t.item())
+
+    # ---- per-op breakdown on one extra step (events on the launching stream)
+    ops = {}
+    if my_cams:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4 * len(my_cams) + 2)]
+        evs[0].record()
+        dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
+                                shifted.sh, None, records.xy_depth, records.conic_opa,
+                                records.rgb, records.box, records.tiles)
+        evs[1].record()
+        for k, cam in enumerate(my_cams):
+            rec = records.view(k)
+            xy, co, rgb, box, tiles = rec
+            dass.dass_bin_sort(cam, n, xy, box, tiles, raster.sort_ws, raster.capacity, None,
+                               raster.sorted_ids, raster.ranges, raster.num_pairs)
+            evs[2 + 4 * k].record()
+            dass.dass_render_fwd(cam, raster.ranges, raster.sorted_ids, xy, co, rgb, box, None,
+                                 raster.img, raster.T, raster.last)
+            evs[3 + 4 * k].record()
+            raster.backward(cam, shifted, rec, dLs[k], grads)
+            evs[4 + 4 * k].record()
+            evs[5 + 4 * k].record()
+        torch.cuda.synchronize()
+        ops["project_views"] = evs[0].elapsed_time(evs[1])
+        ops["bin_sort"] = sum(evs[1 + 4 * k if k == 0 else 1 + 4 * k].elapsed_time(evs[2 + 4 * k])
+                              for k in range(len(my_cams)))
+        ops["render_fwd"] = sum(evs[2 + 4 * k].elapsed_time(evs[3 + 4 * k]) for k in range(len(my_cams)))
+        ops["render_bwd"] = sum(evs[3 + 4 * k].elapsed_time(evs[4 + 4 * k]) for k in range(len(my_cams)))
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        h_in = [pin(scene.pos_opa), pin(scene.scale), pin(scene.rot), pin(scene.sh), pin(mu),
+                pin(sigma), dLs.cpu().pin_memory()]
+        d_in = [base.pos_opa, base.scale, base.rot, base.sh, mu_d, sigma_d, dLs]
+        h_out = torch.empty(flat.numel(), dtype=torch.float32).pin_memory()
+        h2d = sum(x.numel() * x.element_size() for x in h_in)
+        d2h = h_out.numel() * 4
+
+        def e2e_step():
+            for h, d in zip(h_in, d_in):
+                d.copy_(h, non_blocking=True)
+            step()
+            h_out.copy_(flat, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record()
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": len(cams) / (float(ems.item()) / 1e3), "unit": "views/s",
+               "ms_per_step": float(ems.item()), "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    # ---- gather stats to rank 0
+    if world > 1:
+        obj = [None] * world
+        dist.all_gather_object(obj, stats)
+        allst = {k: sum((o[k] for o in obj), []) for k in stats}
+        launches_t = torch.tensor([launches], device=dev, dtype=torch.int64)
+        dist.all_reduce(launches_t)
+        launches = int(launches_t.item())
+    else:
+        allst = stats
+    clocks = clk.summary()
+    result = None
+    if rank == 0:
+        pk, pk_kind = peaks()
+        f_max = pk.get("sm_max_mhz", 1965.0) * 1e6
+        peak_tflops = SM_COUNT * FP32_LANES * 2 * f_max / 1e12
+        # dominant op: render_bwd (raster kernel + fp32 preprocess), algorithmic
+        # flops counted for the raster part only (conservative)
+        flops = sum(a * FLOP_BWD_ACCEPTED + (b - a) * FLOP_BWD_REJECTED
+                    for a, b in zip(stats["accepted"], stats["P_bwd"]))
+        bwd_ms = ops.get("render_bwd", float("nan"))
+        achieved = flops / (bwd_ms / 1e3) / 1e12 if bwd_ms == bwd_ms and bwd_ms > 0 else None
+        views_s = len(cams) / (ms_step / 1e3)
+        result = {
+            "metric": METRIC, "value": round(views_s, 3), "unit": "views/s",
+            "mpix_per_s": round(views_s * W * H / 1e6, 1),
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N3DV-shaped scene and rig)",
+            "config": {"workload": WORKLOAD, "n_gaussians": n, "views": len(cams), "width": W,
+                       "height": H, "sh_degree": deg, "dynamic_frac": 0.3,
+                       "parallelism": f"view-sharded dp{world}",
+                       "l2": "inputs larger than L2 (≈0.5 GB of params, dL/dC and records per step)"},
+            "roofline": {"bound": "alu", "kernel": "render_bwd (raster + preprocess; raster flops only)",
+                         "achieved": None if achieved is None else round(achieved, 2),
+                         "peak": round(peak_tflops, 1), "unit": "TFLOP/s",
+                         "frac": None if achieved is None else round(achieved / peak_tflops, 4),
+                         "traffic": None, "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz ({pk_kind} clock)",
+                         "units_per_step": {"accepted": sum(stats["accepted"]), "P_bwd": sum(stats["P_bwd"])},
+                         "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED, "rejected": FLOP_BWD_REJECTED}},
+            "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
+            "scene_stats": {"K_per_view_mean": float(np.mean(allst["K"])),
+                            "P_fwd_per_px": float(np.sum(allst["P_fwd"]) / (len(allst["K"]) * W * H)),
+                            "P_bwd_per_px": float(np.sum(allst["P_bwd"]) / (len(allst["K"]) * W * H)),
+                            "accepted_per_px": float(np.sum(allst["accepted"]) / (len(allst["K"]) * W * H)),
+                            "early_terminated_frac": float(np.sum(allst["terminated_px"]) / (len(allst["K"]) * W * H)),
+                            "tile_list_mean": float(np.mean(allst["tile_list_mean"])),
+                            "tile_list_max": int(np.max(allst["tile_list_max"]))},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "e2e": e2e,
+        }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result, (cams, scene)
+
+
+# ------------------------------------------------------ oracle baseline ----
+
+def time_oracle(cams, scene, views, seed_base=1000):
+    import oracle
+    W, H = cams[0].width, cams[0].height
+    mu, sigma = __import__("paper_2411_14847_b200.synth", fromlist=["x"]).shift_offsets(scene, seed=33)
+    t0 = time.perf_counter()
+    po, ro = oracle.shift(scene.pos_opa, scene.rot, mu, sigma, scene.dynamic)
+    from paper_2411_14847_b200 import synth
+    sh_scene = synth.Scene(po.astype(np.float32), scene.scale, ro.astype(np.float32), scene.sh,
+                           scene.sh_degree, scene.dynamic)
+    for v in views:
+        dL = synth.grad_image(cams[v], seed_base + v, 1.0 / (3 * W * H))
+        oracle.render_bwd(cams[v], sh_scene, dL)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cams, scene, nviews):
+    import oracle
+    oracle.build()
+    secs = time_oracle(cams, scene, list(range(nviews)))
+    return {"value": round(nviews / secs, 4), "unit": "views/s", "cores": oracle.threads(),
+            "kind": "oracle",
+            "sample": f"{nviews} of the 20 views (fwd+bwd, scatter form, double) + the shift, "
+                      f"{secs:.1f} s on {oracle.threads()} OpenMP threads"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    from paper_2411_14847_b200 import synth
+    import oracle
+    oracle.build()
+    cams, scene = synth.c3(n=args.n, num_views=args.views)
+    W, H = cams[0].width, cams[0].height
+    for k in range(args.warmup):
+        time_oracle(cams, scene, [k % len(cams)])
+    secs = []
+    for k in range(args.steps):
+        secs.append(time_oracle(cams, scene, [k % len(cams)]))
+    s = float(np.mean(secs))
+    value = 1.0 / s
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "views/s",
+            "mpix_per_s": round(value * W * H / 1e6, 3), "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(s * 1e3, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded N3DV-shaped scene and rig)",
+            "config": {"workload": WORKLOAD, "n_gaussians": scene.n, "views": len(cams),
+                       "width": W, "height": H, "sh_degree": scene.sh_degree,
+                       "parallelism": "CPU oracle, OpenMP"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "views/s", "cores": oracle.threads(),
+                             "kind": "oracle",
+                             "sample": "each step = the shift + fwd+bwd of ONE of the 20 views (bounded sample)"},
+            "e2e": {"value": round(value, 4), "unit": "views/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        r = run_reference(args)
+        if r is not None:
+            print(json.dumps(r), flush=True)
+        return
+    result, (cams, scene) = run_ours(args)
+    rank, world, _ = dist_env()
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            result["cpu_baseline"] = cpu_baseline(cams, scene, args.cpu_sample_views)
+        print(json.dumps(result), flush=True)
+
+
+if __name__ == "__main__":
+    main()

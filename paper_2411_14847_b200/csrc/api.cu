@@ -1,0 +1,292 @@
+// api.cu — the extern "C" boundary of libdass.so (include/dass.h).
+// Argument validation happens here, before anything is enqueued; the kernels
+// live in the other translation units.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace dass {
+
+static std::atomic<uint64_t> g_launches{0};
+void launch_counted(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+static thread_local std::string t_last_error;
+
+static int fail(int status, const char* fmt, const char* what = "") {
+  char buf[512];
+  snprintf(buf, sizeof(buf), fmt, what);
+  t_last_error = buf;
+  return status;
+}
+
+static int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return DASS_OK;
+  t_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return DASS_ERR_CUDA;
+}
+
+static int check_camera(const dass_camera* c) {
+  if (c == nullptr) return fail(DASS_ERR_INVALID_ARG, "camera is null%s");
+  if (c->width < 1 || c->width > 65535 || c->height < 1 || c->height > 65535)
+    return fail(DASS_ERR_INVALID_ARG, "camera width/height must be in [1, 65535]%s");
+  if (!(c->fx > 0.0f) || !(c->fy > 0.0f) || !std::isfinite(c->fx) || !std::isfinite(c->fy))
+    return fail(DASS_ERR_INVALID_ARG, "camera fx, fy must be finite and > 0%s");
+  return DASS_OK;
+}
+
+static CamParams to_params(const dass_camera* c) {
+  CamParams p;
+  p.W = c->width;
+  p.H = c->height;
+  p.tiles_x = div_up(c->width, TILE);
+  p.tiles_y = div_up(c->height, TILE);
+  p.fx = c->fx; p.fy = c->fy; p.cx = c->cx; p.cy = c->cy;
+  for (int i = 0; i < 12; ++i) p.V[i] = c->viewmat[i];
+  p.near_plane = c->near_plane;
+  // camera centre −Rᵀ t (SH direction origin)
+  for (int a = 0; a < 3; ++a)
+    p.campos[a] = -(c->viewmat[0 * 4 + a] * c->viewmat[3] + c->viewmat[1 * 4 + a] * c->viewmat[7] +
+                    c->viewmat[2 * 4 + a] * c->viewmat[11]);
+  for (int i = 0; i < 16; ++i) p.T[i] = c->full_proj[i];
+  return p;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace dass
+
+using namespace dass;
+
+extern "C" {
+
+const char* dass_status_string(int status) {
+  switch (status) {
+    case DASS_OK: return "ok";
+    case DASS_ERR_INVALID_ARG: return "invalid argument";
+    case DASS_ERR_DATA: return "data error";
+    case DASS_ERR_NUMERICAL: return "numerical error";
+    case DASS_ERR_CAPACITY: return "pair capacity exceeded";
+    case DASS_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+const char* dass_last_error(void) { return t_last_error.c_str(); }
+
+int dass_abi_version(void) { return DASS_ABI_VERSION; }
+
+uint64_t dass_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int dass_apply_shift(int32_t n, const float* pos_opa, const float* rot, const float* mu,
+                     const float* sigma, const uint8_t* dyn_mask, float* pos_opa_out,
+                     float* rot_out, void* stream) {
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (n == 0) return DASS_OK;
+  if (!pos_opa || !rot || !mu || !sigma || !pos_opa_out || !rot_out)
+    return fail(DASS_ERR_INVALID_ARG, "dass_apply_shift: null required pointer%s");
+  if (!aligned16(pos_opa) || !aligned16(rot) || !aligned16(mu) || !aligned16(sigma) ||
+      !aligned16(pos_opa_out) || !aligned16(rot_out))
+    return fail(DASS_ERR_INVALID_ARG, "dass_apply_shift: float4 arrays must be 16-byte aligned%s");
+  return cuda_status(launch_shift(n, (const float4*)pos_opa, (const float4*)rot, (const float4*)mu,
+                                  (const float4*)sigma, dyn_mask, (float4*)pos_opa_out,
+                                  (float4*)rot_out, (cudaStream_t)stream),
+                     "dass_apply_shift");
+}
+
+int dass_apply_shift_bwd(int32_t n, const float* rot, const float* sigma, const uint8_t* dyn_mask,
+                         const float* g_pos_out, const float* g_rot_out, float* g_mu,
+                         float* g_sigma, void* stream) {
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (n == 0 || (!g_mu && !g_sigma)) return DASS_OK;
+  if (!rot || !sigma || !g_pos_out || !g_rot_out)
+    return fail(DASS_ERR_INVALID_ARG, "dass_apply_shift_bwd: null required pointer%s");
+  return cuda_status(launch_shift_bwd(n, (const float4*)rot, (const float4*)sigma, dyn_mask,
+                                      (const float4*)g_pos_out, (const float4*)g_rot_out,
+                                      (float4*)g_mu, (float4*)g_sigma, (cudaStream_t)stream),
+                     "dass_apply_shift_bwd");
+}
+
+static int project_common(const dass_camera* cams, int32_t num_views, int32_t n, int32_t sh_degree,
+                          const float* pos_opa, const float* scale, const float* rot,
+                          const float* sh, const uint8_t* keep, float* xy_depth, float* conic_opa,
+                          float* rgb, uint32_t* box, uint32_t* tiles, void* stream) {
+  if (num_views < 1 || num_views > 64)
+    return fail(DASS_ERR_INVALID_ARG, "num_views must be in [1, 64]%s");
+  for (int v = 0; v < num_views; ++v) {
+    int st = check_camera(cams + v);
+    if (st) return st;
+  }
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (sh_degree < 0 || sh_degree > 3) return fail(DASS_ERR_INVALID_ARG, "sh_degree must be in [0, 3]%s");
+  if (n == 0) return DASS_OK;
+  if (!pos_opa || !scale || !rot || !sh || !xy_depth || !conic_opa || !rgb || !box || !tiles)
+    return fail(DASS_ERR_INVALID_ARG, "dass_project: null required pointer%s");
+  CamParams cp[64];
+  for (int v = 0; v < num_views; ++v) cp[v] = to_params(cams + v);
+  return cuda_status(launch_project(cp, num_views, n, sh_degree, (const float4*)pos_opa,
+                                    (const float4*)scale, (const float4*)rot, (const float4*)sh,
+                                    keep, (float4*)xy_depth, (float4*)conic_opa, (float4*)rgb,
+                                    (uint2*)box, tiles, (cudaStream_t)stream),
+                     "dass_project");
+}
+
+int dass_project(const dass_camera* cam, int32_t n, int32_t sh_degree, const float* pos_opa,
+                 const float* scale, const float* rot, const float* sh, const uint8_t* keep_mask,
+                 float* xy_depth, float* conic_opa, float* rgb, uint32_t* box,
+                 uint32_t* tiles_touched, void* stream) {
+  return project_common(cam, 1, n, sh_degree, pos_opa, scale, rot, sh, keep_mask, xy_depth,
+                        conic_opa, rgb, box, tiles_touched, stream);
+}
+
+int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n, int32_t sh_degree,
+                       const float* pos_opa, const float* scale, const float* rot, const float* sh,
+                       const uint8_t* keep_mask, float* xy_depth, float* conic_opa, float* rgb,
+                       uint32_t* box, uint32_t* tiles_touched, void* stream) {
+  if (cams == nullptr) return fail(DASS_ERR_INVALID_ARG, "cams is null%s");
+  return project_common(cams, num_views, n, sh_degree, pos_opa, scale, rot, sh, keep_mask,
+                        xy_depth, conic_opa, rgb, box, tiles_touched, stream);
+}
+
+int dass_bin_sort_workspace(int32_t n, int32_t num_tiles, int64_t pair_capacity, size_t* bytes) {
+  if (!bytes) return fail(DASS_ERR_INVALID_ARG, "bytes is null%s");
+  if (n < 0 || num_tiles < 1 || pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30))
+    return fail(DASS_ERR_INVALID_ARG, "need n >= 0, num_tiles >= 1, 0 <= pair_capacity < 2^30%s");
+  *bytes = binsort_workspace(n, num_tiles, pair_capacity);
+  return DASS_OK;
+}
+
+int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, const uint32_t* box,
+                  const uint32_t* tiles_touched, void* ws, size_t ws_bytes, int64_t pair_capacity,
+                  uint64_t* sorted_keys, uint32_t* sorted_ids, uint32_t* tile_ranges,
+                  uint32_t* num_pairs_dev, int64_t* num_pairs_host, void* stream) {
+  int st = check_camera(cam);
+  if (st) return st;
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30))
+    return fail(DASS_ERR_INVALID_ARG, "pair_capacity must be in [0, 2^30)%s");
+  CamParams cp = to_params(cam);
+  const int ntiles = cp.tiles_x * cp.tiles_y;
+  if (!tile_ranges || !num_pairs_dev || !sorted_ids)
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort: null required pointer%s");
+  if (n > 0 && (!xy_depth || !box || !tiles_touched))
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort: null record pointer%s");
+  const size_t need = binsort_workspace(n, ntiles, pair_capacity);
+  if (ws_bytes < need || (need > 0 && ws == nullptr))
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort: workspace too small%s");
+  cudaStream_t s = (cudaStream_t)stream;
+  st = cuda_status(launch_binsort(cp, n, (const float4*)xy_depth, (const uint2*)box, tiles_touched,
+                                  ws, pair_capacity, sorted_keys, sorted_ids, (uint2*)tile_ranges,
+                                  num_pairs_dev, s),
+                   "dass_bin_sort");
+  if (st || num_pairs_host == nullptr) return st;
+  uint32_t h[2];
+  st = cuda_status(cudaMemcpyAsync(h, num_pairs_dev, sizeof(h), cudaMemcpyDeviceToHost, s),
+                   "dass_bin_sort: read K");
+  if (st) return st;
+  st = cuda_status(cudaStreamSynchronize(s), "dass_bin_sort: sync");
+  if (st) return st;
+  *num_pairs_host = (int64_t)h[0];
+  if (h[1]) {
+    char buf[128];
+    snprintf(buf, sizeof(buf), "K = %u pairs exceed capacity %lld", h[0], (long long)pair_capacity);
+    t_last_error = buf;
+    return DASS_ERR_CAPACITY;
+  }
+  return DASS_OK;
+}
+
+int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges, const uint32_t* sorted_ids,
+                    const float* xy_depth, const float* conic_opa, const float* rgb,
+                    const uint32_t* box, const float* bg, float* out_img, float* out_T,
+                    uint32_t* out_last, void* stream) {
+  int st = check_camera(cam);
+  if (st) return st;
+  if (!tile_ranges || !out_img || !out_T || !out_last)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_fwd: null required pointer%s");
+  if (!sorted_ids || !xy_depth || !conic_opa || !rgb || !box)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_fwd: null record pointer%s");
+  CamParams cp = to_params(cam);
+  float3 b = bg ? make_float3(bg[0], bg[1], bg[2]) : make_float3(0.f, 0.f, 0.f);
+  return cuda_status(launch_render_fwd(cp, (const uint2*)tile_ranges, sorted_ids,
+                                       (const float4*)xy_depth, (const float4*)conic_opa,
+                                       (const float4*)rgb, (const uint2*)box, b, out_img, out_T,
+                                       out_last, (cudaStream_t)stream),
+                     "dass_render_fwd");
+}
+
+int dass_render_bwd_workspace(int32_t n, size_t* bytes) {
+  if (!bytes || n < 0) return fail(DASS_ERR_INVALID_ARG, "bad arguments%s");
+  *bytes = render_bwd_workspace(n);
+  return DASS_OK;
+}
+
+int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree, const float* pos_opa,
+                    const float* scale, const float* rot, const float* sh,
+                    const uint8_t* keep_mask, const uint32_t* tile_ranges,
+                    const uint32_t* sorted_ids, const float* xy_depth, const float* conic_opa,
+                    const float* rgb, const uint32_t* box, const float* bg, const float* out_T,
+                    const uint32_t* out_last, const float* dL_dimg, void* ws, size_t ws_bytes,
+                    float* g_pos_opa, float* g_scale, float* g_rot, float* g_sh,
+                    float* gradstat_sum, uint32_t* gradstat_cnt, void* stream) {
+  int st = check_camera(cam);
+  if (st) return st;
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (sh_degree < 0 || sh_degree > 3) return fail(DASS_ERR_INVALID_ARG, "sh_degree must be in [0, 3]%s");
+  if (n == 0) return DASS_OK;
+  if (!pos_opa || !scale || !rot || !sh || !tile_ranges || !sorted_ids || !xy_depth || !conic_opa ||
+      !rgb || !box || !out_T || !out_last || !dL_dimg)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd: null required pointer%s");
+  if (ws_bytes < render_bwd_workspace(n) || !ws)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd: workspace too small%s");
+  if (!aligned16(ws)) return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd: workspace must be 16-byte aligned%s");
+  CamParams cp = to_params(cam);
+  float3 b = bg ? make_float3(bg[0], bg[1], bg[2]) : make_float3(0.f, 0.f, 0.f);
+  return cuda_status(
+      launch_render_bwd(cp, n, sh_degree, (const float4*)pos_opa, (const float4*)scale,
+                        (const float4*)rot, (const float4*)sh, keep_mask,
+                        (const uint2*)tile_ranges, sorted_ids, (const float4*)xy_depth,
+                        (const float4*)conic_opa, (const float4*)rgb, (const uint2*)box, b, out_T,
+                        out_last, dL_dimg, ws, (float4*)g_pos_opa, (float4*)g_scale,
+                        (float4*)g_rot, (float4*)g_sh, gradstat_sum, gradstat_cnt,
+                        (cudaStream_t)stream),
+      "dass_render_bwd");
+}
+
+int dass_error_map(const dass_camera* cam, const float* rendered, const float* gt, float gamma_err,
+                   float* err, uint32_t* dmask, int32_t n_base, const float* pos_opa,
+                   uint8_t* s_err, void* stream) {
+  int st = check_camera(cam);
+  if (st) return st;
+  if (!(gamma_err > 0.0f)) return fail(DASS_ERR_INVALID_ARG, "gamma_err must be > 0 (S:619)%s");
+  if (n_base < 0) return fail(DASS_ERR_INVALID_ARG, "n_base < 0%s");
+  if (!rendered || !gt) return fail(DASS_ERR_DATA, "dass_error_map: rendered and gt are required%s");
+  if (s_err && n_base > 0 && !pos_opa)
+    return fail(DASS_ERR_INVALID_ARG, "dass_error_map: s_err needs pos_opa%s");
+  CamParams cp = to_params(cam);
+  return cuda_status(launch_error_map(cp, rendered, gt, gamma_err, err, dmask, s_err ? n_base : 0,
+                                      (const float4*)pos_opa, s_err, (cudaStream_t)stream),
+                     "dass_error_map");
+}
+
+int dass_render_stats(const dass_camera* cam, const uint32_t* tile_ranges,
+                      const uint32_t* sorted_ids, const float* xy_depth, const float* conic_opa,
+                      const uint32_t* box, const float* out_T, const uint32_t* out_last,
+                      uint64_t* counters, void* stream) {
+  int st = check_camera(cam);
+  if (st) return st;
+  if (!tile_ranges || !sorted_ids || !xy_depth || !conic_opa || !box || !out_T || !out_last ||
+      !counters)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_stats: null required pointer%s");
+  CamParams cp = to_params(cam);
+  return cuda_status(launch_render_stats(cp, (const uint2*)tile_ranges, sorted_ids,
+                                         (const float4*)xy_depth, (const float4*)conic_opa,
+                                         (const uint2*)box, out_T, out_last,
+                                         (unsigned long long*)counters, (cudaStream_t)stream),
+                     "dass_render_stats");
+}
+
+}  // extern "C"

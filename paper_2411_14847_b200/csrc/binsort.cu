@@ -1,0 +1,422 @@
+// binsort.cu — dass_bin_sort: tile binning, in-house onesweep LSD radix sort
+// and per-tile ranges ("tile-based"; A03, A04).
+//
+// Contract: the pairs (key = tile<<32 | bits(z), value = Gaussian id) in
+// ascending (tile, depth bits, id) order.  Equivalent, cheaper order of work
+// (SURVEY §7.3 hard part 4): (1) a stable onesweep sort of the N Gaussians by
+// their 32 depth bits (key = zbits<<32 | id, 4 passes over N, not over K);
+// (2) an exclusive scan of tiles_touched in that depth order (decoupled
+// look-back); (3) emission of the pairs in depth order, so the pair array is
+// already ordered by (depth bits, id) within every tile; (4) a stable onesweep
+// sort of the K pairs on the tile bits only (ceil(tile_bits/8) passes, 2 at
+// 1352×1014); (5) ids + ranges.  All of it is integer work and bit-exact.
+//
+// Onesweep pass (Adinets & Merrill 2022 design, written for sm_100a): one
+// global histogram per digit pass computed up front (fused into the producer
+// kernels), then per pass one kernel whose blocks (a) claim a tile of 2048
+// keys through an atomic counter (forward progress for the look-back),
+// (b) rank digits within each warp with __match_any_sync (stable: item order
+// is (warp, round, lane)), (c) publish per-digit block counts and resolve the
+// exclusive prefix by decoupled look-back over predecessor blocks, (d) scatter.
+// No host synchronisation anywhere: K stays on the device (graph mode).
+#include "common.cuh"
+
+namespace dass {
+namespace {
+
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_IPT = 8;
+constexpr int SORT_ITEMS = SORT_THREADS * SORT_IPT;  // 2048 keys per block
+constexpr int RADIX = 256;
+constexpr int MAX_PASSES = 8;  // hist slots: 0..3 depth presort, 4..7 pair sort
+constexpr uint32_t FLAG_AGG = 1u << 30;
+constexpr uint32_t FLAG_INC = 2u << 30;
+constexpr uint32_t VAL_MASK = (1u << 30) - 1u;
+constexpr unsigned long long SFLAG_AGG = 1ull << 62;
+constexpr unsigned long long SFLAG_INC = 2ull << 62;
+constexpr unsigned long long SVAL_MASK = (1ull << 62) - 1ull;
+constexpr int NUM_COUNTERS = 16;
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+struct WS {
+  uint64_t* dkeysA;
+  uint64_t* dkeysB;
+  uint32_t* offsets;
+  uint64_t* pkeysA;
+  uint64_t* pkeysB;
+  uint32_t* hist;                  // [MAX_PASSES][256]
+  uint32_t* counters;              // [NUM_COUNTERS]
+  unsigned long long* scan_status; // [scan blocks]
+  uint32_t* dstatus;               // [4][nblk_n][256]
+  uint32_t* pstatus;               // [MAX_PASSES-4][nblk_cap][256]
+  size_t ctrl_bytes;               // hist + counters (memset every call)
+  size_t total;
+};
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+WS carve(void* base, int n, int64_t cap) {
+  WS w;
+  char* p = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* r = p ? p + off : nullptr; off += align_up(bytes); return r; };
+  const size_t nblk_n = (size_t)div_up(n > 0 ? n : 1, SORT_ITEMS);
+  const size_t nblk_cap = (size_t)((cap + SORT_ITEMS - 1) / SORT_ITEMS) + 1;
+  w.hist = (uint32_t*)take(sizeof(uint32_t) * MAX_PASSES * RADIX);
+  w.counters = (uint32_t*)take(sizeof(uint32_t) * NUM_COUNTERS);
+  w.ctrl_bytes = off;
+  w.scan_status = (unsigned long long*)take(sizeof(unsigned long long) * nblk_n);
+  w.dstatus = (uint32_t*)take(sizeof(uint32_t) * 4 * nblk_n * RADIX);
+  w.pstatus = (uint32_t*)take(sizeof(uint32_t) * (MAX_PASSES - 4) * nblk_cap * RADIX);
+  w.dkeysA = (uint64_t*)take(sizeof(uint64_t) * (size_t)(n > 0 ? n : 1));
+  w.dkeysB = (uint64_t*)take(sizeof(uint64_t) * (size_t)(n > 0 ? n : 1));
+  w.offsets = (uint32_t*)take(sizeof(uint32_t) * (size_t)(n > 0 ? n : 1));
+  w.pkeysA = (uint64_t*)take(sizeof(uint64_t) * (size_t)(cap > 0 ? cap : 1));
+  w.pkeysB = (uint64_t*)take(sizeof(uint64_t) * (size_t)(cap > 0 ? cap : 1));
+  w.total = off;
+  return w;
+}
+
+// ---------------------------------------------------------------- kernels --
+
+// Depth-presort keys zbits<<32 | i (culled: all-ones depth → sorted last),
+// fused with the 4 digit histograms of bits 32..63 and the clearing of the
+// presort look-back status words.
+__global__ void __launch_bounds__(256) presort_init_kernel(int n, const float4* __restrict__ xy_depth,
+                                                          const uint32_t* __restrict__ tiles,
+                                                          uint64_t* keys, uint32_t* hist,
+                                                          uint32_t* dstatus, size_t dstatus_words,
+                                                          unsigned long long* scan_status,
+                                                          int scan_blocks) {
+  __shared__ uint32_t sh[4][RADIX];
+  for (int k = threadIdx.x; k < 4 * RADIX; k += blockDim.x) (&sh[0][0])[k] = 0u;
+  __syncthreads();
+  const size_t gstride = (size_t)gridDim.x * blockDim.x;
+  const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (size_t i = gid; i < (size_t)n; i += gstride) {
+    const uint32_t zb = tiles[i] ? __float_as_uint(xy_depth[i].z) : 0xFFFFFFFFu;
+    keys[i] = ((uint64_t)zb << 32) | (uint64_t)i;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) atomicAdd(&sh[p][(zb >> (8 * p)) & 255u], 1u);
+  }
+  for (size_t k = gid; k < dstatus_words; k += gstride) dstatus[k] = 0u;
+  for (size_t k = gid; k < (size_t)scan_blocks; k += gstride) scan_status[k] = 0ull;
+  __syncthreads();
+  for (int k = threadIdx.x; k < 4 * RADIX; k += blockDim.x) {
+    const uint32_t v = (&sh[0][0])[k];
+    if (v) atomicAdd(&hist[k], v);
+  }
+}
+
+// One onesweep LSD pass over bits [shift, shift+8) of 64-bit keys.
+__global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
+    const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int n_static,
+    const uint32_t* __restrict__ n_dev, const uint32_t* __restrict__ hist, uint32_t* status,
+    uint32_t* counter, int shift) {
+  __shared__ uint32_t s_whist[SORT_THREADS / 32][RADIX];
+  __shared__ uint32_t s_gbase[RADIX];
+  __shared__ uint32_t s_wsum[SORT_THREADS / 32];
+  __shared__ uint32_t s_blk;
+  const int t = threadIdx.x;
+  const int warp = t >> 5;
+  const uint32_t lane = lane_id();
+  const int n = n_static >= 0 ? n_static : (n_dev[1] ? 0 : (int)n_dev[0]);
+  if (t == 0) s_blk = atomicAdd(counter, 1u);
+  for (int k = t; k < (SORT_THREADS / 32) * RADIX; k += SORT_THREADS) (&s_whist[0][0])[k] = 0u;
+  __syncthreads();
+  const uint32_t blk = s_blk;
+  const long long base = (long long)blk * SORT_ITEMS;
+  if (base >= n) return;
+
+  uint64_t keys[SORT_IPT];
+  uint32_t digit[SORT_IPT];
+  uint32_t rank[SORT_IPT];
+  const long long wbase = base + warp * (SORT_IPT * 32);
+#pragma unroll
+  for (int j = 0; j < SORT_IPT; ++j) {
+    const long long idx = wbase + j * 32 + lane;
+    if (idx < n) {
+      keys[j] = in[idx];
+      digit[j] = (uint32_t)(keys[j] >> shift) & 255u;
+    } else {
+      keys[j] = 0ull;
+      digit[j] = 256u;  // invalid: ranks only among invalid lanes, never scattered
+    }
+  }
+  const uint32_t lt_mask = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < SORT_IPT; ++j) {
+    const uint32_t d = digit[j];
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    uint32_t pre = 0u;
+    if (d < 256u) pre = s_whist[warp][d];
+    __syncwarp();
+    if (d < 256u) {
+      rank[j] = pre + __popc(peers & lt_mask);
+      const uint32_t leader = 31u - __clz(peers);
+      if (lane == leader) s_whist[warp][d] = pre + __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive scan over warps, block count
+  uint32_t count = 0u;
+#pragma unroll
+  for (int w = 0; w < SORT_THREADS / 32; ++w) {
+    const uint32_t c = s_whist[w][t];
+    s_whist[w][t] = count;
+    count += c;
+  }
+  // exclusive scan of the global histogram over digits (digit = t)
+  const uint32_t hv = hist[t];
+  uint32_t incl = hv;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((int)lane >= o) incl += y;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  // decoupled look-back for digit t
+  uint32_t excl = 0u;
+  uint32_t* my = status + (size_t)blk * RADIX + t;
+  if (blk == 0) {
+    st_relaxed(my, FLAG_INC | count);
+  } else {
+    st_relaxed(my, FLAG_AGG | count);
+    long long j = (long long)blk - 1;
+    while (true) {
+      const uint32_t v = ld_relaxed(status + (size_t)j * RADIX + t);
+      const uint32_t f = v & ~VAL_MASK;
+      if (f == 0u) continue;  // predecessor not published yet: spin
+      excl += v & VAL_MASK;
+      if (f == FLAG_INC) break;
+      --j;
+    }
+    st_relaxed(my, FLAG_INC | (excl + count));
+  }
+  __syncthreads();
+  uint32_t gofs = incl - hv;
+  for (int w = 0; w < warp; ++w) gofs += s_wsum[w];
+  s_gbase[t] = gofs + excl;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < SORT_IPT; ++j) {
+    const uint32_t d = digit[j];
+    if (d < 256u) out[s_gbase[d] + s_whist[warp][d] + rank[j]] = keys[j];
+  }
+}
+
+// Exclusive scan of tiles_touched in depth order → offsets; K and the
+// overflow flag → num_pairs_dev.  Single pass, decoupled look-back.
+__global__ void __launch_bounds__(256) tile_scan_kernel(int n, const uint64_t* __restrict__ dkeys,
+                                                       const uint32_t* __restrict__ tiles,
+                                                       uint32_t* offsets,
+                                                       unsigned long long* status,
+                                                       uint32_t* counter, long long cap,
+                                                       uint32_t* num_pairs_dev) {
+  constexpr int IPT = 8;
+  __shared__ unsigned long long s_w[8];
+  __shared__ unsigned long long s_excl;
+  __shared__ uint32_t s_blk;
+  const int t = threadIdx.x;
+  const uint32_t lane = lane_id();
+  const int warp = t >> 5;
+  if (t == 0) s_blk = atomicAdd(counter, 1u);
+  __syncthreads();
+  const uint32_t blk = s_blk;
+  const long long base = (long long)blk * (256 * IPT) + (long long)t * IPT;
+  uint32_t c[IPT];
+  unsigned long long tsum = 0ull;
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const long long r = base + j;
+    c[j] = r < n ? tiles[(uint32_t)dkeys[r]] : 0u;
+    tsum += c[j];
+  }
+  unsigned long long incl = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((int)lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  unsigned long long wexcl = 0ull, btotal = 0ull;
+  for (int w = 0; w < 8; ++w) {
+    if (w < warp) wexcl += s_w[w];
+    btotal += s_w[w];
+  }
+  if (t == 0) {
+    unsigned long long* my = status + blk;
+    unsigned long long excl = 0ull;
+    if (blk == 0) {
+      st_relaxed64(my, SFLAG_INC | btotal);
+    } else {
+      st_relaxed64(my, SFLAG_AGG | btotal);
+      long long j = (long long)blk - 1;
+      while (true) {
+        const unsigned long long v = ld_relaxed64(status + j);
+        const unsigned long long f = v & ~SVAL_MASK;
+        if (f == 0ull) continue;
+        excl += v & SVAL_MASK;
+        if (f == SFLAG_INC) break;
+        --j;
+      }
+      st_relaxed64(my, SFLAG_INC | (excl + btotal));
+    }
+    s_excl = excl;
+    if (blk == gridDim.x - 1) {
+      const unsigned long long K = excl + btotal;
+      num_pairs_dev[0] = K > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)K;
+      num_pairs_dev[1] = K > (unsigned long long)cap ? 1u : 0u;
+    }
+  }
+  __syncthreads();
+  unsigned long long run = s_excl + wexcl + (incl - tsum);
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const long long r = base + j;
+    if (r < n) offsets[r] = (uint32_t)run;
+    run += c[j];
+  }
+}
+
+// Emit pairs (tile<<32 | id) in depth order; histogram their tile digits;
+// clear the pair-sort look-back status words for the blocks that will run.
+__global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __restrict__ dkeys,
+                                                  const uint32_t* __restrict__ tiles,
+                                                  const uint2* __restrict__ box,
+                                                  const uint32_t* __restrict__ offsets,
+                                                  const uint32_t* __restrict__ num_pairs_dev,
+                                                  int tiles_x, int npass, uint64_t* pkeys,
+                                                  uint32_t* hist, uint32_t* pstatus,
+                                                  size_t pstatus_stride) {
+  __shared__ uint32_t sh[MAX_PASSES - 4][RADIX];
+  if (num_pairs_dev[1]) return;  // overflow: every range stays [0,0)
+  for (int k = threadIdx.x; k < (MAX_PASSES - 4) * RADIX; k += blockDim.x) (&sh[0][0])[k] = 0u;
+  __syncthreads();
+  const uint32_t K = num_pairs_dev[0];
+  const size_t gstride = (size_t)gridDim.x * blockDim.x;
+  const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t words = (size_t)div_up((int)K, SORT_ITEMS) * RADIX;
+  for (int p = 0; p < npass; ++p)
+    for (size_t k = gid; k < words; k += gstride) pstatus[p * pstatus_stride + k] = 0u;
+  for (size_t r = gid; r < (size_t)n; r += gstride) {
+    const uint32_t id = (uint32_t)dkeys[r];
+    if (tiles[id] == 0u) continue;
+    const uint2 b = box[id];
+    const int tx0 = (int)(b.x & 0xFFFFu) / TILE, tx1 = (int)(b.x >> 16) / TILE;
+    const int ty0 = (int)(b.y & 0xFFFFu) / TILE, ty1 = (int)(b.y >> 16) / TILE;
+    uint32_t o = offsets[r];
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
+        pkeys[o++] = ((uint64_t)tile << 32) | id;
+        for (int p = 0; p < npass; ++p) atomicAdd(&sh[p][(tile >> (8 * p)) & 255u], 1u);
+      }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < npass * RADIX; k += blockDim.x) {
+    const uint32_t v = (&sh[0][0])[k];
+    if (v) atomicAdd(&hist[4 * RADIX + k], v);
+  }
+}
+
+// Sorted pairs → ids, optional (tile|zbits) keys, per-tile [start, end).
+__global__ void __launch_bounds__(256) finalize_kernel(const uint64_t* __restrict__ pk,
+                                                      const uint32_t* __restrict__ num_pairs_dev,
+                                                      const float4* __restrict__ xy_depth,
+                                                      uint64_t* sorted_keys, uint32_t* ids,
+                                                      uint2* ranges) {
+  if (num_pairs_dev[1]) return;
+  const uint32_t K = num_pairs_dev[0];
+  const size_t gstride = (size_t)gridDim.x * blockDim.x;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gstride) {
+    const uint64_t key = pk[k];
+    const uint32_t id = (uint32_t)key;
+    const uint32_t tile = (uint32_t)(key >> 32);
+    ids[k] = id;
+    if (sorted_keys) sorted_keys[k] = ((uint64_t)tile << 32) | __float_as_uint(xy_depth[id].z);
+    if (k == 0 || (uint32_t)(pk[k - 1] >> 32) != tile) ranges[tile].x = (uint32_t)k;
+    if (k + 1 == K || (uint32_t)(pk[k + 1] >> 32) != tile) ranges[tile].y = (uint32_t)(k + 1);
+  }
+}
+
+}  // namespace
+
+size_t binsort_workspace(int n, int num_tiles, int64_t capacity) {
+  (void)num_tiles;
+  return carve(nullptr, n, capacity).total;
+}
+
+cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, const uint2* box,
+                           const uint32_t* tiles, void* ws_ptr, int64_t capacity,
+                           uint64_t* sorted_keys, uint32_t* sorted_ids, uint2* ranges,
+                           uint32_t* num_pairs_dev, cudaStream_t s) {
+  const int num_tiles = cam.tiles_x * cam.tiles_y;
+  WS w = carve(ws_ptr, n, capacity);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)num_tiles, s))) return e;
+  if ((e = cudaMemsetAsync(w.hist, 0, w.ctrl_bytes, s))) return e;
+  if (n == 0) {
+    return cudaMemsetAsync(num_pairs_dev, 0, 2 * sizeof(uint32_t), s);
+  }
+  const int tile_bits = num_tiles > 1 ? 32 - __builtin_clz((unsigned)(num_tiles - 1)) : 0;
+  const int npass = (tile_bits + 7) / 8;
+  const int nblk_n = div_up(n, SORT_ITEMS);
+  const size_t nblk_cap = (size_t)((capacity + SORT_ITEMS - 1) / SORT_ITEMS) + 1;
+  const int grid_n = div_up(n, 256) < 148 * 8 ? div_up(n, 256) : 148 * 8;
+  presort_init_kernel<<<grid_n, 256, 0, s>>>(n, xy_depth, tiles, w.dkeysA, w.hist, w.dstatus,
+                                             (size_t)4 * nblk_n * RADIX, w.scan_status, nblk_n);
+  launch_counted();
+  uint64_t* a = w.dkeysA;
+  uint64_t* b = w.dkeysB;
+  for (int p = 0; p < 4; ++p) {
+    onesweep_kernel<<<nblk_n, SORT_THREADS, 0, s>>>(a, b, n, nullptr, w.hist + p * RADIX,
+                                                    w.dstatus + (size_t)p * nblk_n * RADIX,
+                                                    w.counters + p, 32 + 8 * p);
+    launch_counted();
+    uint64_t* tmp = a; a = b; b = tmp;
+  }
+  // a = depth-sorted (zbits, id)
+  tile_scan_kernel<<<nblk_n, 256, 0, s>>>(n, a, tiles, w.offsets, w.scan_status, w.counters + 4,
+                                          (long long)capacity, num_pairs_dev);
+  launch_counted();
+  emit_kernel<<<grid_n, 256, 0, s>>>(n, a, tiles, box, w.offsets, num_pairs_dev, cam.tiles_x,
+                                     npass, w.pkeysA, w.hist, w.pstatus, nblk_cap * RADIX);
+  launch_counted();
+  uint64_t* pa = w.pkeysA;
+  uint64_t* pb = w.pkeysB;
+  const int grid_cap = (int)nblk_cap;
+  for (int p = 0; p < npass; ++p) {
+    onesweep_kernel<<<grid_cap, SORT_THREADS, 0, s>>>(pa, pb, -1, num_pairs_dev,
+                                                      w.hist + (4 + p) * RADIX,
+                                                      w.pstatus + (size_t)p * nblk_cap * RADIX,
+                                                      w.counters + 5 + p, 32 + 8 * p);
+    launch_counted();
+    uint64_t* tmp = pa; pa = pb; pb = tmp;
+  }
+  const int grid_f = 148 * 8;
+  finalize_kernel<<<grid_f, 256, 0, s>>>(pa, num_pairs_dev, xy_depth, sorted_keys, sorted_ids,
+                                         ranges);
+  launch_counted();
+  return cudaGetLastError();
+}
+
+}  // namespace dass

@@ -1,0 +1,114 @@
+// common.cuh — shared device helpers of libdass.so (sm_100a).
+// The CUDA path shares nothing with oracle/ (see DESIGN.md §Boundary).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "dass.h"
+
+namespace dass {
+
+constexpr int TILE = DASS_TILE;  // 16×16 pixel tiles (A04)
+constexpr float ALPHA_MIN = 1.0f / 255.0f;  // A11
+constexpr float ALPHA_MAX = 0.99f;          // A11
+constexpr float T_MIN = 1e-4f;              // A12
+constexpr float LOG2E = 1.4426950408889634f;
+
+// Camera passed by value as a kernel parameter (__grid_constant__).
+struct CamParams {
+  int W, H, tiles_x, tiles_y;
+  float fx, fy, cx, cy;
+  float V[12];       // world→camera [R|t] row-major
+  float near_plane;
+  float campos[3];   // −Rᵀ t (SH direction origin)
+  float T[16];       // Alg. 1 full projection (row-vector convention)
+};
+
+void launch_counted(int n = 1);  // bumps the dass_kernel_launches() counter
+
+// Per-pixel α of Eq. 8, shared by render_fwd and render_bwd so both take the
+// same fp32 decisions (power > 0 guard, α < 1/255 skip) bit-for-bit.
+struct Splat2D {
+  float u, v;        // tile-local mean (pixels, relative to the tile origin)
+  float A, B, C, o;  // conic and effective opacity
+};
+
+// power = −½(A dx² + C dy²) − B dx dy   (Eq. 5 restricted to 2D).  Written
+// with explicit-rounding intrinsics so the compiler can neither contract nor
+// re-associate it: the forward and the backward kernels get identical bits.
+__device__ __forceinline__ float splat_power(float A, float B, float C, float dx, float dy) {
+  const float adx2 = __fmul_rn(__fmul_rn(A, dx), dx);
+  const float q = __fmaf_rn(__fmul_rn(C, dy), dy, adx2);
+  const float bxy = __fmul_rn(__fmul_rn(B, dx), dy);
+  return __fmaf_rn(-0.5f, q, -bxy);
+}
+
+// exp(power) on the MUFU pipe: ex2.approx(power · log2 e).
+__device__ __forceinline__ float splat_exp(float power) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmul_rn(power, LOG2E)));
+  return y;
+}
+
+// α = min(0.99, o·G) — Eq. 8's α_i with the 0.99 cap (A11).
+__device__ __forceinline__ float splat_alpha(float o, float G) {
+  return fminf(ALPHA_MAX, __fmul_rn(o, G));
+}
+
+__device__ __forceinline__ uint32_t lane_id() {
+  uint32_t l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
+
+// Vector reduction to global memory (sm_90+): one instruction adds 4 floats.
+__device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+               :: "l"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+__host__ __device__ __forceinline__ int div_up(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace dass
+
+// Internal launchers (defined in the .cu files, called by api.cu).
+namespace dass {
+cudaError_t launch_shift(int n, const float4* pos, const float4* rot, const float4* mu,
+                         const float4* sigma, const uint8_t* mask, float4* pos_out,
+                         float4* rot_out, cudaStream_t s);
+cudaError_t launch_shift_bwd(int n, const float4* rot, const float4* sigma, const uint8_t* mask,
+                             const float4* g_pos_out, const float4* g_rot_out, float4* g_mu,
+                             float4* g_sigma, cudaStream_t s);
+cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_degree,
+                           const float4* pos_opa, const float4* scale, const float4* rot,
+                           const float4* sh, const uint8_t* keep, float4* xy_depth,
+                           float4* conic_opa, float4* rgb, uint2* box, uint32_t* tiles,
+                           cudaStream_t s);
+size_t binsort_workspace(int n, int num_tiles, int64_t capacity);
+cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, const uint2* box,
+                           const uint32_t* tiles, void* ws, int64_t capacity,
+                           uint64_t* sorted_keys, uint32_t* sorted_ids, uint2* ranges,
+                           uint32_t* num_pairs_dev, cudaStream_t s);
+cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
+                              const float4* xy_depth, const float4* conic_opa, const float4* rgb,
+                              const uint2* box, float3 bg, float* out_img, float* out_T,
+                              uint32_t* out_last, cudaStream_t s);
+size_t render_bwd_workspace(int n);
+cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const float4* pos_opa,
+                              const float4* scale, const float4* rot, const float4* sh,
+                              const uint8_t* keep, const uint2* ranges, const uint32_t* ids,
+                              const float4* xy_depth, const float4* conic_opa, const float4* rgb,
+                              const uint2* box, float3 bg, const float* out_T,
+                              const uint32_t* out_last, const float* dL_dimg, void* ws,
+                              float4* g_pos_opa, float4* g_scale, float4* g_rot, float4* g_sh,
+                              float* gradstat_sum, uint32_t* gradstat_cnt, cudaStream_t s);
+cudaError_t launch_error_map(const CamParams& cam, const float* rendered, const float* gt,
+                             float gamma, float* err, uint32_t* dmask, int n_base,
+                             const float4* pos_opa, uint8_t* s_err, cudaStream_t s);
+cudaError_t launch_render_stats(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
+                                const float4* xy_depth, const float4* conic_opa, const uint2* box,
+                                const float* out_T, const uint32_t* out_last,
+                                unsigned long long* counters, cudaStream_t s);
+}  // namespace dass

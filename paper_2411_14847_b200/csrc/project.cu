@@ -1,0 +1,284 @@
+// project.cu — dass_project / dass_project_views: EWA projection + SH colour
+// (Eqs. 5-7, colour P:351).  One thread per Gaussian, looping over
+// the views of the launch so the 240 B/G of parameters are read once for all
+// views (multi-view batching).  HBM-bound.
+//
+// Three precisions, by purpose:
+//  * the KEY CHAIN (depth bits, pixel box, visibility) in IEEE fp32 with
+//    explicit-rounding intrinsics, in exactly the op order documented in
+//    include/dass.h, so the (tile|depth) keys are reproducible bit-for-bit;
+//  * the per-pixel records (u, v, conic) in fp64 then rounded once to fp32:
+//    the mean is stored as fp32 hi + fp16 lo so the renderer can form the
+//    tile-local offset u − X to ~1e-7 px instead of ulp(1000) = 6e-5 px;
+//  * the SH colour in fp32.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "sh.cuh"
+
+namespace dass {
+namespace {
+
+constexpr int MAXV = 16;  // views per launch (kernel-parameter budget)
+
+struct ProjectArgs {
+  CamParams cam[MAXV];
+  int num_views;
+  int n;
+  int view_offset;  // records of view v go to [(view_offset + v)·n, …)
+  const float4* pos_opa;
+  const float4* scale;
+  const float4* rot;
+  const float4* sh;
+  const uint8_t* keep;
+  float4* xy_depth;
+  float4* conic_opa;
+  float4* rgb;
+  uint2* box;
+  uint32_t* tiles;
+};
+
+#define FM __fmul_rn
+#define FA __fadd_rn
+#define FS __fsub_rn
+#define FD __fdiv_rn
+
+struct KeyResult {
+  bool visible;
+  float z;
+  int x0, x1, y0, y1;
+};
+
+// The KEY CHAIN of include/dass.h, steps 1-11.
+__device__ __forceinline__ KeyResult key_chain(const CamParams& c, float px, float py, float pz,
+                                               float o, float s0, float s1, float s2, float4 q) {
+  KeyResult k;
+  k.visible = false; k.z = 0.f; k.x0 = 1; k.x1 = 0; k.y0 = 1; k.y1 = 0;
+  const float* V = c.V;
+  float t[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    t[a] = FA(FA(FA(FM(V[4 * a + 0], px), FM(V[4 * a + 1], py)), FM(V[4 * a + 2], pz)), V[4 * a + 3]);
+  if (!(t[2] > c.near_plane)) return k;
+  const float nn = FA(FA(FA(FM(q.x, q.x), FM(q.y, q.y)), FM(q.z, q.z)), FM(q.w, q.w));
+  const float nq = __fsqrt_rn(nn);
+  if (!(nq > 0.f) || !isfinite(nq)) return k;
+  const float w = FD(q.x, nq), x = FD(q.y, nq), y = FD(q.z, nq), z = FD(q.w, nq);
+  const float xx = FM(x, x), yy = FM(y, y), zz = FM(z, z), xy = FM(x, y), xz = FM(x, z),
+              yz = FM(y, z), wx = FM(w, x), wy = FM(w, y), wz = FM(w, z);
+  float R[3][3];
+  R[0][0] = FS(1.f, FM(2.f, FA(yy, zz)));
+  R[0][1] = FM(2.f, FS(xy, wz));
+  R[0][2] = FM(2.f, FA(xz, wy));
+  R[1][0] = FM(2.f, FA(xy, wz));
+  R[1][1] = FS(1.f, FM(2.f, FA(xx, zz)));
+  R[1][2] = FM(2.f, FS(yz, wx));
+  R[2][0] = FM(2.f, FS(xz, wy));
+  R[2][1] = FM(2.f, FA(yz, wx));
+  R[2][2] = FS(1.f, FM(2.f, FA(xx, yy)));
+  const float s[3] = {s0, s1, s2};
+  float m[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) m[a][b] = FM(R[a][b], s[b]);
+  float S[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      const float acc = FA(FA(FM(m[a][0], m[b][0]), FM(m[a][1], m[b][1])), FM(m[a][2], m[b][2]));
+      S[a][b] = acc;
+      S[b][a] = acc;
+    }
+  const float Wf = (float)c.W, Hf = (float)c.H;
+  const float lx = FD(FM(1.3f, Wf), FM(2.0f, c.fx));
+  const float ly = FD(FM(1.3f, Hf), FM(2.0f, c.fy));
+  const float xt = FM(fminf(lx, fmaxf(-lx, FD(t[0], t[2]))), t[2]);
+  const float yt = FM(fminf(ly, fmaxf(-ly, FD(t[1], t[2]))), t[2]);
+  const float tz2 = FM(t[2], t[2]);
+  const float J00 = FD(c.fx, t[2]);
+  const float J02 = -FD(FM(c.fx, xt), tz2);
+  const float J11 = FD(c.fy, t[2]);
+  const float J12 = -FD(FM(c.fy, yt), tz2);
+  float M[2][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    M[0][b] = FA(FM(J00, V[0 * 4 + b]), FM(J02, V[2 * 4 + b]));
+    M[1][b] = FA(FM(J11, V[1 * 4 + b]), FM(J12, V[2 * 4 + b]));
+  }
+  float P[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      P[a][b] = FA(FA(FM(M[a][0], S[0][b]), FM(M[a][1], S[1][b])), FM(M[a][2], S[2][b]));
+  const float ca = FA(FA(FA(FM(P[0][0], M[0][0]), FM(P[0][1], M[0][1])), FM(P[0][2], M[0][2])), 0.3f);
+  const float cb = FA(FA(FM(P[0][0], M[1][0]), FM(P[0][1], M[1][1])), FM(P[0][2], M[1][2]));
+  const float cc = FA(FA(FA(FM(P[1][0], M[1][0]), FM(P[1][1], M[1][1])), FM(P[1][2], M[1][2])), 0.3f);
+  const float det = FS(FM(ca, cc), FM(cb, cb));
+  if (!(det > 0.f)) return k;
+  const float mid = FM(0.5f, FA(ca, cc));
+  const float lam = FA(mid, __fsqrt_rn(fmaxf(0.1f, FS(FM(mid, mid), det))));
+  const float r = ceilf(FM(3.0f, __fsqrt_rn(lam)));
+  const float u = FA(FD(FM(c.fx, t[0]), t[2]), c.cx);
+  const float v = FA(FD(FM(c.fy, t[1]), t[2]), c.cy);
+  if (!isfinite(u) || !isfinite(v) || !isfinite(lam)) return k;
+  const float fx0 = fmaxf(0.f, ceilf(FS(u, r)));
+  const float fx1 = fminf(FS(Wf, 1.f), floorf(FA(u, r)));
+  const float fy0 = fmaxf(0.f, ceilf(FS(v, r)));
+  const float fy1 = fminf(FS(Hf, 1.f), floorf(FA(v, r)));
+  if (!(fx0 <= fx1) || !(fy0 <= fy1)) return k;
+  if (!(o >= ALPHA_MIN)) return k;
+  k.visible = true;
+  k.z = t[2];
+  k.x0 = (int)fx0; k.x1 = (int)fx1; k.y0 = (int)fy0; k.y1 = (int)fy1;
+  return k;
+}
+
+#undef FM
+#undef FA
+#undef FS
+#undef FD
+
+// fp64 records: tile-independent mean (hi/lo) and conic of Eq. 7.
+struct Records {
+  float u_hi, v_hi;
+  __half u_lo, v_lo;
+  float A, B, C;
+};
+
+__device__ __forceinline__ Records accurate_records(const CamParams& c, float4 po, float4 sc,
+                                                    float4 q, float keepf) {
+  Records r;
+  const double px = po.x, py = po.y, pz = po.z;
+  double t[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    t[a] = (double)c.V[4 * a] * px + (double)c.V[4 * a + 1] * py + (double)c.V[4 * a + 2] * pz +
+           (double)c.V[4 * a + 3];
+  const double nq = sqrt((double)q.x * q.x + (double)q.y * q.y + (double)q.z * q.z + (double)q.w * q.w);
+  const double w = q.x / nq, x = q.y / nq, y = q.z / nq, z = q.w / nq;
+  double R[3][3];
+  R[0][0] = 1 - 2 * (y * y + z * z); R[0][1] = 2 * (x * y - w * z); R[0][2] = 2 * (x * z + w * y);
+  R[1][0] = 2 * (x * y + w * z); R[1][1] = 1 - 2 * (x * x + z * z); R[1][2] = 2 * (y * z - w * x);
+  R[2][0] = 2 * (x * z - w * y); R[2][1] = 2 * (y * z + w * x); R[2][2] = 1 - 2 * (x * x + y * y);
+  const double s[3] = {(double)sc.x * keepf, (double)sc.y * keepf, (double)sc.z * keepf};
+  // N = J W R S (2×3); Σ' = N Nᵀ + 0.3 I
+  const double lx = 1.3 * c.W / (2.0 * c.fx), ly = 1.3 * c.H / (2.0 * c.fy);
+  const double xt = t[2] * fmin(lx, fmax(-lx, t[0] / t[2]));
+  const double yt = t[2] * fmin(ly, fmax(-ly, t[1] / t[2]));
+  const double J00 = c.fx / t[2], J02 = -c.fx * xt / (t[2] * t[2]);
+  const double J11 = c.fy / t[2], J12 = -c.fy * yt / (t[2] * t[2]);
+  double M[2][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    M[0][b] = J00 * c.V[b] + J02 * c.V[8 + b];
+    M[1][b] = J11 * c.V[4 + b] + J12 * c.V[8 + b];
+  }
+  double N[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      N[a][b] = (M[a][0] * R[0][b] + M[a][1] * R[1][b] + M[a][2] * R[2][b]) * s[b];
+  const double a2 = N[0][0] * N[0][0] + N[0][1] * N[0][1] + N[0][2] * N[0][2] + 0.3;
+  const double b2 = N[0][0] * N[1][0] + N[0][1] * N[1][1] + N[0][2] * N[1][2];
+  const double c2 = N[1][0] * N[1][0] + N[1][1] * N[1][1] + N[1][2] * N[1][2] + 0.3;
+  const double det = a2 * c2 - b2 * b2;
+  r.A = (float)(c2 / det);
+  r.B = (float)(-b2 / det);
+  r.C = (float)(a2 / det);
+  const double u = c.fx * t[0] / t[2] + c.cx;
+  const double v = c.fy * t[1] / t[2] + c.cy;
+  r.u_hi = (float)u;
+  r.v_hi = (float)v;
+  r.u_lo = __double2half(u - (double)r.u_hi);
+  r.v_lo = __double2half(v - (double)r.v_hi);
+  return r;
+}
+
+template <int DEG>
+__global__ void __launch_bounds__(256) project_kernel(const __grid_constant__ ProjectArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const float4 po = a.pos_opa[i];
+  const float4 sc = a.scale[i];
+  const float4 q = a.rot[i];
+  const bool kept = a.keep == nullptr || a.keep[i] != 0;
+  const float o_eff = kept ? po.w : 0.f;
+  const float keepf = kept ? 1.f : 0.f;
+  using L = SHLayout<DEG>;
+  float coef[4 * L::K4];
+#pragma unroll
+  for (int j = 0; j < L::K4; ++j) {
+    const float4 c4 = a.sh[(size_t)j * a.n + i];
+    coef[4 * j + 0] = c4.x; coef[4 * j + 1] = c4.y; coef[4 * j + 2] = c4.z; coef[4 * j + 3] = c4.w;
+  }
+  for (int v = 0; v < a.num_views; ++v) {
+    const CamParams& c = a.cam[v];
+    const size_t o = (size_t)(a.view_offset + v) * a.n + i;
+    const KeyResult k = key_chain(c, po.x, po.y, po.z, o_eff, sc.x * keepf, sc.y * keepf,
+                                  sc.z * keepf, q);
+    if (!k.visible) {
+      a.xy_depth[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a.conic_opa[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a.rgb[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a.box[o] = make_uint2(1u, 1u);
+      a.tiles[o] = 0u;
+      continue;
+    }
+    const Records r = accurate_records(c, po, sc, q, keepf);
+    // colour: d = (p − c_cam)/‖p − c_cam‖, col = Σ Y_k(d) sh_k + 0.5, clamp ≥ 0
+    float dx = po.x - c.campos[0], dy = po.y - c.campos[1], dz = po.z - c.campos[2];
+    const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+    dx *= inv; dy *= inv; dz *= inv;
+    float Y[L::NC];
+    sh_eval<DEG>(dx, dy, dz, Y);
+    float col[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+    for (int kk = 0; kk < L::NC; ++kk)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) col[ch] += Y[kk] * coef[3 * kk + ch];
+    int bits = 0;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+      if (col[ch] < 0.f) { bits |= 1 << ch; col[ch] = 0.f; }
+    const __half2 lo = __halves2half2(r.u_lo, r.v_lo);
+    a.xy_depth[o] = make_float4(r.u_hi, r.v_hi, k.z, __uint_as_float(*(const uint32_t*)&lo));
+    a.conic_opa[o] = make_float4(r.A, r.B, r.C, o_eff);
+    a.rgb[o] = make_float4(col[0], col[1], col[2], (float)bits);
+    a.box[o] = make_uint2((uint32_t)k.x0 | ((uint32_t)k.x1 << 16), (uint32_t)k.y0 | ((uint32_t)k.y1 << 16));
+    a.tiles[o] = (uint32_t)((k.x1 / TILE - k.x0 / TILE + 1) * (k.y1 / TILE - k.y0 / TILE + 1));
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_degree,
+                           const float4* pos_opa, const float4* scale, const float4* rot,
+                           const float4* sh, const uint8_t* keep, float4* xy_depth,
+                           float4* conic_opa, float4* rgb, uint2* box, uint32_t* tiles,
+                           cudaStream_t s) {
+  for (int v0 = 0; v0 < num_views; v0 += MAXV) {
+    ProjectArgs a;
+    a.num_views = num_views - v0 < MAXV ? num_views - v0 : MAXV;
+    for (int v = 0; v < a.num_views; ++v) a.cam[v] = cams[v0 + v];
+    a.n = n; a.view_offset = v0;
+    a.pos_opa = pos_opa; a.scale = scale; a.rot = rot; a.sh = sh; a.keep = keep;
+    a.xy_depth = xy_depth; a.conic_opa = conic_opa; a.rgb = rgb; a.box = box; a.tiles = tiles;
+    const int grid = div_up(n, 256);
+    switch (sh_degree) {
+      case 0: project_kernel<0><<<grid, 256, 0, s>>>(a); break;
+      case 1: project_kernel<1><<<grid, 256, 0, s>>>(a); break;
+      case 2: project_kernel<2><<<grid, 256, 0, s>>>(a); break;
+      default: project_kernel<3><<<grid, 256, 0, s>>>(a); break;
+    }
+    launch_counted();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace dass

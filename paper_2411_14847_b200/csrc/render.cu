@@ -1,0 +1,546 @@
+// render.cu — dass_render_fwd / dass_render_bwd (Eq. 8 P:349-351 and its
+// reverse-mode derivative).
+//
+// Tile kernels: one CTA per 16×16 tile, NT = 256/PPT threads, each thread
+// owning PPT pixels of one column.  The tile's sorted list is streamed in
+// batches of NT entries staged into shared memory (gathered by sorted id), in
+// a tile-local frame: u_rel = (u_hi − tileX0) + u_lo keeps the mean offset
+// accurate to ~1e-7 px, and the integer pixel box becomes a 16+16-bit
+// column/row mask so the per-pixel box test (A05) is one LOP3 + compare.
+//
+// Backward reduction (hard part 2): per (warp, entry) the 9 per-pixel
+// gradient terms are summed with a reduce-scatter butterfly (12 SHFL for 9
+// values instead of 45), skipped when no lane of the warp contributes; the
+// warp result is added into a shared-memory accumulator of the batch entry,
+// and the batch is flushed with two 128-bit vector reductions
+// (red.global.add.v4.f32) + one scalar per Gaussian and tile.
+//
+// The per-pixel terms are accumulated in a "moment" form that folds the
+// per-Gaussian constants out of the pixel loop: with e = G·∂L/∂α (0 when α is
+// clamped), the pixel contributes (e·dx, e·dy, e·dx², e·dx·dy, e·dy², e,
+// αT·g_r, αT·g_g, αT·g_b), and the preprocess kernel forms
+// ∂L/∂u = −o(A Σe·dx + B Σe·dy), ∂L/∂A = −½ o Σe·dx², … (exact algebra).
+#include "common.cuh"
+#include "sh.cuh"
+
+namespace dass {
+namespace {
+
+struct TileRec {   // 40 B per staged entry
+  float2 uv;       // tile-local mean
+  float4 co;       // A, B, C, o
+  float4 cm;       // r, g, b, box mask bits (x: bits 0..15, y: bits 16..31)
+};
+
+__device__ __forceinline__ uint32_t box_mask(uint2 b, int tx0, int ty0) {
+  const int x0 = max((int)(b.x & 0xFFFFu) - tx0, 0), x1 = min((int)(b.x >> 16) - tx0, TILE - 1);
+  const int y0 = max((int)(b.y & 0xFFFFu) - ty0, 0), y1 = min((int)(b.y >> 16) - ty0, TILE - 1);
+  if (x0 > x1 || y0 > y1) return 0u;
+  const uint32_t mx = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
+  const uint32_t my = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
+  return mx | (my << 16);
+}
+
+__device__ __forceinline__ TileRec stage(uint32_t id, const float4* __restrict__ xy_depth,
+                                         const float4* __restrict__ conic_opa,
+                                         const float4* __restrict__ rgb,
+                                         const uint2* __restrict__ box, int tx0, int ty0) {
+  TileRec r;
+  const float4 xy = xy_depth[id];
+  const uint32_t lo_bits = __float_as_uint(xy.w);
+  const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
+  r.uv.x = __fadd_rn(xy.x - (float)tx0, __low2float(lo));
+  r.uv.y = __fadd_rn(xy.y - (float)ty0, __high2float(lo));
+  r.co = conic_opa[id];
+  const float4 c = rgb[id];
+  r.cm = make_float4(c.x, c.y, c.z, __uint_as_float(box_mask(box[id], tx0, ty0)));
+  return r;
+}
+
+// ------------------------------------------------------------- forward ----
+template <int PPT>
+__global__ void __launch_bounds__(256 / PPT) render_fwd_kernel(
+    const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
+    const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
+    const uint2* __restrict__ box, float3 bg, float* __restrict__ out_img,
+    float* __restrict__ out_T, uint32_t* __restrict__ out_last) {
+  constexpr int NT = 256 / PPT;
+  __shared__ TileRec s_rec[NT];
+  const int tile = blockIdx.x;
+  const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
+  const int tx0 = txi * TILE, ty0 = tyi * TILE;
+  const int t = threadIdx.x;
+  const int lx = t & 15, ly0 = (t >> 4) * PPT;
+  const int X = tx0 + lx;
+  const uint2 range = ranges[tile];
+  float T[PPT], C[PPT][3];
+  uint32_t last[PPT], pm[PPT];
+  bool done[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int Y = ty0 + ly0 + p;
+    T[p] = 1.f; C[p][0] = C[p][1] = C[p][2] = 0.f;
+    last[p] = range.x;
+    pm[p] = (1u << lx) | (1u << (16 + ly0 + p));
+    done[p] = !(X < cam.W && Y < cam.H);
+  }
+  const float fx = (float)lx;
+  for (uint32_t b0 = range.x; b0 < range.y; b0 += NT) {
+    bool alive = false;
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) alive |= !done[p];
+    if (__syncthreads_count(alive) == 0) break;
+    const uint32_t idx = b0 + t;
+    if (idx < range.y) s_rec[t] = stage(ids[idx], xy_depth, conic_opa, rgb, box, tx0, ty0);
+    __syncthreads();
+    const int cnt = min((uint32_t)NT, range.y - b0);
+    for (int j = 0; j < cnt; ++j) {
+      const TileRec r = s_rec[j];
+      const uint32_t m = __float_as_uint(r.cm.w);
+      const float dx = r.uv.x - fx;
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        if (done[p] || (m & pm[p]) != pm[p]) continue;
+        const float dy = r.uv.y - (float)(ly0 + p);
+        const float power = splat_power(r.co.x, r.co.y, r.co.z, dx, dy);
+        if (power > 0.f) continue;
+        const float alpha = splat_alpha(r.co.w, splat_exp(power));
+        if (alpha < ALPHA_MIN) continue;
+        const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
+        if (tn < T_MIN) { done[p] = true; continue; }
+        const float w = alpha * T[p];
+        C[p][0] += r.cm.x * w; C[p][1] += r.cm.y * w; C[p][2] += r.cm.z * w;
+        T[p] = tn;
+        last[p] = b0 + j + 1;
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int Y = ty0 + ly0 + p;
+    if (X < cam.W && Y < cam.H) {
+      const size_t pix = (size_t)Y * cam.W + X, np = (size_t)cam.W * cam.H;
+      out_img[pix] = C[p][0] + T[p] * bg.x;
+      out_img[np + pix] = C[p][1] + T[p] * bg.y;
+      out_img[2 * np + pix] = C[p][2] + T[p] * bg.z;
+      out_T[pix] = T[p];
+      out_last[pix] = last[p];
+    }
+  }
+}
+
+// ------------------------------------------------ backward: raster part ----
+// 9 values → each lane ends with the warp sum of one value index (or a pad).
+// Returns the index (0..8) the lane owns, or −1.
+__device__ __forceinline__ int reduce_scatter9(const float (&v)[9], float& out) {
+  const uint32_t lane = lane_id();
+  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4, b2 = lane & 2;
+  float r[6];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const float lo_v = v[i];
+    const float hi_v = i + 5 < 9 ? v[i + 5] : 0.f;
+    const float send = b16 ? lo_v : hi_v;
+    const float keep = b16 ? hi_v : lo_v;
+    r[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  r[5] = 0.f;
+  float s[4];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float send = b8 ? r[i] : r[i + 3];
+    const float keep = b8 ? r[i + 3] : r[i];
+    s[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  s[3] = 0.f;
+  float q[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b4 ? s[i] : s[i + 2];
+    const float keep = b4 ? s[i + 2] : s[i];
+    q[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const float send = b2 ? q[0] : q[1];
+    const float keep = b2 ? q[1] : q[0];
+    out = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  out += __shfl_xor_sync(0xffffffffu, out, 1);
+  const int pos = (b8 ? 3 : 0) + (b4 ? 2 : 0) + (b2 ? 1 : 0);
+  // valid positions inside the group of 5: b8=0 → {0,1,2}; b8=1 → {3,4}
+  const bool valid = (lane & 1) == 0 && (b8 ? pos <= 4 : pos <= 2);
+  const int idx = (b16 ? 5 : 0) + pos;
+  return (valid && idx < 9) ? idx : -1;
+}
+
+template <int PPT>
+__global__ void __launch_bounds__(256 / PPT) render_bwd_raster_kernel(
+    const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
+    const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
+    const uint2* __restrict__ box, float3 bg, const float* __restrict__ out_T,
+    const uint32_t* __restrict__ out_last, const float* __restrict__ dL_dimg,
+    float4* __restrict__ g2d) {
+  constexpr int NT = 256 / PPT;
+  __shared__ TileRec s_rec[NT];
+  __shared__ uint32_t s_id[NT];
+  __shared__ float s_acc[NT][9];
+  __shared__ uint32_t s_maxlast;
+  const int tile = blockIdx.x;
+  const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
+  const int tx0 = txi * TILE, ty0 = tyi * TILE;
+  const int t = threadIdx.x;
+  const int lx = t & 15, ly0 = (t >> 4) * PPT;
+  const int X = tx0 + lx;
+  const uint2 range = ranges[tile];
+  if (t == 0) s_maxlast = range.x;
+  __syncthreads();
+  float T[PPT], S[PPT][3], g[PPT][3], Tbg[PPT][3];
+  uint32_t last[PPT], pm[PPT];
+  uint32_t mylast = range.x;
+  const size_t np = (size_t)cam.W * cam.H;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int Y = ty0 + ly0 + p;
+    pm[p] = (1u << lx) | (1u << (16 + ly0 + p));
+    S[p][0] = S[p][1] = S[p][2] = 0.f;
+    if (X < cam.W && Y < cam.H) {
+      const size_t pix = (size_t)Y * cam.W + X;
+      T[p] = out_T[pix];
+      last[p] = out_last[pix];
+      g[p][0] = dL_dimg[pix]; g[p][1] = dL_dimg[np + pix]; g[p][2] = dL_dimg[2 * np + pix];
+    } else {
+      T[p] = 1.f; last[p] = range.x;
+      g[p][0] = g[p][1] = g[p][2] = 0.f;
+    }
+    Tbg[p][0] = T[p] * bg.x; Tbg[p][1] = T[p] * bg.y; Tbg[p][2] = T[p] * bg.z;
+    mylast = max(mylast, last[p]);
+  }
+  atomicMax(&s_maxlast, mylast);
+  __syncthreads();
+  const uint32_t end = s_maxlast;
+  const float fx = (float)lx;
+  for (uint32_t b1 = end; b1 > range.x;) {
+    const uint32_t b0 = b1 - range.x > (uint32_t)NT ? b1 - NT : range.x;
+    const int cnt = (int)(b1 - b0);
+    __syncthreads();  // previous batch fully flushed
+    if (t < cnt) {
+      const uint32_t id = ids[b0 + t];
+      s_id[t] = id;
+      s_rec[t] = stage(id, xy_depth, conic_opa, rgb, box, tx0, ty0);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) s_acc[t][k] = 0.f;
+    }
+    __syncthreads();
+    for (int j = cnt - 1; j >= 0; --j) {
+      const TileRec r = s_rec[j];
+      const uint32_t m = __float_as_uint(r.cm.w);
+      const uint32_t gidx = b0 + j;
+      const float dx = r.uv.x - fx;
+      float v[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) v[k] = 0.f;
+      bool any = false;
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        if (gidx >= last[p] || (m & pm[p]) != pm[p]) continue;
+        const float dy = r.uv.y - (float)(ly0 + p);
+        const float power = splat_power(r.co.x, r.co.y, r.co.z, dx, dy);
+        if (power > 0.f) continue;
+        const float G = splat_exp(power);
+        const float oG = __fmul_rn(r.co.w, G);
+        const float alpha = fminf(ALPHA_MAX, oG);
+        if (alpha < ALPHA_MIN) continue;
+        any = true;
+        const float inv = __frcp_rn(1.f - alpha);
+        T[p] *= inv;                       // transmittance before this entry
+        const float w = alpha * T[p];
+        float dLda = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const float col = (&r.cm.x)[ch];
+          dLda += g[p][ch] * (col * T[p] - (S[p][ch] + Tbg[p][ch]) * inv);
+          S[p][ch] += col * w;
+          v[6 + ch] += w * g[p][ch];
+        }
+        const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
+        const float ex = e * dx, ey = e * dy;
+        v[0] += ex; v[1] += ey; v[2] += ex * dx; v[3] += ex * dy; v[4] += ey * dy; v[5] += e;
+      }
+      if (__any_sync(0xffffffffu, any)) {
+        float sum;
+        const int k = reduce_scatter9(v, sum);
+        if (k >= 0 && sum != 0.f) atomicAdd(&s_acc[j][k], sum);
+      }
+    }
+    __syncthreads();
+    if (t < cnt) {
+      const float* a = s_acc[t];
+      bool nz = false;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) nz |= a[k] != 0.f;
+      if (nz) {
+        float4* dst = g2d + 3 * (size_t)s_id[t];
+        red_add_v4(dst, make_float4(a[0], a[1], a[2], a[3]));
+        red_add_v4(dst + 1, make_float4(a[4], a[5], a[6], a[7]));
+        atomicAdd(&dst[2].x, a[8]);
+      }
+    }
+    b1 = b0;
+  }
+}
+
+// --------------------------------------------- backward: preprocess part ----
+// Per Gaussian: 2D moments → ∂L/∂(u, v, A, B, C, o, rgb) → chain through
+// Eqs. 5-7 and the SH colour to ∂L/∂(p, s, q, o, sh); accumulate (+=).
+template <int DEG>
+__global__ void __launch_bounds__(256) preprocess_bwd_kernel(
+    const __grid_constant__ CamParams cam, int n, const float4* __restrict__ pos_opa,
+    const float4* __restrict__ scale, const float4* __restrict__ rot,
+    const float4* __restrict__ sh, const uint8_t* __restrict__ keep,
+    const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
+    const uint2* __restrict__ box, const float4* __restrict__ g2d, float4* g_pos_opa,
+    float4* g_scale, float4* g_rot, float4* g_sh, float* gradstat_sum, uint32_t* gradstat_cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint2 bx = box[i];
+  if ((bx.x & 0xFFFFu) > (bx.x >> 16)) return;  // culled in this view
+  const float4 m0 = g2d[3 * (size_t)i], m1 = g2d[3 * (size_t)i + 1], m2 = g2d[3 * (size_t)i + 2];
+  const float4 co = conic_opa[i];
+  const float A = co.x, B = co.y, Cc = co.z, o = co.w;
+  // 2D gradients from the moments
+  const float gu = -o * (A * m0.x + B * m0.y);
+  const float gv = -o * (B * m0.x + Cc * m0.y);
+  const float gA = -0.5f * o * m0.z;
+  const float gB = -o * m0.w;
+  const float gC = -0.5f * o * m1.x;
+  const float go = m1.y;
+  const float4 cl = rgb[i];
+  const int bits = (int)cl.w;
+  const float gcol[3] = {(bits & 1) ? 0.f : m1.z, (bits & 2) ? 0.f : m1.w, (bits & 4) ? 0.f : m2.x};
+  if (gradstat_sum) {
+    const float a = gu * 0.5f * cam.W, b = gv * 0.5f * cam.H;
+    gradstat_sum[i] += sqrtf(a * a + b * b);
+  }
+  if (gradstat_cnt) gradstat_cnt[i] += 1u;
+  const bool kp = keep == nullptr || keep[i] != 0;
+  const float4 po = pos_opa[i];
+  float gp[3] = {0.f, 0.f, 0.f};
+  // ---- colour / SH
+  {
+    float dx = po.x - cam.campos[0], dy = po.y - cam.campos[1], dz = po.z - cam.campos[2];
+    const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
+    const float inv = 1.f / dist;
+    dx *= inv; dy *= inv; dz *= inv;
+    using L = SHLayout<DEG>;
+    float Y[L::NC];
+    sh_eval<DEG>(dx, dy, dz, Y);
+    float wk[L::NC];
+#pragma unroll
+    for (int k = 0; k < L::NC; ++k) wk[k] = 0.f;
+#pragma unroll
+    for (int j = 0; j < L::K4; ++j) {
+      const size_t off = (size_t)j * n + i;
+      const float4 c4 = sh[off];
+      float4 gg = g_sh ? g_sh[off] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int f = 4 * j + e;
+        if (f < L::NF) {
+          const int k = f / 3, ch = f % 3;
+          wk[k] += gcol[ch] * (&c4.x)[e];
+          (&gg.x)[e] += Y[k] * gcol[ch];
+        }
+      }
+      if (g_sh) g_sh[off] = gg;
+    }
+    if (DEG > 0) {
+      const float3 gd = sh_dir_grad<DEG>(dx, dy, dz, wk);
+      const float dd = dx * gd.x + dy * gd.y + dz * gd.z;
+      gp[0] += (gd.x - dx * dd) * inv;
+      gp[1] += (gd.y - dy * dd) * inv;
+      gp[2] += (gd.z - dz * dd) * inv;
+    }
+  }
+  if (!g_pos_opa && !g_scale && !g_rot) return;
+  // ---- recompute the projection quantities (fp32)
+  const float* V = cam.V;
+  float t[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) t[a] = V[4 * a] * po.x + V[4 * a + 1] * po.y + V[4 * a + 2] * po.z + V[4 * a + 3];
+  const float4 q = rot[i];
+  const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+  const float qi = 1.f / qn;
+  const float w = q.x * qi, x = q.y * qi, y = q.z * qi, z = q.w * qi;
+  float R[3][3];
+  R[0][0] = 1.f - 2.f * (y * y + z * z); R[0][1] = 2.f * (x * y - w * z); R[0][2] = 2.f * (x * z + w * y);
+  R[1][0] = 2.f * (x * y + w * z); R[1][1] = 1.f - 2.f * (x * x + z * z); R[1][2] = 2.f * (y * z - w * x);
+  R[2][0] = 2.f * (x * z - w * y); R[2][1] = 2.f * (y * z + w * x); R[2][2] = 1.f - 2.f * (x * x + y * y);
+  const float4 sc = scale[i];
+  const float s[3] = {kp ? sc.x : 0.f, kp ? sc.y : 0.f, kp ? sc.z : 0.f};
+  float Sig[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      Sig[a][b] = R[a][0] * s[0] * s[0] * R[b][0] + R[a][1] * s[1] * s[1] * R[b][1] +
+                  R[a][2] * s[2] * s[2] * R[b][2];
+  const float lx = 1.3f * cam.W / (2.f * cam.fx), ly = 1.3f * cam.H / (2.f * cam.fy);
+  const float txtz = t[0] / t[2], tytz = t[1] / t[2];
+  const bool clx = txtz < -lx || txtz > lx, cly = tytz < -ly || tytz > ly;
+  const float xt = t[2] * fminf(lx, fmaxf(-lx, txtz));
+  const float yt = t[2] * fminf(ly, fmaxf(-ly, tytz));
+  const float tz = t[2], tz2 = tz * tz, tz3 = tz2 * tz;
+  const float J00 = cam.fx / tz, J02 = -cam.fx * xt / tz2;
+  const float J11 = cam.fy / tz, J12 = -cam.fy * yt / tz2;
+  float M[2][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    M[0][b] = J00 * V[b] + J02 * V[8 + b];
+    M[1][b] = J11 * V[4 + b] + J12 * V[8 + b];
+  }
+  // conic → Σ': Gs = −K Ĝ K, Ĝ = [[gA, gB/2],[gB/2, gC]]
+  const float K00 = A, K01 = B, K11 = Cc;
+  const float G00 = gA, G01 = 0.5f * gB, G11 = gC;
+  const float KG00 = K00 * G00 + K01 * G01, KG01 = K00 * G01 + K01 * G11;
+  const float KG10 = K01 * G00 + K11 * G01, KG11 = K01 * G01 + K11 * G11;
+  const float Gs00 = -(KG00 * K00 + KG01 * K01);
+  const float Gs01 = -(KG00 * K01 + KG01 * K11);
+  const float Gs11 = -(KG10 * K01 + KG11 * K11);
+  const float Gs[2][2] = {{Gs00, Gs01}, {Gs01, Gs11}};
+  // dL/dΣ = Mᵀ Gs M ; dL/dM = 2 Gs M Σ
+  float GM1[2][3];  // Gs M
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) GM1[a][b] = Gs[a][0] * M[0][b] + Gs[a][1] * M[1][b];
+  float GSig[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) GSig[a][b] = M[0][a] * GM1[0][b] + M[1][a] * GM1[1][b];
+  float GM[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      GM[a][b] = 2.f * (GM1[a][0] * Sig[0][b] + GM1[a][1] * Sig[1][b] + GM1[a][2] * Sig[2][b]);
+  // dL/dJ = dL/dM Wᵀ (rotation part of the view matrix)
+  const float GJ00 = GM[0][0] * V[0] + GM[0][1] * V[1] + GM[0][2] * V[2];
+  const float GJ02 = GM[0][0] * V[8] + GM[0][1] * V[9] + GM[0][2] * V[10];
+  const float GJ11 = GM[1][0] * V[4] + GM[1][1] * V[5] + GM[1][2] * V[6];
+  const float GJ12 = GM[1][0] * V[8] + GM[1][1] * V[9] + GM[1][2] * V[10];
+  float gt[3] = {0.f, 0.f, 0.f};
+  gt[2] += GJ00 * (-cam.fx / tz2) + GJ11 * (-cam.fy / tz2);
+  if (!clx) {
+    gt[0] += GJ02 * (-cam.fx / tz2);
+    gt[2] += GJ02 * (2.f * cam.fx * t[0] / tz3);
+  } else {
+    gt[2] += GJ02 * (cam.fx * xt / tz3);
+  }
+  if (!cly) {
+    gt[1] += GJ12 * (-cam.fy / tz2);
+    gt[2] += GJ12 * (2.f * cam.fy * t[1] / tz3);
+  } else {
+    gt[2] += GJ12 * (cam.fy * yt / tz3);
+  }
+  gt[0] += gu * cam.fx / tz;
+  gt[2] += gu * (-cam.fx * t[0] / tz2);
+  gt[1] += gv * cam.fy / tz;
+  gt[2] += gv * (-cam.fy * t[1] / tz2);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) gp[a] += V[a] * gt[0] + V[4 + a] * gt[1] + V[8 + a] * gt[2];
+  if (g_pos_opa) {
+    float4 gpo = g_pos_opa[i];
+    gpo.x += gp[0]; gpo.y += gp[1]; gpo.z += gp[2];
+    gpo.w += kp ? go : 0.f;
+    g_pos_opa[i] = gpo;
+  }
+  // Σ = R diag(s²) Rᵀ : dL/ds_k = 2 s_k (Rᵀ GΣ R)_kk ; dL/dR = 2 GΣ R diag(s²)
+  float GR[3][3];
+  float gs[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float GSr[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) GSr[a] = GSig[a][0] * R[0][k] + GSig[a][1] * R[1][k] + GSig[a][2] * R[2][k];
+    gs[k] = 2.f * s[k] * (R[0][k] * GSr[0] + R[1][k] * GSr[1] + R[2][k] * GSr[2]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) GR[a][k] = 2.f * GSr[a] * s[k] * s[k];
+  }
+  if (g_scale) {
+    float4 g4 = g_scale[i];
+    if (kp) { g4.x += gs[0]; g4.y += gs[1]; g4.z += gs[2]; }
+    g_scale[i] = g4;
+  }
+  if (g_rot) {
+    float gq[4];
+    gq[0] = GR[0][1] * (-2.f * z) + GR[0][2] * (2.f * y) + GR[1][0] * (2.f * z) + GR[1][2] * (-2.f * x) +
+            GR[2][0] * (-2.f * y) + GR[2][1] * (2.f * x);
+    gq[1] = GR[0][1] * (2.f * y) + GR[0][2] * (2.f * z) + GR[1][0] * (2.f * y) + GR[1][1] * (-4.f * x) +
+            GR[1][2] * (-2.f * w) + GR[2][0] * (2.f * z) + GR[2][1] * (2.f * w) + GR[2][2] * (-4.f * x);
+    gq[2] = GR[0][0] * (-4.f * y) + GR[0][1] * (2.f * x) + GR[0][2] * (2.f * w) + GR[1][0] * (2.f * x) +
+            GR[1][2] * (2.f * z) + GR[2][0] * (-2.f * w) + GR[2][1] * (2.f * z) + GR[2][2] * (-4.f * y);
+    gq[3] = GR[0][0] * (-4.f * z) + GR[0][1] * (-2.f * w) + GR[0][2] * (2.f * x) + GR[1][0] * (2.f * w) +
+            GR[1][1] * (-4.f * z) + GR[1][2] * (2.f * y) + GR[2][0] * (2.f * x) + GR[2][1] * (2.f * y);
+    const float dot = w * gq[0] + x * gq[1] + y * gq[2] + z * gq[3];
+    float4 g4 = g_rot[i];
+    g4.x += (gq[0] - w * dot) * qi;
+    g4.y += (gq[1] - x * dot) * qi;
+    g4.z += (gq[2] - y * dot) * qi;
+    g4.w += (gq[3] - z * dot) * qi;
+    g_rot[i] = g4;
+  }
+}
+
+constexpr int FWD_PPT = 1;
+constexpr int BWD_PPT = 1;
+
+}  // namespace
+
+cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
+                              const float4* xy_depth, const float4* conic_opa, const float4* rgb,
+                              const uint2* box, float3 bg, float* out_img, float* out_T,
+                              uint32_t* out_last, cudaStream_t s) {
+  const int ntiles = cam.tiles_x * cam.tiles_y;
+  render_fwd_kernel<FWD_PPT><<<ntiles, 256 / FWD_PPT, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa,
+                                                              rgb, box, bg, out_img, out_T, out_last);
+  launch_counted();
+  return cudaGetLastError();
+}
+
+size_t render_bwd_workspace(int n) { return sizeof(float4) * 3 * (size_t)(n > 0 ? n : 1); }
+
+cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const float4* pos_opa,
+                              const float4* scale, const float4* rot, const float4* sh,
+                              const uint8_t* keep, const uint2* ranges, const uint32_t* ids,
+                              const float4* xy_depth, const float4* conic_opa, const float4* rgb,
+                              const uint2* box, float3 bg, const float* out_T,
+                              const uint32_t* out_last, const float* dL_dimg, void* ws,
+                              float4* g_pos_opa, float4* g_scale, float4* g_rot, float4* g_sh,
+                              float* gradstat_sum, uint32_t* gradstat_cnt, cudaStream_t s) {
+  float4* g2d = (float4*)ws;
+  cudaError_t e = cudaMemsetAsync(g2d, 0, render_bwd_workspace(n), s);
+  if (e != cudaSuccess) return e;
+  const int ntiles = cam.tiles_x * cam.tiles_y;
+  render_bwd_raster_kernel<BWD_PPT><<<ntiles, 256 / BWD_PPT, 0, s>>>(
+      cam, ranges, ids, xy_depth, conic_opa, rgb, box, bg, out_T, out_last, dL_dimg, g2d);
+  launch_counted();
+  const int grid = div_up(n, 256);
+  switch (sh_degree) {
+#define PRE(D)                                                                                    \
+  preprocess_bwd_kernel<D><<<grid, 256, 0, s>>>(cam, n, pos_opa, scale, rot, sh, keep, conic_opa, \
+                                                rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh,   \
+                                                gradstat_sum, gradstat_cnt)
+    case 0: PRE(0); break;
+    case 1: PRE(1); break;
+    case 2: PRE(2); break;
+    default: PRE(3); break;
+#undef PRE
+  }
+  launch_counted();
+  return cudaGetLastError();
+}
+
+}  // namespace dass

@@ -1,0 +1,222 @@
+"""Thin Python binding of libdass.so (include/dass.h), same names as the C-ABI.
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels of libdass.so.  Tensors must be CUDA tensors of the documented dtype
+and layout; the binding passes `tensor.data_ptr()` and the current torch
+stream.  There is no CPU fallback: if libdass.so is missing or a GPU is not
+available, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdass.so")
+
+DASS_OK = 0
+DASS_ERR_INVALID_ARG = 1
+DASS_ERR_DATA = 2
+DASS_ERR_NUMERICAL = 3
+DASS_ERR_CAPACITY = 4
+DASS_ERR_CUDA = 5
+
+EXPORTS = (
+    "dass_status_string", "dass_last_error", "dass_abi_version", "dass_kernel_launches",
+    "dass_apply_shift", "dass_apply_shift_bwd", "dass_project", "dass_project_views",
+    "dass_bin_sort_workspace", "dass_bin_sort", "dass_render_fwd", "dass_render_bwd_workspace",
+    "dass_render_bwd", "dass_error_map", "dass_render_stats",
+)
+
+
+class DassError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: status {status}: {msg}")
+        self.status = status
+
+
+class dass_camera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32),
+                ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("viewmat", C.c_float * 12), ("near_plane", C.c_float),
+                ("full_proj", C.c_float * 16)]
+
+
+def camera_struct(cam) -> dass_camera:
+    """From any object with width/height/fx/fy/cx/cy/viewmat/near/full_proj."""
+    c = dass_camera()
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    vm = np.asarray(cam.viewmat, np.float32).reshape(12)
+    for i in range(12):
+        c.viewmat[i] = float(vm[i])
+    c.near_plane = float(getattr(cam, "near", getattr(cam, "near_plane", 0.2)))
+    fp = np.asarray(cam.full_proj, np.float32).reshape(16)
+    for i in range(16):
+        c.full_proj[i] = float(fp[i])
+    return c
+
+
+_lib = None
+
+
+def lib():
+    """Load libdass.so; raise loudly if it is missing (no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2411_14847_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        L.dass_status_string.restype = C.c_char_p
+        L.dass_last_error.restype = C.c_char_p
+        L.dass_kernel_launches.restype = C.c_uint64
+        P = C.c_void_p
+        i32, i64 = C.c_int32, C.c_int64
+        L.dass_apply_shift.argtypes = [i32, P, P, P, P, P, P, P, P]
+        L.dass_apply_shift_bwd.argtypes = [i32, P, P, P, P, P, P, P, P]
+        L.dass_project.argtypes = [P, i32, i32, P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_project_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_bin_sort_workspace.argtypes = [i32, i32, i64, P]
+        L.dass_bin_sort.argtypes = [P, i32, P, P, P, P, C.c_size_t, i64, P, P, P, P, P, P]
+        L.dass_render_fwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_render_bwd_workspace.argtypes = [i32, P]
+        L.dass_render_bwd.argtypes = [P, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
+                                      P, C.c_size_t, P, P, P, P, P, P, P]
+        L.dass_error_map.argtypes = [P, P, P, C.c_float, P, P, i32, P, P, P]
+        L.dass_render_stats.argtypes = [P, P, P, P, P, P, P, P, P, P]
+        _lib = L
+    return _lib
+
+
+def _check(status: int, where: str):
+    if status != DASS_OK:
+        raise DassError(status, where, lib().dass_last_error().decode())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libdass takes CUDA tensors only (no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _cam(cam):
+    return cam if isinstance(cam, dass_camera) else camera_struct(cam)
+
+
+def kernel_launches() -> int:
+    return int(lib().dass_kernel_launches())
+
+
+def abi_version() -> int:
+    return int(lib().dass_abi_version())
+
+
+def dass_apply_shift(pos_opa, rot, mu, sigma, dyn_mask, pos_opa_out, rot_out, stream=None):
+    n = pos_opa.shape[0]
+    _check(lib().dass_apply_shift(n, _ptr(pos_opa), _ptr(rot), _ptr(mu), _ptr(sigma),
+                                  _ptr(dyn_mask), _ptr(pos_opa_out), _ptr(rot_out),
+                                  _stream(stream)), "dass_apply_shift")
+
+
+def dass_apply_shift_bwd(rot, sigma, dyn_mask, g_pos_out, g_rot_out, g_mu, g_sigma, stream=None):
+    n = rot.shape[0]
+    _check(lib().dass_apply_shift_bwd(n, _ptr(rot), _ptr(sigma), _ptr(dyn_mask), _ptr(g_pos_out),
+                                      _ptr(g_rot_out), _ptr(g_mu), _ptr(g_sigma),
+                                      _stream(stream)), "dass_apply_shift_bwd")
+
+
+def dass_project(cam, sh_degree, pos_opa, scale, rot, sh, keep_mask, xy_depth, conic_opa, rgb,
+                 box, tiles_touched, stream=None):
+    c = _cam(cam)
+    _check(lib().dass_project(C.byref(c), pos_opa.shape[0], sh_degree, _ptr(pos_opa), _ptr(scale),
+                              _ptr(rot), _ptr(sh), _ptr(keep_mask), _ptr(xy_depth),
+                              _ptr(conic_opa), _ptr(rgb), _ptr(box), _ptr(tiles_touched),
+                              _stream(stream)), "dass_project")
+
+
+def dass_project_views(cams, sh_degree, pos_opa, scale, rot, sh, keep_mask, xy_depth, conic_opa,
+                       rgb, box, tiles_touched, stream=None):
+    arr = (dass_camera * len(cams))(*[_cam(c) for c in cams])
+    _check(lib().dass_project_views(arr, len(cams), pos_opa.shape[0], sh_degree, _ptr(pos_opa),
+                                    _ptr(scale), _ptr(rot), _ptr(sh), _ptr(keep_mask),
+                                    _ptr(xy_depth), _ptr(conic_opa), _ptr(rgb), _ptr(box),
+                                    _ptr(tiles_touched), _stream(stream)), "dass_project_views")
+
+
+def dass_bin_sort_workspace(n, num_tiles, pair_capacity) -> int:
+    out = C.c_size_t(0)
+    _check(lib().dass_bin_sort_workspace(n, num_tiles, pair_capacity, C.byref(out)),
+           "dass_bin_sort_workspace")
+    return out.value
+
+
+def dass_bin_sort(cam, n, xy_depth, box, tiles_touched, ws, pair_capacity, sorted_keys,
+                  sorted_ids, tile_ranges, num_pairs_dev, host_mode=False, stream=None):
+    """Returns K in host mode (raises DassError(CAPACITY) on overflow), else None."""
+    c = _cam(cam)
+    k = C.c_int64(-1)
+    st = lib().dass_bin_sort(C.byref(c), n, _ptr(xy_depth), _ptr(box), _ptr(tiles_touched),
+                             _ptr(ws), ws.numel() * ws.element_size(), pair_capacity,
+                             _ptr(sorted_keys), _ptr(sorted_ids), _ptr(tile_ranges),
+                             _ptr(num_pairs_dev), C.byref(k) if host_mode else None,
+                             _stream(stream))
+    _check(st, "dass_bin_sort")
+    return k.value if host_mode else None
+
+
+def dass_render_fwd(cam, tile_ranges, sorted_ids, xy_depth, conic_opa, rgb, box, bg, out_img,
+                    out_T, out_last, stream=None):
+    c = _cam(cam)
+    b = None if bg is None else (C.c_float * 3)(*[float(x) for x in bg])
+    _check(lib().dass_render_fwd(C.byref(c), _ptr(tile_ranges), _ptr(sorted_ids), _ptr(xy_depth),
+                                 _ptr(conic_opa), _ptr(rgb), _ptr(box), b, _ptr(out_img),
+                                 _ptr(out_T), _ptr(out_last), _stream(stream)), "dass_render_fwd")
+
+
+def dass_render_bwd_workspace(n) -> int:
+    out = C.c_size_t(0)
+    _check(lib().dass_render_bwd_workspace(n, C.byref(out)), "dass_render_bwd_workspace")
+    return out.value
+
+
+def dass_render_bwd(cam, sh_degree, pos_opa, scale, rot, sh, keep_mask, tile_ranges, sorted_ids,
+                    xy_depth, conic_opa, rgb, box, bg, out_T, out_last, dL_dimg, ws, g_pos_opa,
+                    g_scale, g_rot, g_sh, gradstat_sum, gradstat_cnt, stream=None):
+    c = _cam(cam)
+    b = None if bg is None else (C.c_float * 3)(*[float(x) for x in bg])
+    _check(lib().dass_render_bwd(C.byref(c), pos_opa.shape[0], sh_degree, _ptr(pos_opa),
+                                 _ptr(scale), _ptr(rot), _ptr(sh), _ptr(keep_mask),
+                                 _ptr(tile_ranges), _ptr(sorted_ids), _ptr(xy_depth),
+                                 _ptr(conic_opa), _ptr(rgb), _ptr(box), b, _ptr(out_T),
+                                 _ptr(out_last), _ptr(dL_dimg), _ptr(ws),
+                                 ws.numel() * ws.element_size(), _ptr(g_pos_opa), _ptr(g_scale),
+                                 _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum), _ptr(gradstat_cnt),
+                                 _stream(stream)), "dass_render_bwd")
+
+
+def dass_error_map(cam, rendered, gt, gamma_err, err, dmask, n_base, pos_opa, s_err, stream=None):
+    c = _cam(cam)
+    _check(lib().dass_error_map(C.byref(c), _ptr(rendered), _ptr(gt), gamma_err, _ptr(err),
+                                _ptr(dmask), n_base, _ptr(pos_opa), _ptr(s_err), _stream(stream)),
+           "dass_error_map")
+
+
+def dass_render_stats(cam, tile_ranges, sorted_ids, xy_depth, conic_opa, box, out_T, out_last,
+                      counters, stream=None):
+    c = _cam(cam)
+    _check(lib().dass_render_stats(C.byref(c), _ptr(tile_ranges), _ptr(sorted_ids),
+                                   _ptr(xy_depth), _ptr(conic_opa), _ptr(box), _ptr(out_T),
+                                   _ptr(out_last), _ptr(counters), _stream(stream)),
+           "dass_render_stats")

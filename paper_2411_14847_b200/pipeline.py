@@ -1,0 +1,141 @@
+"""Device buffers and the per-view call sequence around libdass (plumbing).
+
+PyTorch supplies device memory and streams; every arithmetic step runs in the
+CUDA kernels behind `paper_2411_14847_b200.dass` (the C-ABI).  This module only
+allocates the documented layouts and calls the exports in order:
+
+  step:  [dass_apply_shift] → dass_project_views (all views, params read once)
+         → per view: dass_bin_sort (graph mode) → dass_render_fwd → dass_render_bwd
+         → [dass_apply_shift_bwd]
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import dass
+from .synth import sh_planes
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class DeviceScene:
+    pos_opa: "torch.Tensor"   # [N,4] f32
+    scale: "torch.Tensor"     # [N,4] f32
+    rot: "torch.Tensor"       # [N,4] f32
+    sh: "torch.Tensor"        # [K4,N,4] f32
+    sh_degree: int
+    dynamic: "torch.Tensor | None" = None  # [N] u8
+
+    @property
+    def n(self) -> int:
+        return self.pos_opa.shape[0]
+
+    @staticmethod
+    def from_host(scene, device="cuda", pin=False) -> "DeviceScene":
+        torch = _torch()
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        dyn = None if scene.dynamic is None else t(scene.dynamic.astype(np.uint8))
+        return DeviceScene(t(scene.pos_opa), t(scene.scale), t(scene.rot), t(scene.sh),
+                           scene.sh_degree, dyn)
+
+
+@dataclass
+class Grads:
+    pos_opa: "torch.Tensor"
+    scale: "torch.Tensor"
+    rot: "torch.Tensor"
+    sh: "torch.Tensor"
+    gradstat_sum: "torch.Tensor"
+    gradstat_cnt: "torch.Tensor"
+
+    @staticmethod
+    def zeros(n, sh_degree, device="cuda") -> "Grads":
+        torch = _torch()
+        f = lambda *s: torch.zeros(*s, dtype=torch.float32, device=device)
+        return Grads(f(n, 4), f(n, 4), f(n, 4), f(sh_planes(sh_degree), n, 4), f(n),
+                     torch.zeros(n, dtype=torch.int32, device=device))
+
+    def zero_(self):
+        for t in (self.pos_opa, self.scale, self.rot, self.sh, self.gradstat_sum, self.gradstat_cnt):
+            t.zero_()
+
+    def flat_views(self):
+        return [self.pos_opa, self.scale, self.rot, self.sh, self.gradstat_sum]
+
+
+class ViewRecords:
+    """Per-view projected records for V views of N Gaussians ([V,N,…] layout)."""
+
+    def __init__(self, num_views: int, n: int, device="cuda"):
+        torch = _torch()
+        self.V, self.n = num_views, n
+        f = lambda *s: torch.empty(*s, dtype=torch.float32, device=device)
+        self.xy_depth = f(num_views, n, 4)
+        self.conic_opa = f(num_views, n, 4)
+        self.rgb = f(num_views, n, 4)
+        self.box = torch.empty(num_views, n, 2, dtype=torch.int32, device=device)
+        self.tiles = torch.empty(num_views, n, dtype=torch.int32, device=device)
+
+    def view(self, v: int):
+        return self.xy_depth[v], self.conic_opa[v], self.rgb[v], self.box[v], self.tiles[v]
+
+
+class Raster:
+    """Scratch for one view at a time: sorted pairs, ranges, fwd outputs, bwd workspace."""
+
+    def __init__(self, width: int, height: int, n: int, capacity: int, device="cuda"):
+        torch = _torch()
+        self.W, self.H, self.n, self.capacity = width, height, n, capacity
+        self.num_tiles = ((width + 15) // 16) * ((height + 15) // 16)
+        ws = dass.dass_bin_sort_workspace(n, self.num_tiles, capacity)
+        self.sort_ws = torch.empty(max(ws, 16), dtype=torch.uint8, device=device)
+        self.sorted_ids = torch.empty(max(capacity, 1), dtype=torch.int32, device=device)
+        self.ranges = torch.empty(self.num_tiles, 2, dtype=torch.int32, device=device)
+        self.num_pairs = torch.zeros(2, dtype=torch.int32, device=device)
+        self.img = torch.empty(3, height, width, dtype=torch.float32, device=device)
+        self.T = torch.empty(height, width, dtype=torch.float32, device=device)
+        self.last = torch.empty(height, width, dtype=torch.int32, device=device)
+        bws = dass.dass_render_bwd_workspace(n)
+        self.bwd_ws = torch.empty(bws // 4, dtype=torch.float32, device=device)
+
+    def forward(self, cam, rec, host_mode=False, bg=None, sorted_keys=None):
+        xy, co, rgb, box, tiles = rec
+        K = dass.dass_bin_sort(cam, self.n, xy, box, tiles, self.sort_ws, self.capacity,
+                               sorted_keys, self.sorted_ids, self.ranges, self.num_pairs,
+                               host_mode=host_mode)
+        dass.dass_render_fwd(cam, self.ranges, self.sorted_ids, xy, co, rgb, box, bg, self.img,
+                             self.T, self.last)
+        return K
+
+    def backward(self, cam, scene: DeviceScene, rec, dL_dimg, grads: Grads, keep=None, bg=None,
+                 want=("pos", "scale", "rot", "sh", "stat")):
+        xy, co, rgb, box, tiles = rec
+        g = lambda name, t: t if name in want else None
+        dass.dass_render_bwd(cam, scene.sh_degree, scene.pos_opa, scene.scale, scene.rot,
+                             scene.sh, keep, self.ranges, self.sorted_ids, xy, co, rgb, box, bg,
+                             self.T, self.last, dL_dimg, self.bwd_ws, g("pos", grads.pos_opa),
+                             g("scale", grads.scale), g("rot", grads.rot), g("sh", grads.sh),
+                             g("stat", grads.gradstat_sum), g("stat", grads.gradstat_cnt))
+
+
+def project_all(cams, scene: DeviceScene, records: ViewRecords, keep=None):
+    dass.dass_project_views(cams, scene.sh_degree, scene.pos_opa, scene.scale, scene.rot,
+                            scene.sh, keep, records.xy_depth, records.conic_opa, records.rgb,
+                            records.box, records.tiles)
+
+
+def fwd_bwd_views(cams, scene: DeviceScene, records: ViewRecords, raster: Raster, dL_dimgs,
+                  grads: Grads, keep=None, bg=None):
+    """One fwd+bwd pass over `cams` (all §8(a) steps a2-a9): project all views
+    once, then per view bin/sort → composite → backward (+= into grads)."""
+    project_all(cams, scene, records, keep)
+    for v, cam in enumerate(cams):
+        rec = records.view(v)
+        raster.forward(cam, rec, bg=bg)
+        raster.backward(cam, scene, rec, dL_dimgs[v], grads, keep=keep, bg=bg)

@@ -1,0 +1,105 @@
+"""CPU-side checks of the C-ABI boundary (no GPU needed): libdass.so loads,
+exports every function include/dass.h declares, and validates its arguments
+before touching CUDA (status codes mirror SPEC's exit codes)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2411_14847_b200 import build as dass_build
+from paper_2411_14847_b200 import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dass.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    dass_build.build()
+    from paper_2411_14847_b200 import dass
+    return dass
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dass_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_six_calls_plus_helpers():
+    f = declared_functions()
+    for name in ("dass_project", "dass_bin_sort", "dass_render_fwd", "dass_render_bwd",
+                 "dass_apply_shift", "dass_error_map"):
+        assert name in f
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.check_output(["nm", "-D", "--defined-only", lib.LIB_PATH]).decode()
+    exported = set(re.findall(r"\bT (dass_\w+)", out))
+    declared = set(declared_functions())
+    assert declared <= exported, declared - exported
+    assert set(lib.EXPORTS) == declared
+    L = lib.lib()
+    for name in declared:
+        assert getattr(L, name) is not None
+
+
+def test_library_is_sm100a_only(lib):
+    out = subprocess.check_output(["cuobjdump", "--list-elf", lib.LIB_PATH]).decode()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(80|86|89|90)\b", out)
+
+
+def test_status_strings_and_version(lib):
+    L = lib.lib()
+    assert lib.abi_version() == 1
+    for s, txt in [(0, b"ok"), (1, b"invalid argument"), (4, b"pair capacity exceeded")]:
+        assert L.dass_status_string(s) == txt
+    assert L.dass_status_string(99) == b"unknown status"
+
+
+def test_validation_before_any_cuda_call(lib):
+    L = lib.lib()
+    cam = lib.camera_struct(synth.tiny_camera(64, 64))
+    P = None
+    # null camera / bad sizes / bad degree
+    assert L.dass_project(None, 10, 0, P, P, P, P, P, P, P, P, P, P, P) == 1
+    bad = lib.camera_struct(synth.tiny_camera(64, 64)); bad.width = 0
+    assert L.dass_project(C.byref(bad), 10, 0, P, P, P, P, P, P, P, P, P, P, P) == 1
+    bad.width = 64; bad.fx = -1.0
+    assert L.dass_project(C.byref(bad), 10, 0, P, P, P, P, P, P, P, P, P, P, P) == 1
+    assert L.dass_project(C.byref(cam), 10, 4, P, P, P, P, P, P, P, P, P, P, P) == 1
+    assert L.dass_project(C.byref(cam), -1, 0, P, P, P, P, P, P, P, P, P, P, P) == 1
+    assert L.dass_project(C.byref(cam), 10, 0, P, P, P, P, P, P, P, P, P, P, P) == 1  # null ptrs
+    assert b"null" in L.dass_last_error()
+    # n = 0 is OK and enqueues nothing
+    assert L.dass_project(C.byref(cam), 0, 3, P, P, P, P, P, P, P, P, P, P, P) == 0
+    assert L.dass_apply_shift(0, P, P, P, P, P, P, P, P) == 0
+    assert L.dass_apply_shift(-3, P, P, P, P, P, P, P, P) == 1
+    # error map: γ ≤ 0 is a usage error; missing images are a data error
+    assert L.dass_error_map(C.byref(cam), C.c_void_p(16), C.c_void_p(16), C.c_float(0.0), P, P, 0, P, P, P) == 1
+    assert L.dass_error_map(C.byref(cam), None, None, C.c_float(0.1), P, P, 0, P, P, P) == 2
+    # capacity must stay below 2^30
+    out = C.c_size_t(0)
+    assert L.dass_bin_sort_workspace(1000, 16, 1 << 30, C.byref(out)) == 1
+    assert L.dass_bin_sort_workspace(1000, 16, 1 << 20, C.byref(out)) == 0 and out.value > (1 << 20) * 16
+    assert L.dass_render_bwd_workspace(1000, C.byref(out)) == 0 and out.value == 1000 * 48
+    assert lib.kernel_launches() == 0
+
+
+def test_binding_refuses_cpu_tensors(lib):
+    torch = pytest.importorskip("torch")
+    t = torch.zeros(4, 4)
+    with pytest.raises(ValueError):
+        lib.dass_apply_shift(t, t, t, t, None, t, t)
+
+
+def test_camera_struct_layout_matches_generator(lib):
+    cam = synth.n3dv_rig()[3]
+    a = bytes(lib.camera_struct(cam))
+    b = cam.to_struct().tobytes()
+    assert C.sizeof(lib.dass_camera) == synth.CAMERA_DTYPE.itemsize == 140
+    assert a == b

@@ -1,0 +1,311 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, on the
+same seeded inputs (paper_2411_14847_b200/synth.py).
+
+Bars (BASELINE.json north star; SURVEY §8(c) comparison policy):
+  * keys, sort order, ranges, K, depth bits, pixel boxes, tiles: bit-exact;
+  * image ≤ 1e-4 absolute on non-tie pixels, T_final ≤ 1e-5, tie pixels < 1e-3;
+  * gradients |Δ| ≤ 1e-3·max(|g_ref|, 1e-2·rms_field) excluding Gaussians
+    whose box holds a tie pixel;
+  * shift ≤ 1e-6; error map E ≤ 1e-6, D and s_err exact off ties.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2411_14847_b200 import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2411_14847_b200 import dass  # noqa: E402
+from paper_2411_14847_b200.pipeline import DeviceScene, Grads, Raster, ViewRecords  # noqa: E402
+
+DEV = "cuda"
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def run_view(cam, scene, dL=None, keep=None, bg=None, capacity=1 << 22):
+    """Project + bin_sort (host mode) + fwd (+ bwd) through the C-ABI."""
+    ds = DeviceScene.from_host(scene, DEV)
+    rec = ViewRecords(1, scene.n, DEV)
+    kd = None if keep is None else torch.from_numpy(keep.astype(np.uint8)).to(DEV)
+    dass.dass_project(cam, scene.sh_degree, ds.pos_opa, ds.scale, ds.rot, ds.sh, kd,
+                      rec.xy_depth[0], rec.conic_opa[0], rec.rgb[0], rec.box[0], rec.tiles[0])
+    ras = Raster(cam.width, cam.height, scene.n, capacity, DEV)
+    keys = torch.empty(max(capacity, 1), dtype=torch.int64, device=DEV)
+    K = ras.forward(cam, rec.view(0), host_mode=True, bg=bg, sorted_keys=keys)
+    out = dict(rec=rec, ras=ras, K=K, keys=np_(keys[:K]).view(np.uint64), ids=np_(ras.sorted_ids[:K]).view(np.uint32),
+               ranges=np_(ras.ranges).view(np.uint32), img=np_(ras.img), T=np_(ras.T),
+               last=np_(ras.last).view(np.uint32))
+    if dL is not None:
+        g = Grads.zeros(scene.n, scene.sh_degree, DEV)
+        ras.backward(cam, ds, rec.view(0), torch.from_numpy(dL).to(DEV), g, keep=kd, bg=bg)
+        torch.cuda.synchronize()
+        out["grads"] = g
+    torch.cuda.synchronize()
+    return out
+
+
+def gpu_projection(rec):
+    xy = np_(rec.xy_depth[0]); co = np_(rec.conic_opa[0]); rgb = np_(rec.rgb[0])
+    box = np_(rec.box[0]).view(np.uint32); tiles = np_(rec.tiles[0]).view(np.uint32)
+    lo = xy[:, 3].copy().view(np.uint32)
+    ulo = (lo & 0xFFFF).astype(np.uint16).view(np.float16).astype(np.float64)
+    vlo = (lo >> 16).astype(np.uint16).view(np.float16).astype(np.float64)
+    b4 = np.stack([box[:, 0] & 0xFFFF, box[:, 0] >> 16, box[:, 1] & 0xFFFF, box[:, 1] >> 16], 1)
+    return dict(u=xy[:, 0].astype(np.float64) + ulo, v=xy[:, 1].astype(np.float64) + vlo,
+                zbits=xy[:, 2].view(np.uint32), conic=co[:, :3], opa=co[:, 3], rgb=rgb[:, :3],
+                clampbits=rgb[:, 3].astype(np.int32), box=b4.astype(np.int32), tiles=tiles,
+                visible=(tiles > 0).astype(np.uint8))
+
+
+def check_projection(cam, scene, rec, keep=None):
+    o = oracle.project(cam, scene, keep=keep)
+    g = gpu_projection(rec)
+    vis = o["visible"] == 1
+    # key chain: bit-exact
+    assert np.array_equal(g["visible"], o["visible"])
+    assert np.array_equal(g["zbits"][vis], o["zbits"][vis])
+    assert np.array_equal(g["box"][vis], o["box"][vis])
+    assert np.array_equal(g["tiles"], o["tiles"])
+    # records: fp32 rounding of the fp64 values
+    np.testing.assert_allclose(g["u"][vis], o["uvz"][vis, 0], rtol=0, atol=2e-6)
+    np.testing.assert_allclose(g["v"][vis], o["uvz"][vis, 1], rtol=0, atol=2e-6)
+    np.testing.assert_allclose(g["conic"][vis], o["conic"][vis], rtol=1e-6, atol=1e-7 * np.abs(o["conic"][vis]).max())
+    np.testing.assert_allclose(g["rgb"][vis], o["rgb"][vis], rtol=0, atol=1e-5)
+    np.testing.assert_allclose(g["opa"][vis], o["opa"][vis], rtol=0, atol=0)
+    near0 = np.any(np.abs(o["rgb"][vis]) < 1e-5, axis=1)
+    assert np.array_equal(g["clampbits"][vis][~near0], o["clampbits"][vis][~near0])
+    return o
+
+
+def check_binsort(cam, out, g):
+    """Layer 1 of the comparison policy: the GPU's sort of its own projection
+    equals the oracle's brute-force sort of the same (visible, zbits, box)."""
+    keys, ids, ranges = oracle.bin_sort(cam, dict(visible=g["visible"], zbits=g["zbits"], box=g["box"]))
+    assert out["K"] == len(keys)
+    assert np.array_equal(out["keys"], keys)
+    assert np.array_equal(out["ids"], ids)
+    assert np.array_equal(out["ranges"], ranges)
+
+
+def check_image(cam, scene, out, keep=None, bg=None, atol=1e-4, max_tie=1e-3):
+    o = oracle.render(cam, scene, keep=keep, bg=bg)
+    tie = o["tie"] == 1
+    assert tie.mean() < max_tie
+    ok = ~tie
+    d = np.abs(out["img"] - o["img"])
+    assert d[:, ok].max() <= atol, f"max |Δimg| {d[:, ok].max():.3g} at non-tie pixels"
+    assert np.abs(out["T"] - o["T"])[ok].max() <= 1e-5
+    # last contributor: the id at out_last−1 is the oracle's last accepted Gaussian
+    has = ok & (o["nacc"] > 0)
+    li = out["last"][has].astype(np.int64) - 1
+    assert np.array_equal(out["ids"][li].astype(np.int64), o["last_id"][has].astype(np.int64))
+    return o
+
+
+def check_grads(cam, scene, out, dL, keep=None, bg=None, tol=1e-3):
+    o = oracle.render_bwd(cam, scene, dL, keep=keep, bg=bg)
+    g = out["grads"]
+    ok = o["gtie"] == 0
+    nc = (scene.sh_degree + 1) ** 2
+    gsh = np_(g.sh).transpose(1, 0, 2).reshape(scene.n, -1)[:, :3 * nc].reshape(scene.n, nc, 3)
+    pairs = [("pos", np_(g.pos_opa)[:, :3], o["g_pos_opa"][:, :3]),
+             ("opa", np_(g.pos_opa)[:, 3], o["g_pos_opa"][:, 3]),
+             ("scale", np_(g.scale)[:, :3], o["g_scale"][:, :3]),
+             ("rot", np_(g.rot), o["g_rot"]),
+             ("sh", gsh, o["g_sh"]),
+             ("gradstat", np_(g.gradstat_sum), o["gradstat_sum"])]
+    for name, a, b in pairs:
+        a, b = a[ok], b[ok]
+        rms = np.sqrt(np.mean(b ** 2)) if b.size else 0.0
+        bound = tol * np.maximum(np.abs(b), 1e-2 * rms)
+        bad = np.abs(a - b) > bound
+        assert not bad.any(), (f"{name}: {bad.sum()} of {bad.size} over tolerance; worst rel "
+                               f"{(np.abs(a - b) / np.maximum(np.abs(b), 1e-2 * rms + 1e-30)).max():.3g}")
+    assert np.array_equal(np_(g.gradstat_cnt), o["gradstat_cnt"])
+    return o
+
+
+# ---------------------------------------------------------------- tests ----
+
+def test_c1_full_chain_parity():
+    """Config C1 (64×64, 1k Gaussians, SH0): every output against the oracle."""
+    cam, sc = synth.c1()
+    dL = synth.grad_image(cam, 101)
+    out = run_view(cam, sc, dL=dL)
+    check_projection(cam, sc, out["rec"])
+    check_binsort(cam, out, gpu_projection(out["rec"]))
+    check_image(cam, sc, out)
+    check_grads(cam, sc, out, dL)
+
+
+@pytest.mark.parametrize("W,H,n,deg,seed", [(100, 70, 3000, 1, 11), (333, 177, 20000, 3, 12),
+                                            (16, 16, 50, 2, 13), (1, 1, 20, 0, 14), (17, 300, 5000, 3, 15)])
+def test_ragged_sizes_parity(W, H, n, deg, seed):
+    """Ragged tails (W, H not multiples of 16), several tiles, degrees 0-3."""
+    cam = synth.n3dv_rig(width=W, height=H)[seed % 20]
+    sc = synth.n3dv_scene(n=n, seed=seed, degree=deg, fx=cam.fx)
+    dL = synth.grad_image(cam, seed + 1)
+    bg = np.array([0.1, 0.5, 0.9], np.float32)
+    out = run_view(cam, sc, dL=dL, bg=bg)
+    check_projection(cam, sc, out["rec"])
+    check_binsort(cam, out, gpu_projection(out["rec"]))
+    check_image(cam, sc, out, bg=bg)
+    check_grads(cam, sc, out, dL, bg=bg)
+
+
+def test_empty_and_all_culled():
+    cam = synth.tiny_camera(40, 24)
+    sc = synth.random_scene(30, cam, seed=3)
+    sc.pos_opa[:, 2] = -2.0  # all behind the camera
+    bg = np.array([0.3, 0.2, 0.1], np.float32)
+    out = run_view(cam, sc, dL=synth.grad_image(cam, 4), bg=bg)
+    assert out["K"] == 0 and not out["ranges"].any()
+    np.testing.assert_array_equal(out["img"], np.broadcast_to(bg[:, None, None], out["img"].shape))
+    assert np.all(out["T"] == 1.0)
+    assert not np_(out["grads"].pos_opa).any()
+
+
+def test_masked_equals_deleted_bit_exact():
+    """Eq. 1 with Quant = 0 ≡ deleting the Gaussian, bit-exact on GPU."""
+    cam, sc = synth.c1()
+    keep = (np.arange(sc.n) % 4 != 1).astype(np.uint8)
+    a = run_view(cam, sc, keep=keep)
+    idx = np.nonzero(keep)[0]
+    sd = synth.Scene(sc.pos_opa[idx], sc.scale[idx], sc.rot[idx], sc.sh[:, idx], 0)
+    b = run_view(cam, sd)
+    assert np.array_equal(a["img"], b["img"]) and np.array_equal(a["T"], b["T"])
+    check_image(cam, sc, a, keep=keep)
+
+
+def test_equal_depth_ties_bit_exact():
+    """A planar scene (all depth bits equal): order by index (A03)."""
+    cam = synth.tiny_camera(80, 64)
+    sc = synth.random_scene(2000, cam, seed=21)
+    sc.pos_opa[:, 2] = 3.0
+    out = run_view(cam, sc)
+    g = gpu_projection(out["rec"])
+    assert len(np.unique(g["zbits"][g["visible"] == 1])) == 1
+    check_binsort(cam, out, g)
+    check_image(cam, sc, out, max_tie=3e-3)   # 2000 splats on one plane: more near-threshold pixels
+
+
+def test_capacity_overflow_host_and_graph_mode():
+    cam, sc = synth.c1()
+    with pytest.raises(dass.DassError) as ei:
+        run_view(cam, sc, capacity=100)
+    assert ei.value.status == dass.DASS_ERR_CAPACITY
+    ds = DeviceScene.from_host(sc, DEV)
+    rec = ViewRecords(1, sc.n, DEV)
+    dass.dass_project(cam, 0, ds.pos_opa, ds.scale, ds.rot, ds.sh, None, *rec.view(0))
+    ras = Raster(cam.width, cam.height, sc.n, 100, DEV)
+    ras.forward(cam, rec.view(0), host_mode=False)
+    torch.cuda.synchronize()
+    K, flag = np_(ras.num_pairs).view(np.uint32)
+    assert flag == 1 and K > 100 and not np_(ras.ranges).any()
+
+
+def test_project_views_equals_per_view():
+    cams = synth.n3dv_rig(width=200, height=150, num_views=20)
+    sc = synth.n3dv_scene(n=5000, seed=5, fx=cams[0].fx)
+    ds = DeviceScene.from_host(sc, DEV)
+    rec = ViewRecords(len(cams), sc.n, DEV)
+    dass.dass_project_views(cams, 3, ds.pos_opa, ds.scale, ds.rot, ds.sh, None, rec.xy_depth,
+                            rec.conic_opa, rec.rgb, rec.box, rec.tiles)
+    one = ViewRecords(1, sc.n, DEV)
+    for v in (0, 7, 16, 19):
+        dass.dass_project(cams[v], 3, ds.pos_opa, ds.scale, ds.rot, ds.sh, None, *one.view(0))
+        for a, b in zip(rec.view(v), one.view(0)):
+            assert torch.equal(a, b)
+
+
+def test_shift_parity():
+    cams, sc = synth.c3(n=20000, num_views=1)
+    mu, sigma = synth.shift_offsets(sc, seed=33)
+    sigma[:5] = 0  # ‖σ‖ < 1e-8 → identity
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    pos, rot, m, s, dyn = t(sc.pos_opa), t(sc.rot), t(mu), t(sigma), t(sc.dynamic)
+    po, ro = torch.empty_like(pos), torch.empty_like(rot)
+    dass.dass_apply_shift(pos, rot, m, s, dyn, po, ro)
+    ref_p, ref_r = oracle.shift(sc.pos_opa, sc.rot, mu, sigma, sc.dynamic)
+    np.testing.assert_allclose(np_(po), ref_p, atol=1e-6, rtol=0)
+    np.testing.assert_allclose(np_(ro), ref_r, atol=1e-6, rtol=0)
+    off = sc.dynamic == 0
+    assert np.array_equal(np_(po)[off], sc.pos_opa[off]) and np.array_equal(np_(ro)[off], sc.rot[off])
+    g = np.random.default_rng(2)
+    gp = g.normal(size=(sc.n, 4)).astype(np.float32)
+    gq = g.normal(size=(sc.n, 4)).astype(np.float32)
+    gm, gs = torch.zeros_like(pos), torch.zeros_like(rot)
+    dass.dass_apply_shift_bwd(rot, s, dyn, t(gp), t(gq), gm, gs)
+    rm, rs = oracle.shift_bwd(sc.rot, sigma, sc.dynamic, gp.astype(np.float64), gq.astype(np.float64))
+    np.testing.assert_allclose(np_(gm)[:, :3], rm[:, :3], atol=1e-6)
+    np.testing.assert_allclose(np_(gs), rs, atol=1e-5, rtol=1e-5)
+    # in place
+    dass.dass_apply_shift(pos, rot, m, s, dyn, pos, rot)
+    np.testing.assert_allclose(np_(pos), ref_p, atol=1e-6, rtol=0)
+
+
+def test_error_map_parity():
+    cams = synth.meetroom_rig(width=160, height=90, num_views=3)
+    sc = synth.n3dv_scene(n=8000, seed=41, fx=cams[0].fx)
+    n_base = 6000
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    s_err = torch.zeros(sc.n, dtype=torch.uint8, device=DEV)
+    ref = np.zeros(sc.n, np.uint8)
+    tie_any = np.zeros(sc.n, bool)
+    for k, cam in enumerate(cams):
+        a = synth.random_image(cam, 60 + k); b = synth.random_image(cam, 70 + k)
+        err = torch.empty(cam.height, cam.width, device=DEV)
+        dm = torch.zeros((cam.height * cam.width + 31) // 32, dtype=torch.int32, device=DEV)
+        dass.dass_error_map(cam, t(a), t(b), 0.3, err, dm, n_base, t(sc.pos_opa), s_err)
+        o = oracle.error_map(cam, a, b, 0.3, sc.pos_opa, n_base=n_base, s_err=ref)
+        ref = o["s_err"]
+        tie_any |= o["tie_g"] == 1
+        np.testing.assert_allclose(np_(err), o["err"], atol=1e-6)
+        bits = np.unpackbits(np_(dm).view(np.uint8), bitorder="little")[:cam.height * cam.width]
+        okp = o["tie_px"].reshape(-1) == 0
+        assert np.array_equal(bits[okp], o["D"].reshape(-1)[okp])
+    torch.cuda.synchronize()
+    got = np_(s_err)
+    assert not got[n_base:].any()
+    assert np.array_equal(got[~tie_any], ref[~tie_any])
+
+
+def test_render_stats_match_oracle_counts():
+    cam, sc = synth.c1()
+    out = run_view(cam, sc)
+    ras, rec = out["ras"], out["rec"]
+    cnt = torch.zeros(8, dtype=torch.int64, device=DEV)
+    dass.dass_render_stats(cam, ras.ranges, ras.sorted_ids, rec.xy_depth[0], rec.conic_opa[0],
+                           rec.box[0], ras.T, ras.last, cnt)
+    c = np_(cnt)
+    o = oracle.render(cam, sc)
+    ok = o["tie"] == 0
+    # counts agree exactly away from tie pixels; allow the tie pixels' share
+    slack = int(o["pfwd"][~ok].sum()) + 1
+    assert abs(int(c[0]) - int(o["pfwd"].sum())) <= slack
+    assert abs(int(c[1]) - int(o["pbwd"].sum())) <= slack
+    assert abs(int(c[2]) - int(o["nacc"].sum())) <= slack
+    assert abs(int(c[3]) - int(o["term"].sum())) <= (~ok).sum()
+    assert int(c[4]) == out["K"]
+
+
+@pytest.mark.slow
+def test_c2_full_size_parity():
+    """Config C2 at full size (1352×1014, 300k Gaussians, SH3) in the launch
+    configuration bench.py times: image and every gradient vs the oracle's
+    scatter form (identical per-pixel op sequence at O(Σ box area) cost)."""
+    cam, sc = synth.c2()
+    dL = synth.grad_image(cam, 202)
+    out = run_view(cam, sc, dL=dL, capacity=1 << 24)
+    check_projection(cam, sc, out["rec"])
+    check_binsort(cam, out, gpu_projection(out["rec"]))
+    check_image(cam, sc, out)
+    check_grads(cam, sc, out, dL)
