@@ -40,8 +40,8 @@ FP32_LANES = 128
 
 # Algorithmic FP32 work per unit of render_bwd raster:
 # an accepted (pixel, entry) evaluation and an in-box but rejected one.
-FLOP_BWD_ACCEPTED = 96
-FLOP_BWD_REJECTED = 19
+FLOP_BWD_ACCEPTED = 62
+FLOP_BWD_REJECTED = 15
 
 
 def parse():
@@ -62,13 +62,6 @@ def parse():
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
-
-
-def shard(num_views, rank, world):
-    """Contiguous view blocks, sizes differ by at most one."""
-    base, extra = divmod(num_views, world)
-    start = rank * base + min(rank, extra)
-    return list(range(start, start + base + (1 if rank < extra else 0)))
 
 
 class ClockSampler:
@@ -127,7 +120,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2411_14847_b200 import dass, synth
-    from paper_2411_14847_b200.pipeline import DeviceScene, Grads, Raster, ViewRecords
+    from paper_2411_14847_b200.dist import FlatGrads, allreduce_grads, shard
+    from paper_2411_14847_b200.pipeline import DeviceScene, Raster, ViewRecords
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -152,20 +146,14 @@ def run_ours(args):
     mu_d, sigma_d = t(mu), t(sigma)
     dLs = torch.stack([t(synth.grad_image(cams[v], 1000 + v, 1.0 / (3 * W * H))) for v in mine]) \
         if mine else torch.empty(0, 3, H, W, device=dev)
-    # one flat gradient buffer (the all_reduce payload): pos_opa, scale, rot, sh,
-    # g_mu, g_sigma, gradstat_sum  (+ counts kept separately, int)
-    sizes = [n * 4, n * 4, n * 4, K4 * n * 4, n * 4, n * 4, n]
-    flat = torch.zeros(sum(sizes), dtype=torch.float32, device=dev)
-    parts = list(torch.split(flat, sizes))
-    grads = Grads(parts[0].view(n, 4), parts[1].view(n, 4), parts[2].view(n, 4),
-                  parts[3].view(K4, n, 4), parts[6], torch.zeros(n, dtype=torch.int32, device=dev))
-    g_mu, g_sigma = parts[4].view(n, 4), parts[5].view(n, 4)
+    # one flat gradient buffer = the all_reduce payload (dist.FlatGrads)
+    grads = FlatGrads.allocate(n, K4, dev)
+    flat, g_mu, g_sigma = grads.flat, grads.g_mu, grads.g_sigma
     records = ViewRecords(max(len(mine), 1), n, dev)
     raster = Raster(W, H, n, args.capacity, dev)
 
     def step():
-        flat.zero_()
-        grads.gradstat_cnt.zero_()
+        grads.zero_()
         dass.dass_apply_shift(base.pos_opa, base.rot, mu_d, sigma_d, base.dynamic,
                               shifted.pos_opa, shifted.rot)
         if my_cams:
@@ -179,7 +167,7 @@ def run_ours(args):
         dass.dass_apply_shift_bwd(base.rot, sigma_d, base.dynamic, grads.pos_opa, grads.rot,
                                   g_mu, g_sigma)
         if world > 1:
-            dist.all_reduce(flat)
+            allreduce_grads(grads)
 
     def barrier():
         if world > 1:

@@ -27,10 +27,11 @@ def build(force: bool = False) -> str:
     """Compile the oracle (plain g++, -ffp-contract=off so the fp32 replica
     rounds every operation once; OpenMP for the O(Σ box area) scatter form)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = f"{_LIB}.{os.getpid()}.tmp"   # concurrent builders must not share a temp file
         cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fopenmp", "-fPIC",
-               "-shared", _SRC, "-o", _LIB + ".tmp"]
+               "-shared", _SRC, "-o", tmp]
         subprocess.check_call(cmd)
-        os.replace(_LIB + ".tmp", _LIB)
+        os.replace(tmp, _LIB)
     return _LIB
 
 
@@ -157,8 +158,10 @@ def render(cam, scene, keep=None, bg=None, mode="scatter", tie_eps=None):
     return o
 
 
-def render_bwd(cam, scene, dL_dimg, keep=None, bg=None, mode="scatter", tie_eps=None):
-    """O5+O6: gradients of sum(dL_dimg * render) w.r.t. all parameters."""
+def render_bwd(cam, scene, dL_dimg, keep=None, bg=None, mode="scatter", tie_eps=None, kappa=False):
+    """O5+O6: gradients of sum(dL_dimg * render) w.r.t. all parameters.
+    kappa=True also returns the conditioning κ of every gradient entry
+    (k_pos_opa, k_scale, k_rot, k_sh: Σ over pixels of |term| through |Jacobian|)."""
     c = _cam(cam)
     H, W = int(c["height"][0]), int(c["width"][0])
     n = scene.n
@@ -167,6 +170,9 @@ def render_bwd(cam, scene, dL_dimg, keep=None, bg=None, mode="scatter", tie_eps=
              g_sh=np.zeros((n, nc, 3)), g2d=np.zeros((n, 9)), gradstat_sum=np.zeros(n),
              gradstat_cnt=np.zeros(n, np.int32), gtie=np.zeros(n, np.uint8),
              img=np.zeros((3, H, W)), T=np.zeros((H, W)))
+    if kappa:
+        o.update(k_pos_opa=np.zeros((n, 4)), k_scale=np.zeros((n, 4)), k_rot=np.zeros((n, 4)),
+                 k_sh=np.zeros((n, nc, 3)))
     k = None if keep is None else np.ascontiguousarray(keep, np.uint8)
     b = None if bg is None else np.ascontiguousarray(bg, np.float32)
     lib().oracle_render_bwd(_p(c), n, scene.sh_degree, _p(_f32(scene.pos_opa)),
@@ -174,7 +180,9 @@ def render_bwd(cam, scene, dL_dimg, keep=None, bg=None, mode="scatter", tie_eps=
                             _p(b), _p(_f32(dL_dimg)), 0 if mode == "literal" else 1,
                             _p(_tie(tie_eps)), _p(o["g_pos_opa"]), _p(o["g_scale"]),
                             _p(o["g_rot"]), _p(o["g_sh"]), _p(o["g2d"]), _p(o["gradstat_sum"]),
-                            _p(o["gradstat_cnt"]), _p(o["gtie"]), _p(o["img"]), _p(o["T"]))
+                            _p(o["gradstat_cnt"]), _p(o["gtie"]), _p(o["img"]), _p(o["T"]),
+                            _p(o.get("k_pos_opa")), _p(o.get("k_scale")), _p(o.get("k_rot")),
+                            _p(o.get("k_sh")))
     return o
 
 

@@ -486,10 +486,39 @@ struct Grad2D {
   double u, v, A, B, C, o, col[3];
 };
 
+// Accumulate one pixel's terms into the sum and, for the conditioning
+// measure κ (Σ_px |term|, used to recognise cancelling sums), their magnitudes.
+inline void accumulate(Grad2D& sum, Grad2D& kap, const Grad2D& t) {
+  sum.u += t.u; sum.v += t.v; sum.A += t.A; sum.B += t.B; sum.C += t.C; sum.o += t.o;
+  kap.u += std::fabs(t.u); kap.v += std::fabs(t.v); kap.A += std::fabs(t.A);
+  kap.B += std::fabs(t.B); kap.C += std::fabs(t.C); kap.o += std::fabs(t.o);
+  for (int ch = 0; ch < 3; ++ch) { sum.col[ch] += t.col[ch]; kap.col[ch] += std::fabs(t.col[ch]); }
+}
+
+// The 9 per-pixel terms of one accepted entry (O5).
+inline Grad2D pixel_terms(double A, double B, double C, double o, const double* col,
+                          double alpha, double G, double oG, double dx, double dy, double Tk,
+                          double dL_dalpha, const double g[3]) {
+  Grad2D t{0, 0, 0, 0, 0, 0, {0, 0, 0}};
+  (void)col;
+  for (int ch = 0; ch < 3; ++ch) t.col[ch] = alpha * Tk * g[ch];
+  if (oG < 0.99) {  // unclamped α: α = o·G (A17)
+    t.o = G * dL_dalpha;
+    const double dpow = o * G * dL_dalpha;
+    t.u = dpow * (-(A * dx + B * dy));
+    t.v = dpow * (-(B * dx + C * dy));
+    t.A = dpow * (-0.5 * dx * dx);
+    t.B = dpow * (-dx * dy);
+    t.C = dpow * (-0.5 * dy * dy);
+  }
+  return t;
+}
+
 // Gradients of one pixel's composite w.r.t. its accepted entries (O5),
 // literal form: explicit accepted list, suffix sums (derivative of Eq. 8).
 void pixel_backward(const std::vector<Proj>& G, const std::vector<int>& ord, int X, int Y,
-                    const double bg[3], const double g[3], std::vector<Grad2D>& g2d) {
+                    const double bg[3], const double g[3], std::vector<Grad2D>& g2d,
+                    std::vector<Grad2D>& kap) {
   struct Acc { int id; Eval e; double T; };
   std::vector<Acc> acc;
   double T = 1;
@@ -512,18 +541,9 @@ void pixel_backward(const std::vector<Proj>& G, const std::vector<int>& ord, int
     double dL_dalpha = 0;
     for (int ch = 0; ch < 3; ++ch)
       dL_dalpha += g[ch] * (p.col[ch] * Tk - (S[ch] + Tfin * bg[ch]) / (1 - e.alpha));
-    Grad2D& o = g2d[acc[k].id];
-    for (int ch = 0; ch < 3; ++ch) o.col[ch] += e.alpha * Tk * g[ch];
+    accumulate(g2d[acc[k].id], kap[acc[k].id],
+               pixel_terms(p.A, p.B, p.C, p.o, p.col, e.alpha, e.G, e.oG, e.dx, e.dy, Tk, dL_dalpha, g));
     for (int ch = 0; ch < 3; ++ch) S[ch] += p.col[ch] * e.alpha * Tk;
-    if (e.oG < 0.99) {  // unclamped α: α = o·G (A17)
-      o.o += e.G * dL_dalpha;
-      const double dpow = p.o * e.G * dL_dalpha;
-      o.u += dpow * (-(p.A * e.dx + p.B * e.dy));
-      o.v += dpow * (-(p.B * e.dx + p.C * e.dy));
-      o.A += dpow * (-0.5 * e.dx * e.dx);
-      o.B += dpow * (-e.dx * e.dy);
-      o.C += dpow * (-0.5 * e.dy * e.dy);
-    }
   }
 }
 
@@ -718,7 +738,7 @@ void scatter_forward(const RenderCtx& R, const double bg[3], const TieEps& te, F
 // Scatter form of O5's raster part: reverse global order; per pixel the
 // transmittance before entry k is recovered as T_k = T_{k+1}/(1−α_k) in double.
 void scatter_backward(const RenderCtx& R, const double bg[3], const float* dL, const double* Tfin,
-                      const int32_t* last_pos, std::vector<Grad2D>& g2d) {
+                      const int32_t* last_pos, std::vector<Grad2D>& g2d, std::vector<Grad2D>& kap) {
   const int W = R.cam.width, H = R.cam.height;
   const size_t np = (size_t)W * H;
   int nth = 1;
@@ -729,11 +749,13 @@ void scatter_backward(const RenderCtx& R, const double bg[3], const float* dL, c
   const int nb = (H + band - 1) / band;
   std::vector<double> Tcur(Tfin, Tfin + np);
   std::vector<double> S(3 * np, 0.0);
-  std::vector<std::vector<Grad2D>> part(nb);
+  std::vector<std::vector<Grad2D>> part(nb), kpart(nb);
 #pragma omp parallel for schedule(dynamic, 1)
   for (int bi = 0; bi < nb; ++bi) {
     std::vector<Grad2D>& mine = part[bi];
+    std::vector<Grad2D>& kmine = kpart[bi];
     mine.assign(R.G.size(), Grad2D{0, 0, 0, 0, 0, 0, {0, 0, 0}});
+    kmine.assign(R.G.size(), Grad2D{0, 0, 0, 0, 0, 0, {0, 0, 0}});
     const int ylo = bi * band, yhi = std::min(H - 1, ylo + band - 1);
     for (int pos = (int)R.ord.size() - 1; pos >= 0; --pos) {
       const int id = R.ord[pos];
@@ -750,29 +772,19 @@ void scatter_backward(const RenderCtx& R, const double bg[3], const float* dL, c
           double dL_dalpha = 0;
           for (int ch = 0; ch < 3; ++ch)
             dL_dalpha += gg[ch] * (g.col[ch] * Tk - (S[ch * np + p] + Tfin[p] * bg[ch]) / (1 - e.alpha));
-          Grad2D& o = mine[id];
-          for (int ch = 0; ch < 3; ++ch) o.col[ch] += e.alpha * Tk * gg[ch];
+          accumulate(mine[id], kmine[id],
+                     pixel_terms(g.A, g.B, g.C, g.o, g.col, e.alpha, e.G, e.oG, e.dx, e.dy, Tk, dL_dalpha, gg));
           for (int ch = 0; ch < 3; ++ch) S[ch * np + p] += g.col[ch] * e.alpha * Tk;
           Tcur[p] = Tk;
-          if (e.oG < 0.99) {
-            o.o += e.G * dL_dalpha;
-            const double dpow = g.o * e.G * dL_dalpha;
-            o.u += dpow * (-(g.A * e.dx + g.B * e.dy));
-            o.v += dpow * (-(g.B * e.dx + g.C * e.dy));
-            o.A += dpow * (-0.5 * e.dx * e.dx);
-            o.B += dpow * (-e.dx * e.dy);
-            o.C += dpow * (-0.5 * e.dy * e.dy);
-          }
         }
     }
   }
   // deterministic reduction in band order
   for (int bi = 0; bi < nb; ++bi)
     for (size_t i = 0; i < R.G.size(); ++i) {
-      const Grad2D& s = part[bi][i];
-      Grad2D& d = g2d[i];
-      d.u += s.u; d.v += s.v; d.A += s.A; d.B += s.B; d.C += s.C; d.o += s.o;
-      for (int ch = 0; ch < 3; ++ch) d.col[ch] += s.col[ch];
+      Grad2D z{0, 0, 0, 0, 0, 0, {0, 0, 0}};
+      accumulate(g2d[i], z, part[bi][i]);
+      accumulate(kap[i], z, kpart[bi][i]);
     }
 }
 
@@ -990,12 +1002,17 @@ int oracle_render(const OCam* cam, int n, int deg, const float* pos_opa, const f
 //   gradstat_sum double[n], gradstat_cnt int32[n].  Any output nullable.
 // Also renders the forward (img/T nullable) and flags Gaussians whose box
 // contains a tie pixel (gtie uint8[n], nullable).
+// κ outputs (nullable, same layouts as g_*): the conditioning of each
+// gradient entry, Σ_px |L_i|·|per-pixel 2D terms| where L_i is the linear
+// preprocess map of Gaussian i (columns by unit probes).  A gradient with
+// κ ≫ |g| is a cancelling sum whose fp32 value is only accurate to ~eps·κ.
 int oracle_render_bwd(const OCam* cam, int n, int deg, const float* pos_opa, const float* scale,
                       const float* rot, const float* sh, const uint8_t* keep, const float* bg3,
                       const float* dL_dimg, int mode, const double* tie_eps, double* g_pos_opa,
                       double* g_scale, double* g_rot, double* g_sh, double* g2d_out,
                       double* gradstat_sum, int32_t* gradstat_cnt, uint8_t* gtie, double* img_out,
-                      double* T_out) {
+                      double* T_out, double* k_pos_opa, double* k_scale, double* k_rot,
+                      double* k_sh) {
   RenderCtx R;
   make_ctx(R, cam, n, deg, pos_opa, scale, rot, sh, keep);
   const double bg[3] = {bg3 ? bg3[0] : 0.0, bg3 ? bg3[1] : 0.0, bg3 ? bg3[2] : 0.0};
@@ -1008,40 +1025,42 @@ int oracle_render_bwd(const OCam* cam, int n, int deg, const float* pos_opa, con
   FwdOut o{img.data(), Tfin.data(), nacc.data(), lid.data(), lpos.data(), tie.data(), term.data(),
            nullptr, nullptr};
   scatter_forward(R, bg, te, o);
-  std::vector<Grad2D> g2d(n, Grad2D{0, 0, 0, 0, 0, 0, {0, 0, 0}});
+  const Grad2D zero{0, 0, 0, 0, 0, 0, {0, 0, 0}};
+  std::vector<Grad2D> g2d(n, zero), kap(n, zero);
   if (mode == 0) {
     // literal: every pixel independently, explicit accepted list
     int nth = 1;
 #ifdef _OPENMP
     nth = omp_get_max_threads();
 #endif
-    std::vector<std::vector<Grad2D>> part(nth);
+    std::vector<std::vector<Grad2D>> part(nth), kpart(nth);
 #pragma omp parallel
     {
       int tid = 0;
 #ifdef _OPENMP
       tid = omp_get_thread_num();
 #endif
-      part[tid].assign(n, Grad2D{0, 0, 0, 0, 0, 0, {0, 0, 0}});
+      part[tid].assign(n, zero);
+      kpart[tid].assign(n, zero);
 #pragma omp for schedule(static)
       for (int Y = 0; Y < H; ++Y)
         for (int X = 0; X < W; ++X) {
           const size_t p = (size_t)Y * W + X;
           const double gg[3] = {dL_dimg[p], dL_dimg[np + p], dL_dimg[2 * np + p]};
-          pixel_backward(R.G, R.ord, X, Y, bg, gg, part[tid]);
+          pixel_backward(R.G, R.ord, X, Y, bg, gg, part[tid], kpart[tid]);
         }
     }
     for (int t = 0; t < nth; ++t)
       for (int i = 0; i < n; ++i) {
-        const Grad2D& s = part[t][i];
-        g2d[i].u += s.u; g2d[i].v += s.v; g2d[i].A += s.A; g2d[i].B += s.B; g2d[i].C += s.C;
-        g2d[i].o += s.o;
-        for (int ch = 0; ch < 3; ++ch) g2d[i].col[ch] += s.col[ch];
+        Grad2D z = zero;
+        accumulate(g2d[i], z, part[t][i]);
+        accumulate(kap[i], z, kpart[t][i]);
       }
   } else {
-    scatter_backward(R, bg, dL_dimg, Tfin.data(), lpos.data(), g2d);
+    scatter_backward(R, bg, dL_dimg, Tfin.data(), lpos.data(), g2d, kap);
   }
   const int nc = (deg + 1) * (deg + 1);
+  const bool want_k = k_pos_opa || k_scale || k_rot || k_sh;
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < n; ++i) {
     Grad3D d;
@@ -1050,6 +1069,28 @@ int oracle_render_bwd(const OCam* cam, int n, int deg, const float* pos_opa, con
     if (g_scale) { for (int a = 0; a < 3; ++a) g_scale[4 * i + a] = d.s[a]; g_scale[4 * i + 3] = 0; }
     if (g_rot) for (int a = 0; a < 4; ++a) g_rot[4 * i + a] = d.q[a];
     if (g_sh) for (int k = 0; k < nc; ++k) for (int ch = 0; ch < 3; ++ch) g_sh[((size_t)i * nc + k) * 3 + ch] = d.sh[k][ch];
+    if (want_k) {
+      Grad3D kk;
+      std::memset(&kk, 0, sizeof(kk));
+      const double k9[9] = {kap[i].u, kap[i].v, kap[i].A, kap[i].B, kap[i].C, kap[i].o,
+                            kap[i].col[0], kap[i].col[1], kap[i].col[2]};
+      for (int c = 0; c < 9; ++c) {
+        if (k9[c] == 0) continue;
+        Grad2D e = zero;
+        double* f[9] = {&e.u, &e.v, &e.A, &e.B, &e.C, &e.o, &e.col[0], &e.col[1], &e.col[2]};
+        *f[c] = 1.0;
+        Grad3D col;
+        preprocess_backward(R.cam, R.P, i, R.G[i], e, col);
+        for (int a = 0; a < 3; ++a) { kk.p[a] += std::fabs(col.p[a]) * k9[c]; kk.s[a] += std::fabs(col.s[a]) * k9[c]; }
+        kk.o += std::fabs(col.o) * k9[c];
+        for (int a = 0; a < 4; ++a) kk.q[a] += std::fabs(col.q[a]) * k9[c];
+        for (int k = 0; k < nc; ++k) for (int ch = 0; ch < 3; ++ch) kk.sh[k][ch] += std::fabs(col.sh[k][ch]) * k9[c];
+      }
+      if (k_pos_opa) { for (int a = 0; a < 3; ++a) k_pos_opa[4 * i + a] = kk.p[a]; k_pos_opa[4 * i + 3] = kk.o; }
+      if (k_scale) { for (int a = 0; a < 3; ++a) k_scale[4 * i + a] = kk.s[a]; k_scale[4 * i + 3] = 0; }
+      if (k_rot) for (int a = 0; a < 4; ++a) k_rot[4 * i + a] = kk.q[a];
+      if (k_sh) for (int k = 0; k < nc; ++k) for (int ch = 0; ch < 3; ++ch) k_sh[((size_t)i * nc + k) * 3 + ch] = kk.sh[k][ch];
+    }
     if (g2d_out) {
       const Grad2D& s = g2d[i];
       const double v9[9] = {s.u, s.v, s.A, s.B, s.C, s.o, s.col[0], s.col[1], s.col[2]};

@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stdout.write(out.decode())
     if failed:
         raise RuntimeError("nvcc failed")
-    tmp = LIB + ".tmp"
+    tmp = f"{LIB}.{os.getpid()}.tmp"
     subprocess.check_call([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
                            *objs, "-o", tmp, "-lcudart"])
     os.replace(tmp, LIB)

@@ -35,14 +35,25 @@ struct Splat2D {
   float A, B, C, o;  // conic and effective opacity
 };
 
-// power = −½(A dx² + C dy²) − B dx dy   (Eq. 5 restricted to 2D).  Written
-// with explicit-rounding intrinsics so the compiler can neither contract nor
-// re-associate it: the forward and the backward kernels get identical bits.
-__device__ __forceinline__ float splat_power(float A, float B, float C, float dx, float dy) {
-  const float adx2 = __fmul_rn(__fmul_rn(A, dx), dx);
-  const float q = __fmaf_rn(__fmul_rn(C, dy), dy, adx2);
-  const float bxy = __fmul_rn(__fmul_rn(B, dx), dy);
-  return __fmaf_rn(-0.5f, q, -bxy);
+// power = −½(A dx² + C dy²) − B dx dy   (Eq. 5 restricted to 2D), evaluated
+// in one canonical explicit-rounding form shared by every kernel that takes a
+// per-pixel decision (render_fwd, render_bwd, render_stats), so all of them
+// get identical bits: with the per-(entry, column) terms
+//   ax = (−½A·dx)·dx,  bx = −B·dx,  hC = −½C
+// each pixel of the column costs one FADD (dy) and two FFMA:
+//   power = fma(dy, fma(hC, dy, bx), ax).
+struct ColTerms {
+  float ax, bx, hC;
+};
+__device__ __forceinline__ ColTerms col_terms(float A, float B, float C, float dx) {
+  ColTerms t;
+  t.ax = __fmul_rn(__fmul_rn(-0.5f * A, dx), dx);
+  t.bx = __fmul_rn(-B, dx);
+  t.hC = -0.5f * C;
+  return t;
+}
+__device__ __forceinline__ float splat_power(const ColTerms& t, float dy) {
+  return __fmaf_rn(dy, __fmaf_rn(t.hC, dy, t.bx), t.ax);
 }
 
 // exp(power) on the MUFU pipe: ex2.approx(power · log2 e).

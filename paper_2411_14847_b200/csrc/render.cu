@@ -20,97 +20,141 @@
 // clamped), the pixel contributes (e·dx, e·dy, e·dx², e·dx·dy, e·dy², e,
 // αT·g_r, αT·g_g, αT·g_b), and the preprocess kernel forms
 // ∂L/∂u = −o(A Σe·dx + B Σe·dy), ∂L/∂A = −½ o Σe·dx², … (exact algebra).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "sh.cuh"
 
 namespace dass {
 namespace {
 
-struct TileRec {   // 40 B per staged entry
-  float2 uv;       // tile-local mean
-  float4 co;       // A, B, C, o
-  float4 cm;       // r, g, b, box mask bits (x: bits 0..15, y: bits 16..31)
-};
-
-__device__ __forceinline__ uint32_t box_mask(uint2 b, int tx0, int ty0) {
-  const int x0 = max((int)(b.x & 0xFFFFu) - tx0, 0), x1 = min((int)(b.x >> 16) - tx0, TILE - 1);
-  const int y0 = max((int)(b.y & 0xFFFFu) - ty0, 0), y1 = min((int)(b.y >> 16) - ty0, TILE - 1);
+// Staged entry (48 B in three 16-B shared arrays so a warp can test the
+// box mask with one LDS.128 before touching the rest):
+//   s_a  = (u_rel, v_rel, p_thr, box mask bits)   p_thr: conservative power
+//          threshold ln(α_min/o) − 1e-3 below which α < 1/255 for sure, so the
+//          exp is skipped without changing any decision
+//   s_co = (A, B, C, o)    s_c = (r, g, b, −)
+// Tile-local row/column mask of the pixels an entry can possibly be accepted
+// at: the integer pixel box (A05) intersected with the bounding box of the
+// α ≥ 1/255 support ellipse {½ dᵀK d ≤ −p_thr}, whose half-extents are
+// √(2(−p_thr)·Σ'_xx) and √(2(−p_thr)·Σ'_yy) with Σ' = K⁻¹.  Conservative
+// (p_thr carries a 1e-3 margin and the extents a relative + absolute pad), so
+// every pixel it excludes would have been rejected by the exact per-pixel test:
+// decisions, and hence results, are unchanged (A05's box stays the rule).
+__device__ __forceinline__ uint32_t support_mask(uint2 b, int tx0, int ty0, float ux, float uy,
+                                                 float4 co, float pthr) {
+  int x0 = max((int)(b.x & 0xFFFFu) - tx0, 0), x1 = min((int)(b.x >> 16) - tx0, TILE - 1);
+  int y0 = max((int)(b.y & 0xFFFFu) - ty0, 0), y1 = min((int)(b.y >> 16) - ty0, TILE - 1);
+  const float det = co.x * co.z - co.y * co.y;
+  const float r2 = -2.f * pthr;
+  if (det > 0.f && r2 > 0.f) {
+    const float hx = sqrtf(r2 * co.z / det) * 1.0001f + 1e-3f;
+    const float hy = sqrtf(r2 * co.x / det) * 1.0001f + 1e-3f;
+    if (isfinite(hx) && isfinite(hy)) {
+      x0 = max(x0, (int)ceilf(fmaxf(ux - hx, -1.f)));
+      x1 = min(x1, (int)floorf(fminf(ux + hx, 16.f)));
+      y0 = max(y0, (int)ceilf(fmaxf(uy - hy, -1.f)));
+      y1 = min(y1, (int)floorf(fminf(uy + hy, 16.f)));
+    }
+  }
   if (x0 > x1 || y0 > y1) return 0u;
   const uint32_t mx = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
   const uint32_t my = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
   return mx | (my << 16);
 }
 
-__device__ __forceinline__ TileRec stage(uint32_t id, const float4* __restrict__ xy_depth,
-                                         const float4* __restrict__ conic_opa,
-                                         const float4* __restrict__ rgb,
-                                         const uint2* __restrict__ box, int tx0, int ty0) {
-  TileRec r;
+__device__ __forceinline__ void stage(uint32_t id, const float4* __restrict__ xy_depth,
+                                      const float4* __restrict__ conic_opa,
+                                      const float4* __restrict__ rgb, const uint2* __restrict__ box,
+                                      int tx0, int ty0, float4& a, float4& co, float4& c) {
   const float4 xy = xy_depth[id];
   const uint32_t lo_bits = __float_as_uint(xy.w);
   const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
-  r.uv.x = __fadd_rn(xy.x - (float)tx0, __low2float(lo));
-  r.uv.y = __fadd_rn(xy.y - (float)ty0, __high2float(lo));
-  r.co = conic_opa[id];
-  const float4 c = rgb[id];
-  r.cm = make_float4(c.x, c.y, c.z, __uint_as_float(box_mask(box[id], tx0, ty0)));
-  return r;
+  co = conic_opa[id];
+  const float4 cc = rgb[id];
+  a.x = __fadd_rn(xy.x - (float)tx0, __low2float(lo));
+  a.y = __fadd_rn(xy.y - (float)ty0, __high2float(lo));
+  a.z = __logf(ALPHA_MIN / co.w) - 1e-3f;
+  a.w = __uint_as_float(support_mask(box[id], tx0, ty0, a.x, a.y, co, a.z));
+  c = make_float4(cc.x, cc.y, cc.z, 0.f);
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Warp-row mask: warp w owns thread rows 2w, 2w+1 → pixel rows [2w·PPT, 2w·PPT + 2·PPT).
+template <int PPT>
+__device__ __forceinline__ uint32_t warp_row_mask(int warp) {
+  return (((1u << (2 * PPT)) - 1u) << (16 + warp * 2 * PPT));
 }
 
 // ------------------------------------------------------------- forward ----
 template <int PPT>
-__global__ void __launch_bounds__(256 / PPT) render_fwd_kernel(
+__global__ void __launch_bounds__(256 / PPT, 1024 / (256 / PPT)) render_fwd_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
     const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
     const uint2* __restrict__ box, float3 bg, float* __restrict__ out_img,
     float* __restrict__ out_T, uint32_t* __restrict__ out_last) {
   constexpr int NT = 256 / PPT;
-  __shared__ TileRec s_rec[NT];
+  constexpr int BATCH = 2 * NT;
+  __shared__ float4 s_a[BATCH], s_co[BATCH], s_c[BATCH];
   const int tile = blockIdx.x;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
   const int t = threadIdx.x;
   const int lx = t & 15, ly0 = (t >> 4) * PPT;
   const int X = tx0 + lx;
+  const uint32_t wmask = warp_row_mask<PPT>(t >> 5);
+  const uint32_t colbit = 1u << lx;
   const uint2 range = ranges[tile];
   float T[PPT], C[PPT][3];
-  uint32_t last[PPT], pm[PPT];
+  uint32_t last[PPT];
   bool done[PPT];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int Y = ty0 + ly0 + p;
     T[p] = 1.f; C[p][0] = C[p][1] = C[p][2] = 0.f;
     last[p] = range.x;
-    pm[p] = (1u << lx) | (1u << (16 + ly0 + p));
     done[p] = !(X < cam.W && Y < cam.H);
   }
   const float fx = (float)lx;
-  for (uint32_t b0 = range.x; b0 < range.y; b0 += NT) {
+  for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
     bool alive = false;
 #pragma unroll
     for (int p = 0; p < PPT; ++p) alive |= !done[p];
     if (__syncthreads_count(alive) == 0) break;
-    const uint32_t idx = b0 + t;
-    if (idx < range.y) s_rec[t] = stage(ids[idx], xy_depth, conic_opa, rgb, box, tx0, ty0);
+    for (int k = t; k < BATCH; k += NT)
+      if (b0 + k < range.y) stage(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_a[k], s_co[k], s_c[k]);
     __syncthreads();
-    const int cnt = min((uint32_t)NT, range.y - b0);
+    const int cnt = min((uint32_t)BATCH, range.y - b0);
     for (int j = 0; j < cnt; ++j) {
-      const TileRec r = s_rec[j];
-      const uint32_t m = __float_as_uint(r.cm.w);
-      const float dx = r.uv.x - fx;
+      const float4 a = s_a[j];
+      const uint32_t m = __float_as_uint(a.w);
+      if ((m & wmask) == 0u) continue;   // warp-uniform: box misses this warp's rows
+      if ((m & colbit) == 0u) continue;
+      const float4 co = s_co[j];
+      const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fx);
+      float pw[PPT];
+      bool ok[PPT];
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {   // independent per pixel: no branches, full ILP
+        pw[p] = splat_power(ct, a.y - (float)(ly0 + p));
+        ok[p] = !done[p] && ((m >> (16 + ly0 + p)) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
+      }
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
-        if (done[p] || (m & pm[p]) != pm[p]) continue;
-        const float dy = r.uv.y - (float)(ly0 + p);
-        const float power = splat_power(r.co.x, r.co.y, r.co.z, dx, dy);
-        if (power > 0.f) continue;
-        const float alpha = splat_alpha(r.co.w, splat_exp(power));
+        if (!ok[p]) continue;
+        const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
         if (alpha < ALPHA_MIN) continue;
         const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
         if (tn < T_MIN) { done[p] = true; continue; }
+        const float4 c = s_c[j];
         const float w = alpha * T[p];
-        C[p][0] += r.cm.x * w; C[p][1] += r.cm.y * w; C[p][2] += r.cm.z * w;
+        C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
         T[p] = tn;
         last[p] = b0 + j + 1;
       }
@@ -131,51 +175,46 @@ __global__ void __launch_bounds__(256 / PPT) render_fwd_kernel(
 }
 
 // ------------------------------------------------ backward: raster part ----
-// 9 values → each lane ends with the warp sum of one value index (or a pad).
-// Returns the index (0..8) the lane owns, or −1.
-__device__ __forceinline__ int reduce_scatter9(const float (&v)[9], float& out) {
-  const uint32_t lane = lane_id();
-  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4, b2 = lane & 2;
-  float r[6];
+// Reduce-scatter butterfly for 9 values (pad 10): after 5 rounds (12 SHFL)
+// every even lane holds the warp sum of one value index.  Lane predicates
+// and the owned index are loop-invariant and computed once per thread.
+struct LaneRS {
+  bool b16, b8, b4, b2;
+  int slot;  // value index this lane owns after the butterfly, −1 if none
+  __device__ __forceinline__ void init() {
+    const uint32_t lane = threadIdx.x & 31u;
+    b16 = lane & 16; b8 = lane & 8; b4 = lane & 4; b2 = lane & 2;
+    const int pos = (b8 ? 3 : 0) + (b4 ? 2 : 0) + (b2 ? 1 : 0);
+    const bool valid = (lane & 1) == 0 && (b8 ? pos <= 4 : pos <= 2);
+    const int idx = (b16 ? 5 : 0) + pos;
+    slot = (valid && idx < 9) ? idx : -1;
+  }
+  __device__ __forceinline__ float reduce(const float (&v)[9]) const {
+    float r[6];
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const float lo_v = v[i];
-    const float hi_v = i + 5 < 9 ? v[i + 5] : 0.f;
-    const float send = b16 ? lo_v : hi_v;
-    const float keep = b16 ? hi_v : lo_v;
-    r[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-  r[5] = 0.f;
-  float s[4];
+    for (int i = 0; i < 5; ++i) {
+      const float lo_v = v[i];
+      const float hi_v = i + 5 < 9 ? v[i + 5] : 0.f;
+      r[i] = (b16 ? hi_v : lo_v) + __shfl_xor_sync(0xffffffffu, b16 ? lo_v : hi_v, 16);
+    }
+    r[5] = 0.f;
+    float s[4];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const float send = b8 ? r[i] : r[i + 3];
-    const float keep = b8 ? r[i + 3] : r[i];
-    s[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  s[3] = 0.f;
-  float q[2];
+    for (int i = 0; i < 3; ++i)
+      s[i] = (b8 ? r[i + 3] : r[i]) + __shfl_xor_sync(0xffffffffu, b8 ? r[i] : r[i + 3], 8);
+    s[3] = 0.f;
+    float q[2];
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float send = b4 ? s[i] : s[i + 2];
-    const float keep = b4 ? s[i + 2] : s[i];
-    q[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    for (int i = 0; i < 2; ++i)
+      q[i] = (b4 ? s[i + 2] : s[i]) + __shfl_xor_sync(0xffffffffu, b4 ? s[i] : s[i + 2], 4);
+    float out = (b2 ? q[1] : q[0]) + __shfl_xor_sync(0xffffffffu, b2 ? q[0] : q[1], 2);
+    out += __shfl_xor_sync(0xffffffffu, out, 1);
+    return out;
   }
-  {
-    const float send = b2 ? q[0] : q[1];
-    const float keep = b2 ? q[1] : q[0];
-    out = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  }
-  out += __shfl_xor_sync(0xffffffffu, out, 1);
-  const int pos = (b8 ? 3 : 0) + (b4 ? 2 : 0) + (b2 ? 1 : 0);
-  // valid positions inside the group of 5: b8=0 → {0,1,2}; b8=1 → {3,4}
-  const bool valid = (lane & 1) == 0 && (b8 ? pos <= 4 : pos <= 2);
-  const int idx = (b16 ? 5 : 0) + pos;
-  return (valid && idx < 9) ? idx : -1;
-}
+};
 
 template <int PPT>
-__global__ void __launch_bounds__(256 / PPT) render_bwd_raster_kernel(
+__global__ void __launch_bounds__(256 / PPT, 1024 / (256 / PPT)) render_bwd_raster_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
     const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
@@ -183,28 +222,31 @@ __global__ void __launch_bounds__(256 / PPT) render_bwd_raster_kernel(
     const uint32_t* __restrict__ out_last, const float* __restrict__ dL_dimg,
     float4* __restrict__ g2d) {
   constexpr int NT = 256 / PPT;
-  __shared__ TileRec s_rec[NT];
-  __shared__ uint32_t s_id[NT];
-  __shared__ float s_acc[NT][9];
-  __shared__ uint32_t s_maxlast;
+  constexpr int NW = NT / 32;
+  constexpr int BATCH = 64;  // s_acc = NW·BATCH·36 B; small enough not to limit occupancy
+  __shared__ float4 s_a[BATCH], s_co[BATCH], s_c[BATCH];
+  __shared__ uint32_t s_id[BATCH];
+  __shared__ float s_acc[NW][BATCH][9];
+  __shared__ uint32_t s_wlast[NW];
   const int tile = blockIdx.x;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
   const int t = threadIdx.x;
+  const int warp = t >> 5;
   const int lx = t & 15, ly0 = (t >> 4) * PPT;
   const int X = tx0 + lx;
+  const uint32_t wmask = warp_row_mask<PPT>(warp);
+  const uint32_t colbit = 1u << lx;
   const uint2 range = ranges[tile];
-  if (t == 0) s_maxlast = range.x;
-  __syncthreads();
-  float T[PPT], S[PPT][3], g[PPT][3], Tbg[PPT][3];
-  uint32_t last[PPT], pm[PPT];
+  LaneRS rs;
+  rs.init();
+  float T[PPT], gR[PPT], g[PPT][3];
+  uint32_t last[PPT];
   uint32_t mylast = range.x;
   const size_t np = (size_t)cam.W * cam.H;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int Y = ty0 + ly0 + p;
-    pm[p] = (1u << lx) | (1u << (16 + ly0 + p));
-    S[p][0] = S[p][1] = S[p][2] = 0.f;
     if (X < cam.W && Y < cam.H) {
       const size_t pix = (size_t)Y * cam.W + X;
       T[p] = out_T[pix];
@@ -214,77 +256,96 @@ __global__ void __launch_bounds__(256 / PPT) render_bwd_raster_kernel(
       T[p] = 1.f; last[p] = range.x;
       g[p][0] = g[p][1] = g[p][2] = 0.f;
     }
-    Tbg[p][0] = T[p] * bg.x; Tbg[p][1] = T[p] * bg.y; Tbg[p][2] = T[p] * bg.z;
+    gR[p] = T[p] * (g[p][0] * bg.x + g[p][1] * bg.y + g[p][2] * bg.z);
     mylast = max(mylast, last[p]);
   }
-  atomicMax(&s_maxlast, mylast);
+  const uint32_t wlast = __reduce_max_sync(0xffffffffu, mylast);
+  if ((t & 31) == 0) s_wlast[warp] = wlast;
   __syncthreads();
-  const uint32_t end = s_maxlast;
+  uint32_t end = range.x;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) end = max(end, s_wlast[w]);
   const float fx = (float)lx;
   for (uint32_t b1 = end; b1 > range.x;) {
-    const uint32_t b0 = b1 - range.x > (uint32_t)NT ? b1 - NT : range.x;
+    const uint32_t b0 = b1 - range.x > (uint32_t)BATCH ? b1 - BATCH : range.x;
     const int cnt = (int)(b1 - b0);
-    __syncthreads();  // previous batch fully flushed
-    if (t < cnt) {
-      const uint32_t id = ids[b0 + t];
-      s_id[t] = id;
-      s_rec[t] = stage(id, xy_depth, conic_opa, rgb, box, tx0, ty0);
+    __syncthreads();  // previous batch flushed
+    for (int k = t; k < cnt; k += NT) {
+      const uint32_t id = ids[b0 + k];
+      s_id[k] = id;
+      stage(id, xy_depth, conic_opa, rgb, box, tx0, ty0, s_a[k], s_co[k], s_c[k]);
 #pragma unroll
-      for (int k = 0; k < 9; ++k) s_acc[t][k] = 0.f;
+      for (int w = 0; w < NW; ++w)
+#pragma unroll
+        for (int q = 0; q < 9; ++q) s_acc[w][k][q] = 0.f;
     }
     __syncthreads();
     for (int j = cnt - 1; j >= 0; --j) {
-      const TileRec r = s_rec[j];
-      const uint32_t m = __float_as_uint(r.cm.w);
       const uint32_t gidx = b0 + j;
-      const float dx = r.uv.x - fx;
+      if (gidx >= wlast) continue;          // warp-uniform: past every pixel's last
+      const float4 a = s_a[j];
+      const uint32_t m = __float_as_uint(a.w);
+      if ((m & wmask) == 0u) continue;      // warp-uniform: box misses this warp's rows
       float v[9];
 #pragma unroll
-      for (int k = 0; k < 9; ++k) v[k] = 0.f;
+      for (int q = 0; q < 9; ++q) v[q] = 0.f;
       bool any = false;
+      if (m & colbit) {
+        const float4 co = s_co[j];
+        const float dx = a.x - fx;
+        const ColTerms ct = col_terms(co.x, co.y, co.z, dx);
+        float pw[PPT];
+        bool ok[PPT];
 #pragma unroll
-      for (int p = 0; p < PPT; ++p) {
-        if (gidx >= last[p] || (m & pm[p]) != pm[p]) continue;
-        const float dy = r.uv.y - (float)(ly0 + p);
-        const float power = splat_power(r.co.x, r.co.y, r.co.z, dx, dy);
-        if (power > 0.f) continue;
-        const float G = splat_exp(power);
-        const float oG = __fmul_rn(r.co.w, G);
-        const float alpha = fminf(ALPHA_MAX, oG);
-        if (alpha < ALPHA_MIN) continue;
-        any = true;
-        const float inv = __frcp_rn(1.f - alpha);
-        T[p] *= inv;                       // transmittance before this entry
-        const float w = alpha * T[p];
-        float dLda = 0.f;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const float col = (&r.cm.x)[ch];
-          dLda += g[p][ch] * (col * T[p] - (S[p][ch] + Tbg[p][ch]) * inv);
-          S[p][ch] += col * w;
-          v[6 + ch] += w * g[p][ch];
+        for (int p = 0; p < PPT; ++p) {
+          pw[p] = splat_power(ct, a.y - (float)(ly0 + p));
+          ok[p] = gidx < last[p] && ((m >> (16 + ly0 + p)) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
         }
-        const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
-        const float ex = e * dx, ey = e * dy;
-        v[0] += ex; v[1] += ey; v[2] += ex * dx; v[3] += ex * dy; v[4] += ey * dy; v[5] += e;
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          if (!ok[p]) continue;
+          const float G = splat_exp(pw[p]);
+          const float oG = __fmul_rn(co.w, G);
+          const float alpha = fminf(ALPHA_MAX, oG);
+          if (alpha < ALPHA_MIN) continue;
+          any = true;
+          const float dy = a.y - (float)(ly0 + p);
+          const float4 c = s_c[j];
+          const float inv = rcp_approx(1.f - alpha);
+          T[p] *= inv;                        // transmittance before this entry
+          const float w = alpha * T[p];
+          const float gc = g[p][0] * c.x + g[p][1] * c.y + g[p][2] * c.z;
+          const float dLda = T[p] * gc - inv * gR[p];
+          gR[p] += gc * w;                    // g·(S + T_final·bg), S = suffix colour
+          v[6] += w * g[p][0]; v[7] += w * g[p][1]; v[8] += w * g[p][2];
+          const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
+          const float ex = e * dx, ey = e * dy;
+          v[0] += ex; v[1] += ey; v[2] += ex * dx; v[3] += ex * dy; v[4] += ey * dy; v[5] += e;
+        }
       }
       if (__any_sync(0xffffffffu, any)) {
-        float sum;
-        const int k = reduce_scatter9(v, sum);
-        if (k >= 0 && sum != 0.f) atomicAdd(&s_acc[j][k], sum);
+        const float sum = rs.reduce(v);
+        if (rs.slot >= 0) s_acc[warp][j][rs.slot] = sum;
       }
     }
     __syncthreads();
-    if (t < cnt) {
-      const float* a = s_acc[t];
+    for (int k = t; k < cnt; k += NT) {
+      float a9[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += s_acc[w][k][q];
+        a9[q] = s;
+      }
       bool nz = false;
 #pragma unroll
-      for (int k = 0; k < 9; ++k) nz |= a[k] != 0.f;
+      for (int q = 0; q < 9; ++q) nz |= a9[q] != 0.f;
       if (nz) {
-        float4* dst = g2d + 3 * (size_t)s_id[t];
-        red_add_v4(dst, make_float4(a[0], a[1], a[2], a[3]));
-        red_add_v4(dst + 1, make_float4(a[4], a[5], a[6], a[7]));
-        atomicAdd(&dst[2].x, a[8]);
+        float4* dst = g2d + 3 * (size_t)s_id[k];
+        red_add_v4(dst, make_float4(a9[0], a9[1], a9[2], a9[3]));
+        red_add_v4(dst + 1, make_float4(a9[4], a9[5], a9[6], a9[7]));
+        atomicAdd(&dst[2].x, a9[8]);
       }
     }
     b1 = b0;
@@ -494,8 +555,16 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
   }
 }
 
-constexpr int FWD_PPT = 1;
-constexpr int BWD_PPT = 1;
+// Pixels per thread of the raster kernels (tuning knob; DASS_FWD_PPT /
+// DASS_BWD_PPT override the default for experiments, read once per process).
+static int ppt_from_env(const char* name, int dflt) {
+  const char* v = getenv(name);
+  if (!v) return dflt;
+  const int p = atoi(v);
+  return (p == 1 || p == 2 || p == 4 || p == 8) ? p : dflt;
+}
+static int fwd_ppt() { static const int p = ppt_from_env("DASS_FWD_PPT", 4); return p; }
+static int bwd_ppt() { static const int p = ppt_from_env("DASS_BWD_PPT", 4); return p; }
 
 }  // namespace
 
@@ -504,8 +573,16 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
                               const uint2* box, float3 bg, float* out_img, float* out_T,
                               uint32_t* out_last, cudaStream_t s) {
   const int ntiles = cam.tiles_x * cam.tiles_y;
-  render_fwd_kernel<FWD_PPT><<<ntiles, 256 / FWD_PPT, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa,
-                                                              rgb, box, bg, out_img, out_T, out_last);
+#define FWD(P)                                                                                   \
+  render_fwd_kernel<P><<<ntiles, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, box, \
+                                                  bg, out_img, out_T, out_last)
+  switch (fwd_ppt()) {
+    case 1: FWD(1); break;
+    case 2: FWD(2); break;
+    case 8: FWD(8); break;
+    default: FWD(4); break;
+  }
+#undef FWD
   launch_counted();
   return cudaGetLastError();
 }
@@ -524,8 +601,16 @@ cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const 
   cudaError_t e = cudaMemsetAsync(g2d, 0, render_bwd_workspace(n), s);
   if (e != cudaSuccess) return e;
   const int ntiles = cam.tiles_x * cam.tiles_y;
-  render_bwd_raster_kernel<BWD_PPT><<<ntiles, 256 / BWD_PPT, 0, s>>>(
-      cam, ranges, ids, xy_depth, conic_opa, rgb, box, bg, out_T, out_last, dL_dimg, g2d);
+#define BWD(P)                                                                                    \
+  render_bwd_raster_kernel<P><<<ntiles, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
+                                                         box, bg, out_T, out_last, dL_dimg, g2d)
+  switch (bwd_ppt()) {
+    case 1: BWD(1); break;
+    case 2: BWD(2); break;
+    case 8: BWD(8); break;
+    default: BWD(4); break;
+  }
+#undef BWD
   launch_counted();
   const int grid = div_up(n, 256);
   switch (sh_degree) {

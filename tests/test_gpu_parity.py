@@ -110,25 +110,35 @@ def check_image(cam, scene, out, keep=None, bg=None, atol=1e-4, max_tie=1e-3):
     return o
 
 
-def check_grads(cam, scene, out, dL, keep=None, bg=None, tol=1e-3):
-    o = oracle.render_bwd(cam, scene, dL, keep=keep, bg=bg)
+def check_grads(cam, scene, out, dL, keep=None, bg=None, tol=1e-3, eps_kappa=1e-5):
+    """|Δ| ≤ 1e-3·max(|g_ref|, 1e-2·rms_field) — or, for cancelling sums,
+    |Δ| ≤ eps_kappa·κ where κ = Σ_px |per-pixel term| pushed through |Jacobian|
+    (oracle), the fp32 accuracy limit of such a sum.  The κ clause may rescue at
+    most 1e-3 of the entries; both counts are asserted."""
+    o = oracle.render_bwd(cam, scene, dL, keep=keep, bg=bg, kappa=True)
     g = out["grads"]
     ok = o["gtie"] == 0
     nc = (scene.sh_degree + 1) ** 2
     gsh = np_(g.sh).transpose(1, 0, 2).reshape(scene.n, -1)[:, :3 * nc].reshape(scene.n, nc, 3)
-    pairs = [("pos", np_(g.pos_opa)[:, :3], o["g_pos_opa"][:, :3]),
-             ("opa", np_(g.pos_opa)[:, 3], o["g_pos_opa"][:, 3]),
-             ("scale", np_(g.scale)[:, :3], o["g_scale"][:, :3]),
-             ("rot", np_(g.rot), o["g_rot"]),
-             ("sh", gsh, o["g_sh"]),
-             ("gradstat", np_(g.gradstat_sum), o["gradstat_sum"])]
-    for name, a, b in pairs:
+    pairs = [("pos", np_(g.pos_opa)[:, :3], o["g_pos_opa"][:, :3], o["k_pos_opa"][:, :3]),
+             ("opa", np_(g.pos_opa)[:, 3], o["g_pos_opa"][:, 3], o["k_pos_opa"][:, 3]),
+             ("scale", np_(g.scale)[:, :3], o["g_scale"][:, :3], o["k_scale"][:, :3]),
+             ("rot", np_(g.rot), o["g_rot"], o["k_rot"]),
+             ("sh", gsh, o["g_sh"], o["k_sh"]),
+             ("gradstat", np_(g.gradstat_sum), o["gradstat_sum"], None)]
+    report = {}
+    for name, a, b, k in pairs:
         a, b = a[ok], b[ok]
         rms = np.sqrt(np.mean(b ** 2)) if b.size else 0.0
-        bound = tol * np.maximum(np.abs(b), 1e-2 * rms)
-        bad = np.abs(a - b) > bound
+        rel_bound = tol * np.maximum(np.abs(b), 1e-2 * rms)
+        err = np.abs(a - b)
+        kb = 0.0 if k is None else eps_kappa * k[ok]
+        bad = err > np.maximum(rel_bound, kb)
+        rescued = int(((err > rel_bound) & ~bad).sum())
+        report[name] = (rescued, b.size)
         assert not bad.any(), (f"{name}: {bad.sum()} of {bad.size} over tolerance; worst rel "
-                               f"{(np.abs(a - b) / np.maximum(np.abs(b), 1e-2 * rms + 1e-30)).max():.3g}")
+                               f"{(err / np.maximum(np.abs(b), 1e-2 * rms + 1e-30)).max():.3g}")
+        assert rescued <= max(1, 1e-3 * b.size), f"{name}: {rescued} entries need the κ clause"
     assert np.array_equal(np_(g.gradstat_cnt), o["gradstat_cnt"])
     return o
 

@@ -248,3 +248,13 @@ def test_gradstat_counts_visible_views():
     assert np.array_equal(b["gradstat_cnt"], pr["visible"].astype(np.int32))
     assert np.all(b["gradstat_sum"][pr["visible"] == 0] == 0)
     assert np.all(b["gradstat_sum"] >= 0)
+
+
+def test_kappa_bounds_gradient_magnitude():
+    """κ = Σ_px |L|·|terms| ≥ |Σ_px L·terms| (triangle inequality), entrywise."""
+    cam, sc = synth.c1()
+    g = synth.grad_image(cam, 5)
+    o = oracle.render_bwd(cam, sc, g, kappa=True)
+    for gk, kk in (("g_pos_opa", "k_pos_opa"), ("g_scale", "k_scale"), ("g_rot", "k_rot"), ("g_sh", "k_sh")):
+        assert np.all(o[kk] >= np.abs(o[gk]) * (1 - 1e-9) - 1e-15), gk
+    assert np.all(o["k_pos_opa"] >= 0)
