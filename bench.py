@@ -38,10 +38,10 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 SM_COUNT = 148
 FP32_LANES = 128
 
-# Algorithmic FP32 work per unit of render_bwd raster:
-# an accepted (pixel, entry) evaluation and an in-box but rejected one.
-FLOP_BWD_ACCEPTED = 62
-FLOP_BWD_REJECTED = 15
+# Algorithmic FP32 work per accepted (pixel, entry) unit of render_bwd's raster
+# part (FMA = 2 flop).  Rejected in-box evaluations are not
+# counted, so the reported fraction is conservative.
+FLOP_BWD_ACCEPTED = 48
 
 
 def parse():
@@ -290,8 +290,7 @@ def run_ours(args):
         peak_tflops = SM_COUNT * FP32_LANES * 2 * f_max / 1e12
         # dominant op: render_bwd (raster kernel + fp32 preprocess), algorithmic
         # flops counted for the raster part only (conservative)
-        flops = sum(a * FLOP_BWD_ACCEPTED + (b - a) * FLOP_BWD_REJECTED
-                    for a, b in zip(stats["accepted"], stats["P_bwd"]))
+        flops = sum(a * FLOP_BWD_ACCEPTED for a in stats["accepted"])
         bwd_ms = ops.get("render_bwd", float("nan"))
         achieved = flops / (bwd_ms / 1e3) / 1e12 if bwd_ms == bwd_ms and bwd_ms > 0 else None
         views_s = len(cams) / (ms_step / 1e3)
@@ -311,7 +310,7 @@ def run_ours(args):
                          "frac": None if achieved is None else round(achieved / peak_tflops, 4),
                          "traffic": None, "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz ({pk_kind} clock)",
                          "units_per_step": {"accepted": sum(stats["accepted"]), "P_bwd": sum(stats["P_bwd"])},
-                         "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED, "rejected": FLOP_BWD_REJECTED}},
+                         "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED}},
             "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
             "scene_stats": {"K_per_view_mean": float(np.mean(allst["K"])),
                             "P_fwd_per_px": float(np.sum(allst["P_fwd"]) / (len(allst["K"]) * W * H)),

@@ -213,8 +213,8 @@ struct LaneRS {
   }
 };
 
-template <int PPT>
-__global__ void __launch_bounds__(256 / PPT, 1024 / (256 / PPT)) render_bwd_raster_kernel(
+template <int PPT, int MINB>
+__global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
     const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
@@ -565,6 +565,14 @@ static int ppt_from_env(const char* name, int dflt) {
 }
 static int fwd_ppt() { static const int p = ppt_from_env("DASS_FWD_PPT", 4); return p; }
 static int bwd_ppt() { static const int p = ppt_from_env("DASS_BWD_PPT", 4); return p; }
+static int bwd_minb() {
+  static const int m = [] {
+    const char* v = getenv("DASS_BWD_MINB");
+    const int p = v ? atoi(v) : 16;
+    return (p == 8 || p == 12 || p == 16) ? p : 16;
+  }();
+  return bwd_ppt() == 4 ? m : (bwd_ppt() == 1 ? 16 : (bwd_ppt() == 2 ? 8 : 16));
+}
 
 }  // namespace
 
@@ -601,14 +609,16 @@ cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const 
   cudaError_t e = cudaMemsetAsync(g2d, 0, render_bwd_workspace(n), s);
   if (e != cudaSuccess) return e;
   const int ntiles = cam.tiles_x * cam.tiles_y;
-#define BWD(P)                                                                                    \
-  render_bwd_raster_kernel<P><<<ntiles, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
-                                                         box, bg, out_T, out_last, dL_dimg, g2d)
-  switch (bwd_ppt()) {
-    case 1: BWD(1); break;
-    case 2: BWD(2); break;
-    case 8: BWD(8); break;
-    default: BWD(4); break;
+#define BWD(P, MB)                                                                          \
+  render_bwd_raster_kernel<P, MB><<<ntiles, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, \
+                                                             rgb, box, bg, out_T, out_last, dL_dimg, g2d)
+  switch (bwd_ppt() * 100 + bwd_minb()) {
+    case 116: BWD(1, 4); break;
+    case 208: BWD(2, 8); break;
+    case 816: BWD(8, 16); break;
+    case 412: BWD(4, 12); break;
+    case 408: BWD(4, 8); break;
+    default: BWD(4, 16); break;
   }
 #undef BWD
   launch_counted();
