@@ -52,7 +52,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--n", type=int, default=300_000)
     p.add_argument("--views", type=int, default=20)
-    p.add_argument("--capacity", type=int, default=1 << 24)
+    p.add_argument("--capacity", type=int, default=1 << 22, help="pair capacity per view")
+    p.add_argument("--streams", type=int, default=4, help="overlapping per-view streams")
+    p.add_argument("--no-graph", action="store_true", help="do not capture the step in a CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-views", type=int, default=2)
@@ -121,7 +123,7 @@ def run_ours(args):
 
     from paper_2411_14847_b200 import dass, synth
     from paper_2411_14847_b200.dist import FlatGrads, allreduce_grads, shard
-    from paper_2411_14847_b200.pipeline import DeviceScene, Raster, ViewRecords
+    from paper_2411_14847_b200.pipeline import DeviceScene, MultiViewPass, Raster, ViewRecords
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -150,9 +152,11 @@ def run_ours(args):
     grads = FlatGrads.allocate(n, K4, dev)
     flat, g_mu, g_sigma = grads.flat, grads.g_mu, grads.g_sigma
     records = ViewRecords(max(len(mine), 1), n, dev)
-    raster = Raster(W, H, n, args.capacity, dev)
+    raster = Raster(W, H, n, args.capacity, dev)   # single-stream scratch for stats/diagnostics
+    mvp = MultiViewPass(my_cams, n, args.capacity, dev, streams=args.streams) if my_cams else None
 
-    def step():
+    def step_local():
+        """Everything on this GPU (capturable: no host sync, no collective)."""
         grads.zero_()
         dass.dass_apply_shift(base.pos_opa, base.rot, mu_d, sigma_d, base.dynamic,
                               shifted.pos_opa, shifted.rot)
@@ -160,14 +164,21 @@ def run_ours(args):
             dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
                                     shifted.sh, None, records.xy_depth, records.conic_opa,
                                     records.rgb, records.box, records.tiles)
-        for k, cam in enumerate(my_cams):
-            rec = records.view(k)
-            raster.forward(cam, rec)
-            raster.backward(cam, shifted, rec, dLs[k], grads)
+        if mvp is not None:
+            mvp.run(shifted, records, dLs, grads)
         dass.dass_apply_shift_bwd(base.rot, sigma_d, base.dynamic, grads.pos_opa, grads.rot,
                                   g_mu, g_sigma)
+
+    def run_step(graph=None):
+        if graph is None:
+            step_local()
+        else:
+            graph.replay()
         if world > 1:
-            allreduce_grads(grads)
+            allreduce_grads(grads)   # the one cross-GPU exchange (NCCL over NVLink)
+
+    def step():
+        run_step(None)
 
     def barrier():
         if world > 1:
@@ -191,53 +202,84 @@ def run_ours(args):
         stats["tile_list_mean"].append(float(c[4]) / max(int(c[6]), 1))
         stats["tile_list_max"].append(int(c[5]))
 
-    # ---- warm-up, then exactly K timed steps
+    # ---- warm-up (eager), then capture the step in a CUDA graph
     for _ in range(args.warmup):
         step()
     barrier()
+    graph = None
+    per_step_launches = None
+    if not args.no_graph:
+        l0 = dass.kernel_launches()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step_local()
+        per_step_launches = dass.kernel_launches() - l0
+        for _ in range(2):
+            run_step(graph)
+        barrier()
+
+    def timed():
+        run_step(graph)
+
+    # ---- exactly K timed steps
     l0 = dass.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         ev0.record()
         for _ in range(args.steps):
-            step()
+            timed()
         ev1.record()
         barrier()
     launches = dass.kernel_launches() - l0
+    if graph is not None:
+        launches = per_step_launches * args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_step = float(ms_t.item())
 
-    # ---- per-op breakdown on one extra step (events on the launching stream)
+    # ---- per-op breakdown: one extra SEQUENTIAL step, CUDA events on the
+    # launching stream around each export (diagnostic; the timed step overlaps views)
     ops = {}
     if my_cams:
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4 * len(my_cams) + 2)]
-        evs[0].record()
+        E = lambda: torch.cuda.Event(enable_timing=True)
+        e_proj = [E(), E()]
+        e_proj[0].record()
         dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
                                 shifted.sh, None, records.xy_depth, records.conic_opa,
                                 records.rgb, records.box, records.tiles)
-        evs[1].record()
+        e_proj[1].record()
+        per = []
         for k, cam in enumerate(my_cams):
-            rec = records.view(k)
-            xy, co, rgb, box, tiles = rec
+            xy, co, rgb, box, tiles = records.view(k)
+            ev = [E() for _ in range(4)]
+            ev[0].record()
             dass.dass_bin_sort(cam, n, xy, box, tiles, raster.sort_ws, raster.capacity, None,
                                raster.sorted_ids, raster.ranges, raster.num_pairs)
-            evs[2 + 4 * k].record()
+            ev[1].record()
             dass.dass_render_fwd(cam, raster.ranges, raster.sorted_ids, xy, co, rgb, box, None,
                                  raster.img, raster.T, raster.last)
-            evs[3 + 4 * k].record()
-            raster.backward(cam, shifted, rec, dLs[k], grads)
-            evs[4 + 4 * k].record()
-            evs[5 + 4 * k].record()
+            ev[2].record()
+            dass.dass_render_bwd_raster(cam, n, raster.ranges, raster.sorted_ids, xy, co, rgb, box,
+                                        None, raster.T, raster.last, dLs[k], mvp.g2d[k])
+            ev[3].record()
+            per.append(ev)
+        e_pre = [E(), E()]
+        e_pre[0].record()
+        dass.dass_render_bwd_preprocess_views(
+            my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot, shifted.sh, None,
+            records.conic_opa[:len(my_cams)], records.rgb[:len(my_cams)], records.box[:len(my_cams)],
+            mvp.g2d[:len(my_cams)], grads.pos_opa, grads.scale, grads.rot, grads.sh,
+            grads.gradstat_sum, grads.gradstat_cnt)
+        e_pre[1].record()
         torch.cuda.synchronize()
-        ops["project_views"] = evs[0].elapsed_time(evs[1])
-        ops["bin_sort"] = sum(evs[1 + 4 * k if k == 0 else 1 + 4 * k].elapsed_time(evs[2 + 4 * k])
-                              for k in range(len(my_cams)))
-        ops["render_fwd"] = sum(evs[2 + 4 * k].elapsed_time(evs[3 + 4 * k]) for k in range(len(my_cams)))
-        ops["render_bwd"] = sum(evs[3 + 4 * k].elapsed_time(evs[4 + 4 * k]) for k in range(len(my_cams)))
+        ops["project_views"] = e_proj[0].elapsed_time(e_proj[1])
+        ops["bin_sort"] = sum(ev[0].elapsed_time(ev[1]) for ev in per)
+        ops["render_fwd"] = sum(ev[1].elapsed_time(ev[2]) for ev in per)
+        ops["render_bwd_raster"] = sum(ev[2].elapsed_time(ev[3]) for ev in per)
+        ops["render_bwd_preprocess_views"] = e_pre[0].elapsed_time(e_pre[1])
 
     # ---- end-to-end through the public API with host buffers
     e2e = None
@@ -253,7 +295,7 @@ def run_ours(args):
         def e2e_step():
             for h, d in zip(h_in, d_in):
                 d.copy_(h, non_blocking=True)
-            step()
+            run_step(graph)
             h_out.copy_(flat, non_blocking=True)
 
         for _ in range(2):
@@ -291,7 +333,7 @@ def run_ours(args):
         # dominant op: render_bwd (raster kernel + fp32 preprocess), algorithmic
         # flops counted for the raster part only (conservative)
         flops = sum(a * FLOP_BWD_ACCEPTED for a in stats["accepted"])
-        bwd_ms = ops.get("render_bwd", float("nan"))
+        bwd_ms = ops.get("render_bwd_raster", float("nan"))
         achieved = flops / (bwd_ms / 1e3) / 1e12 if bwd_ms == bwd_ms and bwd_ms > 0 else None
         views_s = len(cams) / (ms_step / 1e3)
         result = {
@@ -302,9 +344,10 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N3DV-shaped scene and rig)",
             "config": {"workload": WORKLOAD, "n_gaussians": n, "views": len(cams), "width": W,
                        "height": H, "sh_degree": deg, "dynamic_frac": 0.3,
+                       "cuda_graph": graph is not None, "streams": args.streams,
                        "parallelism": f"view-sharded dp{world}",
                        "l2": "inputs larger than L2 (≈0.5 GB of params, dL/dC and records per step)"},
-            "roofline": {"bound": "alu", "kernel": "render_bwd (raster + preprocess; raster flops only)",
+            "roofline": {"bound": "alu", "kernel": "render_bwd_raster_kernel (accepted units only)",
                          "achieved": None if achieved is None else round(achieved, 2),
                          "peak": round(peak_tflops, 1), "unit": "TFLOP/s",
                          "frac": None if achieved is None else round(achieved / peak_tflops, 4),

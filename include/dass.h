@@ -276,6 +276,38 @@ int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree,
                     void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Two-phase backward for multi-view batches (same mathematics as
+ * dass_render_bwd, which is exactly phase 1 + phase 2 for V = 1):
+ *
+ * dass_render_bwd_raster — phase 1, one view: the per-pixel reverse pass of
+ *   Eq. 8.  Writes (overwrites) the view's per-Gaussian 2D moment workspace
+ *   g2d: float[N][12] (3 float4 per Gaussian, dass_render_bwd_workspace
+ *   bytes): (Σe·dx, Σe·dy, Σe·dx², Σe·dx·dy, Σe·dy², Σe, Σ αT·g_rgb) with
+ *   e = G·∂L/∂α (0 where α is clamped).  Views on distinct streams may run
+ *   concurrently (each writes only its own g2d).
+ *
+ * dass_render_bwd_preprocess_views — phase 2, V views at once: chains every
+ *   view's moments through Eqs. 5-7 and the SH colour into ∂L/∂(p, s, q, o,
+ *   sh) and ∇p̄, reading the parameters once and updating each output once
+ *   (+=).  cams[V]; records as written by dass_project_views ([V][N]
+ *   concatenations of conic_opa, rgb, box); g2d: V phase-1 workspaces
+ *   concatenated ([V][N][12] floats).
+ * ------------------------------------------------------------------------- */
+int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* tile_ranges,
+                           const uint32_t* sorted_ids, const float* xy_depth,
+                           const float* conic_opa, const float* rgb, const uint32_t* box,
+                           const float* bg, const float* out_T, const uint32_t* out_last,
+                           const float* dL_dimg, float* g2d, void* stream);
+int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views, int32_t n,
+                                     int32_t sh_degree, const float* pos_opa,
+                                     const float* scale, const float* rot, const float* sh,
+                                     const uint8_t* keep_mask, const float* conic_opa,
+                                     const float* rgb, const uint32_t* box, const float* g2d,
+                                     float* g_pos_opa, float* g_scale, float* g_rot,
+                                     float* g_sh, float* gradstat_sum,
+                                     uint32_t* gradstat_cnt, void* stream);
+
+/* ---------------------------------------------------------------------------
  * dass_error_map — error map, binarisation and Alg. 1 (§3.4 P:164-165, P:174;
  * Alg. 1 P:403-415 with the garble fixed, A20-A22).
  *   E(X,Y) = (1/3)·Σ_ch |rendered − gt|  → err (float [H][W], nullable)

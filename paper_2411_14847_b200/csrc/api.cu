@@ -256,6 +256,61 @@ int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree, const 
       "dass_render_bwd");
 }
 
+int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* tile_ranges,
+                           const uint32_t* sorted_ids, const float* xy_depth,
+                           const float* conic_opa, const float* rgb, const uint32_t* box,
+                           const float* bg, const float* out_T, const uint32_t* out_last,
+                           const float* dL_dimg, float* g2d, void* stream) {
+  int st = check_camera(cam);
+  if (st) return st;
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (n == 0) return DASS_OK;
+  if (!tile_ranges || !sorted_ids || !xy_depth || !conic_opa || !rgb || !box || !out_T ||
+      !out_last || !dL_dimg || !g2d)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_raster: null required pointer%s");
+  if (!aligned16(g2d)) return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_raster: g2d must be 16-byte aligned%s");
+  CamParams cp = to_params(cam);
+  float3 b = bg ? make_float3(bg[0], bg[1], bg[2]) : make_float3(0.f, 0.f, 0.f);
+  return cuda_status(launch_render_bwd_raster(cp, n, (const uint2*)tile_ranges, sorted_ids,
+                                              (const float4*)xy_depth, (const float4*)conic_opa,
+                                              (const float4*)rgb, (const uint2*)box, b, out_T,
+                                              out_last, dL_dimg, (float4*)g2d,
+                                              (cudaStream_t)stream),
+                     "dass_render_bwd_raster");
+}
+
+int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views, int32_t n,
+                                     int32_t sh_degree, const float* pos_opa,
+                                     const float* scale, const float* rot, const float* sh,
+                                     const uint8_t* keep_mask, const float* conic_opa,
+                                     const float* rgb, const uint32_t* box, const float* g2d,
+                                     float* g_pos_opa, float* g_scale, float* g_rot,
+                                     float* g_sh, float* gradstat_sum,
+                                     uint32_t* gradstat_cnt, void* stream) {
+  if (cams == nullptr) return fail(DASS_ERR_INVALID_ARG, "cams is null%s");
+  if (num_views < 1 || num_views > 64) return fail(DASS_ERR_INVALID_ARG, "num_views must be in [1, 64]%s");
+  for (int v = 0; v < num_views; ++v) {
+    int st = check_camera(cams + v);
+    if (st) return st;
+  }
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (sh_degree < 0 || sh_degree > 3) return fail(DASS_ERR_INVALID_ARG, "sh_degree must be in [0, 3]%s");
+  if (n == 0) return DASS_OK;
+  if (!pos_opa || !scale || !rot || !sh || !conic_opa || !rgb || !box || !g2d)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_preprocess_views: null required pointer%s");
+  CamParams cp[64];
+  for (int v = 0; v < num_views; ++v) cp[v] = to_params(cams + v);
+  return cuda_status(launch_preprocess_views(cp, num_views, n, sh_degree, (const float4*)pos_opa,
+                                             (const float4*)scale, (const float4*)rot,
+                                             (const float4*)sh, keep_mask,
+                                             (const float4*)conic_opa, (const float4*)rgb,
+                                             (const uint2*)box, (const float4*)g2d,
+                                             (float4*)g_pos_opa, (float4*)g_scale,
+                                             (float4*)g_rot, (float4*)g_sh, gradstat_sum,
+                                             gradstat_cnt, (cudaStream_t)stream),
+                     "dass_render_bwd_preprocess_views");
+}
+
 int dass_error_map(const dass_camera* cam, const float* rendered, const float* gt, float gamma_err,
                    float* err, uint32_t* dmask, int32_t n_base, const float* pos_opa,
                    uint8_t* s_err, void* stream) {

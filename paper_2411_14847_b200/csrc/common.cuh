@@ -115,6 +115,18 @@ cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const 
                               const uint32_t* out_last, const float* dL_dimg, void* ws,
                               float4* g_pos_opa, float4* g_scale, float4* g_rot, float4* g_sh,
                               float* gradstat_sum, uint32_t* gradstat_cnt, cudaStream_t s);
+cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* ranges,
+                                     const uint32_t* ids, const float4* xy_depth,
+                                     const float4* conic_opa, const float4* rgb, const uint2* box,
+                                     float3 bg, const float* out_T, const uint32_t* out_last,
+                                     const float* dL_dimg, float4* g2d, cudaStream_t s);
+cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n, int sh_degree,
+                                    const float4* pos_opa, const float4* scale, const float4* rot,
+                                    const float4* sh, const uint8_t* keep,
+                                    const float4* conic_opa, const float4* rgb, const uint2* box,
+                                    const float4* g2d, float4* g_pos_opa, float4* g_scale,
+                                    float4* g_rot, float4* g_sh, float* gradstat_sum,
+                                    uint32_t* gradstat_cnt, cudaStream_t s);
 cudaError_t launch_error_map(const CamParams& cam, const float* rendered, const float* gt,
                              float gamma, float* err, uint32_t* dmask, int n_base,
                              const float4* pos_opa, uint8_t* s_err, cudaStream_t s);

@@ -93,7 +93,7 @@ __device__ __forceinline__ uint32_t warp_row_mask(int warp) {
 
 // ------------------------------------------------------------- forward ----
 template <int PPT>
-__global__ void __launch_bounds__(256 / PPT, 1024 / (256 / PPT)) render_fwd_kernel(
+__global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
     const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
@@ -122,6 +122,9 @@ __global__ void __launch_bounds__(256 / PPT, 1024 / (256 / PPT)) render_fwd_kern
     done[p] = !(X < cam.W && Y < cam.H);
   }
   const float fx = (float)lx;
+  float fy[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) fy[p] = (float)(ly0 + p);
   for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
     bool alive = false;
 #pragma unroll
@@ -138,12 +141,13 @@ __global__ void __launch_bounds__(256 / PPT, 1024 / (256 / PPT)) render_fwd_kern
       if ((m & colbit) == 0u) continue;
       const float4 co = s_co[j];
       const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fx);
+      const uint32_t mr = m >> (16 + ly0);   // this thread's PPT row bits
       float pw[PPT];
       bool ok[PPT];
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {   // independent per pixel: no branches, full ILP
-        pw[p] = splat_power(ct, a.y - (float)(ly0 + p));
-        ok[p] = !done[p] && ((m >> (16 + ly0 + p)) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
+        pw[p] = splat_power(ct, a.y - fy[p]);
+        ok[p] = !done[p] && ((mr >> p) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
       }
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
@@ -266,6 +270,9 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
 #pragma unroll
   for (int w = 0; w < NW; ++w) end = max(end, s_wlast[w]);
   const float fx = (float)lx;
+  float fy[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) fy[p] = (float)(ly0 + p);
   for (uint32_t b1 = end; b1 > range.x;) {
     const uint32_t b0 = b1 - range.x > (uint32_t)BATCH ? b1 - BATCH : range.x;
     const int cnt = (int)(b1 - b0);
@@ -294,12 +301,13 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
         const float4 co = s_co[j];
         const float dx = a.x - fx;
         const ColTerms ct = col_terms(co.x, co.y, co.z, dx);
+        const uint32_t mr = m >> (16 + ly0);   // this thread's PPT row bits
         float pw[PPT];
         bool ok[PPT];
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
-          pw[p] = splat_power(ct, a.y - (float)(ly0 + p));
-          ok[p] = gidx < last[p] && ((m >> (16 + ly0 + p)) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
+          pw[p] = splat_power(ct, a.y - fy[p]);
+          ok[p] = gidx < last[p] && ((mr >> p) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
         }
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
           const float alpha = fminf(ALPHA_MAX, oG);
           if (alpha < ALPHA_MIN) continue;
           any = true;
-          const float dy = a.y - (float)(ly0 + p);
+          const float dy = a.y - fy[p];
           const float4 c = s_c[j];
           const float inv = rcp_approx(1.f - alpha);
           T[p] *= inv;                        // transmittance before this entry
@@ -353,84 +361,44 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
 }
 
 // --------------------------------------------- backward: preprocess part ----
-// Per Gaussian: 2D moments → ∂L/∂(u, v, A, B, C, o, rgb) → chain through
-// Eqs. 5-7 and the SH colour to ∂L/∂(p, s, q, o, sh); accumulate (+=).
+// Per Gaussian, over V views: each view's 2D moments → ∂L/∂(u, v, A, B, C, o,
+// rgb) → chained through Eqs. 5-7 and the SH colour.  The parameters are read
+// once, R and Σ are built once, and the view-independent ∂L/∂Σ is summed over
+// the views before the scale/rotation chain, so every output is updated once
+// (+=) per launch (multi-view batching).
+constexpr int PRE_MAXV = 32;  // views per launch (kernel-parameter budget)
+
+struct PreArgs {
+  CamParams cam[PRE_MAXV];
+  int num_views, n;
+  const float4* pos_opa;
+  const float4* scale;
+  const float4* rot;
+  const float4* sh;
+  const uint8_t* keep;
+  const float4* conic_opa;  // [V][N]
+  const float4* rgb;        // [V][N]
+  const uint2* box;         // [V][N]
+  const float4* g2d;        // [V][N][3]
+  float4* g_pos_opa;
+  float4* g_scale;
+  float4* g_rot;
+  float4* g_sh;
+  float* gradstat_sum;
+  uint32_t* gradstat_cnt;
+};
+
 template <int DEG>
-__global__ void __launch_bounds__(256) preprocess_bwd_kernel(
-    const __grid_constant__ CamParams cam, int n, const float4* __restrict__ pos_opa,
-    const float4* __restrict__ scale, const float4* __restrict__ rot,
-    const float4* __restrict__ sh, const uint8_t* __restrict__ keep,
-    const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
-    const uint2* __restrict__ box, const float4* __restrict__ g2d, float4* g_pos_opa,
-    float4* g_scale, float4* g_rot, float4* g_sh, float* gradstat_sum, uint32_t* gradstat_cnt) {
+__global__ void __launch_bounds__(256, 2) preprocess_views_kernel(const __grid_constant__ PreArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint2 bx = box[i];
-  if ((bx.x & 0xFFFFu) > (bx.x >> 16)) return;  // culled in this view
-  const float4 m0 = g2d[3 * (size_t)i], m1 = g2d[3 * (size_t)i + 1], m2 = g2d[3 * (size_t)i + 2];
-  const float4 co = conic_opa[i];
-  const float A = co.x, B = co.y, Cc = co.z, o = co.w;
-  // 2D gradients from the moments
-  const float gu = -o * (A * m0.x + B * m0.y);
-  const float gv = -o * (B * m0.x + Cc * m0.y);
-  const float gA = -0.5f * o * m0.z;
-  const float gB = -o * m0.w;
-  const float gC = -0.5f * o * m1.x;
-  const float go = m1.y;
-  const float4 cl = rgb[i];
-  const int bits = (int)cl.w;
-  const float gcol[3] = {(bits & 1) ? 0.f : m1.z, (bits & 2) ? 0.f : m1.w, (bits & 4) ? 0.f : m2.x};
-  if (gradstat_sum) {
-    const float a = gu * 0.5f * cam.W, b = gv * 0.5f * cam.H;
-    gradstat_sum[i] += sqrtf(a * a + b * b);
-  }
-  if (gradstat_cnt) gradstat_cnt[i] += 1u;
-  const bool kp = keep == nullptr || keep[i] != 0;
-  const float4 po = pos_opa[i];
-  float gp[3] = {0.f, 0.f, 0.f};
-  // ---- colour / SH
-  {
-    float dx = po.x - cam.campos[0], dy = po.y - cam.campos[1], dz = po.z - cam.campos[2];
-    const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
-    const float inv = 1.f / dist;
-    dx *= inv; dy *= inv; dz *= inv;
-    using L = SHLayout<DEG>;
-    float Y[L::NC];
-    sh_eval<DEG>(dx, dy, dz, Y);
-    float wk[L::NC];
-#pragma unroll
-    for (int k = 0; k < L::NC; ++k) wk[k] = 0.f;
-#pragma unroll
-    for (int j = 0; j < L::K4; ++j) {
-      const size_t off = (size_t)j * n + i;
-      const float4 c4 = sh[off];
-      float4 gg = g_sh ? g_sh[off] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int f = 4 * j + e;
-        if (f < L::NF) {
-          const int k = f / 3, ch = f % 3;
-          wk[k] += gcol[ch] * (&c4.x)[e];
-          (&gg.x)[e] += Y[k] * gcol[ch];
-        }
-      }
-      if (g_sh) g_sh[off] = gg;
-    }
-    if (DEG > 0) {
-      const float3 gd = sh_dir_grad<DEG>(dx, dy, dz, wk);
-      const float dd = dx * gd.x + dy * gd.y + dz * gd.z;
-      gp[0] += (gd.x - dx * dd) * inv;
-      gp[1] += (gd.y - dy * dd) * inv;
-      gp[2] += (gd.z - dz * dd) * inv;
-    }
-  }
-  if (!g_pos_opa && !g_scale && !g_rot) return;
-  // ---- recompute the projection quantities (fp32)
-  const float* V = cam.V;
-  float t[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) t[a] = V[4 * a] * po.x + V[4 * a + 1] * po.y + V[4 * a + 2] * po.z + V[4 * a + 3];
-  const float4 q = rot[i];
+  if (i >= a.n) return;
+  const int n = a.n;
+  using L = SHLayout<DEG>;
+  const bool kp = a.keep == nullptr || a.keep[i] != 0;
+  const float4 po = a.pos_opa[i];
+  const float4 q = a.rot[i];
+  const float4 sc = a.scale[i];
+  // view-independent geometry: q̂, R, s, Σ
   const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
   const float qi = 1.f / qn;
   const float w = q.x * qi, x = q.y * qi, y = q.z * qi, z = q.w * qi;
@@ -438,86 +406,170 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
   R[0][0] = 1.f - 2.f * (y * y + z * z); R[0][1] = 2.f * (x * y - w * z); R[0][2] = 2.f * (x * z + w * y);
   R[1][0] = 2.f * (x * y + w * z); R[1][1] = 1.f - 2.f * (x * x + z * z); R[1][2] = 2.f * (y * z - w * x);
   R[2][0] = 2.f * (x * z - w * y); R[2][1] = 2.f * (y * z + w * x); R[2][2] = 1.f - 2.f * (x * x + y * y);
-  const float4 sc = scale[i];
   const float s[3] = {kp ? sc.x : 0.f, kp ? sc.y : 0.f, kp ? sc.z : 0.f};
   float Sig[3][3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
+  for (int r0 = 0; r0 < 3; ++r0)
 #pragma unroll
-    for (int b = 0; b < 3; ++b)
-      Sig[a][b] = R[a][0] * s[0] * s[0] * R[b][0] + R[a][1] * s[1] * s[1] * R[b][1] +
-                  R[a][2] * s[2] * s[2] * R[b][2];
-  const float lx = 1.3f * cam.W / (2.f * cam.fx), ly = 1.3f * cam.H / (2.f * cam.fy);
-  const float txtz = t[0] / t[2], tytz = t[1] / t[2];
-  const bool clx = txtz < -lx || txtz > lx, cly = tytz < -ly || tytz > ly;
-  const float xt = t[2] * fminf(lx, fmaxf(-lx, txtz));
-  const float yt = t[2] * fminf(ly, fmaxf(-ly, tytz));
-  const float tz = t[2], tz2 = tz * tz, tz3 = tz2 * tz;
-  const float J00 = cam.fx / tz, J02 = -cam.fx * xt / tz2;
-  const float J11 = cam.fy / tz, J12 = -cam.fy * yt / tz2;
-  float M[2][3];
+    for (int c0 = 0; c0 < 3; ++c0)
+      Sig[r0][c0] = R[r0][0] * s[0] * s[0] * R[c0][0] + R[r0][1] * s[1] * s[1] * R[c0][1] +
+                    R[r0][2] * s[2] * s[2] * R[c0][2];
+  // accumulators over views
+  float gp[3] = {0.f, 0.f, 0.f};
+  float go = 0.f;
+  float GS[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+  float gsh[4 * L::K4];
 #pragma unroll
-  for (int b = 0; b < 3; ++b) {
-    M[0][b] = J00 * V[b] + J02 * V[8 + b];
-    M[1][b] = J11 * V[4 + b] + J12 * V[8 + b];
+  for (int f = 0; f < 4 * L::K4; ++f) gsh[f] = 0.f;
+  float gstat = 0.f;
+  uint32_t nvis = 0;
+  for (int v = 0; v < a.num_views; ++v) {
+    const size_t o = (size_t)v * n + i;
+    const uint2 bx = a.box[o];
+    if ((bx.x & 0xFFFFu) > (bx.x >> 16)) continue;  // culled in this view
+    const CamParams& cam = a.cam[v];
+    ++nvis;
+    const float4 m0 = a.g2d[3 * o], m1 = a.g2d[3 * o + 1], m2 = a.g2d[3 * o + 2];
+    const float4 co = a.conic_opa[o];
+    const float A = co.x, B = co.y, Cc = co.z, op = co.w;
+    // 2D gradients from the moments
+    const float gu = -op * (A * m0.x + B * m0.y);
+    const float gv = -op * (B * m0.x + Cc * m0.y);
+    const float gA = -0.5f * op * m0.z;
+    const float gB = -op * m0.w;
+    const float gC = -0.5f * op * m1.x;
+    go += m1.y;
+    const int bits = (int)a.rgb[o].w;
+    const float gcol[3] = {(bits & 1) ? 0.f : m1.z, (bits & 2) ? 0.f : m1.w, (bits & 4) ? 0.f : m2.x};
+    {
+      const float ga = gu * 0.5f * cam.W, gb = gv * 0.5f * cam.H;
+      gstat += sqrtf(ga * ga + gb * gb);
+    }
+    // ---- colour / SH (direction from this view's camera centre)
+    {
+      float dx = po.x - cam.campos[0], dy = po.y - cam.campos[1], dz = po.z - cam.campos[2];
+      const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
+      const float inv = 1.f / dist;
+      dx *= inv; dy *= inv; dz *= inv;
+      float Y[L::NC];
+      sh_eval<DEG>(dx, dy, dz, Y);
+      float wk[L::NC];
+#pragma unroll
+      for (int k = 0; k < L::NC; ++k) wk[k] = 0.f;
+#pragma unroll
+      for (int j = 0; j < L::K4; ++j) {
+        // re-read per view (L1-resident) instead of pinning 48 registers
+        const float4 c4 = a.sh[(size_t)j * n + i];
+        const float cf[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int f = 4 * j + e;
+          if (f < L::NF) {
+            const int k = f / 3, ch = f % 3;
+            wk[k] += gcol[ch] * cf[e];
+            gsh[f] += Y[k] * gcol[ch];
+          }
+        }
+      }
+      if (DEG > 0) {
+        const float3 gd = sh_dir_grad<DEG>(dx, dy, dz, wk);
+        const float dd = dx * gd.x + dy * gd.y + dz * gd.z;
+        gp[0] += (gd.x - dx * dd) * inv;
+        gp[1] += (gd.y - dy * dd) * inv;
+        gp[2] += (gd.z - dz * dd) * inv;
+      }
+    }
+    // ---- projection chain for this view
+    const float* V = cam.V;
+    float t[3];
+#pragma unroll
+    for (int r0 = 0; r0 < 3; ++r0)
+      t[r0] = V[4 * r0] * po.x + V[4 * r0 + 1] * po.y + V[4 * r0 + 2] * po.z + V[4 * r0 + 3];
+    const float lx = 1.3f * cam.W / (2.f * cam.fx), ly = 1.3f * cam.H / (2.f * cam.fy);
+    const float txtz = t[0] / t[2], tytz = t[1] / t[2];
+    const bool clx = txtz < -lx || txtz > lx, cly = tytz < -ly || tytz > ly;
+    const float xt = t[2] * fminf(lx, fmaxf(-lx, txtz));
+    const float yt = t[2] * fminf(ly, fmaxf(-ly, tytz));
+    const float tz = t[2], tz2 = tz * tz, tz3 = tz2 * tz;
+    const float J00 = cam.fx / tz, J02 = -cam.fx * xt / tz2;
+    const float J11 = cam.fy / tz, J12 = -cam.fy * yt / tz2;
+    float M[2][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      M[0][b] = J00 * V[b] + J02 * V[8 + b];
+      M[1][b] = J11 * V[4 + b] + J12 * V[8 + b];
+    }
+    // conic → Σ': Gs = −K Ĝ K, Ĝ = [[gA, gB/2],[gB/2, gC]]
+    const float G01h = 0.5f * gB;
+    const float KG00 = A * gA + B * G01h, KG01 = A * G01h + B * gC;
+    const float KG10 = B * gA + Cc * G01h, KG11 = B * G01h + Cc * gC;
+    const float Gs00 = -(KG00 * A + KG01 * B);
+    const float Gs01 = -(KG00 * B + KG01 * Cc);
+    const float Gs11 = -(KG10 * B + KG11 * Cc);
+    float GM1[2][3];  // Gs M
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      GM1[0][b] = Gs00 * M[0][b] + Gs01 * M[1][b];
+      GM1[1][b] = Gs01 * M[0][b] + Gs11 * M[1][b];
+    }
+    // ∂L/∂Σ += Mᵀ Gs M  (summed over views, chained once below)
+#pragma unroll
+    for (int r0 = 0; r0 < 3; ++r0)
+#pragma unroll
+      for (int c0 = 0; c0 < 3; ++c0) GS[r0][c0] += M[0][r0] * GM1[0][c0] + M[1][r0] * GM1[1][c0];
+    // ∂L/∂M = 2 Gs M Σ → ∂L/∂J = ∂L/∂M Wᵀ
+    float GM[2][3];
+#pragma unroll
+    for (int r0 = 0; r0 < 2; ++r0)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        GM[r0][b] = 2.f * (GM1[r0][0] * Sig[0][b] + GM1[r0][1] * Sig[1][b] + GM1[r0][2] * Sig[2][b]);
+    const float GJ00 = GM[0][0] * V[0] + GM[0][1] * V[1] + GM[0][2] * V[2];
+    const float GJ02 = GM[0][0] * V[8] + GM[0][1] * V[9] + GM[0][2] * V[10];
+    const float GJ11 = GM[1][0] * V[4] + GM[1][1] * V[5] + GM[1][2] * V[6];
+    const float GJ12 = GM[1][0] * V[8] + GM[1][1] * V[9] + GM[1][2] * V[10];
+    float gt[3] = {0.f, 0.f, 0.f};
+    gt[2] += GJ00 * (-cam.fx / tz2) + GJ11 * (-cam.fy / tz2);
+    if (!clx) {
+      gt[0] += GJ02 * (-cam.fx / tz2);
+      gt[2] += GJ02 * (2.f * cam.fx * t[0] / tz3);
+    } else {
+      gt[2] += GJ02 * (cam.fx * xt / tz3);
+    }
+    if (!cly) {
+      gt[1] += GJ12 * (-cam.fy / tz2);
+      gt[2] += GJ12 * (2.f * cam.fy * t[1] / tz3);
+    } else {
+      gt[2] += GJ12 * (cam.fy * yt / tz3);
+    }
+    gt[0] += gu * cam.fx / tz;
+    gt[2] += gu * (-cam.fx * t[0] / tz2);
+    gt[1] += gv * cam.fy / tz;
+    gt[2] += gv * (-cam.fy * t[1] / tz2);
+#pragma unroll
+    for (int c0 = 0; c0 < 3; ++c0) gp[c0] += V[c0] * gt[0] + V[4 + c0] * gt[1] + V[8 + c0] * gt[2];
   }
-  // conic → Σ': Gs = −K Ĝ K, Ĝ = [[gA, gB/2],[gB/2, gC]]
-  const float K00 = A, K01 = B, K11 = Cc;
-  const float G00 = gA, G01 = 0.5f * gB, G11 = gC;
-  const float KG00 = K00 * G00 + K01 * G01, KG01 = K00 * G01 + K01 * G11;
-  const float KG10 = K01 * G00 + K11 * G01, KG11 = K01 * G01 + K11 * G11;
-  const float Gs00 = -(KG00 * K00 + KG01 * K01);
-  const float Gs01 = -(KG00 * K01 + KG01 * K11);
-  const float Gs11 = -(KG10 * K01 + KG11 * K11);
-  const float Gs[2][2] = {{Gs00, Gs01}, {Gs01, Gs11}};
-  // dL/dΣ = Mᵀ Gs M ; dL/dM = 2 Gs M Σ
-  float GM1[2][3];  // Gs M
+  if (nvis == 0) return;
+  if (a.gradstat_sum) a.gradstat_sum[i] += gstat;
+  if (a.gradstat_cnt) a.gradstat_cnt[i] += nvis;
+  if (a.g_sh) {
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) GM1[a][b] = Gs[a][0] * M[0][b] + Gs[a][1] * M[1][b];
-  float GSig[3][3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) GSig[a][b] = M[0][a] * GM1[0][b] + M[1][a] * GM1[1][b];
-  float GM[2][3];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-      GM[a][b] = 2.f * (GM1[a][0] * Sig[0][b] + GM1[a][1] * Sig[1][b] + GM1[a][2] * Sig[2][b]);
-  // dL/dJ = dL/dM Wᵀ (rotation part of the view matrix)
-  const float GJ00 = GM[0][0] * V[0] + GM[0][1] * V[1] + GM[0][2] * V[2];
-  const float GJ02 = GM[0][0] * V[8] + GM[0][1] * V[9] + GM[0][2] * V[10];
-  const float GJ11 = GM[1][0] * V[4] + GM[1][1] * V[5] + GM[1][2] * V[6];
-  const float GJ12 = GM[1][0] * V[8] + GM[1][1] * V[9] + GM[1][2] * V[10];
-  float gt[3] = {0.f, 0.f, 0.f};
-  gt[2] += GJ00 * (-cam.fx / tz2) + GJ11 * (-cam.fy / tz2);
-  if (!clx) {
-    gt[0] += GJ02 * (-cam.fx / tz2);
-    gt[2] += GJ02 * (2.f * cam.fx * t[0] / tz3);
-  } else {
-    gt[2] += GJ02 * (cam.fx * xt / tz3);
+    for (int j = 0; j < L::K4; ++j) {
+      const size_t off = (size_t)j * n + i;
+      float4 gg = a.g_sh[off];
+      gg.x += gsh[4 * j]; gg.y += gsh[4 * j + 1];
+      if (4 * j + 2 < L::NF) gg.z += gsh[4 * j + 2];
+      if (4 * j + 3 < L::NF) gg.w += gsh[4 * j + 3];
+      a.g_sh[off] = gg;
+    }
   }
-  if (!cly) {
-    gt[1] += GJ12 * (-cam.fy / tz2);
-    gt[2] += GJ12 * (2.f * cam.fy * t[1] / tz3);
-  } else {
-    gt[2] += GJ12 * (cam.fy * yt / tz3);
-  }
-  gt[0] += gu * cam.fx / tz;
-  gt[2] += gu * (-cam.fx * t[0] / tz2);
-  gt[1] += gv * cam.fy / tz;
-  gt[2] += gv * (-cam.fy * t[1] / tz2);
-#pragma unroll
-  for (int a = 0; a < 3; ++a) gp[a] += V[a] * gt[0] + V[4 + a] * gt[1] + V[8 + a] * gt[2];
-  if (g_pos_opa) {
-    float4 gpo = g_pos_opa[i];
+  if (a.g_pos_opa) {
+    float4 gpo = a.g_pos_opa[i];
     gpo.x += gp[0]; gpo.y += gp[1]; gpo.z += gp[2];
     gpo.w += kp ? go : 0.f;
-    g_pos_opa[i] = gpo;
+    a.g_pos_opa[i] = gpo;
   }
+  if (!a.g_scale && !a.g_rot) return;
   // Σ = R diag(s²) Rᵀ : dL/ds_k = 2 s_k (Rᵀ GΣ R)_kk ; dL/dR = 2 GΣ R diag(s²)
   float GR[3][3];
   float gs[3];
@@ -525,17 +577,17 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
   for (int k = 0; k < 3; ++k) {
     float GSr[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) GSr[a] = GSig[a][0] * R[0][k] + GSig[a][1] * R[1][k] + GSig[a][2] * R[2][k];
+    for (int r0 = 0; r0 < 3; ++r0) GSr[r0] = GS[r0][0] * R[0][k] + GS[r0][1] * R[1][k] + GS[r0][2] * R[2][k];
     gs[k] = 2.f * s[k] * (R[0][k] * GSr[0] + R[1][k] * GSr[1] + R[2][k] * GSr[2]);
 #pragma unroll
-    for (int a = 0; a < 3; ++a) GR[a][k] = 2.f * GSr[a] * s[k] * s[k];
+    for (int r0 = 0; r0 < 3; ++r0) GR[r0][k] = 2.f * GSr[r0] * s[k] * s[k];
   }
-  if (g_scale) {
-    float4 g4 = g_scale[i];
+  if (a.g_scale) {
+    float4 g4 = a.g_scale[i];
     if (kp) { g4.x += gs[0]; g4.y += gs[1]; g4.z += gs[2]; }
-    g_scale[i] = g4;
+    a.g_scale[i] = g4;
   }
-  if (g_rot) {
+  if (a.g_rot) {
     float gq[4];
     gq[0] = GR[0][1] * (-2.f * z) + GR[0][2] * (2.f * y) + GR[1][0] * (2.f * z) + GR[1][2] * (-2.f * x) +
             GR[2][0] * (-2.f * y) + GR[2][1] * (2.f * x);
@@ -546,12 +598,12 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
     gq[3] = GR[0][0] * (-4.f * z) + GR[0][1] * (-2.f * w) + GR[0][2] * (2.f * x) + GR[1][0] * (2.f * w) +
             GR[1][1] * (-4.f * z) + GR[1][2] * (2.f * y) + GR[2][0] * (2.f * x) + GR[2][1] * (2.f * y);
     const float dot = w * gq[0] + x * gq[1] + y * gq[2] + z * gq[3];
-    float4 g4 = g_rot[i];
+    float4 g4 = a.g_rot[i];
     g4.x += (gq[0] - w * dot) * qi;
     g4.y += (gq[1] - x * dot) * qi;
     g4.z += (gq[2] - y * dot) * qi;
     g4.w += (gq[3] - z * dot) * qi;
-    g_rot[i] = g4;
+    a.g_rot[i] = g4;
   }
 }
 
@@ -597,15 +649,11 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
 
 size_t render_bwd_workspace(int n) { return sizeof(float4) * 3 * (size_t)(n > 0 ? n : 1); }
 
-cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const float4* pos_opa,
-                              const float4* scale, const float4* rot, const float4* sh,
-                              const uint8_t* keep, const uint2* ranges, const uint32_t* ids,
-                              const float4* xy_depth, const float4* conic_opa, const float4* rgb,
-                              const uint2* box, float3 bg, const float* out_T,
-                              const uint32_t* out_last, const float* dL_dimg, void* ws,
-                              float4* g_pos_opa, float4* g_scale, float4* g_rot, float4* g_sh,
-                              float* gradstat_sum, uint32_t* gradstat_cnt, cudaStream_t s) {
-  float4* g2d = (float4*)ws;
+cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* ranges,
+                                     const uint32_t* ids, const float4* xy_depth,
+                                     const float4* conic_opa, const float4* rgb, const uint2* box,
+                                     float3 bg, const float* out_T, const uint32_t* out_last,
+                                     const float* dL_dimg, float4* g2d, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(g2d, 0, render_bwd_workspace(n), s);
   if (e != cudaSuccess) return e;
   const int ntiles = cam.tiles_x * cam.tiles_y;
@@ -622,20 +670,55 @@ cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const 
   }
 #undef BWD
   launch_counted();
-  const int grid = div_up(n, 256);
-  switch (sh_degree) {
-#define PRE(D)                                                                                    \
-  preprocess_bwd_kernel<D><<<grid, 256, 0, s>>>(cam, n, pos_opa, scale, rot, sh, keep, conic_opa, \
-                                                rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh,   \
-                                                gradstat_sum, gradstat_cnt)
-    case 0: PRE(0); break;
-    case 1: PRE(1); break;
-    case 2: PRE(2); break;
-    default: PRE(3); break;
-#undef PRE
-  }
-  launch_counted();
   return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n, int sh_degree,
+                                    const float4* pos_opa, const float4* scale, const float4* rot,
+                                    const float4* sh, const uint8_t* keep,
+                                    const float4* conic_opa, const float4* rgb, const uint2* box,
+                                    const float4* g2d, float4* g_pos_opa, float4* g_scale,
+                                    float4* g_rot, float4* g_sh, float* gradstat_sum,
+                                    uint32_t* gradstat_cnt, cudaStream_t s) {
+  for (int v0 = 0; v0 < num_views; v0 += PRE_MAXV) {
+    PreArgs a;
+    a.num_views = num_views - v0 < PRE_MAXV ? num_views - v0 : PRE_MAXV;
+    for (int v = 0; v < a.num_views; ++v) a.cam[v] = cams[v0 + v];
+    const size_t off = (size_t)v0 * n;
+    a.n = n;
+    a.pos_opa = pos_opa; a.scale = scale; a.rot = rot; a.sh = sh; a.keep = keep;
+    a.conic_opa = conic_opa + off; a.rgb = rgb + off; a.box = box + off; a.g2d = g2d + 3 * off;
+    a.g_pos_opa = g_pos_opa; a.g_scale = g_scale; a.g_rot = g_rot; a.g_sh = g_sh;
+    a.gradstat_sum = gradstat_sum; a.gradstat_cnt = gradstat_cnt;
+    const int grid = div_up(n, 256);
+    switch (sh_degree) {
+      case 0: preprocess_views_kernel<0><<<grid, 256, 0, s>>>(a); break;
+      case 1: preprocess_views_kernel<1><<<grid, 256, 0, s>>>(a); break;
+      case 2: preprocess_views_kernel<2><<<grid, 256, 0, s>>>(a); break;
+      default: preprocess_views_kernel<3><<<grid, 256, 0, s>>>(a); break;
+    }
+    launch_counted();
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const float4* pos_opa,
+                              const float4* scale, const float4* rot, const float4* sh,
+                              const uint8_t* keep, const uint2* ranges, const uint32_t* ids,
+                              const float4* xy_depth, const float4* conic_opa, const float4* rgb,
+                              const uint2* box, float3 bg, const float* out_T,
+                              const uint32_t* out_last, const float* dL_dimg, void* ws,
+                              float4* g_pos_opa, float4* g_scale, float4* g_rot, float4* g_sh,
+                              float* gradstat_sum, uint32_t* gradstat_cnt, cudaStream_t s) {
+  float4* g2d = (float4*)ws;
+  cudaError_t e = launch_render_bwd_raster(cam, n, ranges, ids, xy_depth, conic_opa, rgb, box, bg,
+                                           out_T, out_last, dL_dimg, g2d, s);
+  if (e != cudaSuccess) return e;
+  return launch_preprocess_views(&cam, 1, n, sh_degree, pos_opa, scale, rot, sh, keep, conic_opa,
+                                 rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh, gradstat_sum,
+                                 gradstat_cnt, s);
 }
 
 }  // namespace dass

@@ -27,7 +27,8 @@ EXPORTS = (
     "dass_status_string", "dass_last_error", "dass_abi_version", "dass_kernel_launches",
     "dass_apply_shift", "dass_apply_shift_bwd", "dass_project", "dass_project_views",
     "dass_bin_sort_workspace", "dass_bin_sort", "dass_render_fwd", "dass_render_bwd_workspace",
-    "dass_render_bwd", "dass_error_map", "dass_render_stats",
+    "dass_render_bwd", "dass_render_bwd_raster", "dass_render_bwd_preprocess_views",
+    "dass_error_map", "dass_render_stats",
 )
 
 
@@ -84,6 +85,9 @@ def lib():
         L.dass_render_bwd_workspace.argtypes = [i32, P]
         L.dass_render_bwd.argtypes = [P, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
                                       P, C.c_size_t, P, P, P, P, P, P, P]
+        L.dass_render_bwd_raster.argtypes = [P, i32, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_render_bwd_preprocess_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P,
+                                                       P, P, P, P, P, P, P]
         L.dass_error_map.argtypes = [P, P, P, C.c_float, P, P, i32, P, P, P]
         L.dass_render_stats.argtypes = [P, P, P, P, P, P, P, P, P, P]
         _lib = L
@@ -204,6 +208,27 @@ def dass_render_bwd(cam, sh_degree, pos_opa, scale, rot, sh, keep_mask, tile_ran
                                  ws.numel() * ws.element_size(), _ptr(g_pos_opa), _ptr(g_scale),
                                  _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum), _ptr(gradstat_cnt),
                                  _stream(stream)), "dass_render_bwd")
+
+
+def dass_render_bwd_raster(cam, n, tile_ranges, sorted_ids, xy_depth, conic_opa, rgb, box, bg,
+                           out_T, out_last, dL_dimg, g2d, stream=None):
+    c = _cam(cam)
+    b = None if bg is None else (C.c_float * 3)(*[float(x) for x in bg])
+    _check(lib().dass_render_bwd_raster(C.byref(c), n, _ptr(tile_ranges), _ptr(sorted_ids),
+                                        _ptr(xy_depth), _ptr(conic_opa), _ptr(rgb), _ptr(box), b,
+                                        _ptr(out_T), _ptr(out_last), _ptr(dL_dimg), _ptr(g2d),
+                                        _stream(stream)), "dass_render_bwd_raster")
+
+
+def dass_render_bwd_preprocess_views(cams, sh_degree, pos_opa, scale, rot, sh, keep_mask,
+                                     conic_opa, rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh,
+                                     gradstat_sum, gradstat_cnt, stream=None):
+    arr = (dass_camera * len(cams))(*[_cam(c) for c in cams])
+    _check(lib().dass_render_bwd_preprocess_views(
+        arr, len(cams), pos_opa.shape[0], sh_degree, _ptr(pos_opa), _ptr(scale), _ptr(rot),
+        _ptr(sh), _ptr(keep_mask), _ptr(conic_opa), _ptr(rgb), _ptr(box), _ptr(g2d),
+        _ptr(g_pos_opa), _ptr(g_scale), _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum),
+        _ptr(gradstat_cnt), _stream(stream)), "dass_render_bwd_preprocess_views")
 
 
 def dass_error_map(cam, rendered, gt, gamma_err, err, dmask, n_base, pos_opa, s_err, stream=None):

@@ -139,3 +139,43 @@ def fwd_bwd_views(cams, scene: DeviceScene, records: ViewRecords, raster: Raster
         rec = records.view(v)
         raster.forward(cam, rec, bg=bg)
         raster.backward(cam, scene, rec, dL_dimgs[v], grads, keep=keep, bg=bg)
+
+
+class MultiViewPass:
+    """fwd+bwd over a fixed list of cameras with S overlapping streams."""
+
+    def __init__(self, cams, n: int, capacity: int, device="cuda", streams: int = 4):
+        torch = _torch()
+        self.cams = list(cams)
+        self.V = len(self.cams)
+        self.n = n
+        W, H = self.cams[0].width, self.cams[0].height
+        for c in self.cams:
+            if (c.width, c.height) != (W, H):
+                raise ValueError("all cameras of a pass must share the image size")
+        self.S = max(1, min(streams, self.V))
+        self.slots = [Raster(W, H, n, capacity, device) for _ in range(self.S)]
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(self.S)]
+        self.g2d = torch.empty(max(self.V, 1), n, 12, dtype=torch.float32, device=device)
+
+    def run(self, scene: DeviceScene, records: ViewRecords, dL_dimgs, grads, keep=None, bg=None):
+        torch = _torch()
+        main = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(main)
+        for v, cam in enumerate(self.cams):
+            k = v % self.S
+            ras, st = self.slots[k], self.streams[k]
+            with torch.cuda.stream(st):
+                rec = records.view(v)
+                xy, co, rgb, box, tiles = rec
+                ras.forward(cam, rec, bg=bg)
+                dass.dass_render_bwd_raster(cam, self.n, ras.ranges, ras.sorted_ids, xy, co, rgb,
+                                            box, bg, ras.T, ras.last, dL_dimgs[v], self.g2d[v])
+        for s in self.streams:
+            main.wait_stream(s)
+        dass.dass_render_bwd_preprocess_views(
+            self.cams, scene.sh_degree, scene.pos_opa, scene.scale, scene.rot, scene.sh, keep,
+            records.conic_opa[:self.V], records.rgb[:self.V], records.box[:self.V],
+            self.g2d[:self.V], grads.pos_opa, grads.scale, grads.rot, grads.sh,
+            grads.gradstat_sum, grads.gradstat_cnt)

