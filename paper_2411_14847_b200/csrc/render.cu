@@ -63,6 +63,10 @@ __device__ __forceinline__ uint32_t support_mask(uint2 b, int tx0, int ty0, floa
   return mx | (my << 16);
 }
 
+struct Staged {  // one entry: three 16-B fields at fixed offsets from one base address
+  float4 a, co, c;
+};
+
 __device__ __forceinline__ void stage(uint32_t id, const float4* __restrict__ xy_depth,
                                       const float4* __restrict__ conic_opa,
                                       const float4* __restrict__ rgb, const uint2* __restrict__ box,
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
     float* __restrict__ out_T, uint32_t* __restrict__ out_last) {
   constexpr int NT = 256 / PPT;
   constexpr int BATCH = 2 * NT;
-  __shared__ float4 s_a[BATCH], s_co[BATCH], s_c[BATCH];
+  __shared__ Staged s_st[BATCH];
   const int tile = blockIdx.x;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
@@ -131,15 +135,16 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
     for (int p = 0; p < PPT; ++p) alive |= !done[p];
     if (__syncthreads_count(alive) == 0) break;
     for (int k = t; k < BATCH; k += NT)
-      if (b0 + k < range.y) stage(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_a[k], s_co[k], s_c[k]);
+      if (b0 + k < range.y) stage(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
     __syncthreads();
     const int cnt = min((uint32_t)BATCH, range.y - b0);
     for (int j = 0; j < cnt; ++j) {
-      const float4 a = s_a[j];
+      const Staged& st = s_st[j];
+      const float4 a = st.a;
       const uint32_t m = __float_as_uint(a.w);
       if ((m & wmask) == 0u) continue;   // warp-uniform: box misses this warp's rows
       if ((m & colbit) == 0u) continue;
-      const float4 co = s_co[j];
+      const float4 co = st.co;
       const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fx);
       const uint32_t mr = m >> (16 + ly0);   // this thread's PPT row bits
       float pw[PPT];
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
         if (alpha < ALPHA_MIN) continue;
         const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
         if (tn < T_MIN) { done[p] = true; continue; }
-        const float4 c = s_c[j];
+        const float4 c = st.c;
         const float w = alpha * T[p];
         C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
         T[p] = tn;
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
   constexpr int NT = 256 / PPT;
   constexpr int NW = NT / 32;
   constexpr int BATCH = 64;  // s_acc = NW·BATCH·36 B; small enough not to limit occupancy
-  __shared__ float4 s_a[BATCH], s_co[BATCH], s_c[BATCH];
+  __shared__ Staged s_st[BATCH];
   __shared__ uint32_t s_id[BATCH];
   __shared__ float s_acc[NW][BATCH][9];
   __shared__ uint32_t s_wlast[NW];
@@ -280,7 +285,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
     for (int k = t; k < cnt; k += NT) {
       const uint32_t id = ids[b0 + k];
       s_id[k] = id;
-      stage(id, xy_depth, conic_opa, rgb, box, tx0, ty0, s_a[k], s_co[k], s_c[k]);
+      stage(id, xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
 #pragma unroll
       for (int w = 0; w < NW; ++w)
 #pragma unroll
@@ -290,7 +295,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
     for (int j = cnt - 1; j >= 0; --j) {
       const uint32_t gidx = b0 + j;
       if (gidx >= wlast) continue;          // warp-uniform: past every pixel's last
-      const float4 a = s_a[j];
+      const Staged& st = s_st[j];
+      const float4 a = st.a;
       const uint32_t m = __float_as_uint(a.w);
       if ((m & wmask) == 0u) continue;      // warp-uniform: box misses this warp's rows
       float v[9];
@@ -298,7 +304,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
       for (int q = 0; q < 9; ++q) v[q] = 0.f;
       bool any = false;
       if (m & colbit) {
-        const float4 co = s_co[j];
+        const float4 co = st.co;
         const float dx = a.x - fx;
         const ColTerms ct = col_terms(co.x, co.y, co.z, dx);
         const uint32_t mr = m >> (16 + ly0);   // this thread's PPT row bits
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
           if (alpha < ALPHA_MIN) continue;
           any = true;
           const float dy = a.y - fy[p];
-          const float4 c = s_c[j];
+          const float4 c = st.c;
           const float inv = rcp_approx(1.f - alpha);
           T[p] *= inv;                        // transmittance before this entry
           const float w = alpha * T[p];
