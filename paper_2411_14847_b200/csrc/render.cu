@@ -41,16 +41,48 @@ namespace {
 // (p_thr carries a 1e-3 margin and the extents a relative + absolute pad), so
 // every pixel it excludes would have been rejected by the exact per-pixel test:
 // decisions, and hence results, are unchanged (A05's box stays the rule).
+// Minimum over the rectangle [a0,a1]×[b0,b1] (offsets from the mean) of the
+// convex quadratic q(d) = A dx² + 2B dx dy + C dy²: 0 if the mean is inside,
+// else the minimum over the four edges (1-D minimisation, clamped).
+__device__ __forceinline__ float rect_qmin(float A, float B, float C, float a0, float a1, float b0,
+                                           float b1) {
+  if (a0 <= 0.f && a1 >= 0.f && b0 <= 0.f && b1 >= 0.f) return 0.f;
+  const float iA = 1.f / A, iC = 1.f / C;
+  float best = INFINITY;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const float dx = e ? a1 : a0;
+    const float dy = fminf(fmaxf(-B * dx * iC, b0), b1);
+    best = fminf(best, A * dx * dx + 2.f * B * dx * dy + C * dy * dy);
+    const float ey = e ? b1 : b0;
+    const float ex = fminf(fmaxf(-B * ey * iA, a0), a1);
+    best = fminf(best, A * ex * ex + 2.f * B * ex * ey + C * ey * ey);
+  }
+  return best;
+}
+
+// Tile-local row/column mask of the pixels an entry can possibly be accepted
+// at: the integer pixel box (A05) intersected with the bounding box of the
+// α ≥ 1/255 support ellipse {dᵀK d ≤ R² = −2·p_thr}, whose half-extents are
+// √(R²·Σ'_xx) and √(R²·Σ'_yy) with Σ' = K⁻¹; then, for every warp region of
+// RPW rows, the region's row bits are cleared when the ellipse misses the
+// region entirely (exact ellipse-rectangle test, A36).  Conservative (p_thr
+// carries a 1e-3 margin, the extents and the ellipse test carry relative and
+// absolute pads), so every pixel it excludes would have been rejected by the
+// exact per-pixel test: decisions, and hence results, are unchanged.
+template <int RPW>
 __device__ __forceinline__ uint32_t support_mask(uint2 b, int tx0, int ty0, float ux, float uy,
                                                  float4 co, float pthr) {
   int x0 = max((int)(b.x & 0xFFFFu) - tx0, 0), x1 = min((int)(b.x >> 16) - tx0, TILE - 1);
   int y0 = max((int)(b.y & 0xFFFFu) - ty0, 0), y1 = min((int)(b.y >> 16) - ty0, TILE - 1);
   const float det = co.x * co.z - co.y * co.y;
   const float r2 = -2.f * pthr;
+  bool tight = false;
   if (det > 0.f && r2 > 0.f) {
     const float hx = sqrtf(r2 * co.z / det) * 1.0001f + 1e-3f;
     const float hy = sqrtf(r2 * co.x / det) * 1.0001f + 1e-3f;
     if (isfinite(hx) && isfinite(hy)) {
+      tight = true;
       x0 = max(x0, (int)ceilf(fmaxf(ux - hx, -1.f)));
       x1 = min(x1, (int)floorf(fminf(ux + hx, 16.f)));
       y0 = max(y0, (int)ceilf(fmaxf(uy - hy, -1.f)));
@@ -59,14 +91,26 @@ __device__ __forceinline__ uint32_t support_mask(uint2 b, int tx0, int ty0, floa
   }
   if (x0 > x1 || y0 > y1) return 0u;
   const uint32_t mx = ((2u << x1) - 1u) & ~((1u << x0) - 1u);
-  const uint32_t my = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
-  return mx | (my << 16);
+  uint32_t my = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
+  if (tight && RPW < 16) {
+    const float lim = r2 * 1.0001f + 1e-3f;
+#pragma unroll
+    for (int w = 0; w < 16 / RPW; ++w) {
+      const int ry0 = max(y0, w * RPW), ry1 = min(y1, w * RPW + RPW - 1);
+      if (ry0 > ry1) continue;
+      const float q = rect_qmin(co.x, co.y, co.z, (float)x0 - ux, (float)x1 - ux, (float)ry0 - uy,
+                                (float)ry1 - uy);
+      if (q > lim) my &= ~(((1u << RPW) - 1u) << (w * RPW));
+    }
+  }
+  return my ? (mx | (my << 16)) : 0u;
 }
 
 struct Staged {  // one entry: three 16-B fields at fixed offsets from one base address
   float4 a, co, c;
 };
 
+template <int RPW>
 __device__ __forceinline__ void stage(uint32_t id, const float4* __restrict__ xy_depth,
                                       const float4* __restrict__ conic_opa,
                                       const float4* __restrict__ rgb, const uint2* __restrict__ box,
@@ -79,7 +123,7 @@ __device__ __forceinline__ void stage(uint32_t id, const float4* __restrict__ xy
   a.x = __fadd_rn(xy.x - (float)tx0, __low2float(lo));
   a.y = __fadd_rn(xy.y - (float)ty0, __high2float(lo));
   a.z = __logf(ALPHA_MIN / co.w) - 1e-3f;
-  a.w = __uint_as_float(support_mask(box[id], tx0, ty0, a.x, a.y, co, a.z));
+  a.w = __uint_as_float(support_mask<RPW>(box[id], tx0, ty0, a.x, a.y, co, a.z));
   c = make_float4(cc.x, cc.y, cc.z, 0.f);
 }
 
@@ -135,9 +179,9 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
     for (int p = 0; p < PPT; ++p) alive |= !done[p];
     if (__syncthreads_count(alive) == 0) break;
     for (int k = t; k < BATCH; k += NT)
-      if (b0 + k < range.y) stage(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
+      if (b0 + k < range.y) stage<16>(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
     __syncthreads();
-    const int cnt = min((uint32_t)BATCH, range.y - b0);
+    const int cnt = __any_sync(0xffffffffu, alive) ? (int)min((uint32_t)BATCH, range.y - b0) : 0;
     for (int j = 0; j < cnt; ++j) {
       const Staged& st = s_st[j];
       const float4 a = st.a;
@@ -285,7 +329,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
     for (int k = t; k < cnt; k += NT) {
       const uint32_t id = ids[b0 + k];
       s_id[k] = id;
-      stage(id, xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
+      stage<2 * PPT>(id, xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
 #pragma unroll
       for (int w = 0; w < NW; ++w)
 #pragma unroll
