@@ -55,9 +55,11 @@ def parse():
     p.add_argument("--capacity", type=int, default=1 << 22, help="pair capacity per view")
     p.add_argument("--streams", type=int, default=4, help="overlapping per-view streams")
     p.add_argument("--no-graph", action="store_true", help="do not capture the step in a CUDA graph")
+    p.add_argument("--lean", action="store_true",
+                   help="only warm-up + timed steps (no stats/diagnostic passes): for ncu launch lists")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--cpu-sample-views", type=int, default=2)
+    p.add_argument("--cpu-sample-views", type=int, default=10)
     return p.parse_args()
 
 
@@ -191,7 +193,7 @@ def run_ours(args):
     step()
     torch.cuda.synchronize()
     cnt = torch.zeros(8, dtype=torch.int64, device=dev)
-    for k, cam in enumerate(my_cams):
+    for k, cam in enumerate([] if args.lean else my_cams):
         rec = records.view(k)
         K = raster.forward(cam, rec, host_mode=True)
         dass.dass_render_stats(cam, raster.ranges, raster.sorted_ids, rec[0], rec[1], rec[3],
@@ -243,7 +245,7 @@ def run_ours(args):
     # ---- per-op breakdown: one extra SEQUENTIAL step, CUDA events on the
     # launching stream around each export (diagnostic; the timed step overlaps views)
     ops = {}
-    if my_cams:
+    if my_cams and not args.lean:
         E = lambda: torch.cuda.Event(enable_timing=True)
         e_proj = [E(), E()]
         e_proj[0].record()
@@ -281,30 +283,73 @@ def run_ours(args):
         ops["render_bwd_raster"] = sum(ev[2].elapsed_time(ev[3]) for ev in per)
         ops["render_bwd_preprocess_views"] = e_pre[0].elapsed_time(e_pre[1])
 
-    # ---- end-to-end through the public API with host buffers
+    # ---- end-to-end through the public API with host buffers: every step
+    # uploads its inputs from pinned host memory and downloads its gradients.
+    # Double-buffered: step k+1's upload (copy stream) overlaps step k's
+    # compute, and step k's download overlaps step k+1; all inside the timed
+    # region (first upload → last download).
     e2e = None
     if not args.no_e2e:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         h_in = [pin(scene.pos_opa), pin(scene.scale), pin(scene.rot), pin(scene.sh), pin(mu),
                 pin(sigma), dLs.cpu().pin_memory()]
         d_in = [base.pos_opa, base.scale, base.rot, base.sh, mu_d, sigma_d, dLs]
-        h_out = torch.empty(flat.numel(), dtype=torch.float32).pin_memory()
+        stage_in = [[torch.empty_like(d) for d in d_in] for _ in range(2)]
+        stage_out = [torch.empty_like(flat) for _ in range(2)]
+        h_out = [torch.empty(flat.numel(), dtype=torch.float32).pin_memory() for _ in range(2)]
         h2d = sum(x.numel() * x.element_size() for x in h_in)
-        d2h = h_out.numel() * 4
+        d2h = flat.numel() * 4
+        comp = torch.cuda.current_stream()
+        copy_in = torch.cuda.Stream(device=dev)
+        copy_out = torch.cuda.Stream(device=dev)
+        ev_in = [torch.cuda.Event() for _ in range(2)]      # upload k done
+        ev_free = [torch.cuda.Event() for _ in range(2)]    # staging k consumed
+        ev_res = [torch.cuda.Event() for _ in range(2)]     # result k staged
+        ev_out = [torch.cuda.Event() for _ in range(2)]     # download k done
 
-        def e2e_step():
-            for h, d in zip(h_in, d_in):
-                d.copy_(h, non_blocking=True)
+        def upload(k):
+            b = k % 2
+            with torch.cuda.stream(copy_in):
+                copy_in.wait_event(ev_free[b])
+                for h, d in zip(h_in, stage_in[b]):
+                    d.copy_(h, non_blocking=True)
+                ev_in[b].record(copy_in)
+
+        def compute(k):
+            b = k % 2
+            comp.wait_event(ev_in[b])
+            for src, dst in zip(stage_in[b], d_in):
+                dst.copy_(src, non_blocking=True)
+            ev_free[b].record(comp)
             run_step(graph)
-            h_out.copy_(flat, non_blocking=True)
+            comp.wait_event(ev_out[b])           # previous download from this slot done
+            stage_out[b].copy_(flat, non_blocking=True)
+            ev_res[b].record(comp)
 
-        for _ in range(2):
-            e2e_step()
+        def download(k):
+            b = k % 2
+            with torch.cuda.stream(copy_out):
+                copy_out.wait_event(ev_res[b])
+                h_out[b].copy_(stage_out[b], non_blocking=True)
+                ev_out[b].record(copy_out)
+
+        def run_e2e(nsteps):
+            for b in range(2):
+                ev_free[b].record(comp)
+                ev_out[b].record(comp)
+            upload(0)
+            for k in range(nsteps):
+                if k + 1 < nsteps:
+                    upload(k + 1)
+                compute(k)
+                download(k)
+            comp.wait_stream(copy_out)
+
+        run_e2e(2)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(args.steps):
-            e2e_step()
+        run_e2e(args.steps)
         e1.record()
         barrier()
         ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
@@ -312,7 +357,8 @@ def run_ours(args):
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e2e = {"value": len(cams) / (float(ems.item()) / 1e3), "unit": "views/s",
                "ms_per_step": float(ems.item()), "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h)}
+               "d2h_bytes_per_step": int(d2h),
+               "pipelining": "double-buffered: upload k+1 and download k-1 overlap compute k"}
 
     # ---- gather stats to rank 0
     if world > 1:
@@ -355,7 +401,7 @@ def run_ours(args):
                          "units_per_step": {"accepted": sum(stats["accepted"]), "P_bwd": sum(stats["P_bwd"])},
                          "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED}},
             "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
-            "scene_stats": {"K_per_view_mean": float(np.mean(allst["K"])),
+            "scene_stats": None if args.lean else {"K_per_view_mean": float(np.mean(allst["K"])),
                             "P_fwd_per_px": float(np.sum(allst["P_fwd"]) / (len(allst["K"]) * W * H)),
                             "P_bwd_per_px": float(np.sum(allst["P_bwd"]) / (len(allst["K"]) * W * H)),
                             "accepted_per_px": float(np.sum(allst["accepted"]) / (len(allst["K"]) * W * H)),
