@@ -308,6 +308,28 @@ int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views,
                                      uint32_t* gradstat_cnt, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Selective inheritance, Eq. 1 with the straight-through estimator
+ * — SURVEY §8(f) f3.
+ *
+ * dass_inherit_mask: keep[i] = Quant(sigmoid(m_i)) with Quant(x) = 1[x ≥ 0.5]
+ *   (A26), i.e. keep = 1[m ≥ 0] (sigmoid(0) = 0.5 keeps).  Feed `keep`
+ *   as keep_mask to dass_project / dass_render_bwd*: o_r = keep·o and
+ *   s_r = keep·s, and a Quant = 0 Gaussian is culled (A10).  m: float[n].
+ *
+ * dass_inherit_mask_bwd: the STE gradient of m_op = detach(Quant(σ(m)) − σ(m))
+ *   + σ(m) plus the mask loss λ_inher·Σ σ(m) of Eq. 2:
+ *     g_m[i] += (o_i·∂L/∂o_r,i + Σ_k s_i,k·∂L/∂s_r,i,k + λ_inher)·σ'(m_i),
+ *   σ'(m) = σ(m)(1 − σ(m)).  ∂L/∂o_r and ∂L/∂s_r are g_pos_opa.w and g_scale
+ *   from dass_render_bwd* (gradients w.r.t. the effective o, s; zero for
+ *   culled Gaussians).  pos_opa/scale: the un-masked o, s.
+ * ------------------------------------------------------------------------- */
+int dass_inherit_mask(int32_t n, const float* m, uint8_t* keep, void* stream);
+int dass_inherit_mask_bwd(int32_t n, const float* m, const float* pos_opa,
+                          const float* scale, const float* g_pos_opa,
+                          const float* g_scale, float lambda_inher, float* g_m,
+                          void* stream);
+
+/* ---------------------------------------------------------------------------
  * dass_error_map — error map, binarisation and Alg. 1 (§3.4 P:164-165, P:174;
  * Alg. 1 P:403-415 with the garble fixed, A20-A22).
  *   E(X,Y) = (1/3)·Σ_ch |rendered − gt|  → err (float [H][W], nullable)

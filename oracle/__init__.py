@@ -199,3 +199,22 @@ def error_map(cam, rendered, gt, gamma, pos_opa, n_base=None, s_err=None):
                            _p(_f32(pos_opa)), _p(o["err"]), _p(o["D"]), _p(o["s_err"]),
                            _p(o["xy"]), _p(o["tie_g"]), _p(o["tie_px"]))
     return o
+
+
+def inherit(m):
+    """f3: keep = Quant(sigmoid(m)) (Eq. 1)."""
+    m = _f32(m)
+    keep = np.zeros(m.shape[0], np.uint8)
+    lib().oracle_inherit(m.shape[0], _p(m), _p(keep))
+    return keep
+
+
+def inherit_bwd(m, pos_opa, scale, g_pos_opa, g_scale, lambda_inher=0.0):
+    """f3: STE gradient of m + the mask loss λ_inher·Σσ(m) (Eq. 2)."""
+    m = _f32(m)
+    g = np.zeros(m.shape[0])
+    lib().oracle_inherit_bwd(m.shape[0], _p(m), _p(_f32(pos_opa)), _p(_f32(scale)),
+                             _p(np.ascontiguousarray(g_pos_opa, np.float64)),
+                             _p(np.ascontiguousarray(g_scale, np.float64)),
+                             C.c_double(lambda_inher), _p(g))
+    return g

@@ -1121,6 +1121,33 @@ int oracle_render_bwd(const OCam* cam, int n, int deg, const float* pos_opa, con
   return 0;
 }
 
+// ------------------------------------------------------------ f3 / Eq. 1 ---
+// Selective inheritance: o_r = Quant(sigmoid(m))∘o, s_r = Quant(sigmoid(m))∘s
+// with Quant(x) = 1[x ≥ 0.5] (A26).
+int oracle_inherit(int n, const float* m, uint8_t* keep) {
+  for (int i = 0; i < n; ++i) {
+    const double sig = 1.0 / (1.0 + std::exp(-(double)m[i]));
+    keep[i] = sig >= 0.5 ? 1 : 0;
+  }
+  return 0;
+}
+
+// STE: m_op = detach(Quant(σ(m)) − σ(m)) + σ(m), so ∂m_op/∂m = σ'(m);
+// with o_r = m_op·o and s_r = m_op·s, ∂L/∂m_op = o·∂L/∂o_r + Σ_k s_k·∂L/∂s_r,k.
+// Mask loss λ_inher·Σσ(m) of Eq. 2 adds λ_inher·σ'(m).  g_m is written (=).
+int oracle_inherit_bwd(int n, const float* m, const float* pos_opa, const float* scale,
+                       const double* g_pos_opa, const double* g_scale, double lambda_inher,
+                       double* g_m) {
+  for (int i = 0; i < n; ++i) {
+    const double sig = 1.0 / (1.0 + std::exp(-(double)m[i]));
+    const double dsig = sig * (1.0 - sig);
+    double dmop = (double)pos_opa[4 * i + 3] * g_pos_opa[4 * i + 3];
+    for (int k = 0; k < 3; ++k) dmop += (double)scale[4 * i + k] * g_scale[4 * i + k];
+    g_m[i] = (dmop + lambda_inher) * dsig;
+  }
+  return 0;
+}
+
 // ------------------------------------------------------------------ O7 -----
 // §3.4: E = channel-mean |rendered − gt|, D = E > γ (strict,
 // S:626).  Alg. 1 (garble fixed per A20): s_err |= D[y_n][x_n] for

@@ -311,6 +311,27 @@ int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views,
                      "dass_render_bwd_preprocess_views");
 }
 
+int dass_inherit_mask(int32_t n, const float* m, uint8_t* keep, void* stream) {
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (n == 0) return DASS_OK;
+  if (!m || !keep) return fail(DASS_ERR_INVALID_ARG, "dass_inherit_mask: null required pointer%s");
+  return cuda_status(launch_inherit_mask(n, m, keep, (cudaStream_t)stream), "dass_inherit_mask");
+}
+
+int dass_inherit_mask_bwd(int32_t n, const float* m, const float* pos_opa, const float* scale,
+                          const float* g_pos_opa, const float* g_scale, float lambda_inher,
+                          float* g_m, void* stream) {
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (n == 0) return DASS_OK;
+  if (!m || !pos_opa || !scale || !g_pos_opa || !g_scale || !g_m)
+    return fail(DASS_ERR_INVALID_ARG, "dass_inherit_mask_bwd: null required pointer%s");
+  if (!std::isfinite(lambda_inher)) return fail(DASS_ERR_INVALID_ARG, "lambda_inher must be finite%s");
+  return cuda_status(launch_inherit_mask_bwd(n, m, (const float4*)pos_opa, (const float4*)scale,
+                                             (const float4*)g_pos_opa, (const float4*)g_scale,
+                                             lambda_inher, g_m, (cudaStream_t)stream),
+                     "dass_inherit_mask_bwd");
+}
+
 int dass_error_map(const dass_camera* cam, const float* rendered, const float* gt, float gamma_err,
                    float* err, uint32_t* dmask, int32_t n_base, const float* pos_opa,
                    uint8_t* s_err, void* stream) {

@@ -127,6 +127,11 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
                                     const float4* g2d, float4* g_pos_opa, float4* g_scale,
                                     float4* g_rot, float4* g_sh, float* gradstat_sum,
                                     uint32_t* gradstat_cnt, cudaStream_t s);
+cudaError_t launch_inherit_mask(int n, const float* m, uint8_t* keep, cudaStream_t s);
+cudaError_t launch_inherit_mask_bwd(int n, const float* m, const float4* pos_opa,
+                                    const float4* scale, const float4* g_pos_opa,
+                                    const float4* g_scale, float lambda_inher, float* g_m,
+                                    cudaStream_t s);
 cudaError_t launch_error_map(const CamParams& cam, const float* rendered, const float* gt,
                              float gamma, float* err, uint32_t* dmask, int n_base,
                              const float4* pos_opa, uint8_t* s_err, cudaStream_t s);

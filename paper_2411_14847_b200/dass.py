@@ -28,7 +28,7 @@ EXPORTS = (
     "dass_apply_shift", "dass_apply_shift_bwd", "dass_project", "dass_project_views",
     "dass_bin_sort_workspace", "dass_bin_sort", "dass_render_fwd", "dass_render_bwd_workspace",
     "dass_render_bwd", "dass_render_bwd_raster", "dass_render_bwd_preprocess_views",
-    "dass_error_map", "dass_render_stats",
+    "dass_inherit_mask", "dass_inherit_mask_bwd", "dass_error_map", "dass_render_stats",
 )
 
 
@@ -88,6 +88,8 @@ def lib():
         L.dass_render_bwd_raster.argtypes = [P, i32, P, P, P, P, P, P, P, P, P, P, P, P]
         L.dass_render_bwd_preprocess_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P,
                                                        P, P, P, P, P, P, P]
+        L.dass_inherit_mask.argtypes = [i32, P, P, P]
+        L.dass_inherit_mask_bwd.argtypes = [i32, P, P, P, P, P, C.c_float, P, P]
         L.dass_error_map.argtypes = [P, P, P, C.c_float, P, P, i32, P, P, P]
         L.dass_render_stats.argtypes = [P, P, P, P, P, P, P, P, P, P]
         _lib = L
@@ -229,6 +231,17 @@ def dass_render_bwd_preprocess_views(cams, sh_degree, pos_opa, scale, rot, sh, k
         _ptr(sh), _ptr(keep_mask), _ptr(conic_opa), _ptr(rgb), _ptr(box), _ptr(g2d),
         _ptr(g_pos_opa), _ptr(g_scale), _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum),
         _ptr(gradstat_cnt), _stream(stream)), "dass_render_bwd_preprocess_views")
+
+
+def dass_inherit_mask(m, keep, stream=None):
+    _check(lib().dass_inherit_mask(m.shape[0], _ptr(m), _ptr(keep), _stream(stream)),
+           "dass_inherit_mask")
+
+
+def dass_inherit_mask_bwd(m, pos_opa, scale, g_pos_opa, g_scale, lambda_inher, g_m, stream=None):
+    _check(lib().dass_inherit_mask_bwd(m.shape[0], _ptr(m), _ptr(pos_opa), _ptr(scale),
+                                       _ptr(g_pos_opa), _ptr(g_scale), float(lambda_inher),
+                                       _ptr(g_m), _stream(stream)), "dass_inherit_mask_bwd")
 
 
 def dass_error_map(cam, rendered, gt, gamma_err, err, dmask, n_base, pos_opa, s_err, stream=None):

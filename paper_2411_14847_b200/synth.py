@@ -306,6 +306,14 @@ def c3(n: int = 300_000, num_views: int = 20):
     return cams, n3dv_scene(n=n, seed=3, degree=3, fx=cams[0].fx)
 
 
+def c4(n: int = 200_000, num_views: int = 13):
+    """Meet-Room-shaped timestep (BASELINE configs[3]): 13 cameras on a 100° arc
+    around (0,0,3), 1280×720; the N3DV-shaped generator places the background
+    4-9 units and the clusters 1.5-3.5 units in front of the central camera."""
+    cams = meetroom_rig(seed=4, num_views=num_views)
+    return cams, n3dv_scene(n=n, seed=4, degree=3, fx=cams[0].fx)
+
+
 def c5(n: int = 1_000_000):
     cams = n3dv_rig(seed=3)
     return cams, n3dv_scene(n=n, seed=5, degree=3, fx=cams[0].fx,

