@@ -262,10 +262,11 @@ def run_ours(args):
                                raster.sorted_ids, raster.ranges, raster.num_pairs)
             ev[1].record()
             dass.dass_render_fwd(cam, raster.ranges, raster.sorted_ids, xy, co, rgb, box, None,
-                                 raster.img, raster.T, raster.last)
+                                 raster.img, raster.T, raster.last, raster.accept, raster.capacity)
             ev[2].record()
             dass.dass_render_bwd_raster(cam, n, raster.ranges, raster.sorted_ids, xy, co, rgb, box,
-                                        None, raster.T, raster.last, dLs[k], mvp.g2d[k])
+                                        None, raster.T, raster.last, dLs[k], mvp.g2d[k],
+                                        raster.accept, raster.capacity)
             ev[3].record()
             per.append(ev)
         e_pre = [E(), E()]

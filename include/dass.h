@@ -241,12 +241,23 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth,
  * out_img[ch] = C + T·bg[ch] (bg: host float[3], nullable = black);
  * out_T = final T; out_last = one past the sorted-list index of the last
  * accepted entry (the range start if none).  Both are needed by the backward.
+ *
+ * accept (nullable): acceptance-list workspace of dass_render_accept_workspace
+ *   (num_tiles, pair_capacity) bytes.  When given, the forward also records,
+ *   for every (tile, 16×8 half-tile) and every list entry accepted by at least
+ *   one of its pixels, the entry index and which of its pixels accepted it;
+ *   dass_render_bwd* then walk only those (pair_capacity must be the one given
+ *   to dass_bin_sort).  Opaque layout; valid until the next dass_render_fwd on
+ *   the same buffer.
  * ------------------------------------------------------------------------- */
+int dass_render_accept_workspace(int32_t num_tiles, int64_t pair_capacity,
+                                 size_t* bytes);
 int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges,
                     const uint32_t* sorted_ids, const float* xy_depth,
                     const float* conic_opa, const float* rgb,
                     const uint32_t* box, const float* bg, float* out_img,
-                    float* out_T, uint32_t* out_last, void* stream);
+                    float* out_T, uint32_t* out_last, void* accept,
+                    int64_t pair_capacity, void* stream);
 
 /* ---------------------------------------------------------------------------
  * dass_render_bwd — reverse-mode gradient of dass_project + dass_render_fwd
@@ -261,6 +272,8 @@ int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges,
  *   every Gaussian visible in this view (A23).  Both nullable.
  * The caller must pass the SAME records and fwd outputs; the ABI
  * cannot check this.  dL_dimg: float [3][H][W].  ws: dass_render_bwd_workspace.
+ * accept/pair_capacity: the forward's acceptance lists (nullable: the pass
+ * then re-derives the accepted set from out_last; same result).
  * ------------------------------------------------------------------------- */
 int dass_render_bwd_workspace(int32_t n, size_t* bytes);
 int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree,
@@ -270,7 +283,8 @@ int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree,
                     const float* xy_depth, const float* conic_opa,
                     const float* rgb, const uint32_t* box, const float* bg,
                     const float* out_T, const uint32_t* out_last,
-                    const float* dL_dimg, void* ws, size_t ws_bytes,
+                    const float* dL_dimg, const void* accept,
+                    int64_t pair_capacity, void* ws, size_t ws_bytes,
                     float* g_pos_opa, float* g_scale, float* g_rot,
                     float* g_sh, float* gradstat_sum, uint32_t* gradstat_cnt,
                     void* stream);
@@ -297,7 +311,8 @@ int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* ti
                            const uint32_t* sorted_ids, const float* xy_depth,
                            const float* conic_opa, const float* rgb, const uint32_t* box,
                            const float* bg, const float* out_T, const uint32_t* out_last,
-                           const float* dL_dimg, float* g2d, void* stream);
+                           const float* dL_dimg, const void* accept, int64_t pair_capacity,
+                           float* g2d, void* stream);
 int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views, int32_t n,
                                      int32_t sh_degree, const float* pos_opa,
                                      const float* scale, const float* rot, const float* sh,

@@ -199,22 +199,31 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, cons
   return DASS_OK;
 }
 
+int dass_render_accept_workspace(int32_t num_tiles, int64_t pair_capacity, size_t* bytes) {
+  if (!bytes || num_tiles < 1 || pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30))
+    return fail(DASS_ERR_INVALID_ARG, "need num_tiles >= 1 and 0 <= pair_capacity < 2^30%s");
+  *bytes = render_accept_workspace(num_tiles, pair_capacity);
+  return DASS_OK;
+}
+
 int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges, const uint32_t* sorted_ids,
                     const float* xy_depth, const float* conic_opa, const float* rgb,
                     const uint32_t* box, const float* bg, float* out_img, float* out_T,
-                    uint32_t* out_last, void* stream) {
+                    uint32_t* out_last, void* accept, int64_t pair_capacity, void* stream) {
   int st = check_camera(cam);
   if (st) return st;
   if (!tile_ranges || !out_img || !out_T || !out_last)
     return fail(DASS_ERR_INVALID_ARG, "dass_render_fwd: null required pointer%s");
   if (!sorted_ids || !xy_depth || !conic_opa || !rgb || !box)
     return fail(DASS_ERR_INVALID_ARG, "dass_render_fwd: null record pointer%s");
+  if (accept && (pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30) || !aligned16(accept)))
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_fwd: accept needs a 16-byte aligned buffer and 0 <= pair_capacity < 2^30%s");
   CamParams cp = to_params(cam);
   float3 b = bg ? make_float3(bg[0], bg[1], bg[2]) : make_float3(0.f, 0.f, 0.f);
   return cuda_status(launch_render_fwd(cp, (const uint2*)tile_ranges, sorted_ids,
                                        (const float4*)xy_depth, (const float4*)conic_opa,
                                        (const float4*)rgb, (const uint2*)box, b, out_img, out_T,
-                                       out_last, (cudaStream_t)stream),
+                                       out_last, accept, pair_capacity, (cudaStream_t)stream),
                      "dass_render_fwd");
 }
 
@@ -229,7 +238,8 @@ int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree, const 
                     const uint8_t* keep_mask, const uint32_t* tile_ranges,
                     const uint32_t* sorted_ids, const float* xy_depth, const float* conic_opa,
                     const float* rgb, const uint32_t* box, const float* bg, const float* out_T,
-                    const uint32_t* out_last, const float* dL_dimg, void* ws, size_t ws_bytes,
+                    const uint32_t* out_last, const float* dL_dimg, const void* accept,
+                    int64_t pair_capacity, void* ws, size_t ws_bytes,
                     float* g_pos_opa, float* g_scale, float* g_rot, float* g_sh,
                     float* gradstat_sum, uint32_t* gradstat_cnt, void* stream) {
   int st = check_camera(cam);
@@ -250,7 +260,7 @@ int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree, const 
                         (const float4*)rot, (const float4*)sh, keep_mask,
                         (const uint2*)tile_ranges, sorted_ids, (const float4*)xy_depth,
                         (const float4*)conic_opa, (const float4*)rgb, (const uint2*)box, b, out_T,
-                        out_last, dL_dimg, ws, (float4*)g_pos_opa, (float4*)g_scale,
+                        out_last, dL_dimg, accept, pair_capacity, ws, (float4*)g_pos_opa, (float4*)g_scale,
                         (float4*)g_rot, (float4*)g_sh, gradstat_sum, gradstat_cnt,
                         (cudaStream_t)stream),
       "dass_render_bwd");
@@ -260,7 +270,8 @@ int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* ti
                            const uint32_t* sorted_ids, const float* xy_depth,
                            const float* conic_opa, const float* rgb, const uint32_t* box,
                            const float* bg, const float* out_T, const uint32_t* out_last,
-                           const float* dL_dimg, float* g2d, void* stream) {
+                           const float* dL_dimg, const void* accept, int64_t pair_capacity,
+                           float* g2d, void* stream) {
   int st = check_camera(cam);
   if (st) return st;
   if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
@@ -274,8 +285,8 @@ int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* ti
   return cuda_status(launch_render_bwd_raster(cp, n, (const uint2*)tile_ranges, sorted_ids,
                                               (const float4*)xy_depth, (const float4*)conic_opa,
                                               (const float4*)rgb, (const uint2*)box, b, out_T,
-                                              out_last, dL_dimg, (float4*)g2d,
-                                              (cudaStream_t)stream),
+                                              out_last, dL_dimg, accept, pair_capacity,
+                                              (float4*)g2d, (cudaStream_t)stream),
                      "dass_render_bwd_raster");
 }
 

@@ -102,24 +102,27 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
                            const uint32_t* tiles, void* ws, int64_t capacity,
                            uint64_t* sorted_keys, uint32_t* sorted_ids, uint2* ranges,
                            uint32_t* num_pairs_dev, cudaStream_t s);
+size_t render_accept_workspace(int ntiles, int64_t capacity);
 cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
                               const float4* xy_depth, const float4* conic_opa, const float4* rgb,
                               const uint2* box, float3 bg, float* out_img, float* out_T,
-                              uint32_t* out_last, cudaStream_t s);
+                              uint32_t* out_last, void* accept, int64_t capacity, cudaStream_t s);
 size_t render_bwd_workspace(int n);
 cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const float4* pos_opa,
                               const float4* scale, const float4* rot, const float4* sh,
                               const uint8_t* keep, const uint2* ranges, const uint32_t* ids,
                               const float4* xy_depth, const float4* conic_opa, const float4* rgb,
                               const uint2* box, float3 bg, const float* out_T,
-                              const uint32_t* out_last, const float* dL_dimg, void* ws,
-                              float4* g_pos_opa, float4* g_scale, float4* g_rot, float4* g_sh,
-                              float* gradstat_sum, uint32_t* gradstat_cnt, cudaStream_t s);
+                              const uint32_t* out_last, const float* dL_dimg, const void* accept,
+                              int64_t capacity, void* ws, float4* g_pos_opa, float4* g_scale,
+                              float4* g_rot, float4* g_sh, float* gradstat_sum,
+                              uint32_t* gradstat_cnt, cudaStream_t s);
 cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* ranges,
                                      const uint32_t* ids, const float4* xy_depth,
                                      const float4* conic_opa, const float4* rgb, const uint2* box,
                                      float3 bg, const float* out_T, const uint32_t* out_last,
-                                     const float* dL_dimg, float4* g2d, cudaStream_t s);
+                                     const float* dL_dimg, const void* accept, int64_t capacity,
+                                     float4* g2d, cudaStream_t s);
 cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n, int sh_degree,
                                     const float4* pos_opa, const float4* scale, const float4* rot,
                                     const float4* sh, const uint8_t* keep,

@@ -139,15 +139,29 @@ __device__ __forceinline__ uint32_t warp_row_mask(int warp) {
   return (((1u << (2 * PPT)) - 1u) << (16 + warp * 2 * PPT));
 }
 
+// Per-(tile, warp) acceptance lists written by the forward (PPT = 4, two
+// warps of 16×8 pixels per tile): for every tile-list entry accepted by at
+// least one pixel of the warp, its absolute list index and 32 bytes — byte
+// `lane` holds the 4-bit set of that lane's pixels that accepted it (one
+// coalesced 32-B store per entry, no ballots).  Warp w of tile t stores its
+// list at [2·range.x + w·len, …), len = range length; cnt[2t + w].
+struct AcceptLists {
+  uint32_t* cnt;
+  uint32_t* idx;
+  uint8_t* bytes;
+};
+
 // ------------------------------------------------------------- forward ----
-template <int PPT>
+template <int PPT, bool LISTS>
 __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
     const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
     const uint2* __restrict__ box, float3 bg, float* __restrict__ out_img,
-    float* __restrict__ out_T, uint32_t* __restrict__ out_last) {
+    float* __restrict__ out_T, uint32_t* __restrict__ out_last, AcceptLists acc) {
+  static_assert(!LISTS || PPT == 4, "acceptance lists are defined for the PPT = 4 mapping");
   constexpr int NT = 256 / PPT;
+  constexpr int NW = NT / 32;
   constexpr int BATCH = 2 * NT;
   __shared__ Staged s_st[BATCH];
   const int tile = blockIdx.x;
@@ -173,6 +187,10 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
   float fy[PPT];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) fy[p] = (float)(ly0 + p);
+  // acceptance list of this warp: entries (absolute list index, 4 ballot words)
+  const uint32_t warp = t >> 5, lane = t & 31u;
+  const size_t lbase = (size_t)NW * range.x + (size_t)warp * (range.y - range.x);
+  uint32_t nlist = 0;
   for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
     bool alive = false;
 #pragma unroll
@@ -187,32 +205,44 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
       const float4 a = st.a;
       const uint32_t m = __float_as_uint(a.w);
       if ((m & wmask) == 0u) continue;   // warp-uniform: box misses this warp's rows
-      if ((m & colbit) == 0u) continue;
-      const float4 co = st.co;
-      const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fx);
-      const uint32_t mr = m >> (16 + ly0);   // this thread's PPT row bits
-      float pw[PPT];
-      bool ok[PPT];
+      uint32_t accb = 0;                 // this lane's accepted pixels of the entry
+      if (m & colbit) {
+        const float4 co = st.co;
+        const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fx);
+        const uint32_t mr = m >> (16 + ly0);   // this thread's PPT row bits
+        float pw[PPT];
+        bool ok[PPT];
 #pragma unroll
-      for (int p = 0; p < PPT; ++p) {   // independent per pixel: no branches, full ILP
-        pw[p] = splat_power(ct, a.y - fy[p]);
-        ok[p] = !done[p] && ((mr >> p) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
+        for (int p = 0; p < PPT; ++p) {   // independent per pixel: no branches, full ILP
+          pw[p] = splat_power(ct, a.y - fy[p]);
+          ok[p] = !done[p] && ((mr >> p) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
+        }
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          if (!ok[p]) continue;
+          const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
+          if (alpha < ALPHA_MIN) continue;
+          const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
+          if (tn < T_MIN) { done[p] = true; continue; }
+          const float4 c = st.c;
+          const float w = alpha * T[p];
+          C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
+          T[p] = tn;
+          last[p] = b0 + j + 1;
+          accb |= 1u << p;
+        }
       }
-#pragma unroll
-      for (int p = 0; p < PPT; ++p) {
-        if (!ok[p]) continue;
-        const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
-        if (alpha < ALPHA_MIN) continue;
-        const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
-        if (tn < T_MIN) { done[p] = true; continue; }
-        const float4 c = st.c;
-        const float w = alpha * T[p];
-        C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
-        T[p] = tn;
-        last[p] = b0 + j + 1;
+      if (LISTS) {
+        if (__any_sync(0xffffffffu, accb != 0u)) {
+          const size_t e = lbase + nlist;
+          acc.bytes[e * 32 + lane] = (uint8_t)accb;
+          if (lane == 0) acc.idx[e] = b0 + j;
+          ++nlist;
+        }
       }
     }
   }
+  if (LISTS && lane == 0) acc.cnt[(size_t)NW * tile + warp] = nlist;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int Y = ty0 + ly0 + p;
@@ -410,6 +440,130 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
   }
 }
 
+// --------------------------------- backward: raster part from the lists ----
+// Each warp walks ITS acceptance list (written by the forward) backwards in
+// chunks of 32 entries: the chunk's records are gathered into per-warp shared
+// memory (one entry per lane), then for every entry only the accepted pixels
+// are evaluated (bit-identical α: same canonical power, same staging
+// arithmetic as the forward), the 9 per-pixel terms are reduce-scattered
+// (every list entry has ≥ 1 accepted pixel, so every butterfly is needed) and
+// the chunk is flushed with vector reductions.  Warps are independent: no
+// block barrier, no iteration over entries the warp never accepted.
+template <int PPT>
+__global__ void __launch_bounds__(256 / PPT, 1024 / (256 / PPT)) render_bwd_list_kernel(
+    const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
+    const float4* __restrict__ conic_opa, const float4* __restrict__ rgb, float3 bg,
+    const float* __restrict__ out_T, const float* __restrict__ dL_dimg, AcceptLists acc,
+    float4* __restrict__ g2d) {
+  static_assert(PPT == 4, "acceptance lists are defined for the PPT = 4 mapping");
+  constexpr int NT = 256 / PPT;
+  constexpr int NW = NT / 32;
+  __shared__ float4 s_a[NW][32];    // (u_rel, v_rel, −, −)
+  __shared__ float4 s_co[NW][32];   // (A, B, C, o)
+  __shared__ float4 s_c[NW][32];    // (r, g, b, −)
+  __shared__ uint4 s_bytes[NW][32][2];   // 32 acceptance bytes per staged entry
+  __shared__ uint32_t s_id[NW][32];
+  __shared__ float s_acc[NW][32][9];
+  const int tile = blockIdx.x;
+  const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
+  const int tx0 = txi * TILE, ty0 = tyi * TILE;
+  const int t = threadIdx.x;
+  const int warp = t >> 5;
+  const uint32_t lane = t & 31u;
+  const int lx = t & 15, ly0 = (t >> 4) * PPT;
+  const int X = tx0 + lx;
+  const uint2 range = ranges[tile];
+  const size_t lbase = (size_t)NW * range.x + (size_t)warp * (range.y - range.x);
+  const uint32_t n = acc.cnt[(size_t)NW * tile + warp];
+  if (n == 0) return;  // warp-uniform; nothing this warp accepted (no block barrier below)
+  LaneRS rs;
+  rs.init();
+  float T[PPT], gR[PPT], g[PPT][3];
+  const size_t np = (size_t)cam.W * cam.H;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int Y = ty0 + ly0 + p;
+    if (X < cam.W && Y < cam.H) {
+      const size_t pix = (size_t)Y * cam.W + X;
+      T[p] = out_T[pix];
+      g[p][0] = dL_dimg[pix]; g[p][1] = dL_dimg[np + pix]; g[p][2] = dL_dimg[2 * np + pix];
+    } else {
+      T[p] = 1.f;
+      g[p][0] = g[p][1] = g[p][2] = 0.f;
+    }
+    gR[p] = T[p] * (g[p][0] * bg.x + g[p][1] * bg.y + g[p][2] * bg.z);
+  }
+  const float fx = (float)lx;
+  float fy[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) fy[p] = (float)(ly0 + p);
+  for (int ptr = (int)n; ptr > 0;) {
+    const int k0 = ptr > 32 ? ptr - 32 : 0;
+    const int cnt = ptr - k0;
+    if ((int)lane < cnt) {
+      const size_t e = lbase + k0 + lane;
+      const uint32_t id = ids[acc.idx[e]];
+      const uint4* src = reinterpret_cast<const uint4*>(acc.bytes + e * 32);
+      s_bytes[warp][lane][0] = src[0];
+      s_bytes[warp][lane][1] = src[1];
+      s_id[warp][lane] = id;
+      // the forward's staging arithmetic for (u_rel, v_rel): identical bits
+      const float4 xy = xy_depth[id];
+      const uint32_t lo_bits = __float_as_uint(xy.w);
+      const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
+      s_a[warp][lane] = make_float4(__fadd_rn(xy.x - (float)tx0, __low2float(lo)),
+                                    __fadd_rn(xy.y - (float)ty0, __high2float(lo)), 0.f, 0.f);
+      s_co[warp][lane] = conic_opa[id];
+      s_c[warp][lane] = rgb[id];
+    }
+    __syncwarp();
+    for (int k = cnt - 1; k >= 0; --k) {
+      const uint32_t bits = reinterpret_cast<const uint8_t*>(&s_bytes[warp][k][0])[lane];
+      float v[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) v[q] = 0.f;
+      if (bits) {
+        const float4 a = s_a[warp][k];
+        const float4 co = s_co[warp][k];
+        const float4 c = s_c[warp][k];
+        const float dx = a.x - fx;
+        const ColTerms ct = col_terms(co.x, co.y, co.z, dx);
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          if (!((bits >> p) & 1u)) continue;
+          const float dy = a.y - fy[p];
+          const float G = splat_exp(splat_power(ct, dy));
+          const float oG = __fmul_rn(co.w, G);
+          const float alpha = fminf(ALPHA_MAX, oG);
+          const float inv = rcp_approx(1.f - alpha);
+          T[p] *= inv;                        // transmittance before this entry
+          const float w = alpha * T[p];
+          const float gc = g[p][0] * c.x + g[p][1] * c.y + g[p][2] * c.z;
+          const float dLda = T[p] * gc - inv * gR[p];
+          gR[p] += gc * w;                    // g·(S + T_final·bg), S = suffix colour
+          v[6] += w * g[p][0]; v[7] += w * g[p][1]; v[8] += w * g[p][2];
+          const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
+          const float ex = e * dx, ey = e * dy;
+          v[0] += ex; v[1] += ey; v[2] += ex * dx; v[3] += ex * dy; v[4] += ey * dy; v[5] += e;
+        }
+      }
+      const float sum = rs.reduce(v);
+      if (rs.slot >= 0) s_acc[warp][k][rs.slot] = sum;
+    }
+    __syncwarp();
+    if ((int)lane < cnt) {
+      const float* a9 = s_acc[warp][lane];
+      float4* dst = g2d + 3 * (size_t)s_id[warp][lane];
+      red_add_v4(dst, make_float4(a9[0], a9[1], a9[2], a9[3]));
+      red_add_v4(dst + 1, make_float4(a9[4], a9[5], a9[6], a9[7]));
+      atomicAdd(&dst[2].x, a9[8]);
+    }
+    __syncwarp();
+    ptr = k0;
+  }
+}
+
 // --------------------------------------------- backward: preprocess part ----
 // Per Gaussian, over V views: each view's 2D moments → ∂L/∂(u, v, A, B, C, o,
 // rgb) → chained through Eqs. 5-7 and the SH colour.  The parameters are read
@@ -438,8 +592,17 @@ struct PreArgs {
   uint32_t* gradstat_cnt;
 };
 
-template <int DEG>
-__global__ void __launch_bounds__(256, 2) preprocess_views_kernel(const __grid_constant__ PreArgs a) {
+// PART 1: geometry (p, s, q, o, ∇p̄ and the SH direction term), fp64 chain.
+// PART 2: SH coefficient gradients (fp32, 3(d+1)² register accumulators).
+// Split so neither part spills.
+template <int DEG, int PART>
+__global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? 3 : 2) preprocess_views_kernel(
+    const __grid_constant__ PreArgs a) {
+  // The per-Gaussian chain is evaluated in fp64: the kernel is HBM-bound, so
+  // the wider arithmetic is free, and it removes the chain's own rounding
+  // (conic → Σ' → Σ → R(q), J(t) with its clamp) from the gradient error
+  // budget, leaving only the fp32 per-pixel sums of the raster pass.
+  using F = double;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   const int n = a.n;
@@ -449,15 +612,15 @@ __global__ void __launch_bounds__(256, 2) preprocess_views_kernel(const __grid_c
   const float4 q = a.rot[i];
   const float4 sc = a.scale[i];
   // view-independent geometry: q̂, R, s, Σ
-  const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
-  const float qi = 1.f / qn;
-  const float w = q.x * qi, x = q.y * qi, y = q.z * qi, z = q.w * qi;
-  float R[3][3];
-  R[0][0] = 1.f - 2.f * (y * y + z * z); R[0][1] = 2.f * (x * y - w * z); R[0][2] = 2.f * (x * z + w * y);
-  R[1][0] = 2.f * (x * y + w * z); R[1][1] = 1.f - 2.f * (x * x + z * z); R[1][2] = 2.f * (y * z - w * x);
-  R[2][0] = 2.f * (x * z - w * y); R[2][1] = 2.f * (y * z + w * x); R[2][2] = 1.f - 2.f * (x * x + y * y);
-  const float s[3] = {kp ? sc.x : 0.f, kp ? sc.y : 0.f, kp ? sc.z : 0.f};
-  float Sig[3][3];
+  const F qn = sqrt((F)q.x * q.x + (F)q.y * q.y + (F)q.z * q.z + (F)q.w * q.w);
+  const F qi = 1.0 / qn;
+  const F w = q.x * qi, x = q.y * qi, y = q.z * qi, z = q.w * qi;
+  F R[3][3];
+  R[0][0] = 1 - 2 * (y * y + z * z); R[0][1] = 2 * (x * y - w * z); R[0][2] = 2 * (x * z + w * y);
+  R[1][0] = 2 * (x * y + w * z); R[1][1] = 1 - 2 * (x * x + z * z); R[1][2] = 2 * (y * z - w * x);
+  R[2][0] = 2 * (x * z - w * y); R[2][1] = 2 * (y * z + w * x); R[2][2] = 1 - 2 * (x * x + y * y);
+  const F s[3] = {kp ? (F)sc.x : 0.0, kp ? (F)sc.y : 0.0, kp ? (F)sc.z : 0.0};
+  F Sig[3][3];
 #pragma unroll
   for (int r0 = 0; r0 < 3; ++r0)
 #pragma unroll
@@ -465,12 +628,13 @@ __global__ void __launch_bounds__(256, 2) preprocess_views_kernel(const __grid_c
       Sig[r0][c0] = R[r0][0] * s[0] * s[0] * R[c0][0] + R[r0][1] * s[1] * s[1] * R[c0][1] +
                     R[r0][2] * s[2] * s[2] * R[c0][2];
   // accumulators over views
-  float gp[3] = {0.f, 0.f, 0.f};
-  float go = 0.f;
-  float GS[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-  float gsh[4 * L::K4];
+  F gp[3] = {0, 0, 0};
+  F go = 0;
+  F GS[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  constexpr int NGSH = PART == 2 ? 4 * L::K4 : 1;
+  float gsh[NGSH];
 #pragma unroll
-  for (int f = 0; f < 4 * L::K4; ++f) gsh[f] = 0.f;
+  for (int f = 0; f < NGSH; ++f) gsh[f] = 0.f;
   float gstat = 0.f;
   uint32_t nvis = 0;
   for (int v = 0; v < a.num_views; ++v) {
@@ -479,30 +643,38 @@ __global__ void __launch_bounds__(256, 2) preprocess_views_kernel(const __grid_c
     if ((bx.x & 0xFFFFu) > (bx.x >> 16)) continue;  // culled in this view
     const CamParams& cam = a.cam[v];
     ++nvis;
-    const float4 m0 = a.g2d[3 * o], m1 = a.g2d[3 * o + 1], m2 = a.g2d[3 * o + 2];
-    const float4 co = a.conic_opa[o];
-    const float A = co.x, B = co.y, Cc = co.z, op = co.w;
-    // 2D gradients from the moments
-    const float gu = -op * (A * m0.x + B * m0.y);
-    const float gv = -op * (B * m0.x + Cc * m0.y);
-    const float gA = -0.5f * op * m0.z;
-    const float gB = -op * m0.w;
-    const float gC = -0.5f * op * m1.x;
-    go += m1.y;
+    const float4 m1 = a.g2d[3 * o + 1], m2 = a.g2d[3 * o + 2];
     const int bits = (int)a.rgb[o].w;
     const float gcol[3] = {(bits & 1) ? 0.f : m1.z, (bits & 2) ? 0.f : m1.w, (bits & 4) ? 0.f : m2.x};
+    if (PART == 2) {
+      F dx = (F)po.x - cam.campos[0], dy = (F)po.y - cam.campos[1], dz = (F)po.z - cam.campos[2];
+      const F inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+      float Y[L::NC];
+      sh_eval<DEG>((float)(dx * inv), (float)(dy * inv), (float)(dz * inv), Y);
+#pragma unroll
+      for (int f = 0; f < L::NF; ++f) gsh[f] += Y[f / 3] * gcol[f % 3];
+      continue;
+    }
+    const float4 m0 = a.g2d[3 * o];
+    const float4 co = a.conic_opa[o];
+    const F A = co.x, B = co.y, Cc = co.z, op = co.w;
+    // 2D gradients from the moments
+    const F gu = -op * (A * m0.x + B * m0.y);
+    const F gv = -op * (B * m0.x + Cc * m0.y);
+    const F gA = -0.5 * op * m0.z;
+    const F gB = -op * m0.w;
+    const F gC = -0.5 * op * m1.x;
+    go += m1.y;
     {
-      const float ga = gu * 0.5f * cam.W, gb = gv * 0.5f * cam.H;
-      gstat += sqrtf(ga * ga + gb * gb);
+      const F ga = gu * 0.5 * cam.W, gb = gv * 0.5 * cam.H;
+      gstat += (float)sqrt(ga * ga + gb * gb);
     }
     // ---- colour / SH (direction from this view's camera centre)
     {
-      float dx = po.x - cam.campos[0], dy = po.y - cam.campos[1], dz = po.z - cam.campos[2];
-      const float dist = sqrtf(dx * dx + dy * dy + dz * dz);
-      const float inv = 1.f / dist;
+      F dx = (F)po.x - cam.campos[0], dy = (F)po.y - cam.campos[1], dz = (F)po.z - cam.campos[2];
+      const F dist = sqrt(dx * dx + dy * dy + dz * dz);
+      const F inv = 1.0 / dist;
       dx *= inv; dy *= inv; dz *= inv;
-      float Y[L::NC];
-      sh_eval<DEG>(dx, dy, dz, Y);
       float wk[L::NC];
 #pragma unroll
       for (int k = 0; k < L::NC; ++k) wk[k] = 0.f;
@@ -514,16 +686,12 @@ __global__ void __launch_bounds__(256, 2) preprocess_views_kernel(const __grid_c
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int f = 4 * j + e;
-          if (f < L::NF) {
-            const int k = f / 3, ch = f % 3;
-            wk[k] += gcol[ch] * cf[e];
-            gsh[f] += Y[k] * gcol[ch];
-          }
+          if (f < L::NF) wk[f / 3] += gcol[f % 3] * cf[e];
         }
       }
       if (DEG > 0) {
-        const float3 gd = sh_dir_grad<DEG>(dx, dy, dz, wk);
-        const float dd = dx * gd.x + dy * gd.y + dz * gd.z;
+        const float3 gd = sh_dir_grad<DEG>((float)dx, (float)dy, (float)dz, wk);
+        const F dd = dx * gd.x + dy * gd.y + dz * gd.z;
         gp[0] += (gd.x - dx * dd) * inv;
         gp[1] += (gd.y - dy * dd) * inv;
         gp[2] += (gd.z - dz * dd) * inv;
@@ -531,32 +699,33 @@ __global__ void __launch_bounds__(256, 2) preprocess_views_kernel(const __grid_c
     }
     // ---- projection chain for this view
     const float* V = cam.V;
-    float t[3];
+    F t[3];
 #pragma unroll
     for (int r0 = 0; r0 < 3; ++r0)
-      t[r0] = V[4 * r0] * po.x + V[4 * r0 + 1] * po.y + V[4 * r0 + 2] * po.z + V[4 * r0 + 3];
-    const float lx = 1.3f * cam.W / (2.f * cam.fx), ly = 1.3f * cam.H / (2.f * cam.fy);
-    const float txtz = t[0] / t[2], tytz = t[1] / t[2];
+      t[r0] = (F)V[4 * r0] * po.x + (F)V[4 * r0 + 1] * po.y + (F)V[4 * r0 + 2] * po.z + (F)V[4 * r0 + 3];
+    const F lx = 1.3 * cam.W / (2.0 * cam.fx), ly = 1.3 * cam.H / (2.0 * cam.fy);
+    const F txtz = t[0] / t[2], tytz = t[1] / t[2];
     const bool clx = txtz < -lx || txtz > lx, cly = tytz < -ly || tytz > ly;
-    const float xt = t[2] * fminf(lx, fmaxf(-lx, txtz));
-    const float yt = t[2] * fminf(ly, fmaxf(-ly, tytz));
-    const float tz = t[2], tz2 = tz * tz, tz3 = tz2 * tz;
-    const float J00 = cam.fx / tz, J02 = -cam.fx * xt / tz2;
-    const float J11 = cam.fy / tz, J12 = -cam.fy * yt / tz2;
-    float M[2][3];
+    const F xt = t[2] * fmin(lx, fmax(-lx, txtz));
+    const F yt = t[2] * fmin(ly, fmax(-ly, tytz));
+    const F tz = t[2], tz2 = tz * tz, tz3 = tz2 * tz;
+    const F fxc = cam.fx, fyc = cam.fy;
+    const F J00 = fxc / tz, J02 = -fxc * xt / tz2;
+    const F J11 = fyc / tz, J12 = -fyc * yt / tz2;
+    F M[2][3];
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
       M[0][b] = J00 * V[b] + J02 * V[8 + b];
       M[1][b] = J11 * V[4 + b] + J12 * V[8 + b];
     }
     // conic → Σ': Gs = −K Ĝ K, Ĝ = [[gA, gB/2],[gB/2, gC]]
-    const float G01h = 0.5f * gB;
-    const float KG00 = A * gA + B * G01h, KG01 = A * G01h + B * gC;
-    const float KG10 = B * gA + Cc * G01h, KG11 = B * G01h + Cc * gC;
-    const float Gs00 = -(KG00 * A + KG01 * B);
-    const float Gs01 = -(KG00 * B + KG01 * Cc);
-    const float Gs11 = -(KG10 * B + KG11 * Cc);
-    float GM1[2][3];  // Gs M
+    const F G01h = 0.5 * gB;
+    const F KG00 = A * gA + B * G01h, KG01 = A * G01h + B * gC;
+    const F KG10 = B * gA + Cc * G01h, KG11 = B * G01h + Cc * gC;
+    const F Gs00 = -(KG00 * A + KG01 * B);
+    const F Gs01 = -(KG00 * B + KG01 * Cc);
+    const F Gs11 = -(KG10 * B + KG11 * Cc);
+    F GM1[2][3];  // Gs M
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
       GM1[0][b] = Gs00 * M[0][b] + Gs01 * M[1][b];
@@ -568,41 +737,40 @@ __global__ void __launch_bounds__(256, 2) preprocess_views_kernel(const __grid_c
 #pragma unroll
       for (int c0 = 0; c0 < 3; ++c0) GS[r0][c0] += M[0][r0] * GM1[0][c0] + M[1][r0] * GM1[1][c0];
     // ∂L/∂M = 2 Gs M Σ → ∂L/∂J = ∂L/∂M Wᵀ
-    float GM[2][3];
+    F GM[2][3];
 #pragma unroll
     for (int r0 = 0; r0 < 2; ++r0)
 #pragma unroll
       for (int b = 0; b < 3; ++b)
-        GM[r0][b] = 2.f * (GM1[r0][0] * Sig[0][b] + GM1[r0][1] * Sig[1][b] + GM1[r0][2] * Sig[2][b]);
-    const float GJ00 = GM[0][0] * V[0] + GM[0][1] * V[1] + GM[0][2] * V[2];
-    const float GJ02 = GM[0][0] * V[8] + GM[0][1] * V[9] + GM[0][2] * V[10];
-    const float GJ11 = GM[1][0] * V[4] + GM[1][1] * V[5] + GM[1][2] * V[6];
-    const float GJ12 = GM[1][0] * V[8] + GM[1][1] * V[9] + GM[1][2] * V[10];
-    float gt[3] = {0.f, 0.f, 0.f};
-    gt[2] += GJ00 * (-cam.fx / tz2) + GJ11 * (-cam.fy / tz2);
+        GM[r0][b] = 2 * (GM1[r0][0] * Sig[0][b] + GM1[r0][1] * Sig[1][b] + GM1[r0][2] * Sig[2][b]);
+    const F GJ00 = GM[0][0] * V[0] + GM[0][1] * V[1] + GM[0][2] * V[2];
+    const F GJ02 = GM[0][0] * V[8] + GM[0][1] * V[9] + GM[0][2] * V[10];
+    const F GJ11 = GM[1][0] * V[4] + GM[1][1] * V[5] + GM[1][2] * V[6];
+    const F GJ12 = GM[1][0] * V[8] + GM[1][1] * V[9] + GM[1][2] * V[10];
+    F gt[3] = {0, 0, 0};
+    gt[2] += GJ00 * (-fxc / tz2) + GJ11 * (-fyc / tz2);
     if (!clx) {
-      gt[0] += GJ02 * (-cam.fx / tz2);
-      gt[2] += GJ02 * (2.f * cam.fx * t[0] / tz3);
+      gt[0] += GJ02 * (-fxc / tz2);
+      gt[2] += GJ02 * (2 * fxc * t[0] / tz3);
     } else {
-      gt[2] += GJ02 * (cam.fx * xt / tz3);
+      gt[2] += GJ02 * (fxc * xt / tz3);
     }
     if (!cly) {
-      gt[1] += GJ12 * (-cam.fy / tz2);
-      gt[2] += GJ12 * (2.f * cam.fy * t[1] / tz3);
+      gt[1] += GJ12 * (-fyc / tz2);
+      gt[2] += GJ12 * (2 * fyc * t[1] / tz3);
     } else {
-      gt[2] += GJ12 * (cam.fy * yt / tz3);
+      gt[2] += GJ12 * (fyc * yt / tz3);
     }
-    gt[0] += gu * cam.fx / tz;
-    gt[2] += gu * (-cam.fx * t[0] / tz2);
-    gt[1] += gv * cam.fy / tz;
-    gt[2] += gv * (-cam.fy * t[1] / tz2);
+    gt[0] += gu * fxc / tz;
+    gt[2] += gu * (-fxc * t[0] / tz2);
+    gt[1] += gv * fyc / tz;
+    gt[2] += gv * (-fyc * t[1] / tz2);
 #pragma unroll
     for (int c0 = 0; c0 < 3; ++c0) gp[c0] += V[c0] * gt[0] + V[4 + c0] * gt[1] + V[8 + c0] * gt[2];
   }
   if (nvis == 0) return;
-  if (a.gradstat_sum) a.gradstat_sum[i] += gstat;
-  if (a.gradstat_cnt) a.gradstat_cnt[i] += nvis;
-  if (a.g_sh) {
+  if (PART == 2) {
+    if (!a.g_sh) return;
 #pragma unroll
     for (int j = 0; j < L::K4; ++j) {
       const size_t off = (size_t)j * n + i;
@@ -612,59 +780,81 @@ __global__ void __launch_bounds__(256, 2) preprocess_views_kernel(const __grid_c
       if (4 * j + 3 < L::NF) gg.w += gsh[4 * j + 3];
       a.g_sh[off] = gg;
     }
+    return;
   }
+  if (a.gradstat_sum) a.gradstat_sum[i] += gstat;
+  if (a.gradstat_cnt) a.gradstat_cnt[i] += nvis;
   if (a.g_pos_opa) {
     float4 gpo = a.g_pos_opa[i];
-    gpo.x += gp[0]; gpo.y += gp[1]; gpo.z += gp[2];
-    gpo.w += kp ? go : 0.f;
+    gpo.x += (float)gp[0]; gpo.y += (float)gp[1]; gpo.z += (float)gp[2];
+    gpo.w += kp ? (float)go : 0.f;
     a.g_pos_opa[i] = gpo;
   }
   if (!a.g_scale && !a.g_rot) return;
   // Σ = R diag(s²) Rᵀ : dL/ds_k = 2 s_k (Rᵀ GΣ R)_kk ; dL/dR = 2 GΣ R diag(s²)
-  float GR[3][3];
-  float gs[3];
+  F GR[3][3];
+  F gs[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    float GSr[3];
+    F GSr[3];
 #pragma unroll
     for (int r0 = 0; r0 < 3; ++r0) GSr[r0] = GS[r0][0] * R[0][k] + GS[r0][1] * R[1][k] + GS[r0][2] * R[2][k];
-    gs[k] = 2.f * s[k] * (R[0][k] * GSr[0] + R[1][k] * GSr[1] + R[2][k] * GSr[2]);
+    gs[k] = 2 * s[k] * (R[0][k] * GSr[0] + R[1][k] * GSr[1] + R[2][k] * GSr[2]);
 #pragma unroll
-    for (int r0 = 0; r0 < 3; ++r0) GR[r0][k] = 2.f * GSr[r0] * s[k] * s[k];
+    for (int r0 = 0; r0 < 3; ++r0) GR[r0][k] = 2 * GSr[r0] * s[k] * s[k];
   }
   if (a.g_scale) {
     float4 g4 = a.g_scale[i];
-    if (kp) { g4.x += gs[0]; g4.y += gs[1]; g4.z += gs[2]; }
+    if (kp) { g4.x += (float)gs[0]; g4.y += (float)gs[1]; g4.z += (float)gs[2]; }
     a.g_scale[i] = g4;
   }
   if (a.g_rot) {
-    float gq[4];
-    gq[0] = GR[0][1] * (-2.f * z) + GR[0][2] * (2.f * y) + GR[1][0] * (2.f * z) + GR[1][2] * (-2.f * x) +
-            GR[2][0] * (-2.f * y) + GR[2][1] * (2.f * x);
-    gq[1] = GR[0][1] * (2.f * y) + GR[0][2] * (2.f * z) + GR[1][0] * (2.f * y) + GR[1][1] * (-4.f * x) +
-            GR[1][2] * (-2.f * w) + GR[2][0] * (2.f * z) + GR[2][1] * (2.f * w) + GR[2][2] * (-4.f * x);
-    gq[2] = GR[0][0] * (-4.f * y) + GR[0][1] * (2.f * x) + GR[0][2] * (2.f * w) + GR[1][0] * (2.f * x) +
-            GR[1][2] * (2.f * z) + GR[2][0] * (-2.f * w) + GR[2][1] * (2.f * z) + GR[2][2] * (-4.f * y);
-    gq[3] = GR[0][0] * (-4.f * z) + GR[0][1] * (-2.f * w) + GR[0][2] * (2.f * x) + GR[1][0] * (2.f * w) +
-            GR[1][1] * (-4.f * z) + GR[1][2] * (2.f * y) + GR[2][0] * (2.f * x) + GR[2][1] * (2.f * y);
-    const float dot = w * gq[0] + x * gq[1] + y * gq[2] + z * gq[3];
+    F gq[4];
+    gq[0] = GR[0][1] * (-2 * z) + GR[0][2] * (2 * y) + GR[1][0] * (2 * z) + GR[1][2] * (-2 * x) +
+            GR[2][0] * (-2 * y) + GR[2][1] * (2 * x);
+    gq[1] = GR[0][1] * (2 * y) + GR[0][2] * (2 * z) + GR[1][0] * (2 * y) + GR[1][1] * (-4 * x) +
+            GR[1][2] * (-2 * w) + GR[2][0] * (2 * z) + GR[2][1] * (2 * w) + GR[2][2] * (-4 * x);
+    gq[2] = GR[0][0] * (-4 * y) + GR[0][1] * (2 * x) + GR[0][2] * (2 * w) + GR[1][0] * (2 * x) +
+            GR[1][2] * (2 * z) + GR[2][0] * (-2 * w) + GR[2][1] * (2 * z) + GR[2][2] * (-4 * y);
+    gq[3] = GR[0][0] * (-4 * z) + GR[0][1] * (-2 * w) + GR[0][2] * (2 * x) + GR[1][0] * (2 * w) +
+            GR[1][1] * (-4 * z) + GR[1][2] * (2 * y) + GR[2][0] * (2 * x) + GR[2][1] * (2 * y);
+    const F dot = w * gq[0] + x * gq[1] + y * gq[2] + z * gq[3];
     float4 g4 = a.g_rot[i];
-    g4.x += (gq[0] - w * dot) * qi;
-    g4.y += (gq[1] - x * dot) * qi;
-    g4.z += (gq[2] - y * dot) * qi;
-    g4.w += (gq[3] - z * dot) * qi;
+    g4.x += (float)((gq[0] - w * dot) * qi);
+    g4.y += (float)((gq[1] - x * dot) * qi);
+    g4.z += (float)((gq[2] - y * dot) * qi);
+    g4.w += (float)((gq[3] - z * dot) * qi);
     a.g_rot[i] = g4;
   }
 }
 
-// Pixels per thread of the raster kernels (tuning knob; DASS_FWD_PPT /
-// DASS_BWD_PPT override the default for experiments, read once per process).
+// Pixels per thread of the raster kernels without acceptance lists (tuning
+// knob; DASS_FWD_PPT / DASS_BWD_PPT override the default, read once).
 static int ppt_from_env(const char* name, int dflt) {
   const char* v = getenv(name);
   if (!v) return dflt;
   const int p = atoi(v);
   return (p == 1 || p == 2 || p == 4 || p == 8) ? p : dflt;
 }
+
+// Acceptance-list workspace: cnt[2·ntiles] u32 | idx[2·capacity] u32 | bytes[2·capacity][32].
+static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+size_t accept_bytes(int ntiles, int64_t capacity) {
+  const size_t c = (size_t)(capacity > 0 ? capacity : 1);
+  return al(sizeof(uint32_t) * 2 * (size_t)ntiles) + al(sizeof(uint32_t) * 2 * c) + al(32 * 2 * c);
+}
+AcceptLists carve_accept(void* base, int ntiles, int64_t capacity) {
+  const size_t c = (size_t)(capacity > 0 ? capacity : 1);
+  char* p = (char*)base;
+  AcceptLists a;
+  a.cnt = (uint32_t*)p;
+  p += al(sizeof(uint32_t) * 2 * (size_t)ntiles);
+  a.idx = (uint32_t*)p;
+  p += al(sizeof(uint32_t) * 2 * c);
+  a.bytes = (uint8_t*)p;
+  return a;
+}
+
 static int fwd_ppt() { static const int p = ppt_from_env("DASS_FWD_PPT", 4); return p; }
 static int bwd_ppt() { static const int p = ppt_from_env("DASS_BWD_PPT", 4); return p; }
 static int bwd_minb() {
@@ -678,14 +868,24 @@ static int bwd_minb() {
 
 }  // namespace
 
+size_t render_accept_workspace(int ntiles, int64_t capacity) { return accept_bytes(ntiles, capacity); }
+
 cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
                               const float4* xy_depth, const float4* conic_opa, const float4* rgb,
                               const uint2* box, float3 bg, float* out_img, float* out_T,
-                              uint32_t* out_last, cudaStream_t s) {
+                              uint32_t* out_last, void* accept, int64_t capacity, cudaStream_t s) {
   const int ntiles = cam.tiles_x * cam.tiles_y;
-#define FWD(P)                                                                                   \
-  render_fwd_kernel<P><<<ntiles, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, box, \
-                                                  bg, out_img, out_T, out_last)
+  if (accept != nullptr) {
+    const AcceptLists acc = carve_accept(accept, ntiles, capacity);
+    render_fwd_kernel<4, true><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, box,
+                                                     bg, out_img, out_T, out_last, acc);
+    launch_counted();
+    return cudaGetLastError();
+  }
+  const AcceptLists none{nullptr, nullptr, nullptr};
+#define FWD(P)                                                                                    \
+  render_fwd_kernel<P, false><<<ntiles, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
+                                                         box, bg, out_img, out_T, out_last, none)
   switch (fwd_ppt()) {
     case 1: FWD(1); break;
     case 2: FWD(2); break;
@@ -703,10 +903,18 @@ cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* r
                                      const uint32_t* ids, const float4* xy_depth,
                                      const float4* conic_opa, const float4* rgb, const uint2* box,
                                      float3 bg, const float* out_T, const uint32_t* out_last,
-                                     const float* dL_dimg, float4* g2d, cudaStream_t s) {
+                                     const float* dL_dimg, const void* accept, int64_t capacity,
+                                     float4* g2d, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(g2d, 0, render_bwd_workspace(n), s);
   if (e != cudaSuccess) return e;
   const int ntiles = cam.tiles_x * cam.tiles_y;
+  if (accept != nullptr) {
+    const AcceptLists acc = carve_accept(const_cast<void*>(accept), ntiles, capacity);
+    render_bwd_list_kernel<4><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg,
+                                                    out_T, dL_dimg, acc, g2d);
+    launch_counted();
+    return cudaGetLastError();
+  }
 #define BWD(P, MB)                                                                          \
   render_bwd_raster_kernel<P, MB><<<ntiles, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, \
                                                              rgb, box, bg, out_T, out_last, dL_dimg, g2d)
@@ -742,12 +950,16 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
     a.gradstat_sum = gradstat_sum; a.gradstat_cnt = gradstat_cnt;
     const int grid = div_up(n, 256);
     switch (sh_degree) {
-      case 0: preprocess_views_kernel<0><<<grid, 256, 0, s>>>(a); break;
-      case 1: preprocess_views_kernel<1><<<grid, 256, 0, s>>>(a); break;
-      case 2: preprocess_views_kernel<2><<<grid, 256, 0, s>>>(a); break;
-      default: preprocess_views_kernel<3><<<grid, 256, 0, s>>>(a); break;
+#define PRE(D)                                                                \
+  preprocess_views_kernel<D, 1><<<div_up(n, 128), 128, 0, s>>>(a);           \
+  preprocess_views_kernel<D, 2><<<grid, 256, 0, s>>>(a)
+      case 0: PRE(0); break;
+      case 1: PRE(1); break;
+      case 2: PRE(2); break;
+      default: PRE(3); break;
+#undef PRE
     }
-    launch_counted();
+    launch_counted(2);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -759,12 +971,13 @@ cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const 
                               const uint8_t* keep, const uint2* ranges, const uint32_t* ids,
                               const float4* xy_depth, const float4* conic_opa, const float4* rgb,
                               const uint2* box, float3 bg, const float* out_T,
-                              const uint32_t* out_last, const float* dL_dimg, void* ws,
-                              float4* g_pos_opa, float4* g_scale, float4* g_rot, float4* g_sh,
-                              float* gradstat_sum, uint32_t* gradstat_cnt, cudaStream_t s) {
+                              const uint32_t* out_last, const float* dL_dimg, const void* accept,
+                              int64_t capacity, void* ws, float4* g_pos_opa, float4* g_scale,
+                              float4* g_rot, float4* g_sh, float* gradstat_sum,
+                              uint32_t* gradstat_cnt, cudaStream_t s) {
   float4* g2d = (float4*)ws;
   cudaError_t e = launch_render_bwd_raster(cam, n, ranges, ids, xy_depth, conic_opa, rgb, box, bg,
-                                           out_T, out_last, dL_dimg, g2d, s);
+                                           out_T, out_last, dL_dimg, accept, capacity, g2d, s);
   if (e != cudaSuccess) return e;
   return launch_preprocess_views(&cam, 1, n, sh_degree, pos_opa, scale, rot, sh, keep, conic_opa,
                                  rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh, gradstat_sum,

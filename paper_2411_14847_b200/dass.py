@@ -26,7 +26,8 @@ DASS_ERR_CUDA = 5
 EXPORTS = (
     "dass_status_string", "dass_last_error", "dass_abi_version", "dass_kernel_launches",
     "dass_apply_shift", "dass_apply_shift_bwd", "dass_project", "dass_project_views",
-    "dass_bin_sort_workspace", "dass_bin_sort", "dass_render_fwd", "dass_render_bwd_workspace",
+    "dass_bin_sort_workspace", "dass_bin_sort", "dass_render_accept_workspace", "dass_render_fwd",
+    "dass_render_bwd_workspace",
     "dass_render_bwd", "dass_render_bwd_raster", "dass_render_bwd_preprocess_views",
     "dass_inherit_mask", "dass_inherit_mask_bwd", "dass_error_map", "dass_render_stats",
 )
@@ -81,11 +82,12 @@ def lib():
         L.dass_project_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P]
         L.dass_bin_sort_workspace.argtypes = [i32, i32, i64, P]
         L.dass_bin_sort.argtypes = [P, i32, P, P, P, P, C.c_size_t, i64, P, P, P, P, P, P]
-        L.dass_render_fwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_render_accept_workspace.argtypes = [i32, i64, P]
+        L.dass_render_fwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, i64, P]
         L.dass_render_bwd_workspace.argtypes = [i32, P]
         L.dass_render_bwd.argtypes = [P, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
-                                      P, C.c_size_t, P, P, P, P, P, P, P]
-        L.dass_render_bwd_raster.argtypes = [P, i32, P, P, P, P, P, P, P, P, P, P, P, P]
+                                      P, i64, P, C.c_size_t, P, P, P, P, P, P, P]
+        L.dass_render_bwd_raster.argtypes = [P, i32, P, P, P, P, P, P, P, P, P, P, P, i64, P, P]
         L.dass_render_bwd_preprocess_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P,
                                                        P, P, P, P, P, P, P]
         L.dass_inherit_mask.argtypes = [i32, P, P, P]
@@ -182,13 +184,21 @@ def dass_bin_sort(cam, n, xy_depth, box, tiles_touched, ws, pair_capacity, sorte
     return k.value if host_mode else None
 
 
+def dass_render_accept_workspace(num_tiles, pair_capacity) -> int:
+    out = C.c_size_t(0)
+    _check(lib().dass_render_accept_workspace(num_tiles, pair_capacity, C.byref(out)),
+           "dass_render_accept_workspace")
+    return out.value
+
+
 def dass_render_fwd(cam, tile_ranges, sorted_ids, xy_depth, conic_opa, rgb, box, bg, out_img,
-                    out_T, out_last, stream=None):
+                    out_T, out_last, accept=None, pair_capacity=0, stream=None):
     c = _cam(cam)
     b = None if bg is None else (C.c_float * 3)(*[float(x) for x in bg])
     _check(lib().dass_render_fwd(C.byref(c), _ptr(tile_ranges), _ptr(sorted_ids), _ptr(xy_depth),
                                  _ptr(conic_opa), _ptr(rgb), _ptr(box), b, _ptr(out_img),
-                                 _ptr(out_T), _ptr(out_last), _stream(stream)), "dass_render_fwd")
+                                 _ptr(out_T), _ptr(out_last), _ptr(accept), pair_capacity,
+                                 _stream(stream)), "dass_render_fwd")
 
 
 def dass_render_bwd_workspace(n) -> int:
@@ -199,27 +209,31 @@ def dass_render_bwd_workspace(n) -> int:
 
 def dass_render_bwd(cam, sh_degree, pos_opa, scale, rot, sh, keep_mask, tile_ranges, sorted_ids,
                     xy_depth, conic_opa, rgb, box, bg, out_T, out_last, dL_dimg, ws, g_pos_opa,
-                    g_scale, g_rot, g_sh, gradstat_sum, gradstat_cnt, stream=None):
+                    g_scale, g_rot, g_sh, gradstat_sum, gradstat_cnt, accept=None,
+                    pair_capacity=0, stream=None):
     c = _cam(cam)
     b = None if bg is None else (C.c_float * 3)(*[float(x) for x in bg])
     _check(lib().dass_render_bwd(C.byref(c), pos_opa.shape[0], sh_degree, _ptr(pos_opa),
                                  _ptr(scale), _ptr(rot), _ptr(sh), _ptr(keep_mask),
                                  _ptr(tile_ranges), _ptr(sorted_ids), _ptr(xy_depth),
                                  _ptr(conic_opa), _ptr(rgb), _ptr(box), b, _ptr(out_T),
-                                 _ptr(out_last), _ptr(dL_dimg), _ptr(ws),
-                                 ws.numel() * ws.element_size(), _ptr(g_pos_opa), _ptr(g_scale),
+                                 _ptr(out_last), _ptr(dL_dimg), _ptr(accept), pair_capacity,
+                                 _ptr(ws), ws.numel() * ws.element_size(), _ptr(g_pos_opa),
+                                 _ptr(g_scale),
                                  _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum), _ptr(gradstat_cnt),
                                  _stream(stream)), "dass_render_bwd")
 
 
 def dass_render_bwd_raster(cam, n, tile_ranges, sorted_ids, xy_depth, conic_opa, rgb, box, bg,
-                           out_T, out_last, dL_dimg, g2d, stream=None):
+                           out_T, out_last, dL_dimg, g2d, accept=None, pair_capacity=0,
+                           stream=None):
     c = _cam(cam)
     b = None if bg is None else (C.c_float * 3)(*[float(x) for x in bg])
     _check(lib().dass_render_bwd_raster(C.byref(c), n, _ptr(tile_ranges), _ptr(sorted_ids),
                                         _ptr(xy_depth), _ptr(conic_opa), _ptr(rgb), _ptr(box), b,
-                                        _ptr(out_T), _ptr(out_last), _ptr(dL_dimg), _ptr(g2d),
-                                        _stream(stream)), "dass_render_bwd_raster")
+                                        _ptr(out_T), _ptr(out_last), _ptr(dL_dimg), _ptr(accept),
+                                        pair_capacity, _ptr(g2d), _stream(stream)),
+           "dass_render_bwd_raster")
 
 
 def dass_render_bwd_preprocess_views(cams, sh_degree, pos_opa, scale, rot, sh, keep_mask,

@@ -10,6 +10,7 @@ allocates the documented layouts and calls the exports in order:
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -89,7 +90,8 @@ class ViewRecords:
 class Raster:
     """Scratch for one view at a time: sorted pairs, ranges, fwd outputs, bwd workspace."""
 
-    def __init__(self, width: int, height: int, n: int, capacity: int, device="cuda"):
+    def __init__(self, width: int, height: int, n: int, capacity: int, device="cuda",
+                 accept_lists: bool = True):
         torch = _torch()
         self.W, self.H, self.n, self.capacity = width, height, n, capacity
         self.num_tiles = ((width + 15) // 16) * ((height + 15) // 16)
@@ -103,6 +105,11 @@ class Raster:
         self.last = torch.empty(height, width, dtype=torch.int32, device=device)
         bws = dass.dass_render_bwd_workspace(n)
         self.bwd_ws = torch.empty(bws // 4, dtype=torch.float32, device=device)
+        self.accept = None
+        if accept_lists and os.environ.get("DASS_NO_LISTS") != "1":
+            # forward-recorded acceptance lists consumed by the backward
+            ab = dass.dass_render_accept_workspace(self.num_tiles, capacity)
+            self.accept = torch.empty(ab // 4, dtype=torch.int32, device=device)
 
     def forward(self, cam, rec, host_mode=False, bg=None, sorted_keys=None):
         xy, co, rgb, box, tiles = rec
@@ -110,7 +117,7 @@ class Raster:
                                sorted_keys, self.sorted_ids, self.ranges, self.num_pairs,
                                host_mode=host_mode)
         dass.dass_render_fwd(cam, self.ranges, self.sorted_ids, xy, co, rgb, box, bg, self.img,
-                             self.T, self.last)
+                             self.T, self.last, self.accept, self.capacity)
         return K
 
     def backward(self, cam, scene: DeviceScene, rec, dL_dimg, grads: Grads, keep=None, bg=None,
@@ -121,7 +128,8 @@ class Raster:
                              scene.sh, keep, self.ranges, self.sorted_ids, xy, co, rgb, box, bg,
                              self.T, self.last, dL_dimg, self.bwd_ws, g("pos", grads.pos_opa),
                              g("scale", grads.scale), g("rot", grads.rot), g("sh", grads.sh),
-                             g("stat", grads.gradstat_sum), g("stat", grads.gradstat_cnt))
+                             g("stat", grads.gradstat_sum), g("stat", grads.gradstat_cnt),
+                             self.accept, self.capacity)
 
 
 def project_all(cams, scene: DeviceScene, records: ViewRecords, keep=None):
@@ -171,7 +179,8 @@ class MultiViewPass:
                 xy, co, rgb, box, tiles = rec
                 ras.forward(cam, rec, bg=bg)
                 dass.dass_render_bwd_raster(cam, self.n, ras.ranges, ras.sorted_ids, xy, co, rgb,
-                                            box, bg, ras.T, ras.last, dL_dimgs[v], self.g2d[v])
+                                            box, bg, ras.T, ras.last, dL_dimgs[v], self.g2d[v],
+                                            ras.accept, ras.capacity)
         for s in self.streams:
             main.wait_stream(s)
         dass.dass_render_bwd_preprocess_views(
