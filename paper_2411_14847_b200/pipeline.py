@@ -164,6 +164,7 @@ class MultiViewPass:
         self.S = max(1, min(streams, self.V))
         self.slots = [Raster(W, H, n, capacity, device) for _ in range(self.S)]
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.S)]
+        self.pre_stream = torch.cuda.Stream(device=device)
         self.g2d = torch.empty(max(self.V, 1), n, 12, dtype=torch.float32, device=device)
 
     def run(self, scene: DeviceScene, records: ViewRecords, dL_dimgs, grads, keep=None, bg=None):
@@ -171,6 +172,7 @@ class MultiViewPass:
         main = torch.cuda.current_stream()
         for s in self.streams:
             s.wait_stream(main)
+        half = self.V // 2 if self.V >= 2 * self.S else 0
         for v, cam in enumerate(self.cams):
             k = v % self.S
             ras, st = self.slots[k], self.streams[k]
@@ -181,10 +183,23 @@ class MultiViewPass:
                 dass.dass_render_bwd_raster(cam, self.n, ras.ranges, ras.sorted_ids, xy, co, rgb,
                                             box, bg, ras.T, ras.last, dL_dimgs[v], self.g2d[v],
                                             ras.accept, ras.capacity)
+            if half and v == half - 1:
+                # the first half's preprocess (HBM-bound) overlaps the second half's
+                # raster kernels (ALU-bound) on a side stream
+                self.pre_stream.wait_stream(main)
+                for s in self.streams:
+                    self.pre_stream.wait_stream(s)
+                with torch.cuda.stream(self.pre_stream):
+                    self._preprocess(scene, records, grads, keep, 0, half)
         for s in self.streams:
             main.wait_stream(s)
+        if half:
+            main.wait_stream(self.pre_stream)
+        self._preprocess(scene, records, grads, keep, half, self.V)
+
+    def _preprocess(self, scene, records, grads, keep, v0, v1):
         dass.dass_render_bwd_preprocess_views(
-            self.cams, scene.sh_degree, scene.pos_opa, scene.scale, scene.rot, scene.sh, keep,
-            records.conic_opa[:self.V], records.rgb[:self.V], records.box[:self.V],
-            self.g2d[:self.V], grads.pos_opa, grads.scale, grads.rot, grads.sh,
+            self.cams[v0:v1], scene.sh_degree, scene.pos_opa, scene.scale, scene.rot, scene.sh,
+            keep, records.conic_opa[v0:v1], records.rgb[v0:v1], records.box[v0:v1],
+            self.g2d[v0:v1], grads.pos_opa, grads.scale, grads.rot, grads.sh,
             grads.gradstat_sum, grads.gradstat_cnt)
