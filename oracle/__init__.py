@@ -218,3 +218,13 @@ def inherit_bwd(m, pos_opa, scale, g_pos_opa, g_scale, lambda_inher=0.0):
                              _p(np.ascontiguousarray(g_scale, np.float64)),
                              C.c_double(lambda_inher), _p(g))
     return g
+
+
+def fidelity_loss(img, gt, lam=0.2, grad=True):
+    """f1 / Eq. 3: returns (L, L1, SSIM, dL/dI or None) in double."""
+    img = _f32(img); gt = _f32(gt)
+    H, W = img.shape[1], img.shape[2]
+    out = np.zeros(3)
+    g = np.zeros(img.shape) if grad else None
+    lib().oracle_fidelity_loss(W, H, _p(img), _p(gt), C.c_double(lam), _p(out), _p(g))
+    return out[0], out[1], out[2], g

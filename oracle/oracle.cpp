@@ -1121,6 +1121,91 @@ int oracle_render_bwd(const OCam* cam, int n, int deg, const float* pos_opa, con
   return 0;
 }
 
+// ------------------------------------------------------------ f1 / Eq. 3 ---
+// Fidelity loss: L = (1−λ)·L1 + λ·L_D-SSIM, "the fidelity loss in
+// the vanilla 3DGS": L1 = mean |I − G| over 3HW values; D-SSIM = 1 − SSIM
+// (A39); SSIM = mean over 3HW of S(q) = ((2μ_Iμ_G + C1)(2σ_IG + C2)) /
+// ((μ_I² + μ_G² + C1)(σ_I² + σ_G² + C2)) with windowed statistics over an
+// 11×11 Gaussian window (σ = 1.5, normalised to sum 1), per channel, zero
+// padding outside the image, C1 = 0.01², C2 = 0.03² (S:306-307 design choice).
+// Direct (non-separable) window sums: O(121·HW) per statistic, plain.
+namespace {
+void gauss_window(double w[11][11]) {
+  double g[11], sum = 0;
+  for (int k = 0; k < 11; ++k) { g[k] = std::exp(-((k - 5) * (k - 5)) / (2.0 * 1.5 * 1.5)); sum += g[k]; }
+  for (int a = 0; a < 11; ++a)
+    for (int b = 0; b < 11; ++b) w[a][b] = (g[a] / sum) * (g[b] / sum);
+}
+}  // namespace
+
+// loss_out[0] = L, [1] = L1, [2] = SSIM.  dL (double[3HW], nullable) = ∂L/∂I.
+int oracle_fidelity_loss(int W, int H, const float* img, const float* gt, double lambda,
+                         double* loss_out, double* dL) {
+  const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+  double w[11][11];
+  gauss_window(w);
+  const size_t np = (size_t)W * H;
+  const double M = 3.0 * (double)np;
+  std::vector<double> P1(3 * np), P2(3 * np), P3(3 * np);
+  double sum_l1 = 0, sum_s = 0;
+  for (int ch = 0; ch < 3; ++ch) {
+    const float* I = img + ch * np;
+    const float* G = gt + ch * np;
+#pragma omp parallel for reduction(+ : sum_l1, sum_s) schedule(static)
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        double m1 = 0, m2 = 0, s11 = 0, s22 = 0, s12 = 0;
+        for (int a = -5; a <= 5; ++a)
+          for (int b = -5; b <= 5; ++b) {
+            const int yy = y + a, xx = x + b;
+            if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;  // zero padding
+            const double wi = w[a + 5][b + 5];
+            const double iv = I[(size_t)yy * W + xx], gv = G[(size_t)yy * W + xx];
+            m1 += wi * iv; m2 += wi * gv; s11 += wi * iv * iv; s22 += wi * gv * gv; s12 += wi * iv * gv;
+          }
+        const double v1 = s11 - m1 * m1, v2 = s22 - m2 * m2, v12 = s12 - m1 * m2;
+        const double A1 = 2 * m1 * m2 + C1, A2 = 2 * v12 + C2;
+        const double B1 = m1 * m1 + m2 * m2 + C1, B2 = v1 + v2 + C2;
+        const double S = A1 * A2 / (B1 * B2);
+        sum_s += S;
+        const size_t q = (size_t)y * W + x;
+        sum_l1 += std::fabs((double)I[q] - (double)G[q]);
+        // ∂S/∂μ_I, ∂S/∂E[I²], ∂S/∂E[IG] at q (μ_G, E[G²] do not depend on I)
+        P1[ch * np + q] = 2 * m2 * (A2 - A1) / (B1 * B2) - 2 * m1 * A1 * A2 * (B2 - B1) / (B1 * B1 * B2 * B2);
+        P2[ch * np + q] = -A1 * A2 / (B1 * B2 * B2);
+        P3[ch * np + q] = 2 * A1 / (B1 * B2);
+      }
+  }
+  const double L1 = sum_l1 / M, SSIM = sum_s / M;
+  loss_out[0] = (1 - lambda) * L1 + lambda * (1 - SSIM);
+  loss_out[1] = L1;
+  loss_out[2] = SSIM;
+  if (!dL) return 0;
+  for (int ch = 0; ch < 3; ++ch) {
+    const float* I = img + ch * np;
+    const float* G = gt + ch * np;
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        const size_t p = (size_t)y * W + x;
+        // ∂SSIM/∂I(p) = (1/M) Σ_q w(p − q) [P1(q) + 2 I(p) P2(q) + G(p) P3(q)]
+        double acc = 0;
+        for (int a = -5; a <= 5; ++a)
+          for (int b = -5; b <= 5; ++b) {
+            const int yy = y + a, xx = x + b;
+            if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+            const size_t q = (size_t)yy * W + xx;
+            const double wi = w[a + 5][b + 5];
+            acc += wi * (P1[ch * np + q] + 2 * (double)I[p] * P2[ch * np + q] + (double)G[p] * P3[ch * np + q]);
+          }
+        const double d = (double)I[p] - (double)G[p];
+        const double sgn = d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0);
+        dL[ch * np + p] = (1 - lambda) * sgn / M - lambda * acc / M;
+      }
+  }
+  return 0;
+}
+
 // ------------------------------------------------------------ f3 / Eq. 1 ---
 // Selective inheritance: o_r = Quant(sigmoid(m))∘o, s_r = Quant(sigmoid(m))∘s
 // with Quant(x) = 1[x ≥ 0.5] (A26).

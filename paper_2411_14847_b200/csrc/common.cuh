@@ -130,6 +130,9 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
                                     const float4* g2d, float4* g_pos_opa, float4* g_scale,
                                     float4* g_rot, float4* g_sh, float* gradstat_sum,
                                     uint32_t* gradstat_cnt, cudaStream_t s);
+size_t fidelity_loss_workspace(int W, int H);
+cudaError_t launch_fidelity_loss(int W, int H, const float* img, const float* gt, float lambda,
+                                 void* ws, float* loss, float* dL, cudaStream_t s);
 cudaError_t launch_inherit_mask(int n, const float* m, uint8_t* keep, cudaStream_t s);
 cudaError_t launch_inherit_mask_bwd(int n, const float* m, const float4* pos_opa,
                                     const float4* scale, const float4* g_pos_opa,

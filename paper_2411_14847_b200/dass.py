@@ -29,7 +29,8 @@ EXPORTS = (
     "dass_bin_sort_workspace", "dass_bin_sort", "dass_render_accept_workspace", "dass_render_fwd",
     "dass_render_bwd_workspace",
     "dass_render_bwd", "dass_render_bwd_raster", "dass_render_bwd_preprocess_views",
-    "dass_inherit_mask", "dass_inherit_mask_bwd", "dass_error_map", "dass_render_stats",
+    "dass_fidelity_loss_workspace", "dass_fidelity_loss", "dass_inherit_mask",
+    "dass_inherit_mask_bwd", "dass_error_map", "dass_render_stats",
 )
 
 
@@ -90,6 +91,8 @@ def lib():
         L.dass_render_bwd_raster.argtypes = [P, i32, P, P, P, P, P, P, P, P, P, P, P, i64, P, P]
         L.dass_render_bwd_preprocess_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P,
                                                        P, P, P, P, P, P, P]
+        L.dass_fidelity_loss_workspace.argtypes = [i32, i32, P]
+        L.dass_fidelity_loss.argtypes = [i32, i32, P, P, C.c_float, P, C.c_size_t, P, P, P]
         L.dass_inherit_mask.argtypes = [i32, P, P, P]
         L.dass_inherit_mask_bwd.argtypes = [i32, P, P, P, P, P, C.c_float, P, P]
         L.dass_error_map.argtypes = [P, P, P, C.c_float, P, P, i32, P, P, P]
@@ -245,6 +248,21 @@ def dass_render_bwd_preprocess_views(cams, sh_degree, pos_opa, scale, rot, sh, k
         _ptr(sh), _ptr(keep_mask), _ptr(conic_opa), _ptr(rgb), _ptr(box), _ptr(g2d),
         _ptr(g_pos_opa), _ptr(g_scale), _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum),
         _ptr(gradstat_cnt), _stream(stream)), "dass_render_bwd_preprocess_views")
+
+
+def dass_fidelity_loss_workspace(width, height) -> int:
+    out = C.c_size_t(0)
+    _check(lib().dass_fidelity_loss_workspace(width, height, C.byref(out)),
+           "dass_fidelity_loss_workspace")
+    return out.value
+
+
+def dass_fidelity_loss(img, gt, lam, ws, loss, dL_dimg=None, stream=None):
+    """Eq. 3: loss (device float[3] = L, L1, SSIM) and optionally ∂L/∂img."""
+    H, W = img.shape[1], img.shape[2]
+    _check(lib().dass_fidelity_loss(W, H, _ptr(img), _ptr(gt), float(lam), _ptr(ws),
+                                    ws.numel() * ws.element_size(), _ptr(loss), _ptr(dL_dimg),
+                                    _stream(stream)), "dass_fidelity_loss")
 
 
 def dass_inherit_mask(m, keep, stream=None):

@@ -447,3 +447,27 @@ def test_inheritance_mask_and_ste_gradient():
     # culled Gaussians (Quant = 0) get only the mask-loss term λ·σ'(m)
     off = ref_keep == 0
     np.testing.assert_allclose(np_(gm)[off], ref[off], rtol=1e-5, atol=1e-9)
+
+
+@pytest.mark.parametrize("W,H,lam,seed", [(100, 70, 0.2, 1), (37, 300, 0.5, 2), (1, 1, 0.2, 3),
+                                           (1352, 1014, 0.2, 4)])
+def test_fidelity_loss_parity(W, H, lam, seed):
+    """f1 (Eq. 3): loss value and ∂L/∂img against the oracle (direct windows)."""
+    g = np.random.default_rng(seed)
+    img = g.uniform(0, 1, size=(3, H, W)).astype(np.float32)
+    gt = np.clip(img + g.normal(0, 0.1, size=img.shape), 0, 1).astype(np.float32)
+    gt[:, : H // 3] = img[:, : H // 3]   # an identical band (sign(0) = 0, S = 1 region)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    ws = torch.empty(dass.dass_fidelity_loss_workspace(W, H) // 4 + 64, dtype=torch.float32, device=DEV)
+    loss = torch.zeros(3, device=DEV)
+    dL = torch.empty(3, H, W, device=DEV)
+    dass.dass_fidelity_loss(t(img), t(gt), lam, ws, loss, dL)
+    torch.cuda.synchronize()
+    L, l1, ssim, ref = oracle.fidelity_loss(img, gt, lam)
+    got = np_(loss)
+    assert got[0] == pytest.approx(L, rel=1e-5, abs=1e-7)
+    assert got[1] == pytest.approx(l1, rel=1e-5, abs=1e-7)
+    assert got[2] == pytest.approx(ssim, rel=1e-5)
+    d = np_(dL)
+    rms = np.sqrt(np.mean(ref ** 2))
+    assert np.all(np.abs(d - ref) <= 1e-3 * np.abs(ref) + 1e-3 * rms)
