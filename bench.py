@@ -242,6 +242,62 @@ def run_ours(args):
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_step = float(ms_t.item())
 
+    # ---- the full training iteration: ∂L/∂C from the fused fidelity loss of
+    # Eq. 3 against per-view ground truth (the render of 𝒢_{t−1} before the
+    # shift), instead of a fixed ∂L/∂C.  Reported next to the metric.
+    train = None
+    if my_cams and not args.lean:
+        mvp.enable_loss(0.2)
+        gts = torch.empty(len(my_cams), 3, H, W, device=dev)
+        dass.dass_project_views(my_cams, deg, base.pos_opa, base.scale, base.rot, base.sh, None,
+                                records.xy_depth, records.conic_opa, records.rgb, records.box,
+                                records.tiles)
+        for k, cam in enumerate(my_cams):
+            raster.forward(cam, records.view(k))
+            gts[k].copy_(raster.img)
+
+        def train_local():
+            grads.zero_()
+            dass.dass_apply_shift(base.pos_opa, base.rot, mu_d, sigma_d, base.dynamic,
+                                  shifted.pos_opa, shifted.rot)
+            dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
+                                    shifted.sh, None, records.xy_depth, records.conic_opa,
+                                    records.rgb, records.box, records.tiles)
+            mvp.run(shifted, records, None, grads, gts=gts)
+            dass.dass_apply_shift_bwd(base.rot, sigma_d, base.dynamic, grads.pos_opa, grads.rot,
+                                      g_mu, g_sigma)
+
+        for _ in range(2):
+            train_local()
+        barrier()
+        tgraph = None
+        if not args.no_graph:
+            tgraph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(tgraph):
+                train_local()
+            tgraph.replay()
+        barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nt = max(3, args.steps // 2)
+        t0.record()
+        for _ in range(nt):
+            if tgraph is None:
+                train_local()
+            else:
+                tgraph.replay()
+            if world > 1:
+                allreduce_grads(grads)
+        t1.record()
+        barrier()
+        tms = torch.tensor([t0.elapsed_time(t1) / nt], device=dev)
+        if world > 1:
+            dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+        train = {"value": round(len(cams) / (float(tms.item()) / 1e3), 3), "unit": "views/s",
+                 "ms_per_step": round(float(tms.item()), 4),
+                 "loss_mean": float(mvp.losses[:, 0].mean().item()),
+                 "what": "shift + fwd + fused L1/D-SSIM loss (Eq. 3) + bwd over the views",
+                 "graph": tgraph is not None}
+
     # ---- per-op breakdown: one extra SEQUENTIAL step, CUDA events on the
     # launching stream around each export (diagnostic; the timed step overlaps views)
     ops = {}
@@ -277,12 +333,21 @@ def run_ours(args):
             mvp.g2d[:len(my_cams)], grads.pos_opa, grads.scale, grads.rot, grads.sh,
             grads.gradstat_sum, grads.gradstat_cnt)
         e_pre[1].record()
+        e_loss = [E(), E()]
+        if train is not None:
+            e_loss[0].record()
+            for k in range(len(my_cams)):
+                dass.dass_fidelity_loss(raster.img, gts[k], 0.2, mvp.loss_ws[0], mvp.losses[k],
+                                        mvp.loss_dL[0])
+            e_loss[1].record()
         torch.cuda.synchronize()
         ops["project_views"] = e_proj[0].elapsed_time(e_proj[1])
         ops["bin_sort"] = sum(ev[0].elapsed_time(ev[1]) for ev in per)
         ops["render_fwd"] = sum(ev[1].elapsed_time(ev[2]) for ev in per)
         ops["render_bwd_raster"] = sum(ev[2].elapsed_time(ev[3]) for ev in per)
         ops["render_bwd_preprocess_views"] = e_pre[0].elapsed_time(e_pre[1])
+        if train is not None:
+            ops["fidelity_loss"] = e_loss[0].elapsed_time(e_loss[1])
 
     # ---- end-to-end through the public API with host buffers: every step
     # uploads its inputs from pinned host memory and downloads its gradients.
@@ -409,6 +474,7 @@ def run_ours(args):
                             "early_terminated_frac": float(np.sum(allst["terminated_px"]) / (len(allst["K"]) * W * H)),
                             "tile_list_mean": float(np.mean(allst["tile_list_mean"])),
                             "tile_list_max": int(np.max(allst["tile_list_max"]))},
+            "training_step_with_loss": train,
             "gpu_launches": int(launches),
             "clocks": clocks,
             "e2e": e2e,

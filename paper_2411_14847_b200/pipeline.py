@@ -167,7 +167,22 @@ class MultiViewPass:
         self.pre_stream = torch.cuda.Stream(device=device)
         self.g2d = torch.empty(max(self.V, 1), n, 12, dtype=torch.float32, device=device)
 
-    def run(self, scene: DeviceScene, records: ViewRecords, dL_dimgs, grads, keep=None, bg=None):
+    def enable_loss(self, lam: float = 0.2):
+        """Allocate per-slot scratch so run(gts=...) computes dL/dC itself with the
+        fused fidelity loss of Eq. 3 (dass_fidelity_loss) from ground-truth views."""
+        torch = _torch()
+        dev = self.g2d.device
+        W, H = self.cams[0].width, self.cams[0].height
+        self.lam = lam
+        nb = dass.dass_fidelity_loss_workspace(W, H)
+        self.loss_ws = [torch.empty(nb // 4 + 64, dtype=torch.float32, device=dev) for _ in range(self.S)]
+        self.loss_dL = [torch.empty(3, H, W, dtype=torch.float32, device=dev) for _ in range(self.S)]
+        self.losses = torch.zeros(self.V, 3, dtype=torch.float32, device=dev)
+
+    def run(self, scene: DeviceScene, records: ViewRecords, dL_dimgs, grads, keep=None, bg=None,
+            gts=None):
+        """dL_dimgs: fixed per-view ∂L/∂C, or None with gts (per-view ground truth,
+        requires enable_loss): then ∂L/∂C comes from the fidelity loss."""
         torch = _torch()
         main = torch.cuda.current_stream()
         for s in self.streams:
@@ -180,8 +195,14 @@ class MultiViewPass:
                 rec = records.view(v)
                 xy, co, rgb, box, tiles = rec
                 ras.forward(cam, rec, bg=bg)
+                if gts is not None:
+                    dL = self.loss_dL[k]
+                    dass.dass_fidelity_loss(ras.img, gts[v], self.lam, self.loss_ws[k],
+                                            self.losses[v], dL)
+                else:
+                    dL = dL_dimgs[v]
                 dass.dass_render_bwd_raster(cam, self.n, ras.ranges, ras.sorted_ids, xy, co, rgb,
-                                            box, bg, ras.T, ras.last, dL_dimgs[v], self.g2d[v],
+                                            box, bg, ras.T, ras.last, dL, self.g2d[v],
                                             ras.accept, ras.capacity)
             if half and v == half - 1:
                 # the first half's preprocess (HBM-bound) overlaps the second half's
