@@ -459,11 +459,13 @@ def run_ours(args):
                        "cuda_graph": graph is not None, "streams": args.streams,
                        "parallelism": f"view-sharded dp{world}",
                        "l2": "inputs larger than L2 (≈0.5 GB of params, dL/dC and records per step)"},
-            "roofline": {"bound": "alu", "kernel": "render_bwd_raster_kernel (accepted units only)",
+            "roofline": {"bound": "alu", "kernel": "render_bwd_list_kernel<4> via dass_render_bwd_raster (accepted units only)",
                          "achieved": None if achieved is None else round(achieved, 2),
                          "peak": round(peak_tflops, 1), "unit": "TFLOP/s",
                          "frac": None if achieved is None else round(achieved / peak_tflops, 4),
-                         "traffic": None, "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz ({pk_kind} clock)",
+                         "traffic": profiled_traffic("render_bwd"),
+                         "traffic_source": "profiles/r01_ncu_render_bwd.txt (ncu --set full, dram read+write per launch = one view)",
+                         "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz ({pk_kind} clock)",
                          "units_per_step": {"accepted": sum(stats["accepted"]), "P_bwd": sum(stats["P_bwd"])},
                          "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED}},
             "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
@@ -541,6 +543,19 @@ def run_reference(args):
                              "sample": "each step = the shift + fwd+bwd of ONE of the 20 views (bounded sample)"},
             "e2e": {"value": round(value, 4), "unit": "views/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+
+
+def profiled_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary (null if absent)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        f"r01_ncu_{kernel}.txt")
+    try:
+        for line in open(path):
+            if line.startswith("dram_bytes_per_launch:"):
+                return int(line.split()[1])
+    except OSError:
+        pass
+    return None
 
 
 def main():

@@ -363,6 +363,71 @@ int dass_inherit_mask_bwd(int32_t n, const float* m, const float* pos_opa,
                           void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Dual hash-grid deformation (§3.3; supplement §B) —
+ * SURVEY §8(f) f2.  Each field 𝓗 (𝓗_dyn for the dynamic group, 𝓗_st for the
+ * static one) maps a Gaussian position p to (μ, σ):
+ *   enc(p):  per level l < levels with resolution N_l = resolution[l]:
+ *            x̂ = clamp((p − aabb_min)/(aabb_max − aabb_min), 0, 1),
+ *            s = x̂·N_l, i0 = min(⌊s⌋, N_l − 1), w = s − i0 (per axis);
+ *            the 8 corners i0 + c, c ∈ {0,1}³, read table row
+ *              (N_l+1)³ ≤ T:  x + y(N_l+1) + z(N_l+1)²               (dense)
+ *              otherwise:     (x ⊕ y·2654435761 ⊕ z·805459861) mod T (u32)
+ *            weighted Π_k (c_k ? w_k : 1 − w_k); features of the levels
+ *            concatenated (I-NGP; A41).
+ *   MLP:     in = levels·features → 64 → 64 → 7, ReLU hidden, linear head.
+ *   μ = out[0:3], σ = (1, 0, 0, 0) + out[3:7] (a zero head is the identity
+ *   deformation; A42).  Feed μ, σ to dass_apply_shift (q' = n(q) ⊗ n(σ)).
+ * T_Hash / F_Hash per group and dataset: N3DV 2^16/4 (dyn), 2^14/2 (st); Meet
+ * Room 2^15/4, 2^13/2.
+ *
+ * Memory (all device, caller-owned, float32):
+ *   table: [levels][T][features] (16-byte aligned for features = 4, 8 for 2);
+ *   mlp:   flat W1[64][in] b1[64] W2[64][64] b2[64] W3[7][64] b3[7]
+ *          (dass_deform_param_count gives both sizes);
+ *   pos_opa, mu, sigma, g_mu, g_sigma: float4[n_gauss] (16-byte aligned);
+ *     mu.w is written 0; sigma = (w, x, y, z).
+ * Rows: row k < (count ? *count : n) processes Gaussian i = idx ? idx[k] : k
+ * (count is a DEVICE int, so a partition can feed it without a host sync;
+ * n bounds it and sizes the grid).  Rows ≥ the count are untouched.
+ * dass_deform_fwd writes mu[i], sigma[i].  dass_deform_bwd recomputes the
+ * forward and ACCUMULATES (+=) ∂L/∂table into g_table and ∂L/∂mlp into g_mlp
+ * from ∂L/∂μ = g_mu[i].xyz and ∂L/∂σ = g_sigma[i] (float atomics: the
+ * summation order is not deterministic).  ReLU'(0) = 0.
+ * INVALID_ARG: levels ∉ [1, 16], features ∉ {1, 2, 4}, in = levels·features
+ *   not a multiple of 4 or > 64, log2_table ∉ [1, 24], resolution[l] ∉
+ *   [1, 2^20], aabb not finite or max ≤ min, n < 0, a null required pointer
+ *   or a misaligned one.
+ *
+ * dass_partition: the stable split of the Gaussians by the dynamics mask
+ *   (§3.3): idx_dyn = ascending {i : mask[i] ≠ 0}, idx_st = ascending
+ *   {i : mask[i] = 0} (each int32[n]), counts (device int32[2]) = (#dyn, #st).
+ *   ws: dass_partition_workspace bytes (4-byte aligned).  Deterministic.
+ * ------------------------------------------------------------------------- */
+#define DASS_MLP_HIDDEN 64
+typedef struct dass_hashgrid {
+  int32_t levels;          /* L */
+  int32_t log2_table;      /* T = 2^log2_table rows per level (T_Hash) */
+  int32_t features;        /* F_Hash */
+  int32_t reserved;        /* 0 */
+  int32_t resolution[16];  /* N_l, l < levels */
+  float aabb_min[3];
+  float aabb_max[3];
+} dass_hashgrid;
+
+int dass_deform_param_count(const dass_hashgrid* cfg, int64_t* table_floats,
+                            int64_t* mlp_floats);
+int dass_deform_fwd(const dass_hashgrid* cfg, const float* table, const float* mlp,
+                    int32_t n, const int32_t* idx, const int32_t* count,
+                    const float* pos_opa, float* mu, float* sigma, void* stream);
+int dass_deform_bwd(const dass_hashgrid* cfg, const float* table, const float* mlp,
+                    int32_t n, const int32_t* idx, const int32_t* count,
+                    const float* pos_opa, const float* g_mu, const float* g_sigma,
+                    float* g_table, float* g_mlp, void* stream);
+int dass_partition_workspace(int32_t n, size_t* bytes);
+int dass_partition(int32_t n, const uint8_t* mask, int32_t* idx_dyn, int32_t* idx_st,
+                   int32_t* counts, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
  * dass_error_map — error map, binarisation and Alg. 1 (§3.4 P:164-165, P:174;
  * Alg. 1 P:403-415 with the garble fixed, A20-A22).
  *   E(X,Y) = (1/3)·Σ_ch |rendered − gt|  → err (float [H][W], nullable)

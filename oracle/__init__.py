@@ -228,3 +228,45 @@ def fidelity_loss(img, gt, lam=0.2, grad=True):
     g = np.zeros(img.shape) if grad else None
     lib().oracle_fidelity_loss(W, H, _p(img), _p(gt), C.c_double(lam), _p(out), _p(g))
     return out[0], out[1], out[2], g
+
+
+# ---- f2: hash-grid deformation (§3.3, §B; A41-A43) ----
+def _hcfg(field):
+    return np.ascontiguousarray(field.to_struct()).reshape(1)
+
+
+def hash_params(inputs):
+    return lib().oracle_hash_params(int(inputs))
+
+
+def hash_encode(field, pos_opa):
+    """enc(p): double [m][L·F]."""
+    po = _f32(pos_opa)
+    m = po.shape[0]
+    feat = np.zeros((m, field.L * field.F))
+    lib().oracle_hash_encode(_p(_hcfg(field)), _p(_f32(field.table)), m, _p(po), _p(feat))
+    return feat
+
+
+def deform(field, pos_opa):
+    """(μ, σ, tie) for every row of pos_opa: double [m][4] ×2, uint8 [m]."""
+    po = _f32(pos_opa)
+    m = po.shape[0]
+    mu = np.zeros((m, 4)); sg = np.zeros((m, 4)); tie = np.zeros(m, np.uint8)
+    lib().oracle_deform_fwd(_p(_hcfg(field)), _p(_f32(field.table)), _p(_f32(field.mlp)), m,
+                            _p(po), _p(mu), _p(sg), _p(tie))
+    return mu, sg, tie
+
+
+def deform_bwd(field, pos_opa, g_mu, g_sigma, kappa=False):
+    """(∂L/∂table [L][T][F], ∂L/∂mlp flat[, κ_table, κ_mlp]) in double."""
+    po = _f32(pos_opa)
+    m = po.shape[0]
+    gt = np.zeros(field.table.shape); gp = np.zeros(field.mlp.shape)
+    kt = np.zeros(field.table.shape) if kappa else None
+    km = np.zeros(field.mlp.shape) if kappa else None
+    lib().oracle_deform_bwd(_p(_hcfg(field)), _p(_f32(field.table)), _p(_f32(field.mlp)), m,
+                            _p(po), _p(np.ascontiguousarray(g_mu, np.float64)),
+                            _p(np.ascontiguousarray(g_sigma, np.float64)), _p(gt), _p(gp),
+                            _p(kt), _p(km))
+    return (gt, gp, kt, km) if kappa else (gt, gp)

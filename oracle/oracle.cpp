@@ -1284,3 +1284,212 @@ int oracle_error_map(const OCam* cam, const float* rendered, const float* gt, do
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ f2 -----------
+// Dual hash-grid deformation (§3.3; supplement §B).  Each
+// field 𝓗 maps a Gaussian position p_n to (μ_n, σ_n) = MLP(enc(p_n)) through
+// an I-NGP multiresolution hash encoding and a small MLP (A41-A43):
+//   enc: per level l (resolution N_l), x̂ = clamp((p − lo)/(hi − lo), 0, 1),
+//        s = x̂·N_l, i0 = min(⌊s⌋, N_l − 1), w = s − i0; the 8 lattice corners
+//        i0 + c (c ∈ {0,1}³) are read from level l's table row
+//          (N_l+1)³ ≤ T:  x + y(N_l+1) + z(N_l+1)²               (dense)
+//          otherwise:     (x·1 ⊕ y·2654435761 ⊕ z·805459861) mod T   (hash, u32)
+//        and trilinearly weighted, Π_k (c_k ? w_k : 1 − w_k); levels concatenated.
+//   MLP: in = L·F → 64 → 64 → 7, ReLU on the hidden layers, linear head;
+//        params flat: W1[64][in], b1[64], W2[64][64], b2[64], W3[7][64], b3[7].
+//   μ = out[0:3];  σ = (1, 0, 0, 0) + out[3:7]  (zero head = identity, A42).
+// Everything in double from the fp32 inputs.
+struct OHash {
+  int32_t L, log2T, F, pad;
+  int32_t res[16];
+  float lo[3], hi[3];
+};
+
+namespace {
+constexpr int OH = 64;  // hidden width (A41)
+
+uint64_t hash_row(const OHash& c, int l, uint32_t x, uint32_t y, uint32_t z) {
+  const uint64_t T = 1ull << c.log2T;
+  const uint64_t n1 = (uint64_t)c.res[l] + 1;
+  if (n1 * n1 * n1 <= T) return x + y * n1 + z * n1 * n1;
+  const uint32_t h = (x * 1u) ^ (y * 2654435761u) ^ (z * 805459861u);
+  return h & (uint32_t)(T - 1);
+}
+
+// the 8 (row, weight) pairs of level l for position p
+void corners(const OHash& c, int l, const float* p, uint64_t row[8], double wt[8]) {
+  uint32_t i0[3];
+  double w[3];
+  for (int k = 0; k < 3; ++k) {
+    double xh = ((double)p[k] - (double)c.lo[k]) / ((double)c.hi[k] - (double)c.lo[k]);
+    xh = std::min(1.0, std::max(0.0, xh));
+    const double s = xh * c.res[l];
+    const double f = std::min(std::floor(s), (double)(c.res[l] - 1));
+    i0[k] = (uint32_t)f;
+    w[k] = s - f;
+  }
+  for (int cc = 0; cc < 8; ++cc) {
+    const uint32_t bx = cc & 1, by = (cc >> 1) & 1, bz = (cc >> 2) & 1;
+    row[cc] = hash_row(c, l, i0[0] + bx, i0[1] + by, i0[2] + bz);
+    wt[cc] = (bx ? w[0] : 1.0 - w[0]) * (by ? w[1] : 1.0 - w[1]) * (bz ? w[2] : 1.0 - w[2]);
+  }
+}
+
+struct MlpView {
+  const float *W1, *b1, *W2, *b2, *W3, *b3;
+  MlpView(const float* p, int in)
+      : W1(p), b1(p + OH * in), W2(b1 + OH), b2(W2 + OH * OH), W3(b2 + OH), b3(W3 + 7 * OH) {}
+};
+}  // namespace
+
+extern "C" {
+
+int oracle_hash_params(int in) { return OH * in + OH + OH * OH + OH + 7 * OH + 7; }
+
+// enc(p) for m positions: feat double[m][L·F]
+int oracle_hash_encode(const OHash* c, const float* table, int m, const float* pos_opa,
+                       double* feat) {
+  const int L = c->L, F = c->F, in = L * F;
+  const uint64_t T = 1ull << c->log2T;
+  for (int i = 0; i < m; ++i) {
+    for (int l = 0; l < L; ++l) {
+      uint64_t row[8];
+      double wt[8];
+      corners(*c, l, pos_opa + 4 * i, row, wt);
+      for (int f = 0; f < F; ++f) {
+        double acc = 0;
+        for (int cc = 0; cc < 8; ++cc) acc += wt[cc] * (double)table[((uint64_t)l * T + row[cc]) * F + f];
+        feat[(size_t)i * in + l * F + f] = acc;
+      }
+    }
+  }
+  return 0;
+}
+
+// (μ, σ) for m positions.  mu, sigma: double[m][4] (mu.w = 0).  tie (nullable,
+// uint8[m]): some hidden pre-activation within 1e-5·(1 + Σ|terms|) of 0, i.e. a
+// ReLU decision that fp32 rounding may take differently (A43).
+int oracle_deform_fwd(const OHash* c, const float* table, const float* mlp, int m,
+                      const float* pos_opa, double* mu, double* sigma, uint8_t* tie) {
+  const int in = c->L * c->F;
+  const MlpView P(mlp, in);
+  std::vector<double> x(in), h1(OH), h2(OH);
+  for (int i = 0; i < m; ++i) {
+    oracle_hash_encode(c, table, 1, pos_opa + 4 * i, x.data());
+    bool t = false;
+    for (int o = 0; o < OH; ++o) {
+      double z = P.b1[o], k = std::fabs((double)P.b1[o]);
+      for (int j = 0; j < in; ++j) { z += (double)P.W1[o * in + j] * x[j]; k += std::fabs((double)P.W1[o * in + j] * x[j]); }
+      t |= std::fabs(z) < 1e-5 * (1.0 + k);
+      h1[o] = z > 0 ? z : 0.0;
+    }
+    for (int o = 0; o < OH; ++o) {
+      double z = P.b2[o], k = std::fabs((double)P.b2[o]);
+      for (int j = 0; j < OH; ++j) { z += (double)P.W2[o * OH + j] * h1[j]; k += std::fabs((double)P.W2[o * OH + j] * h1[j]); }
+      t |= std::fabs(z) < 1e-5 * (1.0 + k);
+      h2[o] = z > 0 ? z : 0.0;
+    }
+    double out[7];
+    for (int o = 0; o < 7; ++o) {
+      double z = P.b3[o];
+      for (int j = 0; j < OH; ++j) z += (double)P.W3[o * OH + j] * h2[j];
+      out[o] = z;
+    }
+    mu[4 * i + 0] = out[0]; mu[4 * i + 1] = out[1]; mu[4 * i + 2] = out[2]; mu[4 * i + 3] = 0.0;
+    sigma[4 * i + 0] = 1.0 + out[3];
+    sigma[4 * i + 1] = out[4]; sigma[4 * i + 2] = out[5]; sigma[4 * i + 3] = out[6];
+    if (tie) tie[i] = t ? 1 : 0;
+  }
+  return 0;
+}
+
+// Reverse of oracle_deform_fwd for ∂L/∂μ (g_mu[m][4], xyz) and ∂L/∂σ
+// (g_sigma[m][4], wxyz): accumulates (+=) ∂L/∂table (double[L][T][F]) and
+// ∂L/∂params (double, the flat MLP layout).  kt / km (nullable): Σ|term| of
+// the same sums (conditioning, A43).
+int oracle_deform_bwd(const OHash* c, const float* table, const float* mlp, int m,
+                      const float* pos_opa, const double* g_mu, const double* g_sigma,
+                      double* g_table, double* g_mlp, double* kt, double* km) {
+  const int L = c->L, F = c->F, in = L * F;
+  const uint64_t T = 1ull << c->log2T;
+  const MlpView P(mlp, in);
+  double* gW1 = g_mlp;
+  double* gb1 = gW1 + OH * in;
+  double* gW2 = gb1 + OH;
+  double* gb2 = gW2 + OH * OH;
+  double* gW3 = gb2 + OH;
+  double* gb3 = gW3 + 7 * OH;
+  const size_t koff[6] = {0, (size_t)OH * in, (size_t)OH * in + OH, (size_t)OH * in + OH + OH * OH,
+                          (size_t)OH * in + 2 * OH + OH * OH, (size_t)OH * in + 2 * OH + OH * OH + 7 * OH};
+  std::vector<double> x(in), z1(OH), h1(OH), z2(OH), h2(OH), d2(OH), d1(OH), dx(in);
+  for (int i = 0; i < m; ++i) {
+    oracle_hash_encode(c, table, 1, pos_opa + 4 * i, x.data());
+    for (int o = 0; o < OH; ++o) {
+      double z = P.b1[o];
+      for (int j = 0; j < in; ++j) z += (double)P.W1[o * in + j] * x[j];
+      z1[o] = z; h1[o] = z > 0 ? z : 0.0;
+    }
+    for (int o = 0; o < OH; ++o) {
+      double z = P.b2[o];
+      for (int j = 0; j < OH; ++j) z += (double)P.W2[o * OH + j] * h1[j];
+      z2[o] = z; h2[o] = z > 0 ? z : 0.0;
+    }
+    // ∂L/∂out: μ = out[0:3], σ = e_w + out[3:7]
+    const double d3[7] = {g_mu[4 * i], g_mu[4 * i + 1], g_mu[4 * i + 2], g_sigma[4 * i],
+                          g_sigma[4 * i + 1], g_sigma[4 * i + 2], g_sigma[4 * i + 3]};
+    for (int o = 0; o < 7; ++o) {
+      gb3[o] += d3[o];
+      if (km) km[koff[5] + o] += std::fabs(d3[o]);
+      for (int j = 0; j < OH; ++j) {
+        gW3[o * OH + j] += d3[o] * h2[j];
+        if (km) km[koff[4] + o * OH + j] += std::fabs(d3[o] * h2[j]);
+      }
+    }
+    for (int j = 0; j < OH; ++j) {
+      double s = 0;
+      for (int o = 0; o < 7; ++o) s += (double)P.W3[o * OH + j] * d3[o];
+      d2[j] = z2[j] > 0 ? s : 0.0;
+    }
+    for (int o = 0; o < OH; ++o) {
+      gb2[o] += d2[o];
+      if (km) km[koff[3] + o] += std::fabs(d2[o]);
+      for (int j = 0; j < OH; ++j) {
+        gW2[o * OH + j] += d2[o] * h1[j];
+        if (km) km[koff[2] + o * OH + j] += std::fabs(d2[o] * h1[j]);
+      }
+    }
+    for (int j = 0; j < OH; ++j) {
+      double s = 0;
+      for (int o = 0; o < OH; ++o) s += (double)P.W2[o * OH + j] * d2[o];
+      d1[j] = z1[j] > 0 ? s : 0.0;
+    }
+    for (int o = 0; o < OH; ++o) {
+      gb1[o] += d1[o];
+      if (km) km[koff[1] + o] += std::fabs(d1[o]);
+      for (int j = 0; j < in; ++j) {
+        gW1[o * in + j] += d1[o] * x[j];
+        if (km) km[koff[0] + o * in + j] += std::fabs(d1[o] * x[j]);
+      }
+    }
+    for (int j = 0; j < in; ++j) {
+      double s = 0;
+      for (int o = 0; o < OH; ++o) s += (double)P.W1[o * in + j] * d1[o];
+      dx[j] = s;
+    }
+    // enc is linear in the table: ∂feat_{l,f}/∂table[l][row_c][f] = wt_c
+    for (int l = 0; l < L; ++l) {
+      uint64_t row[8];
+      double wt[8];
+      corners(*c, l, pos_opa + 4 * i, row, wt);
+      for (int cc = 0; cc < 8; ++cc)
+        for (int f = 0; f < F; ++f) {
+          const size_t e = ((uint64_t)l * T + row[cc]) * F + f;
+          g_table[e] += wt[cc] * dx[l * F + f];
+          if (kt) kt[e] += std::fabs(wt[cc] * dx[l * F + f]);
+        }
+    }
+  }
+  return 0;
+}
+
+}  // extern "C"

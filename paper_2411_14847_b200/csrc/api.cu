@@ -57,6 +57,37 @@ static CamParams to_params(const dass_camera* c) {
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+static int to_hashgrid(const dass_hashgrid* c, HashGridParams* g) {
+  if (!c) return fail(DASS_ERR_INVALID_ARG, "hash-grid config is null%s");
+  if (c->levels < 1 || c->levels > 16) return fail(DASS_ERR_INVALID_ARG, "levels must be in [1, 16]%s");
+  if (c->features != 1 && c->features != 2 && c->features != 4)
+    return fail(DASS_ERR_INVALID_ARG, "features must be 1, 2 or 4%s");
+  const int in = c->levels * c->features;
+  if (in % 4 != 0 || in > 64)
+    return fail(DASS_ERR_INVALID_ARG, "levels*features must be a multiple of 4 and <= 64%s");
+  if (c->log2_table < 1 || c->log2_table > 24)
+    return fail(DASS_ERR_INVALID_ARG, "log2_table must be in [1, 24]%s");
+  g->L = c->levels; g->F = c->features; g->in = in;
+  g->T = 1u << c->log2_table; g->Tmask = g->T - 1u;
+  g->dense_mask = 0;
+  for (int l = 0; l < 16; ++l) g->res[l] = 1;
+  for (int l = 0; l < c->levels; ++l) {
+    const int N = c->resolution[l];
+    if (N < 1 || N > (1 << 20)) return fail(DASS_ERR_INVALID_ARG, "resolution[l] must be in [1, 2^20]%s");
+    g->res[l] = N;
+    const uint64_t n1 = (uint64_t)N + 1;
+    if (n1 * n1 * n1 <= (uint64_t)g->T) g->dense_mask |= 1u << l;
+  }
+  for (int k = 0; k < 3; ++k) {
+    if (!std::isfinite(c->aabb_min[k]) || !std::isfinite(c->aabb_max[k]) ||
+        !(c->aabb_max[k] > c->aabb_min[k]))
+      return fail(DASS_ERR_INVALID_ARG, "aabb must be finite with max > min%s");
+    g->lo[k] = c->aabb_min[k];
+    g->span[k] = c->aabb_max[k] - c->aabb_min[k];
+  }
+  return DASS_OK;
+}
+
 }  // namespace dass
 
 using namespace dass;
@@ -362,6 +393,79 @@ int dass_inherit_mask_bwd(int32_t n, const float* m, const float* pos_opa, const
                                              (const float4*)g_pos_opa, (const float4*)g_scale,
                                              lambda_inher, g_m, (cudaStream_t)stream),
                      "dass_inherit_mask_bwd");
+}
+
+int dass_deform_param_count(const dass_hashgrid* cfg, int64_t* table_floats, int64_t* mlp_floats) {
+  HashGridParams g;
+  const int st = to_hashgrid(cfg, &g);
+  if (st) return st;
+  const int64_t H = DASS_MLP_HIDDEN;
+  if (table_floats) *table_floats = (int64_t)g.L * g.T * g.F;
+  if (mlp_floats) *mlp_floats = H * g.in + H + H * H + H + 7 * H + 7;
+  return DASS_OK;
+}
+
+static int check_table_align(const HashGridParams& g, const void* p) {
+  const uintptr_t a = (uintptr_t)p;
+  if ((g.F == 4 && (a & 15u)) || (g.F == 2 && (a & 7u)) || (a & 3u))
+    return fail(DASS_ERR_INVALID_ARG, "table pointer misaligned for its feature width%s");
+  return DASS_OK;
+}
+
+int dass_deform_fwd(const dass_hashgrid* cfg, const float* table, const float* mlp, int32_t n,
+                    const int32_t* idx, const int32_t* count, const float* pos_opa, float* mu,
+                    float* sigma, void* stream) {
+  HashGridParams g;
+  int st = to_hashgrid(cfg, &g);
+  if (st) return st;
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (n == 0) return DASS_OK;
+  if (!table || !mlp || !pos_opa || !mu || !sigma)
+    return fail(DASS_ERR_INVALID_ARG, "dass_deform_fwd: null required pointer%s");
+  if ((st = check_table_align(g, table))) return st;
+  if (!aligned16(pos_opa) || !aligned16(mu) || !aligned16(sigma))
+    return fail(DASS_ERR_INVALID_ARG, "dass_deform_fwd: float4 arrays must be 16-byte aligned%s");
+  return cuda_status(launch_deform_fwd(g, table, mlp, n, idx, count, (const float4*)pos_opa,
+                                       (float4*)mu, (float4*)sigma, (cudaStream_t)stream),
+                     "dass_deform_fwd");
+}
+
+int dass_deform_bwd(const dass_hashgrid* cfg, const float* table, const float* mlp, int32_t n,
+                    const int32_t* idx, const int32_t* count, const float* pos_opa,
+                    const float* g_mu, const float* g_sigma, float* g_table, float* g_mlp,
+                    void* stream) {
+  HashGridParams g;
+  int st = to_hashgrid(cfg, &g);
+  if (st) return st;
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (n == 0) return DASS_OK;
+  if (!table || !mlp || !pos_opa || !g_mu || !g_sigma || !g_table || !g_mlp)
+    return fail(DASS_ERR_INVALID_ARG, "dass_deform_bwd: null required pointer%s");
+  if ((st = check_table_align(g, table)) || (st = check_table_align(g, g_table))) return st;
+  if (!aligned16(pos_opa) || !aligned16(g_mu) || !aligned16(g_sigma))
+    return fail(DASS_ERR_INVALID_ARG, "dass_deform_bwd: float4 arrays must be 16-byte aligned%s");
+  return cuda_status(launch_deform_bwd(g, table, mlp, n, idx, count, (const float4*)pos_opa,
+                                       (const float4*)g_mu, (const float4*)g_sigma, g_table,
+                                       g_mlp, (cudaStream_t)stream),
+                     "dass_deform_bwd");
+}
+
+int dass_partition_workspace(int32_t n, size_t* bytes) {
+  if (n < 0 || !bytes) return fail(DASS_ERR_INVALID_ARG, "n < 0 or bytes is null%s");
+  *bytes = partition_workspace(n);
+  return DASS_OK;
+}
+
+int dass_partition(int32_t n, const uint8_t* mask, int32_t* idx_dyn, int32_t* idx_st,
+                   int32_t* counts, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (!mask && n > 0) return fail(DASS_ERR_INVALID_ARG, "dass_partition: mask is null%s");
+  if (!idx_dyn || !idx_st || !counts)
+    return fail(DASS_ERR_INVALID_ARG, "dass_partition: null required pointer%s");
+  if (!ws || ws_bytes < partition_workspace(n) || ((uintptr_t)ws & 3u))
+    return fail(DASS_ERR_INVALID_ARG, "dass_partition: workspace too small or misaligned%s");
+  return cuda_status(launch_partition(n, mask, idx_dyn, idx_st, counts, ws, (cudaStream_t)stream),
+                     "dass_partition");
 }
 
 int dass_error_map(const dass_camera* cam, const float* rendered, const float* gt, float gamma_err,

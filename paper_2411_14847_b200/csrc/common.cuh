@@ -82,6 +82,15 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
 
 __host__ __device__ __forceinline__ int div_up(int a, int b) { return (a + b - 1) / b; }
 
+// Kernel-side copy of dass_hashgrid (f2), passed by value (__grid_constant__).
+struct HashGridParams {
+  int L, F, in;          // levels, features per entry, MLP inputs = L·F
+  uint32_t T, Tmask;     // table rows per level (2^log2_table), T − 1
+  uint32_t dense_mask;   // bit l: (res_l + 1)³ ≤ T → direct indexing
+  int res[16];
+  float lo[3], span[3];  // AABB min and (max − min)
+};
+
 }  // namespace dass
 
 // Internal launchers (defined in the .cu files, called by api.cu).
@@ -138,6 +147,16 @@ cudaError_t launch_inherit_mask_bwd(int n, const float* m, const float4* pos_opa
                                     const float4* scale, const float4* g_pos_opa,
                                     const float4* g_scale, float lambda_inher, float* g_m,
                                     cudaStream_t s);
+size_t partition_workspace(int n);
+cudaError_t launch_partition(int n, const uint8_t* mask, int* idx_dyn, int* idx_st, int* counts,
+                             void* ws, cudaStream_t s);
+cudaError_t launch_deform_fwd(const HashGridParams& g, const float* table, const float* mlp, int n,
+                              const int* idx, const int* count, const float4* pos_opa, float4* mu,
+                              float4* sigma, cudaStream_t s);
+cudaError_t launch_deform_bwd(const HashGridParams& g, const float* table, const float* mlp, int n,
+                              const int* idx, const int* count, const float4* pos_opa,
+                              const float4* g_mu, const float4* g_sigma, float* g_table,
+                              float* g_mlp, cudaStream_t s);
 cudaError_t launch_error_map(const CamParams& cam, const float* rendered, const float* gt,
                              float gamma, float* err, uint32_t* dmask, int n_base,
                              const float4* pos_opa, uint8_t* s_err, cudaStream_t s);

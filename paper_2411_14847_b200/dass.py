@@ -31,6 +31,8 @@ EXPORTS = (
     "dass_render_bwd", "dass_render_bwd_raster", "dass_render_bwd_preprocess_views",
     "dass_fidelity_loss_workspace", "dass_fidelity_loss", "dass_inherit_mask",
     "dass_inherit_mask_bwd", "dass_error_map", "dass_render_stats",
+    "dass_deform_param_count", "dass_deform_fwd", "dass_deform_bwd", "dass_partition_workspace",
+    "dass_partition",
 )
 
 
@@ -59,6 +61,26 @@ def camera_struct(cam) -> dass_camera:
     fp = np.asarray(cam.full_proj, np.float32).reshape(16)
     for i in range(16):
         c.full_proj[i] = float(fp[i])
+    return c
+
+
+class dass_hashgrid(C.Structure):
+    _fields_ = [("levels", C.c_int32), ("log2_table", C.c_int32), ("features", C.c_int32),
+                ("reserved", C.c_int32), ("resolution", C.c_int32 * 16),
+                ("aabb_min", C.c_float * 3), ("aabb_max", C.c_float * 3)]
+
+
+def hashgrid_struct(field) -> dass_hashgrid:
+    """From any object with L / log2T / F / res / lo / hi (synth.HashField)."""
+    if isinstance(field, dass_hashgrid):
+        return field
+    c = dass_hashgrid()
+    c.levels, c.log2_table, c.features = int(field.L), int(field.log2T), int(field.F)
+    for i, r in enumerate(field.res):
+        c.resolution[i] = int(r)
+    for k in range(3):
+        c.aabb_min[k] = float(field.lo[k])
+        c.aabb_max[k] = float(field.hi[k])
     return c
 
 
@@ -97,6 +119,11 @@ def lib():
         L.dass_inherit_mask_bwd.argtypes = [i32, P, P, P, P, P, C.c_float, P, P]
         L.dass_error_map.argtypes = [P, P, P, C.c_float, P, P, i32, P, P, P]
         L.dass_render_stats.argtypes = [P, P, P, P, P, P, P, P, P, P]
+        L.dass_deform_param_count.argtypes = [P, P, P]
+        L.dass_deform_fwd.argtypes = [P, P, P, i32, P, P, P, P, P, P]
+        L.dass_deform_bwd.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
+        L.dass_partition_workspace.argtypes = [i32, P]
+        L.dass_partition.argtypes = [i32, P, P, P, P, P, C.c_size_t, P]
         _lib = L
     return _lib
 
@@ -290,3 +317,45 @@ def dass_render_stats(cam, tile_ranges, sorted_ids, xy_depth, conic_opa, box, ou
                                    _ptr(xy_depth), _ptr(conic_opa), _ptr(box), _ptr(out_T),
                                    _ptr(out_last), _ptr(counters), _stream(stream)),
            "dass_render_stats")
+
+
+def dass_deform_param_count(field):
+    """(table floats, mlp floats) of a hash-grid field."""
+    t, m = C.c_int64(0), C.c_int64(0)
+    _check(lib().dass_deform_param_count(C.byref(hashgrid_struct(field)), C.byref(t), C.byref(m)),
+           "dass_deform_param_count")
+    return t.value, m.value
+
+
+def dass_deform_fwd(field, table, mlp, pos_opa, mu, sigma, idx=None, count=None, n=None,
+                    stream=None):
+    """f2: (μ, σ) = 𝓗(p) for rows idx[k], k < *count (device) or n."""
+    if n is None:
+        n = idx.shape[0] if idx is not None else pos_opa.shape[0]
+    _check(lib().dass_deform_fwd(C.byref(hashgrid_struct(field)), _ptr(table), _ptr(mlp), int(n),
+                                 _ptr(idx), _ptr(count), _ptr(pos_opa), _ptr(mu), _ptr(sigma),
+                                 _stream(stream)), "dass_deform_fwd")
+
+
+def dass_deform_bwd(field, table, mlp, pos_opa, g_mu, g_sigma, g_table, g_mlp, idx=None,
+                    count=None, n=None, stream=None):
+    """f2: g_table, g_mlp += ∂L/∂(table, mlp) from ∂L/∂μ, ∂L/∂σ."""
+    if n is None:
+        n = idx.shape[0] if idx is not None else pos_opa.shape[0]
+    _check(lib().dass_deform_bwd(C.byref(hashgrid_struct(field)), _ptr(table), _ptr(mlp), int(n),
+                                 _ptr(idx), _ptr(count), _ptr(pos_opa), _ptr(g_mu), _ptr(g_sigma),
+                                 _ptr(g_table), _ptr(g_mlp), _stream(stream)), "dass_deform_bwd")
+
+
+def dass_partition_workspace(n) -> int:
+    out = C.c_size_t(0)
+    _check(lib().dass_partition_workspace(int(n), C.byref(out)), "dass_partition_workspace")
+    return out.value
+
+
+def dass_partition(mask, idx_dyn, idx_st, counts, ws, stream=None):
+    """Stable split of range(n) by mask ≠ 0 (device counts[2] = #dyn, #st)."""
+    n = mask.shape[0]
+    _check(lib().dass_partition(n, _ptr(mask), _ptr(idx_dyn), _ptr(idx_st), _ptr(counts), _ptr(ws),
+                                ws.numel() * ws.element_size(), _stream(stream)),
+           "dass_partition")

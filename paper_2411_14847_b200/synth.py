@@ -318,3 +318,96 @@ def c5(n: int = 1_000_000):
     cams = n3dv_rig(seed=3)
     return cams, n3dv_scene(n=n, seed=5, degree=3, fx=cams[0].fx,
                             sigma_median=2.5 * math.sqrt(0.3))
+
+
+# ---- f2: hash-grid deformation fields (configuration + seeded parameters) ----
+# The paper fixes only T_Hash and F_Hash per group and dataset; the
+# rest is the I-NGP-style configuration of reading A41: L = 8 levels,
+# geometric resolutions from 16 to 256 (listed, not computed), MLP 64-64.
+HASHGRID_DTYPE = np.dtype([
+    ("L", np.int32), ("log2T", np.int32), ("F", np.int32), ("pad", np.int32),
+    ("res", np.int32, (16,)), ("lo", np.float32, (3,)), ("hi", np.float32, (3,)),
+])
+HASH_LEVEL_RES = (16, 23, 35, 52, 78, 115, 172, 256)   # ⌊16·16^(l/7)⌋, l = 0..7
+HASH_PROFILES = {                                          # (log2 T, F): dyn, static
+    "n3dv": ((16, 4), (14, 2)),
+    "meetroom": ((15, 4), (13, 2)),
+}
+MLP_HIDDEN = 64
+
+
+@dataclass
+class HashField:
+    L: int
+    log2T: int
+    F: int
+    res: tuple
+    lo: np.ndarray
+    hi: np.ndarray
+    table: np.ndarray      # float32 [L][T][F]
+    mlp: np.ndarray        # float32 flat: W1[64][L·F] b1[64] W2[64][64] b2[64] W3[7][64] b3[7]
+
+    @property
+    def inputs(self) -> int:
+        return self.L * self.F
+
+    def to_struct(self) -> np.ndarray:
+        s = np.zeros((), HASHGRID_DTYPE)
+        s["L"], s["log2T"], s["F"] = self.L, self.log2T, self.F
+        s["res"][:self.L] = self.res
+        s["lo"], s["hi"] = self.lo, self.hi
+        return s
+
+
+def mlp_param_count(inputs: int, hidden: int = MLP_HIDDEN) -> int:
+    return hidden * inputs + hidden + hidden * hidden + hidden + 7 * hidden + 7
+
+
+def scene_aabb(pos: np.ndarray, pad: float = 0.1):
+    """Input box of the fields: the positions' bounds padded by 10% of the span."""
+    lo, hi = pos[:, :3].min(0), pos[:, :3].max(0)
+    span = np.maximum(hi - lo, 1e-6)
+    return (lo - pad * span).astype(np.float32), (hi + pad * span).astype(np.float32)
+
+
+def hash_field(log2T: int, F: int, aabb, seed: int, levels: int = 8, trained: bool = True,
+               res=HASH_LEVEL_RES, table_scale: float = 0.5, head_scale: float = 0.02) -> HashField:
+    """Seeded field parameters.  trained=False is the initial state (table
+    U(±1e-4), zero head → identity deformation); trained=True draws a table
+    U(±table_scale) and a head of scale head_scale (μ of order 1e-2, Fig. 3)."""
+    g = rng(seed)
+    T = 1 << log2T
+    inn = levels * F
+    ts = table_scale if trained else 1e-4
+    table = g.uniform(-ts, ts, size=(levels, T, F)).astype(np.float32)
+    H = MLP_HIDDEN
+    W1 = g.normal(size=(H, inn)) * np.sqrt(2.0 / inn)
+    b1 = g.normal(size=H) * 0.05
+    W2 = g.normal(size=(H, H)) * np.sqrt(2.0 / H)
+    b2 = g.normal(size=H) * 0.05
+    if trained:
+        W3 = g.normal(size=(7, H)) * head_scale / np.sqrt(H)
+        b3 = g.normal(size=7) * head_scale * 0.1
+    else:
+        W3 = np.zeros((7, H)); b3 = np.zeros(7)
+    mlp = np.concatenate([W1.ravel(), b1, W2.ravel(), b2, W3.ravel(), b3]).astype(np.float32)
+    lo, hi = aabb
+    return HashField(levels, log2T, F, tuple(res[:levels]), np.asarray(lo, np.float32),
+                     np.asarray(hi, np.float32), table, mlp)
+
+
+def dual_fields(scene: Scene, profile: str = "n3dv", seed: int = 40, trained: bool = True):
+    """(𝓗_dyn, 𝓗_st) for a scene."""
+    (tdyn, fdyn), (tst, fst) = HASH_PROFILES[profile]
+    box = scene_aabb(scene.pos_opa)
+    return (hash_field(tdyn, fdyn, box, seed, trained=trained),
+            hash_field(tst, fst, box, seed + 1, trained=trained))
+
+
+def offset_grads(n: int, seed: int, scale: float = 1.0):
+    """Fixed ∂L/∂μ, ∂L/∂σ (float32 [n][4]) for deformation-backward tests."""
+    g = rng(seed)
+    gm = g.normal(size=(n, 4)).astype(np.float32) * scale
+    gm[:, 3] = 0
+    gs = (g.normal(size=(n, 4)) * scale).astype(np.float32)
+    return gm, gs
