@@ -125,7 +125,8 @@ def run_ours(args):
 
     from paper_2411_14847_b200 import dass, synth
     from paper_2411_14847_b200.dist import FlatGrads, allreduce_grads, shard
-    from paper_2411_14847_b200.pipeline import DeviceScene, MultiViewPass, Raster, ViewRecords
+    from paper_2411_14847_b200.pipeline import (DeformFields, DeviceScene, MultiViewPass, Raster,
+                                                ViewRecords)
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -256,16 +257,26 @@ def run_ours(args):
             raster.forward(cam, records.view(k))
             gts[k].copy_(raster.img)
 
+        # the dual deformation fields (f2) emit (μ, σ) for every Gaussian:
+        # 𝓗_dyn for the dynamic group, 𝓗_st for the static one
+        fields = DeformFields(synth.dual_fields(scene, "n3dv", seed=40), n, dev)
+        fields.partition(base.dynamic)
+        mu_f = torch.empty(n, 4, device=dev)
+        sigma_f = torch.empty(n, 4, device=dev)
+
         def train_local():
             grads.zero_()
-            dass.dass_apply_shift(base.pos_opa, base.rot, mu_d, sigma_d, base.dynamic,
+            fields.zero_grad()
+            fields.forward(base.pos_opa, mu_f, sigma_f)
+            dass.dass_apply_shift(base.pos_opa, base.rot, mu_f, sigma_f, None,
                                   shifted.pos_opa, shifted.rot)
             dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
                                     shifted.sh, None, records.xy_depth, records.conic_opa,
                                     records.rgb, records.box, records.tiles)
             mvp.run(shifted, records, None, grads, gts=gts)
-            dass.dass_apply_shift_bwd(base.rot, sigma_d, base.dynamic, grads.pos_opa, grads.rot,
+            dass.dass_apply_shift_bwd(base.rot, sigma_f, None, grads.pos_opa, grads.rot,
                                       g_mu, g_sigma)
+            fields.backward(base.pos_opa, g_mu, g_sigma)
 
         for _ in range(2):
             train_local()
@@ -287,6 +298,8 @@ def run_ours(args):
                 tgraph.replay()
             if world > 1:
                 allreduce_grads(grads)
+                for x in fields.grad_tensors():
+                    dist.all_reduce(x)
         t1.record()
         barrier()
         tms = torch.tensor([t0.elapsed_time(t1) / nt], device=dev)
@@ -295,7 +308,7 @@ def run_ours(args):
         train = {"value": round(len(cams) / (float(tms.item()) / 1e3), 3), "unit": "views/s",
                  "ms_per_step": round(float(tms.item()), 4),
                  "loss_mean": float(mvp.losses[:, 0].mean().item()),
-                 "what": "shift + fwd + fused L1/D-SSIM loss (Eq. 3) + bwd over the views",
+                 "what": "one full shift-stage iteration (§3.3): dual hash-grid deformation fwd (f2) → shift → fwd + fused L1/D-SSIM loss (Eq. 3, f1) + bwd over the views → shift bwd → deformation bwd (table + MLP grads)",
                  "graph": tgraph is not None}
 
     # ---- per-op breakdown: one extra SEQUENTIAL step, CUDA events on the
@@ -340,6 +353,13 @@ def run_ours(args):
                 dass.dass_fidelity_loss(raster.img, gts[k], 0.2, mvp.loss_ws[0], mvp.losses[k],
                                         mvp.loss_dL[0])
             e_loss[1].record()
+        e_def = [E(), E(), E()]
+        if train is not None:
+            e_def[0].record()
+            fields.forward(base.pos_opa, mu_f, sigma_f)
+            e_def[1].record()
+            fields.backward(base.pos_opa, g_mu, g_sigma)
+            e_def[2].record()
         torch.cuda.synchronize()
         ops["project_views"] = e_proj[0].elapsed_time(e_proj[1])
         ops["bin_sort"] = sum(ev[0].elapsed_time(ev[1]) for ev in per)
@@ -348,6 +368,8 @@ def run_ours(args):
         ops["render_bwd_preprocess_views"] = e_pre[0].elapsed_time(e_pre[1])
         if train is not None:
             ops["fidelity_loss"] = e_loss[0].elapsed_time(e_loss[1])
+            ops["deform_fwd"] = e_def[0].elapsed_time(e_def[1])
+            ops["deform_bwd"] = e_def[1].elapsed_time(e_def[2])
 
     # ---- end-to-end through the public API with host buffers: every step
     # uploads its inputs from pinned host memory and downloads its gradients.

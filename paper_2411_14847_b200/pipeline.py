@@ -224,3 +224,43 @@ class MultiViewPass:
             keep, records.conic_opa[v0:v1], records.rgb[v0:v1], records.box[v0:v1],
             self.g2d[v0:v1], grads.pos_opa, grads.scale, grads.rot, grads.sh,
             grads.gradstat_sum, grads.gradstat_cnt)
+
+
+class DeformFields:
+    """The dual deformation fields 𝓗_dyn / 𝓗_st (§3.3, f2) on the device: tables,
+    MLPs, their gradients and the dynamic/static partition of the Gaussians."""
+
+    def __init__(self, fields, n: int, device="cuda"):
+        torch = _torch()
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        self.cfg = list(fields)                      # (𝓗_dyn, 𝓗_st) synth.HashField-like
+        self.table = [t(f.table) for f in self.cfg]
+        self.mlp = [t(f.mlp) for f in self.cfg]
+        self.g_table = [torch.zeros_like(x) for x in self.table]
+        self.g_mlp = [torch.zeros_like(x) for x in self.mlp]
+        self.n = n
+        self.idx = [torch.empty(max(n, 1), dtype=torch.int32, device=device) for _ in range(2)]
+        self.counts = torch.zeros(2, dtype=torch.int32, device=device)
+        nb = dass.dass_partition_workspace(n)
+        self.part_ws = torch.empty(nb // 4 + 1, dtype=torch.int32, device=device)
+
+    def partition(self, dyn_mask):
+        dass.dass_partition(dyn_mask, self.idx[0], self.idx[1], self.counts, self.part_ws)
+
+    def zero_grad(self):
+        for x in self.g_table + self.g_mlp:
+            x.zero_()
+
+    def forward(self, pos_opa, mu, sigma):
+        for k in range(2):
+            dass.dass_deform_fwd(self.cfg[k], self.table[k], self.mlp[k], pos_opa, mu, sigma,
+                                 idx=self.idx[k], count=self.counts[k:k + 1], n=self.n)
+
+    def backward(self, pos_opa, g_mu, g_sigma):
+        for k in range(2):
+            dass.dass_deform_bwd(self.cfg[k], self.table[k], self.mlp[k], pos_opa, g_mu, g_sigma,
+                                 self.g_table[k], self.g_mlp[k], idx=self.idx[k],
+                                 count=self.counts[k:k + 1], n=self.n)
+
+    def grad_tensors(self):
+        return self.g_table + self.g_mlp
