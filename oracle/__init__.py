@@ -270,3 +270,48 @@ def deform_bwd(field, pos_opa, g_mu, g_sigma, kappa=False):
                             _p(np.ascontiguousarray(g_sigma, np.float64)), _p(gt), _p(gp),
                             _p(kt), _p(km))
     return (gt, gp, kt, km) if kappa else (gt, gp)
+
+
+# ---- f4: error-guided densification + identity-feature render (A44-A47) ----
+def densify_select(gsum, gcnt, s_err, tau_pos, tau_err):
+    """Eq. 4: in_S uint8[n] and |S| (decisions in fp32, A44)."""
+    gsum = _f32(gsum)
+    n = gsum.shape[0]
+    gcnt = np.ascontiguousarray(gcnt, np.uint32)
+    se = None if s_err is None else np.ascontiguousarray(s_err, np.uint8)
+    out = np.zeros(n, np.uint8)
+    c = lib().oracle_densify_select(n, _p(gsum), _p(gcnt), _p(se), C.c_float(tau_pos),
+                                    C.c_float(tau_err), _p(out))
+    return out, c
+
+
+def philox4x64(ctr, key):
+    c = np.ascontiguousarray(ctr, np.uint64); k = np.ascontiguousarray(key, np.uint64)
+    out = np.zeros(4, np.uint64)
+    lib().oracle_philox4x64(_p(c), _p(k), _p(out))
+    return out
+
+
+def spawn(idx, K, shrink, child_opacity, seed, pos_opa, scale, rot, want_z=False):
+    """Spawn densification (A45): child (pos_opa, scale) double [m·K][4] (+ z)."""
+    idx = np.ascontiguousarray(idx, np.int32)
+    m = idx.shape[0]
+    po = np.zeros((m * K, 4)); sc = np.zeros((m * K, 4))
+    z = np.zeros((m * K, 3)) if want_z else None
+    lib().oracle_spawn(m, _p(idx), int(K), C.c_double(shrink), C.c_double(child_opacity),
+                       C.c_uint64(seed), _p(_f32(pos_opa)), _p(_f32(scale)), _p(_f32(rot)),
+                       _p(po), _p(sc), _p(z))
+    return (po, sc, z) if want_z else (po, sc)
+
+
+def render_features(cam, scene, feat, keep=None):
+    """Eq. 9: M double [C][H][W] and tie flags uint8 [H][W]."""
+    feat = _f32(feat)
+    Cn = feat.shape[1]
+    out = np.zeros((Cn, cam.height, cam.width))
+    tie = np.zeros((cam.height, cam.width), np.uint8)
+    k = None if keep is None else np.ascontiguousarray(keep, np.uint8)
+    lib().oracle_render_features(_p(_cam(cam)), scene.n, _p(_f32(scene.pos_opa)),
+                                 _p(_f32(scene.scale)), _p(_f32(scene.rot)), _p(k), Cn, _p(feat),
+                                 _p(out), _p(tie))
+    return out, tie

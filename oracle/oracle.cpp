@@ -1493,3 +1493,139 @@ int oracle_deform_bwd(const OHash* c, const float* table, const float* mlp, int 
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ f4 -----------
+// Error-guided densification (§3.4) and the identity-feature
+// render of Gaussian Grouping (Eq. 9, §A.2).  A44-A47.
+extern "C" {
+
+// Eq. 4, literal set evaluation: S = {n : ∇p̄_n > τ_pos} ∪
+// (S_err ∩ {n : ∇p̄_n > τ_err}), ∇p̄_n = gradstat_sum_n / gradstat_cnt_n (0 when
+// never counted).  The threshold decisions are taken in fp32, the kernel's
+// precision (A44): ∇p̄ is one IEEE fp32 division of the fp32 inputs.
+// in_S uint8[n] (written).  Returns |S|.
+int oracle_densify_select(int n, const float* gsum, const uint32_t* gcnt, const uint8_t* s_err,
+                          float tau_pos, float tau_err, uint8_t* in_S) {
+  int count = 0;
+  for (int i = 0; i < n; ++i) {
+    const float g = gcnt[i] ? gsum[i] / (float)gcnt[i] : 0.0f;
+    const bool a = g > tau_pos;                          // {∇p̄ > τ_pos}
+    const bool b = s_err && s_err[i] && g > tau_err;     // S_err ∩ {∇p̄ > τ_err}
+    in_S[i] = (a || b) ? 1 : 0;
+    count += in_S[i];
+  }
+  return count;
+}
+
+// Philox4x64-10 (Salmon et al., SC'11): the counter-based generator both
+// sides implement for the spawn samples (A45).  out = Philox(ctr, key).
+void oracle_philox4x64(const uint64_t ctr[4], const uint64_t key[2], uint64_t out[4]) {
+  uint64_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    const unsigned __int128 p0 = (unsigned __int128)c0 * 0xD2E7470EE14C6C93ull;
+    const unsigned __int128 p1 = (unsigned __int128)c2 * 0xCA5A826395121157ull;
+    const uint64_t hi0 = (uint64_t)(p0 >> 64), lo0 = (uint64_t)p0;
+    const uint64_t hi1 = (uint64_t)(p1 >> 64), lo1 = (uint64_t)p1;
+    const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B97F4A7C15ull;
+    k1 += 0xBB67AE8584CAA73Bull;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+// Spawn densification (A45): for the k-th selected parent i = idx[k]
+// and child j < K, draw z ~ N(0, I₃) from Philox(ctr = (k·K + j, 0, 0, 0),
+// key = (seed, 0x44415353)) via Box-Muller on u = ((x >> 40) + ½)·2⁻²⁴ and
+// place the child at p + R(n(q))·(s ∘ z), i.e. a sample of N(p, Σ) with
+// Σ = R S Sᵀ Rᵀ (Eq. 6); scale s/shrink, opacity child_opacity,
+// rotation, SH and dynamic flag copied.  Outputs (double): child_pos_opa
+// [m·K][4], child_scale [m·K][4]; z (nullable) [m·K][3].
+int oracle_spawn(int m, const int32_t* idx, int K, double shrink, double child_opacity,
+                 uint64_t seed, const float* pos_opa, const float* scale, const float* rot,
+                 double* child_pos_opa, double* child_scale, double* zout) {
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int k = 0; k < m; ++k) {
+    const int i = idx[k];
+    double q[4];
+    for (int a = 0; a < 4; ++a) q[a] = rot[4 * i + a];
+    const double nq = norm4(q);
+    for (int a = 0; a < 4; ++a) q[a] /= nq;
+    const double w = q[0], x = q[1], y = q[2], z = q[3];
+    const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                            {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                            {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+    for (int j = 0; j < K; ++j) {
+      const uint64_t ctr[4] = {(uint64_t)k * (uint64_t)K + (uint64_t)j, 0, 0, 0};
+      const uint64_t key[2] = {seed, 0x44415353ull};
+      uint64_t r[4];
+      oracle_philox4x64(ctr, key, r);
+      double u[4];
+      for (int a = 0; a < 4; ++a) u[a] = ((double)(r[a] >> 40) + 0.5) * (1.0 / 16777216.0);
+      const double r0 = std::sqrt(-2.0 * std::log(u[0])), r1 = std::sqrt(-2.0 * std::log(u[2]));
+      const double zz[3] = {r0 * std::cos(two_pi * u[1]), r0 * std::sin(two_pi * u[1]),
+                            r1 * std::cos(two_pi * u[3])};
+      const size_t c = (size_t)k * K + j;
+      for (int a = 0; a < 3; ++a) {
+        double off = 0;
+        for (int b = 0; b < 3; ++b) off += R[a][b] * (double)scale[4 * i + b] * zz[b];
+        child_pos_opa[4 * c + a] = (double)pos_opa[4 * i + a] + off;
+        child_scale[4 * c + a] = (double)scale[4 * i + a] / shrink;
+        if (zout) zout[3 * c + a] = zz[a];
+      }
+      child_pos_opa[4 * c + 3] = child_opacity;
+      child_scale[4 * c + 3] = 0.0;
+    }
+  }
+  return 0;
+}
+
+// Identity-feature render, Eq. 9: M = Σ_i e_i α_i Π_{j<i}(1 − α_j)
+// with α, the order, the 1/255 skip and the early stop exactly as in Eq. 8's
+// compositor (O4; A47), features e [n][C] in place of colours, no background.
+// out double[C][H][W]; tie uint8[H][W] (nullable, A29).  Scatter form.
+int oracle_render_features(const OCam* cam, int n, const float* pos_opa, const float* scale,
+                           const float* rot, const uint8_t* keep, int C, const float* feat,
+                           double* out, uint8_t* tie) {
+  std::vector<float> sh0((size_t)n * 4, 0.0f);   // colours are not used (degree 0 placeholder)
+  RenderCtx R;
+  make_ctx(R, cam, n, 0, pos_opa, scale, rot, sh0.data(), keep);
+  const TieEps te = tie_from(nullptr);
+  const int W = cam->width, H = cam->height;
+  const size_t np = (size_t)W * H;
+  std::vector<double> T(np, 1.0);
+  std::vector<uint8_t> done(np, 0), tv(np, 0);
+  for (size_t e = 0; e < (size_t)C * np; ++e) out[e] = 0.0;
+  int nth = 1;
+#ifdef _OPENMP
+  nth = omp_get_max_threads();
+#endif
+  const int band = std::max(1, (H + nth * 4 - 1) / (nth * 4));
+  const int nb = (H + band - 1) / band;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int bi = 0; bi < nb; ++bi) {
+    const int ylo = bi * band, yhi = std::min(H - 1, ylo + band - 1);
+    for (int pos = 0; pos < (int)R.ord.size(); ++pos) {
+      const int gi = R.ord[pos];
+      const Proj& g = R.G[gi];
+      const int y0 = std::max(g.key.y0, ylo), y1 = std::min(g.key.y1, yhi);
+      for (int Y = y0; Y <= y1; ++Y)
+        for (int X = g.key.x0; X <= g.key.x1; ++X) {
+          const size_t p = (size_t)Y * W + X;
+          if (done[p]) continue;
+          Eval e = eval_at(g, X, Y);
+          if (is_tie(g, e, T[p], te)) tv[p] = 1;
+          if (e.power > 0 || e.alpha < ALPHA_MIN) continue;
+          const double tn = T[p] * (1 - e.alpha);
+          if (tn < T_MIN) { done[p] = 1; continue; }
+          for (int ch = 0; ch < C; ++ch) out[ch * np + p] += (double)feat[(size_t)gi * C + ch] * e.alpha * T[p];
+          T[p] = tn;
+        }
+    }
+  }
+  if (tie)
+    for (size_t p = 0; p < np; ++p) tie[p] = tv[p];
+  return 0;
+}
+
+}  // extern "C"
