@@ -428,6 +428,73 @@ int dass_partition(int32_t n, const uint8_t* mask, int32_t* idx_dyn, int32_t* id
                    int32_t* counts, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Error-guided densification (§3.4) — SURVEY §8(f) f4.
+ *
+ * dass_densify_select: Eq. 4
+ *     S = {n : ∇p̄_n > τ_pos} ∪ (S_err ∩ {n : ∇p̄_n > τ_err}),
+ *   ∇p̄_n = gradstat_sum[n] / gradstat_cnt[n] (one IEEE fp32 division; 0 when
+ *   the count is 0; A44), S_err = {n : s_err[n] ≠ 0} from dass_error_map
+ *   (nullable: ∅).  in_S: uint8[n] written (1 = selected); idx: int32[n],
+ *   the first |S| entries = ascending members of S; counts: device int32[2]
+ *   = (|S|, n − |S|).  ws: dass_partition_workspace(n) bytes.  Deterministic.
+ *
+ * dass_spawn: spawn densification (A45).  Writes n_out = n + m·K rows
+ *   to the out arrays (sh planes with stride n_out): rows [0, n) copy the
+ *   input, and child j < K of the k-th listed parent i = idx[k] (k < m, host
+ *   int, e.g. counts[0] of dass_densify_select) goes to row n + k·K + j:
+ *     z ~ N(0, I₃) from Philox4x64-10(counter = (k·K + j, 0, 0, 0),
+ *                                     key = (seed, 0x44415353)),
+ *       Box-Muller on u_a = ((x_a >> 40) + ½)·2⁻²⁴:
+ *       z = (r₀cos 2πu₁, r₀sin 2πu₁, r₁cos 2πu₃), r_b = √(−2 ln u_{2b}),
+ *     p_child = p + R(n(q))·(s ∘ z)   (a sample of N(p, Σ), Σ = R S Sᵀ Rᵀ),
+ *     s_child = s / scale_shrink, o_child = child_opacity,
+ *     q, SH and the dynamic flag copied.
+ *   dyn/out_dyn nullable (both or neither).  K ≥ 1, scale_shrink > 0.
+ *
+ * dass_prune_select: opacity pruning of the candidates (A46): keep
+ *   row i iff i < first (the frozen base rows) or o_i ≥ min_opacity.  keep:
+ *   uint8[n] written; idx / counts as for dass_densify_select (the kept rows,
+ *   ascending).  ws: dass_partition_workspace(n) bytes.
+ *
+ * dass_gather: out row k ← input row idx[k] for k < m (host int), all fields
+ *   (pos_opa, scale, rot, the K4 SH planes with strides n and m, dyn).  With
+ *   dass_prune_select's idx and m = counts[0] it is the pruned set.
+ *
+ * INVALID_ARG: n < 0, m < 0, sh_degree ∉ [0, 3], a null required pointer,
+ *   misaligned float4 arrays, K < 1 or scale_shrink ≤ 0 (spawn), m > n (gather).
+ * ------------------------------------------------------------------------- */
+int dass_densify_select(int32_t n, const float* gradstat_sum, const uint32_t* gradstat_cnt,
+                        const uint8_t* s_err, float tau_pos, float tau_err, uint8_t* in_S,
+                        int32_t* idx, int32_t* counts, void* ws, size_t ws_bytes,
+                        void* stream);
+int dass_spawn(int32_t n, int32_t sh_degree, const float* pos_opa, const float* scale,
+               const float* rot, const float* sh, const uint8_t* dyn, int32_t m,
+               const int32_t* idx, int32_t spawn_count, float scale_shrink,
+               float child_opacity, uint64_t seed, float* out_pos_opa, float* out_scale,
+               float* out_rot, float* out_sh, uint8_t* out_dyn, void* stream);
+int dass_prune_select(int32_t n, int32_t first, const float* pos_opa, float min_opacity,
+                      uint8_t* keep, int32_t* idx, int32_t* counts, void* ws,
+                      size_t ws_bytes, void* stream);
+int dass_gather(int32_t n, int32_t sh_degree, const float* pos_opa, const float* scale,
+                const float* rot, const float* sh, const uint8_t* dyn, int32_t m,
+                const int32_t* idx, float* out_pos_opa, float* out_scale, float* out_rot,
+                float* out_sh, uint8_t* out_dyn, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * dass_render_features — identity-feature render, Eq. 9 (A47):
+ *   M = Σ_i e_i α_i Π_{j<i}(1 − α_j)
+ * over the same sorted tile lists, records, α decisions (Eq. 8, A09-A12,
+ * A35-A36) and early stop as dass_render_fwd, with per-Gaussian features
+ * e (float [n][channels], 16-byte aligned; channels ∈ {4, 8, 12, 16}; 16 in
+ * Gaussian Grouping) in place of the colour and no background term.
+ * out: float [channels][H][W], overwritten.  Inputs as for dass_render_fwd.
+ * ------------------------------------------------------------------------- */
+int dass_render_features(const dass_camera* cam, const uint32_t* tile_ranges,
+                         const uint32_t* sorted_ids, const float* xy_depth,
+                         const float* conic_opa, const uint32_t* box, int32_t channels,
+                         const float* feat, float* out, void* stream);
+
+/* ---------------------------------------------------------------------------
  * dass_error_map — error map, binarisation and Alg. 1 (§3.4 P:164-165, P:174;
  * Alg. 1 P:403-415 with the garble fixed, A20-A22).
  *   E(X,Y) = (1/3)·Σ_ch |rendered − gt|  → err (float [H][W], nullable)

@@ -315,3 +315,11 @@ def render_features(cam, scene, feat, keep=None):
                                  _p(_f32(scene.scale)), _p(_f32(scene.rot)), _p(k), Cn, _p(feat),
                                  _p(out), _p(tie))
     return out, tie
+
+
+def prune_keep(pos_opa, first, min_opacity):
+    """Opacity pruning (A46): keep uint8[n] and the kept count."""
+    po = _f32(pos_opa)
+    keep = np.zeros(po.shape[0], np.uint8)
+    c = lib().oracle_prune_keep(po.shape[0], int(first), _p(po), C.c_float(min_opacity), _p(keep))
+    return keep, c

@@ -1629,3 +1629,17 @@ int oracle_render_features(const OCam* cam, int n, const float* pos_opa, const f
 }
 
 }  // extern "C"
+
+extern "C" {
+// Opacity pruning ("eliminate excessive Gaussian candidates with very
+// low opacity"; A46): rows i < first (the frozen base) are kept; a candidate
+// is kept iff o_i ≥ min_opacity.  keep uint8[n].  Returns the kept count.
+int oracle_prune_keep(int n, int first, const float* pos_opa, float min_opacity, uint8_t* keep) {
+  int c = 0;
+  for (int i = 0; i < n; ++i) {
+    keep[i] = (i < first || !(pos_opa[4 * i + 3] < min_opacity)) ? 1 : 0;
+    c += keep[i];
+  }
+  return c;
+}
+}  // extern "C"

@@ -468,6 +468,118 @@ int dass_partition(int32_t n, const uint8_t* mask, int32_t* idx_dyn, int32_t* id
                      "dass_partition");
 }
 
+static int sh_k4(int deg) { return (3 * (deg + 1) * (deg + 1) + 3) / 4; }
+
+int dass_densify_select(int32_t n, const float* gradstat_sum, const uint32_t* gradstat_cnt,
+                        const uint8_t* s_err, float tau_pos, float tau_err, uint8_t* in_S,
+                        int32_t* idx, int32_t* counts, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if ((n > 0 && (!gradstat_sum || !gradstat_cnt || !in_S || !idx)) || !counts)
+    return fail(DASS_ERR_INVALID_ARG, "dass_densify_select: null required pointer%s");
+  if (!std::isfinite(tau_pos) || !std::isfinite(tau_err))
+    return fail(DASS_ERR_INVALID_ARG, "dass_densify_select: thresholds must be finite%s");
+  if (!ws || ws_bytes < partition_workspace(n) || ((uintptr_t)ws & 3u))
+    return fail(DASS_ERR_INVALID_ARG, "dass_densify_select: workspace too small or misaligned%s");
+  return cuda_status(launch_densify_select(n, gradstat_sum, gradstat_cnt, s_err, tau_pos, tau_err,
+                                           in_S, idx, counts, ws, (cudaStream_t)stream),
+                     "dass_densify_select");
+}
+
+int dass_prune_select(int32_t n, int32_t first, const float* pos_opa, float min_opacity,
+                      uint8_t* keep, int32_t* idx, int32_t* counts, void* ws, size_t ws_bytes,
+                      void* stream) {
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if ((n > 0 && (!pos_opa || !keep || !idx)) || !counts)
+    return fail(DASS_ERR_INVALID_ARG, "dass_prune_select: null required pointer%s");
+  if (pos_opa && !aligned16(pos_opa))
+    return fail(DASS_ERR_INVALID_ARG, "dass_prune_select: pos_opa must be 16-byte aligned%s");
+  if (!std::isfinite(min_opacity)) return fail(DASS_ERR_INVALID_ARG, "min_opacity must be finite%s");
+  if (!ws || ws_bytes < partition_workspace(n) || ((uintptr_t)ws & 3u))
+    return fail(DASS_ERR_INVALID_ARG, "dass_prune_select: workspace too small or misaligned%s");
+  return cuda_status(launch_prune_select(n, first, (const float4*)pos_opa, min_opacity, keep, idx,
+                                         counts, ws, (cudaStream_t)stream),
+                     "dass_prune_select");
+}
+
+static int check_rows(const char* where, const float* a, const float* b, const float* c,
+                      const float* d) {
+  if (!a || !b || !c || !d) return fail(DASS_ERR_INVALID_ARG, "%s: null required pointer", where);
+  if (!aligned16(a) || !aligned16(b) || !aligned16(c) || !aligned16(d))
+    return fail(DASS_ERR_INVALID_ARG, "%s: float4 arrays must be 16-byte aligned", where);
+  return DASS_OK;
+}
+
+int dass_gather(int32_t n, int32_t sh_degree, const float* pos_opa, const float* scale,
+                const float* rot, const float* sh, const uint8_t* dyn, int32_t m,
+                const int32_t* idx, float* out_pos_opa, float* out_scale, float* out_rot,
+                float* out_sh, uint8_t* out_dyn, void* stream) {
+  if (n < 0 || m < 0 || m > n) return fail(DASS_ERR_INVALID_ARG, "dass_gather: need 0 <= m <= n%s");
+  if (sh_degree < 0 || sh_degree > 3) return fail(DASS_ERR_INVALID_ARG, "sh_degree must be in [0, 3]%s");
+  if (m == 0) return DASS_OK;
+  int st;
+  if ((st = check_rows("dass_gather", pos_opa, scale, rot, sh)) ||
+      (st = check_rows("dass_gather", out_pos_opa, out_scale, out_rot, out_sh)))
+    return st;
+  if (!idx) return fail(DASS_ERR_INVALID_ARG, "dass_gather: idx is null%s");
+  return cuda_status(launch_gather(n, sh_k4(sh_degree), (const float4*)pos_opa, (const float4*)scale,
+                                   (const float4*)rot, (const float4*)sh, dyn, m, idx, m, 0,
+                                   (float4*)out_pos_opa, (float4*)out_scale, (float4*)out_rot,
+                                   (float4*)out_sh, out_dyn, (cudaStream_t)stream),
+                     "dass_gather");
+}
+
+int dass_spawn(int32_t n, int32_t sh_degree, const float* pos_opa, const float* scale,
+               const float* rot, const float* sh, const uint8_t* dyn, int32_t m,
+               const int32_t* idx, int32_t spawn_count, float scale_shrink, float child_opacity,
+               uint64_t seed, float* out_pos_opa, float* out_scale, float* out_rot, float* out_sh,
+               uint8_t* out_dyn, void* stream) {
+  if (n < 0 || m < 0) return fail(DASS_ERR_INVALID_ARG, "dass_spawn: n, m must be >= 0%s");
+  if (sh_degree < 0 || sh_degree > 3) return fail(DASS_ERR_INVALID_ARG, "sh_degree must be in [0, 3]%s");
+  if (spawn_count < 1 || !(scale_shrink > 0.f) || !std::isfinite(child_opacity))
+    return fail(DASS_ERR_INVALID_ARG, "dass_spawn: need spawn_count >= 1, scale_shrink > 0, finite opacity%s");
+  const int64_t n_out = (int64_t)n + (int64_t)m * spawn_count;
+  if (n_out > INT32_MAX) return fail(DASS_ERR_INVALID_ARG, "dass_spawn: n + m*K overflows int32%s");
+  if (n_out == 0) return DASS_OK;
+  int st;
+  if ((st = check_rows("dass_spawn", out_pos_opa, out_scale, out_rot, out_sh))) return st;
+  if (n > 0 && (st = check_rows("dass_spawn", pos_opa, scale, rot, sh))) return st;
+  if (m > 0 && !idx) return fail(DASS_ERR_INVALID_ARG, "dass_spawn: idx is null%s");
+  if ((dyn == nullptr) != (out_dyn == nullptr))
+    return fail(DASS_ERR_INVALID_ARG, "dass_spawn: dyn and out_dyn must both be given or both null%s");
+  const int k4 = sh_k4(sh_degree);
+  cudaError_t e = launch_gather(n, k4, (const float4*)pos_opa, (const float4*)scale,
+                                (const float4*)rot, (const float4*)sh, dyn, n, nullptr, (int)n_out,
+                                0, (float4*)out_pos_opa, (float4*)out_scale, (float4*)out_rot,
+                                (float4*)out_sh, out_dyn, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "dass_spawn");
+  return cuda_status(launch_spawn_children(n, k4, (const float4*)pos_opa, (const float4*)scale,
+                                           (const float4*)rot, (const float4*)sh, dyn, m, idx,
+                                           spawn_count, scale_shrink, child_opacity, seed,
+                                           (int)n_out, n, (float4*)out_pos_opa,
+                                           (float4*)out_scale, (float4*)out_rot, (float4*)out_sh,
+                                           out_dyn, (cudaStream_t)stream),
+                     "dass_spawn");
+}
+
+int dass_render_features(const dass_camera* cam, const uint32_t* tile_ranges,
+                         const uint32_t* sorted_ids, const float* xy_depth, const float* conic_opa,
+                         const uint32_t* box, int32_t channels, const float* feat, float* out,
+                         void* stream) {
+  int st = check_camera(cam);
+  if (st) return st;
+  if (channels != 4 && channels != 8 && channels != 12 && channels != 16)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_features: channels must be 4, 8, 12 or 16%s");
+  if (!tile_ranges || !sorted_ids || !xy_depth || !conic_opa || !box || !feat || !out)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_features: null required pointer%s");
+  if (!aligned16(feat)) return fail(DASS_ERR_INVALID_ARG, "dass_render_features: feat must be 16-byte aligned%s");
+  CamParams cp = to_params(cam);
+  return cuda_status(launch_render_features(cp, (const uint2*)tile_ranges, sorted_ids,
+                                            (const float4*)xy_depth, (const float4*)conic_opa,
+                                            (const uint2*)box, channels, feat, out,
+                                            (cudaStream_t)stream),
+                     "dass_render_features");
+}
+
 int dass_error_map(const dass_camera* cam, const float* rendered, const float* gt, float gamma_err,
                    float* err, uint32_t* dmask, int32_t n_base, const float* pos_opa,
                    uint8_t* s_err, void* stream) {

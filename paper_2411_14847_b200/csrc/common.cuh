@@ -147,6 +147,26 @@ cudaError_t launch_inherit_mask_bwd(int n, const float* m, const float4* pos_opa
                                     const float4* scale, const float4* g_pos_opa,
                                     const float4* g_scale, float lambda_inher, float* g_m,
                                     cudaStream_t s);
+cudaError_t launch_render_features(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
+                                   const float4* xy_depth, const float4* conic_opa,
+                                   const uint2* box, int channels, const float* feat, float* out,
+                                   cudaStream_t s);
+cudaError_t launch_densify_select(int n, const float* gsum, const uint32_t* gcnt,
+                                  const uint8_t* s_err, float tau_pos, float tau_err,
+                                  uint8_t* in_S, int* idx, int* counts, void* ws, cudaStream_t s);
+cudaError_t launch_prune_select(int n, int first, const float4* pos_opa, float min_opacity,
+                                uint8_t* keep, int* idx, int* counts, void* ws, cudaStream_t s);
+cudaError_t launch_gather(int n_src, int k4, const float4* pos_opa, const float4* scale,
+                          const float4* rot, const float4* sh, const uint8_t* dyn, int m,
+                          const int* idx, int n_dst, int dst_offset, float4* o_pos_opa,
+                          float4* o_scale, float4* o_rot, float4* o_sh, uint8_t* o_dyn,
+                          cudaStream_t s);
+cudaError_t launch_spawn_children(int n_src, int k4, const float4* pos_opa, const float4* scale,
+                                  const float4* rot, const float4* sh, const uint8_t* dyn, int m,
+                                  const int* idx, int K, float shrink, float child_opacity,
+                                  uint64_t seed, int n_dst, int dst_offset, float4* o_pos_opa,
+                                  float4* o_scale, float4* o_rot, float4* o_sh, uint8_t* o_dyn,
+                                  cudaStream_t s);
 size_t partition_workspace(int n);
 cudaError_t launch_partition(int n, const uint8_t* mask, int* idx_dyn, int* idx_st, int* counts,
                              void* ws, cudaStream_t s);

@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(PB) part_scatter_kernel(int n, const uint8_t* 
   const int dyn_base = boff[blockIdx.x];
   if (d) {
     idx_dyn[dyn_base + rank] = i;
-  } else {
+  } else if (idx_st != nullptr) {
     const int st_base = blockIdx.x * PB - dyn_base;
     idx_st[st_base + (threadIdx.x - rank)] = i;
   }

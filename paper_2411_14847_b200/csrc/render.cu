@@ -257,6 +257,102 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
   }
 }
 
+// ------------------------------------- identity-feature render (Eq. 9) ----
+// M = Σ_i e_i α_i Π_{j<i}(1 − α_j) (f4, A47): the forward's tile walk,
+// PPT = 4 mapping, support masks and canonical α decisions, with NV float4
+// feature planes per entry in place of the colour and no background.
+template <int NV>
+__global__ void __launch_bounds__(64) render_features_kernel(
+    const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
+    const float4* __restrict__ conic_opa, const uint2* __restrict__ box,
+    const float4* __restrict__ feat, float* __restrict__ out) {
+  constexpr int PPT = 4;
+  constexpr int NT = 64;
+  constexpr int BATCH = 2 * NT;
+  __shared__ Staged s_st[BATCH];
+  __shared__ float4 s_f[BATCH][NV];
+  const int tile = blockIdx.x;
+  const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
+  const int tx0 = txi * TILE, ty0 = tyi * TILE;
+  const int t = threadIdx.x;
+  const int lx = t & 15, ly0 = (t >> 4) * PPT;
+  const int X = tx0 + lx;
+  const uint32_t wmask = warp_row_mask<PPT>(t >> 5);
+  const uint32_t colbit = 1u << lx;
+  const uint2 range = ranges[tile];
+  float T[PPT];
+  float4 M[PPT][NV];
+  bool done[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int Y = ty0 + ly0 + p;
+    T[p] = 1.f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) M[p][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    done[p] = !(X < cam.W && Y < cam.H);
+  }
+  const float fx = (float)lx;
+  float fy[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) fy[p] = (float)(ly0 + p);
+  for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
+    bool alive = false;
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) alive |= !done[p];
+    if (__syncthreads_count(alive) == 0) break;
+    for (int k = t; k < BATCH; k += NT) {
+      if (b0 + k < range.y) {
+        const uint32_t id = ids[b0 + k];
+        stage<16>(id, xy_depth, conic_opa, conic_opa, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) s_f[k][v] = feat[(size_t)id * NV + v];
+      }
+    }
+    __syncthreads();
+    const int cnt = (int)min((uint32_t)BATCH, range.y - b0);
+    for (int j = 0; j < cnt; ++j) {
+      const float4 a = s_st[j].a;
+      const uint32_t m = __float_as_uint(a.w);
+      if ((m & wmask) == 0u || !(m & colbit)) continue;
+      const float4 co = s_st[j].co;
+      const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fx);
+      const uint32_t mr = m >> (16 + ly0);
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        if (done[p] || !((mr >> p) & 1u)) continue;
+        const float pw = splat_power(ct, a.y - fy[p]);
+        if (pw > 0.f || pw < a.z) continue;
+        const float alpha = splat_alpha(co.w, splat_exp(pw));
+        if (alpha < ALPHA_MIN) continue;
+        const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
+        if (tn < T_MIN) { done[p] = true; continue; }
+        const float w = alpha * T[p];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const float4 e = s_f[j][v];
+          M[p][v].x += e.x * w; M[p][v].y += e.y * w; M[p][v].z += e.z * w; M[p][v].w += e.w * w;
+        }
+        T[p] = tn;
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int Y = ty0 + ly0 + p;
+    if (X < cam.W && Y < cam.H) {
+      const size_t pix = (size_t)Y * cam.W + X, np = (size_t)cam.W * cam.H;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        out[(4 * v + 0) * np + pix] = M[p][v].x;
+        out[(4 * v + 1) * np + pix] = M[p][v].y;
+        out[(4 * v + 2) * np + pix] = M[p][v].z;
+        out[(4 * v + 3) * np + pix] = M[p][v].w;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------ backward: raster part ----
 // Reduce-scatter butterfly for 9 values (pad 10): after 5 rounds (12 SHFL)
 // every even lane holds the warp sum of one value index.  Lane predicates
@@ -893,6 +989,25 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
     default: FWD(4); break;
   }
 #undef FWD
+  launch_counted();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_render_features(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
+                                   const float4* xy_depth, const float4* conic_opa,
+                                   const uint2* box, int channels, const float* feat, float* out,
+                                   cudaStream_t s) {
+  const int ntiles = cam.tiles_x * cam.tiles_y;
+  const float4* f4 = reinterpret_cast<const float4*>(feat);
+#define FEAT(NV)                                                                                 \
+  render_features_kernel<NV><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, box, f4, out)
+  switch (channels / 4) {
+    case 1: FEAT(1); break;
+    case 2: FEAT(2); break;
+    case 3: FEAT(3); break;
+    default: FEAT(4); break;
+  }
+#undef FEAT
   launch_counted();
   return cudaGetLastError();
 }

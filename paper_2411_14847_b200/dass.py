@@ -32,7 +32,8 @@ EXPORTS = (
     "dass_fidelity_loss_workspace", "dass_fidelity_loss", "dass_inherit_mask",
     "dass_inherit_mask_bwd", "dass_error_map", "dass_render_stats",
     "dass_deform_param_count", "dass_deform_fwd", "dass_deform_bwd", "dass_partition_workspace",
-    "dass_partition",
+    "dass_partition", "dass_densify_select", "dass_spawn", "dass_prune_select", "dass_gather",
+    "dass_render_features",
 )
 
 
@@ -124,6 +125,13 @@ def lib():
         L.dass_deform_bwd.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
         L.dass_partition_workspace.argtypes = [i32, P]
         L.dass_partition.argtypes = [i32, P, P, P, P, P, C.c_size_t, P]
+        L.dass_densify_select.argtypes = [i32, P, P, P, C.c_float, C.c_float, P, P, P, P,
+                                          C.c_size_t, P]
+        L.dass_spawn.argtypes = [i32, i32, P, P, P, P, P, i32, P, i32, C.c_float, C.c_float,
+                                 C.c_uint64, P, P, P, P, P, P]
+        L.dass_prune_select.argtypes = [i32, i32, P, C.c_float, P, P, P, P, C.c_size_t, P]
+        L.dass_gather.argtypes = [i32, i32, P, P, P, P, P, i32, P, P, P, P, P, P, P]
+        L.dass_render_features.argtypes = [P, P, P, P, P, P, i32, P, P, P]
         _lib = L
     return _lib
 
@@ -359,3 +367,51 @@ def dass_partition(mask, idx_dyn, idx_st, counts, ws, stream=None):
     _check(lib().dass_partition(n, _ptr(mask), _ptr(idx_dyn), _ptr(idx_st), _ptr(counts), _ptr(ws),
                                 ws.numel() * ws.element_size(), _stream(stream)),
            "dass_partition")
+
+
+def _ws_bytes(ws):
+    return ws.numel() * ws.element_size()
+
+
+def dass_densify_select(gsum, gcnt, s_err, tau_pos, tau_err, in_S, idx, counts, ws, stream=None):
+    """Eq. 4: in_S flags, idx[:counts[0]] = S ascending (device counts)."""
+    n = gsum.shape[0]
+    _check(lib().dass_densify_select(n, _ptr(gsum), _ptr(gcnt), _ptr(s_err), float(tau_pos),
+                                     float(tau_err), _ptr(in_S), _ptr(idx), _ptr(counts), _ptr(ws),
+                                     _ws_bytes(ws), _stream(stream)), "dass_densify_select")
+
+
+def dass_spawn(sh_degree, pos_opa, scale, rot, sh, dyn, m, idx, spawn_count, scale_shrink,
+               child_opacity, seed, out_pos_opa, out_scale, out_rot, out_sh, out_dyn=None,
+               stream=None):
+    """Spawn densification: out = input rows + m·K children (n_out = n + m·K)."""
+    n = pos_opa.shape[0]
+    _check(lib().dass_spawn(n, int(sh_degree), _ptr(pos_opa), _ptr(scale), _ptr(rot), _ptr(sh),
+                            _ptr(dyn), int(m), _ptr(idx), int(spawn_count), float(scale_shrink),
+                            float(child_opacity), C.c_uint64(int(seed)), _ptr(out_pos_opa),
+                            _ptr(out_scale), _ptr(out_rot), _ptr(out_sh), _ptr(out_dyn),
+                            _stream(stream)), "dass_spawn")
+
+
+def dass_prune_select(pos_opa, first, min_opacity, keep, idx, counts, ws, stream=None):
+    n = pos_opa.shape[0]
+    _check(lib().dass_prune_select(n, int(first), _ptr(pos_opa), float(min_opacity), _ptr(keep),
+                                   _ptr(idx), _ptr(counts), _ptr(ws), _ws_bytes(ws),
+                                   _stream(stream)), "dass_prune_select")
+
+
+def dass_gather(sh_degree, pos_opa, scale, rot, sh, dyn, m, idx, out_pos_opa, out_scale, out_rot,
+                out_sh, out_dyn=None, stream=None):
+    n = pos_opa.shape[0]
+    _check(lib().dass_gather(n, int(sh_degree), _ptr(pos_opa), _ptr(scale), _ptr(rot), _ptr(sh),
+                             _ptr(dyn), int(m), _ptr(idx), _ptr(out_pos_opa), _ptr(out_scale),
+                             _ptr(out_rot), _ptr(out_sh), _ptr(out_dyn), _stream(stream)),
+           "dass_gather")
+
+
+def dass_render_features(cam, ranges, sorted_ids, xy_depth, conic_opa, box, feat, out, stream=None):
+    """Eq. 9: out [C][H][W] from features feat [n][C]."""
+    c = _cam(cam)
+    _check(lib().dass_render_features(C.byref(c), _ptr(ranges), _ptr(sorted_ids), _ptr(xy_depth),
+                                      _ptr(conic_opa), _ptr(box), int(feat.shape[1]), _ptr(feat),
+                                      _ptr(out), _stream(stream)), "dass_render_features")

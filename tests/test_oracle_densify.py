@@ -90,3 +90,10 @@ def test_feature_render_equals_colour_render_and_partition_of_unity():
     assert np.array_equal(tie, ref["tie"])
     ones, _ = oracle.render_features(cam, sc, np.ones((sc.n, 16), np.float32))
     np.testing.assert_allclose(ones, np.broadcast_to(1 - ref["T"], ones.shape), atol=1e-12)
+
+
+def test_prune_keep_definition():
+    po = np.zeros((8, 4), np.float32)
+    po[:, 3] = [0.001, 0.9, 0.005, 0.0049, 0.5, 0.0, 0.006, 0.004]
+    keep, c = oracle.prune_keep(po, 2, 0.005)
+    assert keep.tolist() == [1, 1, 1, 0, 1, 0, 1, 0] and c == 5     # base rows kept; o = τ kept
