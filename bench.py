@@ -371,6 +371,70 @@ def run_ours(args):
             ops["deform_fwd"] = e_def[0].elapsed_time(e_def[1])
             ops["deform_bwd"] = e_def[1].elapsed_time(e_def[2])
 
+    # ---- f4 (once per timestep, not in the step): error-guided densification
+    # on this GPU's state — Eq. 4 selection from the step's ∇p̄ and an S_err
+    # from one view's error map, spawn (K = 2), opacity prune + gather, and the
+    # 16-channel identity-feature render of one view.  CUDA events per op.
+    densify = None
+    if my_cams and not args.lean:
+        k4 = K4
+        E = lambda: torch.cuda.Event(enable_timing=True)
+        ws_p = torch.empty(dass.dass_partition_workspace(n) // 4 + 1, dtype=torch.int32, device=dev)
+        s_err = torch.zeros(n, dtype=torch.uint8, device=dev)
+        err = torch.empty(H, W, device=dev)
+        raster.forward(my_cams[0], records.view(0))
+        dass.dass_error_map(my_cams[0], raster.img, gts[0] if train is not None else raster.img,
+                            0.05, err, None, n, shifted.pos_opa, s_err)
+        in_S = torch.empty(n, dtype=torch.uint8, device=dev)
+        idx = torch.empty(n, dtype=torch.int32, device=dev)
+        cnt = torch.zeros(2, dtype=torch.int32, device=dev)
+        gs = grads.gradstat_sum
+        gcnt = grads.gradstat_cnt
+        torch.cuda.synchronize()
+        gbar = (gs / gcnt.clamp(min=1)).float()
+        tau = float(torch.quantile(gbar[gcnt > 0][:1 << 20], 0.95).item())
+        def timed(fn):
+            """ms of one call on the current stream, after a warm-up call."""
+            fn()
+            a, b = E(), E()
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(b)
+
+        ms = {}
+        ms["densify_select"] = timed(lambda: dass.dass_densify_select(
+            gs, gcnt, s_err, tau, 0.5 * tau, in_S, idx, cnt, ws_p))
+        m = int(cnt[0].item())
+        n_out = n + 2 * m
+        o = [torch.empty(n_out, 4, device=dev) for _ in range(3)]
+        o_sh = torch.empty(k4, n_out, 4, device=dev)
+        o_dyn = torch.empty(n_out, dtype=torch.uint8, device=dev)
+        ms["spawn"] = timed(lambda: dass.dass_spawn(
+            deg, shifted.pos_opa, shifted.scale, shifted.rot, shifted.sh, base.dynamic, m, idx, 2,
+            1.6, 0.1, 7, o[0], o[1], o[2], o_sh, o_dyn))
+        keep = torch.empty(n_out, dtype=torch.uint8, device=dev)
+        kidx = torch.empty(n_out, dtype=torch.int32, device=dev)
+        ws_q = torch.empty(dass.dass_partition_workspace(n_out) // 4 + 1, dtype=torch.int32, device=dev)
+        ms["prune_select"] = timed(lambda: dass.dass_prune_select(o[0], n, 0.05, keep, kidx, cnt, ws_q))
+        mk = int(cnt[0].item())
+        g_out = [torch.empty(mk, 4, device=dev) for _ in range(3)]
+        g_sh = torch.empty(k4, mk, 4, device=dev)
+        ms["gather"] = timed(lambda: dass.dass_gather(deg, o[0], o[1], o[2], o_sh, None, mk, kidx,
+                                                      g_out[0], g_out[1], g_out[2], g_sh))
+        feat = torch.randn(n, 16, device=dev)
+        fout = torch.empty(16, H, W, device=dev)
+        xy, co, rgb, box, _ = records.view(0)
+        ms["render_features_16ch_one_view"] = timed(lambda: dass.dass_render_features(
+            my_cams[0], raster.ranges, raster.sorted_ids, xy, co, box, feat, fout))
+        ms["render_fwd_rgb_same_view"] = timed(lambda: dass.dass_render_fwd(
+            my_cams[0], raster.ranges, raster.sorted_ids, xy, co, rgb, box, None, raster.img,
+            raster.T, raster.last, raster.accept, raster.capacity))
+        densify = {"selected": m, "spawned": 2 * m, "kept_after_prune": mk, "rows": n_out,
+                   "bytes_gather_per_row": 16 * 3 + 16 * k4, "ms": ms}
+        densify["ms"] = {k: round(v, 4) for k, v in densify["ms"].items()}
+
     # ---- end-to-end through the public API with host buffers: every step
     # uploads its inputs from pinned host memory and downloads its gradients.
     # Double-buffered: step k+1's upload (copy stream) overlaps step k's
@@ -499,6 +563,7 @@ def run_ours(args):
                             "tile_list_mean": float(np.mean(allst["tile_list_mean"])),
                             "tile_list_max": int(np.max(allst["tile_list_max"]))},
             "training_step_with_loss": train,
+            "densification_f4": densify,
             "gpu_launches": int(launches),
             "clocks": clocks,
             "e2e": e2e,
