@@ -152,7 +152,7 @@ struct AcceptLists {
 };
 
 // ------------------------------------------------------------- forward ----
-template <int PPT, bool LISTS>
+template <int PPT, bool LISTS, int RPW = 16>
 __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
@@ -175,13 +175,13 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
   const uint2 range = ranges[tile];
   float T[PPT], C[PPT][3];
   uint32_t last[PPT];
-  bool done[PPT];
+  uint32_t live = 0;   // bit p: pixel p is inside the image and not terminated
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int Y = ty0 + ly0 + p;
     T[p] = 1.f; C[p][0] = C[p][1] = C[p][2] = 0.f;
     last[p] = range.x;
-    done[p] = !(X < cam.W && Y < cam.H);
+    if (X < cam.W && Y < cam.H) live |= 1u << p;
   }
   const float fx = (float)lx;
   float fy[PPT];
@@ -192,12 +192,10 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
   const size_t lbase = (size_t)NW * range.x + (size_t)warp * (range.y - range.x);
   uint32_t nlist = 0;
   for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
-    bool alive = false;
-#pragma unroll
-    for (int p = 0; p < PPT; ++p) alive |= !done[p];
+    const bool alive = live != 0u;
     if (__syncthreads_count(alive) == 0) break;
     for (int k = t; k < BATCH; k += NT)
-      if (b0 + k < range.y) stage<16>(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
+      if (b0 + k < range.y) stage<RPW>(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
     __syncthreads();
     const int cnt = __any_sync(0xffffffffu, alive) ? (int)min((uint32_t)BATCH, range.y - b0) : 0;
     for (int j = 0; j < cnt; ++j) {
@@ -206,30 +204,34 @@ __global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kerne
       const uint32_t m = __float_as_uint(a.w);
       if ((m & wmask) == 0u) continue;   // warp-uniform: box misses this warp's rows
       uint32_t accb = 0;                 // this lane's accepted pixels of the entry
-      if (m & colbit) {
+      // candidate pixels: column in the mask, row in the mask, still live
+      const uint32_t cand = (m & colbit) ? ((m >> (16 + ly0)) & live) : 0u;
+      if (cand) {
         const float4 co = st.co;
         const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fx);
-        const uint32_t mr = m >> (16 + ly0);   // this thread's PPT row bits
         float pw[PPT];
-        bool ok[PPT];
+        uint32_t ok = 0;
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {   // independent per pixel: no branches, full ILP
           pw[p] = splat_power(ct, a.y - fy[p]);
-          ok[p] = !done[p] && ((mr >> p) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
+          ok |= (!(pw[p] > 0.f) && !(pw[p] < a.z)) ? (1u << p) : 0u;
         }
-#pragma unroll
-        for (int p = 0; p < PPT; ++p) {
-          if (!ok[p]) continue;
-          const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
-          if (alpha < ALPHA_MIN) continue;
-          const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
-          if (tn < T_MIN) { done[p] = true; continue; }
+        ok &= cand;
+        if (ok) {
           const float4 c = st.c;
-          const float w = alpha * T[p];
-          C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
-          T[p] = tn;
-          last[p] = b0 + j + 1;
-          accb |= 1u << p;
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) {
+            if (!((ok >> p) & 1u)) continue;
+            const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
+            if (alpha < ALPHA_MIN) continue;
+            const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
+            if (tn < T_MIN) { live &= ~(1u << p); continue; }
+            const float w = alpha * T[p];
+            C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
+            T[p] = tn;
+            last[p] = b0 + j + 1;
+            accb |= 1u << p;
+          }
         }
       }
       if (LISTS) {
@@ -973,8 +975,16 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
   const int ntiles = cam.tiles_x * cam.tiles_y;
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(accept, ntiles, capacity);
-    render_fwd_kernel<4, true><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, box,
-                                                     bg, out_img, out_T, out_last, acc);
+    static const int rpw = [] {
+      const char* e = getenv("DASS_FWD_RPW");
+      return e ? atoi(e) : 16;
+    }();
+    if (rpw == 8)
+      render_fwd_kernel<4, true, 8><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
+                                                          box, bg, out_img, out_T, out_last, acc);
+    else
+      render_fwd_kernel<4, true, 16><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
+                                                           box, bg, out_img, out_T, out_last, acc);
     launch_counted();
     return cudaGetLastError();
   }

@@ -1,0 +1,10 @@
+# A/B of env knobs on the lean bench (under gpurun): bash tools/gpu_ab_env.sh "VAR=a" "VAR=b" ...
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+for cfg in "$@"; do
+  for rep in 1 2; do
+    env $cfg python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ab.json 2>/dev/null
+    python -c "
+import json; d=json.load(open('gpurun_out/ab.json')); o=d['ops_ms_per_step_rank0']
+print('$cfg', d['ms_per_step'], 'fwd', o['render_fwd'], 'bwd', o['render_bwd_raster'])"
+  done
+done
