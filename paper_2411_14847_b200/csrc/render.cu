@@ -152,8 +152,8 @@ struct AcceptLists {
 };
 
 // ------------------------------------------------------------- forward ----
-template <int PPT, bool LISTS, int RPW = 16>
-__global__ void __launch_bounds__(256 / PPT, 768 / (256 / PPT)) render_fwd_kernel(
+template <int PPT, bool LISTS, int RPW = 16, int MINB = 768 / (256 / PPT)>
+__global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
     const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
 // (every list entry has ≥ 1 accepted pixel, so every butterfly is needed) and
 // the chunk is flushed with vector reductions.  Warps are independent: no
 // block barrier, no iteration over entries the warp never accepted.
-template <int PPT>
-__global__ void __launch_bounds__(256 / PPT, 1024 / (256 / PPT)) render_bwd_list_kernel(
+template <int PPT, int MINB = 1024 / (256 / PPT)>
+__global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
     const float4* __restrict__ conic_opa, const float4* __restrict__ rgb, float3 bg,
@@ -979,12 +979,19 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
       const char* e = getenv("DASS_FWD_RPW");
       return e ? atoi(e) : 16;
     }();
-    if (rpw == 8)
-      render_fwd_kernel<4, true, 8><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
-                                                          box, bg, out_img, out_T, out_last, acc);
-    else
-      render_fwd_kernel<4, true, 16><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
-                                                           box, bg, out_img, out_T, out_last, acc);
+    static const int fminb = [] {
+      const char* e = getenv("DASS_FWD_MINB");
+      return e ? atoi(e) : 12;
+    }();
+#define FWDL(R, M)                                                                               \
+  render_fwd_kernel<4, true, R, M><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
+                                                         box, bg, out_img, out_T, out_last, acc)
+    if (rpw == 8) FWDL(8, 12);
+    else if (fminb == 16) FWDL(16, 16);
+    else if (fminb == 10) FWDL(16, 10);
+    else if (fminb == 8) FWDL(16, 8);
+    else FWDL(16, 12);
+#undef FWDL
     launch_counted();
     return cudaGetLastError();
   }
@@ -1035,8 +1042,20 @@ cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* r
   const int ntiles = cam.tiles_x * cam.tiles_y;
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(const_cast<void*>(accept), ntiles, capacity);
-    render_bwd_list_kernel<4><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg,
-                                                    out_T, dL_dimg, acc, g2d);
+    static const int lminb = [] {
+      const char* e = getenv("DASS_BWDL_MINB");
+      return e ? atoi(e) : 12;   // 80 registers: measured best (16 → 64 regs rematerialises)
+    }();
+#define BWDL(M)                                                                                  \
+  render_bwd_list_kernel<4, M><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg, \
+                                                     out_T, dL_dimg, acc, g2d)
+    switch (lminb) {
+      case 8: BWDL(8); break;
+      case 10: BWDL(10); break;
+      case 12: BWDL(12); break;
+      default: BWDL(16); break;
+    }
+#undef BWDL
     launch_counted();
     return cudaGetLastError();
   }
