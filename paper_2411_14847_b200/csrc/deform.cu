@@ -20,6 +20,8 @@
 //
 // Everything is fp32 FFMA (SIMT): the MLP is ≈20 kFLOP per Gaussian; the
 // tcgen05 version is listed as next work in DESIGN.md.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace dass {
@@ -494,6 +496,287 @@ deform_bwd_kernel(const __grid_constant__ HashGridParams g, const float* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core forward (tcgen05.mma kind::tf32, sm_100a).  Same tile/thread
+// shape as deform_fwd_kernel; the three layers are GEMMs D[128×N] = A[128×K]·Bᵀ
+// (A = the tile's activations, B = a weight matrix [N×K], both K-major in the
+// canonical no-swizzle core-matrix layout: 8 rows × 16 B per 128-B core
+// matrix, row groups 128 B apart, 4-float k-chunks R·16 B apart), issued by one
+// thread, accumulated in TMEM and read back with tcgen05.ld for the bias/ReLU
+// epilogue, which writes the next layer's A operand.  Precision: 3×TF32 — every
+// operand x = hi + lo with hi = x with the low 13 mantissa bits cleared (exactly
+// a TF32 value) and lo = x − hi, and D = A_hi·B_hi + A_lo·B_hi + A_hi·B_lo, which
+// keeps the products at ≈ fp32 accuracy (the dropped lo·lo term is ≤ 2⁻²²·|ab|).
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+// float offset of element (r, k) of an R-row K-major operand
+__device__ __forceinline__ int kmaj(int r, int k, int R) {
+  return (k >> 2) * (R * 4) + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;   // descriptor version (sm_100)
+  return d;                 // base offset 0, no swizzle
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M×N
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                    uint32_t acc) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+               ::"r"(tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(smem_u32(mbar)));
+}
+__device__ __forceinline__ void wait(uint64_t* mbar, uint32_t parity) {
+  asm volatile("{\n.reg .pred P1;\nWAIT_%=:\n"
+               "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+               "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(mbar)), "r"(parity));
+}
+__device__ __forceinline__ void ld16(uint32_t taddr, float v[16]) {
+  uint32_t r[16];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+                 "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void before_sync() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void after_sync() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[128×N] (=|+=) A·Bᵀ over K with the 3×TF32 split: A hi/lo [128×K], B hi/lo [N×K]
+__device__ __forceinline__ void gemm3(uint32_t tmem, const float* Ah, const float* Al,
+                                      const float* Bh, const float* Bl, int N, int K) {
+  const uint32_t id = idesc_tf32(128, N);
+  const float* As[3] = {Ah, Al, Ah};
+  const float* Bs[3] = {Bh, Bh, Bl};
+#pragma unroll
+  for (int ps = 0; ps < 3; ++ps)
+    for (int kk = 0; kk < K / 8; ++kk) {
+      const uint64_t a = sdesc(smem_u32(As[ps]) + kk * 2 * (128 * 16), 128 * 16, 128);
+      const uint64_t b = sdesc(smem_u32(Bs[ps]) + kk * 2 * (N * 16), N * 16, 128);
+      mma(tmem, a, b, id, (ps > 0 || kk > 0) ? 1u : 0u);
+    }
+}
+
+}  // namespace tc
+
+// stage a weight matrix W[N][K] (global, row-major) as hi/lo K-major operands
+// (rows ≥ Nreal are zero)
+__device__ __forceinline__ void stage_weight(const float* __restrict__ W, int Nreal, int N, int K,
+                                             float* hi, float* lo) {
+  for (int e = threadIdx.x; e < N * K; e += blockDim.x) {
+    const int r = e / K, k = e - r * K;
+    const float x = r < Nreal ? W[r * K + k] : 0.f;
+    const float h = tc::tf32_hi(x);
+    hi[tc::kmaj(r, k, N)] = h;
+    lo[tc::kmaj(r, k, N)] = x - h;
+  }
+}
+
+// enc for levels [l0, l1) of one Gaussian, written as hi/lo into the K-major A
+// operand (row g of 128)
+template <int F>
+__device__ __forceinline__ void encode_levels_tc(const HashGridParams& g, const float* __restrict__ table,
+                                                 float3 p, bool valid, int l0, int l1, int row,
+                                                 float* xh, float* xl) {
+  for (int l = l0; l < l1; ++l) {
+    float acc[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) acc[f] = 0.f;
+    if (valid) {
+      uint32_t rw[8];
+      float wt[8];
+      level_corners(g, l, p, rw, wt);
+      const float* tab = table + (size_t)l * g.T * F;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if constexpr (F == 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(tab) + rw[c]);
+          acc[0] += wt[c] * v.x; acc[1] += wt[c] * v.y; acc[2] += wt[c] * v.z; acc[3] += wt[c] * v.w;
+        } else if constexpr (F == 2) {
+          const float2 v = __ldg(reinterpret_cast<const float2*>(tab) + rw[c]);
+          acc[0] += wt[c] * v.x; acc[1] += wt[c] * v.y;
+        } else {
+          acc[0] += wt[c] * __ldg(tab + rw[c]);
+        }
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      const int o = tc::kmaj(row, l * F + f, GT);
+      const float h = tc::tf32_hi(acc[f]);
+      xh[o] = h;
+      xl[o] = acc[f] - h;
+    }
+  }
+}
+
+// bias + ReLU of 16·NCH accumulator columns [c0, c0 + 16·NCH) of this thread's
+// row, written as the next layer's hi/lo A operand (float4 per 4 columns)
+template <int NCH>
+__device__ __forceinline__ void relu_epilogue(uint32_t taddr, const float* __restrict__ bias, int c0,
+                                              int row, float* hh, float* hl) {
+#pragma unroll
+  for (int half = 0; half < NCH; ++half) {
+    float v[16];
+    tc::ld16(taddr + half * 16, v);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + half * 16 + 4 * q;
+      float4 h4, l4;
+      float* hp = &h4.x;
+      float* lp = &l4.x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float x = fmaxf(v[4 * q + j] + bias[c + j], 0.f);
+        hp[j] = tc::tf32_hi(x);
+        lp[j] = x - hp[j];
+      }
+      const int o = tc::kmaj(row, c, GT);   // 4 consecutive columns: one 16-B chunk
+      *reinterpret_cast<float4*>(hh + o) = h4;
+      *reinterpret_cast<float4*>(hl + o) = l4;
+    }
+  }
+}
+
+constexpr int NT_TC = 512;   // 4 threads per Gaussian row; 16 warps = 4 TMEM lane quadrants × 4 column groups
+
+template <int F>
+__global__ void __launch_bounds__(NT_TC, 1)
+deform_fwd_tc_kernel(const __grid_constant__ HashGridParams g, const float* __restrict__ table,
+                     const float* __restrict__ mlp, int n, const int* __restrict__ idx,
+                     const int* __restrict__ count, const float4* __restrict__ pos_opa,
+                     float4* __restrict__ mu, float4* __restrict__ sigma) {
+  extern __shared__ __align__(1024) float4 smem4[];
+  float* sm = reinterpret_cast<float*>(smem4);
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tbase;
+  const int in = g.in;
+  float* W1h = sm;                      // [64][in]
+  float* W1l = W1h + HID * in;
+  float* W2h = W1l + HID * in;          // [64][64]
+  float* W2l = W2h + HID * HID;
+  float* W3h = W2l + HID * HID;         // [16][64] (rows ≥ 7 zero)
+  float* W3l = W3h + 16 * HID;
+  float* b1 = W3l + 16 * HID;
+  float* b2 = b1 + HID;
+  float* b3 = b2 + HID;                 // [16]
+  float* Xh = b3 + 16;                  // [128][in]
+  float* Xl = Xh + GT * in;
+  float* Hh = Xl + GT * in;             // [128][64]
+  float* Hl = Hh + GT * HID;
+  const MlpOffsets off(in);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  stage_weight(mlp + off.W1, HID, HID, in, W1h, W1l);
+  stage_weight(mlp + off.W2, HID, HID, HID, W2h, W2l);
+  stage_weight(mlp + off.W3, NOUT, 16, HID, W3h, W3l);
+  if (t < HID) { b1[t] = mlp[off.b1 + t]; b2[t] = mlp[off.b2 + t]; }
+  if (t < 16) b3[t] = t < NOUT ? mlp[off.b3 + t] : 0.f;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;"
+                 ::"r"(tc::smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_async_smem();
+  tc::before_sync();
+  __syncthreads();
+  tc::after_sync();
+  const uint32_t tmem = tbase;
+  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;   // this warp's TMEM lanes
+  const int row = (warp & 3) * 32 + lane;                          // tile row = TMEM lane
+  const int h = warp >> 2;                                         // column group (16 columns)
+  uint32_t phase = 0;
+
+  const int m = count ? min(*count, n) : n;
+  const int gi = t & (GT - 1), qq = t >> 7;                         // encode quarter
+  int Lq = (g.L + 3) / 4;
+  Lq = (Lq + (4 / F) - 1) / (4 / F) * (4 / F);                     // Lq·F % 4 == 0
+  const int l0 = min(g.L, qq * Lq), l1 = min(g.L, (qq + 1) * Lq);
+  for (int tile = blockIdx.x; tile * GT < m; tile += gridDim.x) {
+    {
+      const int k = tile * GT + gi;
+      const bool valid = k < m;
+      const int i = valid ? (idx ? idx[k] : k) : 0;
+      float3 p = make_float3(0.f, 0.f, 0.f);
+      if (valid) { const float4 po = pos_opa[i]; p = make_float3(po.x, po.y, po.z); }
+      encode_levels_tc<F>(g, table, p, valid, l0, l1, gi, Xh, Xl);
+    }
+    tc::fence_async_smem();
+    tc::before_sync();
+    __syncthreads();
+    tc::after_sync();
+    if (t == 0) {   // layer 1: Z1 = X·W1ᵀ → TMEM columns [0, 64)
+      tc::gemm3(tmem, Xh, Xl, W1h, W1l, HID, in);
+      tc::commit(&mbar);
+    }
+    tc::wait(&mbar, phase); phase ^= 1u;
+    tc::after_sync();
+    relu_epilogue<1>(tmem + lane_base + 16 * h, b1, 16 * h, row, Hh, Hl);
+    tc::fence_async_smem();
+    tc::before_sync();
+    __syncthreads();
+    tc::after_sync();
+    if (t == 0) {   // layer 2: Z2 = H1·W2ᵀ → TMEM columns [64, 128)
+      tc::gemm3(tmem + 64, Hh, Hl, W2h, W2l, HID, HID);
+      tc::commit(&mbar);
+    }
+    tc::wait(&mbar, phase); phase ^= 1u;
+    tc::after_sync();
+    relu_epilogue<1>(tmem + lane_base + 64 + 16 * h, b2, 16 * h, row, Hh, Hl);
+    tc::fence_async_smem();
+    tc::before_sync();
+    __syncthreads();
+    tc::after_sync();
+    if (t == 0) {   // head: OUT = H2·W3ᵀ (N = 16, rows ≥ 7 zero) → TMEM columns [0, 16)
+      tc::gemm3(tmem, Hh, Hl, W3h, W3l, 16, HID);
+      tc::commit(&mbar);
+    }
+    tc::wait(&mbar, phase); phase ^= 1u;
+    tc::after_sync();
+    if (h == 0) {
+      float v[16];
+      tc::ld16(tmem + lane_base, v);
+      const int k = tile * GT + row;
+      if (k < m) {
+        const int i = idx ? idx[k] : k;
+        mu[i] = make_float4(v[0] + b3[0], v[1] + b3[1], v[2] + b3[2], 0.f);
+        sigma[i] = make_float4(1.f + (v[3] + b3[3]), v[4] + b3[4], v[5] + b3[5], v[6] + b3[6]);
+      }
+    }
+    tc::before_sync();
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
 // ---- stable partition: idx_dyn = ascending {i : mask[i] ≠ 0}, idx_st = the rest
 constexpr int PB = 1024;
 
@@ -596,10 +879,33 @@ int sm_count() {
   return sms;
 }
 
+size_t fwd_tc_smem(int in) {
+  return sizeof(float) * (size_t)(2 * HID * in + 2 * HID * HID + 2 * 16 * HID + 2 * HID + 16 +
+                                  2 * GT * in + 2 * GT * HID);
+}
+
+bool use_tc() {
+  static const int v = [] {
+    const char* e = getenv("DASS_DEFORM_TC");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 template <int F>
 cudaError_t fwd_launch(const HashGridParams& g, const float* table, const float* mlp, int n,
                        const int* idx, const int* count, const float4* pos_opa, float4* mu,
                        float4* sigma, cudaStream_t s) {
+  if (use_tc()) {
+    const size_t sm = fwd_tc_smem(g.in);
+    cudaError_t e = cudaFuncSetAttribute(deform_fwd_tc_kernel<F>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    const int grid = max(1, min(div_up(n, GT), sm_count()));
+    deform_fwd_tc_kernel<F><<<grid, NT_TC, sm, s>>>(g, table, mlp, n, idx, count, pos_opa, mu, sigma);
+    launch_counted();
+    return cudaGetLastError();
+  }
   const size_t sm = fwd_smem<F>(g.in);
   cudaError_t e = cudaFuncSetAttribute(deform_fwd_kernel<F>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
