@@ -884,12 +884,11 @@ size_t fwd_tc_smem(int in) {
                                   2 * GT * in + 2 * GT * HID);
 }
 
+// DASS_DEFORM_TC=0 selects the FP32 SIMT forward (read per call: the parity
+// tests exercise both paths in one process)
 bool use_tc() {
-  static const int v = [] {
-    const char* e = getenv("DASS_DEFORM_TC");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
+  const char* e = getenv("DASS_DEFORM_TC");
+  return e == nullptr || atoi(e) != 0;
 }
 
 template <int F>

@@ -84,8 +84,19 @@ def check_grad(a, ref, kap):
     assert not bad.any(), (int(bad.sum()), float(np.max(np.abs(a - ref))), float(np.max(np.abs(ref))))
 
 
+@pytest.fixture(params=["tcgen05", "simt"])
+def fwd_path(request, monkeypatch):
+    """Both forward implementations: the tcgen05 3×TF32 kernel (default) and the
+    FP32 SIMT kernel (DASS_DEFORM_TC=0)."""
+    if request.param == "simt":
+        monkeypatch.setenv("DASS_DEFORM_TC", "0")
+    else:
+        monkeypatch.delenv("DASS_DEFORM_TC", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("profile", ["n3dv", "meetroom"])
-def test_dual_fields_forward_through_partition(profile):
+def test_dual_fields_forward_through_partition(profile, fwd_path):
     """Both fields over one partition (device counts), several persistent tiles
     per CTA (60k Gaussians) and a ragged tail; rows outside a group untouched."""
     sc = synth.n3dv_scene(n=60_000, seed=71, degree=0)
@@ -106,7 +117,7 @@ def test_dual_fields_forward_through_partition(profile):
         check_fwd(mu[rows], sg[rows], rmu, rsg)
 
 
-def test_identity_at_initialisation():
+def test_identity_at_initialisation(fwd_path):
     sc = synth.n3dv_scene(n=5000, seed=73, degree=0)
     fd, _ = synth.dual_fields(sc, "n3dv", seed=74, trained=False)
     mu, sg = run_fwd(fd, t(sc.pos_opa), None)
@@ -138,7 +149,7 @@ def test_backward_parity(profile, n):
         check_grad(np_(g_mlp).astype(np.float64), 2 * gp_ref, 2 * km)
 
 
-def test_full_size_forward_sampled_and_empty_group():
+def test_full_size_forward_sampled_and_empty_group(fwd_path):
     """C3-sized (300k Gaussians, N3DV profile): sampled rows against the oracle;
     a count of 0 writes nothing."""
     sc = synth.n3dv_scene(n=300_000, seed=3, degree=0)
