@@ -9,3 +9,6 @@ CMD2="python bench.py --views 2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline 
 $CMD2 > gpurun_out/plain2_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:render_bwd_list -s 2 -c 1 -o gpurun_out/prof_bwd_$TAG -f $CMD2 > gpurun_out/ncu_bwd_$TAG.log 2>&1; ncu --set full --clock-control none --import-source on -k regex:render_fwd -s 2 -c 1 -o gpurun_out/prof_fwd_$TAG -f $CMD2 > gpurun_out/ncu_fwd_$TAG.log 2>&1
 ls -la gpurun_out | grep $TAG
+timeout 300 python tools/deform_timing.py > /dev/null 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:deform_fwd_tc -c 1 -o gpurun_out/prof_deformtc_$TAG -f python tools/deform_timing.py > gpurun_out/ncu_deformtc_$TAG.log 2>&1
+ls -la gpurun_out | grep $TAG
