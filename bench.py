@@ -555,6 +555,8 @@ def run_ours(args):
                          "units_per_step": {"accepted": sum(stats["accepted"]), "P_bwd": sum(stats["P_bwd"])},
                          "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED}},
             "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
+            "rows_roofline": rows_roofline(ops, densify, allst, pk, peak_tflops, n, W, H,
+                                           len(my_cams), deg),
             "scene_stats": None if args.lean else {"K_per_view_mean": float(np.mean(allst["K"])),
                             "P_fwd_per_px": float(np.sum(allst["P_fwd"]) / (len(allst["K"]) * W * H)),
                             "P_bwd_per_px": float(np.sum(allst["P_bwd"]) / (len(allst["K"]) * W * H)),
@@ -630,6 +632,63 @@ def run_reference(args):
                              "sample": "each step = the shift + fwd+bwd of ONE of the 20 views (bounded sample)"},
             "e2e": {"value": round(value, 4), "unit": "views/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+
+
+# Algorithmic work of the SURVEY §8(f) rows, per unit:
+FLOP_SSIM_PER_PXCH = 2 * (5 * 11 * 2) + 40 + 2 * (3 * 11 * 2) + 10   # fwd + bwd stencils
+BYTES_LOSS_PER_PX = 3 * 4 * 3                                           # img, gt in; ∂L/∂img out
+DEFORM_IN = {"dyn": 32, "st": 16}                                       # L·F (N3DV profile)
+
+
+def rows_roofline(ops, densify, allst, pk, peak_fp32, n, W, H, views, deg):
+    """Achieved vs peak for the §8(f) kernels timed in this run (rank 0)."""
+    out = {}
+    hbm = pk.get("hbm_gbs", 6650.0)
+    tf32 = pk.get("bf16_tflops", 2250.0) / 2.0        # nominal dense TF32 = bf16 / 2
+    if "fidelity_loss" in ops and views:
+        t = ops["fidelity_loss"] / 1e3
+        fl = views * 3 * W * H * FLOP_SSIM_PER_PXCH
+        by = views * W * H * BYTES_LOSS_PER_PX
+        out["f1_fidelity_loss"] = {"bound": "alu", "achieved_tflops": round(fl / t / 1e12, 2),
+                                   "peak_tflops": round(peak_fp32, 1),
+                                   "frac": round(fl / t / 1e12 / peak_fp32, 4),
+                                   "hbm_gbs": round(by / t / 1e9, 1), "hbm_frac": round(by / t / 1e9 / hbm, 4),
+                                   "unit": f"pixel-channel ({FLOP_SSIM_PER_PXCH} flop)"}
+    if "deform_fwd" in ops:
+        # 0.3 N dynamic (in 32) + 0.7 N static (in 16); 3 TF32 passes per layer
+        per = lambda i: 2 * (64 * i + 64 * 64 + 16 * 64)
+        fl = 3 * (0.3 * n * per(DEFORM_IN["dyn"]) + 0.7 * n * per(DEFORM_IN["st"]))
+        t = ops["deform_fwd"] / 1e3
+        out["f2_deform_fwd_tcgen05"] = {"bound": "tensor", "achieved_tflops": round(fl / t / 1e12, 2),
+                                        "peak_tflops": round(tf32, 1),
+                                        "frac": round(fl / t / 1e12 / tf32, 4),
+                                        "unit": "Gaussian (3×TF32 MMA flops incl. the N = 16 padded head)"}
+    if "deform_bwd" in ops:
+        per = lambda i: 2 * (64 * i + 64 * 64 + 7 * 64)
+        fl = 3 * (0.3 * n * per(DEFORM_IN["dyn"]) + 0.7 * n * per(DEFORM_IN["st"]))
+        t = ops["deform_bwd"] / 1e3
+        out["f2_deform_bwd_simt"] = {"bound": "alu", "achieved_tflops": round(fl / t / 1e12, 2),
+                                     "peak_tflops": round(peak_fp32, 1),
+                                     "frac": round(fl / t / 1e12 / peak_fp32, 4),
+                                     "unit": "Gaussian (recompute + δ chain + weight gradients = 3× fwd flops)"}
+    if densify:
+        ms = densify["ms"]
+        k4 = (3 * (deg + 1) ** 2 + 3) // 4
+        rows = densify["kept_after_prune"]
+        by = 2 * rows * (48 + 16 * k4)
+        t = ms["gather"] / 1e3
+        out["f4_gather"] = {"bound": "hbm", "achieved_gbs": round(by / t / 1e9, 1),
+                            "peak_gbs": hbm, "frac": round(by / t / 1e9 / hbm, 4),
+                            "unit": f"row ({48 + 16 * k4} B read + written)"}
+        acc0 = allst["accepted"][0] if allst.get("accepted") else None
+        if acc0:
+            fl = acc0 * (2 * 16 + 15)
+            t = ms["render_features_16ch_one_view"] / 1e3
+            out["f4_render_features"] = {"bound": "alu", "achieved_tflops": round(fl / t / 1e12, 2),
+                                         "peak_tflops": round(peak_fp32, 1),
+                                         "frac": round(fl / t / 1e12 / peak_fp32, 4),
+                                         "unit": "accepted (pixel, entry) of view 0 (2·16 + 15 flop)"}
+    return out
 
 
 def profiled_traffic(kernel: str):
