@@ -165,6 +165,7 @@ class MultiViewPass:
         self.slots = [Raster(W, H, n, capacity, device) for _ in range(self.S)]
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.S)]
         self.pre_stream = torch.cuda.Stream(device=device)
+        self.pre_chunks = int(os.environ.get("DASS_PRE_CHUNKS", "2"))
         self.g2d = torch.empty(max(self.V, 1), n, 12, dtype=torch.float32, device=device)
 
     def enable_loss(self, lam: float = 0.2):
@@ -187,7 +188,13 @@ class MultiViewPass:
         main = torch.cuda.current_stream()
         for s in self.streams:
             s.wait_stream(main)
-        half = self.V // 2 if self.V >= 2 * self.S else 0
+        # preprocess in chunks: chunk c's views are chained to parameter gradients on a side
+        # stream as soon as they are rasterised (HBM-bound work under the ALU-bound raster
+        # kernels of later views); only the last chunk runs after the final raster kernel.
+        # Chunks run in order on ONE stream: each += into the same gradient buffers.
+        nchunk = max(1, min(self.pre_chunks, self.V // self.S)) if self.V >= 2 * self.S else 1
+        bounds = [round(c * self.V / nchunk) for c in range(nchunk + 1)]
+        ends = {bounds[c + 1] - 1: c for c in range(nchunk - 1)}
         for v, cam in enumerate(self.cams):
             k = v % self.S
             ras, st = self.slots[k], self.streams[k]
@@ -204,19 +211,18 @@ class MultiViewPass:
                 dass.dass_render_bwd_raster(cam, self.n, ras.ranges, ras.sorted_ids, xy, co, rgb,
                                             box, bg, ras.T, ras.last, dL, self.g2d[v],
                                             ras.accept, ras.capacity)
-            if half and v == half - 1:
-                # the first half's preprocess (HBM-bound) overlaps the second half's
-                # raster kernels (ALU-bound) on a side stream
+            if v in ends:
+                c = ends[v]
                 self.pre_stream.wait_stream(main)
                 for s in self.streams:
                     self.pre_stream.wait_stream(s)
                 with torch.cuda.stream(self.pre_stream):
-                    self._preprocess(scene, records, grads, keep, 0, half)
+                    self._preprocess(scene, records, grads, keep, bounds[c], bounds[c + 1])
         for s in self.streams:
             main.wait_stream(s)
-        if half:
+        if nchunk > 1:
             main.wait_stream(self.pre_stream)
-        self._preprocess(scene, records, grads, keep, half, self.V)
+        self._preprocess(scene, records, grads, keep, bounds[nchunk - 1], self.V)
 
     def _preprocess(self, scene, records, grads, keep, v0, v1):
         dass.dass_render_bwd_preprocess_views(
