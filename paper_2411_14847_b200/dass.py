@@ -141,13 +141,25 @@ def _check(status: int, where: str):
         raise DassError(status, where, lib().dass_last_error().decode())
 
 
+_BAD_DTYPES = None
+
+
 def _ptr(t):
+    """Device pointer of a contiguous CUDA tensor.  libdass computes in fp32 and
+    int32/uint8/uint64 only: a float64/float16/bfloat16 tensor is refused rather
+    than reinterpreted."""
+    global _BAD_DTYPES
     if t is None:
         return None
     if not t.is_cuda:
         raise ValueError("libdass takes CUDA tensors only (no CPU path)")
     if not t.is_contiguous():
         raise ValueError("tensor must be contiguous")
+    if _BAD_DTYPES is None:
+        import torch
+        _BAD_DTYPES = (torch.float64, torch.float16, torch.bfloat16)
+    if t.dtype in _BAD_DTYPES:
+        raise TypeError(f"libdass takes float32 arrays, got {t.dtype}")
     return C.c_void_p(t.data_ptr())
 
 

@@ -103,3 +103,43 @@ def test_camera_struct_layout_matches_generator(lib):
     b = cam.to_struct().tobytes()
     assert C.sizeof(lib.dass_camera) == synth.CAMERA_DTYPE.itemsize == 140
     assert a == b
+
+
+def test_hashgrid_struct_layout_and_param_counts(lib):
+    sc = synth.n3dv_scene(n=200, seed=5, degree=0)
+    fd, fs = synth.dual_fields(sc, "n3dv", seed=6)
+    for f in (fd, fs):
+        assert bytes(lib.hashgrid_struct(f)) == f.to_struct().tobytes()
+        t, m = lib.dass_deform_param_count(f)
+        assert t == f.table.size and m == f.mlp.size == synth.mlp_param_count(f.inputs)
+    bad = lib.hashgrid_struct(fd)
+    bad.features = 3
+    with pytest.raises(lib.DassError):
+        lib.dass_deform_param_count(bad)
+    bad = lib.hashgrid_struct(fd)
+    bad.levels, bad.features = 7, 2            # in = 14: not a multiple of 4
+    with pytest.raises(lib.DassError):
+        lib.dass_deform_param_count(bad)
+
+
+def test_f_row_validation_before_any_cuda_call(lib):
+    L = lib.lib()
+    null = None
+    # densify / prune / gather / spawn / partition: bad sizes and null pointers are refused
+    assert L.dass_densify_select(-1, null, null, null, 1.0, 0.5, null, null, null, null, 0, null) == 1
+    assert L.dass_prune_select(10, 0, null, 0.1, null, null, null, null, 0, null) == 1
+    assert L.dass_gather(5, 3, null, null, null, null, null, 6, null, null, null, null, null, null, null) == 1
+    assert L.dass_spawn(5, 3, null, null, null, null, null, 1, null, 0, 1.6, 0.1, 7,
+                        null, null, null, null, null, null) == 1
+    assert L.dass_partition(10, null, null, null, null, null, 0, null) == 1
+    assert L.dass_render_features(null, null, null, null, null, null, 16, null, null, null) == 1
+    assert lib.kernel_launches() == 0
+
+
+def test_binding_refuses_float64_tensors(lib):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA tensors to reach the dtype check")
+    t = torch.zeros(4, 4, dtype=torch.float64, device="cuda")
+    with pytest.raises(TypeError):
+        lib.dass_apply_shift(t, t, t, t, None, t, t)

@@ -1,0 +1,19 @@
+"""bench.py's host-side logic (no GPU): the §8(f) roofline bookkeeping."""
+import bench
+
+
+def test_rows_roofline_fractions():
+    ops = {"fidelity_loss": 2.5, "deform_fwd": 0.15, "deform_bwd": 0.7}
+    densify = {"kept_after_prune": 300_000,
+               "ms": {"gather": 0.03, "render_features_16ch_one_view": 0.6}}
+    allst = {"accepted": [65_000_000]}
+    pk = {"hbm_gbs": 6400.0, "bf16_tflops": 1600.0}
+    out = bench.rows_roofline(ops, densify, allst, pk, 74.4, 300_000, 1352, 1014, 20, 3)
+    assert set(out) == {"f1_fidelity_loss", "f2_deform_fwd_tcgen05", "f2_deform_bwd_simt",
+                        "f4_gather", "f4_render_features"}
+    for v in out.values():
+        assert 0 < v["frac"] < 1
+    # f4 gather: 2 × rows × (48 + 16·K4) bytes at SH3 (K4 = 12)
+    g = out["f4_gather"]
+    assert abs(g["achieved_gbs"] - 2 * 300_000 * 240 / 0.03e-3 / 1e9) < 1.0
+    assert out["f2_deform_fwd_tcgen05"]["peak_tflops"] == 800.0
