@@ -4,7 +4,7 @@
 // SSIM statistics are separable 11-tap Gaussian windows (σ = 1.5, zero
 // padding).  Two stencil kernels on 32×32 output tiles with a 5-px halo
 // staged in shared memory:
-//   ssim_fwd:  5 windowed moments (μ_I, μ_G, E[I²], E[G²], E[IG]) → S(q) and the
+//   ssim_fwd:  4 windowed moments (μ_I, μ_G, E[I² + G²], E[IG]) → S(q) and the
 //              three partials ∂S/∂μ_I, ∂S/∂E[I²], ∂S/∂E[IG] (to workspace), plus
 //              block-reduced Σ S and Σ|I − G| (fp64 atomics);
 //   ssim_bwd:  the partial maps windowed again (the transpose of the
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float
                                                       float* __restrict__ pmaps,
                                                       double* __restrict__ acc) {
   __shared__ float sI[LS][LS + 1], sG[LS][LS + 1];
-  __shared__ float sH[5][LS][LT + 1];
+  __shared__ float sH[4][LS][LT + 1];   // μ_I, μ_G, E[I² + G²], E[IG] (B2 needs only σ_I² + σ_G²)
   __shared__ double s_red[2][8];
   const int ch = blockIdx.z;
   const size_t np = (size_t)W * H;
@@ -74,45 +74,44 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float
   __syncthreads();
   if (t < HTASKS) {
     const int r = t >> 2, c0 = (t & 3) * HS;
-    float xi[HS + 10], xg[HS + 10], xii[HS + 10], xgg[HS + 10], xig[HS + 10];
+    float xi[HS + 10], xg[HS + 10], xsq[HS + 10], xig[HS + 10];
 #pragma unroll
     for (int k = 0; k < HS + 10; ++k) {
       xi[k] = sI[r][c0 + k]; xg[k] = sG[r][c0 + k];
-      xii[k] = xi[k] * xi[k]; xgg[k] = xg[k] * xg[k]; xig[k] = xi[k] * xg[k];
+      xsq[k] = fmaf(xi[k], xi[k], xg[k] * xg[k]); xig[k] = xi[k] * xg[k];
     }
 #pragma unroll
     for (int o = 0; o < HS; ++o) {
-      float a = 0.f, b = 0.f, aa = 0.f, bb = 0.f, ab = 0.f;
+      float a = 0.f, b = 0.f, sq = 0.f, ab = 0.f;
 #pragma unroll
       for (int d = 0; d < 11; ++d) {
         const float w = win.w[d];
-        a = fmaf(w, xi[o + d], a); b = fmaf(w, xg[o + d], b); aa = fmaf(w, xii[o + d], aa);
-        bb = fmaf(w, xgg[o + d], bb); ab = fmaf(w, xig[o + d], ab);
+        a = fmaf(w, xi[o + d], a); b = fmaf(w, xg[o + d], b);
+        sq = fmaf(w, xsq[o + d], sq); ab = fmaf(w, xig[o + d], ab);
       }
-      sH[0][r][c0 + o] = a; sH[1][r][c0 + o] = b; sH[2][r][c0 + o] = aa;
-      sH[3][r][c0 + o] = bb; sH[4][r][c0 + o] = ab;
+      sH[0][r][c0 + o] = a; sH[1][r][c0 + o] = b; sH[2][r][c0 + o] = sq; sH[3][r][c0 + o] = ab;
     }
   }
   __syncthreads();
   const int c = t & 31, r0 = (t >> 5) * VS;
   const int gx = x0 + c;
-  float m[VS][5];
+  float m[VS][4];
 #pragma unroll
   for (int o = 0; o < VS; ++o)
 #pragma unroll
-    for (int q = 0; q < 5; ++q) m[o][q] = 0.f;
+    for (int q = 0; q < 4; ++q) m[o][q] = 0.f;
 #pragma unroll
   for (int k = 0; k < VS + 10; ++k) {
-    float v[5];
+    float v[4];
 #pragma unroll
-    for (int q = 0; q < 5; ++q) v[q] = sH[q][r0 + k][c];
+    for (int q = 0; q < 4; ++q) v[q] = sH[q][r0 + k][c];
 #pragma unroll
     for (int o = 0; o < VS; ++o) {
       const int d = k - o;
       if (d >= 0 && d < 11) {
         const float w = win.w[d];
 #pragma unroll
-        for (int q = 0; q < 5; ++q) m[o][q] = fmaf(w, v[q], m[o][q]);
+        for (int q = 0; q < 4; ++q) m[o][q] = fmaf(w, v[q], m[o][q]);
       }
     }
   }
@@ -123,9 +122,9 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float
     const int r = r0 + o, gy = y0 + r;
     if (gy >= H || gx >= W) continue;
     const float m1 = m[o][0], m2 = m[o][1];
-    const float v1 = m[o][2] - m1 * m1, v2 = m[o][3] - m2 * m2, v12 = m[o][4] - m1 * m2;
+    const float v12 = m[o][3] - m1 * m2;
     const float A1 = 2.f * m1 * m2 + SSIM_C1, A2 = 2.f * v12 + SSIM_C2;
-    const float B1 = m1 * m1 + m2 * m2 + SSIM_C1, B2 = v1 + v2 + SSIM_C2;
+    const float B1 = m1 * m1 + m2 * m2 + SSIM_C1, B2 = (m[o][2] - m1 * m1 - m2 * m2) + SSIM_C2;
     const float iB = 1.f / (B1 * B2);
     const float S = A1 * A2 * iB;
     sum_s += S;
