@@ -53,7 +53,7 @@ def parse():
     p.add_argument("--n", type=int, default=300_000)
     p.add_argument("--views", type=int, default=20)
     p.add_argument("--capacity", type=int, default=1 << 22, help="pair capacity per view")
-    p.add_argument("--streams", type=int, default=4, help="overlapping per-view streams")
+    p.add_argument("--streams", type=int, default=20, help="overlapping per-view streams")
     p.add_argument("--no-graph", action="store_true", help="do not capture the step in a CUDA graph")
     p.add_argument("--lean", action="store_true",
                    help="only warm-up + timed steps (no stats/diagnostic passes): for ncu launch lists")
