@@ -86,8 +86,9 @@ def check_grad(a, ref, kap):
 
 @pytest.fixture(params=["tcgen05", "simt"])
 def fwd_path(request, monkeypatch):
-    """Both forward implementations: the tcgen05 3×TF32 kernel (default) and the
-    FP32 SIMT kernel (DASS_DEFORM_TC=0)."""
+    """Both implementations: the tcgen05 3×TF32 kernels (default; the backward's
+    tcgen05 kernel serves the F = 4 field) and the FP32 SIMT kernels
+    (DASS_DEFORM_TC=0)."""
     if request.param == "simt":
         monkeypatch.setenv("DASS_DEFORM_TC", "0")
     else:
@@ -125,7 +126,7 @@ def test_identity_at_initialisation(fwd_path):
 
 
 @pytest.mark.parametrize("profile,n", [("n3dv", 60_000), ("meetroom", 9_000)])
-def test_backward_parity(profile, n):
+def test_backward_parity(profile, n, fwd_path):
     sc = synth.n3dv_scene(n=n, seed=75, degree=0)
     fd, fs = synth.dual_fields(sc, profile, seed=76)
     gm, gs = synth.offset_grads(sc.n, 77, scale=1e-3)
