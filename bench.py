@@ -42,6 +42,8 @@ FP32_LANES = 128
 # part (FMA = 2 flop).  Rejected in-box evaluations are not
 # counted, so the reported fraction is conservative.
 FLOP_BWD_ACCEPTED = 48
+STEP_OPS = ("project_views", "bin_sort", "render_fwd", "render_bwd_raster",
+            "render_bwd_preprocess_views")
 
 
 def parse():
@@ -553,7 +555,13 @@ def run_ours(args):
                          "traffic_source": "profiles/r01_ncu_render_bwd.txt (ncu --set full, dram read+write per launch = one view)",
                          "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz ({pk_kind} clock)",
                          "units_per_step": {"accepted": sum(stats["accepted"]), "P_bwd": sum(stats["P_bwd"])},
-                         "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED}},
+                         "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED},
+                         "timing": "isolated launches: one sequential pass over the step's kernels "
+                                   "(CUDA events on the launching stream), since in the timed "
+                                   "graph the per-view kernels of 20 streams overlap",
+                         "share_of_step_kernels": round(ops.get("render_bwd_raster", 0.0) /
+                                                        max(sum(v for k, v in ops.items() if k in STEP_OPS), 1e-9), 4),
+                         "ncu_share_source": "profiles/r01_launches.txt"},
             "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
             "rows_roofline": rows_roofline(ops, densify, allst, pk, peak_tflops, n, W, H,
                                            len(my_cams), deg),
