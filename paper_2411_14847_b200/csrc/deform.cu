@@ -1293,7 +1293,7 @@ template <int F>
 cudaError_t fwd_launch(const HashGridParams& g, const float* table, const float* mlp, int n,
                        const int* idx, const int* count, const float4* pos_opa, float4* mu,
                        float4* sigma, cudaStream_t s) {
-  if (use_tc()) {
+  if (use_tc() && g.in % 8 == 0) {   // kind::tf32 consumes K in steps of 8
     const size_t sm = fwd_tc_smem(g.in);
     cudaError_t e = cudaFuncSetAttribute(deform_fwd_tc_kernel<F>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1329,7 +1329,7 @@ cudaError_t bwd_launch(const HashGridParams& g, const float* table, const float*
   // 287 → 243 µs for 90k Gaussians).  For 𝓗_st (F = 2, in = 16) its serialised per-tile
   // MMA/epilogue phases cost more than they save (415 → 444 µs), so the SIMT kernel runs;
   // in > 32 would not fit the M = 64 operands in shared memory.
-  if (use_tc() && F == 4 && g.in <= 32) {
+  if (use_tc() && F == 4 && g.in <= 32 && g.in % 8 == 0) {
     const size_t sm = bwd_tc_smem(g.in);
     cudaError_t e = cudaFuncSetAttribute(deform_bwd_tc_kernel<F>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -192,3 +192,26 @@ def test_invalid_config_rejected():
     bad.aabb_max[0] = bad.aabb_min[0]
     with pytest.raises(dass.DassError):
         dass.dass_deform_fwd(bad, tab, mlp, pos, mu, sg)
+
+
+@pytest.mark.parametrize("levels,log2T,F", [(16, 12, 4), (4, 10, 1), (6, 11, 2), (12, 9, 4)])
+def test_other_field_shapes(levels, log2T, F, fwd_path):
+    """Configurations beyond the N3DV/Meet-Room profiles: in = 64 (the largest
+    MLP input; SIMT backward), F = 1, and odd level counts, with ragged tiles."""
+    sc = synth.n3dv_scene(n=3_001, seed=90 + levels, degree=0)
+    box = synth.scene_aabb(sc.pos_opa)
+    res = tuple(int(round(8 * 1.4 ** l)) for l in range(levels))
+    f = synth.hash_field(log2T, F, box, seed=91, levels=levels, res=res)
+    pos = t(sc.pos_opa)
+    mu, sg = run_fwd(f, pos, None)
+    rmu, rsg, tie = oracle.deform(f, sc.pos_opa)
+    check_fwd(mu, sg, rmu, rsg)
+    gm, gs = synth.offset_grads(sc.n, 92, scale=1e-3)
+    rows = np.flatnonzero(tie == 0)
+    gt_ref, gp_ref, kt, km = oracle.deform_bwd(f, sc.pos_opa[rows], gm[rows], gs[rows], kappa=True)
+    tab, mlp = device_field(f)
+    g_tab = torch.zeros_like(tab); g_mlp = torch.zeros_like(mlp)
+    dass.dass_deform_bwd(f, tab, mlp, pos, t(gm), t(gs), g_tab, g_mlp, idx=t(rows.astype(np.int32)))
+    torch.cuda.synchronize()
+    check_grad(np_(g_tab).astype(np.float64), gt_ref, kt)
+    check_grad(np_(g_mlp).astype(np.float64), gp_ref, km)

@@ -168,3 +168,24 @@ def test_feature_render_parity(case):
     torch.cuda.synchronize()
     assert torch.equal(out4[:3], ras.img)
     assert torch.count_nonzero(out4[3]) == 0
+
+
+def test_spawn_edge_cases():
+    """m = 0 (copy only), K = 3, SH degree 0 and no dynamics flags."""
+    sc = synth.n3dv_scene(n=777, seed=93, degree=0)
+    k4 = synth.sh_planes(0)
+    for m, K in ((0, 2), (5, 3)):
+        sel = np.arange(0, 5 * m, 5, dtype=np.int32)[:m]
+        n_out = sc.n + m * K
+        out = [torch.full((n_out, 4), np.nan, device=DEV) for _ in range(3)]
+        out_sh = torch.full((k4, n_out, 4), np.nan, device=DEV)
+        dass.dass_spawn(0, t(sc.pos_opa), t(sc.scale), t(sc.rot), t(sc.sh), None, m,
+                        t(sel) if m else None, K, 2.0, 0.05, 11, out[0], out[1], out[2], out_sh)
+        torch.cuda.synchronize()
+        assert np.array_equal(np_(out[0])[:sc.n], sc.pos_opa)
+        if m:
+            ref_po, ref_s = oracle.spawn(sel, K, 2.0, 0.05, 11, sc.pos_opa, sc.scale, sc.rot)
+            po = np_(out[0])[sc.n:]
+            assert np.all(np.abs(po[:, :3] - ref_po[:, :3]) <= 1e-6 * (1 + np.abs(ref_po[:, :3])) + 1e-5)
+            np.testing.assert_allclose(np_(out[1])[sc.n:, :3], ref_s[:, :3], rtol=1e-6)
+        assert np.isfinite(np_(out_sh)).all()
