@@ -62,6 +62,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-views", type=int, default=10)
+    p.add_argument("--emulate", default=None, metavar="R/W",
+                   help="diagnostic: run rank R's share of a W-GPU view plan on this one GPU "
+                        "(no collective) — predicts per-rank step time for --gpus W")
     return p.parse_args()
 
 
@@ -126,7 +129,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2411_14847_b200 import dass, synth
-    from paper_2411_14847_b200.dist import FlatGrads, allreduce_grads, shard
+    from paper_2411_14847_b200.dist import FlatGrads, allreduce_grads, view_plan
     from paper_2411_14847_b200.pipeline import (DeformFields, DeviceScene, MultiViewPass, Raster,
                                                 ViewRecords)
 
@@ -138,7 +141,12 @@ def run_ours(args):
 
     cams, scene = synth.c3(n=args.n, num_views=args.views)
     mu, sigma = synth.shift_offsets(scene, seed=33)
-    mine = shard(len(cams), rank, world)
+    W0, H0 = cams[0].width, cams[0].height
+    plan_rank, plan_world = rank, world
+    if args.emulate:
+        plan_rank, plan_world = (int(x) for x in args.emulate.split("/"))
+    plan = view_plan(len(cams), plan_rank, plan_world, ((W0 + 15) // 16) * ((H0 + 15) // 16))
+    mine = plan.views
     my_cams = [cams[v] for v in mine]
     W, H = cams[0].width, cams[0].height
     n = scene.n
@@ -154,11 +162,17 @@ def run_ours(args):
     dLs = torch.stack([t(synth.grad_image(cams[v], 1000 + v, 1.0 / (3 * W * H))) for v in mine]) \
         if mine else torch.empty(0, 3, H, W, device=dev)
     # one flat gradient buffer = the all_reduce payload (dist.FlatGrads)
-    grads = FlatGrads.allocate(n, K4, dev)
+    grads = FlatGrads.allocate(n, K4, dev, num_split=plan.num_split)
     flat, g_mu, g_sigma = grads.flat, grads.g_mu, grads.g_sigma
     records = ViewRecords(max(len(mine), 1), n, dev)
     raster = Raster(W, H, n, args.capacity, dev)   # single-stream scratch for stats/diagnostics
-    mvp = MultiViewPass(my_cams, n, args.capacity, dev, streams=args.streams) if my_cams else None
+    uv_out = [None if sidx < 0 else grads.uv[sidx] for sidx in plan.split]
+    mvp = MultiViewPass(my_cams, n, args.capacity, dev, streams=args.streams, tiles=plan.tiles,
+                        uv_out=uv_out) if my_cams else None
+
+    def finish_split(g):
+        """∇p̄ of the views split across ranks, from their reduced uv partials."""
+        dass.dass_gradstat_from_uv(g.uv, g.gradstat_sum, g.gradstat_cnt)
 
     def step_local():
         """Everything on this GPU (capturable: no host sync, no collective)."""
@@ -180,7 +194,7 @@ def run_ours(args):
         else:
             graph.replay()
         if world > 1:
-            allreduce_grads(grads)   # the one cross-GPU exchange (NCCL over NVLink)
+            allreduce_grads(grads, finish=finish_split)   # the one cross-GPU exchange (NCCL)
 
     def step():
         run_step(None)
@@ -197,6 +211,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     cnt = torch.zeros(8, dtype=torch.int64, device=dev)
     for k, cam in enumerate([] if args.lean else my_cams):
+        if plan.tiles[k] is not None and plan.tiles[k][0] != 0:
+            continue   # a split view's statistics are counted once, by the rank with half 0
         rec = records.view(k)
         K = raster.forward(cam, rec, host_mode=True)
         dass.dass_render_stats(cam, raster.ranges, raster.sorted_ids, rec[0], rec[1], rec[3],
@@ -245,11 +261,27 @@ def run_ours(args):
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_step = float(ms_t.item())
 
+    # ---- the collective's share of the step: the same all_reduce
+    # (+ split-view ∇p̄ finish) timed alone, max over ranks
+    allreduce = None
+    if world > 1:
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a0.record()
+        for _ in range(5):
+            allreduce_grads(grads, finish=finish_split)
+        a1.record()
+        barrier()
+        ar = torch.tensor([a0.elapsed_time(a1) / 5], device=dev)
+        dist.all_reduce(ar, op=dist.ReduceOp.MAX)
+        allreduce = {"ms": round(float(ar.item()), 4), "share_of_step": round(float(ar.item()) / ms_step, 4),
+                     "bytes": int(grads.flat.numel() * 4 + grads.gradstat_cnt.numel() * 4)}
+
     # ---- the full training iteration: ∂L/∂C from the fused fidelity loss of
     # Eq. 3 against per-view ground truth (the render of 𝒢_{t−1} before the
     # shift), instead of a fixed ∂L/∂C.  Reported next to the metric.
     train = None
-    if my_cams and not args.lean:
+    if my_cams and not args.lean and plan.num_split == 0:   # SSIM needs whole views
         mvp.enable_loss(0.2)
         gts = torch.empty(len(my_cams), 3, H, W, device=dev)
         dass.dass_project_views(my_cams, deg, base.pos_opa, base.scale, base.rot, base.sh, None,
@@ -299,7 +331,7 @@ def run_ours(args):
             else:
                 tgraph.replay()
             if world > 1:
-                allreduce_grads(grads)
+                allreduce_grads(grads, finish=finish_split)
                 for x in fields.grad_tensors():
                     dist.all_reduce(x)
         t1.record()
@@ -535,7 +567,9 @@ def run_ours(args):
         flops = sum(a * FLOP_BWD_ACCEPTED for a in stats["accepted"])
         bwd_ms = ops.get("render_bwd_raster", float("nan"))
         achieved = flops / (bwd_ms / 1e3) / 1e12 if bwd_ms == bwd_ms and bwd_ms > 0 else None
-        views_s = len(cams) / (ms_step / 1e3)
+        # whole-job views/s; an --emulate run reports its own share (whole views + halves)
+        views_done = len(cams) if not args.emulate else sum(1.0 if t is None else 0.5 for t in plan.tiles)
+        views_s = views_done / (ms_step / 1e3)
         result = {
             "metric": METRIC, "value": round(views_s, 3), "unit": "views/s",
             "mpix_per_s": round(views_s * W * H / 1e6, 1),
@@ -545,7 +579,9 @@ def run_ours(args):
             "config": {"workload": WORKLOAD, "n_gaussians": n, "views": len(cams), "width": W,
                        "height": H, "sh_degree": deg, "dynamic_frac": 0.3,
                        "cuda_graph": graph is not None, "streams": args.streams,
-                       "parallelism": f"view-sharded dp{world}",
+                       "emulated_share": args.emulate,
+                       "parallelism": f"view-sharded dp{world}" + (
+                           f" ({plan.num_split} views split into tile halves)" if plan.num_split else ""),
                        "l2": "inputs larger than L2 (≈0.5 GB of params, dL/dC and records per step)"},
             "roofline": {"bound": "alu", "kernel": "render_bwd_list_kernel<4> via dass_render_bwd_raster (accepted units only)",
                          "achieved": None if achieved is None else round(achieved, 2),
@@ -572,6 +608,7 @@ def run_ours(args):
                             "early_terminated_frac": float(np.sum(allst["terminated_px"]) / (len(allst["K"]) * W * H)),
                             "tile_list_mean": float(np.mean(allst["tile_list_mean"])),
                             "tile_list_max": int(np.max(allst["tile_list_max"]))},
+            "allreduce": allreduce,
             "training_step_with_loss": train,
             "densification_f4": densify,
             "gpu_launches": int(launches),

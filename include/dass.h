@@ -323,6 +323,57 @@ int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views,
                                      uint32_t* gradstat_cnt, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Tile subsets and split views (multi-GPU load balance).  A view
+ * can be rendered in parts: each part is a tile subset, and the parts' results
+ * add up to the whole view.
+ *
+ * dass_render_fwd_tiles / dass_render_bwd_raster_tiles: as dass_render_fwd /
+ *   dass_render_bwd_raster, restricted to tiles tile_begin + k·tile_stride,
+ *   k < tile_count (tile index = ty·tiles_x + tx; tile_count < 0 = every tile).
+ *   Only those tiles' pixels are written.  g2d is overwritten with the subset's
+ *   partial moments; moments are sums over pixels, so the subsets' g2d add up to
+ *   the whole view's.  INVALID_ARG: tile_stride < 1, tile_begin < 0, or a
+ *   subset reaching past the last tile.
+ *
+ * dass_render_bwd_preprocess_views_uv: dass_render_bwd_preprocess_views with
+ *   uv_out, a host array of num_views device pointers (array nullable; entries
+ *   nullable, else 16-byte aligned float4[n]).  Every gradient is linear in g2d,
+ *   so partial-view moments give partial gradients, except the ∇p̄ norm.  For a
+ *   view with uv_out[v] set, the kernel therefore adds to uv_out[v][i], instead
+ *   of the ∇p̄ terms,
+ *     (∂L/∂u·W/2, ∂L/∂v·H/2, 1, 0)     for every Gaussian visible in the view.
+ *   The caller sums these partials (e.g. inside the gradient all_reduce).
+ * dass_gradstat_from_uv: then, for the num_split reduced blocks
+ *   uv[num_split][n] (float4), adds gradstat_sum[i] += ‖(x, y)‖₂ and
+ *   gradstat_cnt[i] += 1 wherever z > 0 — exactly the terms the whole views
+ *   would have contributed (A23).
+ * ------------------------------------------------------------------------- */
+int dass_render_fwd_tiles(const dass_camera* cam, int32_t tile_begin, int32_t tile_stride,
+                          int32_t tile_count, const uint32_t* tile_ranges,
+                          const uint32_t* sorted_ids, const float* xy_depth,
+                          const float* conic_opa, const float* rgb, const uint32_t* box,
+                          const float* bg, float* out_img, float* out_T, uint32_t* out_last,
+                          void* accept, int64_t pair_capacity, void* stream);
+int dass_render_bwd_raster_tiles(const dass_camera* cam, int32_t tile_begin, int32_t tile_stride,
+                                 int32_t tile_count, int32_t n, const uint32_t* tile_ranges,
+                                 const uint32_t* sorted_ids, const float* xy_depth,
+                                 const float* conic_opa, const float* rgb, const uint32_t* box,
+                                 const float* bg, const float* out_T, const uint32_t* out_last,
+                                 const float* dL_dimg, const void* accept, int64_t pair_capacity,
+                                 float* g2d, void* stream);
+int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_views, int32_t n,
+                                        int32_t sh_degree, const float* pos_opa,
+                                        const float* scale, const float* rot, const float* sh,
+                                        const uint8_t* keep_mask, const float* conic_opa,
+                                        const float* rgb, const uint32_t* box, const float* g2d,
+                                        float* g_pos_opa, float* g_scale, float* g_rot,
+                                        float* g_sh, float* gradstat_sum,
+                                        uint32_t* gradstat_cnt, float* const* uv_out,
+                                        void* stream);
+int dass_gradstat_from_uv(int32_t n, int32_t num_split, const float* uv, float* gradstat_sum,
+                          uint32_t* gradstat_cnt, void* stream);
+
+/* ---------------------------------------------------------------------------
  * dass_fidelity_loss — the fidelity loss of Eq. 3, "the fidelity
  * loss in the vanilla 3DGS": L = (1−λ)·L1 + λ·(1 − SSIM) (A39), with
  *   L1 = mean over the 3·H·W values of |img − gt|;

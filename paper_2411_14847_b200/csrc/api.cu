@@ -52,6 +52,9 @@ static CamParams to_params(const dass_camera* c) {
     p.campos[a] = -(c->viewmat[0 * 4 + a] * c->viewmat[3] + c->viewmat[1 * 4 + a] * c->viewmat[7] +
                     c->viewmat[2 * 4 + a] * c->viewmat[11]);
   for (int i = 0; i < 16; ++i) p.T[i] = c->full_proj[i];
+  p.tile0 = 0;
+  p.tstride = 1;
+  p.tcount = p.tiles_x * p.tiles_y;
   return p;
 }
 
@@ -237,10 +240,24 @@ int dass_render_accept_workspace(int32_t num_tiles, int64_t pair_capacity, size_
   return DASS_OK;
 }
 
-int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges, const uint32_t* sorted_ids,
-                    const float* xy_depth, const float* conic_opa, const float* rgb,
-                    const uint32_t* box, const float* bg, float* out_img, float* out_T,
-                    uint32_t* out_last, void* accept, int64_t pair_capacity, void* stream) {
+static int tile_subset(const dass_camera* cam, int32_t tile_begin, int32_t tile_stride,
+                       int32_t tile_count, CamParams* cp) {
+  const int nt = cp->tiles_x * cp->tiles_y;
+  if (tile_count < 0) { cp->tile0 = 0; cp->tstride = 1; cp->tcount = nt; return DASS_OK; }
+  if (tile_stride < 1 || tile_begin < 0 ||
+      (tile_count > 0 && (int64_t)tile_begin + (int64_t)(tile_count - 1) * tile_stride >= nt))
+    return fail(DASS_ERR_INVALID_ARG, "tile subset outside the image's tiles%s");
+  cp->tile0 = tile_begin; cp->tstride = tile_stride; cp->tcount = tile_count;
+  (void)cam;
+  return DASS_OK;
+}
+
+int dass_render_fwd_tiles(const dass_camera* cam, int32_t tile_begin, int32_t tile_stride,
+                          int32_t tile_count, const uint32_t* tile_ranges,
+                          const uint32_t* sorted_ids, const float* xy_depth,
+                          const float* conic_opa, const float* rgb, const uint32_t* box,
+                          const float* bg, float* out_img, float* out_T, uint32_t* out_last,
+                          void* accept, int64_t pair_capacity, void* stream) {
   int st = check_camera(cam);
   if (st) return st;
   if (!tile_ranges || !out_img || !out_T || !out_last)
@@ -250,12 +267,22 @@ int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges, const u
   if (accept && (pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30) || !aligned16(accept)))
     return fail(DASS_ERR_INVALID_ARG, "dass_render_fwd: accept needs a 16-byte aligned buffer and 0 <= pair_capacity < 2^30%s");
   CamParams cp = to_params(cam);
+  if ((st = tile_subset(cam, tile_begin, tile_stride, tile_count, &cp))) return st;
+  if (cp.tcount == 0) return DASS_OK;
   float3 b = bg ? make_float3(bg[0], bg[1], bg[2]) : make_float3(0.f, 0.f, 0.f);
   return cuda_status(launch_render_fwd(cp, (const uint2*)tile_ranges, sorted_ids,
                                        (const float4*)xy_depth, (const float4*)conic_opa,
                                        (const float4*)rgb, (const uint2*)box, b, out_img, out_T,
                                        out_last, accept, pair_capacity, (cudaStream_t)stream),
                      "dass_render_fwd");
+}
+
+int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges, const uint32_t* sorted_ids,
+                    const float* xy_depth, const float* conic_opa, const float* rgb,
+                    const uint32_t* box, const float* bg, float* out_img, float* out_T,
+                    uint32_t* out_last, void* accept, int64_t pair_capacity, void* stream) {
+  return dass_render_fwd_tiles(cam, 0, 1, -1, tile_ranges, sorted_ids, xy_depth, conic_opa, rgb,
+                               box, bg, out_img, out_T, out_last, accept, pair_capacity, stream);
 }
 
 int dass_render_bwd_workspace(int32_t n, size_t* bytes) {
@@ -297,12 +324,13 @@ int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree, const 
       "dass_render_bwd");
 }
 
-int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* tile_ranges,
-                           const uint32_t* sorted_ids, const float* xy_depth,
-                           const float* conic_opa, const float* rgb, const uint32_t* box,
-                           const float* bg, const float* out_T, const uint32_t* out_last,
-                           const float* dL_dimg, const void* accept, int64_t pair_capacity,
-                           float* g2d, void* stream) {
+int dass_render_bwd_raster_tiles(const dass_camera* cam, int32_t tile_begin, int32_t tile_stride,
+                                 int32_t tile_count, int32_t n, const uint32_t* tile_ranges,
+                                 const uint32_t* sorted_ids, const float* xy_depth,
+                                 const float* conic_opa, const float* rgb, const uint32_t* box,
+                                 const float* bg, const float* out_T, const uint32_t* out_last,
+                                 const float* dL_dimg, const void* accept, int64_t pair_capacity,
+                                 float* g2d, void* stream) {
   int st = check_camera(cam);
   if (st) return st;
   if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
@@ -312,6 +340,7 @@ int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* ti
     return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_raster: null required pointer%s");
   if (!aligned16(g2d)) return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_raster: g2d must be 16-byte aligned%s");
   CamParams cp = to_params(cam);
+  if ((st = tile_subset(cam, tile_begin, tile_stride, tile_count, &cp))) return st;
   float3 b = bg ? make_float3(bg[0], bg[1], bg[2]) : make_float3(0.f, 0.f, 0.f);
   return cuda_status(launch_render_bwd_raster(cp, n, (const uint2*)tile_ranges, sorted_ids,
                                               (const float4*)xy_depth, (const float4*)conic_opa,
@@ -321,14 +350,26 @@ int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* ti
                      "dass_render_bwd_raster");
 }
 
-int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views, int32_t n,
-                                     int32_t sh_degree, const float* pos_opa,
-                                     const float* scale, const float* rot, const float* sh,
-                                     const uint8_t* keep_mask, const float* conic_opa,
-                                     const float* rgb, const uint32_t* box, const float* g2d,
-                                     float* g_pos_opa, float* g_scale, float* g_rot,
-                                     float* g_sh, float* gradstat_sum,
-                                     uint32_t* gradstat_cnt, void* stream) {
+int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* tile_ranges,
+                           const uint32_t* sorted_ids, const float* xy_depth,
+                           const float* conic_opa, const float* rgb, const uint32_t* box,
+                           const float* bg, const float* out_T, const uint32_t* out_last,
+                           const float* dL_dimg, const void* accept, int64_t pair_capacity,
+                           float* g2d, void* stream) {
+  return dass_render_bwd_raster_tiles(cam, 0, 1, -1, n, tile_ranges, sorted_ids, xy_depth,
+                                      conic_opa, rgb, box, bg, out_T, out_last, dL_dimg, accept,
+                                      pair_capacity, g2d, stream);
+}
+
+int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_views, int32_t n,
+                                        int32_t sh_degree, const float* pos_opa,
+                                        const float* scale, const float* rot, const float* sh,
+                                        const uint8_t* keep_mask, const float* conic_opa,
+                                        const float* rgb, const uint32_t* box, const float* g2d,
+                                        float* g_pos_opa, float* g_scale, float* g_rot,
+                                        float* g_sh, float* gradstat_sum,
+                                        uint32_t* gradstat_cnt, float* const* uv_out,
+                                        void* stream) {
   if (cams == nullptr) return fail(DASS_ERR_INVALID_ARG, "cams is null%s");
   if (num_views < 1 || num_views > 64) return fail(DASS_ERR_INVALID_ARG, "num_views must be in [1, 64]%s");
   for (int v = 0; v < num_views; ++v) {
@@ -340,6 +381,10 @@ int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views,
   if (n == 0) return DASS_OK;
   if (!pos_opa || !scale || !rot || !sh || !conic_opa || !rgb || !box || !g2d)
     return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_preprocess_views: null required pointer%s");
+  if (uv_out)
+    for (int v = 0; v < num_views; ++v)
+      if (uv_out[v] && !aligned16(uv_out[v]))
+        return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_preprocess_views: uv_out must be 16-byte aligned%s");
   CamParams cp[64];
   for (int v = 0; v < num_views; ++v) cp[v] = to_params(cams + v);
   return cuda_status(launch_preprocess_views(cp, num_views, n, sh_degree, (const float4*)pos_opa,
@@ -349,8 +394,34 @@ int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views,
                                              (const uint2*)box, (const float4*)g2d,
                                              (float4*)g_pos_opa, (float4*)g_scale,
                                              (float4*)g_rot, (float4*)g_sh, gradstat_sum,
-                                             gradstat_cnt, (cudaStream_t)stream),
+                                             gradstat_cnt,
+                                             reinterpret_cast<float4* const*>(uv_out),
+                                             (cudaStream_t)stream),
                      "dass_render_bwd_preprocess_views");
+}
+
+int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views, int32_t n,
+                                     int32_t sh_degree, const float* pos_opa,
+                                     const float* scale, const float* rot, const float* sh,
+                                     const uint8_t* keep_mask, const float* conic_opa,
+                                     const float* rgb, const uint32_t* box, const float* g2d,
+                                     float* g_pos_opa, float* g_scale, float* g_rot,
+                                     float* g_sh, float* gradstat_sum,
+                                     uint32_t* gradstat_cnt, void* stream) {
+  return dass_render_bwd_preprocess_views_uv(cams, num_views, n, sh_degree, pos_opa, scale, rot,
+                                             sh, keep_mask, conic_opa, rgb, box, g2d, g_pos_opa,
+                                             g_scale, g_rot, g_sh, gradstat_sum, gradstat_cnt,
+                                             nullptr, stream);
+}
+
+int dass_gradstat_from_uv(int32_t n, int32_t num_split, const float* uv, float* gradstat_sum,
+                          uint32_t* gradstat_cnt, void* stream) {
+  if (n < 0 || num_split < 0) return fail(DASS_ERR_INVALID_ARG, "n and num_split must be >= 0%s");
+  if (n == 0 || num_split == 0) return DASS_OK;
+  if (!uv || !aligned16(uv)) return fail(DASS_ERR_INVALID_ARG, "dass_gradstat_from_uv: uv null or misaligned%s");
+  return cuda_status(launch_gradstat_uv(n, num_split, (const float4*)uv, gradstat_sum,
+                                        gradstat_cnt, (cudaStream_t)stream),
+                     "dass_gradstat_from_uv");
 }
 
 int dass_fidelity_loss_workspace(int32_t width, int32_t height, size_t* bytes) {

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
   constexpr int NW = NT / 32;
   constexpr int BATCH = 2 * NT;
   __shared__ Staged s_st[BATCH];
-  const int tile = blockIdx.x;
+  const int tile = cam.tile0 + blockIdx.x * cam.tstride;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
   const int t = threadIdx.x;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(64) render_features_kernel(
   constexpr int BATCH = 2 * NT;
   __shared__ Staged s_st[BATCH];
   __shared__ float4 s_f[BATCH][NV];
-  const int tile = blockIdx.x;
+  const int tile = cam.tile0 + blockIdx.x * cam.tstride;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
   const int t = threadIdx.x;
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
   __shared__ uint32_t s_id[BATCH];
   __shared__ float s_acc[NW][BATCH][9];
   __shared__ uint32_t s_wlast[NW];
-  const int tile = blockIdx.x;
+  const int tile = cam.tile0 + blockIdx.x * cam.tstride;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
   const int t = threadIdx.x;
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
   __shared__ uint4 s_bytes[NW][32][2];   // 32 acceptance bytes per staged entry
   __shared__ uint32_t s_id[NW][32];
   __shared__ float s_acc[NW][32][9];
-  const int tile = blockIdx.x;
+  const int tile = cam.tile0 + blockIdx.x * cam.tstride;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
   const int t = threadIdx.x;
@@ -688,6 +688,10 @@ struct PreArgs {
   float4* g_sh;
   float* gradstat_sum;
   uint32_t* gradstat_cnt;
+  // per view (nullable): instead of adding ‖(∂L/∂u·W/2, ∂L/∂v·H/2)‖ and 1 to the
+  // ∇p̄ statistic, add (∂L/∂u·W/2, ∂L/∂v·H/2, 1, 0) to uv_out[v][i] — the view is
+  // split across GPUs and the norm is taken after the partial sums are reduced
+  float4* uv_out[PRE_MAXV];
 };
 
 // PART 1: geometry (p, s, q, o, ∇p̄ and the SH direction term), fp64 chain.
@@ -734,7 +738,7 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? 3 : 2) prep
 #pragma unroll
   for (int f = 0; f < NGSH; ++f) gsh[f] = 0.f;
   float gstat = 0.f;
-  uint32_t nvis = 0;
+  uint32_t nvis = 0, ncnt = 0;
   for (int v = 0; v < a.num_views; ++v) {
     const size_t o = (size_t)v * n + i;
     const uint2 bx = a.box[o];
@@ -765,7 +769,14 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? 3 : 2) prep
     go += m1.y;
     {
       const F ga = gu * 0.5 * cam.W, gb = gv * 0.5 * cam.H;
-      gstat += (float)sqrt(ga * ga + gb * gb);
+      if (a.uv_out[v] != nullptr) {
+        float4 u = a.uv_out[v][i];
+        u.x += (float)ga; u.y += (float)gb; u.z += 1.f;
+        a.uv_out[v][i] = u;
+      } else {
+        gstat += (float)sqrt(ga * ga + gb * gb);
+        ++ncnt;
+      }
     }
     // ---- colour / SH (direction from this view's camera centre)
     {
@@ -881,7 +892,7 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? 3 : 2) prep
     return;
   }
   if (a.gradstat_sum) a.gradstat_sum[i] += gstat;
-  if (a.gradstat_cnt) a.gradstat_cnt[i] += nvis;
+  if (a.gradstat_cnt) a.gradstat_cnt[i] += ncnt;
   if (a.g_pos_opa) {
     float4 gpo = a.g_pos_opa[i];
     gpo.x += (float)gp[0]; gpo.y += (float)gp[1]; gpo.z += (float)gp[2];
@@ -984,7 +995,7 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
       return e ? atoi(e) : 12;
     }();
 #define FWDL(R, M)                                                                               \
-  render_fwd_kernel<4, true, R, M><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
+  render_fwd_kernel<4, true, R, M><<<cam.tcount, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
                                                          box, bg, out_img, out_T, out_last, acc)
     if (rpw == 8) FWDL(8, 12);
     else if (fminb == 16) FWDL(16, 16);
@@ -997,7 +1008,7 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
   }
   const AcceptLists none{nullptr, nullptr, nullptr};
 #define FWD(P)                                                                                    \
-  render_fwd_kernel<P, false><<<ntiles, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
+  render_fwd_kernel<P, false><<<cam.tcount, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
                                                          box, bg, out_img, out_T, out_last, none)
   switch (fwd_ppt()) {
     case 1: FWD(1); break;
@@ -1017,7 +1028,7 @@ cudaError_t launch_render_features(const CamParams& cam, const uint2* ranges, co
   const int ntiles = cam.tiles_x * cam.tiles_y;
   const float4* f4 = reinterpret_cast<const float4*>(feat);
 #define FEAT(NV)                                                                                 \
-  render_features_kernel<NV><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, box, f4, out)
+  render_features_kernel<NV><<<cam.tcount, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, box, f4, out)
   switch (channels / 4) {
     case 1: FEAT(1); break;
     case 2: FEAT(2); break;
@@ -1039,6 +1050,7 @@ cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* r
                                      float4* g2d, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(g2d, 0, render_bwd_workspace(n), s);
   if (e != cudaSuccess) return e;
+  if (cam.tcount == 0) return cudaSuccess;
   const int ntiles = cam.tiles_x * cam.tiles_y;
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(const_cast<void*>(accept), ntiles, capacity);
@@ -1047,7 +1059,7 @@ cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* r
       return e ? atoi(e) : 12;   // 80 registers: measured best (16 → 64 regs rematerialises)
     }();
 #define BWDL(M)                                                                                  \
-  render_bwd_list_kernel<4, M><<<ntiles, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg, \
+  render_bwd_list_kernel<4, M><<<cam.tcount, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg, \
                                                      out_T, dL_dimg, acc, g2d)
     switch (lminb) {
       case 8: BWDL(8); break;
@@ -1060,7 +1072,7 @@ cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* r
     return cudaGetLastError();
   }
 #define BWD(P, MB)                                                                          \
-  render_bwd_raster_kernel<P, MB><<<ntiles, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, \
+  render_bwd_raster_kernel<P, MB><<<cam.tcount, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, \
                                                              rgb, box, bg, out_T, out_last, dL_dimg, g2d)
   switch (bwd_ppt() * 100 + bwd_minb()) {
     case 116: BWD(1, 4); break;
@@ -1081,7 +1093,8 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
                                     const float4* conic_opa, const float4* rgb, const uint2* box,
                                     const float4* g2d, float4* g_pos_opa, float4* g_scale,
                                     float4* g_rot, float4* g_sh, float* gradstat_sum,
-                                    uint32_t* gradstat_cnt, cudaStream_t s) {
+                                    uint32_t* gradstat_cnt, float4* const* uv_out,
+                                    cudaStream_t s) {
   for (int v0 = 0; v0 < num_views; v0 += PRE_MAXV) {
     PreArgs a;
     a.num_views = num_views - v0 < PRE_MAXV ? num_views - v0 : PRE_MAXV;
@@ -1092,6 +1105,8 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
     a.conic_opa = conic_opa + off; a.rgb = rgb + off; a.box = box + off; a.g2d = g2d + 3 * off;
     a.g_pos_opa = g_pos_opa; a.g_scale = g_scale; a.g_rot = g_rot; a.g_sh = g_sh;
     a.gradstat_sum = gradstat_sum; a.gradstat_cnt = gradstat_cnt;
+    for (int v = 0; v < PRE_MAXV; ++v)
+      a.uv_out[v] = (uv_out != nullptr && v < a.num_views) ? uv_out[v0 + v] : nullptr;
     const int grid = div_up(n, 256);
     switch (sh_degree) {
 #define PRE(D)                                                                \
@@ -1110,6 +1125,36 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
   return cudaSuccess;
 }
 
+// ∇p̄ terms of views split across GPUs, after their (∂L/∂u·W/2, ∂L/∂v·H/2, vis)
+// partial sums were reduced: += ‖(x, y)‖ and += 1 where the view saw the Gaussian.
+__global__ void __launch_bounds__(256) gradstat_uv_kernel(int n, int S, const float4* __restrict__ uv,
+                                                         float* __restrict__ gsum,
+                                                         uint32_t* __restrict__ gcnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float sacc = 0.f;
+  uint32_t c = 0;
+  for (int k = 0; k < S; ++k) {
+    const float4 u = uv[(size_t)k * n + i];
+    if (u.z > 0.f) {
+      sacc += (float)sqrt((double)u.x * u.x + (double)u.y * u.y);
+      ++c;
+    }
+  }
+  if (c) {
+    if (gsum) gsum[i] += sacc;
+    if (gcnt) gcnt[i] += c;
+  }
+}
+
+cudaError_t launch_gradstat_uv(int n, int S, const float4* uv, float* gsum, uint32_t* gcnt,
+                               cudaStream_t s) {
+  if (n == 0 || S == 0) return cudaSuccess;
+  gradstat_uv_kernel<<<div_up(n, 256), 256, 0, s>>>(n, S, uv, gsum, gcnt);
+  launch_counted();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const float4* pos_opa,
                               const float4* scale, const float4* rot, const float4* sh,
                               const uint8_t* keep, const uint2* ranges, const uint32_t* ids,
@@ -1125,7 +1170,7 @@ cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const 
   if (e != cudaSuccess) return e;
   return launch_preprocess_views(&cam, 1, n, sh_degree, pos_opa, scale, rot, sh, keep, conic_opa,
                                  rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh, gradstat_sum,
-                                 gradstat_cnt, s);
+                                 gradstat_cnt, nullptr, s);
 }
 
 }  // namespace dass

@@ -33,7 +33,8 @@ EXPORTS = (
     "dass_inherit_mask_bwd", "dass_error_map", "dass_render_stats",
     "dass_deform_param_count", "dass_deform_fwd", "dass_deform_bwd", "dass_partition_workspace",
     "dass_partition", "dass_densify_select", "dass_spawn", "dass_prune_select", "dass_gather",
-    "dass_render_features",
+    "dass_render_features", "dass_render_fwd_tiles", "dass_render_bwd_raster_tiles",
+    "dass_render_bwd_preprocess_views_uv", "dass_gradstat_from_uv",
 )
 
 
@@ -132,6 +133,13 @@ def lib():
         L.dass_prune_select.argtypes = [i32, i32, P, C.c_float, P, P, P, P, C.c_size_t, P]
         L.dass_gather.argtypes = [i32, i32, P, P, P, P, P, i32, P, P, P, P, P, P, P]
         L.dass_render_features.argtypes = [P, P, P, P, P, P, i32, P, P, P]
+        L.dass_render_fwd_tiles.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P,
+                                            i64, P]
+        L.dass_render_bwd_raster_tiles.argtypes = [P, i32, i32, i32, i32, P, P, P, P, P, P, P, P,
+                                                   P, P, P, i64, P, P]
+        L.dass_render_bwd_preprocess_views_uv.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P,
+                                                          P, P, P, P, P, P, P, P, P, P]
+        L.dass_gradstat_from_uv.argtypes = [i32, i32, P, P, P, P]
         _lib = L
     return _lib
 
@@ -242,13 +250,16 @@ def dass_render_accept_workspace(num_tiles, pair_capacity) -> int:
 
 
 def dass_render_fwd(cam, tile_ranges, sorted_ids, xy_depth, conic_opa, rgb, box, bg, out_img,
-                    out_T, out_last, accept=None, pair_capacity=0, stream=None):
+                    out_T, out_last, accept=None, pair_capacity=0, stream=None, tiles=None):
+    """tiles = (begin, stride, count): render only that tile subset (dass_render_fwd_tiles)."""
     c = _cam(cam)
     b = None if bg is None else (C.c_float * 3)(*[float(x) for x in bg])
-    _check(lib().dass_render_fwd(C.byref(c), _ptr(tile_ranges), _ptr(sorted_ids), _ptr(xy_depth),
-                                 _ptr(conic_opa), _ptr(rgb), _ptr(box), b, _ptr(out_img),
-                                 _ptr(out_T), _ptr(out_last), _ptr(accept), pair_capacity,
-                                 _stream(stream)), "dass_render_fwd")
+    tb, ts, tc = tiles if tiles is not None else (0, 1, -1)
+    _check(lib().dass_render_fwd_tiles(C.byref(c), int(tb), int(ts), int(tc), _ptr(tile_ranges),
+                                       _ptr(sorted_ids), _ptr(xy_depth), _ptr(conic_opa),
+                                       _ptr(rgb), _ptr(box), b, _ptr(out_img), _ptr(out_T),
+                                       _ptr(out_last), _ptr(accept), pair_capacity,
+                                       _stream(stream)), "dass_render_fwd")
 
 
 def dass_render_bwd_workspace(n) -> int:
@@ -276,25 +287,42 @@ def dass_render_bwd(cam, sh_degree, pos_opa, scale, rot, sh, keep_mask, tile_ran
 
 def dass_render_bwd_raster(cam, n, tile_ranges, sorted_ids, xy_depth, conic_opa, rgb, box, bg,
                            out_T, out_last, dL_dimg, g2d, accept=None, pair_capacity=0,
-                           stream=None):
+                           stream=None, tiles=None):
+    """tiles = (begin, stride, count): the tile subset's partial moments."""
     c = _cam(cam)
     b = None if bg is None else (C.c_float * 3)(*[float(x) for x in bg])
-    _check(lib().dass_render_bwd_raster(C.byref(c), n, _ptr(tile_ranges), _ptr(sorted_ids),
-                                        _ptr(xy_depth), _ptr(conic_opa), _ptr(rgb), _ptr(box), b,
-                                        _ptr(out_T), _ptr(out_last), _ptr(dL_dimg), _ptr(accept),
-                                        pair_capacity, _ptr(g2d), _stream(stream)),
-           "dass_render_bwd_raster")
+    tb, ts, tc = tiles if tiles is not None else (0, 1, -1)
+    _check(lib().dass_render_bwd_raster_tiles(C.byref(c), int(tb), int(ts), int(tc), n,
+                                              _ptr(tile_ranges), _ptr(sorted_ids), _ptr(xy_depth),
+                                              _ptr(conic_opa), _ptr(rgb), _ptr(box), b,
+                                              _ptr(out_T), _ptr(out_last), _ptr(dL_dimg),
+                                              _ptr(accept), pair_capacity, _ptr(g2d),
+                                              _stream(stream)), "dass_render_bwd_raster")
 
 
 def dass_render_bwd_preprocess_views(cams, sh_degree, pos_opa, scale, rot, sh, keep_mask,
                                      conic_opa, rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh,
-                                     gradstat_sum, gradstat_cnt, stream=None):
+                                     gradstat_sum, gradstat_cnt, stream=None, uv_out=None):
+    """uv_out: per view None or a float4[n] tensor — split views add their
+    (∂L/∂u·W/2, ∂L/∂v·H/2, 1, 0) there instead of the ∇p̄ terms."""
     arr = (dass_camera * len(cams))(*[_cam(c) for c in cams])
-    _check(lib().dass_render_bwd_preprocess_views(
+    uv = None
+    if uv_out is not None:
+        if len(uv_out) != len(cams):
+            raise ValueError("uv_out needs one entry per view")
+        uv = (C.c_void_p * len(cams))(*[None if u is None else _ptr(u).value for u in uv_out])
+    _check(lib().dass_render_bwd_preprocess_views_uv(
         arr, len(cams), pos_opa.shape[0], sh_degree, _ptr(pos_opa), _ptr(scale), _ptr(rot),
         _ptr(sh), _ptr(keep_mask), _ptr(conic_opa), _ptr(rgb), _ptr(box), _ptr(g2d),
         _ptr(g_pos_opa), _ptr(g_scale), _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum),
-        _ptr(gradstat_cnt), _stream(stream)), "dass_render_bwd_preprocess_views")
+        _ptr(gradstat_cnt), uv, _stream(stream)), "dass_render_bwd_preprocess_views")
+
+
+def dass_gradstat_from_uv(uv, gradstat_sum, gradstat_cnt, stream=None):
+    """∇p̄ terms of split views from their reduced uv blocks (float4 [S][n])."""
+    S, n = uv.shape[0], uv.shape[1]
+    _check(lib().dass_gradstat_from_uv(n, S, _ptr(uv), _ptr(gradstat_sum), _ptr(gradstat_cnt),
+                                       _stream(stream)), "dass_gradstat_from_uv")
 
 
 def dass_fidelity_loss_workspace(width, height) -> int:

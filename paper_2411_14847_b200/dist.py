@@ -22,6 +22,57 @@ def shard(num_views: int, rank: int, world: int) -> list[int]:
 
 
 @dataclass
+class ViewPlan:
+    """This rank's share of a timestep's views.
+
+    views: global view indices rendered here; tiles[k] = None for a whole view,
+    else (begin, 2, count) — one of the view's two interleaved tile halves
+    (a checkerboard over tile indices, so both halves see the same content);
+    split[k] = the view's index among all split views, or -1; num_split = the
+    number of views split across ranks (the uv blocks of FlatGrads)."""
+    views: list
+    tiles: list
+    split: list
+    num_split: int
+
+
+def view_plan(num_views: int, rank: int, world: int, num_tiles: int) -> ViewPlan:
+    """Balanced view sharding.  When the views divide evenly,
+    whole views in contiguous blocks (shard()).  Otherwise, when twice the views
+    divide evenly, every view is cut into two interleaved tile halves and each
+    rank takes a contiguous block of halves: 20 views at 8 GPUs → 5 halves each
+    (2 whole views + 1 half) instead of 3,3,3,3,2,2,2,2 views.  A view whose
+    halves land on two ranks is 'split'; its ∇p̄ terms are formed after the
+    all-reduce (dass_gradstat_from_uv).  Anything else falls back to shard()."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    if num_views % world == 0 or (2 * num_views) % world != 0 or num_tiles < 2:
+        v = shard(num_views, rank, world)
+        return ViewPlan(v, [None] * len(v), [-1] * len(v), 0)
+    per = 2 * num_views // world
+    owner = [u // per for u in range(2 * num_views)]             # unit u = 2·view + half
+    split_ids, nsplit = {}, 0
+    for v in range(num_views):
+        if owner[2 * v] != owner[2 * v + 1]:
+            split_ids[v] = nsplit
+            nsplit += 1
+    views, tiles, split = [], [], []
+    for u in range(rank * per, (rank + 1) * per):
+        v, h = divmod(u, 2)
+        if views and views[-1] == v:              # both halves here: the whole view
+            tiles[-1], split[-1] = None, -1
+            continue
+        views.append(v)
+        if v in split_ids:
+            tiles.append((h, 2, (num_tiles - h + 1) // 2))
+            split.append(split_ids[v])
+        else:
+            tiles.append(None)
+            split.append(-1)
+    return ViewPlan(views, tiles, split, nsplit)
+
+
+@dataclass
 class FlatGrads:
     """All per-Gaussian gradient outputs as views of one contiguous buffer, so
     the cross-GPU sum is a single collective: pos_opa, scale, rot [N,4];
@@ -36,16 +87,18 @@ class FlatGrads:
     g_sigma: "torch.Tensor"
     gradstat_sum: "torch.Tensor"
     gradstat_cnt: "torch.Tensor"
+    uv: "torch.Tensor | None" = None     # [S][N][4] split-view ∇p̄ partials (ViewPlan)
 
     @staticmethod
-    def allocate(n: int, k4: int, device="cuda") -> "FlatGrads":
+    def allocate(n: int, k4: int, device="cuda", num_split: int = 0) -> "FlatGrads":
         import torch
-        sizes = [n * 4, n * 4, n * 4, k4 * n * 4, n * 4, n * 4, n]
+        sizes = [num_split * n * 4, n * 4, n * 4, n * 4, k4 * n * 4, n * 4, n * 4, n]
         flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
-        p = list(torch.split(flat, sizes))
-        return FlatGrads(flat, p[0].view(n, 4), p[1].view(n, 4), p[2].view(n, 4),
-                         p[3].view(k4, n, 4), p[4].view(n, 4), p[5].view(n, 4), p[6],
-                         torch.zeros(n, dtype=torch.int32, device=device))
+        p = list(torch.split(flat, sizes))    # uv first: 16-byte aligned like the float4 fields
+        uv = p[0].view(num_split, n, 4) if num_split else None
+        return FlatGrads(flat, p[1].view(n, 4), p[2].view(n, 4), p[3].view(n, 4),
+                         p[4].view(k4, n, 4), p[5].view(n, 4), p[6].view(n, 4), p[7],
+                         torch.zeros(n, dtype=torch.int32, device=device), uv)
 
     @property
     def nbytes(self) -> int:
@@ -56,12 +109,16 @@ class FlatGrads:
         self.gradstat_cnt.zero_()
 
 
-def allreduce_grads(g: FlatGrads, group=None, counts: bool = True):
-    """SUM over ranks of every gradient (A27: gradients are summed over views)."""
+def allreduce_grads(g: FlatGrads, group=None, counts: bool = True, finish=None):
+    """SUM over ranks of every gradient (A27: gradients are summed over views).
+    With split views (g.uv), `finish(g)` then adds their ∇p̄ terms from the
+    reduced uv blocks (dass_gradstat_from_uv), identically on every rank."""
     import torch.distributed as dist
     dist.all_reduce(g.flat, op=dist.ReduceOp.SUM, group=group)
     if counts:
         dist.all_reduce(g.gradstat_cnt, op=dist.ReduceOp.SUM, group=group)
+    if g.uv is not None and finish is not None:
+        finish(g)
 
 
 def allreduce_s_err(s_err, group=None):

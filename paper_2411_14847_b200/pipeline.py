@@ -111,13 +111,13 @@ class Raster:
             ab = dass.dass_render_accept_workspace(self.num_tiles, capacity)
             self.accept = torch.empty(ab // 4, dtype=torch.int32, device=device)
 
-    def forward(self, cam, rec, host_mode=False, bg=None, sorted_keys=None):
-        xy, co, rgb, box, tiles = rec
-        K = dass.dass_bin_sort(cam, self.n, xy, box, tiles, self.sort_ws, self.capacity,
+    def forward(self, cam, rec, host_mode=False, bg=None, sorted_keys=None, tiles=None):
+        xy, co, rgb, box, tt = rec
+        K = dass.dass_bin_sort(cam, self.n, xy, box, tt, self.sort_ws, self.capacity,
                                sorted_keys, self.sorted_ids, self.ranges, self.num_pairs,
                                host_mode=host_mode)
         dass.dass_render_fwd(cam, self.ranges, self.sorted_ids, xy, co, rgb, box, bg, self.img,
-                             self.T, self.last, self.accept, self.capacity)
+                             self.T, self.last, self.accept, self.capacity, tiles=tiles)
         return K
 
     def backward(self, cam, scene: DeviceScene, rec, dL_dimg, grads: Grads, keep=None, bg=None,
@@ -152,9 +152,15 @@ def fwd_bwd_views(cams, scene: DeviceScene, records: ViewRecords, raster: Raster
 class MultiViewPass:
     """fwd+bwd over a fixed list of cameras with S overlapping streams."""
 
-    def __init__(self, cams, n: int, capacity: int, device="cuda", streams: int = 4):
+    def __init__(self, cams, n: int, capacity: int, device="cuda", streams: int = 4,
+                 tiles=None, uv_out=None):
+        """tiles[v]: None or a (begin, stride, count) tile subset of view v (a
+        split view, dist.ViewPlan); uv_out[v]: None or the float4[n] block that
+        view's ∇p̄ partials go to."""
         torch = _torch()
         self.cams = list(cams)
+        self.tiles = list(tiles) if tiles is not None else [None] * len(self.cams)
+        self.uv_out = list(uv_out) if uv_out is not None else [None] * len(self.cams)
         self.V = len(self.cams)
         self.n = n
         W, H = self.cams[0].width, self.cams[0].height
@@ -201,7 +207,7 @@ class MultiViewPass:
             with torch.cuda.stream(st):
                 rec = records.view(v)
                 xy, co, rgb, box, tiles = rec
-                ras.forward(cam, rec, bg=bg)
+                ras.forward(cam, rec, bg=bg, tiles=self.tiles[v])
                 if gts is not None:
                     dL = self.loss_dL[k]
                     dass.dass_fidelity_loss(ras.img, gts[v], self.lam, self.loss_ws[k],
@@ -210,7 +216,7 @@ class MultiViewPass:
                     dL = dL_dimgs[v]
                 dass.dass_render_bwd_raster(cam, self.n, ras.ranges, ras.sorted_ids, xy, co, rgb,
                                             box, bg, ras.T, ras.last, dL, self.g2d[v],
-                                            ras.accept, ras.capacity)
+                                            ras.accept, ras.capacity, tiles=self.tiles[v])
             if v in ends:
                 c = ends[v]
                 self.pre_stream.wait_stream(main)
@@ -229,7 +235,8 @@ class MultiViewPass:
             self.cams[v0:v1], scene.sh_degree, scene.pos_opa, scene.scale, scene.rot, scene.sh,
             keep, records.conic_opa[v0:v1], records.rgb[v0:v1], records.box[v0:v1],
             self.g2d[v0:v1], grads.pos_opa, grads.scale, grads.rot, grads.sh,
-            grads.gradstat_sum, grads.gradstat_cnt)
+            grads.gradstat_sum, grads.gradstat_cnt,
+            uv_out=None if all(u is None for u in self.uv_out[v0:v1]) else self.uv_out[v0:v1])
 
 
 class DeformFields:

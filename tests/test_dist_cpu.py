@@ -103,3 +103,77 @@ def test_gloo_world2_sum_equals_single_process(tmp_path):
     expect[0::7] = 1
     expect[1::7] = 1
     assert np.array_equal(r["s_err"], expect)
+
+
+def test_view_plan_balances_halves():
+    """20 views at 8 ranks: 5 tile halves each (2 whole views + 1 half); every
+    view's two halves covered exactly once; no splits when the views divide."""
+    from paper_2411_14847_b200.dist import view_plan
+    T = 85 * 64
+    for world in (1, 2, 4, 5, 10, 20):
+        for r in range(world):
+            p = view_plan(20, r, world, T)
+            assert p.num_split == 0 and all(t is None for t in p.tiles)
+    plans = [view_plan(20, r, 8, T) for r in range(8)]
+    halves = {}
+    for r, p in enumerate(plans):
+        assert p.num_split == 4
+        work = sum(1.0 if t is None else 0.5 for t in p.tiles)
+        assert work == 2.5
+        for v, t, s in zip(p.views, p.tiles, p.split):
+            if t is None:
+                halves.setdefault(v, []).extend([0, 1])
+                assert s == -1
+            else:
+                begin, stride, count = t
+                assert stride == 2 and count == (T - begin + 1) // 2 and s >= 0
+                halves.setdefault(v, []).append(begin)
+    assert sorted(halves) == list(range(20))
+    assert all(sorted(h) == [0, 1] for h in halves.values())
+    split_views = sorted({v for p in plans for v, s in zip(p.views, p.split) if s >= 0})
+    ids = {v: s for p in plans for v, s in zip(p.views, p.split) if s >= 0}
+    assert [ids[v] for v in split_views] == list(range(4))
+    # 3 ranks: 40 halves do not divide either → whole views (shard)
+    p3 = [view_plan(20, r, 3, T) for r in range(3)]
+    assert sum(len(p.views) for p in p3) == 20 and all(p.num_split == 0 for p in p3)
+
+
+def _uv_worker(rank, world, port, out_path):
+    """Each rank holds one half of a split view: its uv partial (x, y, vis) goes
+    through the same all_reduce as the gradients, then `finish` forms ∇p̄."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 50
+    g = ddist.FlatGrads.allocate(n, 3, device="cpu", num_split=2)
+    rng = np.random.default_rng(rank)
+    g.uv[:, :, :2] = torch.from_numpy(rng.normal(size=(2, n, 2))).float()
+    g.uv[:, ::3, :2] = 0.0                                   # not visible in the split views
+    g.uv[:, :, 2] = 1.0
+    g.uv[:, ::3, 2] = 0.0
+    g.gradstat_sum += 1.0
+
+    def finish(gg):   # the CPU form of dass_gradstat_from_uv
+        u = gg.uv
+        vis = u[..., 2] > 0
+        gg.gradstat_sum += (torch.sqrt(u[..., 0] ** 2 + u[..., 1] ** 2) * vis).sum(0)
+        gg.gradstat_cnt += vis.sum(0).int()
+
+    ddist.allreduce_grads(g, finish=finish)
+    if rank == 0:
+        np.savez(out_path, stat=g.gradstat_sum.numpy(), cnt=g.gradstat_cnt.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_split_view_uv_blocks_through_allreduce(tmp_path):
+    out = str(tmp_path / "uv.npz")
+    mp.spawn(_uv_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r = np.load(out)
+    n = 50
+    parts = [np.random.default_rng(k).normal(size=(2, n, 2)) for k in range(2)]
+    tot = (parts[0] + parts[1]).astype(np.float32)
+    vis = np.ones(n, bool)
+    vis[::3] = False
+    want = 2.0 + (np.sqrt((tot ** 2).sum(-1)) * vis).sum(0)
+    np.testing.assert_allclose(r["stat"], want, rtol=1e-5)
+    assert np.array_equal(r["cnt"], 2 * vis.astype(np.int32))
