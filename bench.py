@@ -172,7 +172,7 @@ def run_ours(args):
 
     def finish_split(g):
         """∇p̄ of the views split across ranks, from their reduced uv partials."""
-        dass.dass_gradstat_from_uv(g.uv, g.gradstat_sum, g.gradstat_cnt)
+        dass.dass_gradstat_from_uv(g.uv, g.gradstat_sum)
 
     def step_local():
         """Everything on this GPU (capturable: no host sync, no collective)."""

@@ -337,16 +337,18 @@ int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views,
  *
  * dass_render_bwd_preprocess_views_uv: dass_render_bwd_preprocess_views with
  *   uv_out, a host array of num_views device pointers (array nullable; entries
- *   nullable, else 16-byte aligned float4[n]).  Every gradient is linear in g2d,
- *   so partial-view moments give partial gradients, except the ∇p̄ norm.  For a
- *   view with uv_out[v] set, the kernel therefore adds to uv_out[v][i], instead
- *   of the ∇p̄ terms,
- *     (∂L/∂u·W/2, ∂L/∂v·H/2, 1, 0)     for every Gaussian visible in the view.
- *   The caller sums these partials (e.g. inside the gradient all_reduce).
+ *   nullable, else 8-byte aligned float2[n]), and uv_count, a host uint8 array
+ *   (nullable).  Every gradient is linear in g2d, so partial-view moments give
+ *   partial gradients, except the ∇p̄ norm.  For a view with uv_out[v] set, the
+ *   kernel therefore adds to uv_out[v][i], instead of the norm,
+ *     (∂L/∂u·W/2, ∂L/∂v·H/2)           for every Gaussian visible in the view,
+ *   and adds the view's gradstat_cnt term only if uv_count[v] ≠ 0 (exactly one
+ *   of the GPUs sharing a view sets it: visibility is the same on each).  The
+ *   caller sums the partials (e.g. inside the gradient all_reduce).
  * dass_gradstat_from_uv: then, for the num_split reduced blocks
- *   uv[num_split][n] (float4), adds gradstat_sum[i] += ‖(x, y)‖₂ and
- *   gradstat_cnt[i] += 1 wherever z > 0 — exactly the terms the whole views
- *   would have contributed (A23).
+ *   uv[num_split][n] (float2), adds gradstat_sum[i] += Σ_k ‖uv[k][i]‖₂ — the
+ *   terms the whole views would have contributed (A23; an invisible Gaussian
+ *   has (0, 0) and adds nothing in either form).
  * ------------------------------------------------------------------------- */
 int dass_render_fwd_tiles(const dass_camera* cam, int32_t tile_begin, int32_t tile_stride,
                           int32_t tile_count, const uint32_t* tile_ranges,
@@ -369,9 +371,9 @@ int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_vie
                                         float* g_pos_opa, float* g_scale, float* g_rot,
                                         float* g_sh, float* gradstat_sum,
                                         uint32_t* gradstat_cnt, float* const* uv_out,
-                                        void* stream);
+                                        const uint8_t* uv_count, void* stream);
 int dass_gradstat_from_uv(int32_t n, int32_t num_split, const float* uv, float* gradstat_sum,
-                          uint32_t* gradstat_cnt, void* stream);
+                          void* stream);
 
 /* ---------------------------------------------------------------------------
  * dass_fidelity_loss — the fidelity loss of Eq. 3, "the fidelity

@@ -369,7 +369,7 @@ int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_vie
                                         float* g_pos_opa, float* g_scale, float* g_rot,
                                         float* g_sh, float* gradstat_sum,
                                         uint32_t* gradstat_cnt, float* const* uv_out,
-                                        void* stream) {
+                                        const uint8_t* uv_count, void* stream) {
   if (cams == nullptr) return fail(DASS_ERR_INVALID_ARG, "cams is null%s");
   if (num_views < 1 || num_views > 64) return fail(DASS_ERR_INVALID_ARG, "num_views must be in [1, 64]%s");
   for (int v = 0; v < num_views; ++v) {
@@ -383,8 +383,8 @@ int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_vie
     return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_preprocess_views: null required pointer%s");
   if (uv_out)
     for (int v = 0; v < num_views; ++v)
-      if (uv_out[v] && !aligned16(uv_out[v]))
-        return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_preprocess_views: uv_out must be 16-byte aligned%s");
+      if (uv_out[v] && ((uintptr_t)uv_out[v] & 7u))
+        return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_preprocess_views: uv_out must be 8-byte aligned%s");
   CamParams cp[64];
   for (int v = 0; v < num_views; ++v) cp[v] = to_params(cams + v);
   return cuda_status(launch_preprocess_views(cp, num_views, n, sh_degree, (const float4*)pos_opa,
@@ -395,7 +395,7 @@ int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_vie
                                              (float4*)g_pos_opa, (float4*)g_scale,
                                              (float4*)g_rot, (float4*)g_sh, gradstat_sum,
                                              gradstat_cnt,
-                                             reinterpret_cast<float4* const*>(uv_out),
+                                             reinterpret_cast<float2* const*>(uv_out), uv_count,
                                              (cudaStream_t)stream),
                      "dass_render_bwd_preprocess_views");
 }
@@ -411,16 +411,17 @@ int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views,
   return dass_render_bwd_preprocess_views_uv(cams, num_views, n, sh_degree, pos_opa, scale, rot,
                                              sh, keep_mask, conic_opa, rgb, box, g2d, g_pos_opa,
                                              g_scale, g_rot, g_sh, gradstat_sum, gradstat_cnt,
-                                             nullptr, stream);
+                                             nullptr, nullptr, stream);
 }
 
 int dass_gradstat_from_uv(int32_t n, int32_t num_split, const float* uv, float* gradstat_sum,
-                          uint32_t* gradstat_cnt, void* stream) {
+                          void* stream) {
   if (n < 0 || num_split < 0) return fail(DASS_ERR_INVALID_ARG, "n and num_split must be >= 0%s");
   if (n == 0 || num_split == 0) return DASS_OK;
-  if (!uv || !aligned16(uv)) return fail(DASS_ERR_INVALID_ARG, "dass_gradstat_from_uv: uv null or misaligned%s");
-  return cuda_status(launch_gradstat_uv(n, num_split, (const float4*)uv, gradstat_sum,
-                                        gradstat_cnt, (cudaStream_t)stream),
+  if (!uv || ((uintptr_t)uv & 7u) || !gradstat_sum)
+    return fail(DASS_ERR_INVALID_ARG, "dass_gradstat_from_uv: null or misaligned pointer%s");
+  return cuda_status(launch_gradstat_uv(n, num_split, (const float2*)uv, gradstat_sum,
+                                        (cudaStream_t)stream),
                      "dass_gradstat_from_uv");
 }
 

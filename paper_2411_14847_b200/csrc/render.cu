@@ -688,10 +688,12 @@ struct PreArgs {
   float4* g_sh;
   float* gradstat_sum;
   uint32_t* gradstat_cnt;
-  // per view (nullable): instead of adding ‖(∂L/∂u·W/2, ∂L/∂v·H/2)‖ and 1 to the
-  // ∇p̄ statistic, add (∂L/∂u·W/2, ∂L/∂v·H/2, 1, 0) to uv_out[v][i] — the view is
-  // split across GPUs and the norm is taken after the partial sums are reduced
-  float4* uv_out[PRE_MAXV];
+  // per view (nullable): instead of adding ‖(∂L/∂u·W/2, ∂L/∂v·H/2)‖ to the ∇p̄
+  // statistic, add (∂L/∂u·W/2, ∂L/∂v·H/2) to uv_out[v][i] — the view is split
+  // across GPUs and the norm is taken after the partial sums are reduced; the
+  // visibility count of such a view is added only where bit v of uv_count is set
+  float2* uv_out[PRE_MAXV];
+  uint32_t uv_count;
 };
 
 // PART 1: geometry (p, s, q, o, ∇p̄ and the SH direction term), fp64 chain.
@@ -770,9 +772,10 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? 3 : 2) prep
     {
       const F ga = gu * 0.5 * cam.W, gb = gv * 0.5 * cam.H;
       if (a.uv_out[v] != nullptr) {
-        float4 u = a.uv_out[v][i];
-        u.x += (float)ga; u.y += (float)gb; u.z += 1.f;
+        float2 u = a.uv_out[v][i];
+        u.x += (float)ga; u.y += (float)gb;
         a.uv_out[v][i] = u;
+        if ((a.uv_count >> v) & 1u) ++ncnt;
       } else {
         gstat += (float)sqrt(ga * ga + gb * gb);
         ++ncnt;
@@ -1093,8 +1096,8 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
                                     const float4* conic_opa, const float4* rgb, const uint2* box,
                                     const float4* g2d, float4* g_pos_opa, float4* g_scale,
                                     float4* g_rot, float4* g_sh, float* gradstat_sum,
-                                    uint32_t* gradstat_cnt, float4* const* uv_out,
-                                    cudaStream_t s) {
+                                    uint32_t* gradstat_cnt, float2* const* uv_out,
+                                    const uint8_t* uv_count, cudaStream_t s) {
   for (int v0 = 0; v0 < num_views; v0 += PRE_MAXV) {
     PreArgs a;
     a.num_views = num_views - v0 < PRE_MAXV ? num_views - v0 : PRE_MAXV;
@@ -1105,8 +1108,11 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
     a.conic_opa = conic_opa + off; a.rgb = rgb + off; a.box = box + off; a.g2d = g2d + 3 * off;
     a.g_pos_opa = g_pos_opa; a.g_scale = g_scale; a.g_rot = g_rot; a.g_sh = g_sh;
     a.gradstat_sum = gradstat_sum; a.gradstat_cnt = gradstat_cnt;
-    for (int v = 0; v < PRE_MAXV; ++v)
+    a.uv_count = 0;
+    for (int v = 0; v < PRE_MAXV; ++v) {
       a.uv_out[v] = (uv_out != nullptr && v < a.num_views) ? uv_out[v0 + v] : nullptr;
+      if (a.uv_out[v] && uv_count && uv_count[v0 + v]) a.uv_count |= 1u << v;
+    }
     const int grid = div_up(n, 256);
     switch (sh_degree) {
 #define PRE(D)                                                                \
@@ -1127,30 +1133,22 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
 
 // ∇p̄ terms of views split across GPUs, after their (∂L/∂u·W/2, ∂L/∂v·H/2, vis)
 // partial sums were reduced: += ‖(x, y)‖ and += 1 where the view saw the Gaussian.
-__global__ void __launch_bounds__(256) gradstat_uv_kernel(int n, int S, const float4* __restrict__ uv,
-                                                         float* __restrict__ gsum,
-                                                         uint32_t* __restrict__ gcnt) {
+// (an invisible Gaussian has (0, 0) and adds nothing, as in the whole-view path)
+__global__ void __launch_bounds__(256) gradstat_uv_kernel(int n, int S, const float2* __restrict__ uv,
+                                                         float* __restrict__ gsum) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float sacc = 0.f;
-  uint32_t c = 0;
   for (int k = 0; k < S; ++k) {
-    const float4 u = uv[(size_t)k * n + i];
-    if (u.z > 0.f) {
-      sacc += (float)sqrt((double)u.x * u.x + (double)u.y * u.y);
-      ++c;
-    }
+    const float2 u = uv[(size_t)k * n + i];
+    sacc += (float)sqrt((double)u.x * u.x + (double)u.y * u.y);
   }
-  if (c) {
-    if (gsum) gsum[i] += sacc;
-    if (gcnt) gcnt[i] += c;
-  }
+  gsum[i] += sacc;
 }
 
-cudaError_t launch_gradstat_uv(int n, int S, const float4* uv, float* gsum, uint32_t* gcnt,
-                               cudaStream_t s) {
+cudaError_t launch_gradstat_uv(int n, int S, const float2* uv, float* gsum, cudaStream_t s) {
   if (n == 0 || S == 0) return cudaSuccess;
-  gradstat_uv_kernel<<<div_up(n, 256), 256, 0, s>>>(n, S, uv, gsum, gcnt);
+  gradstat_uv_kernel<<<div_up(n, 256), 256, 0, s>>>(n, S, uv, gsum);
   launch_counted();
   return cudaGetLastError();
 }
@@ -1170,7 +1168,7 @@ cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const 
   if (e != cudaSuccess) return e;
   return launch_preprocess_views(&cam, 1, n, sh_degree, pos_opa, scale, rot, sh, keep, conic_opa,
                                  rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh, gradstat_sum,
-                                 gradstat_cnt, nullptr, s);
+                                 gradstat_cnt, nullptr, nullptr, s);
 }
 
 }  // namespace dass

@@ -138,8 +138,8 @@ def lib():
         L.dass_render_bwd_raster_tiles.argtypes = [P, i32, i32, i32, i32, P, P, P, P, P, P, P, P,
                                                    P, P, P, i64, P, P]
         L.dass_render_bwd_preprocess_views_uv.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P,
-                                                          P, P, P, P, P, P, P, P, P, P]
-        L.dass_gradstat_from_uv.argtypes = [i32, i32, P, P, P, P]
+                                                          P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_gradstat_from_uv.argtypes = [i32, i32, P, P, P]
         _lib = L
     return _lib
 
@@ -302,27 +302,31 @@ def dass_render_bwd_raster(cam, n, tile_ranges, sorted_ids, xy_depth, conic_opa,
 
 def dass_render_bwd_preprocess_views(cams, sh_degree, pos_opa, scale, rot, sh, keep_mask,
                                      conic_opa, rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh,
-                                     gradstat_sum, gradstat_cnt, stream=None, uv_out=None):
-    """uv_out: per view None or a float4[n] tensor — split views add their
-    (∂L/∂u·W/2, ∂L/∂v·H/2, 1, 0) there instead of the ∇p̄ terms."""
+                                     gradstat_sum, gradstat_cnt, stream=None, uv_out=None,
+                                     uv_count=None):
+    """uv_out: per view None or a float2[n] tensor — split views add their
+    (∂L/∂u·W/2, ∂L/∂v·H/2) there instead of the ∇p̄ norm; uv_count[v] truthy:
+    this GPU adds the split view's visibility count (one GPU per view)."""
     arr = (dass_camera * len(cams))(*[_cam(c) for c in cams])
-    uv = None
+    uv = cnt = None
     if uv_out is not None:
         if len(uv_out) != len(cams):
             raise ValueError("uv_out needs one entry per view")
         uv = (C.c_void_p * len(cams))(*[None if u is None else _ptr(u).value for u in uv_out])
+        flags = uv_count if uv_count is not None else [0] * len(cams)
+        cnt = (C.c_uint8 * len(cams))(*[1 if f else 0 for f in flags])
     _check(lib().dass_render_bwd_preprocess_views_uv(
         arr, len(cams), pos_opa.shape[0], sh_degree, _ptr(pos_opa), _ptr(scale), _ptr(rot),
         _ptr(sh), _ptr(keep_mask), _ptr(conic_opa), _ptr(rgb), _ptr(box), _ptr(g2d),
         _ptr(g_pos_opa), _ptr(g_scale), _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum),
-        _ptr(gradstat_cnt), uv, _stream(stream)), "dass_render_bwd_preprocess_views")
+        _ptr(gradstat_cnt), uv, cnt, _stream(stream)), "dass_render_bwd_preprocess_views")
 
 
-def dass_gradstat_from_uv(uv, gradstat_sum, gradstat_cnt, stream=None):
-    """∇p̄ terms of split views from their reduced uv blocks (float4 [S][n])."""
+def dass_gradstat_from_uv(uv, gradstat_sum, stream=None):
+    """∇p̄ norms of split views from their reduced uv blocks (float2 [S][n])."""
     S, n = uv.shape[0], uv.shape[1]
-    _check(lib().dass_gradstat_from_uv(n, S, _ptr(uv), _ptr(gradstat_sum), _ptr(gradstat_cnt),
-                                       _stream(stream)), "dass_gradstat_from_uv")
+    _check(lib().dass_gradstat_from_uv(n, S, _ptr(uv), _ptr(gradstat_sum), _stream(stream)),
+           "dass_gradstat_from_uv")
 
 
 def dass_fidelity_loss_workspace(width, height) -> int:

@@ -87,15 +87,17 @@ class FlatGrads:
     g_sigma: "torch.Tensor"
     gradstat_sum: "torch.Tensor"
     gradstat_cnt: "torch.Tensor"
-    uv: "torch.Tensor | None" = None     # [S][N][4] split-view ∇p̄ partials (ViewPlan)
+    uv: "torch.Tensor | None" = None     # [S][N][2] split-view ∇p̄ partials (ViewPlan)
 
     @staticmethod
     def allocate(n: int, k4: int, device="cuda", num_split: int = 0) -> "FlatGrads":
         import torch
-        sizes = [num_split * n * 4, n * 4, n * 4, n * 4, k4 * n * 4, n * 4, n * 4, n]
+        u = num_split * n * 2
+        u += (-u) % 4                         # keep the float4 fields 16-byte aligned
+        sizes = [u, n * 4, n * 4, n * 4, k4 * n * 4, n * 4, n * 4, n]
         flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
-        p = list(torch.split(flat, sizes))    # uv first: 16-byte aligned like the float4 fields
-        uv = p[0].view(num_split, n, 4) if num_split else None
+        p = list(torch.split(flat, sizes))
+        uv = p[0][:num_split * n * 2].view(num_split, n, 2) if num_split else None
         return FlatGrads(flat, p[1].view(n, 4), p[2].view(n, 4), p[3].view(n, 4),
                          p[4].view(k4, n, 4), p[5].view(n, 4), p[6].view(n, 4), p[7],
                          torch.zeros(n, dtype=torch.int32, device=device), uv)

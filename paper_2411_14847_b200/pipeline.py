@@ -155,8 +155,8 @@ class MultiViewPass:
     def __init__(self, cams, n: int, capacity: int, device="cuda", streams: int = 4,
                  tiles=None, uv_out=None):
         """tiles[v]: None or a (begin, stride, count) tile subset of view v (a
-        split view, dist.ViewPlan); uv_out[v]: None or the float4[n] block that
-        view's ∇p̄ partials go to."""
+        split view, dist.ViewPlan); uv_out[v]: None or the float2[n] block that
+        view's ∇p̄ partials go to (the GPU with the view's tile half 0 counts it)."""
         torch = _torch()
         self.cams = list(cams)
         self.tiles = list(tiles) if tiles is not None else [None] * len(self.cams)
@@ -236,7 +236,8 @@ class MultiViewPass:
             keep, records.conic_opa[v0:v1], records.rgb[v0:v1], records.box[v0:v1],
             self.g2d[v0:v1], grads.pos_opa, grads.scale, grads.rot, grads.sh,
             grads.gradstat_sum, grads.gradstat_cnt,
-            uv_out=None if all(u is None for u in self.uv_out[v0:v1]) else self.uv_out[v0:v1])
+            uv_out=None if all(u is None for u in self.uv_out[v0:v1]) else self.uv_out[v0:v1],
+            uv_count=[t is not None and t[0] == 0 for t in self.tiles[v0:v1]])
 
 
 class DeformFields:

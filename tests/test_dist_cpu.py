@@ -145,18 +145,19 @@ def _uv_worker(rank, world, port, out_path):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     n = 50
     g = ddist.FlatGrads.allocate(n, 3, device="cpu", num_split=2)
+    assert g.pos_opa.data_ptr() % 16 == 0 and g.uv.shape == (2, n, 2)
     rng = np.random.default_rng(rank)
-    g.uv[:, :, :2] = torch.from_numpy(rng.normal(size=(2, n, 2))).float()
-    g.uv[:, ::3, :2] = 0.0                                   # not visible in the split views
-    g.uv[:, :, 2] = 1.0
-    g.uv[:, ::3, 2] = 0.0
+    g.uv[:] = torch.from_numpy(rng.normal(size=(2, n, 2))).float()
+    g.uv[:, ::3] = 0.0                                        # not visible in the split views
+    vis = torch.ones(n, dtype=torch.int32)
+    vis[::3] = 0
+    if rank == 0:                                             # the half-0 GPU counts the views
+        g.gradstat_cnt += 2 * vis
     g.gradstat_sum += 1.0
 
     def finish(gg):   # the CPU form of dass_gradstat_from_uv
         u = gg.uv
-        vis = u[..., 2] > 0
-        gg.gradstat_sum += (torch.sqrt(u[..., 0] ** 2 + u[..., 1] ** 2) * vis).sum(0)
-        gg.gradstat_cnt += vis.sum(0).int()
+        gg.gradstat_sum += torch.sqrt(u[..., 0] ** 2 + u[..., 1] ** 2).sum(0)
 
     ddist.allreduce_grads(g, finish=finish)
     if rank == 0:
@@ -171,9 +172,11 @@ def test_split_view_uv_blocks_through_allreduce(tmp_path):
     r = np.load(out)
     n = 50
     parts = [np.random.default_rng(k).normal(size=(2, n, 2)) for k in range(2)]
+    for p in parts:
+        p[:, ::3] = 0.0
     tot = (parts[0] + parts[1]).astype(np.float32)
     vis = np.ones(n, bool)
     vis[::3] = False
-    want = 2.0 + (np.sqrt((tot ** 2).sum(-1)) * vis).sum(0)
+    want = 2.0 + np.sqrt((tot ** 2).sum(-1)).sum(0)
     np.testing.assert_allclose(r["stat"], want, rtol=1e-5)
     assert np.array_equal(r["cnt"], 2 * vis.astype(np.int32))

@@ -54,7 +54,7 @@ def test_split_views_sum_to_the_single_gpu_gradients(V, world):
     for p in parts:                       # the all_reduce
         acc.flat += p.flat
         acc.gradstat_cnt += p.gradstat_cnt
-    dass.dass_gradstat_from_uv(acc.uv, acc.gradstat_sum, acc.gradstat_cnt)
+    dass.dass_gradstat_from_uv(acc.uv, acc.gradstat_sum)
     torch.cuda.synchronize()
     for name in ("pos_opa", "scale", "rot", "sh", "gradstat_sum"):
         a = getattr(acc, name).cpu().numpy().astype(np.float64)
