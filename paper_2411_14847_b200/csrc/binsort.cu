@@ -317,19 +317,65 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
   const size_t words = (size_t)div_up((int)K, SORT_ITEMS) * RADIX;
   for (int p = 0; p < npass; ++p)
     for (size_t k = gid; k < words; k += gstride) pstatus[p * pstatus_stride + k] = 0u;
-  for (size_t r = gid; r < (size_t)n; r += gstride) {
-    const uint32_t id = (uint32_t)dkeys[r];
-    if (tiles[id] == 0u) continue;
-    const uint2 b = box[id];
-    const int tx0 = (int)(b.x & 0xFFFFu) / TILE, tx1 = (int)(b.x >> 16) / TILE;
-    const int ty0 = (int)(b.y & 0xFFFFu) / TILE, ty1 = (int)(b.y >> 16) / TILE;
-    uint32_t o = offsets[r];
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx) {
-        const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
-        pkeys[o++] = ((uint64_t)tile << 32) | id;
-        for (int p = 0; p < npass; ++p) atomicAdd(&sh[p][(tile >> (8 * p)) & 255u], 1u);
+  // Warp-cooperative emission: a warp owns 32 consecutive depth-ordered
+  // Gaussians, whose pairs are one contiguous run of pkeys (offsets is their
+  // exclusive scan), and writes that run with consecutive lanes (coalesced);
+  // lane j finds its Gaussian by a binary search over the warp's inclusive
+  // counts.  Histogram increments are aggregated per distinct tile.
+  const uint32_t lane = threadIdx.x & 31u;
+  const size_t wid = gid >> 5, nwarps = gstride >> 5;
+  for (size_t base = wid * 32; base < (size_t)n; base += nwarps * 32) {
+    const size_t r = base + lane;
+    uint32_t id = 0, cnt = 0, w = 1;
+    int tx0 = 0, ty0 = 0;
+    if (r < (size_t)n) {
+      id = (uint32_t)dkeys[r];
+      cnt = tiles[id];
+      if (cnt) {
+        const uint2 b = box[id];
+        tx0 = (int)(b.x & 0xFFFFu) / TILE;
+        ty0 = (int)(b.y & 0xFFFFu) / TILE;
+        w = (uint32_t)((int)(b.x >> 16) / TILE - tx0 + 1);
       }
+    }
+    uint32_t incl = cnt;   // inclusive scan of the counts over the warp
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= (uint32_t)d) incl += u;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    const uint32_t o0 = __shfl_sync(0xffffffffu, r < (size_t)n ? offsets[r] : 0u, 0);
+    for (uint32_t j0 = 0; j0 < total; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      // owner: the first lane whose inclusive count exceeds j
+      uint32_t lo = 0;
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + st - 1);
+        if (v <= j) lo += st;
+      }
+      const uint32_t owner = lo < 32 ? lo : 31;
+      const uint32_t excl = __shfl_sync(0xffffffffu, incl - cnt, owner);
+      const uint32_t oid = __shfl_sync(0xffffffffu, id, owner);
+      const uint32_t ow = __shfl_sync(0xffffffffu, w, owner);
+      const int otx0 = __shfl_sync(0xffffffffu, tx0, owner);
+      const int oty0 = __shfl_sync(0xffffffffu, ty0, owner);
+      const bool act = j < total;
+      uint32_t tile = 0xFFFFFFFFu;
+      if (act) {
+        const uint32_t local = j - excl;
+        const uint32_t dy = local / ow, dx = local - dy * ow;
+        tile = (uint32_t)((oty0 + (int)dy) * tiles_x + otx0 + (int)dx);
+        pkeys[o0 + j] = ((uint64_t)tile << 32) | oid;
+      }
+      const uint32_t peers = __match_any_sync(0xffffffffu, tile);
+      if (act && lane == (uint32_t)(__ffs(peers) - 1)) {
+        const uint32_t c = (uint32_t)__popc(peers);
+        for (int p = 0; p < npass; ++p) atomicAdd(&sh[p][(tile >> (8 * p)) & 255u], c);
+      }
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < npass * RADIX; k += blockDim.x) {
