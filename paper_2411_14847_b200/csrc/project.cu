@@ -13,16 +13,19 @@
 //  * the SH colour in fp32.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "sh.cuh"
 
 namespace dass {
 namespace {
 
-constexpr int MAXV = 16;  // views per launch (kernel-parameter budget)
+constexpr int MAXV = 32;  // views per launch (kernel-parameter budget)
 
 struct ProjectArgs {
   CamParams cam[MAXV];
+  int vpt;                 // views per thread (blockIdx.y groups)
   int num_views;
   int n;
   int view_offset;  // records of view v go to [(view_offset + v)·n, …)
@@ -199,7 +202,7 @@ __device__ __forceinline__ Records accurate_records(const CamParams& c, float4 p
 }
 
 template <int DEG>
-__global__ void __launch_bounds__(256) project_kernel(const __grid_constant__ ProjectArgs a) {
+__global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__ ProjectArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   const float4 po = a.pos_opa[i];
@@ -209,13 +212,10 @@ __global__ void __launch_bounds__(256) project_kernel(const __grid_constant__ Pr
   const float o_eff = kept ? po.w : 0.f;
   const float keepf = kept ? 1.f : 0.f;
   using L = SHLayout<DEG>;
-  float coef[4 * L::K4];
-#pragma unroll
-  for (int j = 0; j < L::K4; ++j) {
-    const float4 c4 = a.sh[(size_t)j * a.n + i];
-    coef[4 * j + 0] = c4.x; coef[4 * j + 1] = c4.y; coef[4 * j + 2] = c4.z; coef[4 * j + 3] = c4.w;
-  }
-  for (int v = 0; v < a.num_views; ++v) {
+  // views [blockIdx.y·vpt, …): a 2-D grid over (Gaussians, view groups) keeps many
+  // warps resident; the per-Gaussian parameters are re-read per group (L2 hits)
+  const int va = blockIdx.y * a.vpt, vb = min(a.num_views, va + a.vpt);
+  for (int v = va; v < vb; ++v) {
     const CamParams& c = a.cam[v];
     const size_t o = (size_t)(a.view_offset + v) * a.n + i;
     const KeyResult k = key_chain(c, po.x, po.y, po.z, o_eff, sc.x * keepf, sc.y * keepf,
@@ -235,11 +235,20 @@ __global__ void __launch_bounds__(256) project_kernel(const __grid_constant__ Pr
     dx *= inv; dy *= inv; dz *= inv;
     float Y[L::NC];
     sh_eval<DEG>(dx, dy, dz, Y);
+    // SH planes re-read per view (L1/L2-resident after the first view) instead
+    // of pinning 4·K4 registers across the view loop: 159 → fewer registers,
+    // 4× the resident warps
     float col[3] = {0.5f, 0.5f, 0.5f};
 #pragma unroll
-    for (int kk = 0; kk < L::NC; ++kk)
+    for (int j = 0; j < L::K4; ++j) {
+      const float4 c4 = __ldg(a.sh + (size_t)j * a.n + i);
+      const float cf[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) col[ch] += Y[kk] * coef[3 * kk + ch];
+      for (int e = 0; e < 4; ++e) {
+        const int f = 4 * j + e;   // coefficient-major, channel-minor: f = 3·kk + ch
+        if (f < L::NF) col[f % 3] += Y[f / 3] * cf[e];
+      }
+    }
     int bits = 0;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
@@ -255,6 +264,15 @@ __global__ void __launch_bounds__(256) project_kernel(const __grid_constant__ Pr
 
 }  // namespace
 
+static int project_vpt() {
+  static const int v = [] {
+    const char* e = getenv("DASS_PROJECT_VPT");
+    const int x = e ? atoi(e) : MAXV;   // measured: more views per thread is faster
+    return x >= 1 ? x : 4;
+  }();
+  return v;
+}
+
 cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_degree,
                            const float4* pos_opa, const float4* scale, const float4* rot,
                            const float4* sh, const uint8_t* keep, float4* xy_depth,
@@ -267,7 +285,8 @@ cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_d
     a.n = n; a.view_offset = v0;
     a.pos_opa = pos_opa; a.scale = scale; a.rot = rot; a.sh = sh; a.keep = keep;
     a.xy_depth = xy_depth; a.conic_opa = conic_opa; a.rgb = rgb; a.box = box; a.tiles = tiles;
-    const int grid = div_up(n, 256);
+    a.vpt = project_vpt();
+    const dim3 grid(div_up(n, 256), div_up(a.num_views, a.vpt));
     switch (sh_degree) {
       case 0: project_kernel<0><<<grid, 256, 0, s>>>(a); break;
       case 1: project_kernel<1><<<grid, 256, 0, s>>>(a); break;
