@@ -146,6 +146,8 @@ def run_ours(args):
     if args.emulate:
         plan_rank, plan_world = (int(x) for x in args.emulate.split("/"))
     plan = view_plan(len(cams), plan_rank, plan_world, ((W0 + 15) // 16) * ((H0 + 15) // 16))
+    # views the timed job covers: all of them, or an --emulate run's own share
+    job_views = len(cams) if not args.emulate else sum(1.0 if t is None else 0.5 for t in plan.tiles)
     mine = plan.views
     my_cams = [cams[v] for v in mine]
     W, H = cams[0].width, cams[0].height
@@ -541,7 +543,7 @@ def run_ours(args):
         ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        e2e = {"value": len(cams) / (float(ems.item()) / 1e3), "unit": "views/s",
+        e2e = {"value": job_views / (float(ems.item()) / 1e3), "unit": "views/s",
                "ms_per_step": float(ems.item()), "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "pipelining": "double-buffered: upload k+1 and download k-1 overlap compute k"}
@@ -567,9 +569,7 @@ def run_ours(args):
         flops = sum(a * FLOP_BWD_ACCEPTED for a in stats["accepted"])
         bwd_ms = ops.get("render_bwd_raster", float("nan"))
         achieved = flops / (bwd_ms / 1e3) / 1e12 if bwd_ms == bwd_ms and bwd_ms > 0 else None
-        # whole-job views/s; an --emulate run reports its own share (whole views + halves)
-        views_done = len(cams) if not args.emulate else sum(1.0 if t is None else 0.5 for t in plan.tiles)
-        views_s = views_done / (ms_step / 1e3)
+        views_s = job_views / (ms_step / 1e3)
         result = {
             "metric": METRIC, "value": round(views_s, 3), "unit": "views/s",
             "mpix_per_s": round(views_s * W * H / 1e6, 1),
