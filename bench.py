@@ -341,7 +341,7 @@ def run_ours(args):
         tms = torch.tensor([t0.elapsed_time(t1) / nt], device=dev)
         if world > 1:
             dist.all_reduce(tms, op=dist.ReduceOp.MAX)
-        train = {"value": round(len(cams) / (float(tms.item()) / 1e3), 3), "unit": "views/s",
+        train = {"value": round(job_views / (float(tms.item()) / 1e3), 3), "unit": "views/s",
                  "ms_per_step": round(float(tms.item()), 4),
                  "loss_mean": float(mvp.losses[:, 0].mean().item()),
                  "what": "one full shift-stage iteration (§3.3): dual hash-grid deformation fwd (f2) → shift → fwd + fused L1/D-SSIM loss (Eq. 3, f1) + bwd over the views → shift bwd → deformation bwd (table + MLP grads)",
