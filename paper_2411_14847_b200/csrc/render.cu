@@ -25,6 +25,10 @@
 #include "common.cuh"
 #include "sh.cuh"
 
+#ifndef PRE1_MINB
+#define PRE1_MINB 4   // preprocess PART 1: 128 registers (4 blocks/SM) measured best (3: 0.63 ms, 4: 0.59, 5: 0.66)
+#endif
+
 namespace dass {
 namespace {
 
@@ -700,7 +704,7 @@ struct PreArgs {
 // PART 2: SH coefficient gradients (fp32, 3(d+1)² register accumulators).
 // Split so neither part spills.
 template <int DEG, int PART>
-__global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? 3 : 2) preprocess_views_kernel(
+__global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB : 2) preprocess_views_kernel(
     const __grid_constant__ PreArgs a) {
   // The per-Gaussian chain is evaluated in fp64: the kernel is HBM-bound, so
   // the wider arithmetic is free, and it removes the chain's own rounding
@@ -1028,7 +1032,6 @@ cudaError_t launch_render_features(const CamParams& cam, const uint2* ranges, co
                                    const float4* xy_depth, const float4* conic_opa,
                                    const uint2* box, int channels, const float* feat, float* out,
                                    cudaStream_t s) {
-  const int ntiles = cam.tiles_x * cam.tiles_y;
   const float4* f4 = reinterpret_cast<const float4*>(feat);
 #define FEAT(NV)                                                                                 \
   render_features_kernel<NV><<<cam.tcount, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, box, f4, out)
