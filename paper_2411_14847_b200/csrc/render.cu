@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
     const float gcol[3] = {(bits & 1) ? 0.f : m1.z, (bits & 2) ? 0.f : m1.w, (bits & 4) ? 0.f : m2.x};
     if (PART == 2) {
       F dx = (F)po.x - cam.campos[0], dy = (F)po.y - cam.campos[1], dz = (F)po.z - cam.campos[2];
-      const F inv = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+      const F inv = rsqrt(dx * dx + dy * dy + dz * dz);
       float Y[L::NC];
       sh_eval<DEG>((float)(dx * inv), (float)(dy * inv), (float)(dz * inv), Y);
 #pragma unroll
@@ -788,8 +788,7 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
     // ---- colour / SH (direction from this view's camera centre)
     {
       F dx = (F)po.x - cam.campos[0], dy = (F)po.y - cam.campos[1], dz = (F)po.z - cam.campos[2];
-      const F dist = sqrt(dx * dx + dy * dy + dz * dz);
-      const F inv = 1.0 / dist;
+      const F inv = rsqrt(dx * dx + dy * dy + dz * dz);
       dx *= inv; dy *= inv; dz *= inv;
       float wk[L::NC];
 #pragma unroll
