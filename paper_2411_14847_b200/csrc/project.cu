@@ -161,7 +161,8 @@ __device__ __forceinline__ Records accurate_records(const CamParams& c, float4 p
     t[a] = (double)c.V[4 * a] * px + (double)c.V[4 * a + 1] * py + (double)c.V[4 * a + 2] * pz +
            (double)c.V[4 * a + 3];
   const double nq = sqrt((double)q.x * q.x + (double)q.y * q.y + (double)q.z * q.z + (double)q.w * q.w);
-  const double w = q.x / nq, x = q.y / nq, y = q.z / nq, z = q.w / nq;
+  const double inq = 1.0 / nq;   // reciprocals instead of repeated fp64 divisions
+  const double w = q.x * inq, x = q.y * inq, y = q.z * inq, z = q.w * inq;
   double R[3][3];
   R[0][0] = 1 - 2 * (y * y + z * z); R[0][1] = 2 * (x * y - w * z); R[0][2] = 2 * (x * z + w * y);
   R[1][0] = 2 * (x * y + w * z); R[1][1] = 1 - 2 * (x * x + z * z); R[1][2] = 2 * (y * z - w * x);
@@ -169,10 +170,11 @@ __device__ __forceinline__ Records accurate_records(const CamParams& c, float4 p
   const double s[3] = {(double)sc.x * keepf, (double)sc.y * keepf, (double)sc.z * keepf};
   // N = J W R S (2×3); Σ' = N Nᵀ + 0.3 I
   const double lx = 1.3 * c.W / (2.0 * c.fx), ly = 1.3 * c.H / (2.0 * c.fy);
-  const double xt = t[2] * fmin(lx, fmax(-lx, t[0] / t[2]));
-  const double yt = t[2] * fmin(ly, fmax(-ly, t[1] / t[2]));
-  const double J00 = c.fx / t[2], J02 = -c.fx * xt / (t[2] * t[2]);
-  const double J11 = c.fy / t[2], J12 = -c.fy * yt / (t[2] * t[2]);
+  const double itz = 1.0 / t[2], itz2 = itz * itz;
+  const double xt = t[2] * fmin(lx, fmax(-lx, t[0] * itz));
+  const double yt = t[2] * fmin(ly, fmax(-ly, t[1] * itz));
+  const double J00 = c.fx * itz, J02 = -c.fx * xt * itz2;
+  const double J11 = c.fy * itz, J12 = -c.fy * yt * itz2;
   double M[2][3];
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
@@ -189,11 +191,12 @@ __device__ __forceinline__ Records accurate_records(const CamParams& c, float4 p
   const double b2 = N[0][0] * N[1][0] + N[0][1] * N[1][1] + N[0][2] * N[1][2];
   const double c2 = N[1][0] * N[1][0] + N[1][1] * N[1][1] + N[1][2] * N[1][2] + 0.3;
   const double det = a2 * c2 - b2 * b2;
-  r.A = (float)(c2 / det);
-  r.B = (float)(-b2 / det);
-  r.C = (float)(a2 / det);
-  const double u = c.fx * t[0] / t[2] + c.cx;
-  const double v = c.fy * t[1] / t[2] + c.cy;
+  const double idet = 1.0 / det;
+  r.A = (float)(c2 * idet);
+  r.B = (float)(-b2 * idet);
+  r.C = (float)(a2 * idet);
+  const double u = c.fx * t[0] * itz + c.cx;
+  const double v = c.fy * t[1] * itz + c.cy;
   r.u_hi = (float)u;
   r.v_hi = (float)v;
   r.u_lo = __double2half(u - (double)r.u_hi);
