@@ -176,27 +176,39 @@ def run_ours(args):
         """∇p̄ of the views split across ranks, from their reduced uv partials."""
         dass.dass_gradstat_from_uv(g.uv, g.gradstat_sum)
 
-    def step_local():
-        """Everything on this GPU (capturable: no host sync, no collective)."""
-        grads.zero_()
-        dass.dass_apply_shift(base.pos_opa, base.rot, mu_d, sigma_d, base.dynamic,
-                              shifted.pos_opa, shifted.rot)
-        if my_cams:
-            dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
-                                    shifted.sh, None, records.xy_depth, records.conic_opa,
-                                    records.rgb, records.box, records.tiles)
-        if mvp is not None:
-            mvp.run(shifted, records, dLs, grads)
-        dass.dass_apply_shift_bwd(base.rot, sigma_d, base.dynamic, grads.pos_opa, grads.rot,
-                                  g_mu, g_sigma)
+    class StepBufs:
+        """A step's inputs and outputs (the e2e pipeline double-buffers them)."""
+        def __init__(self, base, mu, sigma, dLs, grads):
+            self.base, self.mu, self.sigma, self.dLs, self.grads = base, mu, sigma, dLs, grads
+            # 𝒢_t after the shift: pos/rot are per-step scratch, scale/SH are the inputs'
+            self.shifted = DeviceScene(shifted.pos_opa, base.scale, shifted.rot, base.sh, deg,
+                                       base.dynamic)
 
-    def run_step(graph=None):
+    bufs0 = StepBufs(base, mu_d, sigma_d, dLs, grads)
+
+    def step_local(S=bufs0):
+        """Everything on this GPU (capturable: no host sync, no collective)."""
+        g = S.grads
+        g.zero_()
+        dass.dass_apply_shift(S.base.pos_opa, S.base.rot, S.mu, S.sigma, S.base.dynamic,
+                              S.shifted.pos_opa, S.shifted.rot)
+        if my_cams:
+            dass.dass_project_views(my_cams, deg, S.shifted.pos_opa, S.shifted.scale,
+                                    S.shifted.rot, S.shifted.sh, None, records.xy_depth,
+                                    records.conic_opa, records.rgb, records.box, records.tiles)
+        if mvp is not None:
+            mvp.uv_out = [None if sidx < 0 else g.uv[sidx] for sidx in plan.split]
+            mvp.run(S.shifted, records, S.dLs, g)
+        dass.dass_apply_shift_bwd(S.base.rot, S.sigma, S.base.dynamic, g.pos_opa, g.rot,
+                                  g.g_mu, g.g_sigma)
+
+    def run_step(graph=None, S=bufs0):
         if graph is None:
-            step_local()
+            step_local(S)
         else:
             graph.replay()
         if world > 1:
-            allreduce_grads(grads, finish=finish_split)   # the one cross-GPU exchange (NCCL)
+            allreduce_grads(S.grads, finish=finish_split)   # the one cross-GPU exchange (NCCL)
 
     def step():
         run_step(None)
@@ -478,52 +490,60 @@ def run_ours(args):
     # region (first upload → last download).
     e2e = None
     if not args.no_e2e:
+        # Two complete input/output buffer sets, each with its own captured step graph:
+        # step k runs set k mod 2, the upload of step k+1 goes straight into the other
+        # set (copy engine, pinned host → device), and step k's gradients are read
+        # straight out of its set — no device-side staging copies on the compute stream.
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         h_in = [pin(scene.pos_opa), pin(scene.scale), pin(scene.rot), pin(scene.sh), pin(mu),
                 pin(sigma), dLs.cpu().pin_memory()]
-        d_in = [base.pos_opa, base.scale, base.rot, base.sh, mu_d, sigma_d, dLs]
-        stage_in = [[torch.empty_like(d) for d in d_in] for _ in range(2)]
-        stage_out = [torch.empty_like(flat) for _ in range(2)]
+        base1 = DeviceScene(torch.empty_like(base.pos_opa), torch.empty_like(base.scale),
+                            torch.empty_like(base.rot), torch.empty_like(base.sh), deg, base.dynamic)
+        bufs1 = StepBufs(base1, torch.empty_like(mu_d), torch.empty_like(sigma_d),
+                         torch.empty_like(dLs), FlatGrads.allocate(n, K4, dev, num_split=plan.num_split))
+        sets = [bufs0, bufs1]
+        d_in = [[S.base.pos_opa, S.base.scale, S.base.rot, S.base.sh, S.mu, S.sigma, S.dLs]
+                for S in sets]
+        graphs = [graph, None]
+        if graph is not None:
+            graphs[1] = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graphs[1]):
+                step_local(bufs1)
         h_out = [torch.empty(flat.numel(), dtype=torch.float32).pin_memory() for _ in range(2)]
         h2d = sum(x.numel() * x.element_size() for x in h_in)
         d2h = flat.numel() * 4
         comp = torch.cuda.current_stream()
         copy_in = torch.cuda.Stream(device=dev)
         copy_out = torch.cuda.Stream(device=dev)
-        ev_in = [torch.cuda.Event() for _ in range(2)]      # upload k done
-        ev_free = [torch.cuda.Event() for _ in range(2)]    # staging k consumed
-        ev_res = [torch.cuda.Event() for _ in range(2)]     # result k staged
-        ev_out = [torch.cuda.Event() for _ in range(2)]     # download k done
+        ev_in = [torch.cuda.Event() for _ in range(2)]      # upload into set b done
+        ev_res = [torch.cuda.Event() for _ in range(2)]     # step on set b done
+        ev_out = [torch.cuda.Event() for _ in range(2)]     # download from set b done
 
         def upload(k):
             b = k % 2
             with torch.cuda.stream(copy_in):
-                copy_in.wait_event(ev_free[b])
-                for h, d in zip(h_in, stage_in[b]):
+                copy_in.wait_event(ev_res[b])        # the step that last read set b is done
+                for h, d in zip(h_in, d_in[b]):
                     d.copy_(h, non_blocking=True)
                 ev_in[b].record(copy_in)
 
         def compute(k):
             b = k % 2
             comp.wait_event(ev_in[b])
-            for src, dst in zip(stage_in[b], d_in):
-                dst.copy_(src, non_blocking=True)
-            ev_free[b].record(comp)
-            run_step(graph)
-            comp.wait_event(ev_out[b])           # previous download from this slot done
-            stage_out[b].copy_(flat, non_blocking=True)
+            comp.wait_event(ev_out[b])               # set b's previous gradients downloaded
+            run_step(graphs[b], sets[b])
             ev_res[b].record(comp)
 
         def download(k):
             b = k % 2
             with torch.cuda.stream(copy_out):
                 copy_out.wait_event(ev_res[b])
-                h_out[b].copy_(stage_out[b], non_blocking=True)
+                h_out[b].copy_(sets[b].grads.flat, non_blocking=True)
                 ev_out[b].record(copy_out)
 
         def run_e2e(nsteps):
             for b in range(2):
-                ev_free[b].record(comp)
+                ev_res[b].record(comp)
                 ev_out[b].record(comp)
             upload(0)
             for k in range(nsteps):
@@ -546,7 +566,8 @@ def run_ours(args):
         e2e = {"value": job_views / (float(ems.item()) / 1e3), "unit": "views/s",
                "ms_per_step": float(ems.item()), "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
-               "pipelining": "double-buffered: upload k+1 and download k-1 overlap compute k"}
+               "pipelining": "two buffer sets, one captured graph each: the upload of step k+1 "
+                             "and the download of step k−1 overlap step k, with no device-side copies"}
 
     # ---- gather stats to rank 0
     if world > 1:
