@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float
     sum_l1 += fabsf(sI[r + HALO][c + HALO] - sG[r + HALO][c + HALO]);
     const size_t q = (size_t)gy * W + gx;
     P[q] = 2.f * m2 * (A2 - A1) * iB - 2.f * m1 * S * (B2 - B1) * iB;   // ∂S/∂μ_I
-    P[np + q] = -S / B2;                                                 // ∂S/∂E[I²]
+    P[np + q] = -S * B1 * iB;                                            // ∂S/∂E[I²] = −S/B2
     P[2 * np + q] = 2.f * A1 * iB;                                       // ∂S/∂E[IG]
   }
   // block reduction of (Σ S, Σ|I − G|) → fp64 atomics
