@@ -620,6 +620,7 @@ def run_ours(args):
                                                         max(sum(v for k, v in ops.items() if k in STEP_OPS), 1e-9), 4),
                          "ncu_share_source": "profiles/r01_launches.txt"},
             "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
+            "hot_path_roofline": hot_path_roofline(ops, stats, pk, peak_tflops, n, len(my_cams), deg),
             "rows_roofline": rows_roofline(ops, densify, allst, pk, peak_tflops, n, W, H,
                                            len(my_cams), deg),
             "scene_stats": None if args.lean else {"K_per_view_mean": float(np.mean(allst["K"])),
@@ -704,6 +705,47 @@ def run_reference(args):
 FLOP_SSIM_PER_PXCH = 2 * (5 * 11 * 2) + 40 + 2 * (3 * 11 * 2) + 10   # fwd + bwd stencils
 BYTES_LOSS_PER_PX = 3 * 4 * 3                                           # img, gt in; ∂L/∂img out
 DEFORM_IN = {"dyn": 32, "st": 16}                                       # L·F (N3DV profile)
+
+
+def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg):
+    """Every §8(a) kernel group of the step against its own roof,
+    from the sequential per-op pass of rank 0 and that rank's scene statistics."""
+    if not ops or not stats.get("K"):
+        return None
+    hbm = pk.get("hbm_gbs", 6650.0)
+    k4 = (3 * (deg + 1) ** 2 + 3) // 4
+    K = float(sum(stats["K"]))
+    acc = float(sum(stats["accepted"]))
+    pfwd = float(sum(stats["P_fwd"]))
+    out = {}
+
+    def hb(name, by):
+        t = ops[name] / 1e3
+        out[name] = {"bound": "hbm", "bytes": int(by), "achieved_gbs": round(by / t / 1e9, 1),
+                     "peak_gbs": hbm, "frac": round(by / t / 1e9 / hbm, 4)}
+
+    # projection: parameters once per launch (48 + 16·K4 B) + 60 B of records per view
+    hb("project_views", n * (48 + 16 * k4) + n * views * 60)
+    out["project_views"]["note"] = "issue-bound, not HBM: fp64 record chain + the fp32 key-chain replica"
+    # binning + sort: per pair 8 B key written by emit, 2 onesweep passes of 16 B read + 16 B
+    # written (key + id), finalize 8 B read + 4 B id + range writes; N-key presort ≈ 4 × 32 B
+    hb("bin_sort", K * (8 + 2 * 32 + 12) + n * views * 4 * 32)
+    out["bin_sort"]["note"] = "latency-bound launch chain (10 kernels per view), hidden under other views' raster kernels"
+    # preprocess: 88 B of records + moments per Gaussian-view, parameters and gradients once
+    hb("render_bwd_preprocess_views", n * views * 88 + n * 3 * (48 + 16 * k4))
+    t = ops["render_fwd"] / 1e3
+    fl = 15.0 * acc + 8.0 * pfwd            # accepted blend + every in-box α evaluation
+    out["render_fwd"] = {"bound": "alu", "flop": int(fl), "achieved_tflops": round(fl / t / 1e12, 2),
+                         "peak_tflops": round(peak_fp32, 1), "frac": round(fl / t / 1e12 / peak_fp32, 4),
+                         "unit": "15 flop per accepted (pixel, entry) + 8 per in-box evaluation"}
+    t = ops["render_bwd_raster"] / 1e3
+    fl = 48.0 * acc
+    out["render_bwd_raster"] = {"bound": "alu", "flop": int(fl),
+                                "achieved_tflops": round(fl / t / 1e12, 2),
+                                "peak_tflops": round(peak_fp32, 1),
+                                "frac": round(fl / t / 1e12 / peak_fp32, 4),
+                                "unit": "48 flop per accepted (pixel, entry)"}
+    return out
 
 
 def rows_roofline(ops, densify, allst, pk, peak_fp32, n, W, H, views, deg):
