@@ -17,3 +17,16 @@ def test_rows_roofline_fractions():
     g = out["f4_gather"]
     assert abs(g["achieved_gbs"] - 2 * 300_000 * 240 / 0.03e-3 / 1e9) < 1.0
     assert out["f2_deform_fwd_tcgen05"]["peak_tflops"] == 800.0
+
+
+def test_hot_path_roofline():
+    ops = {"project_views": 0.62, "bin_sort": 4.0, "render_fwd": 8.0, "render_bwd_raster": 7.9,
+           "render_bwd_preprocess_views": 0.44}
+    stats = {"K": [2_100_000] * 20, "accepted": [65_000_000] * 20, "P_fwd": [215_000_000] * 20}
+    out = bench.hot_path_roofline(ops, stats, {"hbm_gbs": 6400.0}, 74.4, 300_000, 20, 3)
+    assert set(out) == set(ops)
+    for v in out.values():
+        assert 0 < v["frac"] < 1
+    # the backward's flop count is 48 per accepted unit
+    assert out["render_bwd_raster"]["flop"] == 48 * 65_000_000 * 20
+    assert bench.hot_path_roofline({}, stats, {}, 74.4, 1, 1, 0) is None
