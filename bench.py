@@ -224,9 +224,15 @@ def run_ours(args):
     step()
     torch.cuda.synchronize()
     cnt = torch.zeros(8, dtype=torch.int64, device=dev)
+    stats["n_visible"] = []
+    tiles_hist = []
     for k, cam in enumerate([] if args.lean else my_cams):
         if plan.tiles[k] is not None and plan.tiles[k][0] != 0:
             continue   # a split view's statistics are counted once, by the rank with half 0
+        tt = records.tiles[k]
+        vis = tt[tt > 0]
+        stats["n_visible"].append(int(vis.numel()))
+        tiles_hist.append(torch.bincount(vis.clamp(max=4095), minlength=4096).cpu())
         rec = records.view(k)
         K = raster.forward(cam, rec, host_mode=True)
         dass.dass_render_stats(cam, raster.ranges, raster.sorted_ids, rec[0], rec[1], rec[3],
@@ -259,13 +265,17 @@ def run_ours(args):
     # ---- exactly K timed steps
     l0 = dass.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         barrier()
         ev0.record()
-        for _ in range(args.steps):
+        step_ev[0].record()
+        for k in range(args.steps):
             timed()
+            step_ev[k + 1].record()
         ev1.record()
         barrier()
+    per_step = np.array([step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps)])
     launches = dass.kernel_launches() - l0
     if graph is not None:
         launches = per_step_launches * args.steps
@@ -580,6 +590,12 @@ def run_ours(args):
     else:
         allst = stats
     clocks = clk.summary()
+    tiles_summary = None
+    if tiles_hist:   # rank 0's views (mean, p50, p99 of tiles_touched over visible Gaussians)
+        h = torch.stack(tiles_hist).sum(0).numpy().astype(np.float64)
+        c = np.cumsum(h) / max(h.sum(), 1.0)
+        tiles_summary = {"mean": round(float((np.arange(h.size) * h).sum() / max(h.sum(), 1.0)), 3),
+                         "p50": int(np.searchsorted(c, 0.5)), "p99": int(np.searchsorted(c, 0.99))}
     result = None
     if rank == 0:
         pk, pk_kind = peaks()
@@ -595,7 +611,10 @@ def run_ours(args):
             "metric": METRIC, "value": round(views_s, 3), "unit": "views/s",
             "mpix_per_s": round(views_s * W * H / 1e6, 1),
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": round(ms_step, 4),
+            "ms_per_step_percentiles_rank0": {q: round(float(np.percentile(per_step, v)), 4)
+                                              for q, v in (("p10", 10), ("p50", 50), ("p90", 90))},
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N3DV-shaped scene and rig)",
             "config": {"workload": WORKLOAD, "n_gaussians": n, "views": len(cams), "width": W,
                        "height": H, "sh_degree": deg, "dynamic_frac": 0.3,
@@ -624,6 +643,8 @@ def run_ours(args):
             "rows_roofline": rows_roofline(ops, densify, allst, pk, peak_tflops, n, W, H,
                                            len(my_cams), deg),
             "scene_stats": None if args.lean else {"K_per_view_mean": float(np.mean(allst["K"])),
+                            "n_visible_per_view_mean": float(np.mean(allst["n_visible"])),
+                            "tiles_per_visible_gaussian": tiles_summary,
                             "P_fwd_per_px": float(np.sum(allst["P_fwd"]) / (len(allst["K"]) * W * H)),
                             "P_bwd_per_px": float(np.sum(allst["P_bwd"]) / (len(allst["K"]) * W * H)),
                             "accepted_per_px": float(np.sum(allst["accepted"]) / (len(allst["K"]) * W * H)),
@@ -660,12 +681,25 @@ def time_oracle(cams, scene, views, seed_base=1000):
     return time.perf_counter() - t0
 
 
+def host_cpu():
+    """The CPU the oracle ran on (model, affinity, logical CPUs)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "affinity": len(os.sched_getaffinity(0)), "cpu_count": os.cpu_count()}
+
+
 def cpu_baseline(cams, scene, nviews):
     import oracle
     oracle.build()
     secs = time_oracle(cams, scene, list(range(nviews)))
     return {"value": round(nviews / secs, 4), "unit": "views/s", "cores": oracle.threads(),
-            "kind": "oracle",
+            "kind": "oracle", "host": host_cpu(),
             "sample": f"{nviews} of the 20 views (fwd+bwd, scatter form, double) + the shift, "
                       f"{secs:.1f} s on {oracle.threads()} OpenMP threads"}
 

@@ -44,5 +44,9 @@ for n, v in zip(names, vals):
              "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_lsu.sum",
              "smsp__inst_executed_op_shared_ld.sum", "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum",
              "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
-             "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active"):
+             "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+             "l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum",
+             "l1tex__m_l1tex2xbar_write_sectors_mem_global_op_atom.sum",
+             "SM_A.TriageCompute.sm__inst_executed_pipe_xu_realtime.avg.pct_of_peak_sustained_elapsed",
+             "smsp__thread_inst_executed_per_inst_executed.ratio"):
         print(f"{n:70s} {v}")
