@@ -632,6 +632,7 @@ def run_ours(args):
                          "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz ({pk_kind} clock)",
                          "units_per_step": {"accepted": sum(stats["accepted"]), "P_bwd": sum(stats["P_bwd"])},
                          "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED},
+                         "survey_unit_view": survey_unit_view(stats, bwd_ms, f_max),
                          "timing": "isolated launches: one sequential pass over the step's kernels "
                                    "(CUDA events on the launching stream), since in the timed "
                                    "graph the per-view kernels of 20 streams overlap",
@@ -739,6 +740,23 @@ def run_reference(args):
 FLOP_SSIM_PER_PXCH = 2 * (5 * 11 * 2) + 40 + 2 * (3 * 11 * 2) + 10   # fwd + bwd stencils
 BYTES_LOSS_PER_PX = 3 * 4 * 3                                           # img, gt in; ∂L/∂img out
 DEFORM_IN = {"dyn": 32, "st": 16}                                       # L·F (N3DV profile)
+
+
+def survey_unit_view(stats, bwd_ms, f_max):
+    """The backward against SURVEY §8(d)'s own work unit: every in-box (pixel, entry) up
+    to the pixel's last contributor (P_bwd), ≈55 FP32-pipe instructions each, against the
+    instruction-issue peak (148 SMs × 128 lanes × f).  A 3DGS-style backward evaluates all
+    of them; the acceptance lists skip the rejected ones, so this is an equivalent-work
+    rate, not the algorithmic one the `frac` above reports."""
+    if not stats.get("P_bwd") or not bwd_ms or bwd_ms != bwd_ms:
+        return None
+    units = float(sum(stats["P_bwd"]))
+    acc = float(sum(stats["accepted"]))
+    peak = SM_COUNT * FP32_LANES * f_max / 1e12
+    rate = units * 55 / (bwd_ms / 1e3) / 1e12
+    return {"units": int(units), "instr_per_unit": 55, "achieved_tinstr_s": round(rate, 2),
+            "peak_tinstr_s": round(peak, 1), "frac": round(rate / peak, 4),
+            "evaluated_by_this_kernel": round(acc / units, 4)}
 
 
 def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg):
