@@ -65,6 +65,10 @@ def parse():
     p.add_argument("--emulate", default=None, metavar="R/W",
                    help="diagnostic: run rank R's share of a W-GPU view plan on this one GPU "
                         "(no collective) — predicts per-rank step time for --gpus W")
+    p.add_argument("--nccl-single", action="store_true",
+                   help="diagnostic: open a one-rank NCCL group so the N>1 code path (all_reduce, "
+                        "split-view finish, max over ranks) runs on one GPU; with --emulate R/W it "
+                        "exercises rank R's whole multi-GPU step")
     return p.parse_args()
 
 
@@ -136,8 +140,11 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    distd = world > 1 or args.nccl_single      # a process group is open
+    if distd:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
     cams, scene = synth.c3(n=args.n, num_views=args.views)
     mu, sigma = synth.shift_offsets(scene, seed=33)
@@ -207,14 +214,14 @@ def run_ours(args):
             step_local(S)
         else:
             graph.replay()
-        if world > 1:
+        if distd:
             allreduce_grads(S.grads, finish=finish_split)   # the one cross-GPU exchange (NCCL)
 
     def step():
         run_step(None)
 
     def barrier():
-        if world > 1:
+        if distd:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -281,14 +288,14 @@ def run_ours(args):
         launches = per_step_launches * args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_t = torch.tensor([ms], device=dev)
-    if world > 1:
+    if distd:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_step = float(ms_t.item())
 
     # ---- the collective's share of the step: the same all_reduce
     # (+ split-view ∇p̄ finish) timed alone, max over ranks
     allreduce = None
-    if world > 1:
+    if distd:
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         a0.record()
@@ -354,14 +361,14 @@ def run_ours(args):
                 train_local()
             else:
                 tgraph.replay()
-            if world > 1:
+            if distd:
                 allreduce_grads(grads, finish=finish_split)
                 for x in fields.grad_tensors():
                     dist.all_reduce(x)
         t1.record()
         barrier()
         tms = torch.tensor([t0.elapsed_time(t1) / nt], device=dev)
-        if world > 1:
+        if distd:
             dist.all_reduce(tms, op=dist.ReduceOp.MAX)
         train = {"value": round(job_views / (float(tms.item()) / 1e3), 3), "unit": "views/s",
                  "ms_per_step": round(float(tms.item()), 4),
@@ -571,7 +578,7 @@ def run_ours(args):
         e1.record()
         barrier()
         ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
-        if world > 1:
+        if distd:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e2e = {"value": job_views / (float(ems.item()) / 1e3), "unit": "views/s",
                "ms_per_step": float(ems.item()), "h2d_bytes_per_step": int(h2d),
@@ -580,7 +587,7 @@ def run_ours(args):
                              "and the download of step k−1 overlap step k, with no device-side copies"}
 
     # ---- gather stats to rank 0
-    if world > 1:
+    if distd:
         obj = [None] * world
         dist.all_gather_object(obj, stats)
         allst = {k: sum((o[k] for o in obj), []) for k in stats}
@@ -659,7 +666,7 @@ def run_ours(args):
             "clocks": clocks,
             "e2e": e2e,
         }
-    if world > 1:
+    if distd:
         dist.barrier()
         dist.destroy_process_group()
     return result, (cams, scene)
