@@ -386,7 +386,10 @@ int dass_gradstat_from_uv(int32_t n, int32_t num_split, const float* uv, float* 
  * img, gt: float [3][H][W].  λ ∈ [0, 1] (0.2 in 3DGS).  loss: device float[3]
  * = (L, L1, SSIM), written.  dL_dimg: float [3][H][W] = ∂L/∂img, written
  * (nullable: forward only; sign(0) = 0 for the L1 term).  ws: workspace of
- * dass_fidelity_loss_workspace bytes, 16-byte aligned.
+ * dass_fidelity_loss_workspace bytes, 16-byte aligned.  Any img/gt alignment
+ * is accepted: when W % 4 == 0 and the planes are 16-byte aligned the halo
+ * tiles are staged by TMA (cp.async.bulk.tensor), else by plain loads; both
+ * stage the same values, so the results are bit-identical.
  * ------------------------------------------------------------------------- */
 int dass_fidelity_loss_workspace(int32_t width, int32_t height, size_t* bytes);
 int dass_fidelity_loss(int32_t width, int32_t height, const float* img,

@@ -2,14 +2,20 @@
 // L = (1−λ)·L1 + λ·(1 − SSIM) (A39), forward and ∂L/∂I.
 //
 // SSIM statistics are separable 11-tap Gaussian windows (σ = 1.5, zero
-// padding).  Two stencil kernels on 32×32 output tiles with a 5-px halo
-// staged in shared memory:
+// padding).  Two stencil kernels on 32 × 8·VS output tiles with a 5-px halo
+// staged in shared memory — by TMA (cp.async.bulk.tensor, out-of-bounds boxes
+// zero-filled = the zero padding) when the image rows are 16-byte aligned,
+// else by coalesced loads:
 //   ssim_fwd:  4 windowed moments (μ_I, μ_G, E[I² + G²], E[IG]) → S(q) and the
 //              three partials ∂S/∂μ_I, ∂S/∂E[I²], ∂S/∂E[IG] (to workspace), plus
 //              block-reduced Σ S and Σ|I − G| (fp64 atomics);
 //   ssim_bwd:  the partial maps windowed again (the transpose of the
 //              zero-padded correlation is the same window) → ∂SSIM/∂I, fused
-//              with the L1 term.  HBM/L2-bound (≈ 40 B/px/channel).
+//              with the L1 term.
+// Both are issue-bound on the stencil FMAs (f1).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace dass {
@@ -34,50 +40,149 @@ Win make_window() {
 }
 
 // Both stencil kernels are register-blocked separable passes over a staged
-// 42×42 tile: the horizontal pass gives each thread an 8-column strip of one
-// row (18 inputs per 8 outputs instead of 11 per output), the vertical pass a
-// 4-row strip of one column (14 inputs per 4 outputs), so shared-memory loads
-// per output drop from ≈ 90 to ≈ 25 and the kernels become HBM-bound.
+// (LT + 10) × (LTY + 10) tile: the horizontal pass gives each thread an
+// 8-column strip of one row (18 inputs per 8 outputs instead of 11 per
+// output, read as 5 conflict-free LDS.128 from the 44-float row pitch), the
+// vertical pass a VS-row strip of one column (VS + 10 inputs per VS outputs).
+// The tile is 32 columns × LTY rows with LTY = 8·VS, so the vertical pass is
+// exactly 256 strips and the horizontal pass 4·(LTY + 10) ≤ 256 strips.
+//
+// A staged row starts at column x0 − 8: TMA needs the innermost box
+// coordinate 16-byte aligned (measured: an unaligned x traps with an illegal
+// instruction; negative aligned coordinates are fine and zero-fill), so the
+// 42 needed columns sit at offset XOFF = 3 of a 52-float row.  Pitch 52 keeps
+// the horizontal pass's LDS.128 conflict-free (13r + 2s + j covers all eight
+// 16-B bank groups per quarter-warp).
 constexpr int HS = 8;                  // horizontal strip (columns per thread)
-constexpr int VS = 4;                  // vertical strip (rows per thread)
-constexpr int HTASKS = LS * (LT / HS); // 168 horizontal strips per tile
+constexpr int SX = 52;                 // staged row pitch = TMA box width (208 B)
+constexpr int XOFF = 3;                // staged column of image column x0 − HALO
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// ---- TMA + mbarrier (one elected thread issues, every thread waits)
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tma_stage(uint64_t* bar, uint32_t bytes, float* dst0,
+                                          const CUtensorMap* m0, float* dst1, const CUtensorMap* m1,
+                                          int x, int y, int z) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2, %3, %4}], [%5];"
+               ::"r"(su32(dst0)), "l"((uint64_t)m0), "r"(x), "r"(y), "r"(z), "r"(su32(bar))
+               : "memory");
+  if (m1)
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(su32(dst1)), "l"((uint64_t)m1), "r"(x), "r"(y), "r"(z), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+  asm volatile("{\n.reg .pred P1;\nWAIT_%=:\n"
+               "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+               "@!P1 bra WAIT_%=;\n}\n" ::"r"(su32(bar)) : "memory");
+}
+
+template <int VS>
+struct LossTile {
+  static constexpr int LTY = 8 * VS;              // output rows
+  static constexpr int RY = LTY + 2 * HALO;       // staged rows
+  static constexpr int HTASKS = RY * (LT / HS);   // horizontal strips
+  static_assert(HTASKS <= 256, "horizontal strips exceed the CTA");
+  static constexpr int HX = LT + 1;               // horizontal-result row pitch
+  static constexpr int PL = (RY * SX + 31) / 32 * 32;   // one staged plane, 128-B multiple
+  static constexpr size_t fwd_smem = sizeof(float) * (2 * PL + 4 * RY * HX) + 128;
+  static constexpr size_t bwd_smem = sizeof(float) * (3 * RY * SX + 3 * RY * HX) + 128;
+};
+
+__device__ __forceinline__ float* align128(float* p) {
+  return (float*)(((uintptr_t)p + 127) & ~(uintptr_t)127);
+}
+
+// one staged row's 18 inputs of strip c0: row[c0 + XOFF .. c0 + XOFF + 17] as
+// 6 aligned LDS.128 (c0 + 23 < SX); x[k] = input k of the strip
+__device__ __forceinline__ void load_strip(const float* row, float x[HS + 10]) {
+  const float4* p = reinterpret_cast<const float4*>(row);
+  float v[24];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    const float4 a = p[j];
+    v[4 * j] = a.x; v[4 * j + 1] = a.y; v[4 * j + 2] = a.z; v[4 * j + 3] = a.w;
+  }
+#pragma unroll
+  for (int k = 0; k < HS + 10; ++k) x[k] = v[XOFF + k];
+}
+
+template <int VS, bool TMA>
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float* __restrict__ img,
                                                       const float* __restrict__ gt, Win win,
                                                       float* __restrict__ pmaps,
-                                                      double* __restrict__ acc) {
-  __shared__ float sI[LS][LS + 1], sG[LS][LS + 1];
-  __shared__ float sH[4][LS][LT + 1];   // μ_I, μ_G, E[I² + G²], E[IG] (B2 needs only σ_I² + σ_G²)
-  __shared__ double s_red[2][8];
+                                                      double* __restrict__ acc,
+                                                      const __grid_constant__ CUtensorMap tm_img,
+                                                      const __grid_constant__ CUtensorMap tm_gt) {
+  using T = LossTile<VS>;
+  extern __shared__ float smem_raw[];
+  float* sI = align128(smem_raw);                // [RY][SX]
+  float* sG = sI + T::PL;
+  float* sH = sG + T::PL;                        // [4][RY][HX]: μ_I, μ_G, E[I² + G²], E[IG]
+  __shared__ float s_red[2][8];
+  __shared__ __align__(8) uint64_t bar;
   const int ch = blockIdx.z;
   const size_t np = (size_t)W * H;
-  const float* I = img + ch * np;
-  const float* G = gt + ch * np;
-  const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
+  const int x0 = blockIdx.x * LT, y0 = blockIdx.y * T::LTY;
   const int t = threadIdx.x;
-  {
-    // warp-per-row staging: coalesced row segments, no index division
+  if (TMA) {
+    if (t == 0)
+      tma_stage(&bar, 2u * T::RY * SX * 4u, sI, &tm_img, sG, &tm_gt, x0 - HALO - XOFF, y0 - HALO, ch);
+    __syncthreads();   // the mbarrier is initialised before anyone waits on it
+    mbar_wait0(&bar);
+  } else {
+    // coalesced row segments, fully unrolled so every load is in flight before the first store
+    const float* I = img + ch * np;
+    const float* G = gt + ch * np;
     const int lane = t & 31;
-    for (int r = t >> 5; r < LS; r += 8) {
-      const int gy = y0 - HALO + r;
-      const bool rin = gy >= 0 && gy < H;
-      const size_t rowoff = (size_t)(rin ? gy : 0) * W;
+    constexpr int NR = (T::RY + 7) / 8;
+    float vi[NR][2], vg[NR][2];
 #pragma unroll
-      for (int c = lane; c < LS; c += 32) {
-        const int gx = x0 - HALO + c;
-        const bool in = rin && gx >= 0 && gx < W;
-        sI[r][c] = in ? __ldg(I + rowoff + gx) : 0.f;
-        sG[r][c] = in ? __ldg(G + rowoff + gx) : 0.f;
+    for (int i = 0; i < NR; ++i) {
+      const int r = (t >> 5) + 8 * i;
+      const int gy = y0 - HALO + r;
+      const bool rin = r < T::RY && gy >= 0 && gy < H;
+      const float* Ir = I + (size_t)(rin ? gy : 0) * W;
+      const float* Gr = G + (size_t)(rin ? gy : 0) * W;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = lane + 32 * j, gx = x0 - HALO + c;
+        const bool in = rin && c < LS && gx >= 0 && gx < W;
+        vi[i][j] = in ? __ldg(Ir + gx) : 0.f;
+        vg[i][j] = in ? __ldg(Gr + gx) : 0.f;
       }
     }
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int r = (t >> 5) + 8 * i;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = lane + 32 * j;
+        if (r < T::RY && c < LS) { sI[r * SX + XOFF + c] = vi[i][j]; sG[r * SX + XOFF + c] = vg[i][j]; }
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (t < HTASKS) {
+  if (t < T::HTASKS) {
     const int r = t >> 2, c0 = (t & 3) * HS;
     float xi[HS + 10], xg[HS + 10], xsq[HS + 10], xig[HS + 10];
+    load_strip(sI + r * SX + c0, xi);
+    load_strip(sG + r * SX + c0, xg);
 #pragma unroll
     for (int k = 0; k < HS + 10; ++k) {
-      xi[k] = sI[r][c0 + k]; xg[k] = sG[r][c0 + k];
       xsq[k] = fmaf(xi[k], xi[k], xg[k] * xg[k]); xig[k] = xi[k] * xg[k];
     }
 #pragma unroll
@@ -89,7 +194,8 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float
         a = fmaf(w, xi[o + d], a); b = fmaf(w, xg[o + d], b);
         sq = fmaf(w, xsq[o + d], sq); ab = fmaf(w, xig[o + d], ab);
       }
-      sH[0][r][c0 + o] = a; sH[1][r][c0 + o] = b; sH[2][r][c0 + o] = sq; sH[3][r][c0 + o] = ab;
+      float* h = sH + r * T::HX + c0 + o;
+      h[0] = a; h[T::RY * T::HX] = b; h[2 * T::RY * T::HX] = sq; h[3 * T::RY * T::HX] = ab;
     }
   }
   __syncthreads();
@@ -104,7 +210,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float
   for (int k = 0; k < VS + 10; ++k) {
     float v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = sH[q][r0 + k][c];
+    for (int q = 0; q < 4; ++q) v[q] = sH[(q * T::RY + r0 + k) * T::HX + c];
 #pragma unroll
     for (int o = 0; o < VS; ++o) {
       const int d = k - o;
@@ -115,24 +221,27 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float
       }
     }
   }
-  double sum_s = 0.0, sum_l1 = 0.0;
+  // per-thread partial sums in fp32 (≤ VS terms of magnitude ≤ 1), fp64 across threads
+  float sum_s = 0.f, sum_l1 = 0.f;
   float* P = pmaps + (size_t)ch * 3 * np;
+  if (gx < W) {
 #pragma unroll
-  for (int o = 0; o < VS; ++o) {
-    const int r = r0 + o, gy = y0 + r;
-    if (gy >= H || gx >= W) continue;
-    const float m1 = m[o][0], m2 = m[o][1];
-    const float v12 = m[o][3] - m1 * m2;
-    const float A1 = 2.f * m1 * m2 + SSIM_C1, A2 = 2.f * v12 + SSIM_C2;
-    const float B1 = m1 * m1 + m2 * m2 + SSIM_C1, B2 = (m[o][2] - m1 * m1 - m2 * m2) + SSIM_C2;
-    const float iB = 1.f / (B1 * B2);
-    const float S = A1 * A2 * iB;
-    sum_s += S;
-    sum_l1 += fabsf(sI[r + HALO][c + HALO] - sG[r + HALO][c + HALO]);
-    const size_t q = (size_t)gy * W + gx;
-    P[q] = 2.f * m2 * (A2 - A1) * iB - 2.f * m1 * S * (B2 - B1) * iB;   // ∂S/∂μ_I
-    P[np + q] = -S * B1 * iB;                                            // ∂S/∂E[I²] = −S/B2
-    P[2 * np + q] = 2.f * A1 * iB;                                       // ∂S/∂E[IG]
+    for (int o = 0; o < VS; ++o) {
+      const int r = r0 + o, gy = y0 + r;
+      if (gy >= H) break;
+      const float m1 = m[o][0], m2 = m[o][1];
+      const float v12 = m[o][3] - m1 * m2;
+      const float A1 = 2.f * m1 * m2 + SSIM_C1, A2 = 2.f * v12 + SSIM_C2;
+      const float B1 = m1 * m1 + m2 * m2 + SSIM_C1, B2 = (m[o][2] - m1 * m1 - m2 * m2) + SSIM_C2;
+      const float iB = rcp_approx(B1 * B2);
+      const float S = A1 * A2 * iB;
+      sum_s += S;
+      sum_l1 += fabsf(sI[(r + HALO) * SX + XOFF + c + HALO] - sG[(r + HALO) * SX + XOFF + c + HALO]);
+      float* p = P + (size_t)gy * W + gx;
+      p[0] = 2.f * m2 * (A2 - A1) * iB - 2.f * m1 * S * (B2 - B1) * iB;   // ∂S/∂μ_I
+      p[np] = -S * B1 * iB;                                                // ∂S/∂E[I²] = −S/B2
+      p[2 * np] = 2.f * A1 * iB;                                           // ∂S/∂E[IG]
+    }
   }
   // block reduction of (Σ S, Σ|I − G|) → fp64 atomics
 #pragma unroll
@@ -151,60 +260,96 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float
   }
 }
 
+template <int VS, bool TMA>
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(int W, int H, const float* __restrict__ img,
                                                       const float* __restrict__ gt, Win win,
                                                       const float* __restrict__ pmaps, float lambda,
-                                                      float* __restrict__ dL) {
-  __shared__ float sP[3][LS][LS + 1];
-  __shared__ float sH[3][LS][LT + 1];
+                                                      float* __restrict__ dL,
+                                                      const __grid_constant__ CUtensorMap tm_p) {
+  using T = LossTile<VS>;
+  extern __shared__ float smem_raw[];
+  float* sP = align128(smem_raw);                // [3][RY][SX] (one TMA box of 3 planes)
+  float* sH = sP + 3 * T::RY * SX;               // [3][RY][HX]
+  __shared__ __align__(8) uint64_t bar;
   const int ch = blockIdx.z;
   const size_t np = (size_t)W * H;
-  const float* P = pmaps + (size_t)ch * 3 * np;
-  const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
+  const int x0 = blockIdx.x * LT, y0 = blockIdx.y * T::LTY;
   const int t = threadIdx.x;
-  {
+  if (TMA) {
+    if (t == 0)
+      tma_stage(&bar, 3u * T::RY * SX * 4u, sP, &tm_p, nullptr, nullptr, x0 - HALO - XOFF, y0 - HALO, 3 * ch);
+  } else {
+    const float* P = pmaps + (size_t)ch * 3 * np;
     const int lane = t & 31;
-    for (int r = t >> 5; r < LS; r += 8) {
-      const int gy = y0 - HALO + r;
-      const bool rin = gy >= 0 && gy < H;
-      const size_t rowoff = (size_t)(rin ? gy : 0) * W;
+    constexpr int NR = (T::RY + 7) / 8;
+    float v[NR][2][3];
 #pragma unroll
-      for (int c = lane; c < LS; c += 32) {
-        const int gx = x0 - HALO + c;
-        const bool in = rin && gx >= 0 && gx < W;
-        const size_t q = rowoff + gx;
-        sP[0][r][c] = in ? __ldg(P + q) : 0.f;
-        sP[1][r][c] = in ? __ldg(P + np + q) : 0.f;
-        sP[2][r][c] = in ? __ldg(P + 2 * np + q) : 0.f;
+    for (int i = 0; i < NR; ++i) {
+      const int r = (t >> 5) + 8 * i;
+      const int gy = y0 - HALO + r;
+      const bool rin = r < T::RY && gy >= 0 && gy < H;
+      const float* Pr = P + (size_t)(rin ? gy : 0) * W;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = lane + 32 * j, gx = x0 - HALO + c;
+        const bool in = rin && c < LS && gx >= 0 && gx < W;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) v[i][j][q] = in ? __ldg(Pr + q * np + gx) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int r = (t >> 5) + 8 * i;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = lane + 32 * j;
+        if (r < T::RY && c < LS)
+#pragma unroll
+          for (int q = 0; q < 3; ++q) sP[(q * T::RY + r) * SX + XOFF + c] = v[i][j][q];
       }
     }
   }
+  // this thread's output pixels of I and G, loaded now so the latency hides under the stencils
+  const int c = t & 31, r0 = (t >> 5) * VS;
+  const int gx = x0 + c;
+  float iv[VS], gv[VS];
+  {
+    const float* Ic = img + ch * np;
+    const float* Gc = gt + ch * np;
+#pragma unroll
+    for (int o = 0; o < VS; ++o) {
+      const int gy = y0 + r0 + o;
+      const bool in = gx < W && gy < H;
+      const size_t q = in ? (size_t)gy * W + gx : 0;
+      iv[o] = __ldg(Ic + q);
+      gv[o] = __ldg(Gc + q);
+    }
+  }
   __syncthreads();
-  if (t < HTASKS) {
+  if (TMA) mbar_wait0(&bar);
+  if (t < T::HTASKS) {
     const int r = t >> 2, c0 = (t & 3) * HS;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       float x[HS + 10];
-#pragma unroll
-      for (int k = 0; k < HS + 10; ++k) x[k] = sP[q][r][c0 + k];
+      load_strip(sP + (q * T::RY + r) * SX + c0, x);
 #pragma unroll
       for (int o = 0; o < HS; ++o) {
         float a = 0.f;
 #pragma unroll
         for (int d = 0; d < 11; ++d) a = fmaf(win.w[d], x[o + d], a);
-        sH[q][r][c0 + o] = a;
+        sH[(q * T::RY + r) * T::HX + c0 + o] = a;
       }
     }
   }
   __syncthreads();
-  const int c = t & 31, r0 = (t >> 5) * VS;
-  const int gx = x0 + c;
   float m[VS][3];
 #pragma unroll
   for (int o = 0; o < VS; ++o) m[o][0] = m[o][1] = m[o][2] = 0.f;
 #pragma unroll
   for (int k = 0; k < VS + 10; ++k) {
-    const float v0 = sH[0][r0 + k][c], v1 = sH[1][r0 + k][c], v2 = sH[2][r0 + k][c];
+    const float v0 = sH[(r0 + k) * T::HX + c], v1 = sH[(T::RY + r0 + k) * T::HX + c];
+    const float v2 = sH[(2 * T::RY + r0 + k) * T::HX + c];
 #pragma unroll
     for (int o = 0; o < VS; ++o) {
       const int d = k - o;
@@ -214,17 +359,18 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int W, int H, const float
       }
     }
   }
+  if (gx >= W) return;
   const float invM = 1.f / (3.f * (float)np);
+  float* Dc = dL + ch * np;
 #pragma unroll
   for (int o = 0; o < VS; ++o) {
     const int gy = y0 + r0 + o;
-    if (gy >= H || gx >= W) continue;
+    if (gy >= H) break;
     const size_t q = (size_t)gy * W + gx;
-    const float iv = __ldg(img + ch * np + q), gv = __ldg(gt + ch * np + q);
-    const float dssim = m[o][0] + 2.f * iv * m[o][1] + gv * m[o][2];
-    const float d = iv - gv;
+    const float dssim = m[o][0] + 2.f * iv[o] * m[o][1] + gv[o] * m[o][2];
+    const float d = iv[o] - gv[o];
     const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-    dL[ch * np + q] = ((1.f - lambda) * sgn - lambda * dssim) * invM;
+    Dc[q] = ((1.f - lambda) * sgn - lambda * dssim) * invM;
   }
 }
 
@@ -241,23 +387,99 @@ size_t fidelity_loss_workspace(int W, int H) {
   return 256 + sizeof(float) * 9 * (size_t)W * H;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }();
+  return fn;
+}
+
+// [planes][H][W] fp32 as a 3-D tensor map with a (SX, RY, boxz) box; false when
+// TMA cannot address it (row pitch or base not 16-byte aligned)
+bool plane_map(CUtensorMap* m, const float* base, int W, int H, int planes, int RY, int boxz) {
+  auto enc = tensor_map_encoder();
+  if (!enc || (W & 3) || ((uintptr_t)base & 15)) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)SX, (cuuint32_t)RY, (cuuint32_t)boxz};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_allowed() {
+  static const bool ok = [] {
+    const char* v = getenv("DASS_LOSS_TMA");
+    return !(v && v[0] == '0');
+  }();
+  return ok;
+}
+
+template <int VS, bool TMA>
+void set_smem_attrs() {
+  using T = LossTile<VS>;
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(ssim_fwd_kernel<VS, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)T::fwd_smem);
+    cudaFuncSetAttribute(ssim_bwd_kernel<VS, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)T::bwd_smem);
+    done = true;
+  }
+}
+
+template <int VS>
+cudaError_t fidelity_loss_vs(int W, int H, const float* img, const float* gt, float lambda,
+                             double* acc, float* pmaps, float* loss, float* dL, cudaStream_t s) {
+  using T = LossTile<VS>;
+  static const Win win = make_window();
+  const dim3 grid(div_up(W, LT), div_up(H, T::LTY), 3);
+  CUtensorMap mi, mg, mp;
+  const bool tma = tma_allowed() && plane_map(&mi, img, W, H, 3, T::RY, 1) &&
+                   plane_map(&mg, gt, W, H, 3, T::RY, 1) && plane_map(&mp, pmaps, W, H, 9, T::RY, 3);
+  if (tma) {
+    set_smem_attrs<VS, true>();
+    ssim_fwd_kernel<VS, true><<<grid, 256, T::fwd_smem, s>>>(W, H, img, gt, win, pmaps, acc, mi, mg);
+  } else {
+    set_smem_attrs<VS, false>();
+    memset(&mi, 0, sizeof(mi));
+    ssim_fwd_kernel<VS, false><<<grid, 256, T::fwd_smem, s>>>(W, H, img, gt, win, pmaps, acc, mi, mi);
+  }
+  launch_counted();
+  loss_finalize_kernel<<<1, 1, 0, s>>>(acc, 3.0 * (double)W * H, lambda, loss);
+  launch_counted();
+  if (dL) {
+    if (tma)
+      ssim_bwd_kernel<VS, true><<<grid, 256, T::bwd_smem, s>>>(W, H, img, gt, win, pmaps, lambda, dL, mp);
+    else
+      ssim_bwd_kernel<VS, false><<<grid, 256, T::bwd_smem, s>>>(W, H, img, gt, win, pmaps, lambda, dL, mi);
+    launch_counted();
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fidelity_loss(int W, int H, const float* img, const float* gt, float lambda,
                                  void* ws, float* loss, float* dL, cudaStream_t s) {
   double* acc = (double*)ws;
   float* pmaps = (float*)((char*)ws + 256);
   cudaError_t e = cudaMemsetAsync(acc, 0, 2 * sizeof(double), s);
   if (e != cudaSuccess) return e;
-  static const Win win = make_window();
-  const dim3 grid(div_up(W, LT), div_up(H, LT), 3);
-  ssim_fwd_kernel<<<grid, 256, 0, s>>>(W, H, img, gt, win, pmaps, acc);
-  launch_counted();
-  loss_finalize_kernel<<<1, 1, 0, s>>>(acc, 3.0 * (double)W * H, lambda, loss);
-  launch_counted();
-  if (dL) {
-    ssim_bwd_kernel<<<grid, 256, 0, s>>>(W, H, img, gt, win, pmaps, lambda, dL);
-    launch_counted();
+  static const int vs = [] {
+    const char* v = getenv("DASS_LOSS_VS");
+    return v ? atoi(v) : 4;
+  }();
+  switch (vs) {
+    case 5: return fidelity_loss_vs<5>(W, H, img, gt, lambda, acc, pmaps, loss, dL, s);
+    case 6: return fidelity_loss_vs<6>(W, H, img, gt, lambda, acc, pmaps, loss, dL, s);
+    default: return fidelity_loss_vs<4>(W, H, img, gt, lambda, acc, pmaps, loss, dL, s);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace dass

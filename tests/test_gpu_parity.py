@@ -449,15 +449,22 @@ def test_inheritance_mask_and_ste_gradient():
     np.testing.assert_allclose(np_(gm)[off], ref[off], rtol=1e-5, atol=1e-9)
 
 
-@pytest.mark.parametrize("W,H,lam,seed", [(100, 70, 0.2, 1), (37, 300, 0.5, 2), (1, 1, 0.2, 3),
-                                           (1352, 1014, 0.2, 4)])
-def test_fidelity_loss_parity(W, H, lam, seed):
-    """f1 (Eq. 3): loss value and ∂L/∂img against the oracle (direct windows)."""
+@pytest.mark.parametrize("W,H,lam,seed,off", [(100, 70, 0.2, 1, 0), (37, 300, 0.5, 2, 0), (1, 1, 0.2, 3, 0),
+                                               (1352, 1014, 0.2, 4, 0), (64, 40, 0.3, 5, 1)])
+def test_fidelity_loss_parity(W, H, lam, seed, off):
+    """f1 (Eq. 3): loss value and ∂L/∂img against the oracle (direct windows).
+    W % 4 == 0 with 16-B aligned planes stages tiles by TMA (100, 1352); odd
+    widths (37, 1) and a base offset by one float (off = 1) take the load path."""
     g = np.random.default_rng(seed)
     img = g.uniform(0, 1, size=(3, H, W)).astype(np.float32)
     gt = np.clip(img + g.normal(0, 0.1, size=img.shape), 0, 1).astype(np.float32)
     gt[:, : H // 3] = img[:, : H // 3]   # an identical band (sign(0) = 0, S = 1 region)
-    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+    def t(a):
+        buf = torch.empty(a.size + off, dtype=torch.float32, device=DEV)
+        v = buf[off:].view(a.shape)
+        v.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        return v
     ws = torch.empty(dass.dass_fidelity_loss_workspace(W, H) // 4 + 64, dtype=torch.float32, device=DEV)
     loss = torch.zeros(3, device=DEV)
     dL = torch.empty(3, H, W, device=DEV)
