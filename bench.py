@@ -19,6 +19,7 @@ reference arm of this tier) on a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -133,7 +134,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2411_14847_b200 import dass, synth
-    from paper_2411_14847_b200.dist import FlatGrads, allreduce_grads, view_plan
+    from paper_2411_14847_b200.dist import FlatGrads, FlatParams, allreduce_grads, view_plan
     from paper_2411_14847_b200.pipeline import (DeformFields, DeviceScene, MultiViewPass, Raster,
                                                 ViewRecords)
 
@@ -193,10 +194,13 @@ def run_ours(args):
 
     bufs0 = StepBufs(base, mu_d, sigma_d, dLs, grads)
 
-    def step_local(S=bufs0):
-        """Everything on this GPU (capturable: no host sync, no collective)."""
+    def step_local(S=bufs0, wait_inputs=None):
+        """Everything on this GPU (capturable: no host sync, no collective).
+        wait_inputs(): the end-to-end run's wait for this step's parameter upload."""
         g = S.grads
         g.zero_()
+        if wait_inputs is not None:
+            wait_inputs()
         dass.dass_apply_shift(S.base.pos_opa, S.base.rot, S.mu, S.sigma, S.base.dynamic,
                               S.shifted.pos_opa, S.shifted.rot)
         if my_cams:
@@ -511,44 +515,90 @@ def run_ours(args):
         # step k runs set k mod 2, the upload of step k+1 goes straight into the other
         # set (copy engine, pinned host → device), and step k's gradients are read
         # straight out of its set — no device-side staging copies on the compute stream.
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        h_in = [pin(scene.pos_opa), pin(scene.scale), pin(scene.rot), pin(scene.sh), pin(mu),
-                pin(sigma), dLs.cpu().pin_memory()]
-        base1 = DeviceScene(torch.empty_like(base.pos_opa), torch.empty_like(base.scale),
-                            torch.empty_like(base.rot), torch.empty_like(base.sh), deg, base.dynamic)
-        bufs1 = StepBufs(base1, torch.empty_like(mu_d), torch.empty_like(sigma_d),
-                         torch.empty_like(dLs), FlatGrads.allocate(n, K4, dev, num_split=plan.num_split))
-        sets = [bufs0, bufs1]
-        d_in = [[S.base.pos_opa, S.base.scale, S.base.rot, S.base.sh, S.mu, S.sigma, S.dLs]
-                for S in sets]
-        graphs = [graph, None]
-        if graph is not None:
-            graphs[1] = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graphs[1]):
-                step_local(bufs1)
+        # Inputs: the parameters and shift offsets as one flat buffer (dist.FlatParams) — at
+        # N > 1 each rank uploads only its 1/N shard and an in-place all_gather over NVLink
+        # assembles the rest — plus this rank's own views' ∂L/∂C, uploaded view by view.
+        shard_world = plan_world if args.emulate else world
+        shard_rank = plan_rank if args.emulate else rank
+        hp = FlatParams.allocate(n, K4, "cpu", world=shard_world, pin=True)
+        for dst, src in ((hp.pos_opa, scene.pos_opa), (hp.scale, scene.scale), (hp.rot, scene.rot),
+                         (hp.sh, scene.sh), (hp.mu, mu), (hp.sigma, sigma)):
+            dst.copy_(torch.from_numpy(np.ascontiguousarray(src)))
+        h_dl = dLs.cpu().pin_memory()
+        dps = [FlatParams.allocate(n, K4, dev, world=shard_world) for _ in range(2)]
+        for dp in dps:   # whole buffers once; under --emulate the other shards stay as gathered
+            dp.flat.copy_(hp.flat)
+        sets = [StepBufs(DeviceScene(dp.pos_opa, dp.scale, dp.rot, dp.sh, deg, base.dynamic), dp.mu,
+                         dp.sigma, torch.empty_like(dLs),
+                         FlatGrads.allocate(n, K4, dev, num_split=plan.num_split)) for dp in dps]
         h_out = [torch.empty(flat.numel(), dtype=torch.float32).pin_memory() for _ in range(2)]
-        h2d = sum(x.numel() * x.element_size() for x in h_in)
+        h2d_params = hp.shard(shard_rank).numel() * 4
+        h2d = h2d_params + h_dl.numel() * 4
         d2h = flat.numel() * 4
         comp = torch.cuda.current_stream()
         copy_in = torch.cuda.Stream(device=dev)
         copy_out = torch.cuda.Stream(device=dev)
-        ev_in = [torch.cuda.Event() for _ in range(2)]      # upload into set b done
+        nv = len(mine)
+        ev_par = [torch.cuda.Event() for _ in range(2)]     # parameters + offsets of set b landed
+        ev_dl = [[torch.cuda.Event() for _ in range(nv)] for _ in range(2)]   # view v's ∂L/∂C landed
         ev_res = [torch.cuda.Event() for _ in range(2)]     # step on set b done
         ev_out = [torch.cuda.Event() for _ in range(2)]     # download from set b done
+        for e in ev_par + [x for row in ev_dl for x in row]:
+            e.record(copy_in)                               # create the events before capture
+        torch.cuda.synchronize()
+        cudart = ctypes.CDLL("libcudart.so.12")             # the runtime libdass links
+
+        def wait_external(stream, event):
+            """cudaStreamWaitEvent(…, cudaEventWaitExternal): inside a capture this becomes an
+            event-wait node on the upload stream's record of the current step."""
+            rc = cudart.cudaStreamWaitEvent(ctypes.c_void_p(stream.cuda_stream),
+                                            ctypes.c_void_p(event.cuda_event), ctypes.c_uint(1))
+            if rc != 0:
+                raise RuntimeError(f"cudaStreamWaitEvent failed: {rc}")
+
+        # Each set's step graph waits inside itself: for the parameters before the shift, and on
+        # view v's stream for its ∂L/∂C right before its backward, so a step starts as soon as its
+        # 105 MB of parameters have landed while the 20 views' 16 MB gradients images still stream in.
+        graphs = [None, None]
+
+        def hook(b, capture=True):
+            # cudaEventWaitExternal is valid only under capture; eagerly it is a plain wait
+            w = wait_external if capture else (lambda st, e: st.wait_event(e))
+            if mvp is not None:
+                mvp.before_bwd = None if b is None else (lambda v, st: w(st, ev_dl[b][v]))
+
+        for b in range(2):
+            if graph is not None:
+                hook(b)
+                graphs[b] = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graphs[b]):
+                    step_local(sets[b], wait_inputs=lambda b=b: wait_external(
+                        torch.cuda.current_stream(), ev_par[b]))
+        hook(None)
 
         def upload(k):
             b = k % 2
             with torch.cuda.stream(copy_in):
                 copy_in.wait_event(ev_res[b])        # the step that last read set b is done
-                for h, d in zip(h_in, d_in[b]):
-                    d.copy_(h, non_blocking=True)
-                ev_in[b].record(copy_in)
+                dps[b].upload_shard(hp, shard_rank)
+                if world > 1:
+                    dps[b].allgather(rank)           # NCCL, ordered on copy_in
+                ev_par[b].record(copy_in)
+                for v in range(nv):
+                    sets[b].dLs[v].copy_(h_dl[v], non_blocking=True)
+                    ev_dl[b][v].record(copy_in)
 
         def compute(k):
             b = k % 2
-            comp.wait_event(ev_in[b])
             comp.wait_event(ev_out[b])               # set b's previous gradients downloaded
-            run_step(graphs[b], sets[b])
+            if graphs[b] is not None:
+                run_step(graphs[b], sets[b])
+            else:                                    # eager: the same waits, issued directly
+                hook(b, capture=False)
+                step_local(sets[b], wait_inputs=lambda: comp.wait_event(ev_par[b]))
+                hook(None)
+                if distd:
+                    allreduce_grads(sets[b].grads, finish=finish_split)
             ev_res[b].record(comp)
 
         def download(k):
@@ -582,9 +632,13 @@ def run_ours(args):
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e2e = {"value": job_views / (float(ems.item()) / 1e3), "unit": "views/s",
                "ms_per_step": float(ems.item()), "h2d_bytes_per_step": int(h2d),
+               "h2d_params_shard": f"{h2d_params} B = 1/{shard_world} of the parameters"
+                                   + ("; the all_gather is not run under --emulate" if args.emulate
+                                      and shard_world > 1 else ""),
                "d2h_bytes_per_step": int(d2h),
                "pipelining": "two buffer sets, one captured graph each: the upload of step k+1 "
-                             "and the download of step k−1 overlap step k, with no device-side copies"}
+                             "and the download of step k−1 overlap step k, with no device-side copies; "
+                             "inside a step, view v's backward waits only for its own dL/dC upload"}
 
     # ---- gather stats to rank 0
     if distd:

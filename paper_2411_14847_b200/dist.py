@@ -111,6 +111,60 @@ class FlatGrads:
         self.gradstat_cnt.zero_()
 
 
+@dataclass
+class FlatParams:
+    """A step's per-Gaussian inputs as views of one contiguous fp32 buffer:
+    pos_opa, scale, rot [N,4]; sh [K4,N,4]; mu, sigma [N,4] (the shift
+    offsets).  The buffer length is padded to a multiple of 4·world floats, so
+    the buffer splits into `world` equal 16-byte-aligned shards.
+
+    End to end, every rank needs all of it, but need not upload all of it: rank
+    r copies only shard r from host memory and one in-place all_gather over
+    NVLink assembles the rest (`upload_shard` + `allgather`), so the
+    host→device traffic per rank is 1/world of the parameters."""
+    flat: "torch.Tensor"
+    pos_opa: "torch.Tensor"
+    scale: "torch.Tensor"
+    rot: "torch.Tensor"
+    sh: "torch.Tensor"
+    mu: "torch.Tensor"
+    sigma: "torch.Tensor"
+    world: int = 1
+
+    @staticmethod
+    def sizes(n: int, k4: int) -> list[int]:
+        return [n * 4, n * 4, n * 4, k4 * n * 4, n * 4, n * 4]
+
+    @staticmethod
+    def allocate(n: int, k4: int, device="cuda", world: int = 1, pin: bool = False) -> "FlatParams":
+        import torch
+        sizes = FlatParams.sizes(n, k4)
+        total = sum(sizes)
+        total += (-total) % (4 * world)
+        flat = torch.zeros(total, dtype=torch.float32, device=device)
+        if pin:
+            flat = flat.pin_memory()
+        p = list(torch.split(flat[:sum(sizes)], sizes))
+        return FlatParams(flat, p[0].view(n, 4), p[1].view(n, 4), p[2].view(n, 4),
+                          p[3].view(k4, n, 4), p[4].view(n, 4), p[5].view(n, 4), world)
+
+    def shard(self, rank: int) -> "torch.Tensor":
+        """Rank `rank`'s contiguous 1/world of the buffer."""
+        L = self.flat.numel() // self.world
+        return self.flat[rank * L:(rank + 1) * L]
+
+    def upload_shard(self, host: "FlatParams", rank: int):
+        """Copy shard `rank` of the (pinned) host buffer into this device buffer
+        on the current stream; world == 1 copies everything."""
+        self.shard(rank).copy_(host.shard(rank), non_blocking=True)
+
+    def allgather(self, rank: int, group=None):
+        """Assemble every rank's shard in place (no-op at world 1)."""
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(self.flat, self.shard(rank), group=group)
+
+
 def allreduce_grads(g: FlatGrads, group=None, counts: bool = True, finish=None):
     """SUM over ranks of every gradient (A27: gradients are summed over views).
     With split views (g.uv), `finish(g)` then adds their ∇p̄ terms from the

@@ -172,6 +172,9 @@ class MultiViewPass:
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.S)]
         self.pre_stream = torch.cuda.Stream(device=device)
         self.pre_chunks = int(os.environ.get("DASS_PRE_CHUNKS", "2"))
+        # optional hook(v, stream), called on view v's stream right before its backward:
+        # an end-to-end caller makes the view wait there for its own ∂L/∂C upload
+        self.before_bwd = None
         self.g2d = torch.empty(max(self.V, 1), n, 12, dtype=torch.float32, device=device)
 
     def enable_loss(self, lam: float = 0.2):
@@ -214,6 +217,8 @@ class MultiViewPass:
                                             self.losses[v], dL)
                 else:
                     dL = dL_dimgs[v]
+                if self.before_bwd is not None:
+                    self.before_bwd(v, st)
                 dass.dass_render_bwd_raster(cam, self.n, ras.ranges, ras.sorted_ids, xy, co, rgb,
                                             box, bg, ras.T, ras.last, dL, self.g2d[v],
                                             ras.accept, ras.capacity, tiles=self.tiles[v])

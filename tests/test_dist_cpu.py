@@ -180,3 +180,39 @@ def test_split_view_uv_blocks_through_allreduce(tmp_path):
     want = 2.0 + np.sqrt((tot ** 2).sum(-1)).sum(0)
     np.testing.assert_allclose(r["stat"], want, rtol=1e-5)
     assert np.array_equal(r["cnt"], 2 * vis.astype(np.int32))
+
+
+def _params_worker(rank, world, port, out_path):
+    """Each rank uploads only its shard of the flat parameter buffer; the
+    in-place all_gather gives every rank the whole buffer (bench.py e2e)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, k4 = 37, 3
+    host = ddist.FlatParams.allocate(n, k4, "cpu", world=world)
+    host.flat[:] = torch.arange(host.flat.numel(), dtype=torch.float32)
+    dev = ddist.FlatParams.allocate(n, k4, "cpu", world=world)
+    dev.upload_shard(host, rank)
+    other = dev.shard(1 - rank)
+    assert torch.count_nonzero(other) == 0              # not uploaded here
+    dev.allgather(rank)
+    if rank == 0:
+        np.savez(out_path, flat=dev.flat.numpy(), sh=dev.sh.numpy(), mu=dev.mu.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_flat_params_shard_upload_allgather(tmp_path):
+    n, k4, world = 37, 3, 2
+    p = ddist.FlatParams.allocate(n, k4, "cpu", world=world)
+    L = p.flat.numel()
+    assert L % (4 * world) == 0 and L >= sum(ddist.FlatParams.sizes(n, k4))
+    assert p.shard(0).numel() == p.shard(1).numel() == L // world
+    # the views tile the buffer in order, 16-byte aligned
+    offs = [t.data_ptr() - p.flat.data_ptr() for t in (p.pos_opa, p.scale, p.rot, p.sh, p.mu, p.sigma)]
+    assert offs == [0, 16 * n, 32 * n, 48 * n, 48 * n + 16 * k4 * n, 64 * n + 16 * k4 * n]
+    out = str(tmp_path / "p.npz")
+    mp.spawn(_params_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    r = np.load(out)
+    want = np.arange(L, dtype=np.float32)
+    assert np.array_equal(r["flat"], want)
+    assert np.array_equal(r["sh"].ravel(), want[12 * n:12 * n + 4 * k4 * n])
