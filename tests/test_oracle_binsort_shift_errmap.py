@@ -8,7 +8,6 @@ O7: §3.4, Alg. 1 P:403-415 — pinned by S:213-215/S:630 examples and
 the textbook pinhole projection.
 """
 import json
-import math
 import os
 
 import numpy as np

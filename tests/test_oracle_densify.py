@@ -13,7 +13,6 @@ What pins what:
     forms); all-ones features give 1 − T (partition of unity).
 """
 import numpy as np
-import pytest
 
 import oracle
 from paper_2411_14847_b200 import synth

@@ -1,6 +1,5 @@
 """Pins of the f3 oracle (Eq. 1, STE P:389-393, Eq. 2)."""
 import json
-import math
 import os
 
 import numpy as np

@@ -1,6 +1,5 @@
 """Pins of the f1 oracle: the fidelity loss of Eq. 3 with
 D-SSIM = 1 − SSIM (A39), 11×11 Gaussian window σ = 1.5, zero padding."""
-import math
 
 import numpy as np
 import pytest
