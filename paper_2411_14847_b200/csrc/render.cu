@@ -747,12 +747,17 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
   uint32_t nvis = 0, ncnt = 0;
   for (int v = 0; v < a.num_views; ++v) {
     const size_t o = (size_t)v * n + i;
+    // every load of this view issued before the visibility branch: one memory
+    // latency per view instead of two in series (a culled view's loads are wasted)
     const uint2 bx = a.box[o];
+    const float4 m1 = a.g2d[3 * o + 1], m2 = a.g2d[3 * o + 2];
+    const float rgbw = a.rgb[o].w;
+    const float4 m0 = PART == 1 ? a.g2d[3 * o] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 co = PART == 1 ? a.conic_opa[o] : make_float4(0.f, 0.f, 0.f, 0.f);
     if ((bx.x & 0xFFFFu) > (bx.x >> 16)) continue;  // culled in this view
     const CamParams& cam = a.cam[v];
     ++nvis;
-    const float4 m1 = a.g2d[3 * o + 1], m2 = a.g2d[3 * o + 2];
-    const int bits = (int)a.rgb[o].w;
+    const int bits = (int)rgbw;
     const float gcol[3] = {(bits & 1) ? 0.f : m1.z, (bits & 2) ? 0.f : m1.w, (bits & 4) ? 0.f : m2.x};
     if (PART == 2) {
       F dx = (F)po.x - cam.campos[0], dy = (F)po.y - cam.campos[1], dz = (F)po.z - cam.campos[2];
@@ -763,8 +768,6 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
       for (int f = 0; f < L::NF; ++f) gsh[f] += Y[f / 3] * gcol[f % 3];
       continue;
     }
-    const float4 m0 = a.g2d[3 * o];
-    const float4 co = a.conic_opa[o];
     const F A = co.x, B = co.y, Cc = co.z, op = co.w;
     // 2D gradients from the moments
     const F gu = -op * (A * m0.x + B * m0.y);
