@@ -42,7 +42,7 @@ FP32_LANES = 128
 # Algorithmic FP32 work per accepted (pixel, entry) unit of render_bwd's raster
 # part (FMA = 2 flop).  Rejected in-box evaluations are not
 # counted, so the reported fraction is conservative.
-FLOP_BWD_ACCEPTED = 48
+FLOP_BWD_ACCEPTED = 42
 STEP_OPS = ("project_views", "bin_sort", "render_fwd", "render_bwd_raster",
             "render_bwd_preprocess_views")
 
@@ -852,12 +852,12 @@ def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg):
                          "peak_tflops": round(peak_fp32, 1), "frac": round(fl / t / 1e12 / peak_fp32, 4),
                          "unit": "15 flop per accepted (pixel, entry) + 8 per in-box evaluation"}
     t = ops["render_bwd_raster"] / 1e3
-    fl = 48.0 * acc
+    fl = float(FLOP_BWD_ACCEPTED) * acc
     out["render_bwd_raster"] = {"bound": "alu", "flop": int(fl),
                                 "achieved_tflops": round(fl / t / 1e12, 2),
                                 "peak_tflops": round(peak_fp32, 1),
                                 "frac": round(fl / t / 1e12 / peak_fp32, 4),
-                                "unit": "48 flop per accepted (pixel, entry)"}
+                                "unit": f"{FLOP_BWD_ACCEPTED} flop per accepted (pixel, entry)"}
     return out
 
 

@@ -509,9 +509,12 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
           gR[p] += gc * w;                    // g·(S + T_final·bg), S = suffix colour
           v[6] += w * g[p][0]; v[7] += w * g[p][1]; v[8] += w * g[p][2];
           const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
-          const float ex = e * dx, ey = e * dy;
-          v[0] += ex; v[1] += ey; v[2] += ex * dx; v[3] += ex * dy; v[4] += ey * dy; v[5] += e;
+          const float ey = e * dy;
+          v[1] += ey; v[4] += ey * dy; v[5] += e;
         }
+        // the lane's PPT pixels share one column, so dx factors out of the
+        // dx-moments: Σe·dx = dx·Σe, Σe·dx² = dx·(dx·Σe), Σe·dx·dy = dx·Σe·dy
+        v[0] = v[5] * dx; v[2] = v[0] * dx; v[3] = v[1] * dx;
       }
       if (__any_sync(0xffffffffu, any)) {
         const float sum = rs.reduce(v);
@@ -646,9 +649,12 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
           gR[p] += gc * w;                    // g·(S + T_final·bg), S = suffix colour
           v[6] += w * g[p][0]; v[7] += w * g[p][1]; v[8] += w * g[p][2];
           const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
-          const float ex = e * dx, ey = e * dy;
-          v[0] += ex; v[1] += ey; v[2] += ex * dx; v[3] += ex * dy; v[4] += ey * dy; v[5] += e;
+          const float ey = e * dy;
+          v[1] += ey; v[4] += ey * dy; v[5] += e;
         }
+        // the lane's PPT pixels share one column, so dx factors out of the
+        // dx-moments: Σe·dx = dx·Σe, Σe·dx² = dx·(dx·Σe), Σe·dx·dy = dx·Σe·dy
+        v[0] = v[5] * dx; v[2] = v[0] * dx; v[3] = v[1] * dx;
       }
       const float sum = rs.reduce(v);
       if (rs.slot >= 0) s_acc[warp][k][rs.slot] = sum;

@@ -27,6 +27,6 @@ def test_hot_path_roofline():
     assert set(out) == set(ops)
     for v in out.values():
         assert 0 < v["frac"] < 1
-    # the backward's flop count is 48 per accepted unit
-    assert out["render_bwd_raster"]["flop"] == 48 * 65_000_000 * 20
+    # the backward's flop count is 42 per accepted unit
+    assert out["render_bwd_raster"]["flop"] == 42 * 65_000_000 * 20
     assert bench.hot_path_roofline({}, stats, {}, 74.4, 1, 1, 0) is None
