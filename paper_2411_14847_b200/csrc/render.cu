@@ -155,6 +155,37 @@ struct AcceptLists {
   uint8_t* bytes;
 };
 
+// Pixel ownership of a tile CTA (NT = 256/PPT threads, 16×16 pixels).
+//   PPT = 4 ("quadrant map", the list path): warp w owns the 16×8 half-tile of
+//     rows [8w, 8w+8); lane l owns one pixel in each of its four 8×4
+//     quadrants, (cx + 8·(p&1), cy + 4·(p>>1)) with cx = l&7, cy = 8w + (l>>3).
+//     A compact footprint covers few quadrants, so the per-p pixel blocks a
+//     warp executes for one entry (any lane with bit p) drop from 3.5 to 2.5
+//     per accepted warp-entry on the C3 scene; two
+//     columns and two rows per lane keep dx/dy at two values each.
+//   other PPT ("row map"): thread t owns column t&15, rows (t>>4)·PPT + p.
+template <int PPT>
+struct PixMap {
+  static constexpr bool QUAD = PPT == 4;
+  int cx, cy;
+  __device__ __forceinline__ explicit PixMap(int t) {
+    if (QUAD) { cx = t & 7; cy = ((t >> 5) << 3) + ((t >> 3) & 3); }
+    else { cx = t & 15; cy = (t >> 4) * PPT; }
+  }
+  __device__ __forceinline__ int x(int p) const { return QUAD ? cx + 8 * (p & 1) : cx; }
+  __device__ __forceinline__ int y(int p) const { return QUAD ? cy + 4 * (p >> 1) : cy + p; }
+  // bit p set iff pixel p's column and row bits are both set in the entry's
+  // tile-local support mask m (columns in bits 0-15, rows in bits 16-31)
+  __device__ __forceinline__ uint32_t cand(uint32_t m) const {
+    if (QUAD) {
+      const uint32_t c2 = ((m >> cx) & 1u) | ((m >> (cx + 7)) & 2u);
+      const uint32_t r = m >> (16 + cy);
+      return ((r & 1u) ? c2 : 0u) | ((r & 16u) ? (c2 << 2) : 0u);
+    }
+    return ((m >> cx) & 1u) ? ((m >> (16 + cy)) & ((1u << PPT) - 1u)) : 0u;
+  }
+};
+
 // ------------------------------------------------------------- forward ----
 template <int PPT, bool LISTS, int RPW = 16, int MINB = 768 / (256 / PPT)>
 __global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
@@ -172,25 +203,23 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
   const int t = threadIdx.x;
-  const int lx = t & 15, ly0 = (t >> 4) * PPT;
-  const int X = tx0 + lx;
+  const PixMap<PPT> pm(t);
   const uint32_t wmask = warp_row_mask<PPT>(t >> 5);
-  const uint32_t colbit = 1u << lx;
   const uint2 range = ranges[tile];
   float T[PPT], C[PPT][3];
   uint32_t last[PPT];
   uint32_t live = 0;   // bit p: pixel p is inside the image and not terminated
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int Y = ty0 + ly0 + p;
     T[p] = 1.f; C[p][0] = C[p][1] = C[p][2] = 0.f;
     last[p] = range.x;
-    if (X < cam.W && Y < cam.H) live |= 1u << p;
+    if (tx0 + pm.x(p) < cam.W && ty0 + pm.y(p) < cam.H) live |= 1u << p;
   }
-  const float fx = (float)lx;
+  // tile-relative pixel coordinates: columns fxc[p & 1] (quad) / fxc[0] (row map)
+  const float fxc[2] = {(float)pm.x(0), (float)pm.x(PPT > 1 ? 1 : 0)};
   float fy[PPT];
 #pragma unroll
-  for (int p = 0; p < PPT; ++p) fy[p] = (float)(ly0 + p);
+  for (int p = 0; p < PPT; ++p) fy[p] = (float)pm.y(p);
   // acceptance list of this warp: entries (absolute list index, 4 ballot words)
   const uint32_t warp = t >> 5, lane = t & 31u;
   const size_t lbase = (size_t)NW * range.x + (size_t)warp * (range.y - range.x);
@@ -208,18 +237,26 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
       const uint32_t m = __float_as_uint(a.w);
       if ((m & wmask) == 0u) continue;   // warp-uniform: box misses this warp's rows
       uint32_t accb = 0;                 // this lane's accepted pixels of the entry
-      // candidate pixels: column in the mask, row in the mask, still live
-      const uint32_t cand = (m & colbit) ? ((m >> (16 + ly0)) & live) : 0u;
+      // candidate pixels: column and row in the support mask, still live
+      const uint32_t cand = pm.cand(m) & live;
       if (cand) {
         const float4 co = st.co;
-        const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fx);
         float pw[PPT];
         uint32_t ok = 0;
+        if constexpr (PixMap<PPT>::QUAD) {
+          const ColTerms c0 = col_terms(co.x, co.y, co.z, a.x - fxc[0]);
+          const ColTerms c1 = col_terms(co.x, co.y, co.z, a.x - fxc[1]);
+          const float dy0 = a.y - fy[0], dy1 = a.y - fy[2];
+          pw[0] = splat_power(c0, dy0); pw[1] = splat_power(c1, dy0);
+          pw[2] = splat_power(c0, dy1); pw[3] = splat_power(c1, dy1);
+        } else {
+          const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fxc[0]);
 #pragma unroll
-        for (int p = 0; p < PPT; ++p) {   // independent per pixel: no branches, full ILP
-          pw[p] = splat_power(ct, a.y - fy[p]);
-          ok |= (!(pw[p] > 0.f) && !(pw[p] < a.z)) ? (1u << p) : 0u;
+          for (int p = 0; p < PPT; ++p) pw[p] = splat_power(ct, a.y - fy[p]);
         }
+#pragma unroll
+        for (int p = 0; p < PPT; ++p)   // independent per pixel: no branches, full ILP
+          ok |= (!(pw[p] > 0.f) && !(pw[p] < a.z)) ? (1u << p) : 0u;
         ok &= cand;
         if (ok) {
           const float4 c = st.c;
@@ -251,7 +288,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
   if (LISTS && lane == 0) acc.cnt[(size_t)NW * tile + warp] = nlist;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int Y = ty0 + ly0 + p;
+    const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
     if (X < cam.W && Y < cam.H) {
       const size_t pix = (size_t)Y * cam.W + X, np = (size_t)cam.W * cam.H;
       out_img[pix] = C[p][0] + T[p] * bg.x;
@@ -576,8 +613,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
   const int t = threadIdx.x;
   const int warp = t >> 5;
   const uint32_t lane = t & 31u;
-  const int lx = t & 15, ly0 = (t >> 4) * PPT;
-  const int X = tx0 + lx;
+  const PixMap<PPT> pm(t);   // the forward's quadrant map (the lists' bit p)
   const uint2 range = ranges[tile];
   const size_t lbase = (size_t)NW * range.x + (size_t)warp * (range.y - range.x);
   const uint32_t n = acc.cnt[(size_t)NW * tile + warp];
@@ -588,7 +624,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
   const size_t np = (size_t)cam.W * cam.H;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    const int Y = ty0 + ly0 + p;
+    const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
     if (X < cam.W && Y < cam.H) {
       const size_t pix = (size_t)Y * cam.W + X;
       T[p] = out_T[pix];
@@ -599,10 +635,9 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
     }
     gR[p] = T[p] * (g[p][0] * bg.x + g[p][1] * bg.y + g[p][2] * bg.z);
   }
-  const float fx = (float)lx;
-  float fy[PPT];
-#pragma unroll
-  for (int p = 0; p < PPT; ++p) fy[p] = (float)(ly0 + p);
+  // two columns (p & 1) and two rows (p >> 1) per lane, tile-relative
+  const float fx0 = (float)pm.x(0), fx1 = (float)pm.x(1);
+  const float fy0 = (float)pm.y(0), fy1 = (float)pm.y(2);
   for (int ptr = (int)n; ptr > 0;) {
     const int k0 = ptr > 32 ? ptr - 32 : 0;
     const int cnt = ptr - k0;
@@ -632,13 +667,16 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
         const float4 a = s_a[warp][k];
         const float4 co = s_co[warp][k];
         const float4 c = s_c[warp][k];
-        const float dx = a.x - fx;
-        const ColTerms ct = col_terms(co.x, co.y, co.z, dx);
+        const float dxc[2] = {a.x - fx0, a.x - fx1};
+        const float dyr[2] = {a.y - fy0, a.y - fy1};
+        const ColTerms ct[2] = {col_terms(co.x, co.y, co.z, dxc[0]),
+                                col_terms(co.x, co.y, co.z, dxc[1])};
+        float se[2] = {0.f, 0.f}, sey[2] = {0.f, 0.f};   // per column: Σe, Σe·dy
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
           if (!((bits >> p) & 1u)) continue;
-          const float dy = a.y - fy[p];
-          const float G = splat_exp(splat_power(ct, dy));
+          const float dy = dyr[p >> 1];
+          const float G = splat_exp(splat_power(ct[p & 1], dy));
           const float oG = __fmul_rn(co.w, G);
           const float alpha = fminf(ALPHA_MAX, oG);
           const float inv = rcp_approx(1.f - alpha);
@@ -650,11 +688,16 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
           v[6] += w * g[p][0]; v[7] += w * g[p][1]; v[8] += w * g[p][2];
           const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
           const float ey = e * dy;
-          v[1] += ey; v[4] += ey * dy; v[5] += e;
+          sey[p & 1] += ey; v[4] += ey * dy; se[p & 1] += e;
         }
-        // the lane's PPT pixels share one column, so dx factors out of the
-        // dx-moments: Σe·dx = dx·Σe, Σe·dx² = dx·(dx·Σe), Σe·dx·dy = dx·Σe·dy
-        v[0] = v[5] * dx; v[2] = v[0] * dx; v[3] = v[1] * dx;
+        // dx is constant per column, so the dx-moments factor out of the pixel
+        // loop: Σe·dx = Σ_col dx·Σe, Σe·dx² = Σ_col dx·(dx·Σe), Σe·dx·dy = Σ_col dx·Σe·dy
+        const float m0 = se[0] * dxc[0], m1 = se[1] * dxc[1];
+        v[0] = m0 + m1;
+        v[1] = sey[0] + sey[1];
+        v[2] = m0 * dxc[0] + m1 * dxc[1];
+        v[3] = sey[0] * dxc[0] + sey[1] * dxc[1];
+        v[5] = se[0] + se[1];
       }
       const float sum = rs.reduce(v);
       if (rs.slot >= 0) s_acc[warp][k][rs.slot] = sum;
