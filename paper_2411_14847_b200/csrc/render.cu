@@ -715,6 +715,246 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
   }
 }
 
+// ------------------------------------- tile-warp list path (TW, PPT = 8) ----
+// One warp per 16×16 tile (32-thread CTAs).  Lane l owns the eight pixels
+// (cx + 8·(p>>2), cy + 4·(p&3)), cx = l&7, cy = l>>3: one per 8×4 block of
+// the tile, so a compact footprint covers few blocks p.  Against the two
+// half-tile warps of the PPT = 4 path, an entry whose accepted pixels span
+// both halves is walked, staged and reduced once instead of twice (a CPU
+// replay of a C3 view: 0.67× the warp-entries, identical pixel blocks).  The
+// list is one per tile: entry k of tile t at [range.x + k], byte `lane` = the
+// lane's 8-bit accepted set, cnt[t].
+struct TileMap {
+  int cx, cy;
+  __device__ __forceinline__ explicit TileMap(int lane) : cx(lane & 7), cy(lane >> 3) {}
+  __device__ __forceinline__ int x(int p) const { return cx + 8 * (p >> 2); }
+  __device__ __forceinline__ int y(int p) const { return cy + 4 * (p & 3); }
+  // bit p set iff pixel p's column and row bits are both set in m
+  __device__ __forceinline__ uint32_t cand(uint32_t m) const {
+    const uint32_t c = ((m >> cx) & 1u) | ((m >> (cx + 4)) & 16u);      // columns cx, cx+8 → bits 0, 4
+    const uint32_t r = m >> (16 + cy);                                  // rows cy+4i at bits 4i
+    const uint32_t r4 = (r & 1u) | ((r >> 3) & 2u) | ((r >> 6) & 4u) | ((r >> 9) & 8u);
+    return c * r4;   // outer product: bit (p&3) + 4·(p>>2)
+  }
+};
+
+template <int MINB>
+__global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
+    const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
+    const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
+    const uint2* __restrict__ box, float3 bg, float* __restrict__ out_img,
+    float* __restrict__ out_T, uint32_t* __restrict__ out_last, AcceptLists acc) {
+  constexpr int PPT = 8;
+  constexpr int BATCH = 64;
+  __shared__ Staged s_st[BATCH];
+  const int tile = cam.tile0 + blockIdx.x * cam.tstride;
+  const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
+  const int tx0 = txi * TILE, ty0 = tyi * TILE;
+  const uint32_t lane = threadIdx.x;
+  const TileMap pm((int)lane);
+  const uint2 range = ranges[tile];
+  float T[PPT], C[PPT][3];
+  uint32_t last[PPT];
+  uint32_t live = 0;   // bit p: pixel p is inside the image and not terminated
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    T[p] = 1.f; C[p][0] = C[p][1] = C[p][2] = 0.f;
+    last[p] = range.x;
+    if (tx0 + pm.x(p) < cam.W && ty0 + pm.y(p) < cam.H) live |= 1u << p;
+  }
+  const float fx0 = (float)pm.x(0), fx1 = (float)pm.x(4);
+  float fy[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) fy[r] = (float)pm.y(r);
+  uint32_t nlist = 0;
+  for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
+    if (!__any_sync(0xffffffffu, live != 0u)) break;
+    __syncwarp();   // the previous batch is consumed
+    for (int k = (int)lane; k < BATCH; k += 32)
+      if (b0 + k < range.y) stage<16>(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
+    __syncwarp();
+    const int cnt = (int)min((uint32_t)BATCH, range.y - b0);
+    for (int j = 0; j < cnt; ++j) {
+      const Staged& st = s_st[j];
+      const float4 a = st.a;
+      const uint32_t m = __float_as_uint(a.w);
+      if (m == 0u) continue;             // warp-uniform: support misses the tile
+      uint32_t accb = 0;                 // this lane's accepted pixels of the entry
+      const uint32_t cand = pm.cand(m) & live;
+      if (cand) {
+        const float4 co = st.co;
+        const ColTerms c0 = col_terms(co.x, co.y, co.z, a.x - fx0);
+        const ColTerms c1 = col_terms(co.x, co.y, co.z, a.x - fx1);
+        float pw[PPT];
+        uint32_t ok = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float dy = a.y - fy[r];
+          pw[r] = splat_power(c0, dy);
+          pw[r + 4] = splat_power(c1, dy);
+        }
+#pragma unroll
+        for (int p = 0; p < PPT; ++p)
+          ok |= (!(pw[p] > 0.f) && !(pw[p] < a.z)) ? (1u << p) : 0u;
+        ok &= cand;
+        if (ok) {
+          const float4 c = st.c;
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) {
+            if (!((ok >> p) & 1u)) continue;
+            const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
+            if (alpha < ALPHA_MIN) continue;
+            const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
+            if (tn < T_MIN) { live &= ~(1u << p); continue; }
+            const float w = alpha * T[p];
+            C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
+            T[p] = tn;
+            last[p] = b0 + j + 1;
+            accb |= 1u << p;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, accb != 0u)) {
+        const size_t e = (size_t)range.x + nlist;
+        acc.bytes[e * 32 + lane] = (uint8_t)accb;
+        if (lane == 0) acc.idx[e] = b0 + j;
+        ++nlist;
+      }
+    }
+  }
+  if (lane == 0) acc.cnt[tile] = nlist;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
+    if (X < cam.W && Y < cam.H) {
+      const size_t pix = (size_t)Y * cam.W + X, np = (size_t)cam.W * cam.H;
+      out_img[pix] = C[p][0] + T[p] * bg.x;
+      out_img[np + pix] = C[p][1] + T[p] * bg.y;
+      out_img[2 * np + pix] = C[p][2] + T[p] * bg.z;
+      out_T[pix] = T[p];
+      out_last[pix] = last[p];
+    }
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
+    const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
+    const float4* __restrict__ conic_opa, const float4* __restrict__ rgb, float3 bg,
+    const float* __restrict__ out_T, const float* __restrict__ dL_dimg, AcceptLists acc,
+    float4* __restrict__ g2d) {
+  constexpr int PPT = 8;
+  __shared__ float4 s_a[32];    // (u_rel, v_rel, −, −)
+  __shared__ float4 s_co[32];   // (A, B, C, o)
+  __shared__ float4 s_c[32];    // (r, g, b, −)
+  __shared__ uint4 s_bytes[32][2];
+  __shared__ uint32_t s_id[32];
+  __shared__ float s_acc[32][9];
+  const int tile = cam.tile0 + blockIdx.x * cam.tstride;
+  const uint32_t n = acc.cnt[tile];
+  if (n == 0) return;
+  const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
+  const int tx0 = txi * TILE, ty0 = tyi * TILE;
+  const uint32_t lane = threadIdx.x;
+  const TileMap pm((int)lane);
+  const uint2 range = ranges[tile];
+  LaneRS rs;
+  rs.init();
+  float T[PPT], gR[PPT], g[PPT][3];
+  const size_t np = (size_t)cam.W * cam.H;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
+    if (X < cam.W && Y < cam.H) {
+      const size_t pix = (size_t)Y * cam.W + X;
+      T[p] = out_T[pix];
+      g[p][0] = dL_dimg[pix]; g[p][1] = dL_dimg[np + pix]; g[p][2] = dL_dimg[2 * np + pix];
+    } else {
+      T[p] = 1.f;
+      g[p][0] = g[p][1] = g[p][2] = 0.f;
+    }
+    gR[p] = T[p] * (g[p][0] * bg.x + g[p][1] * bg.y + g[p][2] * bg.z);
+  }
+  const float fx0 = (float)pm.x(0), fx1 = (float)pm.x(4);
+  float fy[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) fy[r] = (float)pm.y(r);
+  for (int ptr = (int)n; ptr > 0;) {
+    const int k0 = ptr > 32 ? ptr - 32 : 0;
+    const int cnt = ptr - k0;
+    if ((int)lane < cnt) {
+      const size_t e = (size_t)range.x + k0 + lane;
+      const uint32_t id = ids[acc.idx[e]];
+      const uint4* src = reinterpret_cast<const uint4*>(acc.bytes + e * 32);
+      s_bytes[lane][0] = src[0];
+      s_bytes[lane][1] = src[1];
+      s_id[lane] = id;
+      // the forward's staging arithmetic for (u_rel, v_rel): identical bits
+      const float4 xy = xy_depth[id];
+      const uint32_t lo_bits = __float_as_uint(xy.w);
+      const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
+      s_a[lane] = make_float4(__fadd_rn(xy.x - (float)tx0, __low2float(lo)),
+                              __fadd_rn(xy.y - (float)ty0, __high2float(lo)), 0.f, 0.f);
+      s_co[lane] = conic_opa[id];
+      s_c[lane] = rgb[id];
+    }
+    __syncwarp();
+    for (int k = cnt - 1; k >= 0; --k) {
+      const uint32_t bits = reinterpret_cast<const uint8_t*>(&s_bytes[k][0])[lane];
+      float v[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) v[q] = 0.f;
+      if (bits) {
+        const float4 a = s_a[k];
+        const float4 co = s_co[k];
+        const float4 c = s_c[k];
+        const float dxc[2] = {a.x - fx0, a.x - fx1};
+        const ColTerms ct[2] = {col_terms(co.x, co.y, co.z, dxc[0]),
+                                col_terms(co.x, co.y, co.z, dxc[1])};
+        float se[2] = {0.f, 0.f}, sey[2] = {0.f, 0.f};   // per column: Σe, Σe·dy
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          if (!((bits >> p) & 1u)) continue;
+          const float dy = a.y - fy[p & 3];
+          const float G = splat_exp(splat_power(ct[p >> 2], dy));
+          const float oG = __fmul_rn(co.w, G);
+          const float alpha = fminf(ALPHA_MAX, oG);
+          const float inv = rcp_approx(1.f - alpha);
+          T[p] *= inv;                        // transmittance before this entry
+          const float w = alpha * T[p];
+          const float gc = g[p][0] * c.x + g[p][1] * c.y + g[p][2] * c.z;
+          const float dLda = T[p] * gc - inv * gR[p];
+          gR[p] += gc * w;                    // g·(S + T_final·bg), S = suffix colour
+          v[6] += w * g[p][0]; v[7] += w * g[p][1]; v[8] += w * g[p][2];
+          const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
+          const float ey = e * dy;
+          sey[p >> 2] += ey; v[4] += ey * dy; se[p >> 2] += e;
+        }
+        const float m0 = se[0] * dxc[0], m1 = se[1] * dxc[1];
+        v[0] = m0 + m1;
+        v[1] = sey[0] + sey[1];
+        v[2] = m0 * dxc[0] + m1 * dxc[1];
+        v[3] = sey[0] * dxc[0] + sey[1] * dxc[1];
+        v[5] = se[0] + se[1];
+      }
+      const float sum = rs.reduce(v);
+      if (rs.slot >= 0) s_acc[k][rs.slot] = sum;
+    }
+    __syncwarp();
+    if ((int)lane < cnt) {
+      const float* a9 = s_acc[lane];
+      float4* dst = g2d + 3 * (size_t)s_id[lane];
+      red_add_v4(dst, make_float4(a9[0], a9[1], a9[2], a9[3]));
+      red_add_v4(dst + 1, make_float4(a9[4], a9[5], a9[6], a9[7]));
+      atomicAdd(&dst[2].x, a9[8]);
+    }
+    __syncwarp();
+    ptr = k0;
+  }
+}
+
 // --------------------------------------------- backward: preprocess part ----
 // Per Gaussian, over V views: each view's 2D moments → ∂L/∂(u, v, A, B, C, o,
 // rgb) → chained through Eqs. 5-7 and the SH colour.  The parameters are read
@@ -1024,6 +1264,20 @@ AcceptLists carve_accept(void* base, int ntiles, int64_t capacity) {
   return a;
 }
 
+// list path kernel shape: 1 = one warp per tile (TW), 0 = two half-tile warps (default)
+static bool tile_warp() {
+  static const bool v = [] {
+    const char* e = getenv("DASS_TILE_WARP");
+    return e ? atoi(e) != 0 : false;
+  }();
+  return v;
+}
+#ifndef TW_FWD_MINB
+#define TW_FWD_MINB 20
+#endif
+#ifndef TW_BWD_MINB
+#define TW_BWD_MINB 20
+#endif
 static int fwd_ppt() { static const int p = ppt_from_env("DASS_FWD_PPT", 4); return p; }
 static int bwd_ppt() { static const int p = ppt_from_env("DASS_BWD_PPT", 4); return p; }
 static int bwd_minb() {
@@ -1046,6 +1300,12 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
   const int ntiles = cam.tiles_x * cam.tiles_y;
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(accept, ntiles, capacity);
+    if (tile_warp()) {
+      render_fwd_tw_kernel<TW_FWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
+                                                           box, bg, out_img, out_T, out_last, acc);
+      launch_counted();
+      return cudaGetLastError();
+    }
     static const int rpw = [] {
       const char* e = getenv("DASS_FWD_RPW");
       return e ? atoi(e) : 16;
@@ -1113,6 +1373,12 @@ cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* r
   const int ntiles = cam.tiles_x * cam.tiles_y;
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(const_cast<void*>(accept), ntiles, capacity);
+    if (tile_warp()) {
+      render_bwd_tw_kernel<TW_BWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg,
+                                                           out_T, dL_dimg, acc, g2d);
+      launch_counted();
+      return cudaGetLastError();
+    }
     static const int lminb = [] {
       const char* e = getenv("DASS_BWDL_MINB");
       return e ? atoi(e) : 12;   // 80 registers: measured best (16 → 64 regs rematerialises)
