@@ -684,7 +684,7 @@ def run_ours(args):
                        "parallelism": f"view-sharded dp{world}" + (
                            f" ({plan.num_split} views split into tile halves)" if plan.num_split else ""),
                        "l2": "inputs larger than L2 (≈0.5 GB of params, dL/dC and records per step)"},
-            "roofline": {"bound": "alu", "kernel": "render_bwd_list_kernel<4> via dass_render_bwd_raster (accepted units only)",
+            "roofline": {"bound": "alu", "kernel": "render_bwd_tw_kernel via dass_render_bwd_raster (accepted units only)",
                          "achieved": None if achieved is None else round(achieved, 2),
                          "peak": round(peak_tflops, 1), "unit": "TFLOP/s",
                          "frac": None if achieved is None else round(achieved / peak_tflops, 4),

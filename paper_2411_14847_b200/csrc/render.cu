@@ -153,6 +153,7 @@ struct AcceptLists {
   uint32_t* cnt;
   uint32_t* idx;
   uint8_t* bytes;
+  uint32_t* order;   // TW path: launch order of the tiles (longest list first)
 };
 
 // Pixel ownership of a tile CTA (NT = 256/PPT threads, 16×16 pixels).
@@ -716,6 +717,12 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
 }
 
 // ------------------------------------- tile-warp list path (TW, PPT = 8) ----
+#ifndef TW_BWD_CHUNK
+#define TW_BWD_CHUNK 16
+#endif
+#ifndef TW_FWD_BATCH
+#define TW_FWD_BATCH 32
+#endif
 // One warp per 16×16 tile (32-thread CTAs).  Lane l owns the eight pixels
 // (cx + 8·(p>>2), cy + 4·(p&3)), cx = l&7, cy = l>>3: one per 8×4 block of
 // the tile, so a compact footprint covers few blocks p.  Against the two
@@ -738,6 +745,41 @@ struct TileMap {
   }
 };
 
+// Launch order of the TW path: tiles by descending work (one 1024-thread
+// CTA, 64 buckets of 2^SHIFT), so the longest serial tile walks start in the
+// first wave and the short ones fill the tail.  Work = the tile's list length
+// (forward; cnt == nullptr) or its accepted-entry count cnt[tile] (backward).
+__device__ __forceinline__ uint32_t tile_work(const CamParams& cam, const uint2* ranges,
+                                              const uint32_t* cnt, int i) {
+  const int tile = cam.tile0 + i * cam.tstride;
+  if (cnt != nullptr) return cnt[tile];
+  const uint2 r = ranges[tile];
+  return r.y - r.x;
+}
+template <int SHIFT>
+__global__ void __launch_bounds__(1024) tile_order_kernel(const __grid_constant__ CamParams cam,
+                                                          const uint2* __restrict__ ranges,
+                                                          const uint32_t* __restrict__ cnt,
+                                                          uint32_t* __restrict__ order) {
+  constexpr int NB = 64;
+  __shared__ uint32_t hist[NB];
+  const int t = threadIdx.x;
+  if (t < NB) hist[t] = 0u;
+  __syncthreads();
+  for (int i = t; i < cam.tcount; i += blockDim.x)
+    atomicAdd(&hist[NB - 1 - min((uint32_t)(NB - 1), tile_work(cam, ranges, cnt, i) >> SHIFT)], 1u);
+  __syncthreads();
+  if (t == 0) {
+    uint32_t sum = 0;
+    for (int b = 0; b < NB; ++b) { const uint32_t c = hist[b]; hist[b] = sum; sum += c; }
+  }
+  __syncthreads();
+  for (int i = t; i < cam.tcount; i += blockDim.x) {
+    const uint32_t b = NB - 1 - min((uint32_t)(NB - 1), tile_work(cam, ranges, cnt, i) >> SHIFT);
+    order[atomicAdd(&hist[b], 1u)] = (uint32_t)i;
+  }
+}
+
 template <int MINB>
 __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
@@ -746,20 +788,22 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
     const uint2* __restrict__ box, float3 bg, float* __restrict__ out_img,
     float* __restrict__ out_T, uint32_t* __restrict__ out_last, AcceptLists acc) {
   constexpr int PPT = 8;
-  constexpr int BATCH = 64;
+  constexpr int BATCH = TW_FWD_BATCH;
   __shared__ Staged s_st[BATCH];
-  const int tile = cam.tile0 + blockIdx.x * cam.tstride;
+  // (C_r, C_g, C_b, T) of the lane's pixels in shared memory instead of 32
+  // registers (occupancy: 1-warp CTAs); touched once per accepted pixel
+  __shared__ float4 s_px[PPT][32];
+  const int tile = cam.tile0 + (int)acc.order[blockIdx.x] * cam.tstride;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
   const uint32_t lane = threadIdx.x;
   const TileMap pm((int)lane);
   const uint2 range = ranges[tile];
-  float T[PPT], C[PPT][3];
   uint32_t last[PPT];
   uint32_t live = 0;   // bit p: pixel p is inside the image and not terminated
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
-    T[p] = 1.f; C[p][0] = C[p][1] = C[p][2] = 0.f;
+    s_px[p][lane] = make_float4(0.f, 0.f, 0.f, 1.f);
     last[p] = range.x;
     if (tx0 + pm.x(p) < cam.W && ty0 + pm.y(p) < cam.H) live |= 1u << p;
   }
@@ -805,11 +849,13 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
             if (!((ok >> p) & 1u)) continue;
             const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
             if (alpha < ALPHA_MIN) continue;
-            const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
+            float4 px = s_px[p][lane];
+            const float tn = __fmul_rn(px.w, __fsub_rn(1.f, alpha));
             if (tn < T_MIN) { live &= ~(1u << p); continue; }
-            const float w = alpha * T[p];
-            C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
-            T[p] = tn;
+            const float w = alpha * px.w;
+            px.x += c.x * w; px.y += c.y * w; px.z += c.z * w;
+            px.w = tn;
+            s_px[p][lane] = px;
             last[p] = b0 + j + 1;
             accb |= 1u << p;
           }
@@ -829,10 +875,11 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
     const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
     if (X < cam.W && Y < cam.H) {
       const size_t pix = (size_t)Y * cam.W + X, np = (size_t)cam.W * cam.H;
-      out_img[pix] = C[p][0] + T[p] * bg.x;
-      out_img[np + pix] = C[p][1] + T[p] * bg.y;
-      out_img[2 * np + pix] = C[p][2] + T[p] * bg.z;
-      out_T[pix] = T[p];
+      const float4 px = s_px[p][lane];
+      out_img[pix] = px.x + px.w * bg.x;
+      out_img[np + pix] = px.y + px.w * bg.y;
+      out_img[2 * np + pix] = px.z + px.w * bg.z;
+      out_T[pix] = px.w;
       out_last[pix] = last[p];
     }
   }
@@ -846,13 +893,17 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
     const float* __restrict__ out_T, const float* __restrict__ dL_dimg, AcceptLists acc,
     float4* __restrict__ g2d) {
   constexpr int PPT = 8;
-  __shared__ float4 s_a[32];    // (u_rel, v_rel, −, −)
-  __shared__ float4 s_co[32];   // (A, B, C, o)
-  __shared__ float4 s_c[32];    // (r, g, b, −)
-  __shared__ uint4 s_bytes[32][2];
-  __shared__ uint32_t s_id[32];
-  __shared__ float s_acc[32][9];
-  const int tile = cam.tile0 + blockIdx.x * cam.tstride;
+  constexpr int CH = TW_BWD_CHUNK;   // entries staged per chunk
+  __shared__ float4 s_a[CH];    // (u_rel, v_rel, −, −)
+  __shared__ float4 s_co[CH];   // (A, B, C, o)
+  __shared__ float4 s_c[CH];    // (r, g, b, −)
+  __shared__ uint4 s_bytes[CH][2];
+  __shared__ uint32_t s_id[CH];
+  __shared__ float s_acc[CH][9];
+  // dL/dC of the lane's pixels: read once per accepted pixel from shared
+  // memory instead of pinning 24 registers (occupancy: 1-warp CTAs)
+  __shared__ float4 s_g[PPT][32];
+  const int tile = cam.tile0 + (int)acc.order[blockIdx.x] * cam.tstride;
   const uint32_t n = acc.cnt[tile];
   if (n == 0) return;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
@@ -862,27 +913,27 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
   const uint2 range = ranges[tile];
   LaneRS rs;
   rs.init();
-  float T[PPT], gR[PPT], g[PPT][3];
+  float T[PPT], gR[PPT];
   const size_t np = (size_t)cam.W * cam.H;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
+    float4 gg = make_float4(0.f, 0.f, 0.f, 0.f);
+    T[p] = 1.f;
     if (X < cam.W && Y < cam.H) {
       const size_t pix = (size_t)Y * cam.W + X;
       T[p] = out_T[pix];
-      g[p][0] = dL_dimg[pix]; g[p][1] = dL_dimg[np + pix]; g[p][2] = dL_dimg[2 * np + pix];
-    } else {
-      T[p] = 1.f;
-      g[p][0] = g[p][1] = g[p][2] = 0.f;
+      gg = make_float4(dL_dimg[pix], dL_dimg[np + pix], dL_dimg[2 * np + pix], 0.f);
     }
-    gR[p] = T[p] * (g[p][0] * bg.x + g[p][1] * bg.y + g[p][2] * bg.z);
+    s_g[p][lane] = gg;
+    gR[p] = T[p] * (gg.x * bg.x + gg.y * bg.y + gg.z * bg.z);
   }
   const float fx0 = (float)pm.x(0), fx1 = (float)pm.x(4);
   float fy[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) fy[r] = (float)pm.y(r);
   for (int ptr = (int)n; ptr > 0;) {
-    const int k0 = ptr > 32 ? ptr - 32 : 0;
+    const int k0 = ptr > CH ? ptr - CH : 0;
     const int cnt = ptr - k0;
     if ((int)lane < cnt) {
       const size_t e = (size_t)range.x + k0 + lane;
@@ -919,15 +970,16 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
           if (!((bits >> p) & 1u)) continue;
           const float dy = a.y - fy[p & 3];
           const float G = splat_exp(splat_power(ct[p >> 2], dy));
+          const float4 gp = s_g[p][lane];
           const float oG = __fmul_rn(co.w, G);
           const float alpha = fminf(ALPHA_MAX, oG);
           const float inv = rcp_approx(1.f - alpha);
           T[p] *= inv;                        // transmittance before this entry
           const float w = alpha * T[p];
-          const float gc = g[p][0] * c.x + g[p][1] * c.y + g[p][2] * c.z;
+          const float gc = gp.x * c.x + gp.y * c.y + gp.z * c.z;
           const float dLda = T[p] * gc - inv * gR[p];
           gR[p] += gc * w;                    // g·(S + T_final·bg), S = suffix colour
-          v[6] += w * g[p][0]; v[7] += w * g[p][1]; v[8] += w * g[p][2];
+          v[6] += w * gp.x; v[7] += w * gp.y; v[8] += w * gp.z;
           const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
           const float ey = e * dy;
           sey[p >> 2] += ey; v[4] += ey * dy; se[p >> 2] += e;
@@ -1250,7 +1302,8 @@ static int ppt_from_env(const char* name, int dflt) {
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 size_t accept_bytes(int ntiles, int64_t capacity) {
   const size_t c = (size_t)(capacity > 0 ? capacity : 1);
-  return al(sizeof(uint32_t) * 2 * (size_t)ntiles) + al(sizeof(uint32_t) * 2 * c) + al(32 * 2 * c);
+  return al(sizeof(uint32_t) * 2 * (size_t)ntiles) + al(sizeof(uint32_t) * 2 * c) + al(32 * 2 * c) +
+         al(sizeof(uint32_t) * (size_t)ntiles);
 }
 AcceptLists carve_accept(void* base, int ntiles, int64_t capacity) {
   const size_t c = (size_t)(capacity > 0 ? capacity : 1);
@@ -1261,22 +1314,24 @@ AcceptLists carve_accept(void* base, int ntiles, int64_t capacity) {
   a.idx = (uint32_t*)p;
   p += al(sizeof(uint32_t) * 2 * c);
   a.bytes = (uint8_t*)p;
+  p += al(32 * 2 * c);
+  a.order = (uint32_t*)p;
   return a;
 }
 
-// list path kernel shape: 1 = one warp per tile (TW), 0 = two half-tile warps (default)
+// list path kernel shape: 1 = one warp per tile (TW, default), 0 = two half-tile warps
 static bool tile_warp() {
   static const bool v = [] {
     const char* e = getenv("DASS_TILE_WARP");
-    return e ? atoi(e) != 0 : false;
+    return e ? atoi(e) != 0 : true;
   }();
   return v;
 }
 #ifndef TW_FWD_MINB
-#define TW_FWD_MINB 20
+#define TW_FWD_MINB 32
 #endif
 #ifndef TW_BWD_MINB
-#define TW_BWD_MINB 20
+#define TW_BWD_MINB 32
 #endif
 static int fwd_ppt() { static const int p = ppt_from_env("DASS_FWD_PPT", 4); return p; }
 static int bwd_ppt() { static const int p = ppt_from_env("DASS_BWD_PPT", 4); return p; }
@@ -1301,6 +1356,8 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(accept, ntiles, capacity);
     if (tile_warp()) {
+      tile_order_kernel<5><<<1, 1024, 0, s>>>(cam, ranges, nullptr, acc.order);
+      launch_counted();
       render_fwd_tw_kernel<TW_FWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
                                                            box, bg, out_img, out_T, out_last, acc);
       launch_counted();
@@ -1326,7 +1383,7 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
     launch_counted();
     return cudaGetLastError();
   }
-  const AcceptLists none{nullptr, nullptr, nullptr};
+  const AcceptLists none{nullptr, nullptr, nullptr, nullptr};
 #define FWD(P)                                                                                    \
   render_fwd_kernel<P, false><<<cam.tcount, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
                                                          box, bg, out_img, out_T, out_last, none)
@@ -1374,6 +1431,8 @@ cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* r
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(const_cast<void*>(accept), ntiles, capacity);
     if (tile_warp()) {
+      tile_order_kernel<4><<<1, 1024, 0, s>>>(cam, ranges, acc.cnt, acc.order);
+      launch_counted();
       render_bwd_tw_kernel<TW_BWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg,
                                                            out_T, dL_dimg, acc, g2d);
       launch_counted();
