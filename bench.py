@@ -662,11 +662,9 @@ def run_ours(args):
         pk, pk_kind = peaks()
         f_max = pk.get("sm_max_mhz", 1965.0) * 1e6
         peak_tflops = SM_COUNT * FP32_LANES * 2 * f_max / 1e12
-        # dominant op: render_bwd (raster kernel + fp32 preprocess), algorithmic
-        # flops counted for the raster part only (conservative)
-        flops = sum(a * FLOP_BWD_ACCEPTED for a in stats["accepted"])
-        bwd_ms = ops.get("render_bwd_raster", float("nan"))
-        achieved = flops / (bwd_ms / 1e3) / 1e12 if bwd_ms == bwd_ms and bwd_ms > 0 else None
+        # the dominant kernel of the step (the larger of the two raster kernels in the
+        # isolated per-op pass) against the FP32 roof, algorithmic flops only
+        dom = dominant_roofline(ops, stats, f_max, peak_tflops)
         views_s = job_views / (ms_step / 1e3)
         result = {
             "metric": METRIC, "value": round(views_s, 3), "unit": "views/s",
@@ -684,22 +682,7 @@ def run_ours(args):
                        "parallelism": f"view-sharded dp{world}" + (
                            f" ({plan.num_split} views split into tile halves)" if plan.num_split else ""),
                        "l2": "inputs larger than L2 (≈0.5 GB of params, dL/dC and records per step)"},
-            "roofline": {"bound": "alu", "kernel": "render_bwd_tw_kernel via dass_render_bwd_raster (accepted units only)",
-                         "achieved": None if achieved is None else round(achieved, 2),
-                         "peak": round(peak_tflops, 1), "unit": "TFLOP/s",
-                         "frac": None if achieved is None else round(achieved / peak_tflops, 4),
-                         "traffic": profiled_traffic("render_bwd"),
-                         "traffic_source": "profiles/r01_ncu_render_bwd.txt (ncu --set full, dram read+write per launch = one view)",
-                         "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz ({pk_kind} clock)",
-                         "units_per_step": {"accepted": sum(stats["accepted"]), "P_bwd": sum(stats["P_bwd"])},
-                         "flop_per_unit": {"accepted": FLOP_BWD_ACCEPTED},
-                         "survey_unit_view": survey_unit_view(stats, bwd_ms, f_max),
-                         "timing": "isolated launches: one sequential pass over the step's kernels "
-                                   "(CUDA events on the launching stream), since in the timed "
-                                   "graph the per-view kernels of 20 streams overlap",
-                         "share_of_step_kernels": round(ops.get("render_bwd_raster", 0.0) /
-                                                        max(sum(v for k, v in ops.items() if k in STEP_OPS), 1e-9), 4),
-                         "ncu_share_source": "profiles/r01_launches.txt"},
+            "roofline": dom,
             "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
             "hot_path_roofline": hot_path_roofline(ops, stats, pk, peak_tflops, n, len(my_cams), deg),
             "rows_roofline": rows_roofline(ops, densify, allst, pk, peak_tflops, n, W, H,
@@ -803,21 +786,62 @@ BYTES_LOSS_PER_PX = 3 * 4 * 3                                           # img, g
 DEFORM_IN = {"dyn": 32, "st": 16}                                       # L·F (N3DV profile)
 
 
-def survey_unit_view(stats, bwd_ms, f_max):
-    """The backward against SURVEY §8(d)'s own work unit: every in-box (pixel, entry) up
-    to the pixel's last contributor (P_bwd), ≈55 FP32-pipe instructions each, against the
-    instruction-issue peak (148 SMs × 128 lanes × f).  A 3DGS-style backward evaluates all
-    of them; the acceptance lists skip the rejected ones, so this is an equivalent-work
-    rate, not the algorithmic one the `frac` above reports."""
-    if not stats.get("P_bwd") or not bwd_ms or bwd_ms != bwd_ms:
+FLOP_FWD_ACCEPTED = 15   # blend of an accepted (pixel, entry): 1 − α, T·(1 − α), w, 3 colour FMAs
+FLOP_FWD_INBOX = 8       # α of an in-box (pixel, entry): dx, dy, power, exp, o·G, compare
+RASTER_KERNELS = {
+    "render_fwd": ("render_fwd_tw_kernel via dass_render_fwd (lists)", "P_fwd", 20,
+                   f"{FLOP_FWD_ACCEPTED} flop per accepted (pixel, entry) + {FLOP_FWD_INBOX} per "
+                   "in-box (pixel, entry) up to termination"),
+    "render_bwd_raster": ("render_bwd_tw_kernel via dass_render_bwd_raster (accepted units only)",
+                          "P_bwd", 55, f"{FLOP_BWD_ACCEPTED} flop per accepted (pixel, entry)"),
+}
+
+
+def dominant_roofline(ops, stats, f_max, peak_tflops):
+    """Roofline object of the step's dominant kernel: whichever raster kernel (forward
+    or backward) takes longer in the isolated per-op pass.  achieved = algorithmic
+    flops of the step's launches / their summed isolated durations."""
+    cand = {k: ops.get(k, float("nan")) for k in RASTER_KERNELS}
+    cand = {k: v for k, v in cand.items() if v == v and v > 0}
+    if not cand or not stats.get("accepted"):
         return None
-    units = float(sum(stats["P_bwd"]))
+    key = max(cand, key=cand.get)
+    ms = cand[key]
+    name, p_key, instr, unit = RASTER_KERNELS[key]
     acc = float(sum(stats["accepted"]))
-    peak = SM_COUNT * FP32_LANES * f_max / 1e12
-    rate = units * 55 / (bwd_ms / 1e3) / 1e12
-    return {"units": int(units), "instr_per_unit": 55, "achieved_tinstr_s": round(rate, 2),
-            "peak_tinstr_s": round(peak, 1), "frac": round(rate / peak, 4),
-            "evaluated_by_this_kernel": round(acc / units, 4)}
+    if key == "render_fwd":
+        flops = FLOP_FWD_ACCEPTED * acc + FLOP_FWD_INBOX * float(sum(stats["P_fwd"]))
+        per_unit = {"accepted": FLOP_FWD_ACCEPTED, "P_fwd": FLOP_FWD_INBOX}
+    else:
+        flops = FLOP_BWD_ACCEPTED * acc
+        per_unit = {"accepted": FLOP_BWD_ACCEPTED}
+    achieved = flops / (ms / 1e3) / 1e12
+    units = float(sum(stats[p_key]))
+    peak_i = SM_COUNT * FP32_LANES * f_max / 1e12
+    rate = units * instr / (ms / 1e3) / 1e12
+    prof = "render_fwd" if key == "render_fwd" else "render_bwd"
+    return {"bound": "alu", "kernel": name, "achieved": round(achieved, 2),
+            "peak": round(peak_tflops, 1), "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4),
+            "traffic": profiled_traffic(prof),
+            "traffic_source": f"profiles/r01_ncu_{prof}.txt (ncu --set full, dram read+write per "
+                              "launch = one view)",
+            "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz",
+            "flop_unit": unit,
+            "units_per_step": {"accepted": int(acc), p_key: int(units)},
+            "flop_per_unit": per_unit,
+            "survey_unit_view": {"units": int(units), "instr_per_unit": instr,
+                                 "achieved_tinstr_s": round(rate, 2), "peak_tinstr_s": round(peak_i, 1),
+                                 "frac": round(rate / peak_i, 4),
+                                 "evaluated_by_this_kernel": round(acc / units, 4) if key != "render_fwd" else None,
+                                 "what": "SURVEY §8(d)'s unit (every in-box (pixel, entry)) × its FP32-pipe "
+                                         "instruction estimate against the issue peak: an equivalent-work "
+                                         "rate, not the algorithmic one in frac"},
+            "timing": "isolated launches: one sequential pass over the step's kernels (CUDA events on "
+                      "the launching stream), since in the timed graph the per-view kernels of 20 "
+                      "streams overlap",
+            "share_of_step_kernels": round(ms / max(sum(v for k, v in ops.items() if k in STEP_OPS), 1e-9), 4),
+            "ncu_share_source": "profiles/r01_launches.txt"}
+
 
 
 def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg):
@@ -847,7 +871,7 @@ def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg):
     # preprocess: 88 B of records + moments per Gaussian-view, parameters and gradients once
     hb("render_bwd_preprocess_views", n * views * 88 + n * 3 * (48 + 16 * k4))
     t = ops["render_fwd"] / 1e3
-    fl = 15.0 * acc + 8.0 * pfwd            # accepted blend + every in-box α evaluation
+    fl = FLOP_FWD_ACCEPTED * acc + FLOP_FWD_INBOX * pfwd   # accepted blend + every in-box α evaluation
     out["render_fwd"] = {"bound": "alu", "flop": int(fl), "achieved_tflops": round(fl / t / 1e12, 2),
                          "peak_tflops": round(peak_fp32, 1), "frac": round(fl / t / 1e12 / peak_fp32, 4),
                          "unit": "15 flop per accepted (pixel, entry) + 8 per in-box evaluation"}

@@ -30,3 +30,18 @@ def test_hot_path_roofline():
     # the backward's flop count is 42 per accepted unit
     assert out["render_bwd_raster"]["flop"] == 42 * 65_000_000 * 20
     assert bench.hot_path_roofline({}, stats, {}, 74.4, 1, 1, 0) is None
+
+
+def test_dominant_roofline_picks_the_slower_raster_kernel():
+    stats = {"accepted": [65_000_000] * 20, "P_fwd": [215_000_000] * 20, "P_bwd": [210_000_000] * 20}
+    f = 1965e6
+    peak = bench.SM_COUNT * bench.FP32_LANES * 2 * f / 1e12
+    fwd = bench.dominant_roofline({"render_fwd": 7.9, "render_bwd_raster": 6.7}, stats, f, peak)
+    assert fwd["kernel"].startswith("render_fwd")
+    fl = (bench.FLOP_FWD_ACCEPTED * 65e6 + bench.FLOP_FWD_INBOX * 215e6) * 20
+    assert abs(fwd["achieved"] - fl / 7.9e-3 / 1e12) < 0.01
+    assert abs(fwd["frac"] - fwd["achieved"] / peak) < 1e-3
+    bwd = bench.dominant_roofline({"render_fwd": 6.0, "render_bwd_raster": 6.7}, stats, f, peak)
+    assert bwd["kernel"].startswith("render_bwd")
+    assert abs(bwd["achieved"] - bench.FLOP_BWD_ACCEPTED * 65e6 * 20 / 6.7e-3 / 1e12) < 0.01
+    assert bench.dominant_roofline({}, stats, f, peak) is None
