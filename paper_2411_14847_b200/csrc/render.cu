@@ -739,8 +739,10 @@ struct TileMap {
   // bit p set iff pixel p's column and row bits are both set in m
   __device__ __forceinline__ uint32_t cand(uint32_t m) const {
     const uint32_t c = ((m >> cx) & 1u) | ((m >> (cx + 4)) & 16u);      // columns cx, cx+8 → bits 0, 4
-    const uint32_t r = m >> (16 + cy);                                  // rows cy+4i at bits 4i
-    const uint32_t r4 = (r & 1u) | ((r >> 3) & 2u) | ((r >> 6) & 4u) | ((r >> 9) & 8u);
+    const uint32_t r = (m >> (16 + cy)) & 0x1111u;                     // rows cy+4i at bits 4i
+    // gather bits 0, 4, 8, 12 into 9..12: the partial products of ×0x249 sit at
+    // 16 distinct positions, so there are no carries
+    const uint32_t r4 = ((r * 0x249u) >> 9) & 15u;
     return c * r4;   // outer product: bit (p&3) + 4·(p>>2)
   }
 };
@@ -840,7 +842,7 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
         }
 #pragma unroll
         for (int p = 0; p < PPT; ++p)
-          ok |= (!(pw[p] > 0.f) && !(pw[p] < a.z)) ? (1u << p) : 0u;
+          ok |= (uint32_t)(pw[p] >= a.z) << p;   // the power > 0 guard is in the pixel block
         ok &= cand;
         if (ok) {
           const float4 c = st.c;
@@ -848,7 +850,7 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
           for (int p = 0; p < PPT; ++p) {
             if (!((ok >> p) & 1u)) continue;
             const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
-            if (alpha < ALPHA_MIN) continue;
+            if (alpha < ALPHA_MIN || pw[p] > 0.f) continue;   // A11: skip if power > 0
             float4 px = s_px[p][lane];
             const float tn = __fmul_rn(px.w, __fsub_rn(1.f, alpha));
             if (tn < T_MIN) { live &= ~(1u << p); continue; }
