@@ -203,13 +203,14 @@ def run_ours(args):
             wait_inputs()
         dass.dass_apply_shift(S.base.pos_opa, S.base.rot, S.mu, S.sigma, S.base.dynamic,
                               S.shifted.pos_opa, S.shifted.rot)
-        if my_cams:
-            dass.dass_project_views(my_cams, deg, S.shifted.pos_opa, S.shifted.scale,
-                                    S.shifted.rot, S.shifted.sh, None, records.xy_depth,
-                                    records.conic_opa, records.rgb, records.box, records.tiles)
+        def project(v0, v1):
+            dass.dass_project_views(my_cams[v0:v1], deg, S.shifted.pos_opa, S.shifted.scale,
+                                    S.shifted.rot, S.shifted.sh, None, records.xy_depth[v0:v1],
+                                    records.conic_opa[v0:v1], records.rgb[v0:v1],
+                                    records.box[v0:v1], records.tiles[v0:v1])
         if mvp is not None:
             mvp.uv_out = [None if sidx < 0 else g.uv[sidx] for sidx in plan.split]
-            mvp.run(S.shifted, records, S.dLs, g)
+            mvp.run(S.shifted, records, S.dLs, g, project=project)
         dass.dass_apply_shift_bwd(S.base.rot, S.sigma, S.base.dynamic, g.pos_opa, g.rot,
                                   g.g_mu, g.g_sigma)
 
@@ -339,10 +340,12 @@ def run_ours(args):
             fields.forward(base.pos_opa, mu_f, sigma_f)
             dass.dass_apply_shift(base.pos_opa, base.rot, mu_f, sigma_f, None,
                                   shifted.pos_opa, shifted.rot)
-            dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
-                                    shifted.sh, None, records.xy_depth, records.conic_opa,
-                                    records.rgb, records.box, records.tiles)
-            mvp.run(shifted, records, None, grads, gts=gts)
+            def project(v0, v1):
+                dass.dass_project_views(my_cams[v0:v1], deg, shifted.pos_opa, shifted.scale,
+                                        shifted.rot, shifted.sh, None, records.xy_depth[v0:v1],
+                                        records.conic_opa[v0:v1], records.rgb[v0:v1],
+                                        records.box[v0:v1], records.tiles[v0:v1])
+            mvp.run(shifted, records, None, grads, gts=gts, project=project)
             dass.dass_apply_shift_bwd(base.rot, sigma_f, None, grads.pos_opa, grads.rot,
                                       g_mu, g_sigma)
             fields.backward(base.pos_opa, g_mu, g_sigma)

@@ -169,9 +169,14 @@ class MultiViewPass:
                 raise ValueError("all cameras of a pass must share the image size")
         self.S = max(1, min(streams, self.V))
         self.slots = [Raster(W, H, n, capacity, device) for _ in range(self.S)]
-        self.streams = [torch.cuda.Stream(device=device) for _ in range(self.S)]
+        # DASS_STREAM_PRIO=1: the streams of the first half of the views get the higher
+        # priority, so those views finish first and their preprocess chunk overlaps the rest
+        prio = os.environ.get("DASS_STREAM_PRIO", "0") == "1"
+        self.streams = [torch.cuda.Stream(device=device, priority=-1 if prio and 2 * k < self.S else 0)
+                        for k in range(self.S)]
         self.pre_stream = torch.cuda.Stream(device=device)
         self.pre_chunks = int(os.environ.get("DASS_PRE_CHUNKS", "2"))
+        self.proj_chunks = int(os.environ.get("DASS_PROJ_CHUNKS", "1"))
         # optional hook(v, stream), called on view v's stream right before its backward:
         # an end-to-end caller makes the view wait there for its own ∂L/∂C upload
         self.before_bwd = None
@@ -190,23 +195,40 @@ class MultiViewPass:
         self.losses = torch.zeros(self.V, 3, dtype=torch.float32, device=dev)
 
     def run(self, scene: DeviceScene, records: ViewRecords, dL_dimgs, grads, keep=None, bg=None,
-            gts=None):
+            gts=None, project=None):
         """dL_dimgs: fixed per-view ∂L/∂C, or None with gts (per-view ground truth,
-        requires enable_loss): then ∂L/∂C comes from the fidelity loss."""
+        requires enable_loss): then ∂L/∂C comes from the fidelity loss.
+        project(v0, v1): optional; issues the projection of views [v0, v1) on the
+        current stream.  The pass then projects in DASS_PROJ_CHUNKS chunks and each
+        view waits only for its own chunk, so later chunks project under the first
+        chunks' raster kernels."""
         torch = _torch()
         main = torch.cuda.current_stream()
-        for s in self.streams:
-            s.wait_stream(main)
+        V = self.V
+        pc = max(1, min(self.proj_chunks, V)) if project is not None else 1
+        pbounds = [round(c * V / pc) for c in range(pc + 1)]
+        ready = []   # per projection chunk: the event the chunk's views wait on
+        for c in range(pc):
+            if project is not None:
+                project(pbounds[c], pbounds[c + 1])
+            e = torch.cuda.Event()
+            e.record(main)
+            ready.append(e)
+        chunk_of = [max(c for c in range(pc) if pbounds[c] <= v) for v in range(V)]
         # preprocess in chunks: chunk c's views are chained to parameter gradients on a side
         # stream as soon as they are rasterised (HBM-bound work under the ALU-bound raster
         # kernels of later views); only the last chunk runs after the final raster kernel.
         # Chunks run in order on ONE stream: each += into the same gradient buffers.
-        nchunk = max(1, min(self.pre_chunks, self.V // self.S)) if self.V >= 2 * self.S else 1
-        bounds = [round(c * self.V / nchunk) for c in range(nchunk + 1)]
+        # (measured: with one stream per view the raster kernels already fill the GPU
+        # and chunking the preprocess or the projection only adds launches, +0.3-1.8%)
+        nchunk = max(1, min(self.pre_chunks, V // self.S)) if V >= 2 * self.S else 1
+        bounds = [round(c * V / nchunk) for c in range(nchunk + 1)]
         ends = {bounds[c + 1] - 1: c for c in range(nchunk - 1)}
+        done = [None] * V
         for v, cam in enumerate(self.cams):
             k = v % self.S
             ras, st = self.slots[k], self.streams[k]
+            st.wait_event(ready[chunk_of[v]])
             with torch.cuda.stream(st):
                 rec = records.view(v)
                 xy, co, rgb, box, tiles = rec
@@ -222,18 +244,20 @@ class MultiViewPass:
                 dass.dass_render_bwd_raster(cam, self.n, ras.ranges, ras.sorted_ids, xy, co, rgb,
                                             box, bg, ras.T, ras.last, dL, self.g2d[v],
                                             ras.accept, ras.capacity, tiles=self.tiles[v])
+                done[v] = torch.cuda.Event()
+                done[v].record(st)
             if v in ends:
                 c = ends[v]
                 self.pre_stream.wait_stream(main)
-                for s in self.streams:
-                    self.pre_stream.wait_stream(s)
+                for u in range(bounds[c], bounds[c + 1]):
+                    self.pre_stream.wait_event(done[u])
                 with torch.cuda.stream(self.pre_stream):
                     self._preprocess(scene, records, grads, keep, bounds[c], bounds[c + 1])
         for s in self.streams:
             main.wait_stream(s)
         if nchunk > 1:
             main.wait_stream(self.pre_stream)
-        self._preprocess(scene, records, grads, keep, bounds[nchunk - 1], self.V)
+        self._preprocess(scene, records, grads, keep, bounds[nchunk - 1], V)
 
     def _preprocess(self, scene, records, grads, keep, v0, v1):
         dass.dass_render_bwd_preprocess_views(
