@@ -36,6 +36,9 @@ constexpr unsigned long long SFLAG_AGG = 1ull << 62;
 constexpr unsigned long long SFLAG_INC = 2ull << 62;
 constexpr unsigned long long SVAL_MASK = (1ull << 62) - 1ull;
 constexpr int NUM_COUNTERS = 16;
+#ifndef SPIN_NS
+#define SPIN_NS 64
+#endif
 
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
@@ -137,12 +140,15 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
   const int warp = t >> 5;
   const uint32_t lane = lane_id();
   const int n = n_static >= 0 ? n_static : (n_dev[1] ? 0 : (int)n_dev[0]);
+  // blocks past the end (the pair passes launch for the capacity, K is on the
+  // device) leave right after their claim, before touching shared memory
   if (t == 0) s_blk = atomicAdd(counter, 1u);
-  for (int k = t; k < (SORT_THREADS / 32) * RADIX; k += SORT_THREADS) (&s_whist[0][0])[k] = 0u;
   __syncthreads();
   const uint32_t blk = s_blk;
   const long long base = (long long)blk * SORT_ITEMS;
   if (base >= n) return;
+  for (int k = t; k < (SORT_THREADS / 32) * RADIX; k += SORT_THREADS) (&s_whist[0][0])[k] = 0u;
+  __syncthreads();
 
   uint64_t keys[SORT_IPT];
   uint32_t digit[SORT_IPT];
@@ -203,7 +209,10 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     while (true) {
       const uint32_t v = ld_relaxed(status + (size_t)j * RADIX + t);
       const uint32_t f = v & ~VAL_MASK;
-      if (f == 0u) continue;  // predecessor not published yet: spin
+      if (f == 0u) {  // predecessor not published yet: back off, do not burn issue slots
+        __nanosleep(SPIN_NS);
+        continue;
+      }
       excl += v & VAL_MASK;
       if (f == FLAG_INC) break;
       --j;
@@ -273,7 +282,10 @@ __global__ void __launch_bounds__(256) tile_scan_kernel(int n, const uint64_t* _
       while (true) {
         const unsigned long long v = ld_relaxed64(status + j);
         const unsigned long long f = v & ~SVAL_MASK;
-        if (f == 0ull) continue;
+        if (f == 0ull) {
+          __nanosleep(SPIN_NS);
+          continue;
+        }
         excl += v & SVAL_MASK;
         if (f == SFLAG_INC) break;
         --j;
