@@ -231,6 +231,31 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth,
                   int64_t* num_pairs_host, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * dass_bin_sort_views — dass_bin_sort for V views of one timestep at once
+ * (a3-a5 batched over the views of P:74; A03, A04).  All cameras share W×H
+ * (the tile grid T); the records are the [V][N] arrays of
+ * dass_project_views.  Per view v the outputs equal, bit for bit, those of
+ * dass_bin_sort on view v alone (graph mode): sorted_ids[v·view_capacity + k]
+ * for k < K_v, tile_ranges[(v·T + t)·2 + {0,1}] view-relative [s, e) (empty
+ * tiles [0, 0)), num_pairs_dev[2v] = K_v, num_pairs_dev[2v+1] = 1 if K_v >
+ * view_capacity (that view's ranges then stay empty; if the batch total
+ * exceeds V·view_capacity every view is flagged).  One depth presort of the
+ * V·N (view, Gaussian) keys, one emission and one sort of all pairs on the
+ * combined index v·T + tile: a few large kernels instead of V latency-bound
+ * chains.  No host synchronisation.
+ *  INVALID_ARG: V ∉ [1, 64], cameras of different sizes, n < 0, view_capacity
+ *   ∉ [0, 2^30 / V), a null required pointer, workspace too small.
+ * ------------------------------------------------------------------------- */
+int dass_bin_sort_views_workspace(int32_t num_views, int32_t n,
+                                  int64_t view_capacity, size_t* bytes);
+int dass_bin_sort_views(const dass_camera* cams, int32_t num_views, int32_t n,
+                        const float* xy_depth, const uint32_t* box,
+                        const uint32_t* tiles_touched, void* ws, size_t ws_bytes,
+                        int64_t view_capacity, uint32_t* sorted_ids,
+                        uint32_t* tile_ranges, uint32_t* num_pairs_dev,
+                        void* stream);
+
+/* ---------------------------------------------------------------------------
  * dass_render_fwd — front-to-back compositing (Eq. 8; A01, A05,
  * A11-A13).  For pixel (X, Y), over the tile's sorted list, skipping entries
  * whose box does not contain the pixel:
@@ -584,6 +609,15 @@ int dass_render_stats(const dass_camera* cam, const uint32_t* tile_ranges,
                       const float* conic_opa, const uint32_t* box,
                       const float* out_T, const uint32_t* out_last,
                       uint64_t* counters, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * dass_timestamp — diagnostic: one single-thread kernel on `stream` writes the
+ * GPU global timer (ns) to stamps[slot] when it runs, so a captured CUDA graph
+ * can be given a per-stream timeline (tools/timeline.py).  stamps: uint64
+ * device array owned by the caller.  INVALID_ARG if stamps is null or slot < 0.
+ * Not on the hot path.
+ * ------------------------------------------------------------------------- */
+int dass_timestamp(uint64_t* stamps, int32_t slot, void* stream);
 
 #ifdef __cplusplus
 }

@@ -233,6 +233,47 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, cons
   return DASS_OK;
 }
 
+int dass_bin_sort_views_workspace(int32_t num_views, int32_t n, int64_t view_capacity,
+                                  size_t* bytes) {
+  if (!bytes) return fail(DASS_ERR_INVALID_ARG, "bytes is null%s");
+  if (num_views < 1 || num_views > 64 || n < 0 || view_capacity < 0 ||
+      view_capacity >= (int64_t(1) << 30) / num_views)
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views_workspace: bad sizes%s");
+  *bytes = binsort_views_workspace(num_views, n, view_capacity);
+  return DASS_OK;
+}
+
+int dass_bin_sort_views(const dass_camera* cams, int32_t num_views, int32_t n,
+                        const float* xy_depth, const uint32_t* box, const uint32_t* tiles_touched,
+                        void* ws, size_t ws_bytes, int64_t view_capacity, uint32_t* sorted_ids,
+                        uint32_t* tile_ranges, uint32_t* num_pairs_dev, void* stream) {
+  if (!cams) return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: cams is null%s");
+  if (num_views < 1 || num_views > 64)
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: num_views must be in [1, 64]%s");
+  for (int v = 0; v < num_views; ++v) {
+    int st = check_camera(&cams[v]);
+    if (st) return st;
+    if (cams[v].width != cams[0].width || cams[v].height != cams[0].height)
+      return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: cameras differ in size%s");
+  }
+  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (view_capacity < 0 || view_capacity >= (int64_t(1) << 30) / num_views)
+    return fail(DASS_ERR_INVALID_ARG, "view_capacity must be in [0, 2^30 / V)%s");
+  if (!sorted_ids || !tile_ranges || !num_pairs_dev)
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: null required pointer%s");
+  if (n > 0 && (!xy_depth || !box || !tiles_touched))
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: null record pointer%s");
+  const size_t need = binsort_views_workspace(num_views, n, view_capacity);
+  if (ws_bytes < need || (need > 0 && ws == nullptr))
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: workspace too small%s");
+  CamParams cp = to_params(&cams[0]);
+  return cuda_status(launch_binsort_views(cp, num_views, n, (const float4*)xy_depth,
+                                          (const uint2*)box, tiles_touched, ws, view_capacity,
+                                          sorted_ids, (uint2*)tile_ranges, num_pairs_dev,
+                                          (cudaStream_t)stream),
+                     "dass_bin_sort_views");
+}
+
 int dass_render_accept_workspace(int32_t num_tiles, int64_t pair_capacity, size_t* bytes) {
   if (!bytes || num_tiles < 1 || pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30))
     return fail(DASS_ERR_INVALID_ARG, "need num_tiles >= 1 and 0 <= pair_capacity < 2^30%s");
@@ -683,6 +724,11 @@ int dass_render_stats(const dass_camera* cam, const uint32_t* tile_ranges,
                                          (const uint2*)box, out_T, out_last,
                                          (unsigned long long*)counters, (cudaStream_t)stream),
                      "dass_render_stats");
+}
+
+int dass_timestamp(uint64_t* stamps, int32_t slot, void* stream) {
+  if (!stamps || slot < 0) return fail(DASS_ERR_INVALID_ARG, "dass_timestamp: null stamps or slot < 0%s");
+  return cuda_status(launch_timestamp(stamps + slot, (cudaStream_t)stream), "dass_timestamp");
 }
 
 }  // extern "C"

@@ -35,7 +35,8 @@ constexpr uint32_t VAL_MASK = (1u << 30) - 1u;
 constexpr unsigned long long SFLAG_AGG = 1ull << 62;
 constexpr unsigned long long SFLAG_INC = 2ull << 62;
 constexpr unsigned long long SVAL_MASK = (1ull << 62) - 1ull;
-constexpr int NUM_COUNTERS = 16;
+constexpr int NUM_COUNTERS = 16;   // 0-3 presort, 4 scan, 5-8 pair passes, 12-13 batch K
+constexpr int MAX_SORT_VIEWS = 64;
 #ifndef SPIN_NS
 #define SPIN_NS 64
 #endif
@@ -128,13 +129,17 @@ __global__ void __launch_bounds__(256) presort_init_kernel(int n, const float4* 
 }
 
 // One onesweep LSD pass over bits [shift, shift+8) of 64-bit keys.
+template <typename KT = uint64_t>
 __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
-    const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int n_static,
+    const KT* __restrict__ in, KT* __restrict__ out, int n_static,
     const uint32_t* __restrict__ n_dev, const uint32_t* __restrict__ hist, uint32_t* status,
     uint32_t* counter, int shift) {
   __shared__ uint32_t s_whist[SORT_THREADS / 32][RADIX];
   __shared__ uint32_t s_gbase[RADIX];
+  __shared__ uint32_t s_bstart[RADIX];
   __shared__ uint32_t s_wsum[SORT_THREADS / 32];
+  __shared__ uint32_t s_bsum[SORT_THREADS / 32];
+  __shared__ KT s_keys[SORT_ITEMS];
   __shared__ uint32_t s_blk;
   const int t = threadIdx.x;
   const int warp = t >> 5;
@@ -150,7 +155,7 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
   for (int k = t; k < (SORT_THREADS / 32) * RADIX; k += SORT_THREADS) (&s_whist[0][0])[k] = 0u;
   __syncthreads();
 
-  uint64_t keys[SORT_IPT];
+  KT keys[SORT_IPT];
   uint32_t digit[SORT_IPT];
   uint32_t rank[SORT_IPT];
   const long long wbase = base + warp * (SORT_IPT * 32);
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
       keys[j] = in[idx];
       digit[j] = (uint32_t)(keys[j] >> shift) & 255u;
     } else {
-      keys[j] = 0ull;
+      keys[j] = 0;
       digit[j] = 256u;  // invalid: ranks only among invalid lanes, never scattered
     }
   }
@@ -189,15 +194,17 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     s_whist[w][t] = count;
     count += c;
   }
-  // exclusive scan of the global histogram over digits (digit = t)
+  // exclusive scan of the global histogram over digits (digit = t), and of the
+  // block's digit counts (the block-local digit-sorted order for the staging)
   const uint32_t hv = hist[t];
-  uint32_t incl = hv;
+  uint32_t incl = hv, bincl = count;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if ((int)lane >= o) incl += y;
+    const uint32_t z = __shfl_up_sync(0xffffffffu, bincl, o);
+    if ((int)lane >= o) { incl += y; bincl += z; }
   }
-  if (lane == 31) s_wsum[warp] = incl;
+  if (lane == 31) { s_wsum[warp] = incl; s_bsum[warp] = bincl; }
   // decoupled look-back for digit t
   uint32_t excl = 0u;
   uint32_t* my = status + (size_t)blk * RADIX + t;
@@ -220,14 +227,25 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     st_relaxed(my, FLAG_INC | (excl + count));
   }
   __syncthreads();
-  uint32_t gofs = incl - hv;
-  for (int w = 0; w < warp; ++w) gofs += s_wsum[w];
-  s_gbase[t] = gofs + excl;
+  uint32_t gofs = incl - hv, bofs = bincl - count;
+  for (int w = 0; w < warp; ++w) { gofs += s_wsum[w]; bofs += s_bsum[w]; }
+  s_bstart[t] = bofs;                     // first block-local slot of digit t
+  s_gbase[t] = gofs + excl - bofs;        // global index = s_gbase[d] + block-local slot
   __syncthreads();
+  // stage the keys in block-local digit order, then write them out in order:
+  // consecutive threads → consecutive slots → runs of one digit are contiguous
+  // in the output (coalesced), instead of one scattered store per key
 #pragma unroll
   for (int j = 0; j < SORT_IPT; ++j) {
     const uint32_t d = digit[j];
-    if (d < 256u) out[s_gbase[d] + s_whist[warp][d] + rank[j]] = keys[j];
+    if (d < 256u) s_keys[s_bstart[d] + s_whist[warp][d] + rank[j]] = keys[j];
+  }
+  __syncthreads();
+  const int valid = (int)min((long long)SORT_ITEMS, (long long)n - base);
+  for (int i = t; i < valid; i += SORT_THREADS) {
+    const KT key = s_keys[i];
+    const uint32_t d = (uint32_t)(key >> shift) & 255u;
+    out[s_gbase[d] + (uint32_t)i] = key;
   }
 }
 
@@ -318,7 +336,8 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
                                                   const uint32_t* __restrict__ num_pairs_dev,
                                                   int tiles_x, int npass, uint64_t* pkeys,
                                                   uint32_t* hist, uint32_t* pstatus,
-                                                  size_t pstatus_stride) {
+                                                  size_t pstatus_stride, int view_n = 0,
+                                                  int view_tiles = 0) {
   __shared__ uint32_t sh[MAX_PASSES - 4][RADIX];
   if (num_pairs_dev[1]) return;  // overflow: every range stays [0,0)
   for (int k = threadIdx.x; k < (MAX_PASSES - 4) * RADIX; k += blockDim.x) (&sh[0][0])[k] = 0u;
@@ -380,7 +399,13 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
         const uint32_t local = j - excl;
         const uint32_t dy = local / ow, dx = local - dy * ow;
         tile = (uint32_t)((oty0 + (int)dy) * tiles_x + otx0 + (int)dx);
-        pkeys[o0 + j] = ((uint64_t)tile << 32) | oid;
+        uint32_t gid = oid;
+        if (view_n > 0) {   // multi-view batch: Gaussian index v·N + i → (v·T + tile, i)
+          const uint32_t v = oid / (uint32_t)view_n;
+          gid = oid - v * (uint32_t)view_n;
+          tile += v * (uint32_t)view_tiles;
+        }
+        pkeys[o0 + j] = ((uint64_t)tile << 32) | gid;
       }
       const uint32_t peers = __match_any_sync(0xffffffffu, tile);
       if (act && lane == (uint32_t)(__ffs(peers) - 1)) {
@@ -416,6 +441,57 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint64_t* __restric
   }
 }
 
+// Multi-view batch: the pairs sorted by (v·T + tile, depth bits, i) → per view v
+// its ids at sorted_ids[v·view_cap + k − off_v], view-relative tile ranges and
+// (K_v, overflow_v).  off_v = first sorted position of view v (binary search on the
+// monotone combined tile index).  A view with K_v > view_cap keeps empty ranges.
+__global__ void __launch_bounds__(256) finalize_views_kernel(const uint64_t* __restrict__ pk,
+                                                            const uint32_t* __restrict__ num_pairs_g,
+                                                            int V, int T, long long view_cap,
+                                                            uint32_t* ids, uint2* ranges,
+                                                            uint32_t* view_pairs) {
+  __shared__ uint32_t s_off[MAX_SORT_VIEWS + 1];
+  const int t = threadIdx.x;
+  if (num_pairs_g[1]) {   // the batch overflowed its total capacity: every view is flagged
+    if (blockIdx.x == 0)
+      for (int v = t; v < V; v += blockDim.x) {
+        view_pairs[2 * v] = num_pairs_g[0];
+        view_pairs[2 * v + 1] = 1u;
+      }
+    return;
+  }
+  const uint32_t K = num_pairs_g[0];
+  for (int v = t; v <= V; v += blockDim.x) {
+    const uint64_t key = (uint64_t)((uint32_t)v * (uint32_t)T) << 32;
+    uint32_t lo = 0, hi = K;   // first k with pk[k] >= key
+    while (lo < hi) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      if (pk[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    s_off[v] = lo;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int v = t; v < V; v += blockDim.x) {
+      const uint32_t kv = s_off[v + 1] - s_off[v];
+      view_pairs[2 * v] = kv;
+      view_pairs[2 * v + 1] = (long long)kv > view_cap ? 1u : 0u;
+    }
+  const size_t gstride = (size_t)gridDim.x * blockDim.x;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + t; k < K; k += gstride) {
+    const uint64_t key = pk[k];
+    const uint32_t ct = (uint32_t)(key >> 32);
+    const uint32_t v = ct / (uint32_t)T, tile = ct - v * (uint32_t)T;
+    const uint32_t off = s_off[v], end = s_off[v + 1];
+    if ((long long)(end - off) > view_cap) continue;
+    const uint32_t kr = (uint32_t)k - off;
+    ids[(size_t)v * (size_t)view_cap + kr] = (uint32_t)key;
+    uint2* r = ranges + (size_t)v * T + tile;
+    if (k == off || (uint32_t)(pk[k - 1] >> 32) != ct) r->x = kr;
+    if (k + 1 == end || (uint32_t)(pk[k + 1] >> 32) != ct) r->y = kr + 1;
+  }
+}
+
 }  // namespace
 
 size_t binsort_workspace(int n, int num_tiles, int64_t capacity) {
@@ -446,7 +522,7 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   uint64_t* a = w.dkeysA;
   uint64_t* b = w.dkeysB;
   for (int p = 0; p < 4; ++p) {
-    onesweep_kernel<<<nblk_n, SORT_THREADS, 0, s>>>(a, b, n, nullptr, w.hist + p * RADIX,
+    onesweep_kernel<uint64_t><<<nblk_n, SORT_THREADS, 0, s>>>(a, b, n, nullptr, w.hist + p * RADIX,
                                                     w.dstatus + (size_t)p * nblk_n * RADIX,
                                                     w.counters + p, 32 + 8 * p);
     launch_counted();
@@ -463,7 +539,7 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   uint64_t* pb = w.pkeysB;
   const int grid_cap = (int)nblk_cap;
   for (int p = 0; p < npass; ++p) {
-    onesweep_kernel<<<grid_cap, SORT_THREADS, 0, s>>>(pa, pb, -1, num_pairs_dev,
+    onesweep_kernel<uint64_t><<<grid_cap, SORT_THREADS, 0, s>>>(pa, pb, -1, num_pairs_dev,
                                                       w.hist + (4 + p) * RADIX,
                                                       w.pstatus + (size_t)p * nblk_cap * RADIX,
                                                       w.counters + 5 + p, 32 + 8 * p);
@@ -473,6 +549,68 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   const int grid_f = 148 * 8;
   finalize_kernel<<<grid_f, 256, 0, s>>>(pa, num_pairs_dev, xy_depth, sorted_keys, sorted_ids,
                                          ranges);
+  launch_counted();
+  return cudaGetLastError();
+}
+
+size_t binsort_views_workspace(int V, int n, int64_t view_capacity) {
+  return carve(nullptr, V * n, (int64_t)V * view_capacity).total;
+}
+
+// V views at once (same image size): one depth presort over the V·N (view,
+// Gaussian) keys, one emission, one sort of all pairs on the combined tile
+// index v·T + tile, per-view outputs.  Equal to V dass_bin_sort calls
+// (bit-exact) with a handful of large kernels instead of V chains of small,
+// latency-bound ones.
+cudaError_t launch_binsort_views(const CamParams& cam, int V, int n, const float4* xy_depth,
+                                 const uint2* box, const uint32_t* tiles, void* ws_ptr,
+                                 int64_t view_capacity, uint32_t* sorted_ids, uint2* ranges,
+                                 uint32_t* view_pairs, cudaStream_t s) {
+  const int T = cam.tiles_x * cam.tiles_y;
+  const int nn = V * n;
+  const int64_t cap = (int64_t)V * view_capacity;
+  WS w = carve(ws_ptr, nn, cap);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)V * T, s))) return e;
+  if ((e = cudaMemsetAsync(w.hist, 0, w.ctrl_bytes, s))) return e;
+  if (nn == 0) return cudaMemsetAsync(view_pairs, 0, 2 * sizeof(uint32_t) * (size_t)V, s);
+  uint32_t* kg = w.counters + 12;   // (K_total, overflow) of the batch
+  const int vt = V * T;
+  const int ct_bits = vt > 1 ? 32 - __builtin_clz((unsigned)(vt - 1)) : 0;
+  const int npass = (ct_bits + 7) / 8;
+  if (npass > MAX_PASSES - 4) return cudaErrorInvalidValue;
+  const int nblk_n = div_up(nn, SORT_ITEMS);
+  const size_t nblk_cap = (size_t)((cap + SORT_ITEMS - 1) / SORT_ITEMS) + 1;
+  const int grid_n = div_up(nn, 256) < 148 * 8 ? div_up(nn, 256) : 148 * 8;
+  presort_init_kernel<<<grid_n, 256, 0, s>>>(nn, xy_depth, tiles, w.dkeysA, w.hist, w.dstatus,
+                                             (size_t)4 * nblk_n * RADIX, w.scan_status, nblk_n);
+  launch_counted();
+  uint64_t* a = w.dkeysA;
+  uint64_t* b = w.dkeysB;
+  for (int p = 0; p < 4; ++p) {
+    onesweep_kernel<uint64_t><<<nblk_n, SORT_THREADS, 0, s>>>(a, b, nn, nullptr, w.hist + p * RADIX,
+                                                    w.dstatus + (size_t)p * nblk_n * RADIX,
+                                                    w.counters + p, 32 + 8 * p);
+    launch_counted();
+    uint64_t* tmp = a; a = b; b = tmp;
+  }
+  tile_scan_kernel<<<nblk_n, 256, 0, s>>>(nn, a, tiles, w.offsets, w.scan_status, w.counters + 4,
+                                          (long long)cap, kg);
+  launch_counted();
+  emit_kernel<<<grid_n, 256, 0, s>>>(nn, a, tiles, box, w.offsets, kg, cam.tiles_x, npass, w.pkeysA,
+                                     w.hist, w.pstatus, nblk_cap * RADIX, n, T);
+  launch_counted();
+  uint64_t* pa = w.pkeysA;
+  uint64_t* pb = w.pkeysB;
+  for (int p = 0; p < npass; ++p) {
+    onesweep_kernel<uint64_t><<<(int)nblk_cap, SORT_THREADS, 0, s>>>(pa, pb, -1, kg, w.hist + (4 + p) * RADIX,
+                                                           w.pstatus + (size_t)p * nblk_cap * RADIX,
+                                                           w.counters + 5 + p, 32 + 8 * p);
+    launch_counted();
+    uint64_t* tmp = pa; pa = pb; pb = tmp;
+  }
+  finalize_views_kernel<<<148 * 8, 256, 0, s>>>(pa, kg, V, T, (long long)view_capacity, sorted_ids,
+                                                ranges, view_pairs);
   launch_counted();
   return cudaGetLastError();
 }

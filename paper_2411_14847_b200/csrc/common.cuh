@@ -185,6 +185,12 @@ cudaError_t launch_deform_bwd(const HashGridParams& g, const float* table, const
 cudaError_t launch_error_map(const CamParams& cam, const float* rendered, const float* gt,
                              float gamma, float* err, uint32_t* dmask, int n_base,
                              const float4* pos_opa, uint8_t* s_err, cudaStream_t s);
+size_t binsort_views_workspace(int V, int n, int64_t view_capacity);
+cudaError_t launch_binsort_views(const CamParams& cam, int V, int n, const float4* xy_depth,
+                                 const uint2* box, const uint32_t* tiles, void* ws_ptr,
+                                 int64_t view_capacity, uint32_t* sorted_ids, uint2* ranges,
+                                 uint32_t* view_pairs, cudaStream_t s);
+cudaError_t launch_timestamp(uint64_t* out, cudaStream_t s);
 cudaError_t launch_render_stats(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
                                 const float4* xy_depth, const float4* conic_opa, const uint2* box,
                                 const float* out_T, const uint32_t* out_last,

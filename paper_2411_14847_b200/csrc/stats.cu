@@ -92,4 +92,18 @@ cudaError_t launch_render_stats(const CamParams& cam, const uint2* ranges, const
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void timestamp_kernel(uint64_t* out) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+}  // namespace
+
+cudaError_t launch_timestamp(uint64_t* out, cudaStream_t s) {
+  timestamp_kernel<<<1, 1, 0, s>>>(out);
+  launch_counted();
+  return cudaGetLastError();
+}
+
 }  // namespace dass

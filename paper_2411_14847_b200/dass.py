@@ -34,7 +34,8 @@ EXPORTS = (
     "dass_deform_param_count", "dass_deform_fwd", "dass_deform_bwd", "dass_partition_workspace",
     "dass_partition", "dass_densify_select", "dass_spawn", "dass_prune_select", "dass_gather",
     "dass_render_features", "dass_render_fwd_tiles", "dass_render_bwd_raster_tiles",
-    "dass_render_bwd_preprocess_views_uv", "dass_gradstat_from_uv",
+    "dass_render_bwd_preprocess_views_uv", "dass_gradstat_from_uv", "dass_timestamp",
+    "dass_bin_sort_views_workspace", "dass_bin_sort_views",
 )
 
 
@@ -107,6 +108,8 @@ def lib():
         L.dass_project_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P]
         L.dass_bin_sort_workspace.argtypes = [i32, i32, i64, P]
         L.dass_bin_sort.argtypes = [P, i32, P, P, P, P, C.c_size_t, i64, P, P, P, P, P, P]
+        L.dass_bin_sort_views_workspace.argtypes = [i32, i32, i64, P]
+        L.dass_bin_sort_views.argtypes = [P, i32, i32, P, P, P, P, C.c_size_t, i64, P, P, P, P]
         L.dass_render_accept_workspace.argtypes = [i32, i64, P]
         L.dass_render_fwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, i64, P]
         L.dass_render_bwd_workspace.argtypes = [i32, P]
@@ -121,6 +124,7 @@ def lib():
         L.dass_inherit_mask_bwd.argtypes = [i32, P, P, P, P, P, C.c_float, P, P]
         L.dass_error_map.argtypes = [P, P, P, C.c_float, P, P, i32, P, P, P]
         L.dass_render_stats.argtypes = [P, P, P, P, P, P, P, P, P, P]
+        L.dass_timestamp.argtypes = [P, i32, P]
         L.dass_deform_param_count.argtypes = [P, P, P]
         L.dass_deform_fwd.argtypes = [P, P, P, i32, P, P, P, P, P, P]
         L.dass_deform_bwd.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
@@ -240,6 +244,25 @@ def dass_bin_sort(cam, n, xy_depth, box, tiles_touched, ws, pair_capacity, sorte
                              _stream(stream))
     _check(st, "dass_bin_sort")
     return k.value if host_mode else None
+
+
+def dass_bin_sort_views_workspace(num_views, n, view_capacity) -> int:
+    out = C.c_size_t(0)
+    _check(lib().dass_bin_sort_views_workspace(num_views, n, view_capacity, C.byref(out)),
+           "dass_bin_sort_views_workspace")
+    return out.value
+
+
+def dass_bin_sort_views(cams, n, xy_depth, box, tiles_touched, ws, view_capacity, sorted_ids,
+                        tile_ranges, num_pairs_dev, stream=None):
+    """All views of a timestep at once (graph mode): per view v, sorted_ids[v],
+    tile_ranges[v] and num_pairs_dev[v] = (K_v, overflow_v) as dass_bin_sort."""
+    arr = (dass_camera * len(cams))(*[_cam(c) for c in cams])
+    _check(lib().dass_bin_sort_views(arr, len(cams), n, _ptr(xy_depth), _ptr(box),
+                                     _ptr(tiles_touched), _ptr(ws), ws.numel() * ws.element_size(),
+                                     view_capacity, _ptr(sorted_ids), _ptr(tile_ranges),
+                                     _ptr(num_pairs_dev), _stream(stream)),
+           "dass_bin_sort_views")
 
 
 def dass_render_accept_workspace(num_tiles, pair_capacity) -> int:
@@ -369,6 +392,11 @@ def dass_render_stats(cam, tile_ranges, sorted_ids, xy_depth, conic_opa, box, ou
                                    _ptr(xy_depth), _ptr(conic_opa), _ptr(box), _ptr(out_T),
                                    _ptr(out_last), _ptr(counters), _stream(stream)),
            "dass_render_stats")
+
+
+def dass_timestamp(stamps, slot, stream=None):
+    """Diagnostic: GPU global timer (ns) → stamps[slot] when the stream gets there."""
+    _check(lib().dass_timestamp(_ptr(stamps), slot, _stream(stream)), "dass_timestamp")
 
 
 def dass_deform_param_count(field):

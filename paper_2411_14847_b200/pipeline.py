@@ -111,13 +111,24 @@ class Raster:
             ab = dass.dass_render_accept_workspace(self.num_tiles, capacity)
             self.accept = torch.empty(ab // 4, dtype=torch.int32, device=device)
 
-    def forward(self, cam, rec, host_mode=False, bg=None, sorted_keys=None, tiles=None):
+    def sort(self, cam, rec, host_mode=False, sorted_keys=None):
         xy, co, rgb, box, tt = rec
-        K = dass.dass_bin_sort(cam, self.n, xy, box, tt, self.sort_ws, self.capacity,
-                               sorted_keys, self.sorted_ids, self.ranges, self.num_pairs,
-                               host_mode=host_mode)
-        dass.dass_render_fwd(cam, self.ranges, self.sorted_ids, xy, co, rgb, box, bg, self.img,
-                             self.T, self.last, self.accept, self.capacity, tiles=tiles)
+        return dass.dass_bin_sort(cam, self.n, xy, box, tt, self.sort_ws, self.capacity,
+                                  sorted_keys, self.sorted_ids, self.ranges, self.num_pairs,
+                                  host_mode=host_mode)
+
+    def render(self, cam, rec, bg=None, tiles=None, ranges=None, sorted_ids=None):
+        """ranges/sorted_ids: a view's slices of a batched dass_bin_sort_views (else
+        this slot's own sort)."""
+        xy, co, rgb, box, tt = rec
+        dass.dass_render_fwd(cam, self.ranges if ranges is None else ranges,
+                             self.sorted_ids if sorted_ids is None else sorted_ids, xy, co, rgb,
+                             box, bg, self.img, self.T, self.last, self.accept, self.capacity,
+                             tiles=tiles)
+
+    def forward(self, cam, rec, host_mode=False, bg=None, sorted_keys=None, tiles=None):
+        K = self.sort(cam, rec, host_mode=host_mode, sorted_keys=sorted_keys)
+        self.render(cam, rec, bg=bg, tiles=tiles)
         return K
 
     def backward(self, cam, scene: DeviceScene, rec, dL_dimg, grads: Grads, keep=None, bg=None,
@@ -174,6 +185,15 @@ class MultiViewPass:
         prio = os.environ.get("DASS_STREAM_PRIO", "0") == "1"
         self.streams = [torch.cuda.Stream(device=device, priority=-1 if prio and 2 * k < self.S else 0)
                         for k in range(self.S)]
+        # bin_sort chains: with every view's sort on its own stream, the graph runs the
+        # 20 latency-bound sorts in lockstep (≈1.9 ms with no raster work ready).  The
+        # sorts instead run one after another on DASS_SORT_CHAINS streams (0 = on the
+        # view streams), so view 0 rasterises after one sort and the later sorts
+        # overlap the earlier views' raster kernels (tools/timeline.py).
+        nch = int(os.environ.get("DASS_SORT_CHAINS", "0"))
+        prio = -5 if os.environ.get("DASS_SORT_PRIO", "1") == "1" else 0
+        self.sort_streams = ([torch.cuda.Stream(device=device, priority=prio)
+                              for _ in range(min(nch, self.S))] if nch > 0 else None)
         self.pre_stream = torch.cuda.Stream(device=device)
         self.pre_chunks = int(os.environ.get("DASS_PRE_CHUNKS", "2"))
         self.proj_chunks = int(os.environ.get("DASS_PROJ_CHUNKS", "1"))
@@ -181,6 +201,22 @@ class MultiViewPass:
         # an end-to-end caller makes the view wait there for its own ∂L/∂C upload
         self.before_bwd = None
         self.g2d = torch.empty(max(self.V, 1), n, 12, dtype=torch.float32, device=device)
+        # DASS_BATCH_SORT=1: dass_bin_sort_views over chunks of the views instead of a
+        # dass_bin_sort per view.  In the graph the per-view sort chains run in lockstep
+        # (≈1.9 ms of the step with no raster work ready, tools/timeline.py), but the
+        # batched sort is slower still (2.6 ms isolated for 20 views: its 17-bit pair
+        # passes and emission are instruction-bound), so the per-view sorts stay default.
+        self.batch_sort = os.environ.get("DASS_BATCH_SORT", "0") == "1" and self.V > 0
+        if self.batch_sort:
+            T = self.slots[0].num_tiles
+            # sort chunks: chunk c + 1 sorts on the main stream while chunk c rasterises
+            self.sort_chunks = max(1, min(int(os.environ.get("DASS_SORT_BATCH_CHUNKS", "4")), self.V))
+            vmax = -(-self.V // self.sort_chunks)
+            ws = dass.dass_bin_sort_views_workspace(vmax, n, capacity)
+            self.bs_ws = torch.empty(max(ws, 16), dtype=torch.uint8, device=device)
+            self.bs_ids = torch.empty(self.V, max(capacity, 1), dtype=torch.int32, device=device)
+            self.bs_ranges = torch.empty(self.V, T, 2, dtype=torch.int32, device=device)
+            self.bs_pairs = torch.zeros(self.V, 2, dtype=torch.int32, device=device)
 
     def enable_loss(self, lam: float = 0.2):
         """Allocate per-slot scratch so run(gts=...) computes dL/dC itself with the
@@ -205,12 +241,23 @@ class MultiViewPass:
         torch = _torch()
         main = torch.cuda.current_stream()
         V = self.V
-        pc = max(1, min(self.proj_chunks, V)) if project is not None else 1
-        pbounds = [round(c * V / pc) for c in range(pc + 1)]
-        ready = []   # per projection chunk: the event the chunk's views wait on
-        for c in range(pc):
+        if self.batch_sort:   # project all views, then sort them in chunks
             if project is not None:
-                project(pbounds[c], pbounds[c + 1])
+                project(0, V)
+            pc = self.sort_chunks
+        else:
+            pc = max(1, min(self.proj_chunks, V)) if project is not None else 1
+        pbounds = [round(c * V / pc) for c in range(pc + 1)]
+        ready = []   # per chunk: the event the chunk's views wait on
+        for c in range(pc):
+            a, b = pbounds[c], pbounds[c + 1]
+            if self.batch_sort:
+                dass.dass_bin_sort_views(self.cams[a:b], self.n, records.xy_depth[a:b],
+                                         records.box[a:b], records.tiles[a:b], self.bs_ws,
+                                         self.slots[0].capacity, self.bs_ids[a:b],
+                                         self.bs_ranges[a:b], self.bs_pairs[a:b])
+            elif project is not None:
+                project(a, b)
             e = torch.cuda.Event()
             e.record(main)
             ready.append(e)
@@ -228,11 +275,23 @@ class MultiViewPass:
         for v, cam in enumerate(self.cams):
             k = v % self.S
             ras, st = self.slots[k], self.streams[k]
+            rec = records.view(v)
+            xy, co, rgb, box, tiles = rec
             st.wait_event(ready[chunk_of[v]])
+            if self.batch_sort:
+                vr, vi = self.bs_ranges[v], self.bs_ids[v]
+            else:
+                vr, vi = ras.ranges, ras.sorted_ids
+            if self.sort_streams is not None and not self.batch_sort:
+                ss = self.sort_streams[v % len(self.sort_streams)]
+                ss.wait_stream(st)    # projected, and the slot's previous view is done
+                with torch.cuda.stream(ss):
+                    ras.sort(cam, rec)
+                st.wait_stream(ss)
             with torch.cuda.stream(st):
-                rec = records.view(v)
-                xy, co, rgb, box, tiles = rec
-                ras.forward(cam, rec, bg=bg, tiles=self.tiles[v])
+                if self.sort_streams is None and not self.batch_sort:
+                    ras.sort(cam, rec)
+                ras.render(cam, rec, bg=bg, tiles=self.tiles[v], ranges=vr, sorted_ids=vi)
                 if gts is not None:
                     dL = self.loss_dL[k]
                     dass.dass_fidelity_loss(ras.img, gts[v], self.lam, self.loss_ws[k],
@@ -241,7 +300,7 @@ class MultiViewPass:
                     dL = dL_dimgs[v]
                 if self.before_bwd is not None:
                     self.before_bwd(v, st)
-                dass.dass_render_bwd_raster(cam, self.n, ras.ranges, ras.sorted_ids, xy, co, rgb,
+                dass.dass_render_bwd_raster(cam, self.n, vr, vi, xy, co, rgb,
                                             box, bg, ras.T, ras.last, dL, self.g2d[v],
                                             ras.accept, ras.capacity, tiles=self.tiles[v])
                 done[v] = torch.cuda.Event()
@@ -254,6 +313,8 @@ class MultiViewPass:
                 with torch.cuda.stream(self.pre_stream):
                     self._preprocess(scene, records, grads, keep, bounds[c], bounds[c + 1])
         for s in self.streams:
+            main.wait_stream(s)
+        for s in self.sort_streams or []:
             main.wait_stream(s)
         if nchunk > 1:
             main.wait_stream(self.pre_stream)
