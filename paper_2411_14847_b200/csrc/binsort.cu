@@ -136,10 +136,7 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     uint32_t* counter, int shift) {
   __shared__ uint32_t s_whist[SORT_THREADS / 32][RADIX];
   __shared__ uint32_t s_gbase[RADIX];
-  __shared__ uint32_t s_bstart[RADIX];
   __shared__ uint32_t s_wsum[SORT_THREADS / 32];
-  __shared__ uint32_t s_bsum[SORT_THREADS / 32];
-  __shared__ KT s_keys[SORT_ITEMS];
   __shared__ uint32_t s_blk;
   const int t = threadIdx.x;
   const int warp = t >> 5;
@@ -194,17 +191,15 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     s_whist[w][t] = count;
     count += c;
   }
-  // exclusive scan of the global histogram over digits (digit = t), and of the
-  // block's digit counts (the block-local digit-sorted order for the staging)
+  // exclusive scan of the global histogram over digits (digit = t)
   const uint32_t hv = hist[t];
-  uint32_t incl = hv, bincl = count;
+  uint32_t incl = hv;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    const uint32_t z = __shfl_up_sync(0xffffffffu, bincl, o);
-    if ((int)lane >= o) { incl += y; bincl += z; }
+    if ((int)lane >= o) incl += y;
   }
-  if (lane == 31) { s_wsum[warp] = incl; s_bsum[warp] = bincl; }
+  if (lane == 31) s_wsum[warp] = incl;
   // decoupled look-back for digit t
   uint32_t excl = 0u;
   uint32_t* my = status + (size_t)blk * RADIX + t;
@@ -227,25 +222,14 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     st_relaxed(my, FLAG_INC | (excl + count));
   }
   __syncthreads();
-  uint32_t gofs = incl - hv, bofs = bincl - count;
-  for (int w = 0; w < warp; ++w) { gofs += s_wsum[w]; bofs += s_bsum[w]; }
-  s_bstart[t] = bofs;                     // first block-local slot of digit t
-  s_gbase[t] = gofs + excl - bofs;        // global index = s_gbase[d] + block-local slot
+  uint32_t gofs = incl - hv;
+  for (int w = 0; w < warp; ++w) gofs += s_wsum[w];
+  s_gbase[t] = gofs + excl;
   __syncthreads();
-  // stage the keys in block-local digit order, then write them out in order:
-  // consecutive threads → consecutive slots → runs of one digit are contiguous
-  // in the output (coalesced), instead of one scattered store per key
 #pragma unroll
   for (int j = 0; j < SORT_IPT; ++j) {
     const uint32_t d = digit[j];
-    if (d < 256u) s_keys[s_bstart[d] + s_whist[warp][d] + rank[j]] = keys[j];
-  }
-  __syncthreads();
-  const int valid = (int)min((long long)SORT_ITEMS, (long long)n - base);
-  for (int i = t; i < valid; i += SORT_THREADS) {
-    const KT key = s_keys[i];
-    const uint32_t d = (uint32_t)(key >> shift) & 255u;
-    out[s_gbase[d] + (uint32_t)i] = key;
+    if (d < 256u) out[s_gbase[d] + s_whist[warp][d] + rank[j]] = keys[j];
   }
 }
 
