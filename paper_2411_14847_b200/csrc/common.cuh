@@ -55,6 +55,18 @@ __device__ __forceinline__ ColTerms col_terms(float A, float B, float C, float d
   t.hC = -0.5f * C;
   return t;
 }
+// The same terms from a staged conic (−½A, −B, −½C): the scalings are exact in
+// fp32, so the bits equal col_terms(A, B, C, dx).
+__device__ __forceinline__ float4 conic_staged(float4 co) {
+  return make_float4(-0.5f * co.x, -co.y, -0.5f * co.z, co.w);
+}
+__device__ __forceinline__ ColTerms col_terms_staged(const float4& sc, float dx) {
+  ColTerms t;
+  t.ax = __fmul_rn(__fmul_rn(sc.x, dx), dx);
+  t.bx = __fmul_rn(sc.y, dx);
+  t.hC = sc.z;
+  return t;
+}
 __device__ __forceinline__ float splat_power(const ColTerms& t, float dy) {
   return __fmaf_rn(dy, __fmaf_rn(t.hC, dy, t.bx), t.ax);
 }

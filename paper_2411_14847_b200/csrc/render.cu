@@ -37,7 +37,7 @@ namespace {
 //   s_a  = (u_rel, v_rel, p_thr, box mask bits)   p_thr: conservative power
 //          threshold ln(α_min/o) − 1e-3 below which α < 1/255 for sure, so the
 //          exp is skipped without changing any decision
-//   s_co = (A, B, C, o)    s_c = (r, g, b, −)
+//   s_co = (−½A, −B, −½C, o) (conic_staged)    s_c = (r, g, b, −)
 // Tile-local row/column mask of the pixels an entry can possibly be accepted
 // at: the integer pixel box (A05) intersected with the bounding box of the
 // α ≥ 1/255 support ellipse {½ dᵀK d ≤ −p_thr}, whose half-extents are
@@ -122,12 +122,13 @@ __device__ __forceinline__ void stage(uint32_t id, const float4* __restrict__ xy
   const float4 xy = xy_depth[id];
   const uint32_t lo_bits = __float_as_uint(xy.w);
   const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
-  co = conic_opa[id];
+  const float4 con = conic_opa[id];
+  co = conic_staged(con);   // (−½A, −B, −½C, o)
   const float4 cc = rgb[id];
   a.x = __fadd_rn(xy.x - (float)tx0, __low2float(lo));
   a.y = __fadd_rn(xy.y - (float)ty0, __high2float(lo));
   a.z = __logf(ALPHA_MIN / co.w) - 1e-3f;
-  a.w = __uint_as_float(support_mask<RPW>(box[id], tx0, ty0, a.x, a.y, co, a.z));
+  a.w = __uint_as_float(support_mask<RPW>(box[id], tx0, ty0, a.x, a.y, con, a.z));
   c = make_float4(cc.x, cc.y, cc.z, 0.f);
 }
 
@@ -245,13 +246,13 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
         float pw[PPT];
         uint32_t ok = 0;
         if constexpr (PixMap<PPT>::QUAD) {
-          const ColTerms c0 = col_terms(co.x, co.y, co.z, a.x - fxc[0]);
-          const ColTerms c1 = col_terms(co.x, co.y, co.z, a.x - fxc[1]);
+          const ColTerms c0 = col_terms_staged(co, a.x - fxc[0]);
+          const ColTerms c1 = col_terms_staged(co, a.x - fxc[1]);
           const float dy0 = a.y - fy[0], dy1 = a.y - fy[2];
           pw[0] = splat_power(c0, dy0); pw[1] = splat_power(c1, dy0);
           pw[2] = splat_power(c0, dy1); pw[3] = splat_power(c1, dy1);
         } else {
-          const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fxc[0]);
+          const ColTerms ct = col_terms_staged(co, a.x - fxc[0]);
 #pragma unroll
           for (int p = 0; p < PPT; ++p) pw[p] = splat_power(ct, a.y - fy[p]);
         }
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(64) render_features_kernel(
       const uint32_t m = __float_as_uint(a.w);
       if ((m & wmask) == 0u || !(m & colbit)) continue;
       const float4 co = s_st[j].co;
-      const ColTerms ct = col_terms(co.x, co.y, co.z, a.x - fx);
+      const ColTerms ct = col_terms_staged(co, a.x - fx);
       const uint32_t mr = m >> (16 + ly0);
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
       if (m & colbit) {
         const float4 co = st.co;
         const float dx = a.x - fx;
-        const ColTerms ct = col_terms(co.x, co.y, co.z, dx);
+        const ColTerms ct = col_terms_staged(co, dx);
         const uint32_t mr = m >> (16 + ly0);   // this thread's PPT row bits
         float pw[PPT];
         bool ok[PPT];
@@ -603,7 +604,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
   constexpr int NT = 256 / PPT;
   constexpr int NW = NT / 32;
   __shared__ float4 s_a[NW][32];    // (u_rel, v_rel, −, −)
-  __shared__ float4 s_co[NW][32];   // (A, B, C, o)
+  __shared__ float4 s_co[NW][32];   // (−½A, −B, −½C, o)
   __shared__ float4 s_c[NW][32];    // (r, g, b, −)
   __shared__ uint4 s_bytes[NW][32][2];   // 32 acceptance bytes per staged entry
   __shared__ uint32_t s_id[NW][32];
@@ -655,7 +656,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
       const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
       s_a[warp][lane] = make_float4(__fadd_rn(xy.x - (float)tx0, __low2float(lo)),
                                     __fadd_rn(xy.y - (float)ty0, __high2float(lo)), 0.f, 0.f);
-      s_co[warp][lane] = conic_opa[id];
+      s_co[warp][lane] = conic_staged(conic_opa[id]);
       s_c[warp][lane] = rgb[id];
     }
     __syncwarp();
@@ -670,8 +671,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
         const float4 c = s_c[warp][k];
         const float dxc[2] = {a.x - fx0, a.x - fx1};
         const float dyr[2] = {a.y - fy0, a.y - fy1};
-        const ColTerms ct[2] = {col_terms(co.x, co.y, co.z, dxc[0]),
-                                col_terms(co.x, co.y, co.z, dxc[1])};
+        const ColTerms ct[2] = {col_terms_staged(co, dxc[0]),
+                                col_terms_staged(co, dxc[1])};
         float se[2] = {0.f, 0.f}, sey[2] = {0.f, 0.f};   // per column: Σe, Σe·dy
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
@@ -830,8 +831,8 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
       const uint32_t cand = pm.cand(m) & live;
       if (cand) {
         const float4 co = st.co;
-        const ColTerms c0 = col_terms(co.x, co.y, co.z, a.x - fx0);
-        const ColTerms c1 = col_terms(co.x, co.y, co.z, a.x - fx1);
+        const ColTerms c0 = col_terms_staged(co, a.x - fx0);
+        const ColTerms c1 = col_terms_staged(co, a.x - fx1);
         float pw[PPT];
         uint32_t ok = 0;
 #pragma unroll
@@ -897,7 +898,7 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
   constexpr int PPT = 8;
   constexpr int CH = TW_BWD_CHUNK;   // entries staged per chunk
   __shared__ float4 s_a[CH];    // (u_rel, v_rel, −, −)
-  __shared__ float4 s_co[CH];   // (A, B, C, o)
+  __shared__ float4 s_co[CH];   // (−½A, −B, −½C, o)
   __shared__ float4 s_c[CH];    // (r, g, b, −)
   __shared__ uint4 s_bytes[CH][2];
   __shared__ uint32_t s_id[CH];
@@ -950,7 +951,7 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
       const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
       s_a[lane] = make_float4(__fadd_rn(xy.x - (float)tx0, __low2float(lo)),
                               __fadd_rn(xy.y - (float)ty0, __high2float(lo)), 0.f, 0.f);
-      s_co[lane] = conic_opa[id];
+      s_co[lane] = conic_staged(conic_opa[id]);
       s_c[lane] = rgb[id];
     }
     __syncwarp();
@@ -964,8 +965,8 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
         const float4 co = s_co[k];
         const float4 c = s_c[k];
         const float dxc[2] = {a.x - fx0, a.x - fx1};
-        const ColTerms ct[2] = {col_terms(co.x, co.y, co.z, dxc[0]),
-                                col_terms(co.x, co.y, co.z, dxc[1])};
+        const ColTerms ct[2] = {col_terms_staged(co, dxc[0]),
+                                col_terms_staged(co, dxc[1])};
         float se[2] = {0.f, 0.f}, sey[2] = {0.f, 0.f};   // per column: Σe, Σe·dy
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
