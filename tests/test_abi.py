@@ -143,3 +143,34 @@ def test_binding_refuses_float64_tensors(lib):
     t = torch.zeros(4, 4, dtype=torch.float64, device="cuda")
     with pytest.raises(TypeError):
         lib.dass_apply_shift(t, t, t, t, None, t, t)
+
+
+def test_bin_sort_views_and_timestamp_validation_before_any_cuda_call(lib):
+    """dass_bin_sort_views / its workspace query / dass_timestamp refuse bad arguments
+    with INVALID_ARG before enqueueing anything."""
+    L = lib.lib()
+    P = None
+    out = C.c_size_t(0)
+    arr = (lib.dass_camera * 2)(lib.camera_struct(synth.tiny_camera(64, 64)),
+                                lib.camera_struct(synth.tiny_camera(64, 64)))
+    assert L.dass_bin_sort_views_workspace(0, 100, 1000, C.byref(out)) == 1     # V < 1
+    assert L.dass_bin_sort_views_workspace(65, 100, 1000, C.byref(out)) == 1    # V > 64
+    assert L.dass_bin_sort_views_workspace(4, 100, 1 << 28, C.byref(out)) == 1  # V·cap ≥ 2^30
+    assert L.dass_bin_sort_views_workspace(4, 100, 1000, None) == 1
+    assert L.dass_bin_sort_views_workspace(2, 100, 1000, C.byref(out)) == 0
+    one = out.value
+    assert L.dass_bin_sort_views_workspace(2, 100, 2000, C.byref(out)) == 0 and out.value > one
+    # cameras of different sizes, null outputs, workspace too small
+    mixed = (lib.dass_camera * 2)(lib.camera_struct(synth.tiny_camera(64, 64)),
+                                  lib.camera_struct(synth.tiny_camera(32, 64)))
+    args = lambda cams, ws, nb, ids: (cams, 2, 100, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16),
+                                      ws, nb, 1000, ids, C.c_void_p(16), C.c_void_p(16), P)
+    assert L.dass_bin_sort_views(*args(mixed, C.c_void_p(16), one, C.c_void_p(16))) == 1
+    assert b"differ" in L.dass_last_error()
+    assert L.dass_bin_sort_views(*args(arr, C.c_void_p(16), one, None)) == 1
+    assert L.dass_bin_sort_views(*args(arr, C.c_void_p(16), one - 1, C.c_void_p(16))) == 1
+    assert b"workspace" in L.dass_last_error()
+    assert L.dass_bin_sort_views(None, 2, 100, P, P, P, P, 0, 1000, P, P, P, P) == 1
+    assert L.dass_timestamp(None, 0, P) == 1
+    assert L.dass_timestamp(C.c_void_p(16), -1, P) == 1
+    assert lib.kernel_launches() == 0
