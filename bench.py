@@ -800,6 +800,22 @@ RASTER_KERNELS = {
 }
 
 
+def issue_view(prof, ms, launches, f_max):
+    """The kernel against the instruction-issue roof (148 SMs × 4 schedulers × 1 warp
+    instruction per clock): executed warp instructions per launch from the committed ncu
+    summary (one C3 view; the scene is fixed) × the launches, over the live time.  The
+    raster kernels are issue-bound (compares, selects, shuffles, MUFU next to the FMAs),
+    so this is the roof they actually meet; `frac` above counts algorithmic flops only."""
+    instr = profiled_instructions(prof)
+    if not instr or not ms or ms != ms:
+        return None
+    rate = instr * launches / (ms / 1e3)
+    peak = SM_COUNT * 4 * f_max
+    return {"warp_instr_per_launch": instr, "achieved_ginstr_s": round(rate / 1e9, 1),
+            "peak_ginstr_s": round(peak / 1e9, 1), "frac": round(rate / peak, 4),
+            "source": f"profiles/r01_ncu_{prof}.txt (Executed Instructions)"}
+
+
 def dominant_roofline(ops, stats, f_max, peak_tflops):
     """Roofline object of the step's dominant kernel: whichever raster kernel (forward
     or backward) takes longer in the isolated per-op pass.  achieved = algorithmic
@@ -839,6 +855,7 @@ def dominant_roofline(ops, stats, f_max, peak_tflops):
                                  "what": "SURVEY §8(d)'s unit (every in-box (pixel, entry)) × its FP32-pipe "
                                          "instruction estimate against the issue peak: an equivalent-work "
                                          "rate, not the algorithmic one in frac"},
+            "issue_view": issue_view(prof, ms, len(stats["accepted"]), f_max),
             "timing": "isolated launches: one sequential pass over the step's kernels (CUDA events on "
                       "the launching stream), since in the timed graph the per-view kernels of 20 "
                       "streams overlap",
@@ -937,6 +954,19 @@ def rows_roofline(ops, densify, allst, pk, peak_fp32, n, W, H, views, deg):
                                          "frac": round(fl / t / 1e12 / peak_fp32, 4),
                                          "unit": "accepted (pixel, entry) of view 0 (2·16 + 15 flop)"}
     return out
+
+
+def profiled_instructions(kernel: str):
+    """Executed warp instructions per launch of `kernel` from the committed ncu summary."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        f"r01_ncu_{kernel}.txt")
+    try:
+        for line in open(path):
+            if line.startswith("Executed Instructions"):
+                return int(float(line.split()[2].replace(",", "")))
+    except (OSError, ValueError, IndexError):
+        pass
+    return None
 
 
 def profiled_traffic(kernel: str):

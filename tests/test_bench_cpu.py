@@ -45,3 +45,12 @@ def test_dominant_roofline_picks_the_slower_raster_kernel():
     assert bwd["kernel"].startswith("render_bwd")
     assert abs(bwd["achieved"] - bench.FLOP_BWD_ACCEPTED * 65e6 * 20 / 6.7e-3 / 1e12) < 0.01
     assert bench.dominant_roofline({}, stats, f, peak) is None
+
+
+def test_issue_view_reads_the_committed_profile():
+    v = bench.issue_view("render_fwd", 7.4, 20, 1965e6)
+    instr = bench.profiled_instructions("render_fwd")
+    assert instr and instr > 1e8
+    assert abs(v["frac"] - instr * 20 / 7.4e-3 / (148 * 4 * 1965e6)) < 1e-3
+    assert 0 < v["frac"] < 1
+    assert bench.issue_view("no_such_kernel", 7.4, 20, 1965e6) is None
