@@ -35,6 +35,26 @@ if ROOT not in sys.path:
 METRIC = "fwd+bwd views/sec (Mpix/s) at 300k Gaussians, 1352x1014, 1/2/4/8 B200"
 WORKLOAD = ("C3: N3DV-shaped timestep, 20 views 1352x1014, 300k Gaussians SH3, 30% dynamic "
             "masked shift; step = one shift iteration (shift + fwd+bwd over all views)")
+WORKLOADS = {
+    "c3": WORKLOAD,
+    "c4": ("C4: Meet-Room-shaped timestep, 13 views 1280x720, 200k Gaussians SH3, 30% dynamic "
+           "masked shift; step = one shift iteration (shift + fwd+bwd over all views)"),
+    "c5": ("C5: 20 views 1352x1014, 1M Gaussians SH3 (sigma_px median x sqrt(0.3)), 30% dynamic "
+           "masked shift; step = one shift iteration (shift + fwd+bwd over all views)"),
+}
+
+
+def workload(args):
+    """(cameras, scene, workload string) of --config, with --n / --views overrides."""
+    from paper_2411_14847_b200 import synth
+    if args.config == "c4":
+        cams, scene = synth.c4(n=args.n or 200_000, num_views=args.views or 13)
+    elif args.config == "c5":
+        cams, scene = synth.c5(n=args.n or 1_000_000)
+        cams = cams[:args.views] if args.views else cams
+    else:
+        cams, scene = synth.c3(n=args.n or 300_000, num_views=args.views or 20)
+    return cams, scene, WORKLOADS[args.config]
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 SM_COUNT = 148
 FP32_LANES = 128
@@ -53,9 +73,13 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=300_000)
-    p.add_argument("--views", type=int, default=20)
-    p.add_argument("--capacity", type=int, default=1 << 22, help="pair capacity per view")
+    p.add_argument("--config", choices=("c3", "c4", "c5"), default="c3",
+                   help="BASELINE.json workload: c3 (default, the metric's), c4 (Meet-Room "
+                        "shaped), c5 (1M Gaussians)")
+    p.add_argument("--n", type=int, default=None, help="Gaussians (default: the config's)")
+    p.add_argument("--views", type=int, default=None, help="views (default: the config's)")
+    p.add_argument("--capacity", type=int, default=None,
+                   help="pair capacity per view (default 2^22, 2^23 for c5)")
     p.add_argument("--streams", type=int, default=20, help="overlapping per-view streams")
     p.add_argument("--no-graph", action="store_true", help="do not capture the step in a CUDA graph")
     p.add_argument("--lean", action="store_true",
@@ -70,7 +94,10 @@ def parse():
                    help="diagnostic: open a one-rank NCCL group so the N>1 code path (all_reduce, "
                         "split-view finish, max over ranks) runs on one GPU; with --emulate R/W it "
                         "exercises rank R's whole multi-GPU step")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.capacity is None:
+        a.capacity = 1 << 23 if a.config == "c5" else 1 << 22
+    return a
 
 
 def dist_env():
@@ -147,7 +174,7 @@ def run_ours(args):
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
-    cams, scene = synth.c3(n=args.n, num_views=args.views)
+    cams, scene, wl = workload(args)
     mu, sigma = synth.shift_offsets(scene, seed=33)
     W0, H0 = cams[0].width, cams[0].height
     plan_rank, plan_world = rank, world
@@ -667,7 +694,7 @@ def run_ours(args):
         peak_tflops = SM_COUNT * FP32_LANES * 2 * f_max / 1e12
         # the dominant kernel of the step (the larger of the two raster kernels in the
         # isolated per-op pass) against the FP32 roof, algorithmic flops only
-        dom = dominant_roofline(ops, stats, f_max, peak_tflops)
+        dom = dominant_roofline(ops, stats, f_max, peak_tflops, profiled=args.config == "c3")
         views_s = job_views / (ms_step / 1e3)
         result = {
             "metric": METRIC, "value": round(views_s, 3), "unit": "views/s",
@@ -678,7 +705,7 @@ def run_ours(args):
                                               for q, v in (("p10", 10), ("p50", 50), ("p90", 90))},
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N3DV-shaped scene and rig)",
-            "config": {"workload": WORKLOAD, "n_gaussians": n, "views": len(cams), "width": W,
+            "config": {"workload": wl, "n_gaussians": n, "views": len(cams), "width": W,
                        "height": H, "sh_degree": deg, "dynamic_frac": 0.3,
                        "cuda_graph": graph is not None, "streams": args.streams,
                        "emulated_share": args.emulate,
@@ -759,7 +786,7 @@ def run_reference(args):
     from paper_2411_14847_b200 import synth
     import oracle
     oracle.build()
-    cams, scene = synth.c3(n=args.n, num_views=args.views)
+    cams, scene, wl = workload(args)
     W, H = cams[0].width, cams[0].height
     for k in range(args.warmup):
         time_oracle(cams, scene, [k % len(cams)])
@@ -773,7 +800,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": round(s * 1e3, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded N3DV-shaped scene and rig)",
-            "config": {"workload": WORKLOAD, "n_gaussians": scene.n, "views": len(cams),
+            "config": {"workload": wl, "n_gaussians": scene.n, "views": len(cams),
                        "width": W, "height": H, "sh_degree": scene.sh_degree,
                        "parallelism": "CPU oracle, OpenMP"},
             "cpu_baseline": {"value": round(value, 4), "unit": "views/s", "cores": oracle.threads(),
@@ -816,7 +843,7 @@ def issue_view(prof, ms, launches, f_max):
             "source": f"profiles/r01_ncu_{prof}.txt (Executed Instructions)"}
 
 
-def dominant_roofline(ops, stats, f_max, peak_tflops):
+def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True):
     """Roofline object of the step's dominant kernel: whichever raster kernel (forward
     or backward) takes longer in the isolated per-op pass.  achieved = algorithmic
     flops of the step's launches / their summed isolated durations."""
@@ -839,9 +866,10 @@ def dominant_roofline(ops, stats, f_max, peak_tflops):
     peak_i = SM_COUNT * FP32_LANES * f_max / 1e12
     rate = units * instr / (ms / 1e3) / 1e12
     prof = "render_fwd" if key == "render_fwd" else "render_bwd"
+    # the committed ncu summaries are of a C3 view: other configs get no profiled numbers
     return {"bound": "alu", "kernel": name, "achieved": round(achieved, 2),
             "peak": round(peak_tflops, 1), "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4),
-            "traffic": profiled_traffic(prof),
+            "traffic": profiled_traffic(prof) if profiled else None,
             "traffic_source": f"profiles/r01_ncu_{prof}.txt (ncu --set full, dram read+write per "
                               "launch = one view)",
             "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz",
@@ -855,7 +883,7 @@ def dominant_roofline(ops, stats, f_max, peak_tflops):
                                  "what": "SURVEY §8(d)'s unit (every in-box (pixel, entry)) × its FP32-pipe "
                                          "instruction estimate against the issue peak: an equivalent-work "
                                          "rate, not the algorithmic one in frac"},
-            "issue_view": issue_view(prof, ms, len(stats["accepted"]), f_max),
+            "issue_view": issue_view(prof, ms, len(stats["accepted"]), f_max) if profiled else None,
             "timing": "isolated launches: one sequential pass over the step's kernels (CUDA events on "
                       "the launching stream), since in the timed graph the per-view kernels of 20 "
                       "streams overlap",
@@ -984,17 +1012,22 @@ def profiled_traffic(kernel: str):
 
 def main():
     args = parse()
+    # stdout carries exactly the one JSON line: anything else written to fd 1 by the
+    # libraries underneath (e.g. NCCL's "NCCL version …" banner) goes to stderr
+    out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     if args.impl == "reference":
         r = run_reference(args)
         if r is not None:
-            print(json.dumps(r), flush=True)
+            print(json.dumps(r), file=out, flush=True)
         return
     result, (cams, scene) = run_ours(args)
     rank, world, _ = dist_env()
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(cams, scene, args.cpu_sample_views)
-        print(json.dumps(result), flush=True)
+        print(json.dumps(result), file=out, flush=True)
 
 
 if __name__ == "__main__":
