@@ -793,8 +793,10 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
   constexpr int PPT = 8;
   constexpr int BATCH = TW_FWD_BATCH;
   __shared__ Staged s_st[BATCH];
-  // (C_r, C_g, C_b, T) of the lane's pixels in shared memory instead of 32
-  // registers (occupancy: 1-warp CTAs); touched once per accepted pixel
+  // (C_r, C_g, C_b, T) of the lane's pixels in shared memory instead of 24
+  // registers (occupancy: 1-warp CTAs); touched once per accepted pixel (T is
+  // also kept in registers for the termination test; .w is the copy the
+  // output stage reads)
   __shared__ float4 s_px[PPT][32];
   const int tile = cam.tile0 + (int)acc.order[blockIdx.x] * cam.tstride;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
@@ -803,10 +805,12 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
   const TileMap pm((int)lane);
   const uint2 range = ranges[tile];
   uint32_t last[PPT];
+  float T[PPT];   // in registers: the termination decision does not wait on shared memory
   uint32_t live = 0;   // bit p: pixel p is inside the image and not terminated
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     s_px[p][lane] = make_float4(0.f, 0.f, 0.f, 1.f);
+    T[p] = 1.f;
     last[p] = range.x;
     if (tx0 + pm.x(p) < cam.W && ty0 + pm.y(p) < cam.H) live |= 1u << p;
   }
@@ -852,10 +856,11 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
             if (!((ok >> p) & 1u)) continue;
             const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
             if (alpha < ALPHA_MIN || pw[p] > 0.f) continue;   // A11: skip if power > 0
-            float4 px = s_px[p][lane];
-            const float tn = __fmul_rn(px.w, __fsub_rn(1.f, alpha));
+            const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
             if (tn < T_MIN) { live &= ~(1u << p); continue; }
-            const float w = alpha * px.w;
+            const float w = alpha * T[p];
+            T[p] = tn;
+            float4 px = s_px[p][lane];
             px.x += c.x * w; px.y += c.y * w; px.z += c.z * w;
             px.w = tn;
             s_px[p][lane] = px;
