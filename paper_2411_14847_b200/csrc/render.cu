@@ -1335,6 +1335,12 @@ static bool tile_warp() {
   }();
   return v;
 }
+#ifndef TW_FWD_ORDER_SHIFT
+#define TW_FWD_ORDER_SHIFT 4   // forward launch order: list length in 16-entry buckets
+#endif
+#ifndef TW_BWD_ORDER_SHIFT
+#define TW_BWD_ORDER_SHIFT 3   // backward launch order: accepted entries in 8-entry buckets
+#endif
 #ifndef TW_FWD_MINB
 #define TW_FWD_MINB 32
 #endif
@@ -1364,7 +1370,7 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(accept, ntiles, capacity);
     if (tile_warp()) {
-      tile_order_kernel<5><<<1, 1024, 0, s>>>(cam, ranges, nullptr, acc.order);
+      tile_order_kernel<TW_FWD_ORDER_SHIFT><<<1, 1024, 0, s>>>(cam, ranges, nullptr, acc.order);
       launch_counted();
       render_fwd_tw_kernel<TW_FWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
                                                            box, bg, out_img, out_T, out_last, acc);
@@ -1439,7 +1445,7 @@ cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* r
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(const_cast<void*>(accept), ntiles, capacity);
     if (tile_warp()) {
-      tile_order_kernel<4><<<1, 1024, 0, s>>>(cam, ranges, acc.cnt, acc.order);
+      tile_order_kernel<TW_BWD_ORDER_SHIFT><<<1, 1024, 0, s>>>(cam, ranges, acc.cnt, acc.order);
       launch_counted();
       render_bwd_tw_kernel<TW_BWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg,
                                                            out_T, dL_dimg, acc, g2d);
