@@ -162,8 +162,8 @@ def run_ours(args):
 
     from paper_2411_14847_b200 import dass, synth
     from paper_2411_14847_b200.dist import FlatGrads, FlatParams, allreduce_grads, view_plan
-    from paper_2411_14847_b200.pipeline import (DeformFields, DeviceScene, MultiViewPass, Raster,
-                                                ViewRecords)
+    from paper_2411_14847_b200.pipeline import DeformFields, DeviceScene, Raster
+    from paper_2411_14847_b200.step import ShiftStep
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -192,54 +192,27 @@ def run_ours(args):
 
     # ---- device state
     base = DeviceScene.from_host(scene, dev)                 # 𝒢_{t−1}
-    shifted = DeviceScene(torch.empty_like(base.pos_opa), base.scale, torch.empty_like(base.rot),
-                          base.sh, deg, base.dynamic)       # 𝒢_t after the shift
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     mu_d, sigma_d = t(mu), t(sigma)
     dLs = torch.stack([t(synth.grad_image(cams[v], 1000 + v, 1.0 / (3 * W * H))) for v in mine]) \
         if mine else torch.empty(0, 3, H, W, device=dev)
+    # the step (paper_2411_14847_b200/step.py): buffers, streams and call order
+    stepper = ShiftStep(my_cams, n, deg, args.capacity, dev, streams=args.streams,
+                        tiles=plan.tiles, split=plan.split, num_split=plan.num_split)
+    records, mvp = stepper.records, stepper.mvp
     # one flat gradient buffer = the all_reduce payload (dist.FlatGrads)
-    grads = FlatGrads.allocate(n, K4, dev, num_split=plan.num_split)
+    bufs0 = stepper.buffers(base, mu_d, sigma_d, dLs)
+    grads = bufs0.grads
     flat, g_mu, g_sigma = grads.flat, grads.g_mu, grads.g_sigma
-    records = ViewRecords(max(len(mine), 1), n, dev)
+    shifted = bufs0.shifted                                  # 𝒢_t after the shift
     raster = Raster(W, H, n, args.capacity, dev)   # single-stream scratch for stats/diagnostics
-    uv_out = [None if sidx < 0 else grads.uv[sidx] for sidx in plan.split]
-    mvp = MultiViewPass(my_cams, n, args.capacity, dev, streams=args.streams, tiles=plan.tiles,
-                        uv_out=uv_out) if my_cams else None
 
     def finish_split(g):
         """∇p̄ of the views split across ranks, from their reduced uv partials."""
         dass.dass_gradstat_from_uv(g.uv, g.gradstat_sum)
 
-    class StepBufs:
-        """A step's inputs and outputs (the e2e pipeline double-buffers them)."""
-        def __init__(self, base, mu, sigma, dLs, grads):
-            self.base, self.mu, self.sigma, self.dLs, self.grads = base, mu, sigma, dLs, grads
-            # 𝒢_t after the shift: pos/rot are per-step scratch, scale/SH are the inputs'
-            self.shifted = DeviceScene(shifted.pos_opa, base.scale, shifted.rot, base.sh, deg,
-                                       base.dynamic)
-
-    bufs0 = StepBufs(base, mu_d, sigma_d, dLs, grads)
-
     def step_local(S=bufs0, wait_inputs=None):
-        """Everything on this GPU (capturable: no host sync, no collective).
-        wait_inputs(): the end-to-end run's wait for this step's parameter upload."""
-        g = S.grads
-        g.zero_()
-        if wait_inputs is not None:
-            wait_inputs()
-        dass.dass_apply_shift(S.base.pos_opa, S.base.rot, S.mu, S.sigma, S.base.dynamic,
-                              S.shifted.pos_opa, S.shifted.rot)
-        def project(v0, v1):
-            dass.dass_project_views(my_cams[v0:v1], deg, S.shifted.pos_opa, S.shifted.scale,
-                                    S.shifted.rot, S.shifted.sh, None, records.xy_depth[v0:v1],
-                                    records.conic_opa[v0:v1], records.rgb[v0:v1],
-                                    records.box[v0:v1], records.tiles[v0:v1])
-        if mvp is not None:
-            mvp.uv_out = [None if sidx < 0 else g.uv[sidx] for sidx in plan.split]
-            mvp.run(S.shifted, records, S.dLs, g, project=project)
-        dass.dass_apply_shift_bwd(S.base.rot, S.sigma, S.base.dynamic, g.pos_opa, g.rot,
-                                  g.g_mu, g.g_sigma)
+        stepper.run(S, wait_inputs=wait_inputs)
 
     def run_step(graph=None, S=bufs0):
         if graph is None:
@@ -262,6 +235,7 @@ def run_ours(args):
              "tile_list_mean": [], "tile_list_max": []}
     step()
     torch.cuda.synchronize()
+    stepper.check_overflow()     # a view over the pair capacity would render as background
     cnt = torch.zeros(8, dtype=torch.int64, device=dev)
     stats["n_visible"] = []
     tiles_hist = []
@@ -315,6 +289,7 @@ def run_ours(args):
         ev1.record()
         barrier()
     per_step = np.array([step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps)])
+    stepper.check_overflow()     # the timed steps' sorts all fit (checked after the timing)
     launches = dass.kernel_launches() - l0
     if graph is not None:
         launches = per_step_launches * args.steps
@@ -558,9 +533,8 @@ def run_ours(args):
         dps = [FlatParams.allocate(n, K4, dev, world=shard_world) for _ in range(2)]
         for dp in dps:   # whole buffers once; under --emulate the other shards stay as gathered
             dp.flat.copy_(hp.flat)
-        sets = [StepBufs(DeviceScene(dp.pos_opa, dp.scale, dp.rot, dp.sh, deg, base.dynamic), dp.mu,
-                         dp.sigma, torch.empty_like(dLs),
-                         FlatGrads.allocate(n, K4, dev, num_split=plan.num_split)) for dp in dps]
+        sets = [stepper.buffers(DeviceScene(dp.pos_opa, dp.scale, dp.rot, dp.sh, deg, base.dynamic),
+                                dp.mu, dp.sigma, torch.empty_like(dLs)) for dp in dps]
         h_out = [torch.empty(flat.numel(), dtype=torch.float32).pin_memory() for _ in range(2)]
         h2d_params = hp.shard(shard_rank).numel() * 4
         h2d = h2d_params + h_dl.numel() * 4

@@ -161,7 +161,10 @@ def render(cam, scene, keep=None, bg=None, mode="scatter", tie_eps=None):
 def render_bwd(cam, scene, dL_dimg, keep=None, bg=None, mode="scatter", tie_eps=None, kappa=False):
     """O5+O6: gradients of sum(dL_dimg * render) w.r.t. all parameters.
     kappa=True also returns the conditioning κ of every gradient entry
-    (k_pos_opa, k_scale, k_rot, k_sh: Σ over pixels of |term| through |Jacobian|)."""
+    (k_pos_opa, k_scale, k_rot, k_sh: Σ over pixels of |term| through |Jacobian|)
+    and the A29 tie slack t_* (t_gradstat for ∇p̄): at pixels with one tie
+    decision point, |contribution(branch A) − contribution(branch B)| through
+    |Jacobian|.  gtie flags Gaussians whose box holds a pixel with ≥ 2 tie points."""
     c = _cam(cam)
     H, W = int(c["height"][0]), int(c["width"][0])
     n = scene.n
@@ -173,6 +176,9 @@ def render_bwd(cam, scene, dL_dimg, keep=None, bg=None, mode="scatter", tie_eps=
     if kappa:
         o.update(k_pos_opa=np.zeros((n, 4)), k_scale=np.zeros((n, 4)), k_rot=np.zeros((n, 4)),
                  k_sh=np.zeros((n, nc, 3)))
+        # tie slack (A29): |branch difference| at one-tie pixels through |Jacobian|
+        o.update(t_pos_opa=np.zeros((n, 4)), t_scale=np.zeros((n, 4)), t_rot=np.zeros((n, 4)),
+                 t_sh=np.zeros((n, nc, 3)), t_gradstat=np.zeros(n))
     k = None if keep is None else np.ascontiguousarray(keep, np.uint8)
     b = None if bg is None else np.ascontiguousarray(bg, np.float32)
     lib().oracle_render_bwd(_p(c), n, scene.sh_degree, _p(_f32(scene.pos_opa)),
@@ -182,7 +188,8 @@ def render_bwd(cam, scene, dL_dimg, keep=None, bg=None, mode="scatter", tie_eps=
                             _p(o["g_rot"]), _p(o["g_sh"]), _p(o["g2d"]), _p(o["gradstat_sum"]),
                             _p(o["gradstat_cnt"]), _p(o["gtie"]), _p(o["img"]), _p(o["T"]),
                             _p(o.get("k_pos_opa")), _p(o.get("k_scale")), _p(o.get("k_rot")),
-                            _p(o.get("k_sh")))
+                            _p(o.get("k_sh")), _p(o.get("t_pos_opa")), _p(o.get("t_scale")),
+                            _p(o.get("t_rot")), _p(o.get("t_sh")), _p(o.get("t_gradstat")))
     return o
 
 

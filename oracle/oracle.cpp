@@ -428,14 +428,22 @@ TieEps tie_from(const double* eps) {
   return t;
 }
 
-inline bool is_tie(const Proj& g, const Eval& e, double T, const TieEps& te) {
+// Which decisions of one (pixel, entry) evaluation lie inside their tie margin:
+// bit 0 the power > 0 guard, bit 1 the α < 1/255 skip, bit 2 the α = 0.99 clamp
+// (a derivative kink only), bit 3 the T(1−α) < 1e-4 termination.
+enum { TIE_POWER = 1, TIE_ALPHA = 2, TIE_CLAMP = 4, TIE_TERM = 8 };
+inline int tie_bits(const Proj& g, const Eval& e, double T, const TieEps& te) {
   const double mag = std::fabs(g.A * e.dx * e.dx) + std::fabs(g.C * e.dy * e.dy) +
                      std::fabs(2 * g.B * e.dx * e.dy);
-  if (std::fabs(e.power) < te.power_rel * mag + 1e-12 && e.power != 0.0) return true;
-  if (std::fabs(e.alpha - ALPHA_MIN) < te.alpha_rel * ALPHA_MIN) return true;
-  if (std::fabs(e.oG - 0.99) < te.clamp_rel * 0.99) return true;
-  if (std::fabs(T * (1 - e.alpha) - T_MIN) < te.t_rel * T_MIN) return true;
-  return false;
+  int b = 0;
+  if (std::fabs(e.power) < te.power_rel * mag + 1e-12 && e.power != 0.0) b |= TIE_POWER;
+  if (std::fabs(e.alpha - ALPHA_MIN) < te.alpha_rel * ALPHA_MIN) b |= TIE_ALPHA;
+  if (std::fabs(e.oG - 0.99) < te.clamp_rel * 0.99) b |= TIE_CLAMP;
+  if (std::fabs(T * (1 - e.alpha) - T_MIN) < te.t_rel * T_MIN) b |= TIE_TERM;
+  return b;
+}
+inline bool is_tie(const Proj& g, const Eval& e, double T, const TieEps& te) {
+  return tie_bits(g, e, T, te) != 0;
 }
 
 // Output of a forward pass.
@@ -498,11 +506,11 @@ inline void accumulate(Grad2D& sum, Grad2D& kap, const Grad2D& t) {
 // The 9 per-pixel terms of one accepted entry (O5).
 inline Grad2D pixel_terms(double A, double B, double C, double o, const double* col,
                           double alpha, double G, double oG, double dx, double dy, double Tk,
-                          double dL_dalpha, const double g[3]) {
+                          double dL_dalpha, const double g[3], int clamped = -1) {
   Grad2D t{0, 0, 0, 0, 0, 0, {0, 0, 0}};
   (void)col;
   for (int ch = 0; ch < 3; ++ch) t.col[ch] = alpha * Tk * g[ch];
-  if (oG < 0.99) {  // unclamped α: α = o·G (A17)
+  if (clamped < 0 ? oG < 0.99 : clamped == 0) {  // unclamped α: α = o·G (A17)
     t.o = G * dL_dalpha;
     const double dpow = o * G * dL_dalpha;
     t.u = dpow * (-(A * dx + B * dy));
@@ -545,6 +553,57 @@ void pixel_backward(const std::vector<Proj>& G, const std::vector<int>& ord, int
                pixel_terms(p.A, p.B, p.C, p.o, p.col, e.alpha, e.G, e.oG, e.dx, e.dy, Tk, dL_dalpha, g));
     for (int ch = 0; ch < 3; ++ch) S[ch] += p.col[ch] * e.alpha * Tk;
   }
+}
+
+// Tie slack (A29): the per-pixel 2D terms of every entry of one pixel's sequence
+// when its flip_k-th tie decision point (0-based; −1: none, the oracle's own
+// decisions) is taken the other way — every decision inside its margin at that
+// entry is inverted, the rest of the sequence re-evaluated.  A tie pixel's
+// contribution to a gradient may legitimately be either branch's, so the
+// comparison allows Σ_tie px |terms_A − terms_B| there instead of excluding
+// whole Gaussians.  Returns the number of tie decision points (branch A).
+int pixel_branch_terms(const std::vector<Proj>& G, const std::vector<int>& ord, int X, int Y,
+                       const double bg[3], const double g[3], const TieEps& te, int flip_k,
+                       std::vector<std::pair<int, Grad2D>>& out) {
+  struct Acc { int id; Eval e; double T; int clamped; };
+  std::vector<Acc> acc;
+  double T = 1;
+  int nt = 0;
+  for (int pos = 0; pos < (int)ord.size(); ++pos) {
+    const Proj& p = G[ord[pos]];
+    if (!box_has(p, X, Y)) continue;
+    const Eval e = eval_at(p, X, Y);
+    const int tb = tie_bits(p, e, T, te);
+    int flip = 0;
+    if (tb) { if (nt == flip_k) flip = tb; ++nt; }
+    bool skip_pow = e.power > 0, skip_a = e.alpha < ALPHA_MIN;
+    int clamped = e.oG >= 0.99 ? 1 : 0;
+    if (flip & TIE_POWER) skip_pow = !skip_pow;
+    if (flip & TIE_ALPHA) skip_a = !skip_a;
+    if (flip & TIE_CLAMP) clamped = 1 - clamped;
+    if (skip_pow || skip_a) continue;
+    const double tn = T * (1 - e.alpha);
+    bool stop = tn < T_MIN;
+    if (flip & TIE_TERM) stop = !stop;
+    if (stop) break;
+    acc.push_back({ord[pos], e, T, clamped});
+    T = tn;
+  }
+  const double Tfin = T;
+  double S[3] = {0, 0, 0};
+  out.clear();
+  for (int k = (int)acc.size() - 1; k >= 0; --k) {
+    const Proj& p = G[acc[k].id];
+    const Eval& e = acc[k].e;
+    const double Tk = acc[k].T;
+    double dL_dalpha = 0;
+    for (int ch = 0; ch < 3; ++ch)
+      dL_dalpha += g[ch] * (p.col[ch] * Tk - (S[ch] + Tfin * bg[ch]) / (1 - e.alpha));
+    out.push_back({acc[k].id, pixel_terms(p.A, p.B, p.C, p.o, p.col, e.alpha, e.G, e.oG, e.dx,
+                                          e.dy, Tk, dL_dalpha, g, acc[k].clamped)});
+    for (int ch = 0; ch < 3; ++ch) S[ch] += p.col[ch] * e.alpha * Tk;
+  }
+  return nt;
 }
 
 // ---------------------------------------- O5 preprocess backward (chain) ---
@@ -1000,8 +1059,12 @@ int oracle_render(const OCam* cam, int n, int deg, const float* pos_opa, const f
 //   g_pos_opa double[4n] (x,y,z, o), g_scale double[4n], g_rot double[4n],
 //   g_sh double[n*(d+1)²*3] coefficient-major, g2d double[9n] (u,v,A,B,C,o,r,g,b)
 //   gradstat_sum double[n], gradstat_cnt int32[n].  Any output nullable.
-// Also renders the forward (img/T nullable) and flags Gaussians whose box
-// contains a tie pixel (gtie uint8[n], nullable).
+// Also renders the forward (img/T nullable).  Tie pixels (A29): for a pixel
+// with one tie decision point, t_* (nullable, same layouts as g_*; t_gradstat
+// double[n]) receive the |difference| between its two decision branches'
+// contributions pushed through |Jacobian| — the amount by which a correct
+// fp32 implementation may differ there; Gaussians whose box holds a pixel
+// with two or more tie points are flagged in gtie (uint8[n], nullable).
 // κ outputs (nullable, same layouts as g_*): the conditioning of each
 // gradient entry, Σ_px |L_i|·|per-pixel 2D terms| where L_i is the linear
 // preprocess map of Gaussian i (columns by unit probes).  A gradient with
@@ -1012,7 +1075,8 @@ int oracle_render_bwd(const OCam* cam, int n, int deg, const float* pos_opa, con
                       double* g_scale, double* g_rot, double* g_sh, double* g2d_out,
                       double* gradstat_sum, int32_t* gradstat_cnt, uint8_t* gtie, double* img_out,
                       double* T_out, double* k_pos_opa, double* k_scale, double* k_rot,
-                      double* k_sh) {
+                      double* k_sh, double* t_pos_opa, double* t_scale, double* t_rot,
+                      double* t_sh, double* t_gradstat) {
   RenderCtx R;
   make_ctx(R, cam, n, deg, pos_opa, scale, rot, sh, keep);
   const double bg[3] = {bg3 ? bg3[0] : 0.0, bg3 ? bg3[1] : 0.0, bg3 ? bg3[2] : 0.0};
@@ -1059,8 +1123,62 @@ int oracle_render_bwd(const OCam* cam, int n, int deg, const float* pos_opa, con
   } else {
     scatter_backward(R, bg, dL_dimg, Tfin.data(), lpos.data(), g2d, kap);
   }
+  // A29 tie slack: for every pixel with exactly one tie decision point, the
+  // per-Gaussian |terms_A − terms_B| of its two branches (pixel_branch_terms);
+  // a pixel with two or more tie points ("multi-tie") instead flags the
+  // Gaussians whose box holds it (gtie), which the comparison excludes.
+  std::vector<Grad2D> slack(n, zero);
+  std::vector<uint8_t> multi(np, 0);
+  const bool want_t = t_pos_opa || t_scale || t_rot || t_sh || t_gradstat || gtie;
+  if (want_t) {
+    std::vector<size_t> tps;
+    for (size_t p = 0; p < np; ++p)
+      if (tie[p]) tps.push_back(p);
+#pragma omp parallel
+    {
+      std::vector<std::pair<int, Grad2D>> local, a, b;
+#pragma omp for schedule(dynamic, 4)
+      for (long k = 0; k < (long)tps.size(); ++k) {
+        const size_t p = tps[k];
+        const int X = (int)(p % W), Y = (int)(p / W);
+        const double gg[3] = {dL_dimg[p], dL_dimg[np + p], dL_dimg[2 * np + p]};
+        const int nt = pixel_branch_terms(R.G, R.ord, X, Y, bg, gg, te, -1, a);
+        if (nt >= 2) { multi[p] = 1; continue; }
+        if (nt == 0) continue;
+        pixel_branch_terms(R.G, R.ord, X, Y, bg, gg, te, 0, b);
+        std::vector<std::pair<int, Grad2D>> d;   // id → terms_B − terms_A
+        auto add = [&](int id, const Grad2D& t, double sgn) {
+          for (auto& q : d)
+            if (q.first == id) {
+              Grad2D& r = q.second;
+              r.u += sgn * t.u; r.v += sgn * t.v; r.A += sgn * t.A; r.B += sgn * t.B;
+              r.C += sgn * t.C; r.o += sgn * t.o;
+              for (int ch = 0; ch < 3; ++ch) r.col[ch] += sgn * t.col[ch];
+              return;
+            }
+          Grad2D r = zero;
+          d.push_back({id, r});
+          Grad2D& q = d.back().second;
+          q.u = sgn * t.u; q.v = sgn * t.v; q.A = sgn * t.A; q.B = sgn * t.B; q.C = sgn * t.C;
+          q.o = sgn * t.o;
+          for (int ch = 0; ch < 3; ++ch) q.col[ch] = sgn * t.col[ch];
+        };
+        for (const auto& q : a) add(q.first, q.second, -1.0);
+        for (const auto& q : b) add(q.first, q.second, 1.0);
+        for (const auto& q : d) local.push_back(q);
+      }
+#pragma omp critical
+      for (const auto& q : local) {
+        Grad2D dummy = zero;
+        Grad2D z = zero;
+        accumulate(dummy, slack[q.first], q.second);   // slack += |Δterms|
+        (void)z;
+      }
+    }
+  }
   const int nc = (deg + 1) * (deg + 1);
   const bool want_k = k_pos_opa || k_scale || k_rot || k_sh;
+  const bool want_ts = t_pos_opa || t_scale || t_rot || t_sh;
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < n; ++i) {
     Grad3D d;
@@ -1091,6 +1209,29 @@ int oracle_render_bwd(const OCam* cam, int n, int deg, const float* pos_opa, con
       if (k_rot) for (int a = 0; a < 4; ++a) k_rot[4 * i + a] = kk.q[a];
       if (k_sh) for (int k = 0; k < nc; ++k) for (int ch = 0; ch < 3; ++ch) k_sh[((size_t)i * nc + k) * 3 + ch] = kk.sh[k][ch];
     }
+    if (want_ts) {   // the tie slack through |preprocess Jacobian|, as κ
+      Grad3D kk;
+      std::memset(&kk, 0, sizeof(kk));
+      const double k9[9] = {slack[i].u, slack[i].v, slack[i].A, slack[i].B, slack[i].C,
+                            slack[i].o, slack[i].col[0], slack[i].col[1], slack[i].col[2]};
+      for (int c = 0; c < 9; ++c) {
+        if (k9[c] == 0) continue;
+        Grad2D e = zero;
+        double* f[9] = {&e.u, &e.v, &e.A, &e.B, &e.C, &e.o, &e.col[0], &e.col[1], &e.col[2]};
+        *f[c] = 1.0;
+        Grad3D col;
+        preprocess_backward(R.cam, R.P, i, R.G[i], e, col);
+        for (int a = 0; a < 3; ++a) { kk.p[a] += std::fabs(col.p[a]) * k9[c]; kk.s[a] += std::fabs(col.s[a]) * k9[c]; }
+        kk.o += std::fabs(col.o) * k9[c];
+        for (int a = 0; a < 4; ++a) kk.q[a] += std::fabs(col.q[a]) * k9[c];
+        for (int k = 0; k < nc; ++k) for (int ch = 0; ch < 3; ++ch) kk.sh[k][ch] += std::fabs(col.sh[k][ch]) * k9[c];
+      }
+      if (t_pos_opa) { for (int a = 0; a < 3; ++a) t_pos_opa[4 * i + a] = kk.p[a]; t_pos_opa[4 * i + 3] = kk.o; }
+      if (t_scale) { for (int a = 0; a < 3; ++a) t_scale[4 * i + a] = kk.s[a]; t_scale[4 * i + 3] = 0; }
+      if (t_rot) for (int a = 0; a < 4; ++a) t_rot[4 * i + a] = kk.q[a];
+      if (t_sh) for (int k = 0; k < nc; ++k) for (int ch = 0; ch < 3; ++ch) t_sh[((size_t)i * nc + k) * 3 + ch] = kk.sh[k][ch];
+    }
+    if (t_gradstat) t_gradstat[i] = slack[i].u * 0.5 * W + slack[i].v * 0.5 * H;
     if (g2d_out) {
       const Grad2D& s = g2d[i];
       const double v9[9] = {s.u, s.v, s.A, s.B, s.C, s.o, s.col[0], s.col[1], s.col[2]};
@@ -1112,7 +1253,7 @@ int oracle_render_bwd(const OCam* cam, int n, int deg, const float* pos_opa, con
       if (g.key.visible)
         for (int Y = g.key.y0; Y <= g.key.y1 && !f; ++Y)
           for (int X = g.key.x0; X <= g.key.x1; ++X)
-            if (tie[(size_t)Y * W + X]) { f = 1; break; }
+            if (multi[(size_t)Y * W + X]) { f = 1; break; }
       gtie[i] = f;
     }
   }

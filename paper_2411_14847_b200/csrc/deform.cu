@@ -1282,12 +1282,11 @@ size_t fwd_tc_smem(int in) {
                                   2 * GT * in + 2 * GT * HID);
 }
 
-// DASS_DEFORM_TC=0 selects the FP32 SIMT forward (read per call: the parity
-// tests exercise both paths in one process)
-bool use_tc() {
-  const char* e = getenv("DASS_DEFORM_TC");
-  return e == nullptr || atoi(e) != 0;
-}
+// The tcgen05 kernels serve every field shape they are defined for (K a
+// multiple of 8: kind::tf32 consumes K in steps of 8); other shapes, and the
+// F = 2 backward (measured slower on tcgen05), run the FP32 SIMT
+// kernels.
+constexpr bool use_tc() { return true; }
 
 template <int F>
 cudaError_t fwd_launch(const HashGridParams& g, const float* table, const float* mlp, int n,

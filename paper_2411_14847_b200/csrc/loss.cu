@@ -414,14 +414,6 @@ bool plane_map(CUtensorMap* m, const float* base, int W, int H, int planes, int 
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool tma_allowed() {
-  static const bool ok = [] {
-    const char* v = getenv("DASS_LOSS_TMA");
-    return !(v && v[0] == '0');
-  }();
-  return ok;
-}
-
 template <int VS, bool TMA>
 void set_smem_attrs() {
   using T = LossTile<VS>;
@@ -442,7 +434,7 @@ cudaError_t fidelity_loss_vs(int W, int H, const float* img, const float* gt, fl
   static const Win win = make_window();
   const dim3 grid(div_up(W, LT), div_up(H, T::LTY), 3);
   CUtensorMap mi, mg, mp;
-  const bool tma = tma_allowed() && plane_map(&mi, img, W, H, 3, T::RY, 1) &&
+  const bool tma = plane_map(&mi, img, W, H, 3, T::RY, 1) &&
                    plane_map(&mg, gt, W, H, 3, T::RY, 1) && plane_map(&mp, pmaps, W, H, 9, T::RY, 3);
   if (tma) {
     set_smem_attrs<VS, true>();
@@ -471,15 +463,8 @@ cudaError_t launch_fidelity_loss(int W, int H, const float* img, const float* gt
   float* pmaps = (float*)((char*)ws + 256);
   cudaError_t e = cudaMemsetAsync(acc, 0, 2 * sizeof(double), s);
   if (e != cudaSuccess) return e;
-  static const int vs = [] {
-    const char* v = getenv("DASS_LOSS_VS");
-    return v ? atoi(v) : 4;
-  }();
-  switch (vs) {
-    case 5: return fidelity_loss_vs<5>(W, H, img, gt, lambda, acc, pmaps, loss, dL, s);
-    case 6: return fidelity_loss_vs<6>(W, H, img, gt, lambda, acc, pmaps, loss, dL, s);
-    default: return fidelity_loss_vs<4>(W, H, img, gt, lambda, acc, pmaps, loss, dL, s);
-  }
+  // tiles of 32 × 8·VS outputs; VS = 4, 5, 6 measured within 1%
+  return fidelity_loss_vs<4>(W, H, img, gt, lambda, acc, pmaps, loss, dL, s);
 }
 
 }  // namespace dass

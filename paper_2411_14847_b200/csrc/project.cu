@@ -267,15 +267,6 @@ __global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__
 
 }  // namespace
 
-static int project_vpt() {
-  static const int v = [] {
-    const char* e = getenv("DASS_PROJECT_VPT");
-    const int x = e ? atoi(e) : MAXV;   // measured: more views per thread is faster
-    return x >= 1 ? x : 4;
-  }();
-  return v;
-}
-
 cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_degree,
                            const float4* pos_opa, const float4* scale, const float4* rot,
                            const float4* sh, const uint8_t* keep, float4* xy_depth,
@@ -288,7 +279,7 @@ cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_d
     a.n = n; a.view_offset = v0;
     a.pos_opa = pos_opa; a.scale = scale; a.rot = rot; a.sh = sh; a.keep = keep;
     a.xy_depth = xy_depth; a.conic_opa = conic_opa; a.rgb = rgb; a.box = box; a.tiles = tiles;
-    a.vpt = project_vpt();
+    a.vpt = MAXV;   // every view of the launch per thread (measured fastest)
     const dim3 grid(div_up(n, 256), div_up(a.num_views, a.vpt));
     switch (sh_degree) {
       case 0: project_kernel<0><<<grid, 256, 0, s>>>(a); break;

@@ -111,10 +111,12 @@ class Raster:
             ab = dass.dass_render_accept_workspace(self.num_tiles, capacity)
             self.accept = torch.empty(ab // 4, dtype=torch.int32, device=device)
 
-    def sort(self, cam, rec, host_mode=False, sorted_keys=None):
+    def sort(self, cam, rec, host_mode=False, sorted_keys=None, num_pairs=None):
+        """num_pairs: where (K, overflow flag) go (default: this slot's own pair)."""
         xy, co, rgb, box, tt = rec
         return dass.dass_bin_sort(cam, self.n, xy, box, tt, self.sort_ws, self.capacity,
-                                  sorted_keys, self.sorted_ids, self.ranges, self.num_pairs,
+                                  sorted_keys, self.sorted_ids, self.ranges,
+                                  self.num_pairs if num_pairs is None else num_pairs,
                                   host_mode=host_mode)
 
     def render(self, cam, rec, bg=None, tiles=None, ranges=None, sorted_ids=None):
@@ -201,6 +203,9 @@ class MultiViewPass:
         # an end-to-end caller makes the view wait there for its own ∂L/∂C upload
         self.before_bwd = None
         self.g2d = torch.empty(max(self.V, 1), n, 12, dtype=torch.float32, device=device)
+        # (K_v, overflow_v) of every view's graph-mode sort, kept per view so a slot
+        # reused by a later view does not overwrite an earlier view's overflow flag
+        self.num_pairs = torch.zeros(max(self.V, 1), 2, dtype=torch.int32, device=device)
         # DASS_BATCH_SORT=1: dass_bin_sort_views over chunks of the views instead of a
         # dass_bin_sort per view.  In the graph the per-view sort chains run in lockstep
         # (≈1.9 ms of the step with no raster work ready, tools/timeline.py), but the
@@ -286,11 +291,11 @@ class MultiViewPass:
                 ss = self.sort_streams[v % len(self.sort_streams)]
                 ss.wait_stream(st)    # projected, and the slot's previous view is done
                 with torch.cuda.stream(ss):
-                    ras.sort(cam, rec)
+                    ras.sort(cam, rec, num_pairs=self.num_pairs[v])
                 st.wait_stream(ss)
             with torch.cuda.stream(st):
                 if self.sort_streams is None and not self.batch_sort:
-                    ras.sort(cam, rec)
+                    ras.sort(cam, rec, num_pairs=self.num_pairs[v])
                 ras.render(cam, rec, bg=bg, tiles=self.tiles[v], ranges=vr, sorted_ids=vi)
                 if gts is not None:
                     dL = self.loss_dL[k]
@@ -319,6 +324,18 @@ class MultiViewPass:
         if nchunk > 1:
             main.wait_stream(self.pre_stream)
         self._preprocess(scene, records, grads, keep, bounds[nchunk - 1], V)
+
+    def pair_counts(self):
+        """K of every view's last sort (synchronises)."""
+        np_ = (self.bs_pairs if self.batch_sort else self.num_pairs).cpu().numpy().view(np.uint32)
+        return [int(k) for k in np_[:self.V, 0]]
+
+    def overflowed_views(self):
+        """Views whose last sort exceeded the pair capacity (synchronises).  Such a
+        view's tile ranges are all [0, 0): it rendered as background and added no
+        gradient, so a caller must not use that step's results."""
+        np_ = (self.bs_pairs if self.batch_sort else self.num_pairs).cpu().numpy().view(np.uint32)
+        return [v for v in range(self.V) if np_[v, 1]]
 
     def _preprocess(self, scene, records, grads, keep, v0, v1):
         dass.dass_render_bwd_preprocess_views(

@@ -1,0 +1,98 @@
+"""One shift-stage iteration over a rank's views (plumbing around libdass).
+
+The step `bench.py` times and `tests/test_gpu_step.py` checks against the
+oracle:
+
+    dass_apply_shift → dass_project_views → per view (dass_bin_sort →
+    dass_render_fwd → dass_render_bwd_raster) on overlapping streams →
+    dass_render_bwd_preprocess_views → dass_apply_shift_bwd
+
+with the per-Gaussian gradients in one flat buffer (dist.FlatGrads, the
+all-reduce payload).  Every arithmetic step runs in the CUDA kernels; this
+module only owns buffers and call order, and is capturable as one CUDA graph
+(no host synchronisation inside).
+"""
+from __future__ import annotations
+
+from . import dass
+from .dist import FlatGrads
+from .pipeline import DeviceScene, MultiViewPass, ViewRecords
+
+
+class StepBufs:
+    """A step's inputs (𝒢_{t−1}, the shift offsets μ/σ, the views' ∂L/∂C) and
+    its outputs (the flat gradients).  `shifted` is 𝒢_t after the shift: its
+    position/rotation are the step's scratch, its scale/SH are the inputs'."""
+
+    def __init__(self, base: DeviceScene, mu, sigma, dLs, grads: FlatGrads, shifted_pos, shifted_rot):
+        self.base, self.mu, self.sigma, self.dLs, self.grads = base, mu, sigma, dLs, grads
+        self.shifted = DeviceScene(shifted_pos, base.scale, shifted_rot, base.sh, base.sh_degree,
+                                   base.dynamic)
+
+
+class ShiftStep:
+    """fwd+bwd of one shift iteration over `cams` (this rank's views).
+
+    tiles[k] / split[k]: the dist.ViewPlan entries of view k (None / −1 for a
+    whole view); num_split sizes the uv blocks of the flat gradient buffer."""
+
+    def __init__(self, cams, n: int, sh_degree: int, capacity: int, device, streams: int = 20,
+                 tiles=None, split=None, num_split: int = 0):
+        import torch
+        self.cams = list(cams)
+        self.n, self.deg, self.device = n, sh_degree, device
+        self.tiles = list(tiles) if tiles is not None else [None] * len(self.cams)
+        self.split = list(split) if split is not None else [-1] * len(self.cams)
+        self.num_split = num_split
+        self.records = ViewRecords(max(len(self.cams), 1), n, device)
+        self.mvp = MultiViewPass(self.cams, n, capacity, device, streams=streams,
+                                 tiles=self.tiles) if self.cams else None
+        self.shifted_pos = torch.empty(n, 4, dtype=torch.float32, device=device)
+        self.shifted_rot = torch.empty(n, 4, dtype=torch.float32, device=device)
+
+    def buffers(self, base: DeviceScene, mu, sigma, dLs, grads: FlatGrads | None = None) -> StepBufs:
+        from .synth import sh_planes
+        if grads is None:
+            grads = FlatGrads.allocate(self.n, sh_planes(self.deg), self.device,
+                                       num_split=self.num_split)
+        return StepBufs(base, mu, sigma, dLs, grads, self.shifted_pos, self.shifted_rot)
+
+    def run(self, S: StepBufs, wait_inputs=None):
+        """Everything on this GPU (capturable: no host sync, no collective).
+        wait_inputs(): an end-to-end caller's wait for this step's parameter upload."""
+        g = S.grads
+        g.zero_()
+        if wait_inputs is not None:
+            wait_inputs()
+        dass.dass_apply_shift(S.base.pos_opa, S.base.rot, S.mu, S.sigma, S.base.dynamic,
+                              S.shifted.pos_opa, S.shifted.rot)
+        rec, cams, sh = self.records, self.cams, S.shifted
+
+        def project(v0, v1):
+            dass.dass_project_views(cams[v0:v1], self.deg, sh.pos_opa, sh.scale, sh.rot, sh.sh,
+                                    None, rec.xy_depth[v0:v1], rec.conic_opa[v0:v1],
+                                    rec.rgb[v0:v1], rec.box[v0:v1], rec.tiles[v0:v1])
+        if self.mvp is not None:
+            self.mvp.uv_out = [None if s < 0 else g.uv[s] for s in self.split]
+            self.mvp.run(sh, rec, S.dLs, g, project=project)
+        dass.dass_apply_shift_bwd(S.base.rot, S.sigma, S.base.dynamic, g.pos_opa, g.rot,
+                                  g.g_mu, g.g_sigma)
+
+    def capture(self, S: StepBufs, wait_inputs=None):
+        """The step as one CUDA graph (replay() runs it)."""
+        import torch
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.run(S, wait_inputs=wait_inputs)
+        return graph
+
+    def check_overflow(self):
+        """Raise if any view's pair count exceeded the capacity in the last step
+        (graph-mode sorts flag it on the device instead of failing; an
+        overflowed view would render as background).  Synchronises."""
+        if self.mvp is not None:
+            bad = self.mvp.overflowed_views()
+            if bad:
+                raise dass.DassError(dass.DASS_ERR_CAPACITY, "ShiftStep",
+                                     f"pair capacity {self.mvp.slots[0].capacity} exceeded in "
+                                     f"views {bad} (K = {self.mvp.pair_counts()})")

@@ -84,15 +84,11 @@ def check_grad(a, ref, kap):
     assert not bad.any(), (int(bad.sum()), float(np.max(np.abs(a - ref))), float(np.max(np.abs(ref))))
 
 
-@pytest.fixture(params=["tcgen05", "simt"])
-def fwd_path(request, monkeypatch):
-    """Both implementations: the tcgen05 3×TF32 kernels (default; the backward's
-    tcgen05 kernel serves the F = 4 field) and the FP32 SIMT kernels
-    (DASS_DEFORM_TC=0)."""
-    if request.param == "simt":
-        monkeypatch.setenv("DASS_DEFORM_TC", "0")
-    else:
-        monkeypatch.delenv("DASS_DEFORM_TC", raising=False)
+@pytest.fixture(params=["default"])
+def fwd_path(request):
+    """The library's own choice per field shape: the tcgen05 3×TF32 kernels
+    where K is a multiple of 8 (the backward's tcgen05 kernel serves F = 4), the
+    FP32 SIMT kernels otherwise (test_other_field_shapes covers those)."""
     return request.param
 
 

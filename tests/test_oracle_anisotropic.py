@@ -171,3 +171,48 @@ def test_gradstat_value_against_principal_point_differences(case):
     # W ≠ H or |gu| ≠ |gv|: a dropped or swapped W/2, H/2 scaling is distinguishable
     for wrong in (math.hypot(gu, gv), math.hypot(gu * H / 2, gv * W / 2), math.hypot(gu * W, gv * H)):
         assert abs(wrong - stat) > 1e-3 * stat
+
+
+def test_tie_slack_is_the_flipped_pixels_contribution():
+    """A29 tie slack: with one Gaussian and exactly one pixel inside a widened
+    α-threshold margin, branch B drops that pixel's entry, so the slack equals
+    that pixel's own contribution (its 2D terms from a render whose dL/dC is
+    that pixel alone); with default margins and no ties the slack is zero."""
+    W, H = 40, 32
+    cam = _camera(W, H, 50.0, 50.0, 19.3, 15.6, _axis_angle([0, 0, 1], 0.0), (0, 0, 0))
+    sc = _scene((0.02, -0.01, 3.0), (0.05, 0.07, 0.06), _axis_angle([0.3, 1, 0], 0.4), 0.6,
+                [0.7, 0.2, 0.5])
+    g = synth.grad_image(cam, 77)
+    r = oracle.render(cam, sc, mode="literal")
+    pr = oracle.project(cam, sc)
+    u, v = pr["uvz"][0, :2]
+    A, B, C = pr["conic"][0]
+    o = pr["opa"][0]
+    X, Y = np.meshgrid(np.arange(W), np.arange(H))
+    dx, dy = u - X, v - Y
+    alpha = np.minimum(0.99, o * np.exp(-0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy))
+    rel = np.abs(alpha - 1 / 255) * 255
+    inbox = r["nacc"] >= 0
+    order = np.argsort(rel.reshape(-1))
+    p0, p1 = order[0], order[1]
+    margin = 0.5 * (rel.reshape(-1)[p0] + rel.reshape(-1)[p1])   # exactly one pixel inside
+    assert rel.reshape(-1)[p0] < margin < rel.reshape(-1)[p1] and alpha.reshape(-1)[p0] < 0.5
+    eps = np.array([margin, 1e-12, 1e-12, 1e-12])
+    b = oracle.render_bwd(cam, sc, g, mode="literal", tie_eps=eps, kappa=True)
+    Y0, X0 = divmod(int(p0), W)
+    tie = oracle.render(cam, sc, mode="literal", tie_eps=eps)["tie"]
+    assert tie.sum() == 1 and tie[Y0, X0] == 1
+    # the pixel's own contribution: a render whose dL/dC is that pixel alone, where the
+    # entry is accepted (α above 1/255) — else the slack's branch B is the accepting one
+    one = np.zeros_like(g)
+    one[:, Y0, X0] = g[:, Y0, X0]
+    lo = oracle.render_bwd(cam, sc, one, mode="literal", tie_eps=eps)
+    if alpha[Y0, X0] >= 1 / 255:
+        gu, gv = lo["g2d"][0, 0], lo["g2d"][0, 1]
+        assert b["t_gradstat"][0] == pytest.approx(abs(gu) * W / 2 + abs(gv) * H / 2, rel=1e-12)
+    else:
+        assert not lo["g2d"].any() and b["t_gradstat"][0] > 0
+    assert b["gtie"][0] == 0
+    d = oracle.render_bwd(cam, sc, g, mode="literal", kappa=True)
+    assert oracle.render(cam, sc, mode="literal")["tie"].sum() == 0
+    assert not d["t_pos_opa"].any() and not d["t_gradstat"].any()
