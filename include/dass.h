@@ -47,7 +47,13 @@
  *    Gradients use the identical layout (g_pos_opa.w = dL/do).
  *  Per-view projected records (outputs of dass_project):
  *    xy_depth  float4[N]  u, v (pixels), z (camera-frame depth), 0
- *    conic_opa float4[N]  A, B, C (inverse 2D covariance), o_eff
+ *    conic_opa float4[N]  A, β, γ, o_eff: the inverse 2D covariance
+ *                         K = [[A, B], [B, C]] in Cholesky form, B = A·β,
+ *                         C = γ + A·β² (β = −Σ'_xy/Σ'_yy, γ = 1/Σ'_yy, from
+ *                         the fp64 Σ', rounded once), so the per-pixel power
+ *                         −½(A dx² + 2B dx dy + C dy²) = −[(s dx + sβ dy)² +
+ *                         (g dy)²], s = √(A/2), g = √(γ/2), is minus a sum of
+ *                         squares (no cancellation for elongated splats)
  *    rgb       float4[N]  r, g, b (clamped ≥ 0), clamp bits (float 0..7,
  *                         bit ch set when channel ch was clamped)
  *    box       uint32[2N] per Gaussian {x0 | x1<<16, y0 | y1<<16}; a culled
@@ -69,7 +75,7 @@ extern "C" {
 #endif
 
 #define DASS_TILE 16
-#define DASS_ABI_VERSION 1
+#define DASS_ABI_VERSION 2
 
 typedef enum dass_status {
   DASS_OK = 0,
@@ -175,7 +181,8 @@ int dass_apply_shift_bwd(int32_t n, const float* rot, const float* sigma,
  *      (clamped in float before conversion to int); visible iff x0 ≤ x1,
  *      y0 ≤ y1 and o_eff ≥ 1/255 (A05, A10);
  *      tiles_touched = (x1/16 − x0/16 + 1)·(y1/16 − y0/16 + 1).
- *  The conic is (A, B, C) = (c/det, −b/det, a/det).  Colour (fast math
+ *  The conic record is (A, β, γ) = (c/det, −b/c, 1/c), i.e. the conic
+ *  (c, −b, a)/det of Eq. 7 in Cholesky form (see the layout above).  Colour (fast math
  *  allowed): d = (p − c_cam)/‖p − c_cam‖, col = Σ_k Y_k(d)·sh_k + 0.5 with the
  *  real SH basis of degree ≤ 3 listed in DESIGN.md (A14); a channel < 0 sets
  *  its clamp bit and is clamped to 0.
@@ -219,7 +226,8 @@ int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n,
  *    stream once, stores K, and returns DASS_ERR_CAPACITY if K > capacity.
  *    Null = GRAPH MODE: no synchronisation (capturable in a CUDA graph); the
  *    caller reads num_pairs_dev later.
- * Requires pair_capacity < 2^32 and n < 2^31.
+ * Requires 0 ≤ pair_capacity < 2^30 and 0 ≤ n < 2^30 (the onesweep
+ * look-back packs counts into 30 bits).
  * ------------------------------------------------------------------------- */
 int dass_bin_sort_workspace(int32_t n, int32_t num_tiles,
                             int64_t pair_capacity, size_t* bytes);
@@ -259,7 +267,9 @@ int dass_bin_sort_views(const dass_camera* cams, int32_t num_views, int32_t n,
  * dass_render_fwd — front-to-back compositing (Eq. 8; A01, A05,
  * A11-A13).  For pixel (X, Y), over the tile's sorted list, skipping entries
  * whose box does not contain the pixel:
- *   dx = u − X, dy = v − Y; power = −0.5·(A·dx² + C·dy²) − B·dx·dy;
+ *   dx = u − X, dy = v − Y; power = −0.5·(A·dx² + C·dy²) − B·dx·dy
+ *   (evaluated as −[(s dx + sβ dy)² + (g dy)²], the same fp32 bits in every
+ *   kernel, A35);
  *   skip if power > 0; α = min(0.99, o·exp(power)); skip if α < 1/255;
  *   if T·(1 − α) < 1e-4 stop (the entry is NOT added);
  *   otherwise C += rgb·α·T, T ← T·(1 − α).      (T starts at 1)
@@ -269,11 +279,16 @@ int dass_bin_sort_views(const dass_camera* cams, int32_t num_views, int32_t n,
  *
  * accept (nullable): acceptance-list workspace of dass_render_accept_workspace
  *   (num_tiles, pair_capacity) bytes.  When given, the forward also records,
- *   for every (tile, 16×8 half-tile) and every list entry accepted by at least
- *   one of its pixels, the entry index and which of its pixels accepted it;
- *   dass_render_bwd* then walk only those (pair_capacity must be the one given
- *   to dass_bin_sort).  Opaque layout; valid until the next dass_render_fwd on
- *   the same buffer.
+ *   for every tile and every list entry accepted by at least one of its
+ *   pixels, the entry index and which of the tile's pixels accepted it (one
+ *   list per tile, plus the tiles' launch order); dass_render_bwd* then walk
+ *   only those (A38).  pair_capacity must be at least the pair count of the
+ *   sort that produced tile_ranges (the one given to dass_bin_sort): a tile
+ *   range ending past it traps on the device.  Opaque layout; valid until the
+ *   next dass_render_fwd on the same buffer.  accept_bytes = its size.
+ *   INVALID_ARG: accept not 16-byte aligned, accept_bytes below the workspace
+ *   size, pair_capacity ∉ [0, 2^30).  The same holds for the accept argument
+ *   of every dass_render_bwd* call.
  * ------------------------------------------------------------------------- */
 int dass_render_accept_workspace(int32_t num_tiles, int64_t pair_capacity,
                                  size_t* bytes);
@@ -282,7 +297,7 @@ int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges,
                     const float* conic_opa, const float* rgb,
                     const uint32_t* box, const float* bg, float* out_img,
                     float* out_T, uint32_t* out_last, void* accept,
-                    int64_t pair_capacity, void* stream);
+                    size_t accept_bytes, int64_t pair_capacity, void* stream);
 
 /* ---------------------------------------------------------------------------
  * dass_render_bwd — reverse-mode gradient of dass_project + dass_render_fwd
@@ -308,7 +323,7 @@ int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree,
                     const float* xy_depth, const float* conic_opa,
                     const float* rgb, const uint32_t* box, const float* bg,
                     const float* out_T, const uint32_t* out_last,
-                    const float* dL_dimg, const void* accept,
+                    const float* dL_dimg, const void* accept, size_t accept_bytes,
                     int64_t pair_capacity, void* ws, size_t ws_bytes,
                     float* g_pos_opa, float* g_scale, float* g_rot,
                     float* g_sh, float* gradstat_sum, uint32_t* gradstat_cnt,
@@ -336,8 +351,8 @@ int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* ti
                            const uint32_t* sorted_ids, const float* xy_depth,
                            const float* conic_opa, const float* rgb, const uint32_t* box,
                            const float* bg, const float* out_T, const uint32_t* out_last,
-                           const float* dL_dimg, const void* accept, int64_t pair_capacity,
-                           float* g2d, void* stream);
+                           const float* dL_dimg, const void* accept, size_t accept_bytes,
+                           int64_t pair_capacity, float* g2d, void* stream);
 int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views, int32_t n,
                                      int32_t sh_degree, const float* pos_opa,
                                      const float* scale, const float* rot, const float* sh,
@@ -380,14 +395,14 @@ int dass_render_fwd_tiles(const dass_camera* cam, int32_t tile_begin, int32_t ti
                           const uint32_t* sorted_ids, const float* xy_depth,
                           const float* conic_opa, const float* rgb, const uint32_t* box,
                           const float* bg, float* out_img, float* out_T, uint32_t* out_last,
-                          void* accept, int64_t pair_capacity, void* stream);
+                          void* accept, size_t accept_bytes, int64_t pair_capacity, void* stream);
 int dass_render_bwd_raster_tiles(const dass_camera* cam, int32_t tile_begin, int32_t tile_stride,
                                  int32_t tile_count, int32_t n, const uint32_t* tile_ranges,
                                  const uint32_t* sorted_ids, const float* xy_depth,
                                  const float* conic_opa, const float* rgb, const uint32_t* box,
                                  const float* bg, const float* out_T, const uint32_t* out_last,
-                                 const float* dL_dimg, const void* accept, int64_t pair_capacity,
-                                 float* g2d, void* stream);
+                                 const float* dL_dimg, const void* accept, size_t accept_bytes,
+                                 int64_t pair_capacity, float* g2d, void* stream);
 int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_views, int32_t n,
                                         int32_t sh_degree, const float* pos_opa,
                                         const float* scale, const float* rot, const float* sh,

@@ -439,7 +439,11 @@ inline int tie_bits(const Proj& g, const Eval& e, double T, const TieEps& te) {
   if (std::fabs(e.power) < te.power_rel * mag + 1e-12 && e.power != 0.0) b |= TIE_POWER;
   if (std::fabs(e.alpha - ALPHA_MIN) < te.alpha_rel * ALPHA_MIN) b |= TIE_ALPHA;
   if (std::fabs(e.oG - 0.99) < te.clamp_rel * 0.99) b |= TIE_CLAMP;
-  if (std::fabs(T * (1 - e.alpha) - T_MIN) < te.t_rel * T_MIN) b |= TIE_TERM;
+  // the termination test is a decision only for an entry that passes (or ties
+  // at) the power and α tests: a skipped entry's T(1 − α) decides nothing
+  const bool reaches_term = (!(e.power > 0) || (b & TIE_POWER)) &&
+                            (!(e.alpha < ALPHA_MIN) || (b & TIE_ALPHA));
+  if (reaches_term && std::fabs(T * (1 - e.alpha) - T_MIN) < te.t_rel * T_MIN) b |= TIE_TERM;
   return b;
 }
 inline bool is_tie(const Proj& g, const Eval& e, double T, const TieEps& te) {

@@ -187,8 +187,9 @@ int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n, in
 
 int dass_bin_sort_workspace(int32_t n, int32_t num_tiles, int64_t pair_capacity, size_t* bytes) {
   if (!bytes) return fail(DASS_ERR_INVALID_ARG, "bytes is null%s");
-  if (n < 0 || num_tiles < 1 || pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30))
-    return fail(DASS_ERR_INVALID_ARG, "need n >= 0, num_tiles >= 1, 0 <= pair_capacity < 2^30%s");
+  if (n < 0 || n >= (1 << 30) || num_tiles < 1 || pair_capacity < 0 ||
+      pair_capacity >= (int64_t(1) << 30))
+    return fail(DASS_ERR_INVALID_ARG, "need 0 <= n < 2^30, num_tiles >= 1, 0 <= pair_capacity < 2^30%s");
   *bytes = binsort_workspace(n, num_tiles, pair_capacity);
   return DASS_OK;
 }
@@ -199,7 +200,8 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, cons
                   uint32_t* num_pairs_dev, int64_t* num_pairs_host, void* stream) {
   int st = check_camera(cam);
   if (st) return st;
-  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  // the onesweep look-back packs counts into 30 bits (binsort.cu)
+  if (n < 0 || n >= (1 << 30)) return fail(DASS_ERR_INVALID_ARG, "n must be in [0, 2^30)%s");
   if (pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30))
     return fail(DASS_ERR_INVALID_ARG, "pair_capacity must be in [0, 2^30)%s");
   CamParams cp = to_params(cam);
@@ -236,9 +238,9 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, cons
 int dass_bin_sort_views_workspace(int32_t num_views, int32_t n, int64_t view_capacity,
                                   size_t* bytes) {
   if (!bytes) return fail(DASS_ERR_INVALID_ARG, "bytes is null%s");
-  if (num_views < 1 || num_views > 64 || n < 0 || view_capacity < 0 ||
-      view_capacity >= (int64_t(1) << 30) / num_views)
-    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views_workspace: bad sizes%s");
+  if (num_views < 1 || num_views > 64 || n < 0 || (int64_t)num_views * n >= (int64_t(1) << 30) ||
+      view_capacity < 0 || view_capacity >= (int64_t(1) << 30) / num_views)
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views_workspace: bad sizes (V·n and V·capacity must be < 2^30)%s");
   *bytes = binsort_views_workspace(num_views, n, view_capacity);
   return DASS_OK;
 }
@@ -256,7 +258,8 @@ int dass_bin_sort_views(const dass_camera* cams, int32_t num_views, int32_t n,
     if (cams[v].width != cams[0].width || cams[v].height != cams[0].height)
       return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: cameras differ in size%s");
   }
-  if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
+  if (n < 0 || (int64_t)num_views * n >= (int64_t(1) << 30))
+    return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: need 0 <= V·n < 2^30%s");
   if (view_capacity < 0 || view_capacity >= (int64_t(1) << 30) / num_views)
     return fail(DASS_ERR_INVALID_ARG, "view_capacity must be in [0, 2^30 / V)%s");
   if (!sorted_ids || !tile_ranges || !num_pairs_dev)
@@ -281,6 +284,26 @@ int dass_render_accept_workspace(int32_t num_tiles, int64_t pair_capacity, size_
   return DASS_OK;
 }
 
+// Acceptance-list buffer (A38): 16-byte aligned, at least the workspace the
+// image's tile count and pair_capacity need, pair_capacity ∈ [0, 2^30).
+static int check_accept(const CamParams& cp, const void* accept, size_t accept_bytes,
+                        int64_t pair_capacity, const char* where) {
+  if (accept == nullptr) return DASS_OK;
+  char buf[192];
+  if (pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30) || !aligned16(accept)) {
+    snprintf(buf, sizeof(buf), "%s: accept needs a 16-byte aligned buffer and 0 <= pair_capacity < 2^30", where);
+    t_last_error = buf;
+    return DASS_ERR_INVALID_ARG;
+  }
+  const size_t need = render_accept_workspace(cp.tiles_x * cp.tiles_y, pair_capacity);
+  if (accept_bytes < need) {
+    snprintf(buf, sizeof(buf), "%s: accept buffer of %zu bytes < %zu needed", where, accept_bytes, need);
+    t_last_error = buf;
+    return DASS_ERR_INVALID_ARG;
+  }
+  return DASS_OK;
+}
+
 static int tile_subset(const dass_camera* cam, int32_t tile_begin, int32_t tile_stride,
                        int32_t tile_count, CamParams* cp) {
   const int nt = cp->tiles_x * cp->tiles_y;
@@ -298,16 +321,15 @@ int dass_render_fwd_tiles(const dass_camera* cam, int32_t tile_begin, int32_t ti
                           const uint32_t* sorted_ids, const float* xy_depth,
                           const float* conic_opa, const float* rgb, const uint32_t* box,
                           const float* bg, float* out_img, float* out_T, uint32_t* out_last,
-                          void* accept, int64_t pair_capacity, void* stream) {
+                          void* accept, size_t accept_bytes, int64_t pair_capacity, void* stream) {
   int st = check_camera(cam);
   if (st) return st;
   if (!tile_ranges || !out_img || !out_T || !out_last)
     return fail(DASS_ERR_INVALID_ARG, "dass_render_fwd: null required pointer%s");
   if (!sorted_ids || !xy_depth || !conic_opa || !rgb || !box)
     return fail(DASS_ERR_INVALID_ARG, "dass_render_fwd: null record pointer%s");
-  if (accept && (pair_capacity < 0 || pair_capacity >= (int64_t(1) << 30) || !aligned16(accept)))
-    return fail(DASS_ERR_INVALID_ARG, "dass_render_fwd: accept needs a 16-byte aligned buffer and 0 <= pair_capacity < 2^30%s");
   CamParams cp = to_params(cam);
+  if ((st = check_accept(cp, accept, accept_bytes, pair_capacity, "dass_render_fwd"))) return st;
   if ((st = tile_subset(cam, tile_begin, tile_stride, tile_count, &cp))) return st;
   if (cp.tcount == 0) return DASS_OK;
   float3 b = bg ? make_float3(bg[0], bg[1], bg[2]) : make_float3(0.f, 0.f, 0.f);
@@ -321,9 +343,11 @@ int dass_render_fwd_tiles(const dass_camera* cam, int32_t tile_begin, int32_t ti
 int dass_render_fwd(const dass_camera* cam, const uint32_t* tile_ranges, const uint32_t* sorted_ids,
                     const float* xy_depth, const float* conic_opa, const float* rgb,
                     const uint32_t* box, const float* bg, float* out_img, float* out_T,
-                    uint32_t* out_last, void* accept, int64_t pair_capacity, void* stream) {
+                    uint32_t* out_last, void* accept, size_t accept_bytes, int64_t pair_capacity,
+                    void* stream) {
   return dass_render_fwd_tiles(cam, 0, 1, -1, tile_ranges, sorted_ids, xy_depth, conic_opa, rgb,
-                               box, bg, out_img, out_T, out_last, accept, pair_capacity, stream);
+                               box, bg, out_img, out_T, out_last, accept, accept_bytes,
+                               pair_capacity, stream);
 }
 
 int dass_render_bwd_workspace(int32_t n, size_t* bytes) {
@@ -338,7 +362,7 @@ int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree, const 
                     const uint32_t* sorted_ids, const float* xy_depth, const float* conic_opa,
                     const float* rgb, const uint32_t* box, const float* bg, const float* out_T,
                     const uint32_t* out_last, const float* dL_dimg, const void* accept,
-                    int64_t pair_capacity, void* ws, size_t ws_bytes,
+                    size_t accept_bytes, int64_t pair_capacity, void* ws, size_t ws_bytes,
                     float* g_pos_opa, float* g_scale, float* g_rot, float* g_sh,
                     float* gradstat_sum, uint32_t* gradstat_cnt, void* stream) {
   int st = check_camera(cam);
@@ -353,6 +377,7 @@ int dass_render_bwd(const dass_camera* cam, int32_t n, int32_t sh_degree, const 
     return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd: workspace too small%s");
   if (!aligned16(ws)) return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd: workspace must be 16-byte aligned%s");
   CamParams cp = to_params(cam);
+  if ((st = check_accept(cp, accept, accept_bytes, pair_capacity, "dass_render_bwd"))) return st;
   float3 b = bg ? make_float3(bg[0], bg[1], bg[2]) : make_float3(0.f, 0.f, 0.f);
   return cuda_status(
       launch_render_bwd(cp, n, sh_degree, (const float4*)pos_opa, (const float4*)scale,
@@ -370,8 +395,8 @@ int dass_render_bwd_raster_tiles(const dass_camera* cam, int32_t tile_begin, int
                                  const uint32_t* sorted_ids, const float* xy_depth,
                                  const float* conic_opa, const float* rgb, const uint32_t* box,
                                  const float* bg, const float* out_T, const uint32_t* out_last,
-                                 const float* dL_dimg, const void* accept, int64_t pair_capacity,
-                                 float* g2d, void* stream) {
+                                 const float* dL_dimg, const void* accept, size_t accept_bytes,
+                                 int64_t pair_capacity, float* g2d, void* stream) {
   int st = check_camera(cam);
   if (st) return st;
   if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
@@ -381,6 +406,7 @@ int dass_render_bwd_raster_tiles(const dass_camera* cam, int32_t tile_begin, int
     return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_raster: null required pointer%s");
   if (!aligned16(g2d)) return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_raster: g2d must be 16-byte aligned%s");
   CamParams cp = to_params(cam);
+  if ((st = check_accept(cp, accept, accept_bytes, pair_capacity, "dass_render_bwd_raster"))) return st;
   if ((st = tile_subset(cam, tile_begin, tile_stride, tile_count, &cp))) return st;
   float3 b = bg ? make_float3(bg[0], bg[1], bg[2]) : make_float3(0.f, 0.f, 0.f);
   return cuda_status(launch_render_bwd_raster(cp, n, (const uint2*)tile_ranges, sorted_ids,
@@ -395,11 +421,11 @@ int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* ti
                            const uint32_t* sorted_ids, const float* xy_depth,
                            const float* conic_opa, const float* rgb, const uint32_t* box,
                            const float* bg, const float* out_T, const uint32_t* out_last,
-                           const float* dL_dimg, const void* accept, int64_t pair_capacity,
-                           float* g2d, void* stream) {
+                           const float* dL_dimg, const void* accept, size_t accept_bytes,
+                           int64_t pair_capacity, float* g2d, void* stream) {
   return dass_render_bwd_raster_tiles(cam, 0, 1, -1, n, tile_ranges, sorted_ids, xy_depth,
                                       conic_opa, rgb, box, bg, out_T, out_last, dL_dimg, accept,
-                                      pair_capacity, g2d, stream);
+                                      accept_bytes, pair_capacity, g2d, stream);
 }
 
 int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_views, int32_t n,

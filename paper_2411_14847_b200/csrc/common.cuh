@@ -31,44 +31,43 @@ struct CamParams {
 
 void launch_counted(int n = 1);  // bumps the dass_kernel_launches() counter
 
-// Per-pixel α of Eq. 8, shared by render_fwd and render_bwd so both take the
-// same fp32 decisions (power > 0 guard, α < 1/255 skip) bit-for-bit.
-struct Splat2D {
-  float u, v;        // tile-local mean (pixels, relative to the tile origin)
-  float A, B, C, o;  // conic and effective opacity
-};
-
-// power = −½(A dx² + C dy²) − B dx dy   (Eq. 5 restricted to 2D), evaluated
-// in one canonical explicit-rounding form shared by every kernel that takes a
-// per-pixel decision (render_fwd, render_bwd, render_stats), so all of them
-// get identical bits: with the per-(entry, column) terms
-//   ax = (−½A·dx)·dx,  bx = −B·dx,  hC = −½C
-// each pixel of the column costs one FADD (dy) and two FFMA:
-//   power = fma(dy, fma(hC, dy, bx), ax).
-struct ColTerms {
-  float ax, bx, hC;
-};
-__device__ __forceinline__ ColTerms col_terms(float A, float B, float C, float dx) {
-  ColTerms t;
-  t.ax = __fmul_rn(__fmul_rn(-0.5f * A, dx), dx);
-  t.bx = __fmul_rn(-B, dx);
-  t.hC = -0.5f * C;
-  return t;
-}
-// The same terms from a staged conic (−½A, −B, −½C): the scalings are exact in
-// fp32, so the bits equal col_terms(A, B, C, dx).
+// Per-pixel power of Eq. 8, shared by every kernel that takes a per-pixel
+// decision (render_fwd, render_bwd, render_stats, render_features) so all of
+// them get identical fp32 bits (A35).
+//
+// The projected conic record (dass_project) is the Cholesky form of the 2×2
+// inverse covariance K = [[A, B], [B, C]]:
+//   conic_opa = (A, β, γ, o),  β = B/A = −Σ′_xy/Σ′_yy,  γ = C − B²/A = 1/Σ′_yy
+// (β and γ from the fp64 Σ′, then rounded once), because
+//   power = −½(A dx² + 2B dx dy + C dy²) = −[(s·dx + sβ·dy)² + (g·dy)²],
+//   s = √(A/2), g = √(γ/2),
+// is then minus a sum of two squares: an elongated splat's cross term no longer
+// cancels against the diagonal terms (the form −½(A dx² + C dy²) − B dx dy
+// lost up to ~1e-4 of the power in fp32 for needle-like splats, enough to move
+// T by 4e-3 relative after a few dozen entries).  Staged as (s, sβ, g, o), a
+// pixel (dx, dy) costs
+//   column term X = s·dx,  row terms Y = sβ·dy, N = −(g·dy)·(g·dy)
+//   t = X + Y;  power = fma(−t, t, N)          (all explicitly rounded)
+// i.e. one FADD and one FFMA per pixel when X / (Y, N) are shared by the
+// pixels of a column / row.
 __device__ __forceinline__ float4 conic_staged(float4 co) {
-  return make_float4(-0.5f * co.x, -co.y, -0.5f * co.z, co.w);
+  const float s = __fsqrt_rn(__fmul_rn(0.5f, co.x));
+  return make_float4(s, __fmul_rn(s, co.y), __fsqrt_rn(__fmul_rn(0.5f, co.z)), co.w);
 }
-__device__ __forceinline__ ColTerms col_terms_staged(const float4& sc, float dx) {
-  ColTerms t;
-  t.ax = __fmul_rn(__fmul_rn(sc.x, dx), dx);
-  t.bx = __fmul_rn(sc.y, dx);
-  t.hC = sc.z;
-  return t;
+struct RowTerms {
+  float y, n;   // sβ·dy, −(g·dy)²
+};
+__device__ __forceinline__ float col_term(const float4& sc, float dx) { return __fmul_rn(sc.x, dx); }
+__device__ __forceinline__ RowTerms row_terms(const float4& sc, float dy) {
+  const float z = __fmul_rn(sc.z, dy);
+  return RowTerms{__fmul_rn(sc.y, dy), -__fmul_rn(z, z)};
 }
-__device__ __forceinline__ float splat_power(const ColTerms& t, float dy) {
-  return __fmaf_rn(dy, __fmaf_rn(t.hC, dy, t.bx), t.ax);
+__device__ __forceinline__ float splat_power(float X, const RowTerms& r) {
+  const float t = __fadd_rn(X, r.y);
+  return __fmaf_rn(-t, t, r.n);
+}
+__device__ __forceinline__ float splat_power(const float4& sc, float dx, float dy) {
+  return splat_power(col_term(sc, dx), row_terms(sc, dy));
 }
 
 // exp(power) on the MUFU pipe: ex2.approx(power · log2 e).

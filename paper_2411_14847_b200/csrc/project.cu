@@ -144,11 +144,13 @@ __device__ __forceinline__ KeyResult key_chain(const CamParams& c, float px, flo
 #undef FS
 #undef FD
 
-// fp64 records: tile-independent mean (hi/lo) and conic of Eq. 7.
+// fp64 records: tile-independent mean (hi/lo) and the conic of Eq. 7 in its
+// Cholesky form (A, β, γ): K = [[A, B], [B, C]] with B = A·β, C = γ + A·β²,
+// so A dx² + 2B dx dy + C dy² = A(dx + β dy)² + γ dy² (common.cuh, A35).
 struct Records {
   float u_hi, v_hi;
   __half u_lo, v_lo;
-  float A, B, C;
+  float A, beta, gamma;
 };
 
 __device__ __forceinline__ Records accurate_records(const CamParams& c, float4 po, float4 sc,
@@ -191,10 +193,10 @@ __device__ __forceinline__ Records accurate_records(const CamParams& c, float4 p
   const double b2 = N[0][0] * N[1][0] + N[0][1] * N[1][1] + N[0][2] * N[1][2];
   const double c2 = N[1][0] * N[1][0] + N[1][1] * N[1][1] + N[1][2] * N[1][2] + 0.3;
   const double det = a2 * c2 - b2 * b2;
-  const double idet = 1.0 / det;
-  r.A = (float)(c2 * idet);
-  r.B = (float)(-b2 * idet);
-  r.C = (float)(a2 * idet);
+  const double ic = 1.0 / c2;
+  r.A = (float)(c2 / det);
+  r.beta = (float)(-b2 * ic);    // B/A = (−b/det)/(c/det)
+  r.gamma = (float)ic;           // C − B²/A = (ac − b²)/(det·c) = 1/c
   const double u = c.fx * t[0] * itz + c.cx;
   const double v = c.fy * t[1] * itz + c.cy;
   r.u_hi = (float)u;
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__
       if (col[ch] < 0.f) { bits |= 1 << ch; col[ch] = 0.f; }
     const __half2 lo = __halves2half2(r.u_lo, r.v_lo);
     a.xy_depth[o] = make_float4(r.u_hi, r.v_hi, k.z, __uint_as_float(*(const uint32_t*)&lo));
-    a.conic_opa[o] = make_float4(r.A, r.B, r.C, o_eff);
+    a.conic_opa[o] = make_float4(r.A, r.beta, r.gamma, o_eff);
     a.rgb[o] = make_float4(col[0], col[1], col[2], (float)bits);
     a.box[o] = make_uint2((uint32_t)k.x0 | ((uint32_t)k.x1 << 16), (uint32_t)k.y0 | ((uint32_t)k.y1 << 16));
     a.tiles[o] = (uint32_t)((k.x1 / TILE - k.x0 / TILE + 1) * (k.y1 / TILE - k.y0 / TILE + 1));

@@ -20,8 +20,6 @@
 // clamped), the pixel contributes (e·dx, e·dy, e·dx², e·dx·dy, e·dy², e,
 // αT·g_r, αT·g_g, αT·g_b), and the preprocess kernel forms
 // ∂L/∂u = −o(A Σe·dx + B Σe·dy), ∂L/∂A = −½ o Σe·dx², … (exact algebra).
-#include <cstdlib>
-
 #include "common.cuh"
 #include "sh.cuh"
 
@@ -37,7 +35,7 @@ namespace {
 //   s_a  = (u_rel, v_rel, p_thr, box mask bits)   p_thr: conservative power
 //          threshold ln(α_min/o) − 1e-3 below which α < 1/255 for sure, so the
 //          exp is skipped without changing any decision
-//   s_co = (−½A, −B, −½C, o) (conic_staged)    s_c = (r, g, b, −)
+//   s_co = (s, sβ, g, o) (conic_staged)    s_c = (r, g, b, −)
 // Tile-local row/column mask of the pixels an entry can possibly be accepted
 // at: the integer pixel box (A05) intersected with the bounding box of the
 // α ≥ 1/255 support ellipse {½ dᵀK d ≤ −p_thr}, whose half-extents are
@@ -77,14 +75,16 @@ __device__ __forceinline__ float rect_qmin(float A, float B, float C, float a0, 
 template <int RPW>
 __device__ __forceinline__ uint32_t support_mask(uint2 b, int tx0, int ty0, float ux, float uy,
                                                  float4 co, float pthr) {
+  // co = (A, β, γ, o): K = [[A, Aβ], [Aβ, γ + Aβ²]], det K = Aγ, Σ' = K⁻¹ with
+  // Σ'_xx = 1/A + β²/γ and Σ'_yy = 1/γ
   int x0 = max((int)(b.x & 0xFFFFu) - tx0, 0), x1 = min((int)(b.x >> 16) - tx0, TILE - 1);
   int y0 = max((int)(b.y & 0xFFFFu) - ty0, 0), y1 = min((int)(b.y >> 16) - ty0, TILE - 1);
-  const float det = co.x * co.z - co.y * co.y;
   const float r2 = -2.f * pthr;
   bool tight = false;
-  if (det > 0.f && r2 > 0.f) {
-    const float hx = sqrtf(r2 * co.z / det) * 1.0001f + 1e-3f;
-    const float hy = sqrtf(r2 * co.x / det) * 1.0001f + 1e-3f;
+  if (co.x > 0.f && co.z > 0.f && r2 > 0.f) {
+    const float sxx = 1.f / co.x + co.y * co.y / co.z, syy = 1.f / co.z;
+    const float hx = sqrtf(r2 * sxx) * 1.0001f + 1e-3f;
+    const float hy = sqrtf(r2 * syy) * 1.0001f + 1e-3f;
     if (isfinite(hx) && isfinite(hy)) {
       tight = true;
       x0 = max(x0, (int)ceilf(fmaxf(ux - hx, -1.f)));
@@ -98,11 +98,12 @@ __device__ __forceinline__ uint32_t support_mask(uint2 b, int tx0, int ty0, floa
   uint32_t my = ((2u << y1) - 1u) & ~((1u << y0) - 1u);
   if (tight && RPW < 16) {
     const float lim = r2 * 1.0001f + 1e-3f;
+    const float B = co.x * co.y, C = co.z + co.x * co.y * co.y;
 #pragma unroll
     for (int w = 0; w < 16 / RPW; ++w) {
       const int ry0 = max(y0, w * RPW), ry1 = min(y1, w * RPW + RPW - 1);
       if (ry0 > ry1) continue;
-      const float q = rect_qmin(co.x, co.y, co.z, (float)x0 - ux, (float)x1 - ux, (float)ry0 - uy,
+      const float q = rect_qmin(co.x, B, C, (float)x0 - ux, (float)x1 - ux, (float)ry0 - uy,
                                 (float)ry1 - uy);
       if (q > lim) my &= ~(((1u << RPW) - 1u) << (w * RPW));
     }
@@ -123,7 +124,7 @@ __device__ __forceinline__ void stage(uint32_t id, const float4* __restrict__ xy
   const uint32_t lo_bits = __float_as_uint(xy.w);
   const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
   const float4 con = conic_opa[id];
-  co = conic_staged(con);   // (−½A, −B, −½C, o)
+  co = conic_staged(con);   // (s, sβ, g, o)
   const float4 cc = rgb[id];
   a.x = __fadd_rn(xy.x - (float)tx0, __low2float(lo));
   a.y = __fadd_rn(xy.y - (float)ty0, __high2float(lo));
@@ -144,17 +145,18 @@ __device__ __forceinline__ uint32_t warp_row_mask(int warp) {
   return (((1u << (2 * PPT)) - 1u) << (16 + warp * 2 * PPT));
 }
 
-// Per-(tile, warp) acceptance lists written by the forward (PPT = 4, two
-// warps of 16×8 pixels per tile): for every tile-list entry accepted by at
-// least one pixel of the warp, its absolute list index and 32 bytes — byte
-// `lane` holds the 4-bit set of that lane's pixels that accepted it (one
-// coalesced 32-B store per entry, no ballots).  Warp w of tile t stores its
-// list at [2·range.x + w·len, …), len = range length; cnt[2t + w].
+// Per-tile acceptance lists written by the forward (A38; one warp per tile,
+// TW pixel map): for every tile-list entry accepted by at least one pixel of
+// the tile, its absolute list index idx[range.x + k] and 32 bytes
+// bytes[(range.x + k)·32 + lane] — the 8-bit set of lane's pixels that
+// accepted it; cnt[tile] = the number of such entries.  The backward walks
+// exactly these (pixel, entry) pairs.
 struct AcceptLists {
   uint32_t* cnt;
   uint32_t* idx;
   uint8_t* bytes;
-  uint32_t* order;   // TW path: launch order of the tiles (longest list first)
+  uint32_t* order;   // launch order of the tiles (longest list first)
+  uint32_t cap;      // pair capacity the lists were sized for
 };
 
 // Pixel ownership of a tile CTA (NT = 256/PPT threads, 16×16 pixels).
@@ -189,16 +191,17 @@ struct PixMap {
 };
 
 // ------------------------------------------------------------- forward ----
-template <int PPT, bool LISTS, int RPW = 16, int MINB = 768 / (256 / PPT)>
+// Without acceptance lists (dass_render_fwd with accept = nullptr): one CTA of
+// 64 threads per tile, PPT = 4 quadrant map, batches of 128 staged entries.
+template <int PPT, int MINB = 768 / (256 / PPT)>
 __global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
     const float4* __restrict__ conic_opa, const float4* __restrict__ rgb,
     const uint2* __restrict__ box, float3 bg, float* __restrict__ out_img,
-    float* __restrict__ out_T, uint32_t* __restrict__ out_last, AcceptLists acc) {
-  static_assert(!LISTS || PPT == 4, "acceptance lists are defined for the PPT = 4 mapping");
+    float* __restrict__ out_T, uint32_t* __restrict__ out_last) {
+  static_assert(PPT == 4, "the quadrant map");
   constexpr int NT = 256 / PPT;
-  constexpr int NW = NT / 32;
   constexpr int BATCH = 2 * NT;
   __shared__ Staged s_st[BATCH];
   const int tile = cam.tile0 + blockIdx.x * cam.tstride;
@@ -217,20 +220,14 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
     last[p] = range.x;
     if (tx0 + pm.x(p) < cam.W && ty0 + pm.y(p) < cam.H) live |= 1u << p;
   }
-  // tile-relative pixel coordinates: columns fxc[p & 1] (quad) / fxc[0] (row map)
-  const float fxc[2] = {(float)pm.x(0), (float)pm.x(PPT > 1 ? 1 : 0)};
-  float fy[PPT];
-#pragma unroll
-  for (int p = 0; p < PPT; ++p) fy[p] = (float)pm.y(p);
-  // acceptance list of this warp: entries (absolute list index, 4 ballot words)
-  const uint32_t warp = t >> 5, lane = t & 31u;
-  const size_t lbase = (size_t)NW * range.x + (size_t)warp * (range.y - range.x);
-  uint32_t nlist = 0;
+  // tile-relative pixel coordinates: columns fxc[p & 1], rows fy[p]
+  const float fxc[2] = {(float)pm.x(0), (float)pm.x(1)};
+  const float fy0 = (float)pm.y(0), fy1 = (float)pm.y(2);
   for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
     const bool alive = live != 0u;
     if (__syncthreads_count(alive) == 0) break;
     for (int k = t; k < BATCH; k += NT)
-      if (b0 + k < range.y) stage<RPW>(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
+      if (b0 + k < range.y) stage<16>(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
     __syncthreads();
     const int cnt = __any_sync(0xffffffffu, alive) ? (int)min((uint32_t)BATCH, range.y - b0) : 0;
     for (int j = 0; j < cnt; ++j) {
@@ -238,56 +235,38 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_fwd_kernel(
       const float4 a = st.a;
       const uint32_t m = __float_as_uint(a.w);
       if ((m & wmask) == 0u) continue;   // warp-uniform: box misses this warp's rows
-      uint32_t accb = 0;                 // this lane's accepted pixels of the entry
       // candidate pixels: column and row in the support mask, still live
       const uint32_t cand = pm.cand(m) & live;
-      if (cand) {
-        const float4 co = st.co;
-        float pw[PPT];
-        uint32_t ok = 0;
-        if constexpr (PixMap<PPT>::QUAD) {
-          const ColTerms c0 = col_terms_staged(co, a.x - fxc[0]);
-          const ColTerms c1 = col_terms_staged(co, a.x - fxc[1]);
-          const float dy0 = a.y - fy[0], dy1 = a.y - fy[2];
-          pw[0] = splat_power(c0, dy0); pw[1] = splat_power(c1, dy0);
-          pw[2] = splat_power(c0, dy1); pw[3] = splat_power(c1, dy1);
-        } else {
-          const ColTerms ct = col_terms_staged(co, a.x - fxc[0]);
+      if (!cand) continue;
+      const float4 co = st.co;
+      const float dx0 = a.x - fxc[0], dx1 = a.x - fxc[1];
+      const float dy0 = a.y - fy0, dy1 = a.y - fy1;
+      const float X0 = col_term(co, dx0), X1 = col_term(co, dx1);
+      const RowTerms R0 = row_terms(co, dy0), R1 = row_terms(co, dy1);
+      float pw[PPT];
+      pw[0] = splat_power(X0, R0); pw[1] = splat_power(X1, R0);
+      pw[2] = splat_power(X0, R1); pw[3] = splat_power(X1, R1);
+      uint32_t ok = 0;
 #pragma unroll
-          for (int p = 0; p < PPT; ++p) pw[p] = splat_power(ct, a.y - fy[p]);
-        }
+      for (int p = 0; p < PPT; ++p)   // independent per pixel: no branches, full ILP
+        ok |= (!(pw[p] > 0.f) && !(pw[p] < a.z)) ? (1u << p) : 0u;
+      ok &= cand;
+      if (!ok) continue;
+      const float4 c = st.c;
 #pragma unroll
-        for (int p = 0; p < PPT; ++p)   // independent per pixel: no branches, full ILP
-          ok |= (!(pw[p] > 0.f) && !(pw[p] < a.z)) ? (1u << p) : 0u;
-        ok &= cand;
-        if (ok) {
-          const float4 c = st.c;
-#pragma unroll
-          for (int p = 0; p < PPT; ++p) {
-            if (!((ok >> p) & 1u)) continue;
-            const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
-            if (alpha < ALPHA_MIN) continue;
-            const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
-            if (tn < T_MIN) { live &= ~(1u << p); continue; }
-            const float w = alpha * T[p];
-            C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
-            T[p] = tn;
-            last[p] = b0 + j + 1;
-            accb |= 1u << p;
-          }
-        }
-      }
-      if (LISTS) {
-        if (__any_sync(0xffffffffu, accb != 0u)) {
-          const size_t e = lbase + nlist;
-          acc.bytes[e * 32 + lane] = (uint8_t)accb;
-          if (lane == 0) acc.idx[e] = b0 + j;
-          ++nlist;
-        }
+      for (int p = 0; p < PPT; ++p) {
+        if (!((ok >> p) & 1u)) continue;
+        const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
+        if (alpha < ALPHA_MIN) continue;
+        const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
+        if (tn < T_MIN) { live &= ~(1u << p); continue; }
+        const float w = alpha * T[p];
+        C[p][0] += c.x * w; C[p][1] += c.y * w; C[p][2] += c.z * w;
+        T[p] = tn;
+        last[p] = b0 + j + 1;
       }
     }
   }
-  if (LISTS && lane == 0) acc.cnt[(size_t)NW * tile + warp] = nlist;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
@@ -361,12 +340,13 @@ __global__ void __launch_bounds__(64) render_features_kernel(
       const uint32_t m = __float_as_uint(a.w);
       if ((m & wmask) == 0u || !(m & colbit)) continue;
       const float4 co = s_st[j].co;
-      const ColTerms ct = col_terms_staged(co, a.x - fx);
+      const float dx = a.x - fx;
       const uint32_t mr = m >> (16 + ly0);
 #pragma unroll
       for (int p = 0; p < PPT; ++p) {
         if (done[p] || !((mr >> p) & 1u)) continue;
-        const float pw = splat_power(ct, a.y - fy[p]);
+        const float dy = a.y - fy[p];
+        const float pw = splat_power(co, dx, dy);
         if (pw > 0.f || pw < a.z) continue;
         const float alpha = splat_alpha(co.w, splat_exp(pw));
         if (alpha < ALPHA_MIN) continue;
@@ -521,13 +501,13 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
       if (m & colbit) {
         const float4 co = st.co;
         const float dx = a.x - fx;
-        const ColTerms ct = col_terms_staged(co, dx);
         const uint32_t mr = m >> (16 + ly0);   // this thread's PPT row bits
         float pw[PPT];
         bool ok[PPT];
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
-          pw[p] = splat_power(ct, a.y - fy[p]);
+          const float dyp = a.y - fy[p];
+          pw[p] = splat_power(co, dx, dyp);
           ok[p] = gidx < last[p] && ((mr >> p) & 1u) && !(pw[p] > 0.f) && !(pw[p] < a.z);
         }
 #pragma unroll
@@ -581,139 +561,6 @@ __global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_raster_kernel(
       }
     }
     b1 = b0;
-  }
-}
-
-// --------------------------------- backward: raster part from the lists ----
-// Each warp walks ITS acceptance list (written by the forward) backwards in
-// chunks of 32 entries: the chunk's records are gathered into per-warp shared
-// memory (one entry per lane), then for every entry only the accepted pixels
-// are evaluated (bit-identical α: same canonical power, same staging
-// arithmetic as the forward), the 9 per-pixel terms are reduce-scattered
-// (every list entry has ≥ 1 accepted pixel, so every butterfly is needed) and
-// the chunk is flushed with vector reductions.  Warps are independent: no
-// block barrier, no iteration over entries the warp never accepted.
-template <int PPT, int MINB = 1024 / (256 / PPT)>
-__global__ void __launch_bounds__(256 / PPT, MINB) render_bwd_list_kernel(
-    const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
-    const uint32_t* __restrict__ ids, const float4* __restrict__ xy_depth,
-    const float4* __restrict__ conic_opa, const float4* __restrict__ rgb, float3 bg,
-    const float* __restrict__ out_T, const float* __restrict__ dL_dimg, AcceptLists acc,
-    float4* __restrict__ g2d) {
-  static_assert(PPT == 4, "acceptance lists are defined for the PPT = 4 mapping");
-  constexpr int NT = 256 / PPT;
-  constexpr int NW = NT / 32;
-  __shared__ float4 s_a[NW][32];    // (u_rel, v_rel, −, −)
-  __shared__ float4 s_co[NW][32];   // (−½A, −B, −½C, o)
-  __shared__ float4 s_c[NW][32];    // (r, g, b, −)
-  __shared__ uint4 s_bytes[NW][32][2];   // 32 acceptance bytes per staged entry
-  __shared__ uint32_t s_id[NW][32];
-  __shared__ float s_acc[NW][32][9];
-  const int tile = cam.tile0 + blockIdx.x * cam.tstride;
-  const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
-  const int tx0 = txi * TILE, ty0 = tyi * TILE;
-  const int t = threadIdx.x;
-  const int warp = t >> 5;
-  const uint32_t lane = t & 31u;
-  const PixMap<PPT> pm(t);   // the forward's quadrant map (the lists' bit p)
-  const uint2 range = ranges[tile];
-  const size_t lbase = (size_t)NW * range.x + (size_t)warp * (range.y - range.x);
-  const uint32_t n = acc.cnt[(size_t)NW * tile + warp];
-  if (n == 0) return;  // warp-uniform; nothing this warp accepted (no block barrier below)
-  LaneRS rs;
-  rs.init();
-  float T[PPT], gR[PPT], g[PPT][3];
-  const size_t np = (size_t)cam.W * cam.H;
-#pragma unroll
-  for (int p = 0; p < PPT; ++p) {
-    const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
-    if (X < cam.W && Y < cam.H) {
-      const size_t pix = (size_t)Y * cam.W + X;
-      T[p] = out_T[pix];
-      g[p][0] = dL_dimg[pix]; g[p][1] = dL_dimg[np + pix]; g[p][2] = dL_dimg[2 * np + pix];
-    } else {
-      T[p] = 1.f;
-      g[p][0] = g[p][1] = g[p][2] = 0.f;
-    }
-    gR[p] = T[p] * (g[p][0] * bg.x + g[p][1] * bg.y + g[p][2] * bg.z);
-  }
-  // two columns (p & 1) and two rows (p >> 1) per lane, tile-relative
-  const float fx0 = (float)pm.x(0), fx1 = (float)pm.x(1);
-  const float fy0 = (float)pm.y(0), fy1 = (float)pm.y(2);
-  for (int ptr = (int)n; ptr > 0;) {
-    const int k0 = ptr > 32 ? ptr - 32 : 0;
-    const int cnt = ptr - k0;
-    if ((int)lane < cnt) {
-      const size_t e = lbase + k0 + lane;
-      const uint32_t id = ids[acc.idx[e]];
-      const uint4* src = reinterpret_cast<const uint4*>(acc.bytes + e * 32);
-      s_bytes[warp][lane][0] = src[0];
-      s_bytes[warp][lane][1] = src[1];
-      s_id[warp][lane] = id;
-      // the forward's staging arithmetic for (u_rel, v_rel): identical bits
-      const float4 xy = xy_depth[id];
-      const uint32_t lo_bits = __float_as_uint(xy.w);
-      const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
-      s_a[warp][lane] = make_float4(__fadd_rn(xy.x - (float)tx0, __low2float(lo)),
-                                    __fadd_rn(xy.y - (float)ty0, __high2float(lo)), 0.f, 0.f);
-      s_co[warp][lane] = conic_staged(conic_opa[id]);
-      s_c[warp][lane] = rgb[id];
-    }
-    __syncwarp();
-    for (int k = cnt - 1; k >= 0; --k) {
-      const uint32_t bits = reinterpret_cast<const uint8_t*>(&s_bytes[warp][k][0])[lane];
-      float v[9];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) v[q] = 0.f;
-      if (bits) {
-        const float4 a = s_a[warp][k];
-        const float4 co = s_co[warp][k];
-        const float4 c = s_c[warp][k];
-        const float dxc[2] = {a.x - fx0, a.x - fx1};
-        const float dyr[2] = {a.y - fy0, a.y - fy1};
-        const ColTerms ct[2] = {col_terms_staged(co, dxc[0]),
-                                col_terms_staged(co, dxc[1])};
-        float se[2] = {0.f, 0.f}, sey[2] = {0.f, 0.f};   // per column: Σe, Σe·dy
-#pragma unroll
-        for (int p = 0; p < PPT; ++p) {
-          if (!((bits >> p) & 1u)) continue;
-          const float dy = dyr[p >> 1];
-          const float G = splat_exp(splat_power(ct[p & 1], dy));
-          const float oG = __fmul_rn(co.w, G);
-          const float alpha = fminf(ALPHA_MAX, oG);
-          const float inv = rcp_approx(1.f - alpha);
-          T[p] *= inv;                        // transmittance before this entry
-          const float w = alpha * T[p];
-          const float gc = g[p][0] * c.x + g[p][1] * c.y + g[p][2] * c.z;
-          const float dLda = T[p] * gc - inv * gR[p];
-          gR[p] += gc * w;                    // g·(S + T_final·bg), S = suffix colour
-          v[6] += w * g[p][0]; v[7] += w * g[p][1]; v[8] += w * g[p][2];
-          const float e = oG < ALPHA_MAX ? G * dLda : 0.f;
-          const float ey = e * dy;
-          sey[p & 1] += ey; v[4] += ey * dy; se[p & 1] += e;
-        }
-        // dx is constant per column, so the dx-moments factor out of the pixel
-        // loop: Σe·dx = Σ_col dx·Σe, Σe·dx² = Σ_col dx·(dx·Σe), Σe·dx·dy = Σ_col dx·Σe·dy
-        const float m0 = se[0] * dxc[0], m1 = se[1] * dxc[1];
-        v[0] = m0 + m1;
-        v[1] = sey[0] + sey[1];
-        v[2] = m0 * dxc[0] + m1 * dxc[1];
-        v[3] = sey[0] * dxc[0] + sey[1] * dxc[1];
-        v[5] = se[0] + se[1];
-      }
-      const float sum = rs.reduce(v);
-      if (rs.slot >= 0) s_acc[warp][k][rs.slot] = sum;
-    }
-    __syncwarp();
-    if ((int)lane < cnt) {
-      const float* a9 = s_acc[warp][lane];
-      float4* dst = g2d + 3 * (size_t)s_id[warp][lane];
-      red_add_v4(dst, make_float4(a9[0], a9[1], a9[2], a9[3]));
-      red_add_v4(dst + 1, make_float4(a9[4], a9[5], a9[6], a9[7]));
-      atomicAdd(&dst[2].x, a9[8]);
-    }
-    __syncwarp();
-    ptr = k0;
   }
 }
 
@@ -783,6 +630,14 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const __grid_constant_
   }
 }
 
+// Forward, one warp per tile.  Per batch, lane k stages entry b0 + k (its
+// tile-local mean, staged conic, colour, support mask).  Per entry: a
+// warp-uniform skip when its support misses the tile, then every lane tests
+// its eight pixels at once (candidate bits from the support mask, the power
+// threshold) and only the pixel blocks with a candidate execute the α /
+// transmittance update.  Per-pixel colour sits in shared memory (touched only
+// on acceptance), T in registers (the termination test does not wait on a
+// shared load).
 template <int MINB>
 __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
     const __grid_constant__ CamParams cam, const uint2* __restrict__ ranges,
@@ -793,19 +648,16 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
   constexpr int PPT = 8;
   constexpr int BATCH = TW_FWD_BATCH;
   __shared__ Staged s_st[BATCH];
-  // (C_r, C_g, C_b, T) of the lane's pixels in shared memory instead of 24
-  // registers (occupancy: 1-warp CTAs); touched once per accepted pixel (T is
-  // also kept in registers for the termination test; .w is the copy the
-  // output stage reads)
-  __shared__ float4 s_px[PPT][32];
+  __shared__ float4 s_px[PPT][32];   // (C_r, C_g, C_b, T) of the lane's pixels
   const int tile = cam.tile0 + (int)acc.order[blockIdx.x] * cam.tstride;
   const int tyi = tile / cam.tiles_x, txi = tile - tyi * cam.tiles_x;
   const int tx0 = txi * TILE, ty0 = tyi * TILE;
   const uint32_t lane = threadIdx.x;
   const TileMap pm((int)lane);
   const uint2 range = ranges[tile];
+  if (range.y > acc.cap) __trap();   // lists sized for fewer pairs than the sort produced
   uint32_t last[PPT];
-  float T[PPT];   // in registers: the termination decision does not wait on shared memory
+  float T[PPT];
   uint32_t live = 0;   // bit p: pixel p is inside the image and not terminated
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
@@ -818,12 +670,13 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
   float fy[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) fy[r] = (float)pm.y(r);
-  uint32_t nlist = 0;
+  uint8_t* lbytes = acc.bytes + (size_t)range.x * 32 + lane;   // this lane's byte of list entry 0
+  uint32_t* lidx = acc.idx + range.x;
   for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
     if (!__any_sync(0xffffffffu, live != 0u)) break;
     __syncwarp();   // the previous batch is consumed
-    for (int k = (int)lane; k < BATCH; k += 32)
-      if (b0 + k < range.y) stage<16>(ids[b0 + k], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[k].a, s_st[k].co, s_st[k].c);
+    if (b0 + lane < range.y)
+      stage<16>(ids[b0 + lane], xy_depth, conic_opa, rgb, box, tx0, ty0, s_st[lane].a, s_st[lane].co, s_st[lane].c);
     __syncwarp();
     const int cnt = (int)min((uint32_t)BATCH, range.y - b0);
     for (int j = 0; j < cnt; ++j) {
@@ -835,15 +688,14 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
       const uint32_t cand = pm.cand(m) & live;
       if (cand) {
         const float4 co = st.co;
-        const ColTerms c0 = col_terms_staged(co, a.x - fx0);
-        const ColTerms c1 = col_terms_staged(co, a.x - fx1);
+        const float X0 = col_term(co, a.x - fx0), X1 = col_term(co, a.x - fx1);
         float pw[PPT];
         uint32_t ok = 0;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const float dy = a.y - fy[r];
-          pw[r] = splat_power(c0, dy);
-          pw[r + 4] = splat_power(c1, dy);
+          const RowTerms R = row_terms(co, a.y - fy[r]);
+          pw[r] = splat_power(X0, R);
+          pw[r + 4] = splat_power(X1, R);
         }
 #pragma unroll
         for (int p = 0; p < PPT; ++p)
@@ -870,14 +722,14 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
         }
       }
       if (__any_sync(0xffffffffu, accb != 0u)) {
-        const size_t e = (size_t)range.x + nlist;
-        acc.bytes[e * 32 + lane] = (uint8_t)accb;
-        if (lane == 0) acc.idx[e] = b0 + j;
-        ++nlist;
+        *lbytes = (uint8_t)accb;
+        if (lane == 0) *lidx = b0 + j;
+        lbytes += 32;
+        ++lidx;
       }
     }
   }
-  if (lane == 0) acc.cnt[tile] = nlist;
+  if (lane == 0) acc.cnt[tile] = (uint32_t)(lidx - (acc.idx + range.x));
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
@@ -903,7 +755,7 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
   constexpr int PPT = 8;
   constexpr int CH = TW_BWD_CHUNK;   // entries staged per chunk
   __shared__ float4 s_a[CH];    // (u_rel, v_rel, −, −)
-  __shared__ float4 s_co[CH];   // (−½A, −B, −½C, o)
+  __shared__ float4 s_co[CH];   // (s, sβ, g, o)
   __shared__ float4 s_c[CH];    // (r, g, b, −)
   __shared__ uint4 s_bytes[CH][2];
   __shared__ uint32_t s_id[CH];
@@ -919,6 +771,7 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
   const uint32_t lane = threadIdx.x;
   const TileMap pm((int)lane);
   const uint2 range = ranges[tile];
+  if (range.y > acc.cap) __trap();   // lists sized for fewer pairs than the sort produced
   LaneRS rs;
   rs.init();
   float T[PPT], gR[PPT];
@@ -970,14 +823,13 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
         const float4 co = s_co[k];
         const float4 c = s_c[k];
         const float dxc[2] = {a.x - fx0, a.x - fx1};
-        const ColTerms ct[2] = {col_terms_staged(co, dxc[0]),
-                                col_terms_staged(co, dxc[1])};
+        const float Xc[2] = {col_term(co, dxc[0]), col_term(co, dxc[1])};
         float se[2] = {0.f, 0.f}, sey[2] = {0.f, 0.f};   // per column: Σe, Σe·dy
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
           if (!((bits >> p) & 1u)) continue;
           const float dy = a.y - fy[p & 3];
-          const float G = splat_exp(splat_power(ct[p >> 2], dy));
+          const float G = splat_exp(splat_power(Xc[p >> 2], row_terms(co, dy)));
           const float4 gp = s_g[p][lane];
           const float oG = __fmul_rn(co.w, G);
           const float alpha = fminf(ALPHA_MAX, oG);
@@ -1117,7 +969,8 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
       for (int f = 0; f < L::NF; ++f) gsh[f] += Y[f / 3] * gcol[f % 3];
       continue;
     }
-    const F A = co.x, B = co.y, Cc = co.z, op = co.w;
+    // the record's conic in Cholesky form (A, β, γ): B = A·β, C = γ + A·β² (fp64)
+    const F A = co.x, B = A * (F)co.y, Cc = (F)co.z + B * (F)co.y, op = co.w;
     // 2D gradients from the moments
     const F gu = -op * (A * m0.x + B * m0.y);
     const F gv = -op * (B * m0.x + Cc * m0.y);
@@ -1297,20 +1150,11 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
   }
 }
 
-// Pixels per thread of the raster kernels without acceptance lists (tuning
-// knob; DASS_FWD_PPT / DASS_BWD_PPT override the default, read once).
-static int ppt_from_env(const char* name, int dflt) {
-  const char* v = getenv(name);
-  if (!v) return dflt;
-  const int p = atoi(v);
-  return (p == 1 || p == 2 || p == 4 || p == 8) ? p : dflt;
-}
-
-// Acceptance-list workspace: cnt[2·ntiles] u32 | idx[2·capacity] u32 | bytes[2·capacity][32].
+// Acceptance-list workspace: cnt[ntiles] u32 | idx[capacity] u32 | bytes[capacity][32] | order[ntiles].
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 size_t accept_bytes(int ntiles, int64_t capacity) {
   const size_t c = (size_t)(capacity > 0 ? capacity : 1);
-  return al(sizeof(uint32_t) * 2 * (size_t)ntiles) + al(sizeof(uint32_t) * 2 * c) + al(32 * 2 * c) +
+  return al(sizeof(uint32_t) * (size_t)ntiles) + al(sizeof(uint32_t) * c) + al(32 * c) +
          al(sizeof(uint32_t) * (size_t)ntiles);
 }
 AcceptLists carve_accept(void* base, int ntiles, int64_t capacity) {
@@ -1318,45 +1162,23 @@ AcceptLists carve_accept(void* base, int ntiles, int64_t capacity) {
   char* p = (char*)base;
   AcceptLists a;
   a.cnt = (uint32_t*)p;
-  p += al(sizeof(uint32_t) * 2 * (size_t)ntiles);
+  p += al(sizeof(uint32_t) * (size_t)ntiles);
   a.idx = (uint32_t*)p;
-  p += al(sizeof(uint32_t) * 2 * c);
+  p += al(sizeof(uint32_t) * c);
   a.bytes = (uint8_t*)p;
-  p += al(32 * 2 * c);
+  p += al(32 * c);
   a.order = (uint32_t*)p;
+  a.cap = (uint32_t)(capacity > 0 ? capacity : 0);
   return a;
 }
 
-// list path kernel shape: 1 = one warp per tile (TW, default), 0 = two half-tile warps
-static bool tile_warp() {
-  static const bool v = [] {
-    const char* e = getenv("DASS_TILE_WARP");
-    return e ? atoi(e) != 0 : true;
-  }();
-  return v;
-}
-#ifndef TW_FWD_ORDER_SHIFT
-#define TW_FWD_ORDER_SHIFT 4   // forward launch order: list length in 16-entry buckets
-#endif
-#ifndef TW_BWD_ORDER_SHIFT
-#define TW_BWD_ORDER_SHIFT 3   // backward launch order: accepted entries in 8-entry buckets
-#endif
-#ifndef TW_FWD_MINB
-#define TW_FWD_MINB 32
-#endif
-#ifndef TW_BWD_MINB
-#define TW_BWD_MINB 32
-#endif
-static int fwd_ppt() { static const int p = ppt_from_env("DASS_FWD_PPT", 4); return p; }
-static int bwd_ppt() { static const int p = ppt_from_env("DASS_BWD_PPT", 4); return p; }
-static int bwd_minb() {
-  static const int m = [] {
-    const char* v = getenv("DASS_BWD_MINB");
-    const int p = v ? atoi(v) : 16;
-    return (p == 8 || p == 12 || p == 16) ? p : 16;
-  }();
-  return bwd_ppt() == 4 ? m : (bwd_ppt() == 1 ? 16 : (bwd_ppt() == 2 ? 8 : 16));
-}
+// Launch shapes, measured: launch order by list length in
+// 16-entry buckets (forward) / accepted entries in 8-entry buckets (backward);
+// 32 one-warp CTAs per SM (the hardware block limit).
+constexpr int TW_FWD_ORDER_SHIFT = 4;
+constexpr int TW_BWD_ORDER_SHIFT = 3;
+constexpr int TW_FWD_MINB = 32;
+constexpr int TW_BWD_MINB = 32;
 
 }  // namespace
 
@@ -1369,45 +1191,15 @@ cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const u
   const int ntiles = cam.tiles_x * cam.tiles_y;
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(accept, ntiles, capacity);
-    if (tile_warp()) {
-      tile_order_kernel<TW_FWD_ORDER_SHIFT><<<1, 1024, 0, s>>>(cam, ranges, nullptr, acc.order);
-      launch_counted();
-      render_fwd_tw_kernel<TW_FWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
-                                                           box, bg, out_img, out_T, out_last, acc);
-      launch_counted();
-      return cudaGetLastError();
-    }
-    static const int rpw = [] {
-      const char* e = getenv("DASS_FWD_RPW");
-      return e ? atoi(e) : 16;
-    }();
-    static const int fminb = [] {
-      const char* e = getenv("DASS_FWD_MINB");
-      return e ? atoi(e) : 12;
-    }();
-#define FWDL(R, M)                                                                               \
-  render_fwd_kernel<4, true, R, M><<<cam.tcount, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
-                                                         box, bg, out_img, out_T, out_last, acc)
-    if (rpw == 8) FWDL(8, 12);
-    else if (fminb == 16) FWDL(16, 16);
-    else if (fminb == 10) FWDL(16, 10);
-    else if (fminb == 8) FWDL(16, 8);
-    else FWDL(16, 12);
-#undef FWDL
+    tile_order_kernel<TW_FWD_ORDER_SHIFT><<<1, 1024, 0, s>>>(cam, ranges, nullptr, acc.order);
+    launch_counted();
+    render_fwd_tw_kernel<TW_FWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
+                                                                box, bg, out_img, out_T, out_last, acc);
     launch_counted();
     return cudaGetLastError();
   }
-  const AcceptLists none{nullptr, nullptr, nullptr, nullptr};
-#define FWD(P)                                                                                    \
-  render_fwd_kernel<P, false><<<cam.tcount, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, \
-                                                         box, bg, out_img, out_T, out_last, none)
-  switch (fwd_ppt()) {
-    case 1: FWD(1); break;
-    case 2: FWD(2); break;
-    case 8: FWD(8); break;
-    default: FWD(4); break;
-  }
-#undef FWD
+  render_fwd_kernel<4><<<cam.tcount, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, box, bg,
+                                                 out_img, out_T, out_last);
   launch_counted();
   return cudaGetLastError();
 }
@@ -1444,43 +1236,15 @@ cudaError_t launch_render_bwd_raster(const CamParams& cam, int n, const uint2* r
   const int ntiles = cam.tiles_x * cam.tiles_y;
   if (accept != nullptr) {
     const AcceptLists acc = carve_accept(const_cast<void*>(accept), ntiles, capacity);
-    if (tile_warp()) {
-      tile_order_kernel<TW_BWD_ORDER_SHIFT><<<1, 1024, 0, s>>>(cam, ranges, acc.cnt, acc.order);
-      launch_counted();
-      render_bwd_tw_kernel<TW_BWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg,
-                                                           out_T, dL_dimg, acc, g2d);
-      launch_counted();
-      return cudaGetLastError();
-    }
-    static const int lminb = [] {
-      const char* e = getenv("DASS_BWDL_MINB");
-      return e ? atoi(e) : 12;   // 80 registers: measured best (16 → 64 regs rematerialises)
-    }();
-#define BWDL(M)                                                                                  \
-  render_bwd_list_kernel<4, M><<<cam.tcount, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg, \
-                                                     out_T, dL_dimg, acc, g2d)
-    switch (lminb) {
-      case 8: BWDL(8); break;
-      case 10: BWDL(10); break;
-      case 12: BWDL(12); break;
-      default: BWDL(16); break;
-    }
-#undef BWDL
+    tile_order_kernel<TW_BWD_ORDER_SHIFT><<<1, 1024, 0, s>>>(cam, ranges, acc.cnt, acc.order);
+    launch_counted();
+    render_bwd_tw_kernel<TW_BWD_MINB><<<cam.tcount, 32, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb, bg,
+                                                                out_T, dL_dimg, acc, g2d);
     launch_counted();
     return cudaGetLastError();
   }
-#define BWD(P, MB)                                                                          \
-  render_bwd_raster_kernel<P, MB><<<cam.tcount, 256 / P, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, \
-                                                             rgb, box, bg, out_T, out_last, dL_dimg, g2d)
-  switch (bwd_ppt() * 100 + bwd_minb()) {
-    case 116: BWD(1, 4); break;
-    case 208: BWD(2, 8); break;
-    case 816: BWD(8, 16); break;
-    case 412: BWD(4, 12); break;
-    case 408: BWD(4, 8); break;
-    default: BWD(4, 16); break;
-  }
-#undef BWD
+  render_bwd_raster_kernel<4, 16><<<cam.tcount, 64, 0, s>>>(cam, ranges, ids, xy_depth, conic_opa, rgb,
+                                                            box, bg, out_T, out_last, dL_dimg, g2d);
   launch_counted();
   return cudaGetLastError();
 }

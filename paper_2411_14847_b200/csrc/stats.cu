@@ -46,9 +46,8 @@ __global__ void __launch_bounds__(256) stats_kernel(const __grid_constant__ CamP
       const __half2 lo = *reinterpret_cast<const __half2*>(&lo_bits);
       const float u = __fadd_rn(xy.x - (float)tx0, __low2float(lo));
       const float v = __fadd_rn(xy.y - (float)ty0, __high2float(lo));
-      const float4 co = conic_opa[id];
-      const ColTerms ct = col_terms(co.x, co.y, co.z, u - (float)(t & 15));
-      const float power = splat_power(ct, v - (float)(t >> 4));
+      const float4 co = conic_staged(conic_opa[id]);
+      const float power = splat_power(co, u - (float)(t & 15), v - (float)(t >> 4));
       if (power > 0.f) continue;
       const float alpha = splat_alpha(co.w, splat_exp(power));
       if (alpha < ALPHA_MIN) continue;

@@ -111,11 +111,12 @@ def lib():
         L.dass_bin_sort_views_workspace.argtypes = [i32, i32, i64, P]
         L.dass_bin_sort_views.argtypes = [P, i32, i32, P, P, P, P, C.c_size_t, i64, P, P, P, P]
         L.dass_render_accept_workspace.argtypes = [i32, i64, P]
-        L.dass_render_fwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, i64, P]
+        L.dass_render_fwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, C.c_size_t, i64, P]
         L.dass_render_bwd_workspace.argtypes = [i32, P]
         L.dass_render_bwd.argtypes = [P, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
-                                      P, i64, P, C.c_size_t, P, P, P, P, P, P, P]
-        L.dass_render_bwd_raster.argtypes = [P, i32, P, P, P, P, P, P, P, P, P, P, P, i64, P, P]
+                                      P, C.c_size_t, i64, P, C.c_size_t, P, P, P, P, P, P, P]
+        L.dass_render_bwd_raster.argtypes = [P, i32, P, P, P, P, P, P, P, P, P, P, P, C.c_size_t,
+                                             i64, P, P]
         L.dass_render_bwd_preprocess_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P,
                                                        P, P, P, P, P, P, P]
         L.dass_fidelity_loss_workspace.argtypes = [i32, i32, P]
@@ -138,9 +139,9 @@ def lib():
         L.dass_gather.argtypes = [i32, i32, P, P, P, P, P, i32, P, P, P, P, P, P, P]
         L.dass_render_features.argtypes = [P, P, P, P, P, P, i32, P, P, P]
         L.dass_render_fwd_tiles.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P,
-                                            i64, P]
+                                            C.c_size_t, i64, P]
         L.dass_render_bwd_raster_tiles.argtypes = [P, i32, i32, i32, i32, P, P, P, P, P, P, P, P,
-                                                   P, P, P, i64, P, P]
+                                                   P, P, P, C.c_size_t, i64, P, P]
         L.dass_render_bwd_preprocess_views_uv.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P,
                                                           P, P, P, P, P, P, P, P, P, P, P]
         L.dass_gradstat_from_uv.argtypes = [i32, i32, P, P, P]
@@ -154,6 +155,11 @@ def _check(status: int, where: str):
 
 
 _BAD_DTYPES = None
+
+
+def _nbytes(t) -> int:
+    """Size in bytes of a contiguous tensor (0 for None)."""
+    return 0 if t is None else t.numel() * t.element_size()
 
 
 def _ptr(t):
@@ -281,8 +287,8 @@ def dass_render_fwd(cam, tile_ranges, sorted_ids, xy_depth, conic_opa, rgb, box,
     _check(lib().dass_render_fwd_tiles(C.byref(c), int(tb), int(ts), int(tc), _ptr(tile_ranges),
                                        _ptr(sorted_ids), _ptr(xy_depth), _ptr(conic_opa),
                                        _ptr(rgb), _ptr(box), b, _ptr(out_img), _ptr(out_T),
-                                       _ptr(out_last), _ptr(accept), pair_capacity,
-                                       _stream(stream)), "dass_render_fwd")
+                                       _ptr(out_last), _ptr(accept), _nbytes(accept),
+                                       pair_capacity, _stream(stream)), "dass_render_fwd")
 
 
 def dass_render_bwd_workspace(n) -> int:
@@ -301,7 +307,8 @@ def dass_render_bwd(cam, sh_degree, pos_opa, scale, rot, sh, keep_mask, tile_ran
                                  _ptr(scale), _ptr(rot), _ptr(sh), _ptr(keep_mask),
                                  _ptr(tile_ranges), _ptr(sorted_ids), _ptr(xy_depth),
                                  _ptr(conic_opa), _ptr(rgb), _ptr(box), b, _ptr(out_T),
-                                 _ptr(out_last), _ptr(dL_dimg), _ptr(accept), pair_capacity,
+                                 _ptr(out_last), _ptr(dL_dimg), _ptr(accept), _nbytes(accept),
+                                 pair_capacity,
                                  _ptr(ws), ws.numel() * ws.element_size(), _ptr(g_pos_opa),
                                  _ptr(g_scale),
                                  _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum), _ptr(gradstat_cnt),
@@ -319,7 +326,8 @@ def dass_render_bwd_raster(cam, n, tile_ranges, sorted_ids, xy_depth, conic_opa,
                                               _ptr(tile_ranges), _ptr(sorted_ids), _ptr(xy_depth),
                                               _ptr(conic_opa), _ptr(rgb), _ptr(box), b,
                                               _ptr(out_T), _ptr(out_last), _ptr(dL_dimg),
-                                              _ptr(accept), pair_capacity, _ptr(g2d),
+                                              _ptr(accept), _nbytes(accept), pair_capacity,
+                                              _ptr(g2d),
                                               _stream(stream)), "dass_render_bwd_raster")
 
 

@@ -55,7 +55,7 @@ def test_library_is_sm100a_only(lib):
 
 def test_status_strings_and_version(lib):
     L = lib.lib()
-    assert lib.abi_version() == 1
+    assert lib.abi_version() == 2
     for s, txt in [(0, b"ok"), (1, b"invalid argument"), (4, b"pair capacity exceeded")]:
         assert L.dass_status_string(s) == txt
     assert L.dass_status_string(99) == b"unknown status"
@@ -173,4 +173,29 @@ def test_bin_sort_views_and_timestamp_validation_before_any_cuda_call(lib):
     assert L.dass_bin_sort_views(None, 2, 100, P, P, P, P, 0, 1000, P, P, P, P) == 1
     assert L.dass_timestamp(None, 0, P) == 1
     assert L.dass_timestamp(C.c_void_p(16), -1, P) == 1
+    assert lib.kernel_launches() == 0
+
+
+def test_accept_buffer_and_sort_size_validation_before_any_cuda_call(lib):
+    """ADVICE r1: the acceptance-list buffer's size is checked against
+    dass_render_accept_workspace (forward and every backward entry point), and
+    the sort refuses n, V·n ≥ 2^30 (30-bit look-back counts) instead of wrapping."""
+    L = lib.lib()
+    cam = lib.camera_struct(synth.tiny_camera(64, 48))
+    out = C.c_size_t(0)
+    cap = 5000
+    assert L.dass_render_accept_workspace(12, cap, C.byref(out)) == 0
+    need = out.value
+    d = C.c_void_p(256)   # a fake, 16-byte aligned device address: nothing is launched
+    fwd = lambda acc, nb, pc: L.dass_render_fwd(C.byref(cam), d, d, d, d, d, d, None, d, d, d,
+                                               acc, nb, pc, None)
+    assert fwd(d, need - 1, cap) == 1 and b"accept buffer" in L.dass_last_error()
+    assert fwd(C.c_void_p(260), need, cap) == 1                       # misaligned
+    assert fwd(d, need, 1 << 30) == 1                                 # capacity out of range
+    assert L.dass_render_bwd_raster(C.byref(cam), 100, d, d, d, d, d, d, None, d, d, d, d, need - 1,
+                                    cap, d, None) == 1
+    assert b"accept buffer" in L.dass_last_error()
+    assert L.dass_bin_sort_workspace(1 << 30, 12, 100, C.byref(out)) == 1
+    assert L.dass_bin_sort_views_workspace(4, 1 << 28, 100, C.byref(out)) == 1   # V·n = 2^30
+    assert L.dass_bin_sort_views_workspace(4, (1 << 28) - 1, 100, C.byref(out)) == 0
     assert lib.kernel_launches() == 0

@@ -62,8 +62,11 @@ def gpu_projection(rec):
     ulo = (lo & 0xFFFF).astype(np.uint16).view(np.float16).astype(np.float64)
     vlo = (lo >> 16).astype(np.uint16).view(np.float16).astype(np.float64)
     b4 = np.stack([box[:, 0] & 0xFFFF, box[:, 0] >> 16, box[:, 1] & 0xFFFF, box[:, 1] >> 16], 1)
+    # the record's conic is the Cholesky form (A, β, γ): B = A·β, C = γ + A·β² (dass.h)
+    A, beta, gam = (co[:, k].astype(np.float64) for k in range(3))
+    conic = np.stack([A, A * beta, gam + A * beta * beta], 1)
     return dict(u=xy[:, 0].astype(np.float64) + ulo, v=xy[:, 1].astype(np.float64) + vlo,
-                zbits=xy[:, 2].view(np.uint32), conic=co[:, :3], opa=co[:, 3], rgb=rgb[:, :3],
+                zbits=xy[:, 2].view(np.uint32), conic=conic, opa=co[:, 3], rgb=rgb[:, :3],
                 clampbits=rgb[:, 3].astype(np.int32), box=b4.astype(np.int32), tiles=tiles,
                 visible=(tiles > 0).astype(np.uint8))
 
