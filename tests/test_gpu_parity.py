@@ -495,3 +495,22 @@ def test_fidelity_loss_parity(W, H, lam, seed, off):
     d = np_(dL)
     rms = np.sqrt(np.mean(ref ** 2))
     assert np.all(np.abs(d - ref) <= 1e-3 * np.abs(ref) + 1e-3 * rms)
+
+
+def test_dense_tiles_sort_past_shared_memory():
+    """Tiles with lists of thousands of pairs (onesweep blocks of 2048 keys end
+    inside one tile's run): keys, ids and ranges stay bit-exact (A03/A04), and so
+    does the planar equal-depth case inside one long tile."""
+    cam = synth.tiny_camera(48, 48)
+    sc = synth.random_scene(12000, cam, seed=77)
+    g = np.random.default_rng(77)
+    # squeeze every mean into the central 2×2 tiles with small footprints
+    z = sc.pos_opa[:, 2]
+    sc.pos_opa[:, 0] = (g.uniform(-6, 6, sc.n) * z / cam.fx).astype(np.float32)
+    sc.pos_opa[:, 1] = (g.uniform(-6, 6, sc.n) * z / cam.fy).astype(np.float32)
+    sc.scale[:, :3] = (np.abs(sc.scale[:, :3]) * 0.3).astype(np.float32)
+    sc.pos_opa[:3000, 2] = 3.0              # a planar slice: equal depth bits, ordered by id
+    out = run_view(cam, sc, capacity=1 << 20)
+    r = out["ranges"]
+    assert (r[:, 1] - r[:, 0]).max() > 4096
+    check_binsort(cam, out, gpu_projection(out["rec"]))
