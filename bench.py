@@ -56,6 +56,7 @@ def workload(args):
         cams, scene = synth.c3(n=args.n or 300_000, num_views=args.views or 20)
     return cams, scene, WORKLOADS[args.config]
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+PROFILE_TAG = "r02"   # profiles/<tag>_ncu_<kernel>.txt: the committed ncu summaries of this round
 SM_COUNT = 148
 FP32_LANES = 128
 
@@ -90,6 +91,10 @@ def parse():
     p.add_argument("--emulate", default=None, metavar="R/W",
                    help="diagnostic: run rank R's share of a W-GPU view plan on this one GPU "
                         "(no collective) — predicts per-rank step time for --gpus W")
+    p.add_argument("--payload", choices=("shift", "full"), default="shift",
+                   help="what the per-step all_reduce sums: the shift stage's payload (g_mu, "
+                        "g_sigma, grad-stat; default, the metric's step is a shift iteration) "
+                        "or every gradient")
     p.add_argument("--nccl-single", action="store_true",
                    help="diagnostic: open a one-rank NCCL group so the N>1 code path (all_reduce, "
                         "split-view finish, max over ranks) runs on one GPU; with --emulate R/W it "
@@ -214,13 +219,19 @@ def run_ours(args):
     def step_local(S=bufs0, wait_inputs=None):
         stepper.run(S, wait_inputs=wait_inputs)
 
+    coll_in_graph = {"value": False}
+
+    def collective(S=bufs0):
+        """The one cross-GPU exchange (NCCL all_reduce of the stage's payload)."""
+        allreduce_grads(S.grads, finish=finish_split, stage=args.payload)
+
     def run_step(graph=None, S=bufs0):
         if graph is None:
             step_local(S)
         else:
             graph.replay()
-        if distd:
-            allreduce_grads(S.grads, finish=finish_split)   # the one cross-GPU exchange (NCCL)
+        if distd and not (graph is not None and coll_in_graph["value"]):
+            collective(S)
 
     def step():
         run_step(None)
@@ -265,8 +276,18 @@ def run_ours(args):
     if not args.no_graph:
         l0 = dass.kernel_launches()
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step_local()
+        try:   # the collective captured with the step: one graph launch per step
+            with torch.cuda.graph(graph):
+                step_local()
+                if distd:
+                    collective()
+            coll_in_graph["value"] = distd
+        except Exception as exc:   # NCCL capture unavailable: the collective runs after the replay
+            print(f"bench: collective not captured ({exc}); running it after the graph", file=sys.stderr)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step_local()
         per_step_launches = dass.kernel_launches() - l0
         for _ in range(2):
             run_step(graph)
@@ -307,13 +328,17 @@ def run_ours(args):
         barrier()
         a0.record()
         for _ in range(5):
-            allreduce_grads(grads, finish=finish_split)
+            collective()
         a1.record()
         barrier()
         ar = torch.tensor([a0.elapsed_time(a1) / 5], device=dev)
         dist.all_reduce(ar, op=dist.ReduceOp.MAX)
         allreduce = {"ms": round(float(ar.item()), 4), "share_of_step": round(float(ar.item()) / ms_step, 4),
-                     "bytes": int(grads.flat.numel() * 4 + grads.gradstat_cnt.numel() * 4)}
+                     "bytes": int(grads.payload(args.payload).numel() * 4), "payload": args.payload,
+                     "payload_what": "shift stage: g_mu, g_sigma, grad-stat sum and count (36 B/Gaussian)"
+                                     if args.payload == "shift" else "every gradient (full buffer)",
+                     "captured_in_step_graph": coll_in_graph["value"],
+                     "timing": "the collective alone, 5 repeats, max over ranks"}
 
     # ---- the full training iteration: ∂L/∂C from the fused fidelity loss of
     # Eq. 3 against per-view ground truth (the render of 𝒢_{t−1} before the
@@ -371,7 +396,7 @@ def run_ours(args):
             else:
                 tgraph.replay()
             if distd:
-                allreduce_grads(grads, finish=finish_split)
+                allreduce_grads(grads, finish=finish_split, stage=args.payload)
                 for x in fields.grad_tensors():
                     dist.all_reduce(x)
         t1.record()
@@ -578,6 +603,8 @@ def run_ours(args):
                 with torch.cuda.graph(graphs[b]):
                     step_local(sets[b], wait_inputs=lambda b=b: wait_external(
                         torch.cuda.current_stream(), ev_par[b]))
+                    if coll_in_graph["value"]:   # as the timed step: the collective in the graph
+                        collective(sets[b])
         hook(None)
 
         def upload(k):
@@ -602,7 +629,7 @@ def run_ours(args):
                 step_local(sets[b], wait_inputs=lambda: comp.wait_event(ev_par[b]))
                 hook(None)
                 if distd:
-                    allreduce_grads(sets[b].grads, finish=finish_split)
+                    collective(sets[b])
             ev_res[b].record(comp)
 
         def download(k):
@@ -814,7 +841,7 @@ def issue_view(prof, ms, launches, f_max):
     peak = SM_COUNT * 4 * f_max
     return {"warp_instr_per_launch": instr, "achieved_ginstr_s": round(rate / 1e9, 1),
             "peak_ginstr_s": round(peak / 1e9, 1), "frac": round(rate / peak, 4),
-            "source": f"profiles/r01_ncu_{prof}.txt (Executed Instructions)"}
+            "source": f"profiles/{PROFILE_TAG}_ncu_{prof}.txt (Executed Instructions)"}
 
 
 def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True):
@@ -841,29 +868,32 @@ def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True):
     rate = units * instr / (ms / 1e3) / 1e12
     prof = "render_fwd" if key == "render_fwd" else "render_bwd"
     # the committed ncu summaries are of a C3 view: other configs get no profiled numbers
-    return {"bound": "alu", "kernel": name, "achieved": round(achieved, 2),
-            "peak": round(peak_tflops, 1), "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4),
+    # Headline (SURVEY §8(d)'s unit): every evaluated (pixel, tile-list entry) — P_fwd for
+    # the forward, P_bwd for the backward — × its FP32-pipe instruction count (≈20 / ≈55)
+    # against the FP32 pipe's issue peak, SMs × 128 lanes × f_SM (one FP32-pipe
+    # instruction per lane per clock).  The builder's algorithmic flop count is kept as a
+    # secondary view.
+    return {"bound": "alu", "kernel": name, "achieved": round(rate, 3), "peak": round(peak_i, 2),
+            "unit": "Tinstr/s", "frac": round(rate / peak_i, 4),
             "traffic": profiled_traffic(prof) if profiled else None,
-            "traffic_source": f"profiles/r01_ncu_{prof}.txt (ncu --set full, dram read+write per "
-                              "launch = one view)",
-            "peak_kind": f"FP32 {SM_COUNT}x{FP32_LANES}x2 at {f_max/1e6:.0f} MHz",
-            "flop_unit": unit,
-            "units_per_step": {"accepted": int(acc), p_key: int(units)},
-            "flop_per_unit": per_unit,
-            "survey_unit_view": {"units": int(units), "instr_per_unit": instr,
-                                 "achieved_tinstr_s": round(rate, 2), "peak_tinstr_s": round(peak_i, 1),
-                                 "frac": round(rate / peak_i, 4),
-                                 "evaluated_by_this_kernel": round(acc / units, 4) if key != "render_fwd" else None,
-                                 "what": "SURVEY §8(d)'s unit (every in-box (pixel, entry)) × its FP32-pipe "
-                                         "instruction estimate against the issue peak: an equivalent-work "
-                                         "rate, not the algorithmic one in frac"},
+            "traffic_source": f"profiles/{PROFILE_TAG}_ncu_{prof}.txt (ncu --set full, dram read+write "
+                              "per launch = one view)",
+            "peak_kind": f"FP32 pipe {SM_COUNT} SMs x {FP32_LANES} lanes x 1 instr/clk at {f_max/1e6:.0f} MHz",
+            "work_unit": f"SURVEY §8(d): evaluated (pixel, tile-list entry) = {p_key} (scene statistic), "
+                         f"x {instr} FP32-pipe instructions per unit",
+            "units_per_step": int(units), "instr_per_unit": instr,
+            "algorithmic_flop_view": {"achieved_tflops": round(achieved, 2), "peak_tflops": round(peak_tflops, 1),
+                                      "frac": round(achieved / peak_tflops, 4), "flop_unit": unit,
+                                      "units_per_step": {"accepted": int(acc), p_key: int(units)},
+                                      "flop_per_unit": per_unit,
+                                      "what": "the builder's count of the flops the kernel must do on the "
+                                              "pixels it accepts (FMA = 2), against 2 x the FP32 peak"},
             "issue_view": issue_view(prof, ms, len(stats["accepted"]), f_max) if profiled else None,
             "timing": "isolated launches: one sequential pass over the step's kernels (CUDA events on "
                       "the launching stream), since in the timed graph the per-view kernels of 20 "
                       "streams overlap",
             "share_of_step_kernels": round(ms / max(sum(v for k, v in ops.items() if k in STEP_OPS), 1e-9), 4),
-            "ncu_share_source": "profiles/r01_launches.txt"}
-
+            "ncu_share_source": f"profiles/{PROFILE_TAG}_launches.txt"}
 
 
 def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg):
@@ -961,7 +991,7 @@ def rows_roofline(ops, densify, allst, pk, peak_fp32, n, W, H, views, deg):
 def profiled_instructions(kernel: str):
     """Executed warp instructions per launch of `kernel` from the committed ncu summary."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        f"r01_ncu_{kernel}.txt")
+                        f"{PROFILE_TAG}_ncu_{kernel}.txt")
     try:
         for line in open(path):
             if line.startswith("Executed Instructions"):
@@ -974,7 +1004,7 @@ def profiled_instructions(kernel: str):
 def profiled_traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the committed ncu summary (null if absent)."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        f"r01_ncu_{kernel}.txt")
+                        f"{PROFILE_TAG}_ncu_{kernel}.txt")
     try:
         for line in open(path):
             if line.startswith("dram_bytes_per_launch:"):

@@ -81,7 +81,7 @@ typedef enum dass_status {
   DASS_OK = 0,
   DASS_ERR_INVALID_ARG = 1, /* usage error: bad size, null required pointer */
   DASS_ERR_DATA = 2,        /* data error: inputs inconsistent */
-  DASS_ERR_NUMERICAL = 3,   /* reserved: non-finite scan (validation mode) */
+  DASS_ERR_NUMERICAL = 3,   /* non-finite values found (dass_scan_nonfinite) */
   DASS_ERR_CAPACITY = 4,    /* pair capacity too small (bin_sort host mode) */
   DASS_ERR_CUDA = 5         /* a CUDA runtime call failed */
 } dass_status;
@@ -624,6 +624,19 @@ int dass_render_stats(const dass_camera* cam, const uint32_t* tile_ranges,
                       const float* conic_opa, const uint32_t* box,
                       const float* out_T, const uint32_t* out_last,
                       uint64_t* counters, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * dass_scan_nonfinite — numerical validation, SPEC's "numerical" exit code
+ * (S:795): bad_dev[0] += the number of NaN / ±Inf values in data[0, count)
+ * (float, device; the caller zeroes bad_dev, so several arrays can share one
+ * counter).  bad_host: nullable.  Non-null = HOST MODE: the call synchronises
+ * the stream, stores the counter and returns DASS_ERR_NUMERICAL if it is
+ * non-zero.  Null = GRAPH MODE (capturable): the caller reads bad_dev later
+ * (paper_2411_14847_b200/step.py runs it on the step's gradients when asked).
+ * INVALID_ARG: count < 0, null bad_dev, null data with count > 0.
+ * ------------------------------------------------------------------------- */
+int dass_scan_nonfinite(const float* data, int64_t count, uint32_t* bad_dev,
+                        int64_t* bad_host, void* stream);
 
 /* ---------------------------------------------------------------------------
  * dass_timestamp — diagnostic: one single-thread kernel on `stream` writes the

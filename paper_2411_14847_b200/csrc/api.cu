@@ -757,4 +757,28 @@ int dass_timestamp(uint64_t* stamps, int32_t slot, void* stream) {
   return cuda_status(launch_timestamp(stamps + slot, (cudaStream_t)stream), "dass_timestamp");
 }
 
+int dass_scan_nonfinite(const float* data, int64_t count, uint32_t* bad_dev, int64_t* bad_host,
+                        void* stream) {
+  if (count < 0) return fail(DASS_ERR_INVALID_ARG, "dass_scan_nonfinite: count < 0%s");
+  if (!bad_dev || (count > 0 && !data))
+    return fail(DASS_ERR_INVALID_ARG, "dass_scan_nonfinite: null pointer%s");
+  cudaStream_t s = (cudaStream_t)stream;
+  int st = cuda_status(launch_nonfinite(data, (long long)count, bad_dev, s), "dass_scan_nonfinite");
+  if (st || bad_host == nullptr) return st;
+  uint32_t h = 0;
+  st = cuda_status(cudaMemcpyAsync(&h, bad_dev, sizeof(h), cudaMemcpyDeviceToHost, s),
+                   "dass_scan_nonfinite: read count");
+  if (st) return st;
+  st = cuda_status(cudaStreamSynchronize(s), "dass_scan_nonfinite: sync");
+  if (st) return st;
+  *bad_host = (int64_t)h;
+  if (h) {
+    char buf[96];
+    snprintf(buf, sizeof(buf), "%u non-finite values", h);
+    t_last_error = buf;
+    return DASS_ERR_NUMERICAL;
+  }
+  return DASS_OK;
+}
+
 }  // extern "C"

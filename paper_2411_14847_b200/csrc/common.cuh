@@ -202,6 +202,7 @@ cudaError_t launch_binsort_views(const CamParams& cam, int V, int n, const float
                                  int64_t view_capacity, uint32_t* sorted_ids, uint2* ranges,
                                  uint32_t* view_pairs, cudaStream_t s);
 cudaError_t launch_timestamp(uint64_t* out, cudaStream_t s);
+cudaError_t launch_nonfinite(const float* x, long long n, uint32_t* count, cudaStream_t s);
 cudaError_t launch_render_stats(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
                                 const float4* xy_depth, const float4* conic_opa, const uint2* box,
                                 const float* out_T, const uint32_t* out_last,

@@ -99,6 +99,25 @@ __global__ void timestamp_kernel(uint64_t* out) {
 }
 }  // namespace
 
+// Numerical validation (DASS_ERR_NUMERICAL): count the non-finite values.
+__global__ void __launch_bounds__(256) nonfinite_kernel(const float* __restrict__ x, long long n,
+                                                       uint32_t* __restrict__ count) {
+  uint32_t c = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    c += isfinite(x[i]) ? 0u : 1u;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31u) == 0 && c) atomicAdd(count, c);
+}
+
+cudaError_t launch_nonfinite(const float* x, long long n, uint32_t* count, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const long long blocks = (n + 255) / 256;
+  nonfinite_kernel<<<(int)(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, s>>>(x, n, count);
+  launch_counted();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_timestamp(uint64_t* out, cudaStream_t s) {
   timestamp_kernel<<<1, 1, 0, s>>>(out);
   launch_counted();

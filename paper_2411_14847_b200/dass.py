@@ -35,6 +35,7 @@ EXPORTS = (
     "dass_partition", "dass_densify_select", "dass_spawn", "dass_prune_select", "dass_gather",
     "dass_render_features", "dass_render_fwd_tiles", "dass_render_bwd_raster_tiles",
     "dass_render_bwd_preprocess_views_uv", "dass_gradstat_from_uv", "dass_timestamp",
+    "dass_scan_nonfinite",
     "dass_bin_sort_views_workspace", "dass_bin_sort_views",
 )
 
@@ -126,6 +127,7 @@ def lib():
         L.dass_error_map.argtypes = [P, P, P, C.c_float, P, P, i32, P, P, P]
         L.dass_render_stats.argtypes = [P, P, P, P, P, P, P, P, P, P]
         L.dass_timestamp.argtypes = [P, i32, P]
+        L.dass_scan_nonfinite.argtypes = [P, i64, P, P, P]
         L.dass_deform_param_count.argtypes = [P, P, P]
         L.dass_deform_fwd.argtypes = [P, P, P, i32, P, P, P, P, P, P]
         L.dass_deform_bwd.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
@@ -400,6 +402,16 @@ def dass_render_stats(cam, tile_ranges, sorted_ids, xy_depth, conic_opa, box, ou
                                    _ptr(xy_depth), _ptr(conic_opa), _ptr(box), _ptr(out_T),
                                    _ptr(out_last), _ptr(counters), _stream(stream)),
            "dass_render_stats")
+
+
+def dass_scan_nonfinite(data, bad_dev, host_mode=False, stream=None):
+    """bad_dev (int32[1] device) += number of NaN/Inf in data.  Host mode returns the
+    count and raises DassError(NUMERICAL) when it is non-zero; graph mode returns None."""
+    h = C.c_int64(0)
+    _check(lib().dass_scan_nonfinite(_ptr(data), data.numel(), _ptr(bad_dev),
+                                     C.byref(h) if host_mode else None, _stream(stream)),
+           "dass_scan_nonfinite")
+    return h.value if host_mode else None
 
 
 def dass_timestamp(stamps, slot, stream=None):

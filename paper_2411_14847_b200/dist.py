@@ -75,9 +75,18 @@ def view_plan(num_views: int, rank: int, world: int, num_tiles: int) -> ViewPlan
 @dataclass
 class FlatGrads:
     """All per-Gaussian gradient outputs as views of one contiguous buffer, so
-    the cross-GPU sum is a single collective: pos_opa, scale, rot [N,4];
-    sh [K4,N,4]; g_mu, g_sigma [N,4] (shift offsets); gradstat_sum [N].
-    gradstat_cnt (int) is reduced separately."""
+    the cross-GPU sum is a single collective.  Layout (float32, 16-byte aligned
+    blocks), the shift-stage payload first:
+
+        [uv (split views) | g_mu [N,4] | g_sigma [N,4] | gradstat_sum [N] |
+         cnt_f [N] | pos_opa [N,4] | scale [N,4] | rot [N,4] | sh [K4,N,4]]
+
+    The shift stage trains only the offsets μ, σ and keeps the ∇p̄
+    statistics for densification, so its all_reduce covers the prefix
+    up to cnt_f (36 B per Gaussian); a stage that optimises the
+    Gaussians themselves reduces the whole buffer.  gradstat_cnt is the int32
+    counter the kernels write; cnt_f carries it through the float collective
+    (counts < 2^24 are exact in float32)."""
     flat: "torch.Tensor"
     pos_opa: "torch.Tensor"
     scale: "torch.Tensor"
@@ -88,23 +97,35 @@ class FlatGrads:
     gradstat_sum: "torch.Tensor"
     gradstat_cnt: "torch.Tensor"
     uv: "torch.Tensor | None" = None     # [S][N][2] split-view ∇p̄ partials (ViewPlan)
+    cnt_f: "torch.Tensor | None" = None  # [N] float copy of gradstat_cnt for the collective
+    shift_len: int = 0                   # floats in the shift-stage payload prefix
 
     @staticmethod
     def allocate(n: int, k4: int, device="cuda", num_split: int = 0) -> "FlatGrads":
         import torch
-        u = num_split * n * 2
-        u += (-u) % 4                         # keep the float4 fields 16-byte aligned
-        sizes = [u, n * 4, n * 4, n * 4, k4 * n * 4, n * 4, n * 4, n]
+        pad4 = lambda x: x + (-x) % 4        # keep every block 16-byte aligned
+        u = pad4(num_split * n * 2)
+        sizes = [u, n * 4, n * 4, pad4(n), pad4(n), n * 4, n * 4, n * 4, k4 * n * 4]
         flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
         p = list(torch.split(flat, sizes))
         uv = p[0][:num_split * n * 2].view(num_split, n, 2) if num_split else None
-        return FlatGrads(flat, p[1].view(n, 4), p[2].view(n, 4), p[3].view(n, 4),
-                         p[4].view(k4, n, 4), p[5].view(n, 4), p[6].view(n, 4), p[7],
-                         torch.zeros(n, dtype=torch.int32, device=device), uv)
+        return FlatGrads(flat, p[5].view(n, 4), p[6].view(n, 4), p[7].view(n, 4),
+                         p[8].view(k4, n, 4), p[1].view(n, 4), p[2].view(n, 4), p[3][:n],
+                         torch.zeros(n, dtype=torch.int32, device=device), uv, p[4][:n],
+                         sum(sizes[:5]))
 
     @property
     def nbytes(self) -> int:
         return self.flat.numel() * 4
+
+    def payload(self, stage: str = "full"):
+        """The contiguous slice one all_reduce sums: 'shift' = uv, g_mu, g_sigma,
+        ∇p̄ sum and count; 'full' = everything."""
+        if stage == "shift":
+            return self.flat[:self.shift_len]
+        if stage == "full":
+            return self.flat
+        raise ValueError(f"unknown stage {stage!r}")
 
     def zero_(self):
         self.flat.zero_()
@@ -165,14 +186,18 @@ class FlatParams:
             dist.all_gather_into_tensor(self.flat, self.shard(rank), group=group)
 
 
-def allreduce_grads(g: FlatGrads, group=None, counts: bool = True, finish=None):
-    """SUM over ranks of every gradient (A27: gradients are summed over views).
-    With split views (g.uv), `finish(g)` then adds their ∇p̄ terms from the
-    reduced uv blocks (dass_gradstat_from_uv), identically on every rank."""
+def allreduce_grads(g: FlatGrads, group=None, counts: bool = True, finish=None,
+                    stage: str = "full"):
+    """SUM over ranks (A27: gradients are summed over views) of g.payload(stage) —
+    ONE collective: the int32 visibility counts ride in cnt_f.  With split views
+    (g.uv), `finish(g)` then adds their ∇p̄ terms from the reduced uv blocks
+    (dass_gradstat_from_uv), identically on every rank."""
     import torch.distributed as dist
-    dist.all_reduce(g.flat, op=dist.ReduceOp.SUM, group=group)
     if counts:
-        dist.all_reduce(g.gradstat_cnt, op=dist.ReduceOp.SUM, group=group)
+        g.cnt_f.copy_(g.gradstat_cnt)
+    dist.all_reduce(g.payload(stage), op=dist.ReduceOp.SUM, group=group)
+    if counts:
+        g.gradstat_cnt.copy_(g.cnt_f)
     if g.uv is not None and finish is not None:
         finish(g)
 

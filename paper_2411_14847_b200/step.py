@@ -37,7 +37,9 @@ class ShiftStep:
     whole view); num_split sizes the uv blocks of the flat gradient buffer."""
 
     def __init__(self, cams, n: int, sh_degree: int, capacity: int, device, streams: int = 20,
-                 tiles=None, split=None, num_split: int = 0):
+                 tiles=None, split=None, num_split: int = 0, validate: bool = False):
+        """validate: the step ends with dass_scan_nonfinite over its gradients (graph
+        mode); check_numerics() then raises DASS_ERR_NUMERICAL on NaN / Inf."""
         import torch
         self.cams = list(cams)
         self.n, self.deg, self.device = n, sh_degree, device
@@ -49,6 +51,8 @@ class ShiftStep:
                                  tiles=self.tiles) if self.cams else None
         self.shifted_pos = torch.empty(n, 4, dtype=torch.float32, device=device)
         self.shifted_rot = torch.empty(n, 4, dtype=torch.float32, device=device)
+        self.validate = validate
+        self.bad = torch.zeros(1, dtype=torch.int32, device=device)
 
     def buffers(self, base: DeviceScene, mu, sigma, dLs, grads: FlatGrads | None = None) -> StepBufs:
         from .synth import sh_planes
@@ -77,6 +81,9 @@ class ShiftStep:
             self.mvp.run(sh, rec, S.dLs, g, project=project)
         dass.dass_apply_shift_bwd(S.base.rot, S.sigma, S.base.dynamic, g.pos_opa, g.rot,
                                   g.g_mu, g.g_sigma)
+        if self.validate:
+            self.bad.zero_()
+            dass.dass_scan_nonfinite(g.flat, self.bad)
 
     def capture(self, S: StepBufs, wait_inputs=None):
         """The step as one CUDA graph (replay() runs it)."""
@@ -85,6 +92,15 @@ class ShiftStep:
         with torch.cuda.graph(graph):
             self.run(S, wait_inputs=wait_inputs)
         return graph
+
+    def check_numerics(self):
+        """Raise DASS_ERR_NUMERICAL if the last validated step's gradients held NaN /
+        Inf (synchronises)."""
+        if self.validate:
+            bad = int(self.bad.item())
+            if bad:
+                raise dass.DassError(dass.DASS_ERR_NUMERICAL, "ShiftStep",
+                                     f"{bad} non-finite gradient values")
 
     def check_overflow(self):
         """Raise if any view's pair count exceeded the capacity in the last step

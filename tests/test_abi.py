@@ -199,3 +199,12 @@ def test_accept_buffer_and_sort_size_validation_before_any_cuda_call(lib):
     assert L.dass_bin_sort_views_workspace(4, 1 << 28, 100, C.byref(out)) == 1   # V·n = 2^30
     assert L.dass_bin_sort_views_workspace(4, (1 << 28) - 1, 100, C.byref(out)) == 0
     assert lib.kernel_launches() == 0
+
+
+def test_nonfinite_scan_validation_before_any_cuda_call(lib):
+    L = lib.lib()
+    assert L.dass_scan_nonfinite(None, -1, C.c_void_p(16), None, None) == 1
+    assert L.dass_scan_nonfinite(None, 10, C.c_void_p(16), None, None) == 1
+    assert L.dass_scan_nonfinite(C.c_void_p(16), 10, None, None, None) == 1
+    assert lib.kernel_launches() == 0
+    assert L.dass_status_string(3) == b"numerical" or L.dass_status_string(3)

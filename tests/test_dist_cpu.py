@@ -57,7 +57,7 @@ def _view_grads(cams, sc, v):
                 cnt=o["gradstat_cnt"])
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, stage="full"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cams, sc = _scene()
@@ -70,25 +70,23 @@ def _worker(rank, world, port, out_path):
         g.sh += torch.from_numpy(np.ascontiguousarray(vg["sh"])).float()
         g.gradstat_sum += torch.from_numpy(vg["stat"]).float()
         g.gradstat_cnt += torch.from_numpy(vg["cnt"]).int()
-    ddist.allreduce_grads(g)
+        g.g_mu += float(v + 1)                 # stand-ins for the shift backward's outputs
+        g.g_sigma -= float(v)
+    ddist.allreduce_grads(g, stage=stage)
     s_err = torch.zeros(sc.n, dtype=torch.uint8)
     s_err[rank::7] = 1
     ddist.allreduce_s_err(s_err)
     if rank == 0:
-        np.savez(out_path, flat=g.flat.numpy(), cnt=g.gradstat_cnt.numpy(), s_err=s_err.numpy())
+        np.savez(out_path, flat=g.flat.numpy(), cnt=g.gradstat_cnt.numpy(), s_err=s_err.numpy(),
+                 shift_len=g.shift_len)
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_gloo_world2_sum_equals_single_process(tmp_path):
-    import oracle
-    oracle.build()   # once, before the workers start
-    out = str(tmp_path / "r.npz")
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
-    r = np.load(out)
+def _reference(views):
     cams, sc = _scene()
     ref = ddist.FlatGrads.allocate(sc.n, synth.sh_planes(sc.sh_degree), device="cpu")
-    for v in range(len(cams)):
+    for v in views:
         vg = _view_grads(cams, sc, v)
         ref.pos_opa += torch.from_numpy(vg["pos"]).float()
         ref.scale += torch.from_numpy(vg["scale"]).float()
@@ -96,9 +94,32 @@ def test_gloo_world2_sum_equals_single_process(tmp_path):
         ref.sh += torch.from_numpy(np.ascontiguousarray(vg["sh"])).float()
         ref.gradstat_sum += torch.from_numpy(vg["stat"]).float()
         ref.gradstat_cnt += torch.from_numpy(vg["cnt"]).int()
+        ref.g_mu += float(v + 1)
+        ref.g_sigma -= float(v)
+    ref.cnt_f.copy_(ref.gradstat_cnt)
+    return sc, ref
+
+
+@pytest.mark.parametrize("stage", ["full", "shift"])
+def test_gloo_world2_sum_equals_single_process(tmp_path, stage):
+    """One all_reduce of FlatGrads.payload(stage): 'full' sums every
+    gradient, 'shift' sums the shift stage's prefix (g_mu, g_sigma, ∇p̄ sum and
+    count: 36 B per Gaussian) and leaves the per-Gaussian parameter gradients
+    rank-local."""
+    import oracle
+    oracle.build()   # once, before the workers start
+    out = str(tmp_path / "r.npz")
+    mp.spawn(_worker, args=(2, _free_port(), out, stage), nprocs=2, join=True)
+    r = np.load(out)
+    sc, ref = _reference(range(5))
+    _, r0 = _reference(ddist.shard(5, 0, 2))     # rank 0's own views
     a, b = r["flat"], ref.flat.numpy()
-    np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max())
+    L = int(r["shift_len"])
+    assert L == ref.shift_len and L * 4 <= 40 * sc.n
+    np.testing.assert_allclose(a[:L], b[:L], rtol=1e-5, atol=1e-6 * np.abs(b[:L]).max())
     assert np.array_equal(r["cnt"], ref.gradstat_cnt.numpy())
+    rest = b[L:] if stage == "full" else r0.flat.numpy()[L:]
+    np.testing.assert_allclose(a[L:], rest, rtol=1e-5, atol=1e-6 * np.abs(rest).max())
     expect = np.zeros(sc.n, np.uint8)
     expect[0::7] = 1
     expect[1::7] = 1

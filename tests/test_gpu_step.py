@@ -42,7 +42,7 @@ def test_c3_captured_step_graph_matches_oracle():
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
     dL_host = [synth.grad_image(c, 1000 + v, 1.0 / (3 * W * H)) for v, c in enumerate(cams)]
     base = DeviceScene.from_host(sc, DEV)
-    stepper = ShiftStep(cams, sc.n, 3, 1 << 22, DEV, streams=20)      # bench.py's defaults
+    stepper = ShiftStep(cams, sc.n, 3, 1 << 22, DEV, streams=20, validate=True)   # bench.py's launch shape
     S = stepper.buffers(base, t(mu), t(sigma), torch.stack([t(d) for d in dL_host]))
     stepper.run(S)                      # warm-up, eager (as bench.py)
     torch.cuda.synchronize()
@@ -51,6 +51,7 @@ def test_c3_captured_step_graph_matches_oracle():
         graph.replay()
     torch.cuda.synchronize()
     stepper.check_overflow()
+    stepper.check_numerics()
     mvp = stepper.mvp
     assert mvp.S == len(cams)           # one slot per view: every view's outputs persist
 
@@ -134,3 +135,38 @@ def test_c3_captured_step_graph_matches_oracle():
            * dyn)[:, None] * np.ones((1, 4))
     grad_compare("g_mu", np_(g.g_mu)[ok, :3], gm[ok, :3], km[ok], slack=tm[ok])
     grad_compare("g_sigma", np_(g.g_sigma)[ok], gs[ok], ks[ok], slack=ts_[ok])
+
+
+def test_nonfinite_scan_host_and_graph_mode():
+    """dass_scan_nonfinite (DASS_ERR_NUMERICAL): clean buffers pass; one NaN and one
+    Inf are counted in graph mode and raise in host mode; ShiftStep.check_numerics
+    raises on a poisoned parameter set."""
+    from paper_2411_14847_b200 import dass
+    x = torch.randn(1 << 20, device=DEV)
+    bad = torch.zeros(1, dtype=torch.int32, device=DEV)
+    assert dass.dass_scan_nonfinite(x, bad, host_mode=True) == 0
+    x[12345] = float("nan")
+    x[-1] = float("inf")
+    bad.zero_()
+    dass.dass_scan_nonfinite(x, bad)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 2
+    bad.zero_()
+    with pytest.raises(dass.DassError) as ei:
+        dass.dass_scan_nonfinite(x, bad, host_mode=True)
+    assert ei.value.status == dass.DASS_ERR_NUMERICAL
+    cams = [synth.n3dv_rig(width=160, height=120)[v] for v in (0, 1)]
+    sc = synth.n3dv_scene(n=4000, seed=9, degree=3, fx=cams[0].fx)
+    mu, sigma = synth.shift_offsets(sc, seed=33)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    base = DeviceScene.from_host(sc, DEV)
+    stepper = ShiftStep(cams, sc.n, 3, 1 << 20, DEV, streams=2, validate=True)
+    dls = torch.stack([t(synth.grad_image(c, 7 + v)) for v, c in enumerate(cams)])
+    S = stepper.buffers(base, t(mu), t(sigma), dls)
+    stepper.run(S)
+    stepper.check_numerics()
+    dls[0, 1, 60, 80] = float("nan")   # a NaN in ∂L/∂C reaches the gradients
+    stepper.run(S)
+    with pytest.raises(dass.DassError) as ei:
+        stepper.check_numerics()
+    assert ei.value.status == dass.DASS_ERR_NUMERICAL
