@@ -36,9 +36,15 @@ METRIC = "fwd+bwd views/sec (Mpix/s) at 300k Gaussians, 1352x1014, 1/2/4/8 B200"
 WORKLOAD = ("C3: N3DV-shaped timestep, 20 views 1352x1014, 300k Gaussians SH3, 30% dynamic "
             "masked shift; step = one shift iteration (shift + fwd+bwd over all views)")
 WORKLOADS = {
+    "c1": ("C1: 1 camera 64x64, 1k random Gaussians, SH degree 0; step = one fwd+bwd "
+           "(project, bin/sort, composite, raster + preprocess backward)"),
+    "c2": ("C2: 1 camera 1352x1014 (N3DV rig centre view), 300k Gaussians SH3; step = one fwd+bwd "
+           "(project, bin/sort, composite, raster + preprocess backward)"),
     "c3": WORKLOAD,
-    "c4": ("C4: Meet-Room-shaped timestep, 13 views 1280x720, 200k Gaussians SH3, 30% dynamic "
-           "masked shift; step = one shift iteration (shift + fwd+bwd over all views)"),
+    "c4": ("C4: Meet-Room-shaped timestep, 13 views 1280x720, 200k Gaussians SH3 grown to 260k by "
+           "error-guided densification before the timed iterations (13 error maps vs GT, Eq. 4, "
+           "spawn K=2); step = one shift iteration at 260k (shift + fwd + error map + bwd over all "
+           "views)"),
     "c5": ("C5: 20 views 1352x1014, 1M Gaussians SH3 (sigma_px median x sqrt(0.3)), 30% dynamic "
            "masked shift; step = one shift iteration (shift + fwd+bwd over all views)"),
 }
@@ -47,6 +53,12 @@ WORKLOADS = {
 def workload(args):
     """(cameras, scene, workload string) of --config, with --n / --views overrides."""
     from paper_2411_14847_b200 import synth
+    if args.config == "c1":
+        cam, scene = synth.c1()
+        return [cam], scene, WORKLOADS["c1"]
+    if args.config == "c2":
+        cam, scene = synth.c2(n=args.n or 300_000)
+        return [cam], scene, WORKLOADS["c2"]
     if args.config == "c4":
         cams, scene = synth.c4(n=args.n or 200_000, num_views=args.views or 13)
     elif args.config == "c5":
@@ -74,8 +86,9 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", choices=("c3", "c4", "c5"), default="c3",
-                   help="BASELINE.json workload: c3 (default, the metric's), c4 (Meet-Room "
+    p.add_argument("--config", choices=("c1", "c2", "c3", "c4", "c5"), default="c3",
+                   help="BASELINE.json workload: c3 (default, the metric's), c1 (64x64, 1k "
+                        "Gaussians, one fwd+bwd), c2 (one 1352x1014 view, 300k), c4 (Meet-Room "
                         "shaped), c5 (1M Gaussians)")
     p.add_argument("--n", type=int, default=None, help="Gaussians (default: the config's)")
     p.add_argument("--views", type=int, default=None, help="views (default: the config's)")
@@ -101,7 +114,9 @@ def parse():
                         "exercises rank R's whole multi-GPU step")
     a = p.parse_args()
     if a.capacity is None:
-        a.capacity = 1 << 23 if a.config == "c5" else 1 << 22
+        a.capacity = {"c1": 1 << 18, "c5": 1 << 23}.get(a.config, 1 << 22)
+    if a.config in ("c1", "c2"):
+        a.payload = "full"        # a plain fwd+bwd: every gradient is the step's output
     return a
 
 
@@ -161,6 +176,76 @@ def peaks():
 
 # --------------------------------------------------------------- our arm ----
 
+def c4_prepare(cams, scene, dev, growth=60_000, gamma_err=0.10, tau_pos=2e-4, tau_err=1e-4):
+    """BASELINE configs[3] before the timed iterations of a
+    Meet-Room timestep: render the ground truth (5% of the Gaussians moved + an
+    emerging 10k cluster, synth.c4_ground_truth) and the base scene, the 13 error
+    maps → S_err (dass_error_map, Alg. 1), Eq. 4 selection with the
+    synthetic ∇p̄ (dass_densify_select) and spawn of K = 2 children per
+    selected Gaussian up to +60k (dass_spawn): 200k → 260k Gaussians.
+    Returns the grown scene, the ground-truth images [V,3,H,W] and the op times."""
+    import torch
+    from paper_2411_14847_b200 import dass, synth
+    from paper_2411_14847_b200.pipeline import DeviceScene, Raster, ViewRecords
+    W, H = cams[0].width, cams[0].height
+    E = lambda: torch.cuda.Event(enable_timing=True)
+
+    def render_all(sc):
+        ds = DeviceScene.from_host(sc, dev)
+        rec = ViewRecords(1, sc.n, dev)
+        ras = Raster(W, H, sc.n, 1 << 23, dev, accept_lists=False)
+        imgs = torch.empty(len(cams), 3, H, W, device=dev)
+        for v, cam in enumerate(cams):
+            dass.dass_project(cam, sc.sh_degree, ds.pos_opa, ds.scale, ds.rot, ds.sh, None, *rec.view(0))
+            ras.forward(cam, rec.view(0), host_mode=True)
+            imgs[v].copy_(ras.img)
+        return ds, imgs
+
+    _, gts = render_all(synth.c4_ground_truth(scene))
+    ds, imgs = render_all(scene)
+    n = scene.n
+    ms = {}
+    s_err = torch.zeros(n, dtype=torch.uint8, device=dev)
+    err = torch.empty(H, W, device=dev)
+    dm = torch.zeros((H * W + 31) // 32, dtype=torch.int32, device=dev)
+    e = [E(), E()]
+    e[0].record()
+    for v, cam in enumerate(cams):
+        dass.dass_error_map(cam, imgs[v], gts[v], gamma_err, err, dm, n, ds.pos_opa, s_err)
+    e[1].record()
+    gs, gc = synth.gradstat_lognormal(n)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    in_S = torch.empty(n, dtype=torch.uint8, device=dev)
+    idx = torch.empty(n, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int32, device=dev)
+    ws = torch.empty(dass.dass_partition_workspace(n) // 4 + 1, dtype=torch.int32, device=dev)
+    f = [E(), E()]
+    f[0].record()
+    dass.dass_densify_select(t(gs), t(gc), s_err, tau_pos, tau_err, in_S, idx, cnt, ws)
+    f[1].record()
+    torch.cuda.synchronize()
+    sel = int(cnt[0].item())
+    m = min(sel, growth // 2)
+    n_out = n + 2 * m
+    out = [torch.empty(n_out, 4, device=dev) for _ in range(3)]
+    osh = torch.empty(synth.sh_planes(scene.sh_degree), n_out, 4, device=dev)
+    odyn = torch.empty(n_out, dtype=torch.uint8, device=dev)
+    g = [E(), E()]
+    g[0].record()
+    dass.dass_spawn(scene.sh_degree, ds.pos_opa, ds.scale, ds.rot, ds.sh, t(scene.dynamic), m, idx, 2,
+                    1.6, 0.1, 7, out[0], out[1], out[2], osh, odyn)
+    g[1].record()
+    torch.cuda.synchronize()
+    ms = {"error_maps_13_views": round(e[0].elapsed_time(e[1]), 4),
+          "densify_select": round(f[0].elapsed_time(f[1]), 4), "spawn": round(g[0].elapsed_time(g[1]), 4)}
+    h = lambda x: x.cpu().numpy()
+    grown = synth.Scene(h(out[0]), h(out[1]), h(out[2]), h(osh), scene.sh_degree, h(odyn))
+    info = {"n_before": n, "s_err": int(s_err.sum().item()), "selected": sel, "spawned": 2 * m,
+            "n_after": n_out, "gamma_err": gamma_err, "tau_pos": tau_pos, "tau_err": tau_err,
+            "grad_stat": "synthetic LogNormal(ln 1e-4, 1) (SURVEY §8(d) C4)", "ms": ms}
+    return grown, gts, info
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -180,12 +265,22 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
     cams, scene, wl = workload(args)
-    mu, sigma = synth.shift_offsets(scene, seed=33)
+    with_shift = args.config not in ("c1", "c2")      # C1/C2: one plain fwd+bwd
+    c4info = None
+    if args.config == "c4":   # error-guided densification first: 200k → 260k (C4)
+        n_base = scene.n
+        scene, c4_gts, c4info = c4_prepare(cams, scene, dev)
+    if with_shift:
+        mu, sigma = synth.shift_offsets(scene, seed=33)
+    else:
+        mu = np.zeros((scene.n, 4), np.float32)
+        sigma = np.tile(np.array([1, 0, 0, 0], np.float32), (scene.n, 1))
     W0, H0 = cams[0].width, cams[0].height
     plan_rank, plan_world = rank, world
     if args.emulate:
         plan_rank, plan_world = (int(x) for x in args.emulate.split("/"))
-    plan = view_plan(len(cams), plan_rank, plan_world, ((W0 + 15) // 16) * ((H0 + 15) // 16))
+    plan = view_plan(len(cams), plan_rank, plan_world, ((W0 + 15) // 16) * ((H0 + 15) // 16),
+                     allow_split=c4info is None)   # C4's error maps need whole views
     # views the timed job covers: all of them, or an --emulate run's own share
     job_views = len(cams) if not args.emulate else sum(1.0 if t is None else 0.5 for t in plan.tiles)
     mine = plan.views
@@ -203,13 +298,18 @@ def run_ours(args):
         if mine else torch.empty(0, 3, H, W, device=dev)
     # the step (paper_2411_14847_b200/step.py): buffers, streams and call order
     stepper = ShiftStep(my_cams, n, deg, args.capacity, dev, streams=args.streams,
-                        tiles=plan.tiles, split=plan.split, num_split=plan.num_split)
+                        tiles=plan.tiles, split=plan.split, num_split=plan.num_split,
+                        shift=with_shift)
     records, mvp = stepper.records, stepper.mvp
+    if c4info is not None:   # every view's error map inside the step (C4)
+        c4_serr = torch.zeros(scene.n, dtype=torch.uint8, device=dev)
+        stepper.enable_error_map(c4_gts[mine] if mine else c4_gts[:0], c4info["gamma_err"], n_base,
+                                 c4_serr)
     # one flat gradient buffer = the all_reduce payload (dist.FlatGrads)
     bufs0 = stepper.buffers(base, mu_d, sigma_d, dLs)
     grads = bufs0.grads
     flat, g_mu, g_sigma = grads.flat, grads.g_mu, grads.g_sigma
-    shifted = bufs0.shifted                                  # 𝒢_t after the shift
+    shifted = bufs0.shifted if with_shift else base          # 𝒢_t after the shift
     raster = Raster(W, H, n, args.capacity, dev)   # single-stream scratch for stats/diagnostics
 
     def finish_split(g):
@@ -344,7 +444,7 @@ def run_ours(args):
     # Eq. 3 against per-view ground truth (the render of 𝒢_{t−1} before the
     # shift), instead of a fixed ∂L/∂C.  Reported next to the metric.
     train = None
-    if my_cams and not args.lean and plan.num_split == 0:   # SSIM needs whole views
+    if my_cams and not args.lean and plan.num_split == 0 and with_shift:   # SSIM needs whole views
         mvp.enable_loss(0.2)
         gts = torch.empty(len(my_cams), 3, H, W, device=dev)
         dass.dass_project_views(my_cams, deg, base.pos_opa, base.scale, base.rot, base.sh, None,
@@ -707,7 +807,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N3DV-shaped scene and rig)",
             "config": {"workload": wl, "n_gaussians": n, "views": len(cams), "width": W,
-                       "height": H, "sh_degree": deg, "dynamic_frac": 0.3,
+                       "height": H, "sh_degree": deg, "dynamic_frac": 0.3 if with_shift else None,
                        "cuda_graph": graph is not None, "streams": args.streams,
                        "emulated_share": args.emulate,
                        "parallelism": f"view-sharded dp{world}" + (
@@ -730,6 +830,7 @@ def run_ours(args):
             "allreduce": allreduce,
             "training_step_with_loss": train,
             "densification_f4": densify,
+            "densification_c4": c4info,
             "gpu_launches": int(launches),
             "clocks": clocks,
             "e2e": e2e,
@@ -742,18 +843,22 @@ def run_ours(args):
 
 # ------------------------------------------------------ oracle baseline ----
 
-def time_oracle(cams, scene, views, seed_base=1000):
+def time_oracle(cams, scene, views, seed_base=1000, shift=True, mode="scatter"):
+    """Seconds of the oracle doing the step's work for `views`: the shift (O1) when
+    the step has one, then fwd+bwd (O2-O6, double) per view."""
     import oracle
-    W, H = cams[0].width, cams[0].height
-    mu, sigma = __import__("paper_2411_14847_b200.synth", fromlist=["x"]).shift_offsets(scene, seed=33)
-    t0 = time.perf_counter()
-    po, ro = oracle.shift(scene.pos_opa, scene.rot, mu, sigma, scene.dynamic)
     from paper_2411_14847_b200 import synth
-    sh_scene = synth.Scene(po.astype(np.float32), scene.scale, ro.astype(np.float32), scene.sh,
-                           scene.sh_degree, scene.dynamic)
+    W, H = cams[0].width, cams[0].height
+    t0 = time.perf_counter()
+    sc = scene
+    if shift:
+        mu, sigma = synth.shift_offsets(scene, seed=33)
+        po, ro = oracle.shift(scene.pos_opa, scene.rot, mu, sigma, scene.dynamic)
+        sc = synth.Scene(po.astype(np.float32), scene.scale, ro.astype(np.float32), scene.sh,
+                         scene.sh_degree, scene.dynamic)
     for v in views:
         dL = synth.grad_image(cams[v], seed_base + v, 1.0 / (3 * W * H))
-        oracle.render_bwd(cams[v], sh_scene, dL)
+        oracle.render_bwd(cams[v], sc, dL, mode=mode)
     return time.perf_counter() - t0
 
 
@@ -770,14 +875,35 @@ def host_cpu():
     return {"model": model, "affinity": len(os.sched_getaffinity(0)), "cpu_count": os.cpu_count()}
 
 
-def cpu_baseline(cams, scene, nviews):
+def cpu_baseline(cams, scene, nviews, config="c3"):
+    """The oracle as it stands, on the box's host cores: C1 in its
+    literal form (every pixel over every depth-sorted Gaussian) and C2 in its
+    scatter form, each single-threaded and on every OpenMP thread; C3-C5 on a
+    bounded sample of the views, every thread."""
     import oracle
     oracle.build()
+    allt = oracle.threads()
+    if config in ("c1", "c2"):
+        mode = "literal" if config == "c1" else "scatter"
+        out = {}
+        for label, k in (("all_threads", allt), ("single_thread", 1)):
+            oracle.set_threads(k)
+            reps, secs = 0, 0.0
+            while reps < 3 or (secs < 2.0 and reps < 50):
+                secs += time_oracle(cams, scene, [0], shift=False, mode=mode)
+                reps += 1
+            out[label] = {"seconds_per_step": round(secs / reps, 4), "threads": k, "repeats": reps}
+        oracle.set_threads(allt)
+        s1 = out["all_threads"]["seconds_per_step"]
+        return {"value": round(1.0 / s1, 4), "unit": "views/s", "cores": allt, "kind": "oracle",
+                "host": host_cpu(), "form": mode,
+                "sample": f"the whole {config} step (one view fwd+bwd, {mode} form, double), repeated",
+                "seconds": out}
     secs = time_oracle(cams, scene, list(range(nviews)))
-    return {"value": round(nviews / secs, 4), "unit": "views/s", "cores": oracle.threads(),
+    return {"value": round(nviews / secs, 4), "unit": "views/s", "cores": allt,
             "kind": "oracle", "host": host_cpu(),
-            "sample": f"{nviews} of the 20 views (fwd+bwd, scatter form, double) + the shift, "
-                      f"{secs:.1f} s on {oracle.threads()} OpenMP threads"}
+            "sample": f"{nviews} of the {len(cams)} views (fwd+bwd, scatter form, double) + the shift, "
+                      f"{secs:.1f} s on {allt} OpenMP threads"}
 
 
 def run_reference(args):
@@ -789,11 +915,13 @@ def run_reference(args):
     oracle.build()
     cams, scene, wl = workload(args)
     W, H = cams[0].width, cams[0].height
+    shift = args.config not in ("c1", "c2")
+    mode = "literal" if args.config == "c1" else "scatter"
     for k in range(args.warmup):
-        time_oracle(cams, scene, [k % len(cams)])
+        time_oracle(cams, scene, [k % len(cams)], shift=shift, mode=mode)
     secs = []
     for k in range(args.steps):
-        secs.append(time_oracle(cams, scene, [k % len(cams)]))
+        secs.append(time_oracle(cams, scene, [k % len(cams)], shift=shift, mode=mode))
     s = float(np.mean(secs))
     value = 1.0 / s
     return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "views/s",
@@ -806,7 +934,8 @@ def run_reference(args):
                        "parallelism": "CPU oracle, OpenMP"},
             "cpu_baseline": {"value": round(value, 4), "unit": "views/s", "cores": oracle.threads(),
                              "kind": "oracle",
-                             "sample": "each step = the shift + fwd+bwd of ONE of the 20 views (bounded sample)"},
+                             "sample": ("each step = the shift + fwd+bwd of ONE of the views (bounded sample)"
+                                        if shift else f"each step = the whole {args.config} fwd+bwd ({mode} form)")},
             "e2e": {"value": round(value, 4), "unit": "views/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
@@ -1030,7 +1159,8 @@ def main():
     rank, world, _ = dist_env()
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            result["cpu_baseline"] = cpu_baseline(cams, scene, args.cpu_sample_views)
+            result["cpu_baseline"] = cpu_baseline(cams, scene, min(args.cpu_sample_views, len(cams)),
+                                                  args.config)
         print(json.dumps(result), file=out, flush=True)
 
 

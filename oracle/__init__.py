@@ -56,6 +56,11 @@ def threads() -> int:
     return lib().oracle_threads()
 
 
+def set_threads(k: int) -> None:
+    """OpenMP threads of the following oracle calls."""
+    lib().oracle_set_threads(int(k))
+
+
 def _cam(cam):
     s = cam.to_struct() if hasattr(cam, "to_struct") else cam
     return np.ascontiguousarray(s).reshape(1)

@@ -55,6 +55,16 @@ int oracle_threads(void) {
 #endif
 }
 
+// OpenMP threads of the following calls (bench.py times the oracle single-threaded
+// and on every host core).
+void oracle_set_threads(int k) {
+#ifdef _OPENMP
+  if (k > 0) omp_set_num_threads(k);
+#else
+  (void)k;
+#endif
+}
+
 }  // extern "C"
 
 namespace {

@@ -36,17 +36,21 @@ class ViewPlan:
     num_split: int
 
 
-def view_plan(num_views: int, rank: int, world: int, num_tiles: int) -> ViewPlan:
+def view_plan(num_views: int, rank: int, world: int, num_tiles: int,
+              allow_split: bool = True) -> ViewPlan:
     """Balanced view sharding.  When the views divide evenly,
     whole views in contiguous blocks (shard()).  Otherwise, when twice the views
     divide evenly, every view is cut into two interleaved tile halves and each
     rank takes a contiguous block of halves: 20 views at 8 GPUs → 5 halves each
     (2 whole views + 1 half) instead of 3,3,3,3,2,2,2,2 views.  A view whose
     halves land on two ranks is 'split'; its ∇p̄ terms are formed after the
-    all-reduce (dass_gradstat_from_uv).  Anything else falls back to shard()."""
+    all-reduce (dass_gradstat_from_uv).  Anything else falls back to shard(), as
+    does allow_split=False (a step whose per-view work needs whole images, e.g.
+    the error maps of C4)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank/world")
-    if num_views % world == 0 or (2 * num_views) % world != 0 or num_tiles < 2:
+    if (not allow_split or num_views % world == 0 or (2 * num_views) % world != 0
+            or num_tiles < 2):
         v = shard(num_views, rank, world)
         return ViewPlan(v, [None] * len(v), [-1] * len(v), 0)
     per = 2 * num_views // world

@@ -202,6 +202,9 @@ class MultiViewPass:
         # optional hook(v, stream), called on view v's stream right before its backward:
         # an end-to-end caller makes the view wait there for its own ∂L/∂C upload
         self.before_bwd = None
+        # optional hook(v, raster_slot), called on view v's stream right after its
+        # forward (e.g. the error map of error-guided densification)
+        self.after_fwd = None
         self.g2d = torch.empty(max(self.V, 1), n, 12, dtype=torch.float32, device=device)
         # (K_v, overflow_v) of every view's graph-mode sort, kept per view so a slot
         # reused by a later view does not overwrite an earlier view's overflow flag
@@ -297,6 +300,8 @@ class MultiViewPass:
                 if self.sort_streams is None and not self.batch_sort:
                     ras.sort(cam, rec, num_pairs=self.num_pairs[v])
                 ras.render(cam, rec, bg=bg, tiles=self.tiles[v], ranges=vr, sorted_ids=vi)
+                if self.after_fwd is not None:
+                    self.after_fwd(v, ras)
                 if gts is not None:
                     dL = self.loss_dL[k]
                     dass.dass_fidelity_loss(ras.img, gts[v], self.lam, self.loss_ws[k],

@@ -37,9 +37,12 @@ class ShiftStep:
     whole view); num_split sizes the uv blocks of the flat gradient buffer."""
 
     def __init__(self, cams, n: int, sh_degree: int, capacity: int, device, streams: int = 20,
-                 tiles=None, split=None, num_split: int = 0, validate: bool = False):
+                 tiles=None, split=None, num_split: int = 0, validate: bool = False,
+                 shift: bool = True):
         """validate: the step ends with dass_scan_nonfinite over its gradients (graph
-        mode); check_numerics() then raises DASS_ERR_NUMERICAL on NaN / Inf."""
+        mode); check_numerics() then raises DASS_ERR_NUMERICAL on NaN / Inf.
+        shift=False: a plain fwd+bwd of the given Gaussians (BASELINE configs C1/C2),
+        no dass_apply_shift / _bwd."""
         import torch
         self.cams = list(cams)
         self.n, self.deg, self.device = n, sh_degree, device
@@ -51,8 +54,29 @@ class ShiftStep:
                                  tiles=self.tiles) if self.cams else None
         self.shifted_pos = torch.empty(n, 4, dtype=torch.float32, device=device)
         self.shifted_rot = torch.empty(n, 4, dtype=torch.float32, device=device)
+        self._errmap_pos = None
         self.validate = validate
+        self.shift = shift
         self.bad = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def enable_error_map(self, gts, gamma_err: float, n_base: int, s_err):
+        """Every view's error map against its ground truth right after its forward
+        (dass_error_map: E, D and S_err |= Alg. 1 over the n_base base Gaussians;
+        P:164-165) — the C4 step of BASELINE.json.  s_err (uint8[n]) is
+        OR-accumulated; the caller zeroes it once per timestep."""
+        import torch
+        self.gts, self.gamma_err, self.n_base, self.s_err = gts, gamma_err, n_base, s_err
+        W, H = self.cams[0].width, self.cams[0].height
+        self.err = [torch.empty(H, W, device=self.device) for _ in range(self.mvp.S)]
+        self.dmask = [torch.zeros((H * W + 31) // 32, dtype=torch.int32, device=self.device)
+                      for _ in range(self.mvp.S)]
+        self._errmap_pos = None
+
+        def hook(v, ras):
+            k = v % self.mvp.S
+            dass.dass_error_map(self.cams[v], ras.img, self.gts[v], self.gamma_err, self.err[k],
+                                self.dmask[k], self.n_base, self._errmap_pos, self.s_err)
+        self.mvp.after_fwd = hook
 
     def buffers(self, base: DeviceScene, mu, sigma, dLs, grads: FlatGrads | None = None) -> StepBufs:
         from .synth import sh_planes
@@ -68,19 +92,22 @@ class ShiftStep:
         g.zero_()
         if wait_inputs is not None:
             wait_inputs()
-        dass.dass_apply_shift(S.base.pos_opa, S.base.rot, S.mu, S.sigma, S.base.dynamic,
-                              S.shifted.pos_opa, S.shifted.rot)
-        rec, cams, sh = self.records, self.cams, S.shifted
+        if self.shift:
+            dass.dass_apply_shift(S.base.pos_opa, S.base.rot, S.mu, S.sigma, S.base.dynamic,
+                                  S.shifted.pos_opa, S.shifted.rot)
+        rec, cams, sh = self.records, self.cams, (S.shifted if self.shift else S.base)
 
         def project(v0, v1):
             dass.dass_project_views(cams[v0:v1], self.deg, sh.pos_opa, sh.scale, sh.rot, sh.sh,
                                     None, rec.xy_depth[v0:v1], rec.conic_opa[v0:v1],
                                     rec.rgb[v0:v1], rec.box[v0:v1], rec.tiles[v0:v1])
         if self.mvp is not None:
+            self._errmap_pos = sh.pos_opa     # the error map projects 𝒢_t (Alg. 1)
             self.mvp.uv_out = [None if s < 0 else g.uv[s] for s in self.split]
             self.mvp.run(sh, rec, S.dLs, g, project=project)
-        dass.dass_apply_shift_bwd(S.base.rot, S.sigma, S.base.dynamic, g.pos_opa, g.rot,
-                                  g.g_mu, g.g_sigma)
+        if self.shift:
+            dass.dass_apply_shift_bwd(S.base.rot, S.sigma, S.base.dynamic, g.pos_opa, g.rot,
+                                      g.g_mu, g.g_sigma)
         if self.validate:
             self.bad.zero_()
             dass.dass_scan_nonfinite(g.flat, self.bad)

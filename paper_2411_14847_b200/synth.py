@@ -314,6 +314,30 @@ def c4(n: int = 200_000, num_views: int = 13):
     return cams, n3dv_scene(n=n, seed=4, degree=3, fx=cams[0].fx)
 
 
+def c4_ground_truth(scene: Scene, seed: int = 44, moved_frac: float = 0.05,
+                    n_emerging: int = 10_000, fx: float = 914.3) -> Scene:
+    """SURVEY §8(d) C4's ground-truth scene: the C4 Gaussians with a random 5%
+    translated by N(0, 0.05²) per axis, plus an emerging 10k-Gaussian cluster
+    (N((0.3, −0.1, 2.4), 0.12²)) that the base scene lacks — what error-guided
+    densification has to find."""
+    g = rng(seed)
+    pos = scene.pos_opa.copy()
+    sel = g.uniform(size=scene.n) < moved_frac
+    pos[sel, :3] += (g.normal(size=(int(sel.sum()), 3)) * 0.05).astype(np.float32)
+    xyz = np.array([0.3, -0.1, 2.4]) + g.normal(size=(n_emerging, 3)) * 0.12
+    em = _assemble(g, xyz, xyz[:, 2], scene.sh_degree, fx)
+    cat = lambda a, b: np.concatenate([a, b], 0)
+    return Scene(cat(pos, em.pos_opa), cat(scene.scale, em.scale), cat(scene.rot, em.rot),
+                 np.concatenate([scene.sh, em.sh], 1), scene.sh_degree,
+                 cat(scene.dynamic, np.ones(n_emerging, np.uint8)))
+
+
+def gradstat_lognormal(n: int, seed: int = 46):
+    """C4's synthetic ∇p̄ statistic: LogNormal(ln 1e-4, 1), one view."""
+    g = rng(seed)
+    return np.exp(g.normal(math.log(1e-4), 1.0, size=n)).astype(np.float32), np.ones(n, np.int32)
+
+
 def c5(n: int = 1_000_000):
     cams = n3dv_rig(seed=3)
     return cams, n3dv_scene(n=n, seed=5, degree=3, fx=cams[0].fx,
