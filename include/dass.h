@@ -417,13 +417,15 @@ int dass_gradstat_from_uv(int32_t n, int32_t num_split, const float* uv, float* 
 
 /* ---------------------------------------------------------------------------
  * dass_fidelity_loss — the fidelity loss of Eq. 3, "the fidelity
- * loss in the vanilla 3DGS": L = (1−λ)·L1 + λ·(1 − SSIM) (A39), with
+ * loss in the vanilla 3DGS": L = (1−λ)·L1 + λ·D-SSIM with
+ * D-SSIM = dssim_scale·(1 − SSIM): 1 is the 3DGS code's 1 − SSIM (A39, the
+ * default of the Python binding), 0.5 SPEC's (1 − SSIM)/2; with
  *   L1 = mean over the 3·H·W values of |img − gt|;
  *   SSIM = mean over 3·H·W of S = ((2μ_Iμ_G + C1)(2σ_IG + C2)) /
  *          ((μ_I² + μ_G² + C1)(σ_I² + σ_G² + C2)), per channel, windowed
  *          statistics over an 11×11 Gaussian window (σ = 1.5, normalised),
  *          zero padding outside the image, C1 = 0.01², C2 = 0.03².
- * img, gt: float [3][H][W].  λ ∈ [0, 1] (0.2 in 3DGS).  loss: device float[3]
+ * img, gt: float [3][H][W].  λ ∈ [0, 1] (0.2 in 3DGS); dssim_scale ∈ (0, 1].  loss: device float[3]
  * = (L, L1, SSIM), written.  dL_dimg: float [3][H][W] = ∂L/∂img, written
  * (nullable: forward only; sign(0) = 0 for the L1 term).  ws: workspace of
  * dass_fidelity_loss_workspace bytes, 16-byte aligned.  Any img/gt alignment
@@ -433,8 +435,8 @@ int dass_gradstat_from_uv(int32_t n, int32_t num_split, const float* uv, float* 
  * ------------------------------------------------------------------------- */
 int dass_fidelity_loss_workspace(int32_t width, int32_t height, size_t* bytes);
 int dass_fidelity_loss(int32_t width, int32_t height, const float* img,
-                       const float* gt, float lambda, void* ws, size_t ws_bytes,
-                       float* loss, float* dL_dimg, void* stream);
+                       const float* gt, float lambda, float dssim_scale, void* ws,
+                       size_t ws_bytes, float* loss, float* dL_dimg, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Selective inheritance, Eq. 1 with the straight-through estimator

@@ -232,13 +232,15 @@ def inherit_bwd(m, pos_opa, scale, g_pos_opa, g_scale, lambda_inher=0.0):
     return g
 
 
-def fidelity_loss(img, gt, lam=0.2, grad=True):
-    """f1 / Eq. 3: returns (L, L1, SSIM, dL/dI or None) in double."""
+def fidelity_loss(img, gt, lam=0.2, grad=True, dssim_scale=1.0):
+    """f1 / Eq. 3: returns (L, L1, SSIM, dL/dI or None) in double; D-SSIM =
+    dssim_scale·(1 − SSIM) (1: 3DGS code, A39; 0.5: SPEC S:266)."""
     img = _f32(img); gt = _f32(gt)
     H, W = img.shape[1], img.shape[2]
     out = np.zeros(3)
     g = np.zeros(img.shape) if grad else None
-    lib().oracle_fidelity_loss(W, H, _p(img), _p(gt), C.c_double(lam), _p(out), _p(g))
+    lib().oracle_fidelity_loss(W, H, _p(img), _p(gt), C.c_double(lam), C.c_double(dssim_scale),
+                               _p(out), _p(g))
     return out[0], out[1], out[2], g
 
 

@@ -1294,8 +1294,10 @@ void gauss_window(double w[11][11]) {
 }  // namespace
 
 // loss_out[0] = L, [1] = L1, [2] = SSIM.  dL (double[3HW], nullable) = ∂L/∂I.
+// L = (1 − λ)·L1 + λ·D-SSIM with D-SSIM = dssim_scale·(1 − SSIM): 1 for the 3DGS
+// code's 1 − SSIM (A39), 0.5 for SPEC's (1 − SSIM)/2.
 int oracle_fidelity_loss(int W, int H, const float* img, const float* gt, double lambda,
-                         double* loss_out, double* dL) {
+                         double dssim_scale, double* loss_out, double* dL) {
   const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
   double w[11][11];
   gauss_window(w);
@@ -1332,7 +1334,7 @@ int oracle_fidelity_loss(int W, int H, const float* img, const float* gt, double
       }
   }
   const double L1 = sum_l1 / M, SSIM = sum_s / M;
-  loss_out[0] = (1 - lambda) * L1 + lambda * (1 - SSIM);
+  loss_out[0] = (1 - lambda) * L1 + lambda * dssim_scale * (1 - SSIM);
   loss_out[1] = L1;
   loss_out[2] = SSIM;
   if (!dL) return 0;
@@ -1355,7 +1357,7 @@ int oracle_fidelity_loss(int W, int H, const float* img, const float* gt, double
           }
         const double d = (double)I[p] - (double)G[p];
         const double sgn = d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0);
-        dL[ch * np + p] = (1 - lambda) * sgn / M - lambda * acc / M;
+        dL[ch * np + p] = (1 - lambda) * sgn / M - lambda * dssim_scale * acc / M;
       }
   }
   return 0;

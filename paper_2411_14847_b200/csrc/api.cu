@@ -500,16 +500,18 @@ int dass_fidelity_loss_workspace(int32_t width, int32_t height, size_t* bytes) {
 }
 
 int dass_fidelity_loss(int32_t width, int32_t height, const float* img, const float* gt,
-                       float lambda, void* ws, size_t ws_bytes, float* loss, float* dL_dimg,
-                       void* stream) {
+                       float lambda, float dssim_scale, void* ws, size_t ws_bytes, float* loss,
+                       float* dL_dimg, void* stream) {
   if (width < 1 || height < 1 || width > 65535 || height > 65535)
     return fail(DASS_ERR_INVALID_ARG, "width/height must be in [1, 65535]%s");
   if (!(lambda >= 0.f && lambda <= 1.f)) return fail(DASS_ERR_INVALID_ARG, "lambda must be in [0, 1]%s");
+  if (!(dssim_scale > 0.f && dssim_scale <= 1.f))
+    return fail(DASS_ERR_INVALID_ARG, "dssim_scale must be in (0, 1]%s");
   if (!img || !gt || !loss) return fail(DASS_ERR_INVALID_ARG, "dass_fidelity_loss: null required pointer%s");
   if (!ws || ws_bytes < fidelity_loss_workspace(width, height) || ((uintptr_t)ws & 15u))
     return fail(DASS_ERR_INVALID_ARG, "dass_fidelity_loss: workspace too small or unaligned%s");
-  return cuda_status(launch_fidelity_loss(width, height, img, gt, lambda, ws, loss, dL_dimg,
-                                          (cudaStream_t)stream),
+  return cuda_status(launch_fidelity_loss(width, height, img, gt, lambda, dssim_scale, ws, loss,
+                                          dL_dimg, (cudaStream_t)stream),
                      "dass_fidelity_loss");
 }
 

@@ -157,7 +157,8 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
 cudaError_t launch_gradstat_uv(int n, int S, const float2* uv, float* gsum, cudaStream_t s);
 size_t fidelity_loss_workspace(int W, int H);
 cudaError_t launch_fidelity_loss(int W, int H, const float* img, const float* gt, float lambda,
-                                 void* ws, float* loss, float* dL, cudaStream_t s);
+                                 float dssim_scale, void* ws, float* loss, float* dL,
+                                 cudaStream_t s);
 cudaError_t launch_inherit_mask(int n, const float* m, uint8_t* keep, cudaStream_t s);
 cudaError_t launch_inherit_mask_bwd(int n, const float* m, const float4* pos_opa,
                                     const float4* scale, const float4* g_pos_opa,

@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int W, int H, const float
 template <int VS, bool TMA>
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(int W, int H, const float* __restrict__ img,
                                                       const float* __restrict__ gt, Win win,
-                                                      const float* __restrict__ pmaps, float lambda,
-                                                      float* __restrict__ dL,
+                                                      const float* __restrict__ pmaps, float w_l1,
+                                                      float w_ss, float* __restrict__ dL,
                                                       const __grid_constant__ CUtensorMap tm_p) {
   using T = LossTile<VS>;
   extern __shared__ float smem_raw[];
@@ -370,13 +370,14 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int W, int H, const float
     const float dssim = m[o][0] + 2.f * iv[o] * m[o][1] + gv[o] * m[o][2];
     const float d = iv[o] - gv[o];
     const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-    Dc[q] = ((1.f - lambda) * sgn - lambda * dssim) * invM;
+    Dc[q] = (w_l1 * sgn - w_ss * dssim) * invM;
   }
 }
 
-__global__ void loss_finalize_kernel(const double* acc, double M, float lambda, float* loss) {
+// L = w_l1·L1 + w_ss·(1 − SSIM): w_l1 = 1 − λ, w_ss = λ·dssim_scale (Eq. 3, A39)
+__global__ void loss_finalize_kernel(const double* acc, double M, float w_l1, float w_ss, float* loss) {
   const double ssim = acc[0] / M, l1 = acc[1] / M;
-  loss[0] = (float)((1.0 - lambda) * l1 + lambda * (1.0 - ssim));
+  loss[0] = (float)((double)w_l1 * l1 + (double)w_ss * (1.0 - ssim));
   loss[1] = (float)l1;
   loss[2] = (float)ssim;
 }
@@ -428,7 +429,7 @@ void set_smem_attrs() {
 }
 
 template <int VS>
-cudaError_t fidelity_loss_vs(int W, int H, const float* img, const float* gt, float lambda,
+cudaError_t fidelity_loss_vs(int W, int H, const float* img, const float* gt, float w_l1, float w_ss,
                              double* acc, float* pmaps, float* loss, float* dL, cudaStream_t s) {
   using T = LossTile<VS>;
   static const Win win = make_window();
@@ -445,26 +446,28 @@ cudaError_t fidelity_loss_vs(int W, int H, const float* img, const float* gt, fl
     ssim_fwd_kernel<VS, false><<<grid, 256, T::fwd_smem, s>>>(W, H, img, gt, win, pmaps, acc, mi, mi);
   }
   launch_counted();
-  loss_finalize_kernel<<<1, 1, 0, s>>>(acc, 3.0 * (double)W * H, lambda, loss);
+  loss_finalize_kernel<<<1, 1, 0, s>>>(acc, 3.0 * (double)W * H, w_l1, w_ss, loss);
   launch_counted();
   if (dL) {
     if (tma)
-      ssim_bwd_kernel<VS, true><<<grid, 256, T::bwd_smem, s>>>(W, H, img, gt, win, pmaps, lambda, dL, mp);
+      ssim_bwd_kernel<VS, true><<<grid, 256, T::bwd_smem, s>>>(W, H, img, gt, win, pmaps, w_l1, w_ss, dL, mp);
     else
-      ssim_bwd_kernel<VS, false><<<grid, 256, T::bwd_smem, s>>>(W, H, img, gt, win, pmaps, lambda, dL, mi);
+      ssim_bwd_kernel<VS, false><<<grid, 256, T::bwd_smem, s>>>(W, H, img, gt, win, pmaps, w_l1, w_ss, dL, mi);
     launch_counted();
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_fidelity_loss(int W, int H, const float* img, const float* gt, float lambda,
+                                 float dssim_scale,
                                  void* ws, float* loss, float* dL, cudaStream_t s) {
   double* acc = (double*)ws;
   float* pmaps = (float*)((char*)ws + 256);
   cudaError_t e = cudaMemsetAsync(acc, 0, 2 * sizeof(double), s);
   if (e != cudaSuccess) return e;
   // tiles of 32 × 8·VS outputs; VS = 4, 5, 6 measured within 1%
-  return fidelity_loss_vs<4>(W, H, img, gt, lambda, acc, pmaps, loss, dL, s);
+  return fidelity_loss_vs<4>(W, H, img, gt, 1.f - lambda, lambda * dssim_scale, acc, pmaps, loss,
+                            dL, s);
 }
 
 }  // namespace dass

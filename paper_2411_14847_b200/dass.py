@@ -121,7 +121,7 @@ def lib():
         L.dass_render_bwd_preprocess_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P,
                                                        P, P, P, P, P, P, P]
         L.dass_fidelity_loss_workspace.argtypes = [i32, i32, P]
-        L.dass_fidelity_loss.argtypes = [i32, i32, P, P, C.c_float, P, C.c_size_t, P, P, P]
+        L.dass_fidelity_loss.argtypes = [i32, i32, P, P, C.c_float, C.c_float, P, C.c_size_t, P, P, P]
         L.dass_inherit_mask.argtypes = [i32, P, P, P]
         L.dass_inherit_mask_bwd.argtypes = [i32, P, P, P, P, P, C.c_float, P, P]
         L.dass_error_map.argtypes = [P, P, P, C.c_float, P, P, i32, P, P, P]
@@ -369,10 +369,12 @@ def dass_fidelity_loss_workspace(width, height) -> int:
     return out.value
 
 
-def dass_fidelity_loss(img, gt, lam, ws, loss, dL_dimg=None, stream=None):
-    """Eq. 3: loss (device float[3] = L, L1, SSIM) and optionally ∂L/∂img."""
+def dass_fidelity_loss(img, gt, lam, ws, loss, dL_dimg=None, stream=None, dssim_scale=1.0):
+    """Eq. 3: loss (device float[3] = L, L1, SSIM) and optionally ∂L/∂img.
+    D-SSIM = dssim_scale·(1 − SSIM): 1.0 = 3DGS (A39), 0.5 = SPEC's (1 − SSIM)/2."""
     H, W = img.shape[1], img.shape[2]
-    _check(lib().dass_fidelity_loss(W, H, _ptr(img), _ptr(gt), float(lam), _ptr(ws),
+    _check(lib().dass_fidelity_loss(W, H, _ptr(img), _ptr(gt), float(lam), float(dssim_scale),
+                                    _ptr(ws),
                                     ws.numel() * ws.element_size(), _ptr(loss), _ptr(dL_dimg),
                                     _stream(stream)), "dass_fidelity_loss")
 

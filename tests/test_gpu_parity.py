@@ -466,10 +466,12 @@ def test_inheritance_mask_and_ste_gradient():
     np.testing.assert_allclose(np_(gm)[off], ref[off], rtol=1e-5, atol=1e-9)
 
 
-@pytest.mark.parametrize("W,H,lam,seed,off", [(100, 70, 0.2, 1, 0), (37, 300, 0.5, 2, 0), (1, 1, 0.2, 3, 0),
-                                               (1352, 1014, 0.2, 4, 0), (64, 40, 0.3, 5, 1)])
-def test_fidelity_loss_parity(W, H, lam, seed, off):
-    """f1 (Eq. 3): loss value and ∂L/∂img against the oracle (direct windows).
+@pytest.mark.parametrize("W,H,lam,seed,off,ds", [(100, 70, 0.2, 1, 0, 1.0), (37, 300, 0.5, 2, 0, 1.0),
+                                                  (1, 1, 0.2, 3, 0, 1.0), (1352, 1014, 0.2, 4, 0, 1.0),
+                                                  (64, 40, 0.3, 5, 1, 1.0), (96, 64, 1.0, 6, 0, 0.5)])
+def test_fidelity_loss_parity(W, H, lam, seed, off, ds):
+    """f1 (Eq. 3): loss value and ∂L/∂img against the oracle (direct windows);
+    ds = 0.5 is SPEC's D-SSIM (1 − SSIM)/2, 1.0 the 3DGS code's 1 − SSIM (A39).
     W % 4 == 0 with 16-B aligned planes stages tiles by TMA (100, 1352); odd
     widths (37, 1) and a base offset by one float (off = 1) take the load path."""
     g = np.random.default_rng(seed)
@@ -485,9 +487,9 @@ def test_fidelity_loss_parity(W, H, lam, seed, off):
     ws = torch.empty(dass.dass_fidelity_loss_workspace(W, H) // 4 + 64, dtype=torch.float32, device=DEV)
     loss = torch.zeros(3, device=DEV)
     dL = torch.empty(3, H, W, device=DEV)
-    dass.dass_fidelity_loss(t(img), t(gt), lam, ws, loss, dL)
+    dass.dass_fidelity_loss(t(img), t(gt), lam, ws, loss, dL, dssim_scale=ds)
     torch.cuda.synchronize()
-    L, l1, ssim, ref = oracle.fidelity_loss(img, gt, lam)
+    L, l1, ssim, ref = oracle.fidelity_loss(img, gt, lam, dssim_scale=ds)
     got = np_(loss)
     assert got[0] == pytest.approx(L, rel=1e-5, abs=1e-7)
     assert got[1] == pytest.approx(l1, rel=1e-5, abs=1e-7)

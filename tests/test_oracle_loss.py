@@ -63,3 +63,18 @@ def test_gradient_central_differences():
         dh = float(ap[ch, y, x]) - float(am[ch, y, x])
         fd = (oracle.fidelity_loss(ap, b, lam, grad=False)[0] - oracle.fidelity_loss(am, b, lam, grad=False)[0]) / dh
         assert abs(fd - g[ch, y, x]) <= 1e-5 * max(abs(g[ch, y, x]), 1e-3), (ch, y, x, fd, g[ch, y, x])
+
+
+def test_spec_example_dssim_half_scale():
+    """λ = 1, identical images shifted by a constant 0.1 → the loss
+    equals D-SSIM = (1 − SSIM)/2 with SSIM from an independently coded windowed
+    reference, to 1e-6 (dssim_scale = 0.5; A39's default 1 gives 1 − SSIM)."""
+    a = _img(5, lo=0.1, hi=0.8)
+    b = (a + 0.1).astype(np.float32)
+    ref = _ssim_scipy(a, b)
+    L_half, _, ssim, g_half = oracle.fidelity_loss(a, b, 1.0, dssim_scale=0.5)
+    assert ssim == pytest.approx(ref, abs=1e-9)
+    assert L_half == pytest.approx((1 - ref) / 2, abs=1e-6)
+    L_one, _, _, g_one = oracle.fidelity_loss(a, b, 1.0)
+    assert L_one == pytest.approx(1 - ref, abs=1e-6)
+    np.testing.assert_allclose(g_half, 0.5 * g_one, rtol=1e-12, atol=0)
