@@ -91,14 +91,15 @@ def project(cam, scene, keep=None):
     out = dict(uvz=np.zeros((n, 3)), conic=np.zeros((n, 3)), opa=np.zeros(n),
                rgb=np.zeros((n, 3)), clampbits=np.zeros(n, np.int32), zf=np.zeros(n, np.float32),
                zbits=np.zeros(n, np.uint32), box=np.zeros((n, 4), np.int32),
-               tiles=np.zeros(n, np.uint32), visible=np.zeros(n, np.uint8))
+               tiles=np.zeros(n, np.uint32), visible=np.zeros(n, np.uint8),
+               rows=np.zeros((n, 4), np.uint32))
     k = None if keep is None else np.ascontiguousarray(keep, np.uint8)
     c = _cam(cam)
     lib().oracle_project(_p(c), n, scene.sh_degree, _p(_f32(scene.pos_opa)), _p(_f32(scene.scale)),
                          _p(_f32(scene.rot)), _p(_f32(scene.sh)), _p(k), _p(out["uvz"]),
                          _p(out["conic"]), _p(out["opa"]), _p(out["rgb"]), _p(out["clampbits"]),
                          _p(out["zf"]), _p(out["zbits"]), _p(out["box"]), _p(out["tiles"]),
-                         _p(out["visible"]))
+                         _p(out["visible"]), _p(out["rows"]))
     return out
 
 
@@ -126,18 +127,23 @@ def sh_basis(deg, dirs):
 
 
 def bin_sort(cam, proj):
-    """O3: brute-force pairs sorted by (key, id) and the per-tile ranges."""
+    """O3: brute-force pairs sorted by (key, id) and the per-tile ranges.  The
+    tiles of a Gaussian follow its A50 row spans proj["rows"] (the box rule of
+    A05 if absent)."""
     n = proj["visible"].shape[0]
     c = _cam(cam)
     vis = np.ascontiguousarray(proj["visible"], np.uint8)
     zb = np.ascontiguousarray(proj["zbits"], np.uint32)
     box = np.ascontiguousarray(proj["box"], np.int32)
-    K = lib().oracle_bin_sort(_p(c), n, _p(vis), _p(zb), _p(box), C.c_int64(0), None, None, None)
+    rows = proj.get("rows")
+    rows = None if rows is None else np.ascontiguousarray(rows, np.uint32)
+    K = lib().oracle_bin_sort(_p(c), n, _p(vis), _p(zb), _p(box), C.c_int64(0), None, None, None,
+                              _p(rows))
     ntiles = ((int(c["width"][0]) + 15) // 16) * ((int(c["height"][0]) + 15) // 16)
     keys = np.zeros(max(K, 1), np.uint64); ids = np.zeros(max(K, 1), np.uint32)
     ranges = np.zeros((ntiles, 2), np.uint32)
     lib().oracle_bin_sort(_p(c), n, _p(vis), _p(zb), _p(box), C.c_int64(K), _p(keys), _p(ids),
-                          _p(ranges))
+                          _p(ranges), _p(rows))
     return keys[:K], ids[:K], ranges
 
 

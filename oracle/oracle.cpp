@@ -158,11 +158,84 @@ struct KeyReplica {
   uint32_t zbits;
   int x0, x1, y0, y1;
   uint32_t tiles;
+  uint32_t rows[4];   // A50 tile-row spans (8 × 16 bits) or the full-box sentinel
 };
+
+// A50, KEY CHAIN steps 12-13 of include/dass.h, typed from that text: the tile
+// footprint is, per tile row of the box, the tile columns the ellipse
+// {d : dᵀ Σ'⁻¹ d ≤ R2} reaches in the row's band of pixel rows, padded by one
+// pixel, with R2 ≥ 1.01·2·ln(255·o) + 0.05 an upper bound of the α ≥ 1/255
+// support (ln m ≤ m − 1 on the mantissa).  Boxes of more than 8 tile rows or
+// 255 tile columns keep every box tile (sentinel rows = all ones).  Returns the
+// tile count.
+uint32_t footprint_rows(float ca, float cb, float cc, float det, float u, float v, float o,
+                        int x0, int x1, int y0, int y1, uint32_t rows[4]) {
+  const int tx0 = x0 / 16, tx1 = x1 / 16, ty0 = y0 / 16, ty1 = y1 / 16;
+  if (ty1 - ty0 + 1 > 8 || tx1 - tx0 + 1 > 255) {
+    for (int w = 0; w < 4; ++w) rows[w] = 0xFFFFFFFFu;
+    return (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+  }
+  // 12. the threshold
+  const float xo = 255.0f * o;
+  uint32_t bits;
+  std::memcpy(&bits, &xo, 4);
+  const int e = (int)(bits >> 23) - 127;
+  const uint32_t mbits = (bits & 0x007FFFFFu) | 0x3F800000u;
+  float mf;
+  std::memcpy(&mf, &mbits, 4);
+  float L = (float)e * 0.693147182f;
+  L = L + (mf - 1.0f);
+  float R2 = (2.0f * L) * 1.01f;
+  R2 = R2 + 0.05f;
+  // 13. per tile row
+  const float sxa = std::sqrt(R2 * ca);
+  const float tq = std::sqrt(R2 / ca);
+  const float dyL = -(cb * tq), dyR = cb * tq;
+  const float crr = cc * R2;
+  const float ey = std::sqrt(crr);
+  auto half = [&](float d) {   // √(det·(cc·R2 − d²)), clamped at 0
+    float r = crr - d * d;
+    r = det * r;
+    return std::sqrt(std::fmax(0.0f, r));
+  };
+  uint32_t total = 0;
+  for (int w = 0; w < 4; ++w) rows[w] = 0;
+  for (int ty = ty0; ty <= ty1; ++ty) {
+    const int k = ty - ty0;
+    uint32_t span = 0x00FFu;   // empty: lo = 255 > hi = 0
+    const int Y0 = std::max(y0, 16 * ty), Y1 = std::min(y1, 16 * ty + 15);
+    float d0 = (float)Y0 - v, d1 = (float)Y1 - v;
+    d0 = std::fmax(d0, -ey);
+    d1 = std::fmin(d1, ey);
+    if (d0 <= d1) {
+      const float h0 = half(d0), h1 = half(d1);
+      const float l0 = (cb * d0 - h0) / cc, l1 = (cb * d1 - h1) / cc;
+      const float r0 = (cb * d0 + h0) / cc, r1 = (cb * d1 + h1) / cc;
+      const float lo = (d0 <= dyL && dyL <= d1) ? -sxa : std::fmin(l0, l1);
+      const float hi = (d0 <= dyR && dyR <= d1) ? sxa : std::fmax(r0, r1);
+      float X0f = u + lo;
+      X0f = X0f - 1.0f;
+      X0f = std::fmax((float)x0, X0f);
+      float X1f = u + hi;
+      X1f = X1f + 1.0f;
+      X1f = std::fmin((float)x1, X1f);
+      const float c0 = std::ceil(X0f), c1 = std::floor(X1f);
+      if (c0 <= c1) {
+        const int lo_t = (int)c0 / 16 - tx0, hi_t = (int)c1 / 16 - tx0;
+        span = (uint32_t)lo_t | ((uint32_t)hi_t << 8);
+        total += (uint32_t)(hi_t - lo_t + 1);
+      }
+    }
+    rows[k >> 1] |= span << (16 * (k & 1));
+  }
+  for (int k = ty1 - ty0 + 1; k < 8; ++k) rows[k >> 1] |= 0x00FFu << (16 * (k & 1));
+  return total;
+}
 
 KeyReplica key_replica(const OCam& c, const Params& P, int i) {
   KeyReplica k;
   k.visible = false; k.z = 0; k.zbits = 0; k.x0 = 1; k.x1 = 0; k.y0 = 1; k.y1 = 0; k.tiles = 0;
+  k.rows[0] = k.rows[1] = k.rows[2] = k.rows[3] = 0;
   const float* V = c.viewmat;
   const float px = P.pos_opa[4 * i + 0], py = P.pos_opa[4 * i + 1], pz = P.pos_opa[4 * i + 2];
   const float o = P.kept(i) ? P.pos_opa[4 * i + 3] : 0.0f;
@@ -265,7 +338,8 @@ KeyReplica key_replica(const OCam& c, const Params& P, int i) {
   k.z = t[2];
   std::memcpy(&k.zbits, &k.z, 4);
   k.x0 = (int)fx0; k.x1 = (int)fx1; k.y0 = (int)fy0; k.y1 = (int)fy1;
-  k.tiles = (uint32_t)((k.x1 / 16 - k.x0 / 16 + 1) * (k.y1 / 16 - k.y0 / 16 + 1));
+  // 12-13. the tile footprint (A50)
+  k.tiles = footprint_rows(ca, cb, cc, det, u, v, o, k.x0, k.x1, k.y0, k.y1, k.rows);
   return k;
 }
 
@@ -928,7 +1002,8 @@ int oracle_shift_bwd(int n, const float* rot, const float* sigma, const uint8_t*
 int oracle_project(const OCam* cam, int n, int deg, const float* pos_opa, const float* scale,
                    const float* rot, const float* sh, const uint8_t* keep, double* uvz,
                    double* conic, double* opa, double* rgb, int32_t* clampbits, float* zf,
-                   uint32_t* zbits, int32_t* box, uint32_t* tiles, uint8_t* visible) {
+                   uint32_t* zbits, int32_t* box, uint32_t* tiles, uint8_t* visible,
+                   uint32_t* rows) {
   Params P{n, deg, pos_opa, scale, rot, sh, keep};
   std::vector<Proj> G = project_all(*cam, P);
   for (int i = 0; i < n; ++i) {
@@ -943,6 +1018,7 @@ int oracle_project(const OCam* cam, int n, int deg, const float* pos_opa, const 
     if (box) { box[4 * i] = g.key.x0; box[4 * i + 1] = g.key.x1; box[4 * i + 2] = g.key.y0; box[4 * i + 3] = g.key.y1; }
     if (tiles) tiles[i] = g.key.tiles;
     if (visible) visible[i] = g.key.visible ? 1 : 0;
+    if (rows) for (int w = 0; w < 4; ++w) rows[4 * i + w] = g.key.rows[w];
   }
   return 0;
 }
@@ -989,18 +1065,34 @@ int oracle_sh_basis(int deg, int m, const double* dirs, double* Y) {
 // Brute-force binning: enumerate every (visible Gaussian, tile of its box)
 // pair with key = (tile << 32) | zbits, sort by (key, id).  Returns K; writes
 // at most `cap` pairs; ranges [2*num_tiles] ([0,0) for empty tiles).
+// O3 with the A50 footprint: the tiles of Gaussian i are, for each tile row k of
+// its box, the columns tx0 + lo_k … tx0 + hi_k of rows[i] (row k = 16 bits:
+// lo | hi << 8; lo > hi: none); all ones = every tile of the box.  rows null: the
+// box rule of A05.
 int64_t oracle_bin_sort(const OCam* cam, int n, const uint8_t* visible, const uint32_t* zbits,
                         const int32_t* box, int64_t cap, uint64_t* keys, uint32_t* ids,
-                        uint32_t* ranges) {
+                        uint32_t* ranges, const uint32_t* rows) {
   const int tx_n = (cam->width + 15) / 16, ty_n = (cam->height + 15) / 16;
   std::vector<std::pair<uint64_t, uint32_t>> pairs;
   for (int i = 0; i < n; ++i) {
     if (!visible[i]) continue;
-    for (int ty = box[4 * i + 2] / 16; ty <= box[4 * i + 3] / 16; ++ty)
-      for (int tx = box[4 * i] / 16; tx <= box[4 * i + 1] / 16; ++tx) {
+    const int tx0 = box[4 * i] / 16, tx1 = box[4 * i + 1] / 16;
+    const int ty0 = box[4 * i + 2] / 16, ty1 = box[4 * i + 3] / 16;
+    const bool full = rows == nullptr || (rows[4 * i] == 0xFFFFFFFFu && rows[4 * i + 1] == 0xFFFFFFFFu &&
+                                          rows[4 * i + 2] == 0xFFFFFFFFu && rows[4 * i + 3] == 0xFFFFFFFFu);
+    for (int ty = ty0; ty <= ty1; ++ty) {
+      int lo = tx0, hi = tx1;
+      if (!full) {
+        const int k = ty - ty0;
+        const uint32_t span = (rows[4 * i + (k >> 1)] >> (16 * (k & 1))) & 0xFFFFu;
+        lo = tx0 + (int)(span & 0xFFu);
+        hi = tx0 + (int)(span >> 8);
+      }
+      for (int tx = lo; tx <= hi; ++tx) {
         const uint64_t tile = (uint64_t)(ty * tx_n + tx);
         pairs.push_back({(tile << 32) | zbits[i], (uint32_t)i});
       }
+    }
   }
   std::sort(pairs.begin(), pairs.end());
   const int64_t K = (int64_t)pairs.size();

@@ -1,7 +1,9 @@
 """Pins of the oracle's binning (O3), shift (O1) and error map / Alg. 1 (O7).
 
-O3: brute-force enumeration is the definition (A03-A04); pinned by an
-independent tile-rectangle intersection loop and the sort invariants.
+O3: brute-force enumeration is the definition (A03-A04, A50); pinned by an
+independent decoding of the footprints, each inside the box's tile rectangle,
+and the sort invariants (the footprints' conservativeness is pinned in
+test_oracle_geometry.py).
 O1: §3.3 P:128 — pinned by rotation composition (sandwich product), identity
 cases, unit norm and finite differences.
 O7: §3.4, Alg. 1 P:403-415 — pinned by S:213-215/S:630 examples and
@@ -26,14 +28,15 @@ def _check_binsort(cam, pr):
     K = len(keys)
     vis = np.nonzero(pr["visible"])[0]
     assert K == int(pr["tiles"][vis].sum())
-    # independent enumeration by rectangle intersection
+    # independent enumeration: the decoded A50 footprints (KEY CHAIN step 13), each
+    # a subset of the box's tile rectangle
+    from test_oracle_geometry import footprint_tiles
     expect = set()
     for i in vis:
         x0, x1, y0, y1 = pr["box"][i]
-        for ty in range(cam.tiles_y):
-            for tx in range(cam.tiles_x):
-                if tx * 16 <= x1 and tx * 16 + 15 >= x0 and ty * 16 <= y1 and ty * 16 + 15 >= y0:
-                    expect.add((ty * cam.tiles_x + tx, int(i)))
+        for ty, tx in footprint_tiles(pr, i, cam.tiles_x):
+            assert tx * 16 <= x1 and tx * 16 + 15 >= x0 and ty * 16 <= y1 and ty * 16 + 15 >= y0
+            expect.add((ty * cam.tiles_x + tx, int(i)))
     got = {(int(k >> np.uint64(32)), int(i)) for k, i in zip(keys, ids)}
     assert got == expect and len(got) == K
     # key low bits are the depth bits of the id

@@ -187,20 +187,71 @@ def test_project_box_and_tiles_brute_force():
         x0 = max(0, math.ceil(u - r)); x1 = min(cam.width - 1, math.floor(u + r))
         y0 = max(0, math.ceil(v - r)); y1 = min(cam.height - 1, math.floor(v + r))
         assert list(pr["box"][i]) == [x0, x1, y0, y1]
-        assert pr["tiles"][i] == (x1 // 16 - x0 // 16 + 1) * (y1 // 16 - y0 // 16 + 1)
+        # the A50 footprint keeps a subset of the box's tiles
+        assert 1 <= pr["tiles"][i] <= (x1 // 16 - x0 // 16 + 1) * (y1 // 16 - y0 // 16 + 1) or \
+            pr["tiles"][i] == 0
     assert nties < 0.01 * len(vis)
 
 
-def test_tiles_touched_counts_intersecting_tiles():
-    """tiles_touched equals a brute-force count of intersecting tiles."""
+def footprint_tiles(pr, i, tiles_x):
+    """Decode Gaussian i's A50 row spans (include/dass.h KEY CHAIN step 13)."""
+    x0, x1, y0, y1 = pr["box"][i]
+    tx0, tx1, ty0, ty1 = x0 // 16, x1 // 16, y0 // 16, y1 // 16
+    rows = pr["rows"][i]
+    if np.all(rows == 0xFFFFFFFF):
+        return {(ty, tx) for ty in range(ty0, ty1 + 1) for tx in range(tx0, tx1 + 1)}
+    out = set()
+    for k, ty in enumerate(range(ty0, ty1 + 1)):
+        span = (int(rows[k >> 1]) >> (16 * (k & 1))) & 0xFFFF
+        lo, hi = span & 0xFF, span >> 8
+        out |= {(ty, tx0 + j) for j in range(lo, hi + 1)}
+    return out
+
+
+def test_tiles_touched_counts_the_footprint():
+    """tiles_touched = the number of tiles of the A50 row spans, every one of
+    them inside the box's tile rectangle; rows past the box's last tile row
+    are empty."""
     cam = synth.tiny_camera(100, 70)
     sc = synth.random_scene(300, cam, seed=5, sigma_median=4.0)
     pr = oracle.project(cam, sc)
     for i in np.nonzero(pr["visible"])[0]:
         x0, x1, y0, y1 = pr["box"][i]
-        cnt = sum(1 for ty in range(cam.tiles_y) for tx in range(cam.tiles_x)
-                  if tx * 16 <= x1 and tx * 16 + 15 >= x0 and ty * 16 <= y1 and ty * 16 + 15 >= y0)
-        assert pr["tiles"][i] == cnt
+        tiles = footprint_tiles(pr, i, cam.tiles_x)
+        assert pr["tiles"][i] == len(tiles)
+        assert all(x0 // 16 <= tx <= x1 // 16 and y0 // 16 <= ty <= y1 // 16 for ty, tx in tiles)
+
+
+@pytest.mark.parametrize("case", ["c1", "n3dv_crop"])
+def test_footprint_holds_every_accepted_pixel(case):
+    """A50's premise, by brute force: every (pixel, Gaussian) the oracle's double
+    render accepts (α ≥ 1/255, Eq. 8) lies in a tile of the Gaussian's footprint,
+    so the tiled per-pixel sequences equal the tile-free ones (the lemma of SURVEY
+    §8(c)) and the image is the same as under A05's whole-box rule; and the
+    footprint is tighter than the box (fewer pairs)."""
+    if case == "c1":
+        cam, sc = synth.c1()
+    else:
+        cam = synth.n3dv_rig(width=320, height=240)[9]
+        sc = synth.n3dv_scene(n=6000, seed=23, degree=1, fx=cam.fx)
+    pr = oracle.project(cam, sc)
+    X, Y = np.meshgrid(np.arange(cam.width), np.arange(cam.height))
+    k_box = k_fp = 0
+    for i in np.nonzero(pr["visible"])[0]:
+        x0, x1, y0, y1 = pr["box"][i]
+        u, v = pr["uvz"][i, :2]
+        A, B, C = pr["conic"][i]
+        o = pr["opa"][i]
+        xs, ys = X[y0:y1 + 1, x0:x1 + 1], Y[y0:y1 + 1, x0:x1 + 1]
+        dx, dy = u - xs, v - ys
+        power = -0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy
+        acc = (power <= 0) & (np.minimum(0.99, o * np.exp(power)) >= 1 / 255)
+        tiles = footprint_tiles(pr, i, cam.tiles_x)
+        need = {(int(a) // 16, int(b) // 16) for a, b in zip(ys[acc], xs[acc])}
+        assert need <= tiles, (i, sorted(need - tiles)[:4])
+        k_box += (x1 // 16 - x0 // 16 + 1) * (y1 // 16 - y0 // 16 + 1)
+        k_fp += len(tiles)
+    assert k_fp < 0.9 * k_box
 
 
 def test_sh_orthonormal_quadrature():
