@@ -449,7 +449,7 @@ def run_ours(args):
         gts = torch.empty(len(my_cams), 3, H, W, device=dev)
         dass.dass_project_views(my_cams, deg, base.pos_opa, base.scale, base.rot, base.sh, None,
                                 records.xy_depth, records.conic_opa, records.rgb, records.box,
-                                records.tiles)
+                                records.rows, records.tiles)
         for k, cam in enumerate(my_cams):
             raster.forward(cam, records.view(k))
             gts[k].copy_(raster.img)
@@ -471,7 +471,8 @@ def run_ours(args):
                 dass.dass_project_views(my_cams[v0:v1], deg, shifted.pos_opa, shifted.scale,
                                         shifted.rot, shifted.sh, None, records.xy_depth[v0:v1],
                                         records.conic_opa[v0:v1], records.rgb[v0:v1],
-                                        records.box[v0:v1], records.tiles[v0:v1])
+                                        records.box[v0:v1], records.rows[v0:v1],
+                                        records.tiles[v0:v1])
             mvp.run(shifted, records, None, grads, gts=gts, project=project)
             dass.dass_apply_shift_bwd(base.rot, sigma_f, None, grads.pos_opa, grads.rot,
                                       g_mu, g_sigma)
@@ -519,14 +520,14 @@ def run_ours(args):
         e_proj[0].record()
         dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
                                 shifted.sh, None, records.xy_depth, records.conic_opa,
-                                records.rgb, records.box, records.tiles)
+                                records.rgb, records.box, records.rows, records.tiles)
         e_proj[1].record()
         per = []
         for k, cam in enumerate(my_cams):
-            xy, co, rgb, box, tiles = records.view(k)
+            xy, co, rgb, box, rows, tiles = records.view(k)
             ev = [E() for _ in range(4)]
             ev[0].record()
-            dass.dass_bin_sort(cam, n, xy, box, tiles, raster.sort_ws, raster.capacity, None,
+            dass.dass_bin_sort(cam, n, xy, box, rows, tiles, raster.sort_ws, raster.capacity, None,
                                raster.sorted_ids, raster.ranges, raster.num_pairs)
             ev[1].record()
             dass.dass_render_fwd(cam, raster.ranges, raster.sorted_ids, xy, co, rgb, box, None,
@@ -624,7 +625,7 @@ def run_ours(args):
                                                       g_out[0], g_out[1], g_out[2], g_sh))
         feat = torch.randn(n, 16, device=dev)
         fout = torch.empty(16, H, W, device=dev)
-        xy, co, rgb, box, _ = records.view(0)
+        xy, co, rgb, box, _, _ = records.view(0)
         ms["render_features_16ch_one_view"] = timed(lambda: dass.dass_render_features(
             my_cams[0], raster.ranges, raster.sorted_ids, xy, co, box, feat, fout))
         ms["render_fwd_rgb_same_view"] = timed(lambda: dass.dass_render_fwd(

@@ -75,7 +75,7 @@ extern "C" {
 #endif
 
 #define DASS_TILE 16
-#define DASS_ABI_VERSION 2
+#define DASS_ABI_VERSION 3
 
 typedef enum dass_status {
   DASS_OK = 0,
@@ -179,22 +179,49 @@ int dass_apply_shift_bwd(int32_t n, const float* rot, const float* sigma,
  *      cull unless u, v, λ finite.
  *  11. x0 = max(0, ceil(u − r)), x1 = min(W − 1, floor(u + r)), y likewise
  *      (clamped in float before conversion to int); visible iff x0 ≤ x1,
- *      y0 ≤ y1 and o_eff ≥ 1/255 (A05, A10);
- *      tiles_touched = (x1/16 − x0/16 + 1)·(y1/16 − y0/16 + 1).
+ *      y0 ≤ y1 and o_eff ≥ 1/255 (A05, A10).
+ *  12. Footprint threshold (A50): xo = 255·o_eff; with its IEEE bits, e =
+ *      (bits >> 23) − 127 and m = the float with bits (bits & 0x7FFFFF) |
+ *      0x3F800000 (m ∈ [1, 2)); L = ((float)e·0.693147182) + (m − 1)  (≥ ln xo);
+ *      R2 = ((2·L)·1.01) + 0.05.
+ *  13. Tile footprint: tx0 = x0/16, tx1 = x1/16, ty0 = y0/16, ty1 = y1/16.  If
+ *      ty1 − ty0 + 1 > 8 or tx1 − tx0 + 1 > 255: every tile of the box, rows =
+ *      all ones, tiles_touched = (tx1 − tx0 + 1)·(ty1 − ty0 + 1).  Otherwise,
+ *      with sxa = sqrt(R2·a), tq = sqrt(R2/a), dyL = −(b·tq), dyR = b·tq,
+ *      crr = c·R2, ey = sqrt(crr), icc = 1/c, for each tile row ty ∈ [ty0, ty1]
+ *      (k = ty − ty0):
+ *        Y0 = max(y0, 16·ty), Y1 = min(y1, 16·ty + 15);
+ *        d0 = max((float)Y0 − v, −ey), d1 = min((float)Y1 − v, ey);
+ *        if d0 ≤ d1: h_i = sqrt(max(0, det·(crr − d_i·d_i))),
+ *          l_i = (b·d_i − h_i)·icc, r_i = (b·d_i + h_i)·icc (i = 0, 1);
+ *          lo = −sxa if d0 ≤ dyL ≤ d1 else min(l0, l1);
+ *          hi = sxa if d0 ≤ dyR ≤ d1 else max(r0, r1);
+ *          X0 = max((float)x0, (u + lo) − 1), X1 = min((float)x1, (u + hi) + 1);
+ *          if ceil(X0) ≤ floor(X1): row k spans the tiles ceil(X0)/16 …
+ *          floor(X1)/16;
+ *      (the tile columns the ellipse {d : dᵀ Σ'⁻¹ d ≤ R2} reaches in the row's
+ *      band of pixel rows, padded by one pixel; every pixel with α ≥ 1/255
+ *      lies inside it, so the tiled sequences equal the tile-free ones).
+ *      tile_rows[4i..4i+3] (uint32 ×4, 16-byte aligned): row k in bits
+ *      16·(k&1) … of word k>>1 as lo | hi << 8 (tile offsets from tx0; an
+ *      empty row and rows past ty1 are lo = 255, hi = 0);
+ *      tiles_touched = the number of tiles of the rows.
  *  The conic record is (A, β, γ) = (c/det, −b/c, 1/c), i.e. the conic
  *  (c, −b, a)/det of Eq. 7 in Cholesky form (see the layout above).  Colour (fast math
  *  allowed): d = (p − c_cam)/‖p − c_cam‖, col = Σ_k Y_k(d)·sh_k + 0.5 with the
  *  real SH basis of degree ≤ 3 listed in DESIGN.md (A14); a channel < 0 sets
  *  its clamp bit and is clamped to 0.
- * Culled Gaussians: tiles_touched = 0, box = {1, 1} (x0 > x1), other records
- * zero.  Degenerate q is culled, not an error (A15).
+ * Culled Gaussians: tiles_touched = 0, box = {1, 1} (x0 > x1), tile_rows and
+ * other records zero.  A visible Gaussian (box non-empty, o_eff ≥ 1/255) may
+ * still have tiles_touched = 0 (its support reaches no pixel of the image).
+ * Degenerate q is culled, not an error (A15).
  * INVALID_ARG: bad camera, n < 0, sh_degree ∉ [0,3], null required pointer.
  * ------------------------------------------------------------------------- */
 int dass_project(const dass_camera* cam, int32_t n, int32_t sh_degree,
                  const float* pos_opa, const float* scale, const float* rot,
                  const float* sh, const uint8_t* keep_mask, float* xy_depth,
                  float* conic_opa, float* rgb, uint32_t* box,
-                 uint32_t* tiles_touched, void* stream);
+                 uint32_t* tile_rows, uint32_t* tiles_touched, void* stream);
 
 /* dass_project_views — the same as V calls of dass_project (one per camera),
  * in one launch that reads the parameters once for all V views (a2, "multi-
@@ -205,13 +232,14 @@ int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n,
                        const float* scale, const float* rot, const float* sh,
                        const uint8_t* keep_mask, float* xy_depth,
                        float* conic_opa, float* rgb, uint32_t* box,
-                       uint32_t* tiles_touched, void* stream);
+                       uint32_t* tile_rows, uint32_t* tiles_touched, void* stream);
 
 /* ---------------------------------------------------------------------------
  * dass_bin_sort — tile binning + sort + per-tile ranges (a3-a5; P:29
- * "tile-based"; A03, A04).  For every visible Gaussian i and every tile
- * (tx, ty) of its pixel box (tx = x>>4 over [x0>>4, x1>>4], same for y) emit
- * the pair key = (tile_id << 32) | bits_u32(z_i), value = i.  Output: the
+ * "tile-based"; A03, A04, A50).  For every visible Gaussian i and every tile
+ * (tx, ty) of its footprint (tile_rows of dass_project, KEY CHAIN step 13: a
+ * subset of its pixel box's tiles) emit the pair key = (tile_id << 32) |
+ * bits_u32(z_i), value = i.  Output: the
  * pairs in ascending (key, i) order — i.e. lexicographic (tile, depth bits,
  * Gaussian index) — and ranges[t] = [first, one-past-last) of tile t in that
  * order, [0, 0) for an empty tile.  Integer work: bit-exact by contract.
@@ -232,8 +260,9 @@ int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n,
 int dass_bin_sort_workspace(int32_t n, int32_t num_tiles,
                             int64_t pair_capacity, size_t* bytes);
 int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth,
-                  const uint32_t* box, const uint32_t* tiles_touched,
-                  void* ws, size_t ws_bytes, int64_t pair_capacity,
+                  const uint32_t* box, const uint32_t* tile_rows,
+                  const uint32_t* tiles_touched, void* ws, size_t ws_bytes,
+                  int64_t pair_capacity,
                   uint64_t* sorted_keys, uint32_t* sorted_ids,
                   uint32_t* tile_ranges, uint32_t* num_pairs_dev,
                   int64_t* num_pairs_host, void* stream);
@@ -258,7 +287,8 @@ int dass_bin_sort_views_workspace(int32_t num_views, int32_t n,
                                   int64_t view_capacity, size_t* bytes);
 int dass_bin_sort_views(const dass_camera* cams, int32_t num_views, int32_t n,
                         const float* xy_depth, const uint32_t* box,
-                        const uint32_t* tiles_touched, void* ws, size_t ws_bytes,
+                        const uint32_t* tile_rows, const uint32_t* tiles_touched,
+                        void* ws, size_t ws_bytes,
                         int64_t view_capacity, uint32_t* sorted_ids,
                         uint32_t* tile_ranges, uint32_t* num_pairs_dev,
                         void* stream);

@@ -193,6 +193,7 @@ uint32_t footprint_rows(float ca, float cb, float cc, float det, float u, float 
   const float dyL = -(cb * tq), dyR = cb * tq;
   const float crr = cc * R2;
   const float ey = std::sqrt(crr);
+  const float icc = 1.0f / cc;
   auto half = [&](float d) {   // √(det·(cc·R2 − d²)), clamped at 0
     float r = crr - d * d;
     r = det * r;
@@ -209,8 +210,8 @@ uint32_t footprint_rows(float ca, float cb, float cc, float det, float u, float 
     d1 = std::fmin(d1, ey);
     if (d0 <= d1) {
       const float h0 = half(d0), h1 = half(d1);
-      const float l0 = (cb * d0 - h0) / cc, l1 = (cb * d1 - h1) / cc;
-      const float r0 = (cb * d0 + h0) / cc, r1 = (cb * d1 + h1) / cc;
+      const float l0 = (cb * d0 - h0) * icc, l1 = (cb * d1 - h1) * icc;
+      const float r0 = (cb * d0 + h0) * icc, r1 = (cb * d1 + h1) * icc;
       const float lo = (d0 <= dyL && dyL <= d1) ? -sxa : std::fmin(l0, l1);
       const float hi = (d0 <= dyR && dyR <= d1) ? sxa : std::fmax(r0, r1);
       float X0f = u + lo;
@@ -341,6 +342,19 @@ KeyReplica key_replica(const OCam& c, const Params& P, int i) {
   // 12-13. the tile footprint (A50)
   k.tiles = footprint_rows(ca, cb, cc, det, u, v, o, k.x0, k.x1, k.y0, k.y1, k.rows);
   return k;
+}
+
+// Whether pixel (X, Y)'s tile is in the A50 footprint of k (the tile lists the
+// GPU walks): the visited-entry statistics P_fwd / P_bwd count only those.
+inline bool in_footprint(const KeyReplica& k, int X, int Y) {
+  if (k.rows[0] == 0xFFFFFFFFu && k.rows[1] == 0xFFFFFFFFu && k.rows[2] == 0xFFFFFFFFu &&
+      k.rows[3] == 0xFFFFFFFFu)
+    return true;
+  const int kk = Y / 16 - k.y0 / 16;
+  if (kk < 0 || kk > 7) return false;
+  const uint32_t span = (k.rows[kk >> 1] >> (16 * (kk & 1))) & 0xFFFFu;
+  const int tx = X / 16 - k.x0 / 16;
+  return (int)(span & 0xFFu) <= tx && tx <= (int)(span >> 8);
 }
 
 // ------------------------------------------------ O2: double projection ----
@@ -560,7 +574,7 @@ void pixel_forward(const std::vector<Proj>& G, const std::vector<int>& ord, int 
     const Proj& g = G[ord[pos]];
     if (!box_has(g, X, Y)) continue;
     Eval e = eval_at(g, X, Y);
-    ++inbox_count;
+    if (in_footprint(g.key, X, Y)) ++inbox_count;
     if (is_tie(g, e, T, te)) tie = true;
     if (e.power > 0) continue;
     if (e.alpha < ALPHA_MIN) continue;
@@ -860,7 +874,7 @@ void scatter_forward(const RenderCtx& R, const double bg[3], const TieEps& te, F
           const size_t p = (size_t)Y * W + X;
           if (done[p]) continue;
           Eval e = eval_at(g, X, Y);
-          ++inbox[p];
+          if (in_footprint(g.key, X, Y)) ++inbox[p];
           double& T = o.Tfin[p];
           if (is_tie(g, e, T, te)) o.tie[p] = 1;
           if (e.power > 0 || e.alpha < ALPHA_MIN) continue;

@@ -147,7 +147,8 @@ int dass_apply_shift_bwd(int32_t n, const float* rot, const float* sigma, const 
 static int project_common(const dass_camera* cams, int32_t num_views, int32_t n, int32_t sh_degree,
                           const float* pos_opa, const float* scale, const float* rot,
                           const float* sh, const uint8_t* keep, float* xy_depth, float* conic_opa,
-                          float* rgb, uint32_t* box, uint32_t* tiles, void* stream) {
+                          float* rgb, uint32_t* box, uint32_t* tile_rows, uint32_t* tiles,
+                          void* stream) {
   if (num_views < 1 || num_views > 64)
     return fail(DASS_ERR_INVALID_ARG, "num_views must be in [1, 64]%s");
   for (int v = 0; v < num_views; ++v) {
@@ -157,32 +158,34 @@ static int project_common(const dass_camera* cams, int32_t num_views, int32_t n,
   if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
   if (sh_degree < 0 || sh_degree > 3) return fail(DASS_ERR_INVALID_ARG, "sh_degree must be in [0, 3]%s");
   if (n == 0) return DASS_OK;
-  if (!pos_opa || !scale || !rot || !sh || !xy_depth || !conic_opa || !rgb || !box || !tiles)
+  if (!pos_opa || !scale || !rot || !sh || !xy_depth || !conic_opa || !rgb || !box || !tile_rows ||
+      !tiles)
     return fail(DASS_ERR_INVALID_ARG, "dass_project: null required pointer%s");
+  if (!aligned16(tile_rows)) return fail(DASS_ERR_INVALID_ARG, "dass_project: tile_rows must be 16-byte aligned%s");
   CamParams cp[64];
   for (int v = 0; v < num_views; ++v) cp[v] = to_params(cams + v);
   return cuda_status(launch_project(cp, num_views, n, sh_degree, (const float4*)pos_opa,
                                     (const float4*)scale, (const float4*)rot, (const float4*)sh,
                                     keep, (float4*)xy_depth, (float4*)conic_opa, (float4*)rgb,
-                                    (uint2*)box, tiles, (cudaStream_t)stream),
+                                    (uint2*)box, (uint4*)tile_rows, tiles, (cudaStream_t)stream),
                      "dass_project");
 }
 
 int dass_project(const dass_camera* cam, int32_t n, int32_t sh_degree, const float* pos_opa,
                  const float* scale, const float* rot, const float* sh, const uint8_t* keep_mask,
                  float* xy_depth, float* conic_opa, float* rgb, uint32_t* box,
-                 uint32_t* tiles_touched, void* stream) {
+                 uint32_t* tile_rows, uint32_t* tiles_touched, void* stream) {
   return project_common(cam, 1, n, sh_degree, pos_opa, scale, rot, sh, keep_mask, xy_depth,
-                        conic_opa, rgb, box, tiles_touched, stream);
+                        conic_opa, rgb, box, tile_rows, tiles_touched, stream);
 }
 
 int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n, int32_t sh_degree,
                        const float* pos_opa, const float* scale, const float* rot, const float* sh,
                        const uint8_t* keep_mask, float* xy_depth, float* conic_opa, float* rgb,
-                       uint32_t* box, uint32_t* tiles_touched, void* stream) {
+                       uint32_t* box, uint32_t* tile_rows, uint32_t* tiles_touched, void* stream) {
   if (cams == nullptr) return fail(DASS_ERR_INVALID_ARG, "cams is null%s");
   return project_common(cams, num_views, n, sh_degree, pos_opa, scale, rot, sh, keep_mask,
-                        xy_depth, conic_opa, rgb, box, tiles_touched, stream);
+                        xy_depth, conic_opa, rgb, box, tile_rows, tiles_touched, stream);
 }
 
 int dass_bin_sort_workspace(int32_t n, int32_t num_tiles, int64_t pair_capacity, size_t* bytes) {
@@ -195,7 +198,8 @@ int dass_bin_sort_workspace(int32_t n, int32_t num_tiles, int64_t pair_capacity,
 }
 
 int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, const uint32_t* box,
-                  const uint32_t* tiles_touched, void* ws, size_t ws_bytes, int64_t pair_capacity,
+                  const uint32_t* tile_rows, const uint32_t* tiles_touched, void* ws,
+                  size_t ws_bytes, int64_t pair_capacity,
                   uint64_t* sorted_keys, uint32_t* sorted_ids, uint32_t* tile_ranges,
                   uint32_t* num_pairs_dev, int64_t* num_pairs_host, void* stream) {
   int st = check_camera(cam);
@@ -208,13 +212,14 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, cons
   const int ntiles = cp.tiles_x * cp.tiles_y;
   if (!tile_ranges || !num_pairs_dev || !sorted_ids)
     return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort: null required pointer%s");
-  if (n > 0 && (!xy_depth || !box || !tiles_touched))
+  if (n > 0 && (!xy_depth || !box || !tile_rows || !tiles_touched))
     return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort: null record pointer%s");
   const size_t need = binsort_workspace(n, ntiles, pair_capacity);
   if (ws_bytes < need || (need > 0 && ws == nullptr))
     return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort: workspace too small%s");
   cudaStream_t s = (cudaStream_t)stream;
-  st = cuda_status(launch_binsort(cp, n, (const float4*)xy_depth, (const uint2*)box, tiles_touched,
+  st = cuda_status(launch_binsort(cp, n, (const float4*)xy_depth, (const uint2*)box,
+                                  (const uint4*)tile_rows, tiles_touched,
                                   ws, pair_capacity, sorted_keys, sorted_ids, (uint2*)tile_ranges,
                                   num_pairs_dev, s),
                    "dass_bin_sort");
@@ -246,7 +251,8 @@ int dass_bin_sort_views_workspace(int32_t num_views, int32_t n, int64_t view_cap
 }
 
 int dass_bin_sort_views(const dass_camera* cams, int32_t num_views, int32_t n,
-                        const float* xy_depth, const uint32_t* box, const uint32_t* tiles_touched,
+                        const float* xy_depth, const uint32_t* box, const uint32_t* tile_rows,
+                        const uint32_t* tiles_touched,
                         void* ws, size_t ws_bytes, int64_t view_capacity, uint32_t* sorted_ids,
                         uint32_t* tile_ranges, uint32_t* num_pairs_dev, void* stream) {
   if (!cams) return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: cams is null%s");
@@ -264,14 +270,14 @@ int dass_bin_sort_views(const dass_camera* cams, int32_t num_views, int32_t n,
     return fail(DASS_ERR_INVALID_ARG, "view_capacity must be in [0, 2^30 / V)%s");
   if (!sorted_ids || !tile_ranges || !num_pairs_dev)
     return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: null required pointer%s");
-  if (n > 0 && (!xy_depth || !box || !tiles_touched))
+  if (n > 0 && (!xy_depth || !box || !tile_rows || !tiles_touched))
     return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: null record pointer%s");
   const size_t need = binsort_views_workspace(num_views, n, view_capacity);
   if (ws_bytes < need || (need > 0 && ws == nullptr))
     return fail(DASS_ERR_INVALID_ARG, "dass_bin_sort_views: workspace too small%s");
   CamParams cp = to_params(&cams[0]);
   return cuda_status(launch_binsort_views(cp, num_views, n, (const float4*)xy_depth,
-                                          (const uint2*)box, tiles_touched, ws, view_capacity,
+                                          (const uint2*)box, (const uint4*)tile_rows, tiles_touched, ws, view_capacity,
                                           sorted_ids, (uint2*)tile_ranges, num_pairs_dev,
                                           (cudaStream_t)stream),
                      "dass_bin_sort_views");

@@ -315,9 +315,40 @@ __global__ void __launch_bounds__(256) tile_scan_kernel(int n, const uint64_t* _
 
 // Emit pairs (tile<<32 | id) in depth order; histogram their tile digits;
 // clear the pair-sort look-back status words for the blocks that will run.
+// The tile of a Gaussian's local pair index j (A50, include/dass.h KEY CHAIN
+// step 13): rows = 8 row spans of 16 bits (lo | hi << 8, relative to the box's
+// first tile column; lo > hi: no tile) or all ones = every tile of the box, in
+// (row, column) order; w = the box's width in tiles.
+__device__ __forceinline__ void footprint_tile(uint4 rows, uint32_t w, uint32_t j, uint32_t& dy,
+                                               uint32_t& dx) {
+  if ((rows.x & rows.y & rows.z & rows.w) == 0xFFFFFFFFu) {
+    dy = j / w;
+    dx = j - dy * w;
+    return;
+  }
+  const uint32_t wd[4] = {rows.x, rows.y, rows.z, rows.w};
+  dy = 0;
+  dx = 0;
+  uint32_t rem = j;
+  bool found = false;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t span = (wd[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+    const uint32_t lo = span & 0xFFu, hi = span >> 8;
+    const uint32_t width = lo <= hi ? hi - lo + 1u : 0u;
+    if (!found && rem < width) {
+      dy = (uint32_t)k;
+      dx = lo + rem;
+      found = true;
+    }
+    if (!found) rem -= width;
+  }
+}
+
 __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __restrict__ dkeys,
                                                   const uint32_t* __restrict__ tiles,
                                                   const uint2* __restrict__ box,
+                                                  const uint4* __restrict__ rowspans,
                                                   const uint32_t* __restrict__ offsets,
                                                   const uint32_t* __restrict__ num_pairs_dev,
                                                   int tiles_x, int npass, uint64_t* pkeys,
@@ -345,6 +376,7 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
     const size_t r = base + lane;
     uint32_t id = 0, cnt = 0, w = 1;
     int tx0 = 0, ty0 = 0;
+    uint4 rw = make_uint4(0u, 0u, 0u, 0u);
     if (r < (size_t)n) {
       id = (uint32_t)dkeys[r];
       cnt = tiles[id];
@@ -353,6 +385,7 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
         tx0 = (int)(b.x & 0xFFFFu) / TILE;
         ty0 = (int)(b.y & 0xFFFFu) / TILE;
         w = (uint32_t)((int)(b.x >> 16) / TILE - tx0 + 1);
+        rw = rowspans[id];
       }
     }
     uint32_t incl = cnt;   // inclusive scan of the counts over the warp
@@ -379,11 +412,14 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
       const uint32_t ow = __shfl_sync(0xffffffffu, w, owner);
       const int otx0 = __shfl_sync(0xffffffffu, tx0, owner);
       const int oty0 = __shfl_sync(0xffffffffu, ty0, owner);
+      const uint4 orw = make_uint4(__shfl_sync(0xffffffffu, rw.x, owner), __shfl_sync(0xffffffffu, rw.y, owner),
+                                   __shfl_sync(0xffffffffu, rw.z, owner), __shfl_sync(0xffffffffu, rw.w, owner));
       const bool act = j < total;
       uint32_t tile = 0xFFFFFFFFu;
       if (act) {
         const uint32_t local = j - excl;
-        const uint32_t dy = local / ow, dx = local - dy * ow;
+        uint32_t dy, dx;
+        footprint_tile(orw, ow, local, dy, dx);
         tile = (uint32_t)((oty0 + (int)dy) * tiles_x + otx0 + (int)dx);
         uint32_t gid = oid;
         if (view_n > 0) {   // multi-view batch: Gaussian index v·N + i → (v·T + tile, i)
@@ -486,7 +522,7 @@ size_t binsort_workspace(int n, int num_tiles, int64_t capacity) {
 }
 
 cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, const uint2* box,
-                           const uint32_t* tiles, void* ws_ptr, int64_t capacity,
+                           const uint4* rows, const uint32_t* tiles, void* ws_ptr, int64_t capacity,
                            uint64_t* sorted_keys, uint32_t* sorted_ids, uint2* ranges,
                            uint32_t* num_pairs_dev, cudaStream_t s) {
   const int num_tiles = cam.tiles_x * cam.tiles_y;
@@ -518,7 +554,7 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   tile_scan_kernel<<<nblk_n, 256, 0, s>>>(n, a, tiles, w.offsets, w.scan_status, w.counters + 4,
                                           (long long)capacity, num_pairs_dev);
   launch_counted();
-  emit_kernel<<<grid_n, 256, 0, s>>>(n, a, tiles, box, w.offsets, num_pairs_dev, cam.tiles_x,
+  emit_kernel<<<grid_n, 256, 0, s>>>(n, a, tiles, box, rows, w.offsets, num_pairs_dev, cam.tiles_x,
                                      npass, w.pkeysA, w.hist, w.pstatus, nblk_cap * RADIX);
   launch_counted();
   uint64_t* pa = w.pkeysA;
@@ -549,7 +585,8 @@ size_t binsort_views_workspace(int V, int n, int64_t view_capacity) {
 // (bit-exact) with a handful of large kernels instead of V chains of small,
 // latency-bound ones.
 cudaError_t launch_binsort_views(const CamParams& cam, int V, int n, const float4* xy_depth,
-                                 const uint2* box, const uint32_t* tiles, void* ws_ptr,
+                                 const uint2* box, const uint4* rows, const uint32_t* tiles,
+                                 void* ws_ptr,
                                  int64_t view_capacity, uint32_t* sorted_ids, uint2* ranges,
                                  uint32_t* view_pairs, cudaStream_t s) {
   const int T = cam.tiles_x * cam.tiles_y;
@@ -583,7 +620,7 @@ cudaError_t launch_binsort_views(const CamParams& cam, int V, int n, const float
   tile_scan_kernel<<<nblk_n, 256, 0, s>>>(nn, a, tiles, w.offsets, w.scan_status, w.counters + 4,
                                           (long long)cap, kg);
   launch_counted();
-  emit_kernel<<<grid_n, 256, 0, s>>>(nn, a, tiles, box, w.offsets, kg, cam.tiles_x, npass, w.pkeysA,
+  emit_kernel<<<grid_n, 256, 0, s>>>(nn, a, tiles, box, rows, w.offsets, kg, cam.tiles_x, npass, w.pkeysA,
                                      w.hist, w.pstatus, nblk_cap * RADIX, n, T);
   launch_counted();
   uint64_t* pa = w.pkeysA;

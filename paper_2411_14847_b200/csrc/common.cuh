@@ -118,11 +118,11 @@ cudaError_t launch_shift_bwd(int n, const float4* rot, const float4* sigma, cons
 cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_degree,
                            const float4* pos_opa, const float4* scale, const float4* rot,
                            const float4* sh, const uint8_t* keep, float4* xy_depth,
-                           float4* conic_opa, float4* rgb, uint2* box, uint32_t* tiles,
-                           cudaStream_t s);
+                           float4* conic_opa, float4* rgb, uint2* box, uint4* rows,
+                           uint32_t* tiles, cudaStream_t s);
 size_t binsort_workspace(int n, int num_tiles, int64_t capacity);
 cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, const uint2* box,
-                           const uint32_t* tiles, void* ws, int64_t capacity,
+                           const uint4* rows, const uint32_t* tiles, void* ws, int64_t capacity,
                            uint64_t* sorted_keys, uint32_t* sorted_ids, uint2* ranges,
                            uint32_t* num_pairs_dev, cudaStream_t s);
 size_t render_accept_workspace(int ntiles, int64_t capacity);
@@ -199,7 +199,8 @@ cudaError_t launch_error_map(const CamParams& cam, const float* rendered, const 
                              const float4* pos_opa, uint8_t* s_err, cudaStream_t s);
 size_t binsort_views_workspace(int V, int n, int64_t view_capacity);
 cudaError_t launch_binsort_views(const CamParams& cam, int V, int n, const float4* xy_depth,
-                                 const uint2* box, const uint32_t* tiles, void* ws_ptr,
+                                 const uint2* box, const uint4* rows, const uint32_t* tiles,
+                                 void* ws_ptr,
                                  int64_t view_capacity, uint32_t* sorted_ids, uint2* ranges,
                                  uint32_t* view_pairs, cudaStream_t s);
 cudaError_t launch_timestamp(uint64_t* out, cudaStream_t s);

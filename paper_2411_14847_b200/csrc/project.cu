@@ -38,6 +38,7 @@ struct ProjectArgs {
   float4* conic_opa;
   float4* rgb;
   uint2* box;
+  uint4* rows;      // A50 tile-row spans
   uint32_t* tiles;
 };
 
@@ -50,13 +51,75 @@ struct KeyResult {
   bool visible;
   float z;
   int x0, x1, y0, y1;
+  uint32_t tiles;
+  uint4 rows;
 };
 
-// The KEY CHAIN of include/dass.h, steps 1-11.
+// KEY CHAIN steps 12-13 of include/dass.h (A50): per tile row of the box, the
+// tile columns the ellipse {d : dᵀ Σ'⁻¹ d ≤ R2} reaches in the row's band of pixel
+// rows, padded by one pixel; R2 = an upper bound of 2·ln(255·o) (ln m ≤ m − 1 on
+// the mantissa) × 1.01 + 0.05.  Boxes of more than 8 tile rows or 255 tile
+// columns keep every box tile (rows = all ones).  Every op individually rounded
+// (the oracle's replica must get the same bits).  Returns the tile count.
+__device__ __forceinline__ uint32_t footprint_rows(float ca, float cb, float cc, float det, float u,
+                                                   float v, float o, int x0, int x1, int y0, int y1,
+                                                   uint4& rows) {
+  const int tx0 = x0 / 16, tx1 = x1 / 16, ty0 = y0 / 16, ty1 = y1 / 16;
+  if (ty1 - ty0 + 1 > 8 || tx1 - tx0 + 1 > 255) {
+    rows = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    return (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+  }
+  const float xo = FM(255.0f, o);
+  const uint32_t bits = __float_as_uint(xo);
+  const int e = (int)(bits >> 23) - 127;
+  const float mf = __uint_as_float((bits & 0x007FFFFFu) | 0x3F800000u);
+  const float L = FA(FM((float)e, 0.693147182f), FS(mf, 1.0f));
+  const float R2 = FA(FM(FM(2.0f, L), 1.01f), 0.05f);
+  const float sxa = __fsqrt_rn(FM(R2, ca));
+  const float tq = __fsqrt_rn(FD(R2, ca));
+  const float dyL = -FM(cb, tq), dyR = FM(cb, tq);
+  const float crr = FM(cc, R2);
+  const float ey = __fsqrt_rn(crr);
+  const float icc = FD(1.0f, cc);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  uint32_t total = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int ty = ty0 + k;
+    uint32_t span = 0x00FFu;   // empty: lo = 255 > hi = 0
+    if (ty <= ty1) {
+      const int Y0 = max(y0, 16 * ty), Y1 = min(y1, 16 * ty + 15);
+      const float d0 = fmaxf(FS((float)Y0, v), -ey);
+      const float d1 = fminf(FS((float)Y1, v), ey);
+      if (d0 <= d1) {
+        const float h0 = __fsqrt_rn(fmaxf(0.0f, FM(det, FS(crr, FM(d0, d0)))));
+        const float h1 = __fsqrt_rn(fmaxf(0.0f, FM(det, FS(crr, FM(d1, d1)))));
+        const float l0 = FM(FS(FM(cb, d0), h0), icc), l1 = FM(FS(FM(cb, d1), h1), icc);
+        const float r0 = FM(FA(FM(cb, d0), h0), icc), r1 = FM(FA(FM(cb, d1), h1), icc);
+        const float lo = (d0 <= dyL && dyL <= d1) ? -sxa : fminf(l0, l1);
+        const float hi = (d0 <= dyR && dyR <= d1) ? sxa : fmaxf(r0, r1);
+        const float X0f = fmaxf((float)x0, FS(FA(u, lo), 1.0f));
+        const float X1f = fminf((float)x1, FA(FA(u, hi), 1.0f));
+        const float c0 = ceilf(X0f), c1 = floorf(X1f);
+        if (c0 <= c1) {
+          const int lo_t = (int)c0 / 16 - tx0, hi_t = (int)c1 / 16 - tx0;
+          span = (uint32_t)lo_t | ((uint32_t)hi_t << 8);
+          total += (uint32_t)(hi_t - lo_t + 1);
+        }
+      }
+    }
+    w[k >> 1] |= span << (16 * (k & 1));
+  }
+  rows = make_uint4(w[0], w[1], w[2], w[3]);
+  return total;
+}
+
+// The KEY CHAIN of include/dass.h, steps 1-13.
 __device__ __forceinline__ KeyResult key_chain(const CamParams& c, float px, float py, float pz,
                                                float o, float s0, float s1, float s2, float4 q) {
   KeyResult k;
   k.visible = false; k.z = 0.f; k.x0 = 1; k.x1 = 0; k.y0 = 1; k.y1 = 0;
+  k.tiles = 0; k.rows = make_uint4(0u, 0u, 0u, 0u);
   const float* V = c.V;
   float t[3];
 #pragma unroll
@@ -136,6 +199,7 @@ __device__ __forceinline__ KeyResult key_chain(const CamParams& c, float px, flo
   k.visible = true;
   k.z = t[2];
   k.x0 = (int)fx0; k.x1 = (int)fx1; k.y0 = (int)fy0; k.y1 = (int)fy1;
+  k.tiles = footprint_rows(ca, cb, cc, det, u, v, o, k.x0, k.x1, k.y0, k.y1, k.rows);   // 12-13
   return k;
 }
 
@@ -230,6 +294,7 @@ __global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__
       a.conic_opa[o] = make_float4(0.f, 0.f, 0.f, 0.f);
       a.rgb[o] = make_float4(0.f, 0.f, 0.f, 0.f);
       a.box[o] = make_uint2(1u, 1u);
+      a.rows[o] = make_uint4(0u, 0u, 0u, 0u);
       a.tiles[o] = 0u;
       continue;
     }
@@ -263,7 +328,8 @@ __global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__
     a.conic_opa[o] = make_float4(r.A, r.beta, r.gamma, o_eff);
     a.rgb[o] = make_float4(col[0], col[1], col[2], (float)bits);
     a.box[o] = make_uint2((uint32_t)k.x0 | ((uint32_t)k.x1 << 16), (uint32_t)k.y0 | ((uint32_t)k.y1 << 16));
-    a.tiles[o] = (uint32_t)((k.x1 / TILE - k.x0 / TILE + 1) * (k.y1 / TILE - k.y0 / TILE + 1));
+    a.rows[o] = k.rows;
+    a.tiles[o] = k.tiles;
   }
 }
 
@@ -272,15 +338,16 @@ __global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__
 cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_degree,
                            const float4* pos_opa, const float4* scale, const float4* rot,
                            const float4* sh, const uint8_t* keep, float4* xy_depth,
-                           float4* conic_opa, float4* rgb, uint2* box, uint32_t* tiles,
-                           cudaStream_t s) {
+                           float4* conic_opa, float4* rgb, uint2* box, uint4* rows,
+                           uint32_t* tiles, cudaStream_t s) {
   for (int v0 = 0; v0 < num_views; v0 += MAXV) {
     ProjectArgs a;
     a.num_views = num_views - v0 < MAXV ? num_views - v0 : MAXV;
     for (int v = 0; v < a.num_views; ++v) a.cam[v] = cams[v0 + v];
     a.n = n; a.view_offset = v0;
     a.pos_opa = pos_opa; a.scale = scale; a.rot = rot; a.sh = sh; a.keep = keep;
-    a.xy_depth = xy_depth; a.conic_opa = conic_opa; a.rgb = rgb; a.box = box; a.tiles = tiles;
+    a.xy_depth = xy_depth; a.conic_opa = conic_opa; a.rgb = rgb; a.box = box; a.rows = rows;
+    a.tiles = tiles;
     a.vpt = MAXV;   // every view of the launch per thread (measured fastest)
     const dim3 grid(div_up(n, 256), div_up(a.num_views, a.vpt));
     switch (sh_degree) {

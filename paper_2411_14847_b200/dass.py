@@ -105,12 +105,12 @@ def lib():
         i32, i64 = C.c_int32, C.c_int64
         L.dass_apply_shift.argtypes = [i32, P, P, P, P, P, P, P, P]
         L.dass_apply_shift_bwd.argtypes = [i32, P, P, P, P, P, P, P, P]
-        L.dass_project.argtypes = [P, i32, i32, P, P, P, P, P, P, P, P, P, P, P]
-        L.dass_project_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_project.argtypes = [P, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_project_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P]
         L.dass_bin_sort_workspace.argtypes = [i32, i32, i64, P]
-        L.dass_bin_sort.argtypes = [P, i32, P, P, P, P, C.c_size_t, i64, P, P, P, P, P, P]
+        L.dass_bin_sort.argtypes = [P, i32, P, P, P, P, P, C.c_size_t, i64, P, P, P, P, P, P]
         L.dass_bin_sort_views_workspace.argtypes = [i32, i32, i64, P]
-        L.dass_bin_sort_views.argtypes = [P, i32, i32, P, P, P, P, C.c_size_t, i64, P, P, P, P]
+        L.dass_bin_sort_views.argtypes = [P, i32, i32, P, P, P, P, P, C.c_size_t, i64, P, P, P, P]
         L.dass_render_accept_workspace.argtypes = [i32, i64, P]
         L.dass_render_fwd.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, C.c_size_t, i64, P]
         L.dass_render_bwd_workspace.argtypes = [i32, P]
@@ -216,21 +216,23 @@ def dass_apply_shift_bwd(rot, sigma, dyn_mask, g_pos_out, g_rot_out, g_mu, g_sig
 
 
 def dass_project(cam, sh_degree, pos_opa, scale, rot, sh, keep_mask, xy_depth, conic_opa, rgb,
-                 box, tiles_touched, stream=None):
+                 box, tile_rows, tiles_touched, stream=None):
+    """tile_rows: int32 [N,4], the A50 footprint row spans (KEY CHAIN step 13)."""
     c = _cam(cam)
     _check(lib().dass_project(C.byref(c), pos_opa.shape[0], sh_degree, _ptr(pos_opa), _ptr(scale),
                               _ptr(rot), _ptr(sh), _ptr(keep_mask), _ptr(xy_depth),
-                              _ptr(conic_opa), _ptr(rgb), _ptr(box), _ptr(tiles_touched),
-                              _stream(stream)), "dass_project")
+                              _ptr(conic_opa), _ptr(rgb), _ptr(box), _ptr(tile_rows),
+                              _ptr(tiles_touched), _stream(stream)), "dass_project")
 
 
 def dass_project_views(cams, sh_degree, pos_opa, scale, rot, sh, keep_mask, xy_depth, conic_opa,
-                       rgb, box, tiles_touched, stream=None):
+                       rgb, box, tile_rows, tiles_touched, stream=None):
     arr = (dass_camera * len(cams))(*[_cam(c) for c in cams])
     _check(lib().dass_project_views(arr, len(cams), pos_opa.shape[0], sh_degree, _ptr(pos_opa),
                                     _ptr(scale), _ptr(rot), _ptr(sh), _ptr(keep_mask),
                                     _ptr(xy_depth), _ptr(conic_opa), _ptr(rgb), _ptr(box),
-                                    _ptr(tiles_touched), _stream(stream)), "dass_project_views")
+                                    _ptr(tile_rows), _ptr(tiles_touched), _stream(stream)),
+           "dass_project_views")
 
 
 def dass_bin_sort_workspace(n, num_tiles, pair_capacity) -> int:
@@ -240,12 +242,13 @@ def dass_bin_sort_workspace(n, num_tiles, pair_capacity) -> int:
     return out.value
 
 
-def dass_bin_sort(cam, n, xy_depth, box, tiles_touched, ws, pair_capacity, sorted_keys,
+def dass_bin_sort(cam, n, xy_depth, box, tile_rows, tiles_touched, ws, pair_capacity, sorted_keys,
                   sorted_ids, tile_ranges, num_pairs_dev, host_mode=False, stream=None):
     """Returns K in host mode (raises DassError(CAPACITY) on overflow), else None."""
     c = _cam(cam)
     k = C.c_int64(-1)
-    st = lib().dass_bin_sort(C.byref(c), n, _ptr(xy_depth), _ptr(box), _ptr(tiles_touched),
+    st = lib().dass_bin_sort(C.byref(c), n, _ptr(xy_depth), _ptr(box), _ptr(tile_rows),
+                             _ptr(tiles_touched),
                              _ptr(ws), ws.numel() * ws.element_size(), pair_capacity,
                              _ptr(sorted_keys), _ptr(sorted_ids), _ptr(tile_ranges),
                              _ptr(num_pairs_dev), C.byref(k) if host_mode else None,
@@ -261,12 +264,12 @@ def dass_bin_sort_views_workspace(num_views, n, view_capacity) -> int:
     return out.value
 
 
-def dass_bin_sort_views(cams, n, xy_depth, box, tiles_touched, ws, view_capacity, sorted_ids,
-                        tile_ranges, num_pairs_dev, stream=None):
+def dass_bin_sort_views(cams, n, xy_depth, box, tile_rows, tiles_touched, ws, view_capacity,
+                        sorted_ids, tile_ranges, num_pairs_dev, stream=None):
     """All views of a timestep at once (graph mode): per view v, sorted_ids[v],
     tile_ranges[v] and num_pairs_dev[v] = (K_v, overflow_v) as dass_bin_sort."""
     arr = (dass_camera * len(cams))(*[_cam(c) for c in cams])
-    _check(lib().dass_bin_sort_views(arr, len(cams), n, _ptr(xy_depth), _ptr(box),
+    _check(lib().dass_bin_sort_views(arr, len(cams), n, _ptr(xy_depth), _ptr(box), _ptr(tile_rows),
                                      _ptr(tiles_touched), _ptr(ws), ws.numel() * ws.element_size(),
                                      view_capacity, _ptr(sorted_ids), _ptr(tile_ranges),
                                      _ptr(num_pairs_dev), _stream(stream)),

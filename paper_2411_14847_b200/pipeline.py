@@ -81,10 +81,13 @@ class ViewRecords:
         self.conic_opa = f(num_views, n, 4)
         self.rgb = f(num_views, n, 4)
         self.box = torch.empty(num_views, n, 2, dtype=torch.int32, device=device)
+        self.rows = torch.empty(num_views, n, 4, dtype=torch.int32, device=device)   # A50 footprints
         self.tiles = torch.empty(num_views, n, dtype=torch.int32, device=device)
 
     def view(self, v: int):
-        return self.xy_depth[v], self.conic_opa[v], self.rgb[v], self.box[v], self.tiles[v]
+        """View v's records, in dass_project's output order."""
+        return (self.xy_depth[v], self.conic_opa[v], self.rgb[v], self.box[v], self.rows[v],
+                self.tiles[v])
 
 
 class Raster:
@@ -113,8 +116,8 @@ class Raster:
 
     def sort(self, cam, rec, host_mode=False, sorted_keys=None, num_pairs=None):
         """num_pairs: where (K, overflow flag) go (default: this slot's own pair)."""
-        xy, co, rgb, box, tt = rec
-        return dass.dass_bin_sort(cam, self.n, xy, box, tt, self.sort_ws, self.capacity,
+        xy, co, rgb, box, rows, tt = rec
+        return dass.dass_bin_sort(cam, self.n, xy, box, rows, tt, self.sort_ws, self.capacity,
                                   sorted_keys, self.sorted_ids, self.ranges,
                                   self.num_pairs if num_pairs is None else num_pairs,
                                   host_mode=host_mode)
@@ -122,7 +125,7 @@ class Raster:
     def render(self, cam, rec, bg=None, tiles=None, ranges=None, sorted_ids=None):
         """ranges/sorted_ids: a view's slices of a batched dass_bin_sort_views (else
         this slot's own sort)."""
-        xy, co, rgb, box, tt = rec
+        xy, co, rgb, box, rows, tt = rec
         dass.dass_render_fwd(cam, self.ranges if ranges is None else ranges,
                              self.sorted_ids if sorted_ids is None else sorted_ids, xy, co, rgb,
                              box, bg, self.img, self.T, self.last, self.accept, self.capacity,
@@ -135,7 +138,7 @@ class Raster:
 
     def backward(self, cam, scene: DeviceScene, rec, dL_dimg, grads: Grads, keep=None, bg=None,
                  want=("pos", "scale", "rot", "sh", "stat")):
-        xy, co, rgb, box, tiles = rec
+        xy, co, rgb, box, rows, tiles = rec
         g = lambda name, t: t if name in want else None
         dass.dass_render_bwd(cam, scene.sh_degree, scene.pos_opa, scene.scale, scene.rot,
                              scene.sh, keep, self.ranges, self.sorted_ids, xy, co, rgb, box, bg,
@@ -148,7 +151,7 @@ class Raster:
 def project_all(cams, scene: DeviceScene, records: ViewRecords, keep=None):
     dass.dass_project_views(cams, scene.sh_degree, scene.pos_opa, scene.scale, scene.rot,
                             scene.sh, keep, records.xy_depth, records.conic_opa, records.rgb,
-                            records.box, records.tiles)
+                            records.box, records.rows, records.tiles)
 
 
 def fwd_bwd_views(cams, scene: DeviceScene, records: ViewRecords, raster: Raster, dL_dimgs,
@@ -261,7 +264,8 @@ class MultiViewPass:
             a, b = pbounds[c], pbounds[c + 1]
             if self.batch_sort:
                 dass.dass_bin_sort_views(self.cams[a:b], self.n, records.xy_depth[a:b],
-                                         records.box[a:b], records.tiles[a:b], self.bs_ws,
+                                         records.box[a:b], records.rows[a:b], records.tiles[a:b],
+                                         self.bs_ws,
                                          self.slots[0].capacity, self.bs_ids[a:b],
                                          self.bs_ranges[a:b], self.bs_pairs[a:b])
             elif project is not None:
@@ -284,7 +288,7 @@ class MultiViewPass:
             k = v % self.S
             ras, st = self.slots[k], self.streams[k]
             rec = records.view(v)
-            xy, co, rgb, box, tiles = rec
+            xy, co, rgb, box, rows, tiles = rec
             st.wait_event(ready[chunk_of[v]])
             if self.batch_sort:
                 vr, vi = self.bs_ranges[v], self.bs_ids[v]

@@ -55,7 +55,7 @@ def test_library_is_sm100a_only(lib):
 
 def test_status_strings_and_version(lib):
     L = lib.lib()
-    assert lib.abi_version() == 2
+    assert lib.abi_version() == 3
     for s, txt in [(0, b"ok"), (1, b"invalid argument"), (4, b"pair capacity exceeded")]:
         assert L.dass_status_string(s) == txt
     assert L.dass_status_string(99) == b"unknown status"
@@ -66,17 +66,17 @@ def test_validation_before_any_cuda_call(lib):
     cam = lib.camera_struct(synth.tiny_camera(64, 64))
     P = None
     # null camera / bad sizes / bad degree
-    assert L.dass_project(None, 10, 0, P, P, P, P, P, P, P, P, P, P, P) == 1
+    assert L.dass_project(None, 10, 0, P, P, P, P, P, P, P, P, P, P, P, P) == 1
     bad = lib.camera_struct(synth.tiny_camera(64, 64)); bad.width = 0
-    assert L.dass_project(C.byref(bad), 10, 0, P, P, P, P, P, P, P, P, P, P, P) == 1
+    assert L.dass_project(C.byref(bad), 10, 0, P, P, P, P, P, P, P, P, P, P, P, P) == 1
     bad.width = 64; bad.fx = -1.0
-    assert L.dass_project(C.byref(bad), 10, 0, P, P, P, P, P, P, P, P, P, P, P) == 1
-    assert L.dass_project(C.byref(cam), 10, 4, P, P, P, P, P, P, P, P, P, P, P) == 1
-    assert L.dass_project(C.byref(cam), -1, 0, P, P, P, P, P, P, P, P, P, P, P) == 1
-    assert L.dass_project(C.byref(cam), 10, 0, P, P, P, P, P, P, P, P, P, P, P) == 1  # null ptrs
+    assert L.dass_project(C.byref(bad), 10, 0, P, P, P, P, P, P, P, P, P, P, P, P) == 1
+    assert L.dass_project(C.byref(cam), 10, 4, P, P, P, P, P, P, P, P, P, P, P, P) == 1
+    assert L.dass_project(C.byref(cam), -1, 0, P, P, P, P, P, P, P, P, P, P, P, P) == 1
+    assert L.dass_project(C.byref(cam), 10, 0, P, P, P, P, P, P, P, P, P, P, P, P) == 1  # null ptrs
     assert b"null" in L.dass_last_error()
     # n = 0 is OK and enqueues nothing
-    assert L.dass_project(C.byref(cam), 0, 3, P, P, P, P, P, P, P, P, P, P, P) == 0
+    assert L.dass_project(C.byref(cam), 0, 3, P, P, P, P, P, P, P, P, P, P, P, P) == 0
     assert L.dass_apply_shift(0, P, P, P, P, P, P, P, P) == 0
     assert L.dass_apply_shift(-3, P, P, P, P, P, P, P, P) == 1
     # error map: γ ≤ 0 is a usage error; missing images are a data error
@@ -164,13 +164,14 @@ def test_bin_sort_views_and_timestamp_validation_before_any_cuda_call(lib):
     mixed = (lib.dass_camera * 2)(lib.camera_struct(synth.tiny_camera(64, 64)),
                                   lib.camera_struct(synth.tiny_camera(32, 64)))
     args = lambda cams, ws, nb, ids: (cams, 2, 100, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16),
-                                      ws, nb, 1000, ids, C.c_void_p(16), C.c_void_p(16), P)
+                                      C.c_void_p(16), ws, nb, 1000, ids, C.c_void_p(16),
+                                      C.c_void_p(16), P)
     assert L.dass_bin_sort_views(*args(mixed, C.c_void_p(16), one, C.c_void_p(16))) == 1
     assert b"differ" in L.dass_last_error()
     assert L.dass_bin_sort_views(*args(arr, C.c_void_p(16), one, None)) == 1
     assert L.dass_bin_sort_views(*args(arr, C.c_void_p(16), one - 1, C.c_void_p(16))) == 1
     assert b"workspace" in L.dass_last_error()
-    assert L.dass_bin_sort_views(None, 2, 100, P, P, P, P, 0, 1000, P, P, P, P) == 1
+    assert L.dass_bin_sort_views(None, 2, 100, P, P, P, P, P, 0, 1000, P, P, P, P) == 1
     assert L.dass_timestamp(None, 0, P) == 1
     assert L.dass_timestamp(C.c_void_p(16), -1, P) == 1
     assert lib.kernel_launches() == 0

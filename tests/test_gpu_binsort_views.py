@@ -32,7 +32,7 @@ def batched(cams, rec, n, cap):
     ids = torch.full((V, max(cap, 1)), -1, dtype=torch.int32, device=DEV)
     ranges = torch.full((V, T, 2), 7, dtype=torch.int32, device=DEV)
     npairs = torch.zeros(V, 2, dtype=torch.int32, device=DEV)
-    dass.dass_bin_sort_views(cams, n, rec.xy_depth, rec.box, rec.tiles, ws, cap, ids, ranges, npairs)
+    dass.dass_bin_sort_views(cams, n, rec.xy_depth, rec.box, rec.rows, rec.tiles, ws, cap, ids, ranges, npairs)
     torch.cuda.synchronize()
     return np_(ids).view(np.uint32), np_(ranges).view(np.uint32), np_(npairs).view(np.uint32)
 
@@ -41,18 +41,18 @@ def project(cams, sc):
     ds = DeviceScene.from_host(sc, DEV)
     rec = ViewRecords(len(cams), sc.n, DEV)
     dass.dass_project_views(cams, sc.sh_degree, ds.pos_opa, ds.scale, ds.rot, ds.sh, None,
-                            rec.xy_depth, rec.conic_opa, rec.rgb, rec.box, rec.tiles)
+                            rec.xy_depth, rec.conic_opa, rec.rgb, rec.box, rec.rows, rec.tiles)
     return rec
 
 
 def oracle_view(cam, rec, v):
     xy = np_(rec.xy_depth[v])
     box = np_(rec.box[v]).view(np.uint32)
-    tiles = np_(rec.tiles[v]).view(np.uint32)
-    vis = (tiles > 0).astype(np.uint8)
+    rows = np_(rec.rows[v]).view(np.uint32)
     zb = xy[:, 2].copy().view(np.uint32)
     b4 = np.stack([box[:, 0] & 0xFFFF, box[:, 0] >> 16, box[:, 1] & 0xFFFF, box[:, 1] >> 16], 1)
-    return oracle.bin_sort(cam, dict(visible=vis, zbits=zb, box=b4.astype(np.int32)))
+    vis = (b4[:, 0] <= b4[:, 1]).astype(np.uint8)
+    return oracle.bin_sort(cam, dict(visible=vis, zbits=zb, box=b4.astype(np.int32), rows=rows))
 
 
 def tiny_rig(num, W, H, seed):

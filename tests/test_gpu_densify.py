@@ -153,7 +153,7 @@ def test_feature_render_parity(case):
     rec, ras = render_setup(cam, sc)
     feat = np.random.default_rng(88).normal(size=(sc.n, 16)).astype(np.float32)
     out = torch.empty(16, cam.height, cam.width, device=DEV)
-    xy, co, rgb, box, _ = rec.view(0)
+    xy, co, rgb, box, _, _ = rec.view(0)
     dass.dass_render_features(cam, ras.ranges, ras.sorted_ids, xy, co, box, t(feat), out)
     torch.cuda.synchronize()
     ref, tie = oracle.render_features(cam, sc, feat)

@@ -39,7 +39,7 @@ def run_view(cam, scene, dL=None, keep=None, bg=None, capacity=1 << 22, lists=Tr
     rec = ViewRecords(1, scene.n, DEV)
     kd = None if keep is None else torch.from_numpy(keep.astype(np.uint8)).to(DEV)
     dass.dass_project(cam, scene.sh_degree, ds.pos_opa, ds.scale, ds.rot, ds.sh, kd,
-                      rec.xy_depth[0], rec.conic_opa[0], rec.rgb[0], rec.box[0], rec.tiles[0])
+                      rec.xy_depth[0], rec.conic_opa[0], rec.rgb[0], rec.box[0], rec.rows[0], rec.tiles[0])
     ras = Raster(cam.width, cam.height, scene.n, capacity, DEV, accept_lists=lists)
     keys = torch.empty(max(capacity, 1), dtype=torch.int64, device=DEV)
     K = ras.forward(cam, rec.view(0), host_mode=True, bg=bg, sorted_keys=keys)
@@ -65,10 +65,12 @@ def gpu_projection(rec):
     # the record's conic is the Cholesky form (A, β, γ): B = A·β, C = γ + A·β² (dass.h)
     A, beta, gam = (co[:, k].astype(np.float64) for k in range(3))
     conic = np.stack([A, A * beta, gam + A * beta * beta], 1)
+    rows = np_(rec.rows[0]).view(np.uint32)
+    # visible = a non-empty box (a visible Gaussian's A50 footprint may still be empty)
     return dict(u=xy[:, 0].astype(np.float64) + ulo, v=xy[:, 1].astype(np.float64) + vlo,
                 zbits=xy[:, 2].view(np.uint32), conic=conic, opa=co[:, 3], rgb=rgb[:, :3],
                 clampbits=rgb[:, 3].astype(np.int32), box=b4.astype(np.int32), tiles=tiles,
-                visible=(tiles > 0).astype(np.uint8))
+                rows=rows, visible=(b4[:, 0] <= b4[:, 1]).astype(np.uint8))
 
 
 def check_projection(cam, scene, rec, keep=None):
@@ -79,6 +81,7 @@ def check_projection(cam, scene, rec, keep=None):
     assert np.array_equal(g["visible"], o["visible"])
     assert np.array_equal(g["zbits"][vis], o["zbits"][vis])
     assert np.array_equal(g["box"][vis], o["box"][vis])
+    assert np.array_equal(g["rows"], o["rows"])      # A50 footprints (KEY CHAIN 12-13)
     assert np.array_equal(g["tiles"], o["tiles"])
     # records: fp32 rounding of the fp64 values
     np.testing.assert_allclose(g["u"][vis], o["uvz"][vis, 0], rtol=0, atol=2e-6)
@@ -93,8 +96,9 @@ def check_projection(cam, scene, rec, keep=None):
 
 def check_binsort(cam, out, g):
     """Layer 1 of the comparison policy: the GPU's sort of its own projection
-    equals the oracle's brute-force sort of the same (visible, zbits, box)."""
-    keys, ids, ranges = oracle.bin_sort(cam, dict(visible=g["visible"], zbits=g["zbits"], box=g["box"]))
+    equals the oracle's brute-force sort of the same (visible, zbits, box, rows)."""
+    keys, ids, ranges = oracle.bin_sort(cam, dict(visible=g["visible"], zbits=g["zbits"], box=g["box"],
+                                                  rows=g["rows"]))
     assert out["K"] == len(keys)
     assert np.array_equal(out["keys"], keys)
     assert np.array_equal(out["ids"], ids)
@@ -228,7 +232,7 @@ def test_project_views_equals_per_view():
     ds = DeviceScene.from_host(sc, DEV)
     rec = ViewRecords(len(cams), sc.n, DEV)
     dass.dass_project_views(cams, 3, ds.pos_opa, ds.scale, ds.rot, ds.sh, None, rec.xy_depth,
-                            rec.conic_opa, rec.rgb, rec.box, rec.tiles)
+                            rec.conic_opa, rec.rgb, rec.box, rec.rows, rec.tiles)
     one = ViewRecords(1, sc.n, DEV)
     for v in (0, 7, 16, 19):
         dass.dass_project(cams[v], 3, ds.pos_opa, ds.scale, ds.rot, ds.sh, None, *one.view(0))

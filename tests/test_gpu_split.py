@@ -29,7 +29,7 @@ def rank_grads(cams, scene, ds, dLs, plan, capacity=1 << 21):
     my = [cams[v] for v in plan.views]
     rec = ViewRecords(len(my), scene.n, DEV)
     dass.dass_project_views(my, scene.sh_degree, ds.pos_opa, ds.scale, ds.rot, ds.sh, None,
-                            rec.xy_depth, rec.conic_opa, rec.rgb, rec.box, rec.tiles)
+                            rec.xy_depth, rec.conic_opa, rec.rgb, rec.box, rec.rows, rec.tiles)
     uv = [None if s < 0 else g.uv[s] for s in plan.split]
     mvp = MultiViewPass(my, scene.n, capacity, DEV, streams=2, tiles=plan.tiles, uv_out=uv)
     mvp.run(ds, rec, dLs[plan.views], g)

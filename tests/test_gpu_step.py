@@ -73,13 +73,15 @@ def test_c3_captured_step_graph_matches_oracle():
         xy = np_(stepper.records.xy_depth[v])
         box = np_(stepper.records.box[v]).view(np.uint32)
         tiles = np_(stepper.records.tiles[v]).view(np.uint32)
+        rows = np_(stepper.records.rows[v]).view(np.uint32)
         # a2 key chain, bit-exact against the oracle's fp32 replica
         o = oracle.project(cam, shifted)
         vis = o["visible"] == 1
-        assert np.array_equal((tiles > 0).astype(np.uint8), o["visible"]), v
-        assert np.array_equal(xy[:, 2].view(np.uint32)[vis], o["zbits"][vis]), v
         b4 = np.stack([box[:, 0] & 0xFFFF, box[:, 0] >> 16, box[:, 1] & 0xFFFF, box[:, 1] >> 16], 1)
+        assert np.array_equal((b4[:, 0] <= b4[:, 1]).astype(np.uint8), o["visible"]), v
+        assert np.array_equal(xy[:, 2].view(np.uint32)[vis], o["zbits"][vis]), v
         assert np.array_equal(b4[vis].astype(np.int32), o["box"][vis]), v
+        assert np.array_equal(rows, o["rows"]) and np.array_equal(tiles, o["tiles"]), v
         # a3-a5: sorted ids and tile ranges of the graph-mode sort, bit-exact
         keys, ids, ranges = oracle.bin_sort(cam, o)
         assert K[v] == len(ids), v

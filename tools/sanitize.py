@@ -65,7 +65,7 @@ def main():
     dass.dass_error_map(cam, ras.img, gt, 0.1, err, dm, sc.n, ds.pos_opa, s_err)
     feat = t(np.random.default_rng(2).normal(size=(sc.n, 16)).astype(np.float32))
     M = torch.empty(16, cam.height, cam.width, device=DEV)
-    xy, co, _, box, _ = rec.view(0)
+    xy, co, _, box, _, _ = rec.view(0)
     dass.dass_render_features(cam, ras.ranges, ras.sorted_ids, xy, co, box, feat, M)
     bad = torch.zeros(1, dtype=torch.int32, device=DEV)
     dass.dass_scan_nonfinite(g.pos_opa, bad, host_mode=True)
@@ -118,7 +118,7 @@ def main():
     rng = torch.empty(3, stepper.mvp.slots[0].num_tiles, 2, dtype=torch.int32, device=DEV)
     npairs = torch.zeros(3, 2, dtype=torch.int32, device=DEV)
     r = stepper.records
-    dass.dass_bin_sort_views(cams, sc3.n, r.xy_depth, r.box, r.tiles, wsb, 1 << 17, ids, rng, npairs)
+    dass.dass_bin_sort_views(cams, sc3.n, r.xy_depth, r.box, r.rows, r.tiles, wsb, 1 << 17, ids, rng, npairs)
     torch.cuda.synchronize()
     print("sanitize pass done; kernels launched:", dass.kernel_launches())
 
