@@ -96,6 +96,11 @@ def parse():
                    help="pair capacity per view (default 2^22, 2^23 for c5)")
     p.add_argument("--streams", type=int, default=20, help="overlapping per-view streams")
     p.add_argument("--no-graph", action="store_true", help="do not capture the step in a CUDA graph")
+    p.add_argument("--sort-chains", type=int, default=0, help="A/B: pipeline.PassOptions.sort_chains")
+    p.add_argument("--batch-sort", action="store_true", help="A/B: PassOptions.batch_sort")
+    p.add_argument("--sort-batch-chunks", type=int, default=4, help="A/B: PassOptions.sort_batch_chunks")
+    p.add_argument("--pre-chunks", type=int, default=2, help="A/B: PassOptions.pre_chunks")
+    p.add_argument("--proj-chunks", type=int, default=1, help="A/B: PassOptions.proj_chunks")
     p.add_argument("--lean", action="store_true",
                    help="only warm-up + timed steps (no stats/diagnostic passes): for ncu launch lists")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -252,7 +257,7 @@ def run_ours(args):
 
     from paper_2411_14847_b200 import dass, synth
     from paper_2411_14847_b200.dist import FlatGrads, FlatParams, allreduce_grads, view_plan
-    from paper_2411_14847_b200.pipeline import DeformFields, DeviceScene, Raster
+    from paper_2411_14847_b200.pipeline import DeformFields, DeviceScene, PassOptions, Raster
     from paper_2411_14847_b200.step import ShiftStep
 
     rank, world, local = dist_env()
@@ -297,9 +302,12 @@ def run_ours(args):
     dLs = torch.stack([t(synth.grad_image(cams[v], 1000 + v, 1.0 / (3 * W * H))) for v in mine]) \
         if mine else torch.empty(0, 3, H, W, device=dev)
     # the step (paper_2411_14847_b200/step.py): buffers, streams and call order
+    opts = PassOptions(sort_chains=args.sort_chains, batch_sort=args.batch_sort,
+                       sort_batch_chunks=args.sort_batch_chunks,
+                       pre_chunks=args.pre_chunks, proj_chunks=args.proj_chunks)
     stepper = ShiftStep(my_cams, n, deg, args.capacity, dev, streams=args.streams,
                         tiles=plan.tiles, split=plan.split, num_split=plan.num_split,
-                        shift=with_shift)
+                        shift=with_shift, options=opts)
     records, mvp = stepper.records, stepper.mvp
     if c4info is not None:   # every view's error map inside the step (C4)
         c4_serr = torch.zeros(scene.n, dtype=torch.uint8, device=dev)
@@ -810,6 +818,7 @@ def run_ours(args):
             "config": {"workload": wl, "n_gaussians": n, "views": len(cams), "width": W,
                        "height": H, "sh_degree": deg, "dynamic_frac": 0.3 if with_shift else None,
                        "cuda_graph": graph is not None, "streams": args.streams,
+                       "pass_options": vars(opts),
                        "emulated_share": args.emulate,
                        "parallelism": f"view-sharded dp{world}" + (
                            f" ({plan.num_split} views split into tile halves)" if plan.num_split else ""),

@@ -10,7 +10,6 @@ allocates the documented layouts and calls the exports in order:
 """
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -109,7 +108,7 @@ class Raster:
         bws = dass.dass_render_bwd_workspace(n)
         self.bwd_ws = torch.empty(bws // 4, dtype=torch.float32, device=device)
         self.accept = None
-        if accept_lists and os.environ.get("DASS_NO_LISTS") != "1":
+        if accept_lists:
             # forward-recorded acceptance lists consumed by the backward
             ab = dass.dass_render_accept_workspace(self.num_tiles, capacity)
             self.accept = torch.empty(ab // 4, dtype=torch.int32, device=device)
@@ -165,11 +164,33 @@ def fwd_bwd_views(cams, scene: DeviceScene, records: ViewRecords, raster: Raster
         raster.backward(cam, scene, rec, dL_dimgs[v], grads, keep=keep, bg=bg)
 
 
+@dataclass
+class PassOptions:
+    """Scheduling choices of a MultiViewPass (the defaults are the measured best,
+    DESIGN.md §7; bench.py exposes them for A/B runs).
+
+    sort_chains: 0 = every view sorts on its own stream; k > 0 = the sorts run one
+      after another on k high-priority streams.
+    batch_sort: dass_bin_sort_views over sort_batch_chunks chunks of the views
+      instead of one dass_bin_sort per view.
+    pre_chunks: the multi-view preprocess in chunks, each on a side stream as soon
+      as its views are rasterised.
+    proj_chunks: with a projection callback, the projection in chunks, each view
+      waiting only for its own chunk.
+    stream_prio: the first half of the view streams at a higher priority."""
+    sort_chains: int = 0
+    batch_sort: bool = False
+    sort_batch_chunks: int = 4
+    pre_chunks: int = 2
+    proj_chunks: int = 1
+    stream_prio: bool = False
+
+
 class MultiViewPass:
     """fwd+bwd over a fixed list of cameras with S overlapping streams."""
 
     def __init__(self, cams, n: int, capacity: int, device="cuda", streams: int = 4,
-                 tiles=None, uv_out=None):
+                 tiles=None, uv_out=None, options: PassOptions | None = None):
         """tiles[v]: None or a (begin, stride, count) tile subset of view v (a
         split view, dist.ViewPlan); uv_out[v]: None or the float2[n] block that
         view's ∇p̄ partials go to (the GPU with the view's tile half 0 counts it)."""
@@ -184,24 +205,25 @@ class MultiViewPass:
             if (c.width, c.height) != (W, H):
                 raise ValueError("all cameras of a pass must share the image size")
         self.S = max(1, min(streams, self.V))
+        opt = options or PassOptions()
+        self.options = opt
         self.slots = [Raster(W, H, n, capacity, device) for _ in range(self.S)]
-        # DASS_STREAM_PRIO=1: the streams of the first half of the views get the higher
+        # stream_prio: the streams of the first half of the views get the higher
         # priority, so those views finish first and their preprocess chunk overlaps the rest
-        prio = os.environ.get("DASS_STREAM_PRIO", "0") == "1"
-        self.streams = [torch.cuda.Stream(device=device, priority=-1 if prio and 2 * k < self.S else 0)
+        self.streams = [torch.cuda.Stream(device=device,
+                                          priority=-1 if opt.stream_prio and 2 * k < self.S else 0)
                         for k in range(self.S)]
         # bin_sort chains: with every view's sort on its own stream, the graph runs the
-        # 20 latency-bound sorts in lockstep (≈1.9 ms with no raster work ready).  The
-        # sorts instead run one after another on DASS_SORT_CHAINS streams (0 = on the
-        # view streams), so view 0 rasterises after one sort and the later sorts
-        # overlap the earlier views' raster kernels (tools/timeline.py).
-        nch = int(os.environ.get("DASS_SORT_CHAINS", "0"))
-        prio = -5 if os.environ.get("DASS_SORT_PRIO", "1") == "1" else 0
-        self.sort_streams = ([torch.cuda.Stream(device=device, priority=prio)
+        # 20 latency-bound sorts in lockstep.  sort_chains > 0 runs them one after
+        # another on that many high-priority streams instead, so view 0 rasterises
+        # after one sort and the later sorts overlap the earlier views' raster kernels
+        # (measured: not faster).
+        nch = opt.sort_chains
+        self.sort_streams = ([torch.cuda.Stream(device=device, priority=-5)
                               for _ in range(min(nch, self.S))] if nch > 0 else None)
         self.pre_stream = torch.cuda.Stream(device=device)
-        self.pre_chunks = int(os.environ.get("DASS_PRE_CHUNKS", "2"))
-        self.proj_chunks = int(os.environ.get("DASS_PROJ_CHUNKS", "1"))
+        self.pre_chunks = opt.pre_chunks
+        self.proj_chunks = opt.proj_chunks
         # optional hook(v, stream), called on view v's stream right before its backward:
         # an end-to-end caller makes the view wait there for its own ∂L/∂C upload
         self.before_bwd = None
@@ -212,16 +234,15 @@ class MultiViewPass:
         # (K_v, overflow_v) of every view's graph-mode sort, kept per view so a slot
         # reused by a later view does not overwrite an earlier view's overflow flag
         self.num_pairs = torch.zeros(max(self.V, 1), 2, dtype=torch.int32, device=device)
-        # DASS_BATCH_SORT=1: dass_bin_sort_views over chunks of the views instead of a
-        # dass_bin_sort per view.  In the graph the per-view sort chains run in lockstep
-        # (≈1.9 ms of the step with no raster work ready, tools/timeline.py), but the
-        # batched sort is slower still (2.6 ms isolated for 20 views: its 17-bit pair
-        # passes and emission are instruction-bound), so the per-view sorts stay default.
-        self.batch_sort = os.environ.get("DASS_BATCH_SORT", "0") == "1" and self.V > 0
+        # batch_sort: dass_bin_sort_views over chunks of the views instead of a
+        # dass_bin_sort per view.  In the graph the per-view sort chains run in lockstep,
+        # but the batched sort is slower still (its 17-bit pair passes and emission are
+        # instruction-bound), so the per-view sorts stay default.
+        self.batch_sort = opt.batch_sort and self.V > 0
         if self.batch_sort:
             T = self.slots[0].num_tiles
             # sort chunks: chunk c + 1 sorts on the main stream while chunk c rasterises
-            self.sort_chunks = max(1, min(int(os.environ.get("DASS_SORT_BATCH_CHUNKS", "4")), self.V))
+            self.sort_chunks = max(1, min(opt.sort_batch_chunks, self.V))
             vmax = -(-self.V // self.sort_chunks)
             ws = dass.dass_bin_sort_views_workspace(vmax, n, capacity)
             self.bs_ws = torch.empty(max(ws, 16), dtype=torch.uint8, device=device)

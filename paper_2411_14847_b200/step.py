@@ -16,7 +16,7 @@ from __future__ import annotations
 
 from . import dass
 from .dist import FlatGrads
-from .pipeline import DeviceScene, MultiViewPass, ViewRecords
+from .pipeline import DeviceScene, MultiViewPass, PassOptions, ViewRecords
 
 
 class StepBufs:
@@ -38,7 +38,7 @@ class ShiftStep:
 
     def __init__(self, cams, n: int, sh_degree: int, capacity: int, device, streams: int = 20,
                  tiles=None, split=None, num_split: int = 0, validate: bool = False,
-                 shift: bool = True):
+                 shift: bool = True, options: PassOptions | None = None):
         """validate: the step ends with dass_scan_nonfinite over its gradients (graph
         mode); check_numerics() then raises DASS_ERR_NUMERICAL on NaN / Inf.
         shift=False: a plain fwd+bwd of the given Gaussians (BASELINE configs C1/C2),
@@ -51,7 +51,7 @@ class ShiftStep:
         self.num_split = num_split
         self.records = ViewRecords(max(len(self.cams), 1), n, device)
         self.mvp = MultiViewPass(self.cams, n, capacity, device, streams=streams,
-                                 tiles=self.tiles) if self.cams else None
+                                 tiles=self.tiles, options=options) if self.cams else None
         self.shifted_pos = torch.empty(n, 4, dtype=torch.float32, device=device)
         self.shifted_rot = torch.empty(n, 4, dtype=torch.float32, device=device)
         self._errmap_pos = None

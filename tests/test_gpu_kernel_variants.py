@@ -1,12 +1,12 @@
-"""The raster kernels' selectable variants stay parity-green: the two-warp-per-tile
-list kernels (DASS_TILE_WARP=0) and the batched multi-view sort inside the
-overlapped pass (DASS_BATCH_SORT=1).  The switches are read once per process, so
-each variant runs the parity selection in a child pytest process."""
-import os
-import subprocess
-import sys
-
+"""The pass's selectable schedules stay parity-green: the batched multi-view sort
+(PassOptions.batch_sort) and the chained sorts (PassOptions.sort_chains) inside
+the overlapped pass, against the oracle's per-view sums."""
+import numpy as np
 import pytest
+
+import oracle
+from _parity import grad_compare
+from paper_2411_14847_b200 import synth
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -14,17 +14,39 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # pragma: no cover - CPU box
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+from paper_2411_14847_b200.pipeline import (DeviceScene, Grads, MultiViewPass,  # noqa: E402
+                                            PassOptions, ViewRecords, project_all)
+
+DEV = "cuda"
 
 
-@pytest.mark.parametrize("env,sel", [
-    ({"DASS_TILE_WARP": "0"}, "c1_full or ragged or ties or c2_full"),
-    ({"DASS_BATCH_SORT": "1"}, "multiview"),
-])
-def test_variant_parity(env, sel):
-    e = dict(os.environ, **env)
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
-                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", sel],
-                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=1200)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert " passed" in r.stdout
+@pytest.mark.parametrize("opts", [PassOptions(batch_sort=True, sort_batch_chunks=2),
+                                  PassOptions(sort_chains=2), PassOptions(pre_chunks=1, proj_chunks=1)],
+                         ids=["batch_sort", "sort_chains", "single_preprocess"])
+def test_pass_options_parity(opts):
+    cams = synth.n3dv_rig(width=160, height=120, num_views=4)
+    sc = synth.n3dv_scene(n=5000, seed=57, degree=2, fx=cams[0].fx)
+    ds = DeviceScene.from_host(sc, DEV)
+    rec = ViewRecords(len(cams), sc.n, DEV)
+    dLs = np.stack([synth.grad_image(c, 700 + v) for v, c in enumerate(cams)])
+    g = Grads.zeros(sc.n, 2, DEV)
+    mv = MultiViewPass(cams, sc.n, 1 << 20, DEV, streams=2, options=opts)
+    project_all(cams, ds, rec)
+    mv.run(ds, rec, torch.from_numpy(dLs).to(DEV), g)
+    torch.cuda.synchronize()
+    assert mv.overflowed_views() == []
+    keys = ("g_pos_opa", "g_scale", "g_rot", "k_pos_opa", "k_scale", "k_rot", "t_pos_opa",
+            "t_scale", "t_rot", "gradstat_cnt")
+    ref = None
+    gtie = np.zeros(sc.n, bool)
+    for v, cam in enumerate(cams):
+        o = oracle.render_bwd(cam, sc, dLs[v], kappa=True)
+        gtie |= o["gtie"] == 1
+        ref = {k: o[k].copy() for k in keys} if ref is None else {k: ref[k] + o[k] for k in keys}
+    ok = ~gtie
+    np_ = lambda t: t.detach().cpu().numpy()
+    grad_compare("pos", np_(g.pos_opa)[ok], ref["g_pos_opa"][ok], ref["k_pos_opa"][ok], slack=ref["t_pos_opa"][ok])
+    grad_compare("scale", np_(g.scale)[ok, :3], ref["g_scale"][ok, :3], ref["k_scale"][ok, :3],
+                 slack=ref["t_scale"][ok, :3])
+    grad_compare("rot", np_(g.rot)[ok], ref["g_rot"][ok], ref["k_rot"][ok], slack=ref["t_rot"][ok])
+    assert np.array_equal(np_(g.gradstat_cnt), ref["gradstat_cnt"])

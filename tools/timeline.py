@@ -28,19 +28,19 @@ def run():
     main = torch.cuda.current_stream()
     dass.dass_timestamp(stamps, 0, main)
     dass.dass_project_views(cams, sc.sh_degree, ds.pos_opa, ds.scale, ds.rot, ds.sh, None,
-                            rec.xy_depth, rec.conic_opa, rec.rgb, rec.box, rec.tiles)
+                            rec.xy_depth, rec.conic_opa, rec.rgb, rec.box, rec.rows, rec.tiles)
     dass.dass_timestamp(stamps, 1, main)
     for v, cam in enumerate(cams):
         k = v % S
         r, st = slots[k], streams[k]
         st.wait_stream(main)
-        xy, co, rgb, box, tt = rec.view(v)
+        xy, co, rgb, box, rows, tt = rec.view(v)
         ss = sstreams[v % CH] if CH else st
         if CH:
             ss.wait_stream(st)
         with torch.cuda.stream(ss):
             dass.dass_timestamp(stamps, 3 + 4 * v, ss)
-            dass.dass_bin_sort(cam, sc.n, xy, box, tt, r.sort_ws, r.capacity, None, r.sorted_ids,
+            dass.dass_bin_sort(cam, sc.n, xy, box, rows, tt, r.sort_ws, r.capacity, None, r.sorted_ids,
                                r.ranges, r.num_pairs)
             dass.dass_timestamp(stamps, 4 + 4 * v, ss)
         if CH:
