@@ -666,12 +666,15 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
     last[p] = range.x;
     if (tx0 + pm.x(p) < cam.W && ty0 + pm.y(p) < cam.H) live |= 1u << p;
   }
-  const float fx0 = (float)pm.x(0), fx1 = (float)pm.x(4);
-  float fy[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) fy[r] = (float)pm.y(r);
-  uint8_t* lbytes = acc.bytes + (size_t)range.x * 32 + lane;   // this lane's byte of list entry 0
-  uint32_t* lidx = acc.idx + range.x;
+  // the lane's pixel coordinates (tile-local columns fx0, fx1, rows fy0..fy3), read
+  // from shared memory per candidate entry instead of re-derived from the lane id
+  // (the compiler rematerialises registers here: 64-register budget)
+  __shared__ float4 s_pc[32];
+  __shared__ float2 s_pc2[32];
+  s_pc[lane] = make_float4((float)pm.x(0), (float)pm.x(4), (float)pm.y(0), (float)pm.y(1));
+  s_pc2[lane] = make_float2((float)pm.y(2), (float)pm.y(3));
+  uint8_t* const lbytes = acc.bytes + lane;   // this lane's byte of every list entry
+  uint32_t nlist = range.x;                    // next list entry
   for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
     if (!__any_sync(0xffffffffu, live != 0u)) break;
     __syncwarp();   // the previous batch is consumed
@@ -688,7 +691,10 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
       const uint32_t cand = pm.cand(m) & live;
       if (cand) {
         const float4 co = st.co;
-        const float X0 = col_term(co, a.x - fx0), X1 = col_term(co, a.x - fx1);
+        const float4 pc = s_pc[lane];
+        const float2 pc2 = s_pc2[lane];
+        const float fy[4] = {pc.z, pc.w, pc2.x, pc2.y};
+        const float X0 = col_term(co, a.x - pc.x), X1 = col_term(co, a.x - pc.y);
         float pw[PPT];
         uint32_t ok = 0;
 #pragma unroll
@@ -722,14 +728,13 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
         }
       }
       if (__any_sync(0xffffffffu, accb != 0u)) {
-        *lbytes = (uint8_t)accb;
-        if (lane == 0) *lidx = b0 + j;
-        lbytes += 32;
-        ++lidx;
+        lbytes[(size_t)nlist * 32] = (uint8_t)accb;
+        if (lane == 0) acc.idx[nlist] = b0 + j;
+        ++nlist;
       }
     }
   }
-  if (lane == 0) acc.cnt[tile] = (uint32_t)(lidx - (acc.idx + range.x));
+  if (lane == 0) acc.cnt[tile] = nlist - range.x;
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int X = tx0 + pm.x(p), Y = ty0 + pm.y(p);
