@@ -131,7 +131,12 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region.
+
+    A reader thread collects the 100 ms samples as they arrive, so a timed region
+    shorter than a few sampling intervals (C1, C2) can be followed by untimed
+    repeats of the same step until enough samples are in (`extend`); the summary
+    then says how many repeats the window held."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -139,37 +144,60 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.rows = []
+        self.repeats = 0
+
+    def _read(self):
+        for line in self.proc.stdout:
+            if line.count(",") >= 7:
+                self.rows.append(line.split(","))
 
     def __enter__(self):
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
         except OSError:
             self.proc = None
         return self
 
+    def extend(self, step, sync, min_samples=3, max_s=3.0):
+        """Run untimed repeats of `step` until min_samples samples were taken."""
+        if self.proc is None:
+            return
+        t0 = time.time()
+        while len(self.rows) < min_samples and time.time() - t0 < max_s:
+            for _ in range(8):
+                step()
+                self.repeats += 1
+            sync()
+
     def __exit__(self, *a):
-        self.out = ""
         if self.proc is not None:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                self.out, _ = self.proc.communicate()
+            self.thread.join(timeout=5)
 
     def summary(self):
-        rows = [r.split(",") for r in (self.out or "").strip().splitlines() if r.count(",") >= 7]
+        rows = list(self.rows)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         sm = [float(r[0]) for r in rows]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].strip() == "Active"})
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]),
-                "power_w_max": max(float(r[2]) for r in rows), "reasons": reasons,
-                "samples": len(rows)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]),
+               "power_w_max": max(float(r[2]) for r in rows), "reasons": reasons,
+               "samples": len(rows)}
+        if self.repeats:
+            out["window"] = f"the timed steps + {self.repeats} untimed repeats of the same step"
+        return out
 
 
 def peaks():
@@ -417,9 +445,11 @@ def run_ours(args):
             step_ev[k + 1].record()
         ev1.record()
         barrier()
+        launches = dass.kernel_launches() - l0
+        if not distd:            # ranks would disagree on the repeat count (collectives)
+            clk.extend(timed, torch.cuda.synchronize)
     per_step = np.array([step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps)])
     stepper.check_overflow()     # the timed steps' sorts all fit (checked after the timing)
-    launches = dass.kernel_launches() - l0
     if graph is not None:
         launches = per_step_launches * args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
