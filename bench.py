@@ -101,6 +101,8 @@ def parse():
     p.add_argument("--sort-batch-chunks", type=int, default=4, help="A/B: PassOptions.sort_batch_chunks")
     p.add_argument("--pre-chunks", type=int, default=2, help="A/B: PassOptions.pre_chunks")
     p.add_argument("--proj-chunks", type=int, default=1, help="A/B: PassOptions.proj_chunks")
+    p.add_argument("--no-split-project", action="store_true",
+                   help="A/B: PassOptions.split_project=False (keys and records on one stream)")
     p.add_argument("--lean", action="store_true",
                    help="only warm-up + timed steps (no stats/diagnostic passes): for ncu launch lists")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -332,7 +334,8 @@ def run_ours(args):
     # the step (paper_2411_14847_b200/step.py): buffers, streams and call order
     opts = PassOptions(sort_chains=args.sort_chains, batch_sort=args.batch_sort,
                        sort_batch_chunks=args.sort_batch_chunks,
-                       pre_chunks=args.pre_chunks, proj_chunks=args.proj_chunks)
+                       pre_chunks=args.pre_chunks, proj_chunks=args.proj_chunks,
+                       split_project=not args.no_split_project)
     stepper = ShiftStep(my_cams, n, deg, args.capacity, dev, streams=args.streams,
                         tiles=plan.tiles, split=plan.split, num_split=plan.num_split,
                         shift=with_shift, options=opts)
@@ -505,12 +508,12 @@ def run_ours(args):
             fields.forward(base.pos_opa, mu_f, sigma_f)
             dass.dass_apply_shift(base.pos_opa, base.rot, mu_f, sigma_f, None,
                                   shifted.pos_opa, shifted.rot)
-            def project(v0, v1):
-                dass.dass_project_views(my_cams[v0:v1], deg, shifted.pos_opa, shifted.scale,
-                                        shifted.rot, shifted.sh, None, records.xy_depth[v0:v1],
-                                        records.conic_opa[v0:v1], records.rgb[v0:v1],
-                                        records.box[v0:v1], records.rows[v0:v1],
-                                        records.tiles[v0:v1])
+            def project(v0, v1, part=dass.DASS_PROJECT_ALL):
+                dass.dass_project_views_part(part, my_cams[v0:v1], deg, shifted.pos_opa,
+                                             shifted.scale, shifted.rot, shifted.sh, None,
+                                             records.xy_depth[v0:v1], records.conic_opa[v0:v1],
+                                             records.rgb[v0:v1], records.box[v0:v1],
+                                             records.rows[v0:v1], records.tiles[v0:v1])
             mvp.run(shifted, records, None, grads, gts=gts, project=project)
             dass.dass_apply_shift_bwd(base.rot, sigma_f, None, grads.pos_opa, grads.rot,
                                       g_mu, g_sigma)

@@ -234,6 +234,30 @@ int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n,
                        float* conic_opa, float* rgb, uint32_t* box,
                        uint32_t* tile_rows, uint32_t* tiles_touched, void* stream);
 
+/* dass_project_views_part — dass_project_views in two parts that may run on two
+ * streams (same arguments, plus `part`):
+ *  DASS_PROJECT_KEYS (1): the KEY CHAIN with its footprint — writes xy_depth
+ *    as (0, 0, z, 0), box, tile_rows, tiles_touched: everything dass_bin_sort
+ *    reads.  sh and conic_opa / rgb are not touched.
+ *  DASS_PROJECT_RECORDS (2): reads box (the keys' visibility decision) and
+ *    writes words 0, 1 and 3 of xy_depth (u_hi, v_hi, the fp16 lo pair),
+ *    conic_opa and rgb.  Must be ordered after the KEYS part of the same
+ *    arrays; writes no byte the KEYS part or dass_bin_sort reads, so it may run
+ *    concurrently with dass_bin_sort of the same views.  The raster calls
+ *    must be ordered after it.
+ *  DASS_PROJECT_ALL (3): both in order on `stream` (= dass_project_views).
+ * After both parts every output equals dass_project_views' bit for bit.
+ * INVALID_ARG as dass_project_views, or part ∉ {1, 2, 3}. */
+#define DASS_PROJECT_KEYS 1
+#define DASS_PROJECT_RECORDS 2
+#define DASS_PROJECT_ALL 3
+int dass_project_views_part(int32_t part, const dass_camera* cams, int32_t num_views,
+                            int32_t n, int32_t sh_degree, const float* pos_opa,
+                            const float* scale, const float* rot, const float* sh,
+                            const uint8_t* keep_mask, float* xy_depth,
+                            float* conic_opa, float* rgb, uint32_t* box,
+                            uint32_t* tile_rows, uint32_t* tiles_touched, void* stream);
+
 /* ---------------------------------------------------------------------------
  * dass_bin_sort — tile binning + sort + per-tile ranges (a3-a5; P:29
  * "tile-based"; A03, A04, A50).  For every visible Gaussian i and every tile

@@ -144,8 +144,8 @@ int dass_apply_shift_bwd(int32_t n, const float* rot, const float* sigma, const 
                      "dass_apply_shift_bwd");
 }
 
-static int project_common(const dass_camera* cams, int32_t num_views, int32_t n, int32_t sh_degree,
-                          const float* pos_opa, const float* scale, const float* rot,
+static int project_common(int part, const dass_camera* cams, int32_t num_views, int32_t n,
+                          int32_t sh_degree, const float* pos_opa, const float* scale, const float* rot,
                           const float* sh, const uint8_t* keep, float* xy_depth, float* conic_opa,
                           float* rgb, uint32_t* box, uint32_t* tile_rows, uint32_t* tiles,
                           void* stream) {
@@ -157,6 +157,8 @@ static int project_common(const dass_camera* cams, int32_t num_views, int32_t n,
   }
   if (n < 0) return fail(DASS_ERR_INVALID_ARG, "n < 0%s");
   if (sh_degree < 0 || sh_degree > 3) return fail(DASS_ERR_INVALID_ARG, "sh_degree must be in [0, 3]%s");
+  if (part < DASS_PROJECT_KEYS || part > DASS_PROJECT_ALL)
+    return fail(DASS_ERR_INVALID_ARG, "dass_project_views_part: part must be 1, 2 or 3%s");
   if (n == 0) return DASS_OK;
   if (!pos_opa || !scale || !rot || !sh || !xy_depth || !conic_opa || !rgb || !box || !tile_rows ||
       !tiles)
@@ -164,10 +166,11 @@ static int project_common(const dass_camera* cams, int32_t num_views, int32_t n,
   if (!aligned16(tile_rows)) return fail(DASS_ERR_INVALID_ARG, "dass_project: tile_rows must be 16-byte aligned%s");
   CamParams cp[64];
   for (int v = 0; v < num_views; ++v) cp[v] = to_params(cams + v);
-  return cuda_status(launch_project(cp, num_views, n, sh_degree, (const float4*)pos_opa,
-                                    (const float4*)scale, (const float4*)rot, (const float4*)sh,
-                                    keep, (float4*)xy_depth, (float4*)conic_opa, (float4*)rgb,
-                                    (uint2*)box, (uint4*)tile_rows, tiles, (cudaStream_t)stream),
+  return cuda_status(launch_project_part(part, cp, num_views, n, sh_degree, (const float4*)pos_opa,
+                                         (const float4*)scale, (const float4*)rot,
+                                         (const float4*)sh, keep, (float4*)xy_depth,
+                                         (float4*)conic_opa, (float4*)rgb, (uint2*)box,
+                                         (uint4*)tile_rows, tiles, (cudaStream_t)stream),
                      "dass_project");
 }
 
@@ -175,8 +178,8 @@ int dass_project(const dass_camera* cam, int32_t n, int32_t sh_degree, const flo
                  const float* scale, const float* rot, const float* sh, const uint8_t* keep_mask,
                  float* xy_depth, float* conic_opa, float* rgb, uint32_t* box,
                  uint32_t* tile_rows, uint32_t* tiles_touched, void* stream) {
-  return project_common(cam, 1, n, sh_degree, pos_opa, scale, rot, sh, keep_mask, xy_depth,
-                        conic_opa, rgb, box, tile_rows, tiles_touched, stream);
+  return project_common(DASS_PROJECT_ALL, cam, 1, n, sh_degree, pos_opa, scale, rot, sh,
+                        keep_mask, xy_depth, conic_opa, rgb, box, tile_rows, tiles_touched, stream);
 }
 
 int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n, int32_t sh_degree,
@@ -184,7 +187,17 @@ int dass_project_views(const dass_camera* cams, int32_t num_views, int32_t n, in
                        const uint8_t* keep_mask, float* xy_depth, float* conic_opa, float* rgb,
                        uint32_t* box, uint32_t* tile_rows, uint32_t* tiles_touched, void* stream) {
   if (cams == nullptr) return fail(DASS_ERR_INVALID_ARG, "cams is null%s");
-  return project_common(cams, num_views, n, sh_degree, pos_opa, scale, rot, sh, keep_mask,
+  return project_common(DASS_PROJECT_ALL, cams, num_views, n, sh_degree, pos_opa, scale, rot, sh,
+                        keep_mask, xy_depth, conic_opa, rgb, box, tile_rows, tiles_touched, stream);
+}
+
+int dass_project_views_part(int32_t part, const dass_camera* cams, int32_t num_views, int32_t n,
+                            int32_t sh_degree, const float* pos_opa, const float* scale,
+                            const float* rot, const float* sh, const uint8_t* keep_mask,
+                            float* xy_depth, float* conic_opa, float* rgb, uint32_t* box,
+                            uint32_t* tile_rows, uint32_t* tiles_touched, void* stream) {
+  if (cams == nullptr) return fail(DASS_ERR_INVALID_ARG, "cams is null%s");
+  return project_common(part, cams, num_views, n, sh_degree, pos_opa, scale, rot, sh, keep_mask,
                         xy_depth, conic_opa, rgb, box, tile_rows, tiles_touched, stream);
 }
 

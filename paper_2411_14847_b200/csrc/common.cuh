@@ -115,11 +115,14 @@ cudaError_t launch_shift(int n, const float4* pos, const float4* rot, const floa
 cudaError_t launch_shift_bwd(int n, const float4* rot, const float4* sigma, const uint8_t* mask,
                              const float4* g_pos_out, const float4* g_rot_out, float4* g_mu,
                              float4* g_sigma, cudaStream_t s);
-cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_degree,
-                           const float4* pos_opa, const float4* scale, const float4* rot,
-                           const float4* sh, const uint8_t* keep, float4* xy_depth,
-                           float4* conic_opa, float4* rgb, uint2* box, uint4* rows,
-                           uint32_t* tiles, cudaStream_t s);
+// part: PROJECT_KEYS (key chain + footprint), PROJECT_RECORDS (fp64 records +
+// colour; needs the keys' box), or both in that order
+constexpr int PROJECT_KEYS = 1, PROJECT_RECORDS = 2;
+cudaError_t launch_project_part(int part, const CamParams* cams, int num_views, int n,
+                                int sh_degree, const float4* pos_opa, const float4* scale,
+                                const float4* rot, const float4* sh, const uint8_t* keep,
+                                float4* xy_depth, float4* conic_opa, float4* rgb, uint2* box,
+                                uint4* rows, uint32_t* tiles, cudaStream_t s);
 size_t binsort_workspace(int n, int num_tiles, int64_t capacity);
 cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, const uint2* box,
                            const uint4* rows, const uint32_t* tiles, void* ws, int64_t capacity,

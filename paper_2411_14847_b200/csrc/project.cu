@@ -270,8 +270,44 @@ __device__ __forceinline__ Records accurate_records(const CamParams& c, float4 p
   return r;
 }
 
+// The projection runs as two launches ("a1 in two parts"):
+//  * project_keys_kernel — the KEY CHAIN and its footprint: depth, box, tile rows,
+//    tile count, i.e. everything dass_bin_sort reads; xy_depth gets (0, 0, z, 0);
+//  * project_records_kernel — the fp64 records and the SH colour, which only the
+//    raster kernels read: xy_depth's (u_hi, v_hi) and lo word, conic_opa, rgb.
+// The two write disjoint bytes, so the records may run on a side stream while the
+// views' sorts (which read xy_depth.z only) run — off the step's critical path.
+__global__ void __launch_bounds__(256) project_keys_kernel(const __grid_constant__ ProjectArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const float4 po = a.pos_opa[i];
+  const float4 sc = a.scale[i];
+  const float4 q = a.rot[i];
+  const bool kept = a.keep == nullptr || a.keep[i] != 0;
+  const float o_eff = kept ? po.w : 0.f;
+  const float keepf = kept ? 1.f : 0.f;
+  const int va = blockIdx.y * a.vpt, vb = min(a.num_views, va + a.vpt);
+  for (int v = va; v < vb; ++v) {
+    const CamParams& c = a.cam[v];
+    const size_t o = (size_t)(a.view_offset + v) * a.n + i;
+    const KeyResult k = key_chain(c, po.x, po.y, po.z, o_eff, sc.x * keepf, sc.y * keepf,
+                                  sc.z * keepf, q);
+    if (!k.visible) {
+      a.xy_depth[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a.box[o] = make_uint2(1u, 1u);     // x0 = 1 > x1 = 0: the invisible sentinel
+      a.rows[o] = make_uint4(0u, 0u, 0u, 0u);
+      a.tiles[o] = 0u;
+      continue;
+    }
+    a.xy_depth[o] = make_float4(0.f, 0.f, k.z, 0.f);
+    a.box[o] = make_uint2((uint32_t)k.x0 | ((uint32_t)k.x1 << 16), (uint32_t)k.y0 | ((uint32_t)k.y1 << 16));
+    a.rows[o] = k.rows;
+    a.tiles[o] = k.tiles;
+  }
+}
+
 template <int DEG>
-__global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__ ProjectArgs a) {
+__global__ void __launch_bounds__(256) project_records_kernel(const __grid_constant__ ProjectArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   const float4 po = a.pos_opa[i];
@@ -281,21 +317,14 @@ __global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__
   const float o_eff = kept ? po.w : 0.f;
   const float keepf = kept ? 1.f : 0.f;
   using L = SHLayout<DEG>;
-  // views [blockIdx.y·vpt, …): a 2-D grid over (Gaussians, view groups) keeps many
-  // warps resident; the per-Gaussian parameters are re-read per group (L2 hits)
   const int va = blockIdx.y * a.vpt, vb = min(a.num_views, va + a.vpt);
   for (int v = va; v < vb; ++v) {
     const CamParams& c = a.cam[v];
     const size_t o = (size_t)(a.view_offset + v) * a.n + i;
-    const KeyResult k = key_chain(c, po.x, po.y, po.z, o_eff, sc.x * keepf, sc.y * keepf,
-                                  sc.z * keepf, q);
-    if (!k.visible) {
-      a.xy_depth[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint2 bx = a.box[o];           // the key chain's visibility decision
+    if ((bx.x & 0xFFFFu) > (bx.x >> 16)) {
       a.conic_opa[o] = make_float4(0.f, 0.f, 0.f, 0.f);
       a.rgb[o] = make_float4(0.f, 0.f, 0.f, 0.f);
-      a.box[o] = make_uint2(1u, 1u);
-      a.rows[o] = make_uint4(0u, 0u, 0u, 0u);
-      a.tiles[o] = 0u;
       continue;
     }
     const Records r = accurate_records(c, po, sc, q, keepf);
@@ -306,8 +335,7 @@ __global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__
     float Y[L::NC];
     sh_eval<DEG>(dx, dy, dz, Y);
     // SH planes re-read per view (L1/L2-resident after the first view) instead
-    // of pinning 4·K4 registers across the view loop: 159 → fewer registers,
-    // 4× the resident warps
+    // of pinning 4·K4 registers across the view loop
     float col[3] = {0.5f, 0.5f, 0.5f};
 #pragma unroll
     for (int j = 0; j < L::K4; ++j) {
@@ -324,41 +352,58 @@ __global__ void __launch_bounds__(256, 2) project_kernel(const __grid_constant__
     for (int ch = 0; ch < 3; ++ch)
       if (col[ch] < 0.f) { bits |= 1 << ch; col[ch] = 0.f; }
     const __half2 lo = __halves2half2(r.u_lo, r.v_lo);
-    a.xy_depth[o] = make_float4(r.u_hi, r.v_hi, k.z, __uint_as_float(*(const uint32_t*)&lo));
+    float* xyd = reinterpret_cast<float*>(a.xy_depth + o);   // z (word 2) is the key chain's
+    *reinterpret_cast<float2*>(xyd) = make_float2(r.u_hi, r.v_hi);
+    xyd[3] = __uint_as_float(*(const uint32_t*)&lo);
     a.conic_opa[o] = make_float4(r.A, r.beta, r.gamma, o_eff);
     a.rgb[o] = make_float4(col[0], col[1], col[2], (float)bits);
-    a.box[o] = make_uint2((uint32_t)k.x0 | ((uint32_t)k.x1 << 16), (uint32_t)k.y0 | ((uint32_t)k.y1 << 16));
-    a.rows[o] = k.rows;
-    a.tiles[o] = k.tiles;
   }
 }
 
 }  // namespace
 
-cudaError_t launch_project(const CamParams* cams, int num_views, int n, int sh_degree,
-                           const float4* pos_opa, const float4* scale, const float4* rot,
-                           const float4* sh, const uint8_t* keep, float4* xy_depth,
-                           float4* conic_opa, float4* rgb, uint2* box, uint4* rows,
-                           uint32_t* tiles, cudaStream_t s) {
+static ProjectArgs project_args(const CamParams* cams, int v0, int num_views, int n,
+                                const float4* pos_opa, const float4* scale, const float4* rot,
+                                const float4* sh, const uint8_t* keep, float4* xy_depth,
+                                float4* conic_opa, float4* rgb, uint2* box, uint4* rows,
+                                uint32_t* tiles) {
+  ProjectArgs a;
+  a.num_views = num_views - v0 < MAXV ? num_views - v0 : MAXV;
+  for (int v = 0; v < a.num_views; ++v) a.cam[v] = cams[v0 + v];
+  a.n = n; a.view_offset = v0;
+  a.pos_opa = pos_opa; a.scale = scale; a.rot = rot; a.sh = sh; a.keep = keep;
+  a.xy_depth = xy_depth; a.conic_opa = conic_opa; a.rgb = rgb; a.box = box; a.rows = rows;
+  a.tiles = tiles;
+  a.vpt = MAXV;   // every view of the launch per thread (measured fastest)
+  return a;
+}
+
+cudaError_t launch_project_part(int part, const CamParams* cams, int num_views, int n,
+                                int sh_degree, const float4* pos_opa, const float4* scale,
+                                const float4* rot, const float4* sh, const uint8_t* keep,
+                                float4* xy_depth, float4* conic_opa, float4* rgb, uint2* box,
+                                uint4* rows, uint32_t* tiles, cudaStream_t s) {
   for (int v0 = 0; v0 < num_views; v0 += MAXV) {
-    ProjectArgs a;
-    a.num_views = num_views - v0 < MAXV ? num_views - v0 : MAXV;
-    for (int v = 0; v < a.num_views; ++v) a.cam[v] = cams[v0 + v];
-    a.n = n; a.view_offset = v0;
-    a.pos_opa = pos_opa; a.scale = scale; a.rot = rot; a.sh = sh; a.keep = keep;
-    a.xy_depth = xy_depth; a.conic_opa = conic_opa; a.rgb = rgb; a.box = box; a.rows = rows;
-    a.tiles = tiles;
-    a.vpt = MAXV;   // every view of the launch per thread (measured fastest)
+    const ProjectArgs a = project_args(cams, v0, num_views, n, pos_opa, scale, rot, sh, keep,
+                                       xy_depth, conic_opa, rgb, box, rows, tiles);
     const dim3 grid(div_up(n, 256), div_up(a.num_views, a.vpt));
-    switch (sh_degree) {
-      case 0: project_kernel<0><<<grid, 256, 0, s>>>(a); break;
-      case 1: project_kernel<1><<<grid, 256, 0, s>>>(a); break;
-      case 2: project_kernel<2><<<grid, 256, 0, s>>>(a); break;
-      default: project_kernel<3><<<grid, 256, 0, s>>>(a); break;
+    if (part & PROJECT_KEYS) {
+      project_keys_kernel<<<grid, 256, 0, s>>>(a);
+      launch_counted();
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
     }
-    launch_counted();
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    if (part & PROJECT_RECORDS) {
+      switch (sh_degree) {
+        case 0: project_records_kernel<0><<<grid, 256, 0, s>>>(a); break;
+        case 1: project_records_kernel<1><<<grid, 256, 0, s>>>(a); break;
+        case 2: project_records_kernel<2><<<grid, 256, 0, s>>>(a); break;
+        default: project_records_kernel<3><<<grid, 256, 0, s>>>(a); break;
+      }
+      launch_counted();
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
   }
   return cudaSuccess;
 }

@@ -26,6 +26,7 @@ DASS_ERR_CUDA = 5
 EXPORTS = (
     "dass_status_string", "dass_last_error", "dass_abi_version", "dass_kernel_launches",
     "dass_apply_shift", "dass_apply_shift_bwd", "dass_project", "dass_project_views",
+    "dass_project_views_part",
     "dass_bin_sort_workspace", "dass_bin_sort", "dass_render_accept_workspace", "dass_render_fwd",
     "dass_render_bwd_workspace",
     "dass_render_bwd", "dass_render_bwd_raster", "dass_render_bwd_preprocess_views",
@@ -107,6 +108,7 @@ def lib():
         L.dass_apply_shift_bwd.argtypes = [i32, P, P, P, P, P, P, P, P]
         L.dass_project.argtypes = [P, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P]
         L.dass_project_views.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_project_views_part.argtypes = [i32, P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P]
         L.dass_bin_sort_workspace.argtypes = [i32, i32, i64, P]
         L.dass_bin_sort.argtypes = [P, i32, P, P, P, P, P, C.c_size_t, i64, P, P, P, P, P, P]
         L.dass_bin_sort_views_workspace.argtypes = [i32, i32, i64, P]
@@ -233,6 +235,20 @@ def dass_project_views(cams, sh_degree, pos_opa, scale, rot, sh, keep_mask, xy_d
                                     _ptr(xy_depth), _ptr(conic_opa), _ptr(rgb), _ptr(box),
                                     _ptr(tile_rows), _ptr(tiles_touched), _stream(stream)),
            "dass_project_views")
+
+
+DASS_PROJECT_KEYS, DASS_PROJECT_RECORDS, DASS_PROJECT_ALL = 1, 2, 3
+
+
+def dass_project_views_part(part, cams, sh_degree, pos_opa, scale, rot, sh, keep_mask, xy_depth,
+                            conic_opa, rgb, box, tile_rows, tiles_touched, stream=None):
+    arr = (dass_camera * len(cams))(*[_cam(c) for c in cams])
+    _check(lib().dass_project_views_part(part, arr, len(cams), pos_opa.shape[0], sh_degree,
+                                         _ptr(pos_opa), _ptr(scale), _ptr(rot), _ptr(sh),
+                                         _ptr(keep_mask), _ptr(xy_depth), _ptr(conic_opa),
+                                         _ptr(rgb), _ptr(box), _ptr(tile_rows),
+                                         _ptr(tiles_touched), _stream(stream)),
+           "dass_project_views_part")
 
 
 def dass_bin_sort_workspace(n, num_tiles, pair_capacity) -> int:

@@ -177,12 +177,16 @@ class PassOptions:
       as its views are rasterised.
     proj_chunks: with a projection callback, the projection in chunks, each view
       waiting only for its own chunk.
+    split_project: with a projection callback, the projection's records part
+      (fp64 records + colour, DASS_PROJECT_RECORDS) on a side stream under the
+      views' sorts; the sorts wait only for the keys part, the forwards for both.
     stream_prio: the first half of the view streams at a higher priority."""
     sort_chains: int = 0
     batch_sort: bool = False
     sort_batch_chunks: int = 4
     pre_chunks: int = 2
     proj_chunks: int = 1
+    split_project: bool = True
     stream_prio: bool = False
 
 
@@ -222,6 +226,7 @@ class MultiViewPass:
         self.sort_streams = ([torch.cuda.Stream(device=device, priority=-5)
                               for _ in range(min(nch, self.S))] if nch > 0 else None)
         self.pre_stream = torch.cuda.Stream(device=device)
+        self.rec_stream = torch.cuda.Stream(device=device) if opt.split_project else None
         self.pre_chunks = opt.pre_chunks
         self.proj_chunks = opt.proj_chunks
         # optional hook(v, stream), called on view v's stream right before its backward:
@@ -266,10 +271,11 @@ class MultiViewPass:
             gts=None, project=None):
         """dL_dimgs: fixed per-view ∂L/∂C, or None with gts (per-view ground truth,
         requires enable_loss): then ∂L/∂C comes from the fidelity loss.
-        project(v0, v1): optional; issues the projection of views [v0, v1) on the
-        current stream.  The pass then projects in DASS_PROJ_CHUNKS chunks and each
-        view waits only for its own chunk, so later chunks project under the first
-        chunks' raster kernels."""
+        project(v0, v1, part): optional; issues the projection of views [v0, v1) on
+        the current stream (part: dass.DASS_PROJECT_KEYS / _RECORDS / _ALL).  The
+        pass then projects in options.proj_chunks chunks and each view waits only
+        for its own chunk; with options.split_project the records part of each chunk
+        runs on a side stream while the views sort."""
         torch = _torch()
         main = torch.cuda.current_stream()
         V = self.V
@@ -281,6 +287,8 @@ class MultiViewPass:
             pc = max(1, min(self.proj_chunks, V)) if project is not None else 1
         pbounds = [round(c * V / pc) for c in range(pc + 1)]
         ready = []   # per chunk: the event the chunk's views wait on
+        rec_ready = []   # per chunk (split projection): the records part is done
+        split = self.rec_stream is not None and project is not None and not self.batch_sort
         for c in range(pc):
             a, b = pbounds[c], pbounds[c + 1]
             if self.batch_sort:
@@ -290,10 +298,17 @@ class MultiViewPass:
                                          self.slots[0].capacity, self.bs_ids[a:b],
                                          self.bs_ranges[a:b], self.bs_pairs[a:b])
             elif project is not None:
-                project(a, b)
+                project(a, b, dass.DASS_PROJECT_KEYS if split else dass.DASS_PROJECT_ALL)
             e = torch.cuda.Event()
             e.record(main)
             ready.append(e)
+            if split:
+                self.rec_stream.wait_event(e)
+                with torch.cuda.stream(self.rec_stream):
+                    project(a, b, dass.DASS_PROJECT_RECORDS)
+                r = torch.cuda.Event()
+                r.record(self.rec_stream)
+                rec_ready.append(r)
         chunk_of = [max(c for c in range(pc) if pbounds[c] <= v) for v in range(V)]
         # preprocess in chunks: chunk c's views are chained to parameter gradients on a side
         # stream as soon as they are rasterised (HBM-bound work under the ALU-bound raster
@@ -324,6 +339,8 @@ class MultiViewPass:
             with torch.cuda.stream(st):
                 if self.sort_streams is None and not self.batch_sort:
                     ras.sort(cam, rec, num_pairs=self.num_pairs[v])
+                if split:
+                    st.wait_event(rec_ready[chunk_of[v]])
                 ras.render(cam, rec, bg=bg, tiles=self.tiles[v], ranges=vr, sorted_ids=vi)
                 if self.after_fwd is not None:
                     self.after_fwd(v, ras)
@@ -351,6 +368,8 @@ class MultiViewPass:
             main.wait_stream(s)
         for s in self.sort_streams or []:
             main.wait_stream(s)
+        if split:
+            main.wait_stream(self.rec_stream)
         if nchunk > 1:
             main.wait_stream(self.pre_stream)
         self._preprocess(scene, records, grads, keep, bounds[nchunk - 1], V)

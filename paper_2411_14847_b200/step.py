@@ -97,11 +97,11 @@ class ShiftStep:
                                   S.shifted.pos_opa, S.shifted.rot)
         rec, cams, sh = self.records, self.cams, (S.shifted if self.shift else S.base)
 
-        def project(v0, v1):
-            dass.dass_project_views(cams[v0:v1], self.deg, sh.pos_opa, sh.scale, sh.rot, sh.sh,
-                                    None, rec.xy_depth[v0:v1], rec.conic_opa[v0:v1],
-                                    rec.rgb[v0:v1], rec.box[v0:v1], rec.rows[v0:v1],
-                                    rec.tiles[v0:v1])
+        def project(v0, v1, part=dass.DASS_PROJECT_ALL):
+            dass.dass_project_views_part(part, cams[v0:v1], self.deg, sh.pos_opa, sh.scale,
+                                         sh.rot, sh.sh, None, rec.xy_depth[v0:v1],
+                                         rec.conic_opa[v0:v1], rec.rgb[v0:v1], rec.box[v0:v1],
+                                         rec.rows[v0:v1], rec.tiles[v0:v1])
         if self.mvp is not None:
             self._errmap_pos = sh.pos_opa     # the error map projects 𝒢_t (Alg. 1)
             self.mvp.uv_out = [None if s < 0 else g.uv[s] for s in self.split]

@@ -240,6 +240,41 @@ def test_project_views_equals_per_view():
             assert torch.equal(a, b)
 
 
+def test_project_views_part_equals_all():
+    """The split projection (keys on one stream, records on another while the
+    keys' consumer could run) gives dass_project_views' bytes; the keys part alone
+    already holds everything dass_bin_sort reads."""
+    cams = synth.n3dv_rig(width=200, height=150, num_views=5)
+    sc = synth.n3dv_scene(n=7001, seed=6, fx=cams[0].fx)
+    sc.pos_opa[::97, 3] = 0.002            # some Gaussians culled by opacity
+    ds = DeviceScene.from_host(sc, DEV)
+    keep = torch.from_numpy((np.arange(sc.n) % 5 != 0).astype(np.uint8)).to(DEV)
+    args = lambda r: (r.xy_depth, r.conic_opa, r.rgb, r.box, r.rows, r.tiles)
+    ref = ViewRecords(len(cams), sc.n, DEV)
+    dass.dass_project_views(cams, 3, ds.pos_opa, ds.scale, ds.rot, ds.sh, keep, *args(ref))
+    rec = ViewRecords(len(cams), sc.n, DEV)
+    for t in args(rec):
+        t.view(torch.uint8).fill_(0xA5)     # poison: every byte must be written
+    dass.dass_project_views_part(dass.DASS_PROJECT_KEYS, cams, 3, ds.pos_opa, ds.scale, ds.rot,
+                                 ds.sh, keep, *args(rec))
+    torch.cuda.synchronize()
+    assert torch.equal(rec.xy_depth[..., 2], ref.xy_depth[..., 2])
+    for a, b in zip((rec.box, rec.rows, rec.tiles), (ref.box, ref.rows, ref.tiles)):
+        assert torch.equal(a, b)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        dass.dass_project_views_part(dass.DASS_PROJECT_RECORDS, cams, 3, ds.pos_opa, ds.scale,
+                                     ds.rot, ds.sh, keep, *args(rec))
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    for a, b in zip(args(rec), args(ref)):
+        assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+    with pytest.raises(dass.DassError):
+        dass.dass_project_views_part(0, cams, 3, ds.pos_opa, ds.scale, ds.rot, ds.sh, keep,
+                                     *args(rec))
+
+
 def test_shift_parity():
     cams, sc = synth.c3(n=20000, num_views=1)
     mu, sigma = synth.shift_offsets(sc, seed=33)
