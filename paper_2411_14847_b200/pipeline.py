@@ -180,6 +180,9 @@ class PassOptions:
     split_project: with a projection callback, the projection's records part
       (fp64 records + colour, DASS_PROJECT_RECORDS) on a side stream under the
       views' sorts; the sorts wait only for the keys part, the forwards for both.
+    bwd_low_prio: every backward on a low-priority stream of its slot (the sorts and
+      forwards on high-priority ones), so pending forward blocks are scheduled before
+      backward blocks and no view's forward is left to the end of the step.
     stream_prio: the first half of the view streams at a higher priority."""
     sort_chains: int = 0
     batch_sort: bool = False
@@ -187,6 +190,7 @@ class PassOptions:
     pre_chunks: int = 2
     proj_chunks: int = 1
     split_project: bool = True
+    bwd_low_prio: bool = False
     stream_prio: bool = False
 
 
@@ -215,8 +219,11 @@ class MultiViewPass:
         # stream_prio: the streams of the first half of the views get the higher
         # priority, so those views finish first and their preprocess chunk overlaps the rest
         self.streams = [torch.cuda.Stream(device=device,
-                                          priority=-1 if opt.stream_prio and 2 * k < self.S else 0)
+                                          priority=-1 if (opt.bwd_low_prio or
+                                                          (opt.stream_prio and 2 * k < self.S)) else 0)
                         for k in range(self.S)]
+        self.bwd_streams = ([torch.cuda.Stream(device=device, priority=0) for _ in range(self.S)]
+                            if opt.bwd_low_prio else None)
         # bin_sort chains: with every view's sort on its own stream, the graph runs the
         # 20 latency-bound sorts in lockstep.  sort_chains > 0 runs them one after
         # another on that many high-priority streams instead, so view 0 rasterises
@@ -235,6 +242,10 @@ class MultiViewPass:
         # optional hook(v, raster_slot), called on view v's stream right after its
         # forward (e.g. the error map of error-guided densification)
         self.after_fwd = None
+        # optional int64[4V] (diagnostic, bench.py's in-step phase timing): view v's
+        # stream writes the GPU timer at 4v (sort start), 4v+1 (forward start),
+        # 4v+2 (backward start), 4v+3 (backward end)
+        self.stamps = None
         self.g2d = torch.empty(max(self.V, 1), n, 12, dtype=torch.float32, device=device)
         # (K_v, overflow_v) of every view's graph-mode sort, kept per view so a slot
         # reused by a later view does not overwrite an earlier view's overflow flag
@@ -320,12 +331,17 @@ class MultiViewPass:
         bounds = [round(c * V / nchunk) for c in range(nchunk + 1)]
         ends = {bounds[c + 1] - 1: c for c in range(nchunk - 1)}
         done = [None] * V
+        for b in self.bwd_streams or []:
+            b.wait_stream(main)      # joins the capture before any cross-stream wait on it
         for v, cam in enumerate(self.cams):
             k = v % self.S
             ras, st = self.slots[k], self.streams[k]
+            bst = self.bwd_streams[k] if self.bwd_streams else st
             rec = records.view(v)
             xy, co, rgb, box, rows, tiles = rec
             st.wait_event(ready[chunk_of[v]])
+            if bst is not st:
+                st.wait_stream(bst)  # the slot's previous backward is done with its buffers
             if self.batch_sort:
                 vr, vi = self.bs_ranges[v], self.bs_ids[v]
             else:
@@ -336,11 +352,15 @@ class MultiViewPass:
                 with torch.cuda.stream(ss):
                     ras.sort(cam, rec, num_pairs=self.num_pairs[v])
                 st.wait_stream(ss)
+            stamp = ((lambda i, q=st: dass.dass_timestamp(self.stamps, 4 * v + i, q))
+                     if self.stamps is not None else (lambda i, q=None: None))
             with torch.cuda.stream(st):
+                stamp(0)
                 if self.sort_streams is None and not self.batch_sort:
                     ras.sort(cam, rec, num_pairs=self.num_pairs[v])
                 if split:
                     st.wait_event(rec_ready[chunk_of[v]])
+                stamp(1)
                 ras.render(cam, rec, bg=bg, tiles=self.tiles[v], ranges=vr, sorted_ids=vi)
                 if self.after_fwd is not None:
                     self.after_fwd(v, ras)
@@ -350,13 +370,18 @@ class MultiViewPass:
                                             self.losses[v], dL)
                 else:
                     dL = dL_dimgs[v]
+            if bst is not st:
+                bst.wait_stream(st)
+            with torch.cuda.stream(bst):
                 if self.before_bwd is not None:
-                    self.before_bwd(v, st)
+                    self.before_bwd(v, bst)
+                stamp(2, bst)
                 dass.dass_render_bwd_raster(cam, self.n, vr, vi, xy, co, rgb,
                                             box, bg, ras.T, ras.last, dL, self.g2d[v],
                                             ras.accept, ras.capacity, tiles=self.tiles[v])
+                stamp(3, bst)
                 done[v] = torch.cuda.Event()
-                done[v].record(st)
+                done[v].record(bst)
             if v in ends:
                 c = ends[v]
                 self.pre_stream.wait_stream(main)
@@ -364,7 +389,7 @@ class MultiViewPass:
                     self.pre_stream.wait_event(done[u])
                 with torch.cuda.stream(self.pre_stream):
                     self._preprocess(scene, records, grads, keep, bounds[c], bounds[c + 1])
-        for s in self.streams:
+        for s in self.streams + (self.bwd_streams or []):
             main.wait_stream(s)
         for s in self.sort_streams or []:
             main.wait_stream(s)

@@ -1,6 +1,7 @@
 """The pass's selectable schedules stay parity-green: the batched multi-view sort
-(PassOptions.batch_sort) and the chained sorts (PassOptions.sort_chains) inside
-the overlapped pass, against the oracle's per-view sums."""
+(PassOptions.batch_sort), the chained sorts (PassOptions.sort_chains), the
+low-priority backward streams and the one-stream projection inside the
+overlapped pass, against the oracle's per-view sums."""
 import numpy as np
 import pytest
 
@@ -14,15 +15,19 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # pragma: no cover - CPU box
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
+from paper_2411_14847_b200 import dass  # noqa: E402
 from paper_2411_14847_b200.pipeline import (DeviceScene, Grads, MultiViewPass,  # noqa: E402
-                                            PassOptions, ViewRecords, project_all)
+                                            PassOptions, ViewRecords)
 
 DEV = "cuda"
 
 
 @pytest.mark.parametrize("opts", [PassOptions(batch_sort=True, sort_batch_chunks=2),
-                                  PassOptions(sort_chains=2), PassOptions(pre_chunks=1, proj_chunks=1)],
-                         ids=["batch_sort", "sort_chains", "single_preprocess"])
+                                  PassOptions(sort_chains=2), PassOptions(pre_chunks=1, proj_chunks=1),
+                                  PassOptions(bwd_low_prio=True), PassOptions(split_project=False),
+                                  PassOptions(proj_chunks=2, bwd_low_prio=True)],
+                         ids=["batch_sort", "sort_chains", "single_preprocess", "bwd_low_prio",
+                              "unsplit_projection", "chunked_split_projection"])
 def test_pass_options_parity(opts):
     cams = synth.n3dv_rig(width=160, height=120, num_views=4)
     sc = synth.n3dv_scene(n=5000, seed=57, degree=2, fx=cams[0].fx)
@@ -31,8 +36,13 @@ def test_pass_options_parity(opts):
     dLs = np.stack([synth.grad_image(c, 700 + v) for v, c in enumerate(cams)])
     g = Grads.zeros(sc.n, 2, DEV)
     mv = MultiViewPass(cams, sc.n, 1 << 20, DEV, streams=2, options=opts)
-    project_all(cams, ds, rec)
-    mv.run(ds, rec, torch.from_numpy(dLs).to(DEV), g)
+
+    def project(v0, v1, part=dass.DASS_PROJECT_ALL):   # the step's callback (step.py)
+        dass.dass_project_views_part(part, cams[v0:v1], sc.sh_degree, ds.pos_opa, ds.scale, ds.rot,
+                                     ds.sh, None, rec.xy_depth[v0:v1], rec.conic_opa[v0:v1],
+                                     rec.rgb[v0:v1], rec.box[v0:v1], rec.rows[v0:v1],
+                                     rec.tiles[v0:v1])
+    mv.run(ds, rec, torch.from_numpy(dLs).to(DEV), g, project=project)
     torch.cuda.synchronize()
     assert mv.overflowed_views() == []
     keys = ("g_pos_opa", "g_scale", "g_rot", "k_pos_opa", "k_scale", "k_rot", "t_pos_opa",
