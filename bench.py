@@ -102,6 +102,7 @@ def parse():
     p.add_argument("--pre-chunks", type=int, default=2, help="A/B: PassOptions.pre_chunks")
     p.add_argument("--proj-chunks", type=int, default=1, help="A/B: PassOptions.proj_chunks")
     p.add_argument("--bwd-low-prio", action="store_true", help="A/B: PassOptions.bwd_low_prio")
+    p.add_argument("--phase-major", action="store_true", help="A/B: PassOptions.phase_major")
     p.add_argument("--no-split-project", action="store_true",
                    help="A/B: PassOptions.split_project=False (keys and records on one stream)")
     p.add_argument("--lean", action="store_true",
@@ -336,7 +337,8 @@ def run_ours(args):
     opts = PassOptions(sort_chains=args.sort_chains, batch_sort=args.batch_sort,
                        sort_batch_chunks=args.sort_batch_chunks,
                        pre_chunks=args.pre_chunks, proj_chunks=args.proj_chunks,
-                       split_project=not args.no_split_project, bwd_low_prio=args.bwd_low_prio)
+                       split_project=not args.no_split_project, bwd_low_prio=args.bwd_low_prio,
+                       phase_major=args.phase_major)
     stepper = ShiftStep(my_cams, n, deg, args.capacity, dev, streams=args.streams,
                         tiles=plan.tiles, split=plan.split, num_split=plan.num_split,
                         shift=with_shift, options=opts)
@@ -479,6 +481,7 @@ def run_ours(args):
                 collective()
         mvp.stamps = None
         span = {"sort": [], "render_fwd": [], "render_bwd_raster": []}
+        ends = []
         for _ in range(3):
             g2.replay()
             if distd and not coll_in_graph["value"]:
@@ -488,8 +491,11 @@ def run_ours(args):
             span["sort"].append(t[:, 1].max() - t[:, 0].min())
             span["render_fwd"].append(t[:, 2].max() - t[:, 1].min())
             span["render_bwd_raster"].append(t[:, 3].max() - t[:, 2].min())
+            ends.append(t[:, 1:] - t[:, :1].min())
         del g2
         phases = {k: round(float(np.median(v)), 4) for k, v in span.items()}
+        # per view: (sort end, forward end, backward end) in ms from the first sort start
+        phases["per_view_ends_ms"] = np.round(np.median(np.stack(ends), 0), 3).tolist()
         barrier()
 
     # ---- the collective's share of the step: the same all_reduce
@@ -1109,6 +1115,7 @@ def in_step_view(key, phases, units, instr, peak_i, prof, launches, f_max, profi
     removes.  A lower bound: other kernels also run inside the span."""
     if not phases or not phases.get(key):
         return None
+    phases = dict(phases)
     ms = phases[key]
     rate = units * instr / (ms / 1e3) / 1e12
     out = {"phase_ms": ms, "achieved": round(rate, 3), "frac": round(rate / peak_i, 4),

@@ -183,6 +183,8 @@ class PassOptions:
     bwd_low_prio: every backward on a low-priority stream of its slot (the sorts and
       forwards on high-priority ones), so pending forward blocks are scheduled before
       backward blocks and no view's forward is left to the end of the step.
+    phase_major: with a stream per view, issue every view's sort, then every
+      forward, then every backward (instead of view by view).
     stream_prio: the first half of the view streams at a higher priority."""
     sort_chains: int = 0
     batch_sort: bool = False
@@ -191,6 +193,7 @@ class PassOptions:
     proj_chunks: int = 1
     split_project: bool = True
     bwd_low_prio: bool = False
+    phase_major: bool = False
     stream_prio: bool = False
 
 
@@ -333,53 +336,69 @@ class MultiViewPass:
         done = [None] * V
         for b in self.bwd_streams or []:
             b.wait_stream(main)      # joins the capture before any cross-stream wait on it
-        for v, cam in enumerate(self.cams):
+        vr, vi, dLv = {}, {}, {}
+
+        def slot(v):
             k = v % self.S
-            ras, st = self.slots[k], self.streams[k]
-            bst = self.bwd_streams[k] if self.bwd_streams else st
-            rec = records.view(v)
-            xy, co, rgb, box, rows, tiles = rec
+            return k, self.slots[k], self.streams[k], (self.bwd_streams[k] if self.bwd_streams
+                                                       else self.streams[k])
+
+        def stamp(v, i, q):
+            if self.stamps is not None:
+                dass.dass_timestamp(self.stamps, 4 * v + i, q)
+
+        def part_sort(v):
+            k, ras, st, bst = slot(v)
+            cam, rec = self.cams[v], records.view(v)
             st.wait_event(ready[chunk_of[v]])
             if bst is not st:
                 st.wait_stream(bst)  # the slot's previous backward is done with its buffers
             if self.batch_sort:
-                vr, vi = self.bs_ranges[v], self.bs_ids[v]
+                vr[v], vi[v] = self.bs_ranges[v], self.bs_ids[v]
             else:
-                vr, vi = ras.ranges, ras.sorted_ids
+                vr[v], vi[v] = ras.ranges, ras.sorted_ids
             if self.sort_streams is not None and not self.batch_sort:
                 ss = self.sort_streams[v % len(self.sort_streams)]
                 ss.wait_stream(st)    # projected, and the slot's previous view is done
                 with torch.cuda.stream(ss):
                     ras.sort(cam, rec, num_pairs=self.num_pairs[v])
                 st.wait_stream(ss)
-            stamp = ((lambda i, q=st: dass.dass_timestamp(self.stamps, 4 * v + i, q))
-                     if self.stamps is not None else (lambda i, q=None: None))
             with torch.cuda.stream(st):
-                stamp(0)
+                stamp(v, 0, st)
                 if self.sort_streams is None and not self.batch_sort:
                     ras.sort(cam, rec, num_pairs=self.num_pairs[v])
+
+        def part_fwd(v):
+            k, ras, st, bst = slot(v)
+            cam, rec = self.cams[v], records.view(v)
+            with torch.cuda.stream(st):
                 if split:
                     st.wait_event(rec_ready[chunk_of[v]])
-                stamp(1)
-                ras.render(cam, rec, bg=bg, tiles=self.tiles[v], ranges=vr, sorted_ids=vi)
+                stamp(v, 1, st)
+                ras.render(cam, rec, bg=bg, tiles=self.tiles[v], ranges=vr[v], sorted_ids=vi[v])
                 if self.after_fwd is not None:
                     self.after_fwd(v, ras)
                 if gts is not None:
-                    dL = self.loss_dL[k]
+                    dLv[v] = self.loss_dL[k]
                     dass.dass_fidelity_loss(ras.img, gts[v], self.lam, self.loss_ws[k],
-                                            self.losses[v], dL)
+                                            self.losses[v], dLv[v])
                 else:
-                    dL = dL_dimgs[v]
+                    dLv[v] = dL_dimgs[v]
+
+        def part_bwd(v):
+            k, ras, st, bst = slot(v)
+            cam = self.cams[v]
+            xy, co, rgb, box, rows, tiles = records.view(v)
             if bst is not st:
                 bst.wait_stream(st)
             with torch.cuda.stream(bst):
                 if self.before_bwd is not None:
                     self.before_bwd(v, bst)
-                stamp(2, bst)
-                dass.dass_render_bwd_raster(cam, self.n, vr, vi, xy, co, rgb,
-                                            box, bg, ras.T, ras.last, dL, self.g2d[v],
+                stamp(v, 2, bst)
+                dass.dass_render_bwd_raster(cam, self.n, vr[v], vi[v], xy, co, rgb,
+                                            box, bg, ras.T, ras.last, dLv[v], self.g2d[v],
                                             ras.accept, ras.capacity, tiles=self.tiles[v])
-                stamp(3, bst)
+                stamp(v, 3, bst)
                 done[v] = torch.cuda.Event()
                 done[v].record(bst)
             if v in ends:
@@ -389,6 +408,18 @@ class MultiViewPass:
                     self.pre_stream.wait_event(done[u])
                 with torch.cuda.stream(self.pre_stream):
                     self._preprocess(scene, records, grads, keep, bounds[c], bounds[c + 1])
+
+        if self.options.phase_major and self.S >= V:
+            # every sort, then every forward, then every backward issued (same dependencies;
+            # only the order the graph's nodes are created in)
+            for part in (part_sort, part_fwd, part_bwd):
+                for v in range(V):
+                    part(v)
+        else:
+            for v in range(V):
+                part_sort(v)
+                part_fwd(v)
+                part_bwd(v)
         for s in self.streams + (self.bwd_streams or []):
             main.wait_stream(s)
         for s in self.sort_streams or []:
