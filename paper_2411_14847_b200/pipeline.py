@@ -184,7 +184,8 @@ class PassOptions:
       forwards on high-priority ones), so pending forward blocks are scheduled before
       backward blocks and no view's forward is left to the end of the step.
     phase_major: with a stream per view, issue every view's sort, then every
-      forward, then every backward (instead of view by view).
+      forward, then every backward (instead of view by view); with fwd_join, every
+      backward also waits for every forward.
     stream_prio: the first half of the view streams at a higher priority."""
     sort_chains: int = 0
     batch_sort: bool = False
@@ -194,6 +195,7 @@ class PassOptions:
     split_project: bool = True
     bwd_low_prio: bool = False
     phase_major: bool = False
+    fwd_join: bool = False
     stream_prio: bool = False
 
 
@@ -412,9 +414,24 @@ class MultiViewPass:
         if self.options.phase_major and self.S >= V:
             # every sort, then every forward, then every backward issued (same dependencies;
             # only the order the graph's nodes are created in)
-            for part in (part_sort, part_fwd, part_bwd):
+            for v in range(V):
+                part_sort(v)
+            for v in range(V):
+                part_fwd(v)
+            if self.options.fwd_join:
+                # no backward starts before every forward is done: the hardware cannot leave
+                # one view's forward to run under the others' backward kernels
+                fe = []
                 for v in range(V):
-                    part(v)
+                    e = torch.cuda.Event()
+                    e.record(slot(v)[2])
+                    fe.append(e)
+                for v in range(V):
+                    q = slot(v)[3]
+                    for e in fe:
+                        q.wait_event(e)
+            for v in range(V):
+                part_bwd(v)
         else:
             for v in range(V):
                 part_sort(v)

@@ -26,7 +26,7 @@ DEV = "cuda"
                                   PassOptions(sort_chains=2), PassOptions(pre_chunks=1, proj_chunks=1),
                                   PassOptions(bwd_low_prio=True), PassOptions(split_project=False),
                                   PassOptions(proj_chunks=2, bwd_low_prio=True),
-                                  PassOptions(phase_major=True)],
+                                  PassOptions(phase_major=True, fwd_join=True)],
                          ids=["batch_sort", "sort_chains", "single_preprocess", "bwd_low_prio",
                               "unsplit_projection", "chunked_split_projection", "phase_major"])
 def test_pass_options_parity(opts):
