@@ -906,12 +906,46 @@ struct PreArgs {
   uint32_t uv_count;
 };
 
+// Per-thread asynchronous copies global → shared (LDGSTS): the view loop below
+// keeps the next PRE_STAGES − 1 views' records in flight while it computes one,
+// without holding registers for them.  Each thread copies and reads back only
+// its own Gaussian's slots, so no block barrier is needed.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+constexpr int PRE_STAGES = 3;
+
+// One view's records of the block's Gaussians, structure-of-arrays (conflict-free
+// 16-byte shared loads); PART 2 reads only box, m1, m2 and the clamp bits.
+template <int PART, int NT>
+struct PreStage {
+  uint2 bx[NT];
+  float rgbw[NT];
+  float4 m1[NT], m2[NT];
+  float4 m0[PART == 1 ? NT : 1], co[PART == 1 ? NT : 1];
+};
+
 // PART 1: geometry (p, s, q, o, ∇p̄ and the SH direction term), fp64 chain.
 // PART 2: SH coefficient gradients (fp32, 3(d+1)² register accumulators).
 // Split so neither part spills.
 template <int DEG, int PART>
 __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB : 2) preprocess_views_kernel(
     const __grid_constant__ PreArgs a) {
+  constexpr int NT = PART == 1 ? 128 : 256;
+  __shared__ PreStage<PART, NT> stg[PRE_STAGES];
   // The per-Gaussian chain is evaluated in fp64: the kernel is HBM-bound, so
   // the wider arithmetic is free, and it removes the chain's own rounding
   // (conic → Σ' → Σ → R(q), J(t) with its clamp) from the gradient error
@@ -920,6 +954,26 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   const int n = a.n;
+  const int tid = threadIdx.x;
+  // issue view u's copies into stage u % PRE_STAGES (an empty group past the last
+  // view keeps the group count uniform for cp.async.wait_group)
+  auto prefetch = [&](int u) {
+    if (u < a.num_views) {
+      PreStage<PART, NT>& S = stg[u % PRE_STAGES];
+      const size_t o = (size_t)u * n + i;
+      cp_async8(&S.bx[tid], a.box + o);
+      cp_async16(&S.m1[tid], a.g2d + 3 * o + 1);
+      cp_async16(&S.m2[tid], a.g2d + 3 * o + 2);
+      cp_async4(&S.rgbw[tid], &a.rgb[o].w);
+      if (PART == 1) {
+        cp_async16(&S.m0[tid], a.g2d + 3 * o);
+        cp_async16(&S.co[tid], a.conic_opa + o);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int u = 0; u < PRE_STAGES - 1; ++u) prefetch(u);
   using L = SHLayout<DEG>;
   const bool kp = a.keep == nullptr || a.keep[i] != 0;
   const float4 po = a.pos_opa[i];
@@ -952,14 +1006,15 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
   float gstat = 0.f;
   uint32_t nvis = 0, ncnt = 0;
   for (int v = 0; v < a.num_views; ++v) {
-    const size_t o = (size_t)v * n + i;
-    // every load of this view issued before the visibility branch: one memory
-    // latency per view instead of two in series (a culled view's loads are wasted)
-    const uint2 bx = a.box[o];
-    const float4 m1 = a.g2d[3 * o + 1], m2 = a.g2d[3 * o + 2];
-    const float rgbw = a.rgb[o].w;
-    const float4 m0 = PART == 1 ? a.g2d[3 * o] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 co = PART == 1 ? a.conic_opa[o] : make_float4(0.f, 0.f, 0.f, 0.f);
+    // view v's copies have landed; read them, then refill the stage view v − 1 used
+    cp_async_wait<PRE_STAGES - 2>();
+    const PreStage<PART, NT>& S = stg[v % PRE_STAGES];
+    const uint2 bx = S.bx[tid];
+    const float4 m1 = S.m1[tid], m2 = S.m2[tid];
+    const float rgbw = S.rgbw[tid];
+    const float4 m0 = PART == 1 ? S.m0[tid] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 co = PART == 1 ? S.co[tid] : make_float4(0.f, 0.f, 0.f, 0.f);
+    prefetch(v + PRE_STAGES - 1);
     if ((bx.x & 0xFFFFu) > (bx.x >> 16)) continue;  // culled in this view
     const CamParams& cam = a.cam[v];
     ++nvis;

@@ -6,7 +6,7 @@ for v in A B A B A B; do
   timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ab.json 2>/dev/null
   python -c "
 import json; d=json.load(open('gpurun_out/ab.json')); o=d['ops_ms_per_step_rank0']
-print('$v', d['ms_per_step'], 'fwd', o['render_fwd'], 'bwd', o['render_bwd_raster'], 'sort', o['bin_sort'], 'proj', o['project_views'])"
+print('$v', d['ms_per_step'], 'fwd', o['render_fwd'], 'bwd', o['render_bwd_raster'], 'sort', o['bin_sort'], 'proj', o['project_views'], 'pre', o['render_bwd_preprocess_views'])"
 done
 cp tools/ab/libdass_B.so paper_2411_14847_b200/libdass.so
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_step.py -q -x -m gpu 2>&1 | tail -1
