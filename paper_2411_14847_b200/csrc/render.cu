@@ -24,7 +24,7 @@
 #include "sh.cuh"
 
 #ifndef PRE1_MINB
-#define PRE1_MINB 4   // preprocess PART 1: 128 registers (4 blocks/SM) measured best (3: 0.63 ms, 4: 0.59, 5: 0.66)
+#define PRE1_MINB 3   // preprocess PART 1: 3 blocks/SM (166 registers, no spill) with the cp.async view pipeline: 0.352 ms per 20 views against 0.397 at 4 blocks (128 registers, spills)
 #endif
 
 namespace dass {
