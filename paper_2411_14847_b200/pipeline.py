@@ -186,6 +186,9 @@ class PassOptions:
     phase_major: with a stream per view, issue every view's sort, then every
       forward, then every backward (instead of view by view); with fwd_join, every
       backward also waits for every forward.
+    bwd_waves: the backward in that many waves of views, each after the previous
+      wave's backward, with one preprocess chunk per wave (its views' parameter
+      gradients) running under the next wave.
     stream_prio: the first half of the view streams at a higher priority."""
     sort_chains: int = 0
     batch_sort: bool = False
@@ -196,6 +199,7 @@ class PassOptions:
     bwd_low_prio: bool = False
     phase_major: bool = False
     fwd_join: bool = False
+    bwd_waves: int = 1
     stream_prio: bool = False
 
 
@@ -332,8 +336,15 @@ class MultiViewPass:
         # Chunks run in order on ONE stream: each += into the same gradient buffers.
         # (measured: with one stream per view the raster kernels already fill the GPU
         # and chunking the preprocess or the projection only adds launches, +0.3-1.8%)
-        nchunk = max(1, min(self.pre_chunks, V // self.S)) if V >= 2 * self.S else 1
+        waves = max(1, min(self.options.bwd_waves, V))
+        if waves > 1:
+            # the backward in waves (each wave's views wait for the previous wave's
+            # backward), one preprocess chunk per wave under the next wave's raster
+            nchunk = waves
+        else:
+            nchunk = max(1, min(self.pre_chunks, V // self.S)) if V >= 2 * self.S else 1
         bounds = [round(c * V / nchunk) for c in range(nchunk + 1)]
+        wave_of = [max(c for c in range(nchunk) if bounds[c] <= v) for v in range(V)]
         ends = {bounds[c + 1] - 1: c for c in range(nchunk - 1)}
         done = [None] * V
         for b in self.bwd_streams or []:
@@ -393,6 +404,9 @@ class MultiViewPass:
             xy, co, rgb, box, rows, tiles = records.view(v)
             if bst is not st:
                 bst.wait_stream(st)
+            if waves > 1 and wave_of[v] > 0:
+                for u in range(bounds[wave_of[v] - 1], bounds[wave_of[v]]):
+                    bst.wait_event(done[u])
             with torch.cuda.stream(bst):
                 if self.before_bwd is not None:
                     self.before_bwd(v, bst)

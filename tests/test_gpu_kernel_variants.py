@@ -26,9 +26,11 @@ DEV = "cuda"
                                   PassOptions(sort_chains=2), PassOptions(pre_chunks=1, proj_chunks=1),
                                   PassOptions(bwd_low_prio=True), PassOptions(split_project=False),
                                   PassOptions(proj_chunks=2, bwd_low_prio=True),
-                                  PassOptions(phase_major=True, fwd_join=True)],
+                                  PassOptions(phase_major=True, fwd_join=True),
+                                  PassOptions(bwd_waves=2)],
                          ids=["batch_sort", "sort_chains", "single_preprocess", "bwd_low_prio",
-                              "unsplit_projection", "chunked_split_projection", "phase_major"])
+                              "unsplit_projection", "chunked_split_projection", "phase_major",
+                              "bwd_waves"])
 def test_pass_options_parity(opts):
     cams = synth.n3dv_rig(width=160, height=120, num_views=4)
     sc = synth.n3dv_scene(n=5000, seed=57, degree=2, fx=cams[0].fx)
@@ -36,7 +38,7 @@ def test_pass_options_parity(opts):
     rec = ViewRecords(len(cams), sc.n, DEV)
     dLs = np.stack([synth.grad_image(c, 700 + v) for v, c in enumerate(cams)])
     g = Grads.zeros(sc.n, 2, DEV)
-    mv = MultiViewPass(cams, sc.n, 1 << 20, DEV, streams=len(cams) if opts.phase_major else 2,
+    mv = MultiViewPass(cams, sc.n, 1 << 20, DEV, streams=len(cams) if opts.phase_major or opts.bwd_waves > 1 else 2,
                        options=opts)
 
     def project(v0, v1, part=dass.DASS_PROJECT_ALL):   # the step's callback (step.py)
