@@ -186,6 +186,8 @@ class PassOptions:
     phase_major: with a stream per view, issue every view's sort, then every
       forward, then every backward (instead of view by view); with fwd_join, every
       backward also waits for every forward.
+    sort_join: with a stream per view, every forward waits for every view's sort
+      (issued phase-major).
     bwd_waves: the backward in that many waves of views, each after the previous
       wave's backward, with one preprocess chunk per wave (its views' parameter
       gradients) running under the next wave.
@@ -199,6 +201,7 @@ class PassOptions:
     bwd_low_prio: bool = False
     phase_major: bool = False
     fwd_join: bool = False
+    sort_join: bool = False
     bwd_waves: int = 1
     stream_prio: bool = False
 
@@ -425,11 +428,22 @@ class MultiViewPass:
                 with torch.cuda.stream(self.pre_stream):
                     self._preprocess(scene, records, grads, keep, bounds[c], bounds[c + 1])
 
-        if self.options.phase_major and self.S >= V:
+        if (self.options.phase_major or self.options.sort_join) and self.S >= V:
             # every sort, then every forward, then every backward issued (same dependencies;
             # only the order the graph's nodes are created in)
             for v in range(V):
                 part_sort(v)
+            if self.options.sort_join:
+                # no forward starts before every view's sort is done: a late sort kernel
+                # would otherwise queue behind the other views' forward blocks
+                se = []
+                for v in range(V):
+                    e = torch.cuda.Event()
+                    e.record(slot(v)[2])
+                    se.append(e)
+                for v in range(V):
+                    for e in se:
+                        slot(v)[2].wait_event(e)
             for v in range(V):
                 part_fwd(v)
             if self.options.fwd_join:

@@ -555,3 +555,25 @@ def test_dense_tiles_sort_past_shared_memory():
     r = out["ranges"]
     assert (r[:, 1] - r[:, 0]).max() > 4096
     check_binsort(cam, out, gpu_projection(out["rec"]))
+
+
+@pytest.mark.parametrize("n,lo,hi", [(800, 513, 1024), (3000, 1025, 4096), (40000, 4097, 1 << 30)],
+                         ids=["medium_bucket", "large_bucket", "huge_bucket"])
+def test_bucket_classes_bit_exact(n, lo, hi):
+    """dass_bin_sort's bucket sort past the one-warp register sort of ≤ 512 keys:
+    buckets of 513-1024 (one warp, 32 keys per lane), 1025-4096 (one CTA, shared-
+    memory bitonic) and > 4096 (CTA radix sort through global memory), each next
+    to small buckets, with a planar slice of equal depth bits so the id order
+    inside a bucket is checked too (A03/A04)."""
+    cam = synth.tiny_camera(48, 48)
+    sc = synth.random_scene(n, cam, seed=78)
+    g = np.random.default_rng(78)
+    z = sc.pos_opa[:, 2]
+    sc.pos_opa[:, 0] = (g.uniform(-5, 5, sc.n) * z / cam.fx).astype(np.float32)
+    sc.pos_opa[:, 1] = (g.uniform(-5, 5, sc.n) * z / cam.fy).astype(np.float32)
+    sc.scale[:, :3] = (np.abs(sc.scale[:, :3]) * 0.3).astype(np.float32)
+    sc.pos_opa[: n // 4, 2] = 3.0
+    out = run_view(cam, sc, capacity=1 << 21)
+    c = out["ranges"][:, 1] - out["ranges"][:, 0]
+    assert lo <= c.max() <= hi
+    check_binsort(cam, out, gpu_projection(out["rec"]))
