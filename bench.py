@@ -101,11 +101,6 @@ def parse():
     p.add_argument("--sort-batch-chunks", type=int, default=4, help="A/B: PassOptions.sort_batch_chunks")
     p.add_argument("--pre-chunks", type=int, default=2, help="A/B: PassOptions.pre_chunks")
     p.add_argument("--proj-chunks", type=int, default=1, help="A/B: PassOptions.proj_chunks")
-    p.add_argument("--bwd-low-prio", action="store_true", help="A/B: PassOptions.bwd_low_prio")
-    p.add_argument("--phase-major", action="store_true", help="A/B: PassOptions.phase_major")
-    p.add_argument("--fwd-join", action="store_true", help="A/B: PassOptions.fwd_join")
-    p.add_argument("--bwd-waves", type=int, default=1, help="A/B: PassOptions.bwd_waves")
-    p.add_argument("--sort-join", action="store_true", help="A/B: PassOptions.sort_join")
     p.add_argument("--no-split-project", action="store_true",
                    help="A/B: PassOptions.split_project=False (keys and records on one stream)")
     p.add_argument("--lean", action="store_true",
@@ -340,9 +335,7 @@ def run_ours(args):
     opts = PassOptions(sort_chains=args.sort_chains, batch_sort=args.batch_sort,
                        sort_batch_chunks=args.sort_batch_chunks,
                        pre_chunks=args.pre_chunks, proj_chunks=args.proj_chunks,
-                       split_project=not args.no_split_project, bwd_low_prio=args.bwd_low_prio,
-                       phase_major=args.phase_major, fwd_join=args.fwd_join,
-                       bwd_waves=args.bwd_waves, sort_join=args.sort_join)
+                       split_project=not args.no_split_project)
     stepper = ShiftStep(my_cams, n, deg, args.capacity, dev, streams=args.streams,
                         tiles=plan.tiles, split=plan.split, num_split=plan.num_split,
                         shift=with_shift, options=opts)

@@ -180,17 +180,6 @@ class PassOptions:
     split_project: with a projection callback, the projection's records part
       (fp64 records + colour, DASS_PROJECT_RECORDS) on a side stream under the
       views' sorts; the sorts wait only for the keys part, the forwards for both.
-    bwd_low_prio: every backward on a low-priority stream of its slot (the sorts and
-      forwards on high-priority ones), so pending forward blocks are scheduled before
-      backward blocks and no view's forward is left to the end of the step.
-    phase_major: with a stream per view, issue every view's sort, then every
-      forward, then every backward (instead of view by view); with fwd_join, every
-      backward also waits for every forward.
-    sort_join: with a stream per view, every forward waits for every view's sort
-      (issued phase-major).
-    bwd_waves: the backward in that many waves of views, each after the previous
-      wave's backward, with one preprocess chunk per wave (its views' parameter
-      gradients) running under the next wave.
     stream_prio: the first half of the view streams at a higher priority."""
     sort_chains: int = 0
     batch_sort: bool = False
@@ -198,11 +187,6 @@ class PassOptions:
     pre_chunks: int = 2
     proj_chunks: int = 1
     split_project: bool = True
-    bwd_low_prio: bool = False
-    phase_major: bool = False
-    fwd_join: bool = False
-    sort_join: bool = False
-    bwd_waves: int = 1
     stream_prio: bool = False
 
 
@@ -231,11 +215,8 @@ class MultiViewPass:
         # stream_prio: the streams of the first half of the views get the higher
         # priority, so those views finish first and their preprocess chunk overlaps the rest
         self.streams = [torch.cuda.Stream(device=device,
-                                          priority=-1 if (opt.bwd_low_prio or
-                                                          (opt.stream_prio and 2 * k < self.S)) else 0)
+                                          priority=-1 if opt.stream_prio and 2 * k < self.S else 0)
                         for k in range(self.S)]
-        self.bwd_streams = ([torch.cuda.Stream(device=device, priority=0) for _ in range(self.S)]
-                            if opt.bwd_low_prio else None)
         # bin_sort chains: with every view's sort on its own stream, the graph runs the
         # 20 latency-bound sorts in lockstep.  sort_chains > 0 runs them one after
         # another on that many high-priority streams instead, so view 0 rasterises
@@ -339,36 +320,24 @@ class MultiViewPass:
         # Chunks run in order on ONE stream: each += into the same gradient buffers.
         # (measured: with one stream per view the raster kernels already fill the GPU
         # and chunking the preprocess or the projection only adds launches, +0.3-1.8%)
-        waves = max(1, min(self.options.bwd_waves, V))
-        if waves > 1:
-            # the backward in waves (each wave's views wait for the previous wave's
-            # backward), one preprocess chunk per wave under the next wave's raster
-            nchunk = waves
-        else:
-            nchunk = max(1, min(self.pre_chunks, V // self.S)) if V >= 2 * self.S else 1
+        nchunk = max(1, min(self.pre_chunks, V // self.S)) if V >= 2 * self.S else 1
         bounds = [round(c * V / nchunk) for c in range(nchunk + 1)]
-        wave_of = [max(c for c in range(nchunk) if bounds[c] <= v) for v in range(V)]
         ends = {bounds[c + 1] - 1: c for c in range(nchunk - 1)}
         done = [None] * V
-        for b in self.bwd_streams or []:
-            b.wait_stream(main)      # joins the capture before any cross-stream wait on it
         vr, vi, dLv = {}, {}, {}
 
         def slot(v):
             k = v % self.S
-            return k, self.slots[k], self.streams[k], (self.bwd_streams[k] if self.bwd_streams
-                                                       else self.streams[k])
+            return k, self.slots[k], self.streams[k]
 
         def stamp(v, i, q):
             if self.stamps is not None:
                 dass.dass_timestamp(self.stamps, 4 * v + i, q)
 
         def part_sort(v):
-            k, ras, st, bst = slot(v)
+            k, ras, st = slot(v)
             cam, rec = self.cams[v], records.view(v)
             st.wait_event(ready[chunk_of[v]])
-            if bst is not st:
-                st.wait_stream(bst)  # the slot's previous backward is done with its buffers
             if self.batch_sort:
                 vr[v], vi[v] = self.bs_ranges[v], self.bs_ids[v]
             else:
@@ -385,7 +354,7 @@ class MultiViewPass:
                     ras.sort(cam, rec, num_pairs=self.num_pairs[v])
 
         def part_fwd(v):
-            k, ras, st, bst = slot(v)
+            k, ras, st = slot(v)
             cam, rec = self.cams[v], records.view(v)
             with torch.cuda.stream(st):
                 if split:
@@ -402,24 +371,19 @@ class MultiViewPass:
                     dLv[v] = dL_dimgs[v]
 
         def part_bwd(v):
-            k, ras, st, bst = slot(v)
+            k, ras, st = slot(v)
             cam = self.cams[v]
             xy, co, rgb, box, rows, tiles = records.view(v)
-            if bst is not st:
-                bst.wait_stream(st)
-            if waves > 1 and wave_of[v] > 0:
-                for u in range(bounds[wave_of[v] - 1], bounds[wave_of[v]]):
-                    bst.wait_event(done[u])
-            with torch.cuda.stream(bst):
+            with torch.cuda.stream(st):
                 if self.before_bwd is not None:
-                    self.before_bwd(v, bst)
-                stamp(v, 2, bst)
+                    self.before_bwd(v, st)
+                stamp(v, 2, st)
                 dass.dass_render_bwd_raster(cam, self.n, vr[v], vi[v], xy, co, rgb,
                                             box, bg, ras.T, ras.last, dLv[v], self.g2d[v],
                                             ras.accept, ras.capacity, tiles=self.tiles[v])
-                stamp(v, 3, bst)
+                stamp(v, 3, st)
                 done[v] = torch.cuda.Event()
-                done[v].record(bst)
+                done[v].record(st)
             if v in ends:
                 c = ends[v]
                 self.pre_stream.wait_stream(main)
@@ -428,44 +392,11 @@ class MultiViewPass:
                 with torch.cuda.stream(self.pre_stream):
                     self._preprocess(scene, records, grads, keep, bounds[c], bounds[c + 1])
 
-        if (self.options.phase_major or self.options.sort_join) and self.S >= V:
-            # every sort, then every forward, then every backward issued (same dependencies;
-            # only the order the graph's nodes are created in)
-            for v in range(V):
-                part_sort(v)
-            if self.options.sort_join:
-                # no forward starts before every view's sort is done: a late sort kernel
-                # would otherwise queue behind the other views' forward blocks
-                se = []
-                for v in range(V):
-                    e = torch.cuda.Event()
-                    e.record(slot(v)[2])
-                    se.append(e)
-                for v in range(V):
-                    for e in se:
-                        slot(v)[2].wait_event(e)
-            for v in range(V):
-                part_fwd(v)
-            if self.options.fwd_join:
-                # no backward starts before every forward is done: the hardware cannot leave
-                # one view's forward to run under the others' backward kernels
-                fe = []
-                for v in range(V):
-                    e = torch.cuda.Event()
-                    e.record(slot(v)[2])
-                    fe.append(e)
-                for v in range(V):
-                    q = slot(v)[3]
-                    for e in fe:
-                        q.wait_event(e)
-            for v in range(V):
-                part_bwd(v)
-        else:
-            for v in range(V):
-                part_sort(v)
-                part_fwd(v)
-                part_bwd(v)
-        for s in self.streams + (self.bwd_streams or []):
+        for v in range(V):
+            part_sort(v)
+            part_fwd(v)
+            part_bwd(v)
+        for s in self.streams:
             main.wait_stream(s)
         for s in self.sort_streams or []:
             main.wait_stream(s)

@@ -1,7 +1,6 @@
 """The pass's selectable schedules stay parity-green: the batched multi-view sort
-(PassOptions.batch_sort), the chained sorts (PassOptions.sort_chains), the
-low-priority backward streams and the one-stream projection inside the
-overlapped pass, against the oracle's per-view sums."""
+(PassOptions.batch_sort), the chained sorts (PassOptions.sort_chains), and the
+one-stream and chunked projections inside the overlapped pass, against the oracle's per-view sums."""
 import numpy as np
 import pytest
 
@@ -24,13 +23,10 @@ DEV = "cuda"
 
 @pytest.mark.parametrize("opts", [PassOptions(batch_sort=True, sort_batch_chunks=2),
                                   PassOptions(sort_chains=2), PassOptions(pre_chunks=1, proj_chunks=1),
-                                  PassOptions(bwd_low_prio=True), PassOptions(split_project=False),
-                                  PassOptions(proj_chunks=2, bwd_low_prio=True),
-                                  PassOptions(phase_major=True, fwd_join=True),
-                                  PassOptions(bwd_waves=2)],
-                         ids=["batch_sort", "sort_chains", "single_preprocess", "bwd_low_prio",
-                              "unsplit_projection", "chunked_split_projection", "phase_major",
-                              "bwd_waves"])
+                                  PassOptions(split_project=False),
+                                  PassOptions(proj_chunks=2)],
+                         ids=["batch_sort", "sort_chains", "single_preprocess", "unsplit_projection",
+                              "chunked_split_projection"])
 def test_pass_options_parity(opts):
     cams = synth.n3dv_rig(width=160, height=120, num_views=4)
     sc = synth.n3dv_scene(n=5000, seed=57, degree=2, fx=cams[0].fx)
@@ -38,7 +34,7 @@ def test_pass_options_parity(opts):
     rec = ViewRecords(len(cams), sc.n, DEV)
     dLs = np.stack([synth.grad_image(c, 700 + v) for v, c in enumerate(cams)])
     g = Grads.zeros(sc.n, 2, DEV)
-    mv = MultiViewPass(cams, sc.n, 1 << 20, DEV, streams=len(cams) if opts.phase_major or opts.bwd_waves > 1 else 2,
+    mv = MultiViewPass(cams, sc.n, 1 << 20, DEV, streams=2,
                        options=opts)
 
     def project(v0, v1, part=dass.DASS_PROJECT_ALL):   # the step's callback (step.py)

@@ -558,13 +558,12 @@ def test_dense_tiles_sort_past_shared_memory():
 
 
 @pytest.mark.parametrize("n,lo,hi", [(800, 513, 1024), (3000, 1025, 4096), (40000, 4097, 1 << 30)],
-                         ids=["medium_bucket", "large_bucket", "huge_bucket"])
-def test_bucket_classes_bit_exact(n, lo, hi):
-    """dass_bin_sort's bucket sort past the one-warp register sort of ≤ 512 keys:
-    buckets of 513-1024 (one warp, 32 keys per lane), 1025-4096 (one CTA, shared-
-    memory bitonic) and > 4096 (CTA radix sort through global memory), each next
-    to small buckets, with a planar slice of equal depth bits so the id order
-    inside a bucket is checked too (A03/A04)."""
+                         ids=["list_800", "list_3000", "list_40000"])
+def test_long_tile_lists_bit_exact(n, lo, hi):
+    """Tile lists of ~800, ~3000 and ~40000 pairs next to short ones (one tile
+    holds most of the pairs: the onesweep blocks of 2048 keys end inside it), with
+    a planar slice of equal depth bits so the id order inside a tile is checked
+    too (A03/A04)."""
     cam = synth.tiny_camera(48, 48)
     sc = synth.random_scene(n, cam, seed=78)
     g = np.random.default_rng(78)
