@@ -99,7 +99,7 @@ def parse():
     p.add_argument("--sort-chains", type=int, default=0, help="A/B: pipeline.PassOptions.sort_chains")
     p.add_argument("--batch-sort", action="store_true", help="A/B: PassOptions.batch_sort")
     p.add_argument("--sort-batch-chunks", type=int, default=4, help="A/B: PassOptions.sort_batch_chunks")
-    p.add_argument("--pre-chunks", type=int, default=2, help="A/B: PassOptions.pre_chunks")
+    p.add_argument("--pre-chunks", type=int, default=1, help="A/B: PassOptions.pre_chunks")
     p.add_argument("--proj-chunks", type=int, default=1, help="A/B: PassOptions.proj_chunks")
     p.add_argument("--no-split-project", action="store_true",
                    help="A/B: PassOptions.split_project=False (keys and records on one stream)")
