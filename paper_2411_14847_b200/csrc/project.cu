@@ -61,20 +61,25 @@ struct KeyResult {
 // the mantissa) × 1.01 + 0.05.  Boxes of more than 8 tile rows or 255 tile
 // columns keep every box tile (rows = all ones).  Every op individually rounded
 // (the oracle's replica must get the same bits).  Returns the tile count.
+// Step 12: the threshold R2 from o (view-independent).
+__device__ __forceinline__ float footprint_r2(float o) {
+  const float xo = FM(255.0f, o);
+  const uint32_t bits = __float_as_uint(xo);
+  const int e = (int)(bits >> 23) - 127;
+  const float mf = __uint_as_float((bits & 0x007FFFFFu) | 0x3F800000u);
+  const float L = FA(FM((float)e, 0.693147182f), FS(mf, 1.0f));
+  return FA(FM(FM(2.0f, L), 1.01f), 0.05f);
+}
+
+// Step 13 for one view.
 __device__ __forceinline__ uint32_t footprint_rows(float ca, float cb, float cc, float det, float u,
-                                                   float v, float o, int x0, int x1, int y0, int y1,
+                                                   float v, float R2, int x0, int x1, int y0, int y1,
                                                    uint4& rows) {
   const int tx0 = x0 / 16, tx1 = x1 / 16, ty0 = y0 / 16, ty1 = y1 / 16;
   if (ty1 - ty0 + 1 > 8 || tx1 - tx0 + 1 > 255) {
     rows = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
     return (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
   }
-  const float xo = FM(255.0f, o);
-  const uint32_t bits = __float_as_uint(xo);
-  const int e = (int)(bits >> 23) - 127;
-  const float mf = __uint_as_float((bits & 0x007FFFFFu) | 0x3F800000u);
-  const float L = FA(FM((float)e, 0.693147182f), FS(mf, 1.0f));
-  const float R2 = FA(FM(FM(2.0f, L), 1.01f), 0.05f);
   const float sxa = __fsqrt_rn(FM(R2, ca));
   const float tq = __fsqrt_rn(FD(R2, ca));
   const float dyL = -FM(cb, tq), dyR = FM(cb, tq);
@@ -114,21 +119,27 @@ __device__ __forceinline__ uint32_t footprint_rows(float ca, float cb, float cc,
   return total;
 }
 
-// The KEY CHAIN of include/dass.h, steps 1-13.
-__device__ __forceinline__ KeyResult key_chain(const CamParams& c, float px, float py, float pz,
-                                               float o, float s0, float s1, float s2, float4 q) {
-  KeyResult k;
-  k.visible = false; k.z = 0.f; k.x0 = 1; k.x1 = 0; k.y0 = 1; k.y1 = 0;
-  k.tiles = 0; k.rows = make_uint4(0u, 0u, 0u, 0u);
-  const float* V = c.V;
-  float t[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-    t[a] = FA(FA(FA(FM(V[4 * a + 0], px), FM(V[4 * a + 1], py)), FM(V[4 * a + 2], pz)), V[4 * a + 3]);
-  if (!(t[2] > c.near_plane)) return k;
+// The view-independent part of the KEY CHAIN (steps 3-5 and 12): q̂, R(q̂) and
+// Σ = m mᵀ with m = R·diag(s), and R2.  Computed once per Gaussian by the keys
+// kernel; the per-view part below uses the same values in the same op order, so
+// the result is the chain of include/dass.h bit for bit.
+struct KeyPrep {
+  bool qok;        // nq > 0 and finite
+  float S[6];      // Σ00, Σ01, Σ02, Σ11, Σ12, Σ22
+  float R2;
+};
+
+__device__ __forceinline__ KeyPrep key_prep(float o, float s0, float s1, float s2, float4 q) {
+  KeyPrep kp;
+  kp.R2 = footprint_r2(o);
   const float nn = FA(FA(FA(FM(q.x, q.x), FM(q.y, q.y)), FM(q.z, q.z)), FM(q.w, q.w));
   const float nq = __fsqrt_rn(nn);
-  if (!(nq > 0.f) || !isfinite(nq)) return k;
+  kp.qok = (nq > 0.f) && isfinite(nq);
+  if (!kp.qok) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) kp.S[k] = 0.f;
+    return kp;
+  }
   const float w = FD(q.x, nq), x = FD(q.y, nq), y = FD(q.z, nq), z = FD(q.w, nq);
   const float xx = FM(x, x), yy = FM(y, y), zz = FM(z, z), xy = FM(x, y), xz = FM(x, z),
               yz = FM(y, z), wx = FM(w, x), wy = FM(w, y), wz = FM(w, z);
@@ -148,18 +159,31 @@ __device__ __forceinline__ KeyResult key_chain(const CamParams& c, float px, flo
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = 0; b < 3; ++b) m[a][b] = FM(R[a][b], s[b]);
-  float S[3][3];
+  int k = 0;
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
-    for (int b = a; b < 3; ++b) {
-      const float acc = FA(FA(FM(m[a][0], m[b][0]), FM(m[a][1], m[b][1])), FM(m[a][2], m[b][2]));
-      S[a][b] = acc;
-      S[b][a] = acc;
-    }
+    for (int b = a; b < 3; ++b)
+      kp.S[k++] = FA(FA(FM(m[a][0], m[b][0]), FM(m[a][1], m[b][1])), FM(m[a][2], m[b][2]));
+  return kp;
+}
+
+// The per-view part of the KEY CHAIN (steps 1-2, 6-11, 13).  lx, ly: step 6's
+// clamp limits of this camera (computed once per block, same ops).
+__device__ __forceinline__ KeyResult key_view(const CamParams& c, float lx, float ly, float px,
+                                              float py, float pz, float o, const KeyPrep& kp) {
+  KeyResult k;
+  k.visible = false; k.z = 0.f; k.x0 = 1; k.x1 = 0; k.y0 = 1; k.y1 = 0;
+  k.tiles = 0; k.rows = make_uint4(0u, 0u, 0u, 0u);
+  const float* V = c.V;
+  float t[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    t[a] = FA(FA(FA(FM(V[4 * a + 0], px), FM(V[4 * a + 1], py)), FM(V[4 * a + 2], pz)), V[4 * a + 3]);
+  if (!(t[2] > c.near_plane)) return k;
+  if (!kp.qok) return k;
+  const float S[3][3] = {{kp.S[0], kp.S[1], kp.S[2]}, {kp.S[1], kp.S[3], kp.S[4]}, {kp.S[2], kp.S[4], kp.S[5]}};
   const float Wf = (float)c.W, Hf = (float)c.H;
-  const float lx = FD(FM(1.3f, Wf), FM(2.0f, c.fx));
-  const float ly = FD(FM(1.3f, Hf), FM(2.0f, c.fy));
   const float xt = FM(fminf(lx, fmaxf(-lx, FD(t[0], t[2]))), t[2]);
   const float yt = FM(fminf(ly, fmaxf(-ly, FD(t[1], t[2]))), t[2]);
   const float tz2 = FM(t[2], t[2]);
@@ -199,7 +223,7 @@ __device__ __forceinline__ KeyResult key_chain(const CamParams& c, float px, flo
   k.visible = true;
   k.z = t[2];
   k.x0 = (int)fx0; k.x1 = (int)fx1; k.y0 = (int)fy0; k.y1 = (int)fy1;
-  k.tiles = footprint_rows(ca, cb, cc, det, u, v, o, k.x0, k.x1, k.y0, k.y1, k.rows);   // 12-13
+  k.tiles = footprint_rows(ca, cb, cc, det, u, v, kp.R2, k.x0, k.x1, k.y0, k.y1, k.rows);   // 12-13
   return k;
 }
 
@@ -278,6 +302,15 @@ __device__ __forceinline__ Records accurate_records(const CamParams& c, float4 p
 // The two write disjoint bytes, so the records may run on a side stream while the
 // views' sorts (which read xy_depth.z only) run — off the step's critical path.
 __global__ void __launch_bounds__(256) project_keys_kernel(const __grid_constant__ ProjectArgs a) {
+  // step 6's per-camera clamp limits, once per block (the same ops as the chain)
+  __shared__ float s_l[MAXV][2];
+  const int va = blockIdx.y * a.vpt, vb = min(a.num_views, va + a.vpt);
+  if ((int)threadIdx.x < vb - va) {
+    const CamParams& c = a.cam[va + threadIdx.x];
+    s_l[threadIdx.x][0] = __fdiv_rn(__fmul_rn(1.3f, (float)c.W), __fmul_rn(2.0f, c.fx));
+    s_l[threadIdx.x][1] = __fdiv_rn(__fmul_rn(1.3f, (float)c.H), __fmul_rn(2.0f, c.fy));
+  }
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   const float4 po = a.pos_opa[i];
@@ -286,12 +319,11 @@ __global__ void __launch_bounds__(256) project_keys_kernel(const __grid_constant
   const bool kept = a.keep == nullptr || a.keep[i] != 0;
   const float o_eff = kept ? po.w : 0.f;
   const float keepf = kept ? 1.f : 0.f;
-  const int va = blockIdx.y * a.vpt, vb = min(a.num_views, va + a.vpt);
+  const KeyPrep kp = key_prep(o_eff, sc.x * keepf, sc.y * keepf, sc.z * keepf, q);
   for (int v = va; v < vb; ++v) {
     const CamParams& c = a.cam[v];
     const size_t o = (size_t)(a.view_offset + v) * a.n + i;
-    const KeyResult k = key_chain(c, po.x, po.y, po.z, o_eff, sc.x * keepf, sc.y * keepf,
-                                  sc.z * keepf, q);
+    const KeyResult k = key_view(c, s_l[v - va][0], s_l[v - va][1], po.x, po.y, po.z, o_eff, kp);
     if (!k.visible) {
       a.xy_depth[o] = make_float4(0.f, 0.f, 0.f, 0.f);
       a.box[o] = make_uint2(1u, 1u);     // x0 = 1 > x1 = 0: the invisible sentinel
