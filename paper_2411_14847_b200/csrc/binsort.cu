@@ -315,36 +315,6 @@ __global__ void __launch_bounds__(256) tile_scan_kernel(int n, const uint64_t* _
 
 // Emit pairs (tile<<32 | id) in depth order; histogram their tile digits;
 // clear the pair-sort look-back status words for the blocks that will run.
-// The tile of a Gaussian's local pair index j (A50, include/dass.h KEY CHAIN
-// step 13): rows = 8 row spans of 16 bits (lo | hi << 8, relative to the box's
-// first tile column; lo > hi: no tile) or all ones = every tile of the box, in
-// (row, column) order; w = the box's width in tiles.
-__device__ __forceinline__ void footprint_tile(uint4 rows, uint32_t w, uint32_t j, uint32_t& dy,
-                                               uint32_t& dx) {
-  if ((rows.x & rows.y & rows.z & rows.w) == 0xFFFFFFFFu) {
-    dy = j / w;
-    dx = j - dy * w;
-    return;
-  }
-  const uint32_t wd[4] = {rows.x, rows.y, rows.z, rows.w};
-  dy = 0;
-  dx = 0;
-  uint32_t rem = j;
-  bool found = false;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t span = (wd[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
-    const uint32_t lo = span & 0xFFu, hi = span >> 8;
-    const uint32_t width = lo <= hi ? hi - lo + 1u : 0u;
-    if (!found && rem < width) {
-      dy = (uint32_t)k;
-      dx = lo + rem;
-      found = true;
-    }
-    if (!found) rem -= width;
-  }
-}
-
 __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __restrict__ dkeys,
                                                   const uint32_t* __restrict__ tiles,
                                                   const uint2* __restrict__ box,
@@ -365,74 +335,57 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
   const size_t words = (size_t)div_up((int)K, SORT_ITEMS) * RADIX;
   for (int p = 0; p < npass; ++p)
     for (size_t k = gid; k < words; k += gstride) pstatus[p * pstatus_stride + k] = 0u;
-  // Warp-cooperative emission: a warp owns 32 consecutive depth-ordered
-  // Gaussians, whose pairs are one contiguous run of pkeys (offsets is their
-  // exclusive scan), and writes that run with consecutive lanes (coalesced);
-  // lane j finds its Gaussian by a binary search over the warp's inclusive
-  // counts.  Histogram increments are aggregated per distinct tile.
-  const uint32_t lane = threadIdx.x & 31u;
-  const size_t wid = gid >> 5, nwarps = gstride >> 5;
-  for (size_t base = wid * 32; base < (size_t)n; base += nwarps * 32) {
-    const size_t r = base + lane;
-    uint32_t id = 0, cnt = 0, w = 1;
-    int tx0 = 0, ty0 = 0;
-    uint4 rw = make_uint4(0u, 0u, 0u, 0u);
-    if (r < (size_t)n) {
-      id = (uint32_t)dkeys[r];
-      cnt = tiles[id];
-      if (cnt) {
-        const uint2 b = box[id];
-        tx0 = (int)(b.x & 0xFFFFu) / TILE;
-        ty0 = (int)(b.y & 0xFFFFu) / TILE;
-        w = (uint32_t)((int)(b.x >> 16) / TILE - tx0 + 1);
-        rw = rowspans[id];
-      }
+  // One thread per depth-ordered Gaussian: its pairs are one contiguous run of
+  // pkeys (offsets = the exclusive scan of tiles_touched in depth order), written
+  // row by row — each footprint row is a run of consecutive tiles [lo, hi]
+  // (KEY CHAIN step 13), so no per-pair decoding.  Histogram: digit 0 per pair;
+  // the higher digits change at most once along a row's run (L ≤ 255 < 256), so
+  // they are counted per row in one or two increments.
+  for (size_t r = gid; r < (size_t)n; r += gstride) {
+    const uint32_t id = (uint32_t)dkeys[r];
+    if (!tiles[id]) continue;   // culled / empty footprint (sorted last: all-ones depth)
+    const uint2 b = box[id];
+    const int tx0 = (int)(b.x & 0xFFFFu) / TILE, tx1 = (int)(b.x >> 16) / TILE;
+    const int ty0 = (int)(b.y & 0xFFFFu) / TILE, ty1 = (int)(b.y >> 16) / TILE;
+    const uint4 rw = rowspans[id];
+    const bool full = (rw.x & rw.y & rw.z & rw.w) == 0xFFFFFFFFu;
+    uint32_t gidv = id, tbase = 0;
+    if (view_n > 0) {   // multi-view batch: Gaussian index v·N + i → (v·T + tile, i)
+      const uint32_t v = id / (uint32_t)view_n;
+      gidv = id - v * (uint32_t)view_n;
+      tbase = v * (uint32_t)view_tiles;
     }
-    uint32_t incl = cnt;   // inclusive scan of the counts over the warp
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= (uint32_t)d) incl += u;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total == 0) continue;
-    const uint32_t o0 = __shfl_sync(0xffffffffu, r < (size_t)n ? offsets[r] : 0u, 0);
-    for (uint32_t j0 = 0; j0 < total; j0 += 32) {
-      const uint32_t j = j0 + lane;
-      // owner: the first lane whose inclusive count exceeds j
-      uint32_t lo = 0;
-#pragma unroll
-      for (int st = 16; st > 0; st >>= 1) {
-        const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + st - 1);
-        if (v <= j) lo += st;
+    uint64_t* out = pkeys + offsets[r];
+    const int nrows = full ? ty1 - ty0 + 1 : 8;
+    for (int k = 0; k < nrows; ++k) {
+      uint32_t lo, hi;
+      if (full) {
+        lo = 0u;
+        hi = (uint32_t)(tx1 - tx0);
+      } else {
+        const uint32_t word = k < 2 ? rw.x : k < 4 ? rw.y : k < 6 ? rw.z : rw.w;
+        const uint32_t span = (word >> (16 * (k & 1))) & 0xFFFFu;
+        lo = span & 0xFFu;
+        hi = span >> 8;
+        if (lo > hi) continue;
       }
-      const uint32_t owner = lo < 32 ? lo : 31;
-      const uint32_t excl = __shfl_sync(0xffffffffu, incl - cnt, owner);
-      const uint32_t oid = __shfl_sync(0xffffffffu, id, owner);
-      const uint32_t ow = __shfl_sync(0xffffffffu, w, owner);
-      const int otx0 = __shfl_sync(0xffffffffu, tx0, owner);
-      const int oty0 = __shfl_sync(0xffffffffu, ty0, owner);
-      const uint4 orw = make_uint4(__shfl_sync(0xffffffffu, rw.x, owner), __shfl_sync(0xffffffffu, rw.y, owner),
-                                   __shfl_sync(0xffffffffu, rw.z, owner), __shfl_sync(0xffffffffu, rw.w, owner));
-      const bool act = j < total;
-      uint32_t tile = 0xFFFFFFFFu;
-      if (act) {
-        const uint32_t local = j - excl;
-        uint32_t dy, dx;
-        footprint_tile(orw, ow, local, dy, dx);
-        tile = (uint32_t)((oty0 + (int)dy) * tiles_x + otx0 + (int)dx);
-        uint32_t gid = oid;
-        if (view_n > 0) {   // multi-view batch: Gaussian index v·N + i → (v·T + tile, i)
-          const uint32_t v = oid / (uint32_t)view_n;
-          gid = oid - v * (uint32_t)view_n;
-          tile += v * (uint32_t)view_tiles;
+      const uint32_t t0 = tbase + (uint32_t)((ty0 + k) * tiles_x + tx0) + lo;
+      const uint32_t L = hi - lo + 1u;
+      for (uint32_t dx = 0; dx < L; ++dx) {
+        const uint32_t tile = t0 + dx;
+        *out++ = ((uint64_t)tile << 32) | gidv;
+        atomicAdd(&sh[0][tile & 255u], 1u);
+      }
+      const uint32_t t1 = t0 + L - 1u;
+      for (int p = 1; p < npass; ++p) {
+        const uint32_t da = t0 >> (8 * p), db = t1 >> (8 * p);
+        if (da == db) {
+          atomicAdd(&sh[p][da & 255u], L);
+        } else {   // one crossing: [t0, edge) and [edge, t1]
+          const uint32_t edge = db << (8 * p);
+          atomicAdd(&sh[p][da & 255u], edge - t0);
+          atomicAdd(&sh[p][db & 255u], t1 - edge + 1u);
         }
-        pkeys[o0 + j] = ((uint64_t)tile << 32) | gid;
-      }
-      const uint32_t peers = __match_any_sync(0xffffffffu, tile);
-      if (act && lane == (uint32_t)(__ffs(peers) - 1)) {
-        const uint32_t c = (uint32_t)__popc(peers);
-        for (int p = 0; p < npass; ++p) atomicAdd(&sh[p][(tile >> (8 * p)) & 255u], c);
       }
     }
   }
