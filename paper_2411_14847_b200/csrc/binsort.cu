@@ -491,7 +491,10 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   const int nblk_n = div_up(n, SORT_ITEMS);
   const size_t nblk_cap = (size_t)((capacity + SORT_ITEMS - 1) / SORT_ITEMS) + 1;
   const int grid_n = div_up(n, 256) < 148 * 8 ? div_up(n, 256) : 148 * 8;
-  presort_init_kernel<<<grid_n, 256, 0, s>>>(n, xy_depth, tiles, w.dkeysA, w.hist, w.dstatus,
+  // two blocks per SM: every block flushes its 4×256 shared histogram bins with global
+  // atomics onto the same 1024 words, so fewer, longer blocks contend less
+  const int grid_i = div_up(n, 256) < 148 * 2 ? div_up(n, 256) : 148 * 2;
+  presort_init_kernel<<<grid_i, 256, 0, s>>>(n, xy_depth, tiles, w.dkeysA, w.hist, w.dstatus,
                                              (size_t)4 * nblk_n * RADIX, w.scan_status, nblk_n);
   launch_counted();
   uint64_t* a = w.dkeysA;
