@@ -5,5 +5,5 @@ for v in A B C A B C A B C; do
   timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ab.json 2>/dev/null
   python -c "
 import json; d=json.load(open('gpurun_out/ab.json')); o=d['ops_ms_per_step_rank0']
-print('$v', d['ms_per_step'], 'fwd', o['render_fwd'], 'bwd', o['render_bwd_raster'], 'sort', o['bin_sort'], 'proj', o['project_views'], 'pre', o['render_bwd_preprocess_views'])"
+print('$v', d['ms_per_step'], 'fwd', o['render_fwd'], 'bwd', o['render_bwd_raster'], 'sort', o['bin_sort'], 'proj', o['project_views'], 'pre', o['render_bwd_preprocess_views'], 'phase', d['roofline']['in_step']['phases_ms']['sort'])"
 done
