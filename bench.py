@@ -479,8 +479,12 @@ def run_ours(args):
         mvp.stamps = None
         span = {"sort": [], "render_fwd": [], "render_bwd_raster": []}
         ends = []
+        reps = []
         for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             g2.replay()
+            e1.record()
             if distd and not coll_in_graph["value"]:
                 collective()
             torch.cuda.synchronize()
@@ -489,10 +493,12 @@ def run_ours(args):
             span["render_fwd"].append(t[:, 2].max() - t[:, 1].min())
             span["render_bwd_raster"].append(t[:, 3].max() - t[:, 2].min())
             ends.append(t[:, 1:] - t[:, :1].min())
+            reps.append(e0.elapsed_time(e1))
         del g2
         phases = {k: round(float(np.median(v)), 4) for k, v in span.items()}
         # per view: (sort end, forward end, backward end) in ms from the first sort start
         phases["per_view_ends_ms"] = np.round(np.median(np.stack(ends), 0), 3).tolist()
+        phases["stamped_step_ms"] = round(float(np.median(reps)), 4)   # the re-captured step, stamps included
         barrier()
 
     # ---- the collective's share of the step: the same all_reduce
