@@ -15,7 +15,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --lean"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > /dev/null 2>&1
 CMD2="python bench.py --views 2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-graph --streams 1 --lean"
-for k in render_fwd render_bwd onesweep project_keys project_records preprocess preprocess2 emit presort_init; do
+for k in render_fwd render_bwd onesweep project_keys project_records emit presort_init; do
   case $k in
     render_fwd) RX="render_fwd_tw";; render_bwd) RX="render_bwd_tw";; onesweep) RX="onesweep";;
     project_keys) RX="project_keys_kernel";; project_records) RX="project_records_kernel";;
@@ -28,3 +28,4 @@ done
 tail -2 gpurun_out/pytest_gpu_$TAG.log; tail -2 gpurun_out/smoke_$TAG.log
 python -c "
 import json;d=json.loads(open('gpurun_out/bench_c3_$TAG.json').read().strip().splitlines()[-1]);print(d['value'], d['ms_per_step'], d['e2e']['value'], d['clocks'])"
+bash tools/gpu_prof_pre.sh $TAG
