@@ -94,6 +94,13 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
                :: "l"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 
+__device__ __forceinline__ void red_add_f32(float* addr, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" :: "l"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_u32(uint32_t* addr, uint32_t v) {
+  asm volatile("red.global.add.u32 [%0], %1;" :: "l"(addr), "r"(v) : "memory");
+}
+
 __host__ __device__ __forceinline__ int div_up(int a, int b) { return (a + b - 1) / b; }
 
 // Kernel-side copy of dass_hashgrid (f2), passed by value (__grid_constant__).

@@ -1151,27 +1151,29 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
     for (int c0 = 0; c0 < 3; ++c0) gp[c0] += V[c0] * gt[0] + V[4 + c0] * gt[1] + V[8 + c0] * gt[2];
   }
   if (nvis == 0) return;
+  // The outputs are accumulated (+=) with fire-and-forget reductions instead of a
+  // load-add-store: one thread owns Gaussian i in a launch, so each element gets one
+  // add per launch, the same fp32 add as before, without waiting for the old value.
   if (PART == 2) {
     if (!a.g_sh) return;
 #pragma unroll
     for (int j = 0; j < L::K4; ++j) {
-      const size_t off = (size_t)j * n + i;
-      float4 gg = a.g_sh[off];
-      gg.x += gsh[4 * j]; gg.y += gsh[4 * j + 1];
-      if (4 * j + 2 < L::NF) gg.z += gsh[4 * j + 2];
-      if (4 * j + 3 < L::NF) gg.w += gsh[4 * j + 3];
-      a.g_sh[off] = gg;
+      float4* dst = a.g_sh + (size_t)j * n + i;
+      if (4 * j + 3 < L::NF) {
+        red_add_v4(dst, make_float4(gsh[4 * j], gsh[4 * j + 1], gsh[4 * j + 2], gsh[4 * j + 3]));
+      } else {
+        float* d = reinterpret_cast<float*>(dst);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (4 * j + e < L::NF) red_add_f32(d + e, gsh[4 * j + e]);
+      }
     }
     return;
   }
-  if (a.gradstat_sum) a.gradstat_sum[i] += gstat;
-  if (a.gradstat_cnt) a.gradstat_cnt[i] += ncnt;
-  if (a.g_pos_opa) {
-    float4 gpo = a.g_pos_opa[i];
-    gpo.x += (float)gp[0]; gpo.y += (float)gp[1]; gpo.z += (float)gp[2];
-    gpo.w += kp ? (float)go : 0.f;
-    a.g_pos_opa[i] = gpo;
-  }
+  if (a.gradstat_sum) red_add_f32(a.gradstat_sum + i, gstat);
+  if (a.gradstat_cnt) red_add_u32(a.gradstat_cnt + i, ncnt);
+  if (a.g_pos_opa)
+    red_add_v4(a.g_pos_opa + i, make_float4((float)gp[0], (float)gp[1], (float)gp[2], kp ? (float)go : 0.f));
   if (!a.g_scale && !a.g_rot) return;
   // Σ = R diag(s²) Rᵀ : dL/ds_k = 2 s_k (Rᵀ GΣ R)_kk ; dL/dR = 2 GΣ R diag(s²)
   F GR[3][3];
@@ -1185,10 +1187,11 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
 #pragma unroll
     for (int r0 = 0; r0 < 3; ++r0) GR[r0][k] = 2 * GSr[r0] * s[k] * s[k];
   }
-  if (a.g_scale) {
-    float4 g4 = a.g_scale[i];
-    if (kp) { g4.x += (float)gs[0]; g4.y += (float)gs[1]; g4.z += (float)gs[2]; }
-    a.g_scale[i] = g4;
+  if (a.g_scale && kp) {
+    float* d = reinterpret_cast<float*>(a.g_scale + i);
+    red_add_f32(d, (float)gs[0]);
+    red_add_f32(d + 1, (float)gs[1]);
+    red_add_f32(d + 2, (float)gs[2]);
   }
   if (a.g_rot) {
     F gq[4];
@@ -1201,12 +1204,8 @@ __global__ void __launch_bounds__(PART == 1 ? 128 : 256, PART == 1 ? PRE1_MINB :
     gq[3] = GR[0][0] * (-4 * z) + GR[0][1] * (-2 * w) + GR[0][2] * (2 * x) + GR[1][0] * (2 * w) +
             GR[1][1] * (-4 * z) + GR[1][2] * (2 * y) + GR[2][0] * (2 * x) + GR[2][1] * (2 * y);
     const F dot = w * gq[0] + x * gq[1] + y * gq[2] + z * gq[3];
-    float4 g4 = a.g_rot[i];
-    g4.x += (float)((gq[0] - w * dot) * qi);
-    g4.y += (float)((gq[1] - x * dot) * qi);
-    g4.z += (float)((gq[2] - y * dot) * qi);
-    g4.w += (float)((gq[3] - z * dot) * qi);
-    a.g_rot[i] = g4;
+    red_add_v4(a.g_rot + i, make_float4((float)((gq[0] - w * dot) * qi), (float)((gq[1] - x * dot) * qi),
+                                        (float)((gq[2] - y * dot) * qi), (float)((gq[3] - z * dot) * qi)));
   }
 }
 
