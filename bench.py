@@ -101,6 +101,8 @@ def parse():
     p.add_argument("--sort-batch-chunks", type=int, default=4, help="A/B: PassOptions.sort_batch_chunks")
     p.add_argument("--pre-chunks", type=int, default=1, help="A/B: PassOptions.pre_chunks")
     p.add_argument("--proj-chunks", type=int, default=1, help="A/B: PassOptions.proj_chunks")
+    p.add_argument("--no-split-preprocess", action="store_true",
+                   help="A/B: PassOptions.split_preprocess=False (both preprocess parts on one stream)")
     p.add_argument("--no-split-project", action="store_true",
                    help="A/B: PassOptions.split_project=False (keys and records on one stream)")
     p.add_argument("--lean", action="store_true",
@@ -335,7 +337,8 @@ def run_ours(args):
     opts = PassOptions(sort_chains=args.sort_chains, batch_sort=args.batch_sort,
                        sort_batch_chunks=args.sort_batch_chunks,
                        pre_chunks=args.pre_chunks, proj_chunks=args.proj_chunks,
-                       split_project=not args.no_split_project)
+                       split_project=not args.no_split_project,
+                       split_preprocess=not args.no_split_preprocess)
     stepper = ShiftStep(my_cams, n, deg, args.capacity, dev, streams=args.streams,
                         tiles=plan.tiles, split=plan.split, num_split=plan.num_split,
                         shift=with_shift, options=opts)

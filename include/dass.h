@@ -466,6 +466,27 @@ int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_vie
                                         float* g_sh, float* gradstat_sum,
                                         uint32_t* gradstat_cnt, float* const* uv_out,
                                         const uint8_t* uv_count, void* stream);
+
+/* dass_render_bwd_preprocess_views_part — dass_render_bwd_preprocess_views_uv in
+ * two parts that write disjoint outputs and may run on two streams:
+ *  DASS_PREPROCESS_GEOMETRY (1): ∂L/∂(p, o, s, q), the ∇p̄ statistic (or the
+ *    split views' uv blocks) and the visibility counts;
+ *  DASS_PREPROCESS_SH (2): ∂L/∂SH coefficients (g_sh);
+ *  DASS_PREPROCESS_ALL (3): both in order on `stream` (= the _uv call).
+ * Both parts only read the records and the 2-D moments.  INVALID_ARG as the
+ * _uv call, or part ∉ {1, 2, 3}. */
+#define DASS_PREPROCESS_GEOMETRY 1
+#define DASS_PREPROCESS_SH 2
+#define DASS_PREPROCESS_ALL 3
+int dass_render_bwd_preprocess_views_part(int32_t part, const dass_camera* cams, int32_t num_views,
+                                          int32_t n, int32_t sh_degree, const float* pos_opa,
+                                          const float* scale, const float* rot, const float* sh,
+                                          const uint8_t* keep_mask, const float* conic_opa,
+                                          const float* rgb, const uint32_t* box, const float* g2d,
+                                          float* g_pos_opa, float* g_scale, float* g_rot,
+                                          float* g_sh, float* gradstat_sum,
+                                          uint32_t* gradstat_cnt, float* const* uv_out,
+                                          const uint8_t* uv_count, void* stream);
 int dass_gradstat_from_uv(int32_t n, int32_t num_split, const float* uv, float* gradstat_sum,
                           void* stream);
 

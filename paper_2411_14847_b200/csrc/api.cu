@@ -447,15 +447,17 @@ int dass_render_bwd_raster(const dass_camera* cam, int32_t n, const uint32_t* ti
                                       accept_bytes, pair_capacity, g2d, stream);
 }
 
-int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_views, int32_t n,
-                                        int32_t sh_degree, const float* pos_opa,
-                                        const float* scale, const float* rot, const float* sh,
-                                        const uint8_t* keep_mask, const float* conic_opa,
-                                        const float* rgb, const uint32_t* box, const float* g2d,
-                                        float* g_pos_opa, float* g_scale, float* g_rot,
-                                        float* g_sh, float* gradstat_sum,
-                                        uint32_t* gradstat_cnt, float* const* uv_out,
-                                        const uint8_t* uv_count, void* stream) {
+int dass_render_bwd_preprocess_views_part(int32_t part, const dass_camera* cams, int32_t num_views,
+                                          int32_t n, int32_t sh_degree, const float* pos_opa,
+                                          const float* scale, const float* rot, const float* sh,
+                                          const uint8_t* keep_mask, const float* conic_opa,
+                                          const float* rgb, const uint32_t* box, const float* g2d,
+                                          float* g_pos_opa, float* g_scale, float* g_rot,
+                                          float* g_sh, float* gradstat_sum,
+                                          uint32_t* gradstat_cnt, float* const* uv_out,
+                                          const uint8_t* uv_count, void* stream) {
+  if (part < DASS_PREPROCESS_GEOMETRY || part > DASS_PREPROCESS_ALL)
+    return fail(DASS_ERR_INVALID_ARG, "dass_render_bwd_preprocess_views_part: part must be 1, 2 or 3%s");
   if (cams == nullptr) return fail(DASS_ERR_INVALID_ARG, "cams is null%s");
   if (num_views < 1 || num_views > 64) return fail(DASS_ERR_INVALID_ARG, "num_views must be in [1, 64]%s");
   for (int v = 0; v < num_views; ++v) {
@@ -482,8 +484,23 @@ int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_vie
                                              (float4*)g_rot, (float4*)g_sh, gradstat_sum,
                                              gradstat_cnt,
                                              reinterpret_cast<float2* const*>(uv_out), uv_count,
-                                             (cudaStream_t)stream),
+                                             part, (cudaStream_t)stream),
                      "dass_render_bwd_preprocess_views");
+}
+
+int dass_render_bwd_preprocess_views_uv(const dass_camera* cams, int32_t num_views, int32_t n,
+                                        int32_t sh_degree, const float* pos_opa,
+                                        const float* scale, const float* rot, const float* sh,
+                                        const uint8_t* keep_mask, const float* conic_opa,
+                                        const float* rgb, const uint32_t* box, const float* g2d,
+                                        float* g_pos_opa, float* g_scale, float* g_rot,
+                                        float* g_sh, float* gradstat_sum,
+                                        uint32_t* gradstat_cnt, float* const* uv_out,
+                                        const uint8_t* uv_count, void* stream) {
+  return dass_render_bwd_preprocess_views_part(DASS_PREPROCESS_ALL, cams, num_views, n, sh_degree,
+                                               pos_opa, scale, rot, sh, keep_mask, conic_opa, rgb,
+                                               box, g2d, g_pos_opa, g_scale, g_rot, g_sh,
+                                               gradstat_sum, gradstat_cnt, uv_out, uv_count, stream);
 }
 
 int dass_render_bwd_preprocess_views(const dass_camera* cams, int32_t num_views, int32_t n,

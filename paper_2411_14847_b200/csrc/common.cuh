@@ -163,7 +163,7 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
                                     const float4* g2d, float4* g_pos_opa, float4* g_scale,
                                     float4* g_rot, float4* g_sh, float* gradstat_sum,
                                     uint32_t* gradstat_cnt, float2* const* uv_out,
-                                    const uint8_t* uv_count, cudaStream_t s);
+                                    const uint8_t* uv_count, int part, cudaStream_t s);
 cudaError_t launch_gradstat_uv(int n, int S, const float2* uv, float* gsum, cudaStream_t s);
 size_t fidelity_loss_workspace(int W, int H);
 cudaError_t launch_fidelity_loss(int W, int H, const float* img, const float* gt, float lambda,

@@ -1315,7 +1315,7 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
                                     const float4* g2d, float4* g_pos_opa, float4* g_scale,
                                     float4* g_rot, float4* g_sh, float* gradstat_sum,
                                     uint32_t* gradstat_cnt, float2* const* uv_out,
-                                    const uint8_t* uv_count, cudaStream_t s) {
+                                    const uint8_t* uv_count, int part, cudaStream_t s) {
   for (int v0 = 0; v0 < num_views; v0 += PRE_MAXV) {
     PreArgs a;
     a.num_views = num_views - v0 < PRE_MAXV ? num_views - v0 : PRE_MAXV;
@@ -1333,16 +1333,16 @@ cudaError_t launch_preprocess_views(const CamParams* cams, int num_views, int n,
     }
     const int grid = div_up(n, 256);
     switch (sh_degree) {
-#define PRE(D)                                                                \
-  preprocess_views_kernel<D, 1><<<div_up(n, 128), 128, 0, s>>>(a);           \
-  preprocess_views_kernel<D, 2><<<grid, 256, 0, s>>>(a)
+#define PRE(D)                                                                       \
+  if (part & 1) preprocess_views_kernel<D, 1><<<div_up(n, 128), 128, 0, s>>>(a);      \
+  if (part & 2) preprocess_views_kernel<D, 2><<<grid, 256, 0, s>>>(a)
       case 0: PRE(0); break;
       case 1: PRE(1); break;
       case 2: PRE(2); break;
       default: PRE(3); break;
 #undef PRE
     }
-    launch_counted(2);
+    launch_counted(part == 3 ? 2 : 1);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -1386,7 +1386,7 @@ cudaError_t launch_render_bwd(const CamParams& cam, int n, int sh_degree, const 
   if (e != cudaSuccess) return e;
   return launch_preprocess_views(&cam, 1, n, sh_degree, pos_opa, scale, rot, sh, keep, conic_opa,
                                  rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh, gradstat_sum,
-                                 gradstat_cnt, nullptr, nullptr, s);
+                                 gradstat_cnt, nullptr, nullptr, 3, s);
 }
 
 }  // namespace dass

@@ -35,7 +35,8 @@ EXPORTS = (
     "dass_deform_param_count", "dass_deform_fwd", "dass_deform_bwd", "dass_partition_workspace",
     "dass_partition", "dass_densify_select", "dass_spawn", "dass_prune_select", "dass_gather",
     "dass_render_features", "dass_render_fwd_tiles", "dass_render_bwd_raster_tiles",
-    "dass_render_bwd_preprocess_views_uv", "dass_gradstat_from_uv", "dass_timestamp",
+    "dass_render_bwd_preprocess_views_uv", "dass_render_bwd_preprocess_views_part",
+    "dass_gradstat_from_uv", "dass_timestamp",
     "dass_scan_nonfinite",
     "dass_bin_sort_views_workspace", "dass_bin_sort_views",
 )
@@ -148,6 +149,7 @@ def lib():
                                                    P, P, P, C.c_size_t, i64, P, P]
         L.dass_render_bwd_preprocess_views_uv.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P,
                                                           P, P, P, P, P, P, P, P, P, P, P]
+        L.dass_render_bwd_preprocess_views_part.argtypes = [i32] + list(L.dass_render_bwd_preprocess_views_uv.argtypes)
         L.dass_gradstat_from_uv.argtypes = [i32, i32, P, P, P]
         _lib = L
     return _lib
@@ -352,13 +354,17 @@ def dass_render_bwd_raster(cam, n, tile_ranges, sorted_ids, xy_depth, conic_opa,
                                               _stream(stream)), "dass_render_bwd_raster")
 
 
+DASS_PREPROCESS_GEOMETRY, DASS_PREPROCESS_SH, DASS_PREPROCESS_ALL = 1, 2, 3
+
+
 def dass_render_bwd_preprocess_views(cams, sh_degree, pos_opa, scale, rot, sh, keep_mask,
                                      conic_opa, rgb, box, g2d, g_pos_opa, g_scale, g_rot, g_sh,
                                      gradstat_sum, gradstat_cnt, stream=None, uv_out=None,
-                                     uv_count=None):
+                                     uv_count=None, part=DASS_PREPROCESS_ALL):
     """uv_out: per view None or a float2[n] tensor — split views add their
     (∂L/∂u·W/2, ∂L/∂v·H/2) there instead of the ∇p̄ norm; uv_count[v] truthy:
-    this GPU adds the split view's visibility count (one GPU per view)."""
+    this GPU adds the split view's visibility count (one GPU per view).
+    part: DASS_PREPROCESS_GEOMETRY / _SH / _ALL (dass_render_bwd_preprocess_views_part)."""
     arr = (dass_camera * len(cams))(*[_cam(c) for c in cams])
     uv = cnt = None
     if uv_out is not None:
@@ -367,8 +373,8 @@ def dass_render_bwd_preprocess_views(cams, sh_degree, pos_opa, scale, rot, sh, k
         uv = (C.c_void_p * len(cams))(*[None if u is None else _ptr(u).value for u in uv_out])
         flags = uv_count if uv_count is not None else [0] * len(cams)
         cnt = (C.c_uint8 * len(cams))(*[1 if f else 0 for f in flags])
-    _check(lib().dass_render_bwd_preprocess_views_uv(
-        arr, len(cams), pos_opa.shape[0], sh_degree, _ptr(pos_opa), _ptr(scale), _ptr(rot),
+    _check(lib().dass_render_bwd_preprocess_views_part(
+        part, arr, len(cams), pos_opa.shape[0], sh_degree, _ptr(pos_opa), _ptr(scale), _ptr(rot),
         _ptr(sh), _ptr(keep_mask), _ptr(conic_opa), _ptr(rgb), _ptr(box), _ptr(g2d),
         _ptr(g_pos_opa), _ptr(g_scale), _ptr(g_rot), _ptr(g_sh), _ptr(gradstat_sum),
         _ptr(gradstat_cnt), uv, cnt, _stream(stream)), "dass_render_bwd_preprocess_views")

@@ -180,6 +180,8 @@ class PassOptions:
     split_project: with a projection callback, the projection's records part
       (fp64 records + colour, DASS_PROJECT_RECORDS) on a side stream under the
       views' sorts; the sorts wait only for the keys part, the forwards for both.
+    split_preprocess: the preprocess's SH-coefficient part on a side stream next to
+      its geometry part (DASS_PREPROCESS_SH / _GEOMETRY).
     stream_prio: the first half of the view streams at a higher priority."""
     sort_chains: int = 0
     batch_sort: bool = False
@@ -187,6 +189,7 @@ class PassOptions:
     pre_chunks: int = 1
     proj_chunks: int = 1
     split_project: bool = True
+    split_preprocess: bool = True
     stream_prio: bool = False
 
 
@@ -226,6 +229,7 @@ class MultiViewPass:
         self.sort_streams = ([torch.cuda.Stream(device=device, priority=-5)
                               for _ in range(min(nch, self.S))] if nch > 0 else None)
         self.pre_stream = torch.cuda.Stream(device=device)
+        self.sh_stream = torch.cuda.Stream(device=device) if opt.split_preprocess else None
         self.rec_stream = torch.cuda.Stream(device=device) if opt.split_project else None
         self.pre_chunks = opt.pre_chunks
         self.proj_chunks = opt.proj_chunks
@@ -419,13 +423,27 @@ class MultiViewPass:
         return [v for v in range(self.V) if np_[v, 1]]
 
     def _preprocess(self, scene, records, grads, keep, v0, v1):
-        dass.dass_render_bwd_preprocess_views(
-            self.cams[v0:v1], scene.sh_degree, scene.pos_opa, scene.scale, scene.rot, scene.sh,
-            keep, records.conic_opa[v0:v1], records.rgb[v0:v1], records.box[v0:v1],
-            self.g2d[v0:v1], grads.pos_opa, grads.scale, grads.rot, grads.sh,
-            grads.gradstat_sum, grads.gradstat_cnt,
-            uv_out=None if all(u is None for u in self.uv_out[v0:v1]) else self.uv_out[v0:v1],
-            uv_count=[t is not None and t[0] == 0 for t in self.tiles[v0:v1]])
+        torch = _torch()
+
+        def call(part):
+            dass.dass_render_bwd_preprocess_views(
+                self.cams[v0:v1], scene.sh_degree, scene.pos_opa, scene.scale, scene.rot, scene.sh,
+                keep, records.conic_opa[v0:v1], records.rgb[v0:v1], records.box[v0:v1],
+                self.g2d[v0:v1], grads.pos_opa, grads.scale, grads.rot, grads.sh,
+                grads.gradstat_sum, grads.gradstat_cnt,
+                uv_out=None if all(u is None for u in self.uv_out[v0:v1]) else self.uv_out[v0:v1],
+                uv_count=[t is not None and t[0] == 0 for t in self.tiles[v0:v1]], part=part)
+        if self.sh_stream is None:
+            call(dass.DASS_PREPROCESS_ALL)
+            return
+        # the SH-coefficient part on a side stream next to the geometry part (disjoint
+        # outputs, both latency-bound)
+        cur = torch.cuda.current_stream()
+        self.sh_stream.wait_stream(cur)
+        call(dass.DASS_PREPROCESS_GEOMETRY)
+        with torch.cuda.stream(self.sh_stream):
+            call(dass.DASS_PREPROCESS_SH)
+        cur.wait_stream(self.sh_stream)
 
 
 class DeformFields:

@@ -78,6 +78,9 @@ def test_validation_before_any_cuda_call(lib):
     assert b"null" in L.dass_last_error()
     # n = 0 is OK and enqueues nothing
     assert L.dass_project(C.byref(cam), 0, 3, P, P, P, P, P, P, P, P, P, P, P, P) == 0
+    for part, want in ((0, 1), (4, 1)):   # preprocess part ∉ {1, 2, 3}
+        assert L.dass_render_bwd_preprocess_views_part(part, C.byref(cam), 1, 0, 3, P, P, P, P, P, P,
+                                                       P, P, P, P, P, P, P, P, P, P, P, P) == want
     for part, want in ((0, 1), (4, 1), (1, 0), (2, 0), (3, 0)):   # part ∉ {1, 2, 3}
         assert L.dass_project_views_part(part, C.byref(cam), 1, 0, 3, P, P, P, P, P, P, P, P, P,
                                          P, P, P) == want

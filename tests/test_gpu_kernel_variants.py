@@ -24,9 +24,9 @@ DEV = "cuda"
 @pytest.mark.parametrize("opts", [PassOptions(batch_sort=True, sort_batch_chunks=2),
                                   PassOptions(sort_chains=2), PassOptions(pre_chunks=1, proj_chunks=1),
                                   PassOptions(split_project=False),
-                                  PassOptions(proj_chunks=2)],
+                                  PassOptions(proj_chunks=2), PassOptions(split_preprocess=False)],
                          ids=["batch_sort", "sort_chains", "single_preprocess", "unsplit_projection",
-                              "chunked_split_projection"])
+                              "chunked_split_projection", "one_stream_preprocess"])
 def test_pass_options_parity(opts):
     cams = synth.n3dv_rig(width=160, height=120, num_views=4)
     sc = synth.n3dv_scene(n=5000, seed=57, degree=2, fx=cams[0].fx)
