@@ -231,7 +231,10 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
 #pragma unroll
   for (int j = 0; j < SORT_IPT; ++j) {
     const uint32_t d = digit[j];
-    if (d < 256u) out[s_gbase[d] + s_whist[warp][d] + rank[j]] = keys[j];
+    if (d < 256u) {
+      DASS_CHECK((long long)(s_gbase[d] + s_whist[warp][d] + rank[j]) < (long long)n);
+      out[s_gbase[d] + s_whist[warp][d] + rank[j]] = keys[j];
+    }
   }
 }
 
@@ -356,6 +359,9 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
       tbase = v * (uint32_t)view_tiles;
     }
     uint64_t* out = pkeys + offsets[r];
+#ifdef DASS_CHECKED
+    uint64_t* const out0 = out;
+#endif
     const int nrows = full ? ty1 - ty0 + 1 : 8;
     for (int k = 0; k < nrows; ++k) {
       uint32_t lo, hi;
@@ -373,6 +379,7 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
       const uint32_t L = hi - lo + 1u;
       for (uint32_t dx = 0; dx < L; ++dx) {
         const uint32_t tile = t0 + dx;
+        DASS_CHECK(out < pkeys + K);
         *out++ = ((uint64_t)tile << 32) | gidv;
         atomicAdd(&sh[0][tile & 255u], 1u);
       }
@@ -388,6 +395,9 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
         }
       }
     }
+#ifdef DASS_CHECKED
+    DASS_CHECK((uint32_t)(out - out0) == tiles[id]);   // the rows hold tiles_touched pairs
+#endif
   }
   __syncthreads();
   for (int k = threadIdx.x; k < npass * RADIX; k += blockDim.x) {

@@ -8,6 +8,27 @@
 
 #include "dass.h"
 
+// Device-side checks of the checked build (`python -m paper_2411_14847_b200.build --checked`
+// → libdass_checked.so, -DDASS_CHECKED): index bounds and count invariants on the
+// scatter / emission / list paths, a printf and a trap on violation.  This pool has
+// compute-sanitizer closed, so tools/gpu_checked.sh runs the GPU tests on this build
+// instead.  In the product build the checks compile to nothing.
+#ifdef DASS_CHECKED
+#include <cstdio>
+#define DASS_CHECK(cond)                                                                   \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("DASS_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,      \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                 \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define DASS_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace dass {
 
 constexpr int TILE = DASS_TILE;  // 16×16 pixel tiles (A04)

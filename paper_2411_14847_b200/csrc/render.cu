@@ -728,6 +728,7 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
         }
       }
       if (__any_sync(0xffffffffu, accb != 0u)) {
+        DASS_CHECK(nlist < acc.cap);
         lbytes[(size_t)nlist * 32] = (uint8_t)accb;
         if (lane == 0) acc.idx[nlist] = b0 + j;
         ++nlist;
