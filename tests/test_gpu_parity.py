@@ -576,3 +576,16 @@ def test_long_tile_lists_bit_exact(n, lo, hi):
     c = out["ranges"][:, 1] - out["ranges"][:, 0]
     assert lo <= c.max() <= hi
     check_binsort(cam, out, gpu_projection(out["rec"]))
+
+
+@pytest.mark.parametrize("W,H,n", [(1352, 1014, 30000), (4096, 4096, 70000)],
+                         ids=["c3_image", "image_4096"])
+def test_sort_many_tiles_bit_exact(W, H, n):
+    """dass_bin_sort with 5440 and 65536 tiles (2 tile-digit passes, the second
+    one full at 4096²) against the oracle's brute-force sort (A03/A04)."""
+    cam = synth.tiny_camera(W, H)
+    sc = synth.random_scene(n, cam, seed=79)
+    sc.scale[:, :3] = (np.abs(sc.scale[:, :3]) * 0.5).astype(np.float32)
+    out = run_view(cam, sc, capacity=1 << 22)
+    assert out["K"] > n
+    check_binsort(cam, out, gpu_projection(out["rec"]))
