@@ -1111,7 +1111,25 @@ def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True, phases=None
             "share_of_step_kernels": round(ms / max(sum(v for k, v in ops.items() if k in STEP_OPS), 1e-9), 4),
             "ncu_share_source": f"profiles/{PROFILE_TAG}_launches.txt",
             "in_step": in_step_view(key, phases, units, instr, peak_i, prof, len(stats["accepted"]),
-                                    f_max, profiled)}
+                                    f_max, profiled),
+            "other_raster_kernel": other_raster(key, stats, ops, phases, peak_i, f_max, profiled)}
+
+
+def other_raster(key, stats, ops, phases, peak_i, f_max, profiled):
+    """The other raster kernel (forward when the backward dominates, and vice versa) in the
+    same survey unit, alone and inside the step, for comparison."""
+    other = next(k for k in RASTER_KERNELS if k != key)
+    ms = ops.get(other)
+    if not ms or ms != ms:
+        return None
+    name, p_key, instr, _ = RASTER_KERNELS[other]
+    units = float(sum(stats[p_key]))
+    rate = units * instr / (ms / 1e3) / 1e12
+    prof = "render_fwd" if other == "render_fwd" else "render_bwd"
+    return {"kernel": name, "work_unit": f"{p_key} x {instr} FP32-pipe instructions",
+            "achieved": round(rate, 3), "frac": round(rate / peak_i, 4),
+            "in_step": in_step_view(other, phases, units, instr, peak_i, prof,
+                                    len(stats["accepted"]), f_max, profiled)}
 
 
 def in_step_view(key, phases, units, instr, peak_i, prof, launches, f_max, profiled):
