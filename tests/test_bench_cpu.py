@@ -66,3 +66,17 @@ def test_issue_view_reads_the_committed_profile():
     assert abs(v["frac"] - instr * 20 / 7.4e-3 / (148 * 4 * 1965e6)) < 1e-3
     assert 0 < v["frac"] < 1
     assert bench.issue_view("no_such_kernel", 7.4, 20, 1965e6) is None
+
+
+def test_fair_share_attribution():
+    """roofline.in_step: every interval between stamps is split evenly over the views'
+    phases running in it; the attributed times add up to the pass."""
+    import numpy as np
+    # views 0, 1: sort [0, 1), forward [1, 5), backward [5, 9); view 2's forward runs
+    # late, until 8, under the other two backward kernels, and its backward until 10
+    t = np.array([[0, 1, 5, 9], [0, 1, 5, 9], [0, 1, 8, 10]], dtype=np.float64)
+    out = bench.fair_share(t)
+    assert out["sort"] == 1.0
+    assert abs(out["render_fwd"] - (4.0 + 3.0 / 3)) < 1e-12
+    assert abs(out["render_bwd_raster"] - (3.0 * 2 / 3 + 1.0 + 1.0)) < 1e-12
+    assert abs(sum(out.values()) - 10.0) < 1e-12
