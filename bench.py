@@ -392,18 +392,29 @@ def run_ours(args):
     cnt = torch.zeros(8, dtype=torch.int64, device=dev)
     stats["n_visible"] = []
     tiles_hist = []
+    # this rank's raster work, per work unit: "full" = whole views (the isolated per-op pass
+    # renders every view of the rank whole); "step" = weighted by the share of the view's
+    # tiles the rank renders in the step (a split view's tile half: 1/2)
+    work = {"full": {"P_fwd": 0.0, "P_bwd": 0.0, "accepted": 0.0},
+            "step": {"P_fwd": 0.0, "P_bwd": 0.0, "accepted": 0.0}}
+    ntiles = ((W + 15) // 16) * ((H + 15) // 16)
     for k, cam in enumerate([] if args.lean else my_cams):
-        if plan.tiles[k] is not None and plan.tiles[k][0] != 0:
-            continue   # a split view's statistics are counted once, by the rank with half 0
-        tt = records.tiles[k]
-        vis = tt[tt > 0]
-        stats["n_visible"].append(int(vis.numel()))
-        tiles_hist.append(torch.bincount(vis.clamp(max=4095), minlength=4096).cpu())
+        split_half = plan.tiles[k] is not None
         rec = records.view(k)
         K = raster.forward(cam, rec, host_mode=True)
         dass.dass_render_stats(cam, raster.ranges, raster.sorted_ids, rec[0], rec[1], rec[3],
                                raster.T, raster.last, cnt)
         c = cnt.cpu().numpy()
+        wv = plan.tiles[k][2] / ntiles if split_half else 1.0
+        for key, val in (("P_fwd", c[0]), ("P_bwd", c[1]), ("accepted", c[2])):
+            work["full"][key] += float(val)
+            work["step"][key] += wv * float(val)
+        if split_half and plan.tiles[k][0] != 0:
+            continue   # a split view's scene statistics are counted once, by the rank with half 0
+        tt = records.tiles[k]
+        vis = tt[tt > 0]
+        stats["n_visible"].append(int(vis.numel()))
+        tiles_hist.append(torch.bincount(vis.clamp(max=4095), minlength=4096).cpu())
         stats["K"].append(int(K)); stats["P_fwd"].append(int(c[0])); stats["P_bwd"].append(int(c[1]))
         stats["accepted"].append(int(c[2])); stats["terminated_px"].append(int(c[3]))
         stats["tile_list_mean"].append(float(c[4]) / max(int(c[6]), 1))
@@ -887,7 +898,7 @@ def run_ours(args):
         # the dominant kernel of the step (the larger of the two raster kernels in the
         # isolated per-op pass) against the FP32 roof, algorithmic flops only
         dom = dominant_roofline(ops, stats, f_max, peak_tflops, profiled=args.config == "c3",
-                                phases=phases)
+                                phases=phases, work=work)
         views_s = job_views / (ms_step / 1e3)
         result = {
             "metric": METRIC, "value": round(views_s, 3), "unit": "views/s",
@@ -1066,7 +1077,7 @@ def issue_view(prof, ms, launches, f_max):
             "source": f"profiles/{PROFILE_TAG}_ncu_{prof}.txt (Executed Instructions)"}
 
 
-def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True, phases=None):
+def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True, phases=None, work=None):
     """Roofline object of the step's dominant kernel: whichever raster kernel (forward
     or backward) takes longer in the isolated per-op pass.  achieved = algorithmic
     flops of the step's launches / their summed isolated durations."""
@@ -1077,7 +1088,8 @@ def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True, phases=None
     key = max(cand, key=cand.get)
     ms = cand[key]
     name, p_key, instr, unit = RASTER_KERNELS[key]
-    acc = float(sum(stats["accepted"]))
+    full = work["full"] if work and work["full"].get("accepted") else None
+    acc = full["accepted"] if full else float(sum(stats["accepted"]))
     if key == "render_fwd":
         flops = FLOP_FWD_ACCEPTED * acc + FLOP_FWD_INBOX * float(sum(stats["P_fwd"]))
         per_unit = {"accepted": FLOP_FWD_ACCEPTED, "P_fwd": FLOP_FWD_INBOX}
@@ -1085,7 +1097,7 @@ def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True, phases=None
         flops = FLOP_BWD_ACCEPTED * acc
         per_unit = {"accepted": FLOP_BWD_ACCEPTED}
     achieved = flops / (ms / 1e3) / 1e12
-    units = float(sum(stats[p_key]))
+    units = full[p_key] if full else float(sum(stats[p_key]))
     peak_i = SM_COUNT * FP32_LANES * f_max / 1e12
     rate = units * instr / (ms / 1e3) / 1e12
     prof = "render_fwd" if key == "render_fwd" else "render_bwd"
@@ -1116,12 +1128,17 @@ def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True, phases=None
                       "streams overlap",
             "share_of_step_kernels": round(ms / max(sum(v for k, v in ops.items() if k in STEP_OPS), 1e-9), 4),
             "ncu_share_source": f"profiles/{PROFILE_TAG}_launches.txt",
-            "in_step": in_step_view(key, phases, units, instr, peak_i, prof, len(stats["accepted"]),
-                                    f_max, profiled),
-            "other_raster_kernel": other_raster(key, stats, ops, phases, peak_i, f_max, profiled)}
+            "in_step": in_step_view(key, phases, step_units(work, p_key, units), instr, peak_i, prof,
+                                    len(stats["accepted"]), f_max, profiled),
+            "other_raster_kernel": other_raster(key, stats, ops, phases, peak_i, f_max, profiled, work)}
 
 
-def other_raster(key, stats, ops, phases, peak_i, f_max, profiled):
+def step_units(work, p_key, default):
+    """The units the rank's step renders (split views weighted by their tile share)."""
+    return work["step"][p_key] if work and work["step"].get(p_key) else default
+
+
+def other_raster(key, stats, ops, phases, peak_i, f_max, profiled, work=None):
     """The other raster kernel (forward when the backward dominates, and vice versa) in the
     same survey unit, alone and inside the step, for comparison."""
     other = next(k for k in RASTER_KERNELS if k != key)
@@ -1129,13 +1146,14 @@ def other_raster(key, stats, ops, phases, peak_i, f_max, profiled):
     if not ms or ms != ms:
         return None
     name, p_key, instr, _ = RASTER_KERNELS[other]
-    units = float(sum(stats[p_key]))
+    units = (work["full"][p_key] if work and work["full"].get(p_key)
+             else float(sum(stats[p_key])))
     rate = units * instr / (ms / 1e3) / 1e12
     prof = "render_fwd" if other == "render_fwd" else "render_bwd"
     return {"kernel": name, "work_unit": f"{p_key} x {instr} FP32-pipe instructions",
             "achieved": round(rate, 3), "frac": round(rate / peak_i, 4),
-            "in_step": in_step_view(other, phases, units, instr, peak_i, prof,
-                                    len(stats["accepted"]), f_max, profiled)}
+            "in_step": in_step_view(other, phases, step_units(work, p_key, units), instr, peak_i,
+                                    prof, len(stats["accepted"]), f_max, profiled)}
 
 
 def fair_share(t):
