@@ -395,8 +395,8 @@ def run_ours(args):
     # this rank's raster work, per work unit: "full" = whole views (the isolated per-op pass
     # renders every view of the rank whole); "step" = weighted by the share of the view's
     # tiles the rank renders in the step (a split view's tile half: 1/2)
-    work = {"full": {"P_fwd": 0.0, "P_bwd": 0.0, "accepted": 0.0},
-            "step": {"P_fwd": 0.0, "P_bwd": 0.0, "accepted": 0.0}}
+    work = {"full": {"P_fwd": 0.0, "P_bwd": 0.0, "accepted": 0.0, "views": 0.0},
+            "step": {"P_fwd": 0.0, "P_bwd": 0.0, "accepted": 0.0, "views": 0.0}}
     ntiles = ((W + 15) // 16) * ((H + 15) // 16)
     for k, cam in enumerate([] if args.lean else my_cams):
         split_half = plan.tiles[k] is not None
@@ -406,7 +406,7 @@ def run_ours(args):
                                raster.T, raster.last, cnt)
         c = cnt.cpu().numpy()
         wv = plan.tiles[k][2] / ntiles if split_half else 1.0
-        for key, val in (("P_fwd", c[0]), ("P_bwd", c[1]), ("accepted", c[2])):
+        for key, val in (("P_fwd", c[0]), ("P_bwd", c[1]), ("accepted", c[2]), ("views", 1)):
             work["full"][key] += float(val)
             work["step"][key] += wv * float(val)
         if split_half and plan.tiles[k][0] != 0:
@@ -1122,14 +1122,16 @@ def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True, phases=None
                                       "flop_per_unit": per_unit,
                                       "what": "the builder's count of the flops the kernel must do on the "
                                               "pixels it accepts (FMA = 2), against 2 x the FP32 peak"},
-            "issue_view": issue_view(prof, ms, len(stats["accepted"]), f_max) if profiled else None,
+            "issue_view": issue_view(prof, ms, full["views"] if full else len(stats["accepted"]),
+                                     f_max) if profiled else None,
             "timing": "isolated launches: one sequential pass over the step's kernels (CUDA events on "
                       "the launching stream), since in the timed graph the per-view kernels of 20 "
                       "streams overlap",
             "share_of_step_kernels": round(ms / max(sum(v for k, v in ops.items() if k in STEP_OPS), 1e-9), 4),
             "ncu_share_source": f"profiles/{PROFILE_TAG}_launches.txt",
             "in_step": in_step_view(key, phases, step_units(work, p_key, units), instr, peak_i, prof,
-                                    len(stats["accepted"]), f_max, profiled),
+                                    step_units(work, "views", len(stats["accepted"])), f_max,
+                                    profiled),
             "other_raster_kernel": other_raster(key, stats, ops, phases, peak_i, f_max, profiled, work)}
 
 
@@ -1153,7 +1155,8 @@ def other_raster(key, stats, ops, phases, peak_i, f_max, profiled, work=None):
     return {"kernel": name, "work_unit": f"{p_key} x {instr} FP32-pipe instructions",
             "achieved": round(rate, 3), "frac": round(rate / peak_i, 4),
             "in_step": in_step_view(other, phases, step_units(work, p_key, units), instr, peak_i,
-                                    prof, len(stats["accepted"]), f_max, profiled)}
+                                    prof, step_units(work, "views", len(stats["accepted"])), f_max,
+                                    profiled)}
 
 
 def fair_share(t):
