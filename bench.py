@@ -1079,13 +1079,18 @@ def issue_view(prof, ms, launches, f_max):
 
 def dominant_roofline(ops, stats, f_max, peak_tflops, profiled=True, phases=None, work=None):
     """Roofline object of the step's dominant kernel: whichever raster kernel (forward
-    or backward) takes longer in the isolated per-op pass.  achieved = algorithmic
-    flops of the step's launches / their summed isolated durations."""
+    or backward) takes more of the timed step (its fair-share phase time, when the
+    stamped re-capture ran; else its isolated per-op time).  achieved = the work units
+    of the step's launches / their summed isolated durations."""
     cand = {k: ops.get(k, float("nan")) for k in RASTER_KERNELS}
     cand = {k: v for k, v in cand.items() if v == v and v > 0}
     if not cand or not stats.get("accepted"):
         return None
-    key = max(cand, key=cand.get)
+    share = (phases or {}).get("fair_share_ms") or {}
+    if all(share.get(k) for k in cand):
+        key = max(cand, key=lambda k: share[k])
+    else:
+        key = max(cand, key=cand.get)
     ms = cand[key]
     name, p_key, instr, unit = RASTER_KERNELS[key]
     full = work["full"] if work and work["full"].get("accepted") else None
