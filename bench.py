@@ -919,7 +919,8 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (≈0.5 GB of params, dL/dC and records per step)"},
             "roofline": dom,
             "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
-            "hot_path_roofline": hot_path_roofline(ops, stats, pk, peak_tflops, n, len(my_cams), deg),
+            "hot_path_roofline": hot_path_roofline(ops, stats, pk, peak_tflops, n, len(my_cams), deg,
+                                                   f_max),
             "rows_roofline": rows_roofline(ops, densify, allst, pk, peak_tflops, n, W, H,
                                            len(my_cams), deg),
             "scene_stats": None if args.lean else {"K_per_view_mean": float(np.mean(allst["K"])),
@@ -1209,7 +1210,23 @@ def in_step_view(key, phases, units, instr, peak_i, prof, launches, f_max, profi
     return out
 
 
-def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg):
+def issue_view_parts(profs, ms, views, f_max):
+    """Executed warp instructions of the committed 20-view ncu summaries of a kernel
+    group's launches (profiles/<tag>_ncu_<name>.txt, one launch each for all C3 views) over
+    the group's measured time, against the issue roof (148 SMs × 4 per clock).  Only for
+    the 20-view C3 launch the profiles describe."""
+    if views != 20 or not ms or ms != ms:
+        return None
+    instr = [profiled_instructions(p) for p in profs]
+    if not all(instr):
+        return None
+    rate = sum(instr) / (ms / 1e3)
+    peak = SM_COUNT * 4 * f_max
+    return {"warp_instr_per_step": int(sum(instr)), "frac": round(rate / peak, 4),
+            "source": ", ".join(f"profiles/{PROFILE_TAG}_ncu_{p}.txt" for p in profs)}
+
+
+def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg, f_max=1965e6):
     """Every §8(a) kernel group of the step against its own roof,
     from the sequential per-op pass of rank 0 and that rank's scene statistics."""
     if not ops or not stats.get("K"):
@@ -1229,12 +1246,16 @@ def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg):
     # projection: parameters once per launch (48 + 16·K4 B) + 60 B of records per view
     hb("project_views", n * (48 + 16 * k4) + n * views * 60)
     out["project_views"]["note"] = "issue-bound, not HBM: fp64 record chain + the fp32 key-chain replica"
+    out["project_views"]["issue_view"] = issue_view_parts(
+        ("project_keys_20v", "project_records_20v"), ops["project_views"], views, f_max)
     # binning + sort: per pair 8 B key written by emit, 2 onesweep passes of 16 B read + 16 B
     # written (key + id), finalize 8 B read + 4 B id + range writes; N-key presort ≈ 4 × 32 B
     hb("bin_sort", K * (8 + 2 * 32 + 12) + n * views * 4 * 32)
     out["bin_sort"]["note"] = "latency-bound launch chain (10 kernels per view), hidden under other views' raster kernels"
     # preprocess: 88 B of records + moments per Gaussian-view, parameters and gradients once
     hb("render_bwd_preprocess_views", n * views * 88 + n * 3 * (48 + 16 * k4))
+    out["render_bwd_preprocess_views"]["issue_view"] = issue_view_parts(
+        ("preprocess_20v", "preprocess2_20v"), ops["render_bwd_preprocess_views"], views, f_max)
     t = ops["render_fwd"] / 1e3
     fl = FLOP_FWD_ACCEPTED * acc + FLOP_FWD_INBOX * pfwd   # accepted blend + every in-box α evaluation
     out["render_fwd"] = {"bound": "alu", "flop": int(fl), "achieved_tflops": round(fl / t / 1e12, 2),

@@ -1,6 +1,7 @@
 """Write a profiles/ summary of one ncu --set full report: the command, the kernel,
 DRAM bytes per launch, then tools/ncu_summary.py's key metrics and stall breakdown.
-usage: python tools/profile_txt.py rep.ncu-rep "<ncu args>" "<profiled command>" > profiles/…"""
+usage: python tools/profile_txt.py rep.ncu-rep "<ncu args>" "<profiled command>" ["<what one launch is>"]
+  > profiles/…"""
 import csv
 import io
 import subprocess
@@ -24,7 +25,8 @@ rd, _ = val("dram__bytes_read.sum")
 wr, _ = val("dram__bytes_write.sum")
 print(f"# ncu {ncu_args}")
 print(f"#   {cmd}")
-print("# one launch = one 1352x1014 view of the C3 scene (300k Gaussians)")
+print("# one launch = " + (sys.argv[4] if len(sys.argv) > 4 else
+                           "one 1352x1014 view of the C3 scene (300k Gaussians)"))
 print(f"kernel: {vals[col['Kernel Name']][:90]}")
 print(f"dram_bytes_per_launch: {int(rd + wr)}  (read {rd / 1e6:.3f} MB, write {wr / 1e6:.3f} MB)")
 sys.stdout.flush()
