@@ -618,6 +618,9 @@ def run_ours(args):
     if my_cams and not args.lean:
         E = lambda: torch.cuda.Event(enable_timing=True)
         e_proj = [E(), E()]
+        # keep the GPU busy (≈1 ms) while the host marshals the first call, so the events
+        # time the kernels and not the launch latency of the projection's 20 cameras
+        torch.cuda._sleep(2_000_000)
         e_proj[0].record()
         dass.dass_project_views(my_cams, deg, shifted.pos_opa, shifted.scale, shifted.rot,
                                 shifted.sh, None, records.xy_depth, records.conic_opa,
