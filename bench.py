@@ -923,7 +923,7 @@ def run_ours(args):
             "roofline": dom,
             "ops_ms_per_step_rank0": {k: round(v, 4) for k, v in ops.items()},
             "hot_path_roofline": hot_path_roofline(ops, stats, pk, peak_tflops, n, len(my_cams), deg,
-                                                   f_max),
+                                                   f_max, profiled=args.config == "c3"),
             "rows_roofline": rows_roofline(ops, densify, allst, pk, peak_tflops, n, W, H,
                                            len(my_cams), deg),
             "scene_stats": None if args.lean else {"K_per_view_mean": float(np.mean(allst["K"])),
@@ -1229,7 +1229,7 @@ def issue_view_parts(profs, ms, views, f_max):
             "source": ", ".join(f"profiles/{PROFILE_TAG}_ncu_{p}.txt" for p in profs)}
 
 
-def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg, f_max=1965e6):
+def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg, f_max=1965e6, profiled=False):
     """Every §8(a) kernel group of the step against its own roof,
     from the sequential per-op pass of rank 0 and that rank's scene statistics."""
     if not ops or not stats.get("K"):
@@ -1249,16 +1249,18 @@ def hot_path_roofline(ops, stats, pk, peak_fp32, n, views, deg, f_max=1965e6):
     # projection: parameters once per launch (48 + 16·K4 B) + 60 B of records per view
     hb("project_views", n * (48 + 16 * k4) + n * views * 60)
     out["project_views"]["note"] = "issue-bound, not HBM: fp64 record chain + the fp32 key-chain replica"
-    out["project_views"]["issue_view"] = issue_view_parts(
-        ("project_keys_20v", "project_records_20v"), ops["project_views"], views, f_max)
+    if profiled:   # the committed 20-view summaries are of C3
+        out["project_views"]["issue_view"] = issue_view_parts(
+            ("project_keys_20v", "project_records_20v"), ops["project_views"], views, f_max)
     # binning + sort: per pair 8 B key written by emit, 2 onesweep passes of 16 B read + 16 B
     # written (key + id), finalize 8 B read + 4 B id + range writes; N-key presort ≈ 4 × 32 B
     hb("bin_sort", K * (8 + 2 * 32 + 12) + n * views * 4 * 32)
     out["bin_sort"]["note"] = "latency-bound launch chain (10 kernels per view), hidden under other views' raster kernels"
     # preprocess: 88 B of records + moments per Gaussian-view, parameters and gradients once
     hb("render_bwd_preprocess_views", n * views * 88 + n * 3 * (48 + 16 * k4))
-    out["render_bwd_preprocess_views"]["issue_view"] = issue_view_parts(
-        ("preprocess_20v", "preprocess2_20v"), ops["render_bwd_preprocess_views"], views, f_max)
+    if profiled:
+        out["render_bwd_preprocess_views"]["issue_view"] = issue_view_parts(
+            ("preprocess_20v", "preprocess2_20v"), ops["render_bwd_preprocess_views"], views, f_max)
     t = ops["render_fwd"] / 1e3
     fl = FLOP_FWD_ACCEPTED * acc + FLOP_FWD_INBOX * pfwd   # accepted blend + every in-box α evaluation
     out["render_fwd"] = {"bound": "alu", "flop": int(fl), "achieved_tflops": round(fl / t / 1e12, 2),
