@@ -673,8 +673,10 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
   __shared__ float2 s_pc2[32];
   s_pc[lane] = make_float4((float)pm.x(0), (float)pm.x(4), (float)pm.y(0), (float)pm.y(1));
   s_pc2[lane] = make_float2((float)pm.y(2), (float)pm.y(3));
-  uint8_t* const lbytes = acc.bytes + lane;   // this lane's byte of every list entry
   uint32_t nlist = range.x;                    // next list entry
+  // running pointers to the next entry's byte of this lane and (lane 0) its index slot
+  uint8_t* lbyte = acc.bytes + (size_t)nlist * 32 + lane;
+  uint32_t* lidx = acc.idx + nlist;
   for (uint32_t b0 = range.x; b0 < range.y; b0 += BATCH) {
     if (!__any_sync(0xffffffffu, live != 0u)) break;
     __syncwarp();   // the previous batch is consumed
@@ -729,8 +731,10 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
       }
       if (__any_sync(0xffffffffu, accb != 0u)) {
         DASS_CHECK(nlist < acc.cap);
-        lbytes[(size_t)nlist * 32] = (uint8_t)accb;
-        if (lane == 0) acc.idx[nlist] = b0 + j;
+        *lbyte = (uint8_t)accb;
+        if (lane == 0) *lidx = b0 + j;
+        lbyte += 32;
+        ++lidx;
         ++nlist;
       }
     }
