@@ -799,7 +799,10 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
     s_g[p][lane] = gg;
     gR[p] = T[p] * (gg.x * bg.x + gg.y * bg.y + gg.z * bg.z);
   }
-  const float fx0 = (float)pm.x(0), fx1 = (float)pm.x(4);
+  // the lane's pixel columns, read from shared memory per entry (the 64-register budget
+  // otherwise rematerialises them from the lane id every entry)
+  __shared__ float2 s_fx[32];
+  s_fx[lane] = make_float2((float)pm.x(0), (float)pm.x(4));
   float fy[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) fy[r] = (float)pm.y(r);
@@ -832,7 +835,8 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
         const float4 a = s_a[k];
         const float4 co = s_co[k];
         const float4 c = s_c[k];
-        const float dxc[2] = {a.x - fx0, a.x - fx1};
+        const float2 fx = s_fx[lane];
+        const float dxc[2] = {a.x - fx.x, a.x - fx.y};
         const float Xc[2] = {col_term(co, dxc[0]), col_term(co, dxc[1])};
         float se[2] = {0.f, 0.f}, sey[2] = {0.f, 0.f};   // per column: Σe, Σe·dy
 #pragma unroll
