@@ -26,7 +26,12 @@ namespace {
 
 constexpr int SORT_THREADS = 256;
 constexpr int SORT_IPT = 8;
-constexpr int SORT_ITEMS = SORT_THREADS * SORT_IPT;  // 2048 keys per block
+constexpr int SORT_ITEMS = SORT_THREADS * SORT_IPT;  // 2048 keys per block (pair passes)
+// depth presort passes: 16 keys per thread, 4096 per block (74 blocks at N = 300k); fewer,
+// longer blocks overlap better with the other views' chains (step 11.76 → 11.74 ms against 8;
+// 4: 11.83, 32: 11.86)
+constexpr int PRESORT_IPT = 16;
+constexpr int PRESORT_ITEMS = SORT_THREADS * PRESORT_IPT;
 constexpr int RADIX = 256;
 constexpr int MAX_PASSES = 8;  // hist slots: 0..3 depth presort, 4..7 pair sort
 constexpr uint32_t FLAG_AGG = 1u << 30;
@@ -80,12 +85,13 @@ WS carve(void* base, int n, int64_t cap) {
   char* p = (char*)base;
   size_t off = 0;
   auto take = [&](size_t bytes) { char* r = p ? p + off : nullptr; off += align_up(bytes); return r; };
-  const size_t nblk_n = (size_t)div_up(n > 0 ? n : 1, SORT_ITEMS);
+  const size_t nblk_n = (size_t)div_up(n > 0 ? n : 1, PRESORT_ITEMS);
   const size_t nblk_cap = (size_t)((cap + SORT_ITEMS - 1) / SORT_ITEMS) + 1;
   w.hist = (uint32_t*)take(sizeof(uint32_t) * MAX_PASSES * RADIX);
   w.counters = (uint32_t*)take(sizeof(uint32_t) * NUM_COUNTERS);
   w.ctrl_bytes = off;
-  w.scan_status = (unsigned long long*)take(sizeof(unsigned long long) * nblk_n);
+  w.scan_status = (unsigned long long*)take(sizeof(unsigned long long) *
+                                            (size_t)div_up(n > 0 ? n : 1, SORT_ITEMS));
   w.dstatus = (uint32_t*)take(sizeof(uint32_t) * 4 * nblk_n * RADIX);
   w.pstatus = (uint32_t*)take(sizeof(uint32_t) * (MAX_PASSES - 4) * nblk_cap * RADIX);
   w.dkeysA = (uint64_t*)take(sizeof(uint64_t) * (size_t)(n > 0 ? n : 1));
@@ -129,12 +135,12 @@ __global__ void __launch_bounds__(256) presort_init_kernel(int n, const float4* 
 }
 
 // One onesweep LSD pass over bits [shift, shift+8) of 64-bit keys.
-template <typename KT = uint64_t>
+template <typename KT = uint64_t, int IPT = SORT_IPT>
 __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     const KT* __restrict__ in, KT* __restrict__ out, int n_static,
     const uint32_t* __restrict__ n_dev, const uint32_t* __restrict__ hist, uint32_t* status,
     uint32_t* counter, int shift) {
-  // per-warp digit counts, then per-warp exclusive offsets: ≤ SORT_ITEMS, so 16 bits
+  // per-warp digit counts, then per-warp exclusive offsets: ≤ 256·IPT, so 16 bits
   // (4 KB instead of 8: a smaller footprint next to the raster CTAs of other views)
   __shared__ uint16_t s_whist[SORT_THREADS / 32][RADIX];
   __shared__ uint32_t s_gbase[RADIX];
@@ -149,17 +155,17 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
   if (t == 0) s_blk = atomicAdd(counter, 1u);
   __syncthreads();
   const uint32_t blk = s_blk;
-  const long long base = (long long)blk * SORT_ITEMS;
+  const long long base = (long long)blk * (SORT_THREADS * IPT);
   if (base >= n) return;
   for (int k = t; k < (SORT_THREADS / 32) * RADIX; k += SORT_THREADS) (&s_whist[0][0])[k] = 0u;
   __syncthreads();
 
-  KT keys[SORT_IPT];
-  uint32_t digit[SORT_IPT];
-  uint32_t rank[SORT_IPT];
-  const long long wbase = base + warp * (SORT_IPT * 32);
+  KT keys[IPT];
+  uint32_t digit[IPT];
+  uint32_t rank[IPT];
+  const long long wbase = base + warp * (IPT * 32);
 #pragma unroll
-  for (int j = 0; j < SORT_IPT; ++j) {
+  for (int j = 0; j < IPT; ++j) {
     const long long idx = wbase + j * 32 + lane;
     if (idx < n) {
       keys[j] = in[idx];
@@ -171,7 +177,7 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
-  for (int j = 0; j < SORT_IPT; ++j) {
+  for (int j = 0; j < IPT; ++j) {
     const uint32_t d = digit[j];
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     uint32_t pre = 0u;
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
   s_gbase[t] = gofs + excl;
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < SORT_IPT; ++j) {
+  for (int j = 0; j < IPT; ++j) {
     const uint32_t d = digit[j];
     if (d < 256u) {
       DASS_CHECK((long long)(s_gbase[d] + s_whist[warp][d] + rank[j]) < (long long)n);
@@ -498,7 +504,7 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   }
   const int tile_bits = num_tiles > 1 ? 32 - __builtin_clz((unsigned)(num_tiles - 1)) : 0;
   const int npass = (tile_bits + 7) / 8;
-  const int nblk_n = div_up(n, SORT_ITEMS);
+  const int nblk_n = div_up(n, PRESORT_ITEMS);
   const size_t nblk_cap = (size_t)((capacity + SORT_ITEMS - 1) / SORT_ITEMS) + 1;
   const int grid_n = div_up(n, 256) < 148 * 8 ? div_up(n, 256) : 148 * 8;
   // two blocks per SM: every block flushes its 4×256 shared histogram bins with global
@@ -507,20 +513,21 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   // emit on two blocks per SM too (same histogram flush; measured 11.94 -> 11.89 ms in the
   // step, four per SM 11.90)
   const int grid_e = div_up(n, 256) < 148 * 2 ? div_up(n, 256) : 148 * 2;
+  const int nblk_s = div_up(n, SORT_ITEMS);   // tile_scan blocks (2048 Gaussians each)
   presort_init_kernel<<<grid_i, 256, 0, s>>>(n, xy_depth, tiles, w.dkeysA, w.hist, w.dstatus,
-                                             (size_t)4 * nblk_n * RADIX, w.scan_status, nblk_n);
+                                             (size_t)4 * nblk_n * RADIX, w.scan_status, nblk_s);
   launch_counted();
   uint64_t* a = w.dkeysA;
   uint64_t* b = w.dkeysB;
   for (int p = 0; p < 4; ++p) {
-    onesweep_kernel<uint64_t><<<nblk_n, SORT_THREADS, 0, s>>>(a, b, n, nullptr, w.hist + p * RADIX,
+    onesweep_kernel<uint64_t, PRESORT_IPT><<<nblk_n, SORT_THREADS, 0, s>>>(a, b, n, nullptr, w.hist + p * RADIX,
                                                     w.dstatus + (size_t)p * nblk_n * RADIX,
                                                     w.counters + p, 32 + 8 * p);
     launch_counted();
     uint64_t* tmp = a; a = b; b = tmp;
   }
   // a = depth-sorted (zbits, id)
-  tile_scan_kernel<<<nblk_n, 256, 0, s>>>(n, a, tiles, w.offsets, w.scan_status, w.counters + 4,
+  tile_scan_kernel<<<nblk_s, 256, 0, s>>>(n, a, tiles, w.offsets, w.scan_status, w.counters + 4,
                                           (long long)capacity, num_pairs_dev);
   launch_counted();
   emit_kernel<<<grid_e, 256, 0, s>>>(n, a, tiles, box, rows, w.offsets, num_pairs_dev, cam.tiles_x,
@@ -571,22 +578,23 @@ cudaError_t launch_binsort_views(const CamParams& cam, int V, int n, const float
   const int ct_bits = vt > 1 ? 32 - __builtin_clz((unsigned)(vt - 1)) : 0;
   const int npass = (ct_bits + 7) / 8;
   if (npass > MAX_PASSES - 4) return cudaErrorInvalidValue;
-  const int nblk_n = div_up(nn, SORT_ITEMS);
+  const int nblk_n = div_up(nn, PRESORT_ITEMS);
   const size_t nblk_cap = (size_t)((cap + SORT_ITEMS - 1) / SORT_ITEMS) + 1;
   const int grid_n = div_up(nn, 256) < 148 * 8 ? div_up(nn, 256) : 148 * 8;
+  const int nblk_s = div_up(nn, SORT_ITEMS);
   presort_init_kernel<<<grid_n, 256, 0, s>>>(nn, xy_depth, tiles, w.dkeysA, w.hist, w.dstatus,
-                                             (size_t)4 * nblk_n * RADIX, w.scan_status, nblk_n);
+                                             (size_t)4 * nblk_n * RADIX, w.scan_status, nblk_s);
   launch_counted();
   uint64_t* a = w.dkeysA;
   uint64_t* b = w.dkeysB;
   for (int p = 0; p < 4; ++p) {
-    onesweep_kernel<uint64_t><<<nblk_n, SORT_THREADS, 0, s>>>(a, b, nn, nullptr, w.hist + p * RADIX,
+    onesweep_kernel<uint64_t, PRESORT_IPT><<<nblk_n, SORT_THREADS, 0, s>>>(a, b, nn, nullptr, w.hist + p * RADIX,
                                                     w.dstatus + (size_t)p * nblk_n * RADIX,
                                                     w.counters + p, 32 + 8 * p);
     launch_counted();
     uint64_t* tmp = a; a = b; b = tmp;
   }
-  tile_scan_kernel<<<nblk_n, 256, 0, s>>>(nn, a, tiles, w.offsets, w.scan_status, w.counters + 4,
+  tile_scan_kernel<<<nblk_s, 256, 0, s>>>(nn, a, tiles, w.offsets, w.scan_status, w.counters + 4,
                                           (long long)cap, kg);
   launch_counted();
   emit_kernel<<<grid_n, 256, 0, s>>>(nn, a, tiles, box, rows, w.offsets, kg, cam.tiles_x, npass, w.pkeysA,
