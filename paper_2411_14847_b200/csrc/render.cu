@@ -698,22 +698,21 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
         const float fy[4] = {pc.z, pc.w, pc2.x, pc2.y};
         const float X0 = col_term(co, a.x - pc.x), X1 = col_term(co, a.x - pc.y);
         float pw[PPT];
-        uint32_t ok = 0;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const RowTerms R = row_terms(co, a.y - fy[r]);
           pw[r] = splat_power(X0, R);
           pw[r + 4] = splat_power(X1, R);
         }
-#pragma unroll
-        for (int p = 0; p < PPT; ++p)
-          ok |= (uint32_t)(pw[p] >= a.z) << p;   // the power > 0 guard is in the pixel block
-        ok &= cand;
-        if (ok) {
+        // every candidate pixel block tests the power threshold itself: no packed 8-bit
+        // threshold mask first (its 20 compare/select/add instructions and their dependency
+        // chain cost more in the overlapped step than the extra blocks entered: step 11.74 →
+        // 11.59 ms, although the forward alone is 3 % slower)
+        {
           const float4 c = st.c;
 #pragma unroll
           for (int p = 0; p < PPT; ++p) {
-            if (!((ok >> p) & 1u)) continue;
+            if (!((cand >> p) & 1u) || !(pw[p] >= a.z)) continue;
             const float alpha = splat_alpha(co.w, splat_exp(pw[p]));
             if (alpha < ALPHA_MIN || pw[p] > 0.f) continue;   // A11: skip if power > 0
             const float tn = __fmul_rn(T[p], __fsub_rn(1.f, alpha));
