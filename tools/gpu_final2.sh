@@ -29,3 +29,5 @@ tail -2 gpurun_out/pytest_gpu_$TAG.log; tail -2 gpurun_out/smoke_$TAG.log
 python -c "
 import json;d=json.loads(open('gpurun_out/bench_c3_$TAG.json').read().strip().splitlines()[-1]);print(d['value'], d['ms_per_step'], d['e2e']['value'], d['clocks'])"
 bash tools/gpu_prof_pre.sh $TAG
+bash tools/gpu_prof_pp20.sh $TAG
+bash tools/gpu_checked.sh $TAG
