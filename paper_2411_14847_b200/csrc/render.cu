@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(32, MINB) render_fwd_tw_kernel(
       if (m == 0u) continue;             // warp-uniform: support misses the tile
       uint32_t accb = 0;                 // this lane's accepted pixels of the entry
       const uint32_t cand = pm.cand(m) & live;
-      if (cand) {
+      {   // no per-lane guard: a lane without candidates just enters no pixel block
         const float4 co = st.co;
         const float4 pc = s_pc[lane];
         const float2 pc2 = s_pc2[lane];
