@@ -830,7 +830,7 @@ __global__ void __launch_bounds__(32, MINB) render_bwd_tw_kernel(
       float v[9];
 #pragma unroll
       for (int q = 0; q < 9; ++q) v[q] = 0.f;
-      if (bits) {
+      {   // no per-lane guard: a lane without accepted pixels enters no pixel block
         const float4 a = s_a[k];
         const float4 co = s_co[k];
         const float4 c = s_c[k];
