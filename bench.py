@@ -113,6 +113,9 @@ def parse():
     p.add_argument("--emulate", default=None, metavar="R/W",
                    help="diagnostic: run rank R's share of a W-GPU view plan on this one GPU "
                         "(no collective) — predicts per-rank step time for --gpus W")
+    p.add_argument("--late-collective", action="store_true",
+                   help="issue the shift payload's all_reduce after the preprocess SH part joins "
+                        "(default: before, overlapping it; the payload holds no SH gradients)")
     p.add_argument("--payload", choices=("shift", "full"), default="shift",
                    help="what the per-step all_reduce sums: the shift stage's payload (g_mu, "
                         "g_sigma, grad-stat; default, the metric's step is a shift iteration) "
@@ -358,22 +361,26 @@ def run_ours(args):
         """∇p̄ of the views split across ranks, from their reduced uv partials."""
         dass.dass_gradstat_from_uv(g.uv, g.gradstat_sum)
 
-    def step_local(S=bufs0, wait_inputs=None):
-        stepper.run(S, wait_inputs=wait_inputs)
-
-    coll_in_graph = {"value": False}
-
     def collective(S=bufs0):
         """The one cross-GPU exchange (NCCL all_reduce of the stage's payload)."""
         allreduce_grads(S.grads, finish=finish_split, stage=args.payload)
 
+    def step_local(S=bufs0, wait_inputs=None, coll=False):
+        """The step on this GPU; coll: with its collective, which the shift payload (no SH
+        gradients) issues while the preprocess's SH part still runs (ShiftStep.run)."""
+        stepper.run(S, wait_inputs=wait_inputs,
+                    collective=(lambda: collective(S)) if coll else None,
+                    collective_after_sh=args.payload != "shift" or args.late_collective)
+
+    coll_in_graph = {"value": False}
+
     def run_step(graph=None, S=bufs0):
         if graph is None:
-            step_local(S)
+            step_local(S, coll=distd)
         else:
             graph.replay()
-        if distd and not (graph is not None and coll_in_graph["value"]):
-            collective(S)
+            if distd and not coll_in_graph["value"]:
+                collective(S)
 
     def step():
         run_step(None)
@@ -431,9 +438,7 @@ def run_ours(args):
         graph = torch.cuda.CUDAGraph()
         try:   # the collective captured with the step: one graph launch per step
             with torch.cuda.graph(graph):
-                step_local()
-                if distd:
-                    collective()
+                step_local(coll=distd)
             coll_in_graph["value"] = distd
         except Exception as exc:   # NCCL capture unavailable: the collective runs after the replay
             print(f"bench: collective not captured ({exc}); running it after the graph", file=sys.stderr)
@@ -487,9 +492,7 @@ def run_ours(args):
         mvp.stamps = stamps
         g2 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g2):
-            step_local()
-            if distd and coll_in_graph["value"]:
-                collective()
+            step_local(coll=distd and coll_in_graph["value"])
         mvp.stamps = None
         span = {"sort": [], "render_fwd": [], "render_bwd_raster": []}
         share = {"sort": [], "render_fwd": [], "render_bwd_raster": []}
@@ -806,10 +809,9 @@ def run_ours(args):
                 hook(b)
                 graphs[b] = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(graphs[b]):
+                    # as the timed step: the collective in the graph
                     step_local(sets[b], wait_inputs=lambda b=b: wait_external(
-                        torch.cuda.current_stream(), ev_par[b]))
-                    if coll_in_graph["value"]:   # as the timed step: the collective in the graph
-                        collective(sets[b])
+                        torch.cuda.current_stream(), ev_par[b]), coll=coll_in_graph["value"])
         hook(None)
 
         def upload(k):
@@ -831,10 +833,8 @@ def run_ours(args):
                 run_step(graphs[b], sets[b])
             else:                                    # eager: the same waits, issued directly
                 hook(b, capture=False)
-                step_local(sets[b], wait_inputs=lambda: comp.wait_event(ev_par[b]))
+                step_local(sets[b], wait_inputs=lambda: comp.wait_event(ev_par[b]), coll=distd)
                 hook(None)
-                if distd:
-                    collective(sets[b])
             ev_res[b].record(comp)
 
         def download(k):

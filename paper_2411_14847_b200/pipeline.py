@@ -230,6 +230,8 @@ class MultiViewPass:
                               for _ in range(min(nch, self.S))] if nch > 0 else None)
         self.pre_stream = torch.cuda.Stream(device=device)
         self.sh_stream = torch.cuda.Stream(device=device) if opt.split_preprocess else None
+        # leave the SH part unjoined at the end of run(); the caller joins with join_sh()
+        self.defer_sh = False
         self.rec_stream = torch.cuda.Stream(device=device) if opt.split_project else None
         self.pre_chunks = opt.pre_chunks
         self.proj_chunks = opt.proj_chunks
@@ -443,7 +445,14 @@ class MultiViewPass:
         call(dass.DASS_PREPROCESS_GEOMETRY)
         with torch.cuda.stream(self.sh_stream):
             call(dass.DASS_PREPROCESS_SH)
-        cur.wait_stream(self.sh_stream)
+        if not self.defer_sh:
+            cur.wait_stream(self.sh_stream)
+
+    def join_sh(self):
+        """Join the SH-coefficient part deferred by defer_sh (ShiftStep: after the
+        shift stage's collective, which does not carry SH gradients)."""
+        if self.sh_stream is not None:
+            _torch().cuda.current_stream().wait_stream(self.sh_stream)
 
 
 class DeformFields:

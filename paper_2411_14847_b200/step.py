@@ -85,9 +85,13 @@ class ShiftStep:
                                        num_split=self.num_split)
         return StepBufs(base, mu, sigma, dLs, grads, self.shifted_pos, self.shifted_rot)
 
-    def run(self, S: StepBufs, wait_inputs=None):
-        """Everything on this GPU (capturable: no host sync, no collective).
-        wait_inputs(): an end-to-end caller's wait for this step's parameter upload."""
+    def run(self, S: StepBufs, wait_inputs=None, collective=None, collective_after_sh=True):
+        """Everything on this GPU (capturable: no host sync).
+        wait_inputs(): an end-to-end caller's wait for this step's parameter upload.
+        collective(): the caller's cross-GPU exchange of this step, issued on the current
+        stream after the shift backward; with collective_after_sh=False (a payload without
+        SH gradients, the shift stage's) it runs while the preprocess's SH-coefficient part
+        is still going on its side stream."""
         g = S.grads
         g.zero_()
         if wait_inputs is not None:
@@ -102,13 +106,22 @@ class ShiftStep:
                                          sh.rot, sh.sh, None, rec.xy_depth[v0:v1],
                                          rec.conic_opa[v0:v1], rec.rgb[v0:v1], rec.box[v0:v1],
                                          rec.rows[v0:v1], rec.tiles[v0:v1])
+        early = collective is not None and not collective_after_sh
         if self.mvp is not None:
             self._errmap_pos = sh.pos_opa     # the error map projects 𝒢_t (Alg. 1)
             self.mvp.uv_out = [None if s < 0 else g.uv[s] for s in self.split]
+            self.mvp.defer_sh = early
             self.mvp.run(sh, rec, S.dLs, g, project=project)
+            self.mvp.defer_sh = False
         if self.shift:
             dass.dass_apply_shift_bwd(S.base.rot, S.sigma, S.base.dynamic, g.pos_opa, g.rot,
                                       g.g_mu, g.g_sigma)
+        if early:
+            collective()
+        if self.mvp is not None:
+            self.mvp.join_sh()
+        if collective is not None and not early:
+            collective()
         if self.validate:
             self.bad.zero_()
             dass.dass_scan_nonfinite(g.flat, self.bad)

@@ -172,3 +172,43 @@ def test_nonfinite_scan_host_and_graph_mode():
     with pytest.raises(dass.DassError) as ei:
         stepper.check_numerics()
     assert ei.value.status == dass.DASS_ERR_NUMERICAL
+
+
+@pytest.mark.parametrize("graph", [False, True], ids=["eager", "graph"])
+def test_collective_issued_before_sh_join_sees_complete_payload(graph):
+    """ShiftStep.run(collective=…, collective_after_sh=False) — bench.py's shift payload
+    at N>1 — issues the exchange while the preprocess's SH part is still on its side
+    stream.  A stand-in collective snapshots the payload slice on the stream the
+    all_reduce would use: the snapshot must equal the finished payload bit for bit
+    (nothing the shift payload holds is written after it), and the SH gradients,
+    joined afterwards, must equal a run with the collective after the join."""
+    cams = synth.n3dv_rig(width=320, height=240, num_views=6)
+    sc = synth.n3dv_scene(n=20000, seed=61, degree=3, fx=cams[0].fx)
+    mu, sigma = synth.shift_offsets(sc, seed=34)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    base = DeviceScene.from_host(sc, DEV)
+    dls = torch.stack([t(synth.grad_image(c, 70 + v)) for v, c in enumerate(cams)])
+    out = []
+    for after_sh in (True, False):
+        stepper = ShiftStep(cams, sc.n, 3, 1 << 21, DEV, streams=6)
+        S = stepper.buffers(base, t(mu), t(sigma), dls)
+        snap = torch.empty_like(S.grads.payload("shift"))
+        coll = lambda: snap.copy_(S.grads.payload("shift"))
+        if graph:
+            stepper.run(S)
+            torch.cuda.synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                stepper.run(S, collective=coll, collective_after_sh=after_sh)
+            snap.zero_()
+            gr.replay()
+        else:
+            stepper.run(S, collective=coll, collective_after_sh=after_sh)
+        torch.cuda.synchronize()
+        stepper.check_overflow()
+        assert torch.equal(snap.view(torch.int32), S.grads.payload("shift").view(torch.int32))
+        assert float(S.grads.payload("shift").abs().sum()) > 0
+        out.append(S.grads.sh.clone())
+    a, b = out
+    assert float(b.abs().max()) > 0
+    assert float((a - b).abs().max()) <= 1e-5 * float(b.abs().max())
