@@ -146,6 +146,8 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
   __shared__ uint32_t s_gbase[RADIX];
   __shared__ uint32_t s_wsum[SORT_THREADS / 32];
   __shared__ uint32_t s_blk;
+  pdl_trigger();
+  pdl_wait();
   const int t = threadIdx.x;
   const int warp = t >> 5;
   const uint32_t lane = lane_id();
@@ -256,6 +258,8 @@ __global__ void __launch_bounds__(256) tile_scan_kernel(int n, const uint64_t* _
   __shared__ unsigned long long s_w[8];
   __shared__ unsigned long long s_excl;
   __shared__ uint32_t s_blk;
+  pdl_trigger();
+  pdl_wait();
   const int t = threadIdx.x;
   const uint32_t lane = lane_id();
   const int warp = t >> 5;
@@ -335,6 +339,8 @@ __global__ void __launch_bounds__(256) emit_kernel(int n, const uint64_t* __rest
                                                   size_t pstatus_stride, int view_n = 0,
                                                   int view_tiles = 0) {
   __shared__ uint32_t sh[MAX_PASSES - 4][RADIX];
+  pdl_trigger();
+  pdl_wait();
   if (num_pairs_dev[1]) return;  // overflow: every range stays [0,0)
   for (int k = threadIdx.x; k < (MAX_PASSES - 4) * RADIX; k += blockDim.x) (&sh[0][0])[k] = 0u;
   __syncthreads();
@@ -418,6 +424,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint64_t* __restric
                                                       const float4* __restrict__ xy_depth,
                                                       uint64_t* sorted_keys, uint32_t* ids,
                                                       uint2* ranges) {
+  pdl_wait();
   if (num_pairs_dev[1]) return;
   const uint32_t K = num_pairs_dev[0];
   const size_t gstride = (size_t)gridDim.x * blockDim.x;
@@ -485,6 +492,24 @@ __global__ void __launch_bounds__(256) finalize_views_kernel(const uint64_t* __r
 
 }  // namespace
 
+// A chain kernel launched with programmatic stream serialisation: its blocks may be
+// scheduled while the previous kernel of the view's chain drains (they wait in
+// pdl_wait() for its completion), which shortens the 10-kernel chain's gaps.
+template <typename... P, typename... A>
+cudaError_t launch_pdl(void (*k)(P...), int grid, int block, cudaStream_t s, A... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<P>(args)...);
+}
+
 size_t binsort_workspace(int n, int num_tiles, int64_t capacity) {
   (void)num_tiles;
   return carve(nullptr, n, capacity).total;
@@ -520,33 +545,32 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   uint64_t* a = w.dkeysA;
   uint64_t* b = w.dkeysB;
   for (int p = 0; p < 4; ++p) {
-    onesweep_kernel<uint64_t, PRESORT_IPT><<<nblk_n, SORT_THREADS, 0, s>>>(a, b, n, nullptr, w.hist + p * RADIX,
-                                                    w.dstatus + (size_t)p * nblk_n * RADIX,
-                                                    w.counters + p, 32 + 8 * p);
+    if ((e = launch_pdl(onesweep_kernel<uint64_t, PRESORT_IPT>, nblk_n, SORT_THREADS, s, a, b, n,
+                        (const uint32_t*)nullptr, w.hist + p * RADIX,
+                        w.dstatus + (size_t)p * nblk_n * RADIX, w.counters + p, 32 + 8 * p))) return e;
     launch_counted();
     uint64_t* tmp = a; a = b; b = tmp;
   }
   // a = depth-sorted (zbits, id)
-  tile_scan_kernel<<<nblk_s, 256, 0, s>>>(n, a, tiles, w.offsets, w.scan_status, w.counters + 4,
-                                          (long long)capacity, num_pairs_dev);
+  if ((e = launch_pdl(tile_scan_kernel, nblk_s, 256, s, n, a, tiles, w.offsets, w.scan_status,
+                      w.counters + 4, (long long)capacity, num_pairs_dev))) return e;
   launch_counted();
-  emit_kernel<<<grid_e, 256, 0, s>>>(n, a, tiles, box, rows, w.offsets, num_pairs_dev, cam.tiles_x,
-                                     npass, w.pkeysA, w.hist, w.pstatus, nblk_cap * RADIX);
+  if ((e = launch_pdl(emit_kernel, grid_e, 256, s, n, a, tiles, box, rows, w.offsets, num_pairs_dev,
+                      cam.tiles_x, npass, w.pkeysA, w.hist, w.pstatus, nblk_cap * RADIX, 0, 0))) return e;
   launch_counted();
   uint64_t* pa = w.pkeysA;
   uint64_t* pb = w.pkeysB;
   const int grid_cap = (int)nblk_cap;
   for (int p = 0; p < npass; ++p) {
-    onesweep_kernel<uint64_t><<<grid_cap, SORT_THREADS, 0, s>>>(pa, pb, -1, num_pairs_dev,
-                                                      w.hist + (4 + p) * RADIX,
-                                                      w.pstatus + (size_t)p * nblk_cap * RADIX,
-                                                      w.counters + 5 + p, 32 + 8 * p);
+    if ((e = launch_pdl(onesweep_kernel<uint64_t, SORT_IPT>, grid_cap, SORT_THREADS, s, pa, pb, -1,
+                        num_pairs_dev, w.hist + (4 + p) * RADIX,
+                        w.pstatus + (size_t)p * nblk_cap * RADIX, w.counters + 5 + p, 32 + 8 * p))) return e;
     launch_counted();
     uint64_t* tmp = pa; pa = pb; pb = tmp;
   }
   const int grid_f = 148 * 8;
-  finalize_kernel<<<grid_f, 256, 0, s>>>(pa, num_pairs_dev, xy_depth, sorted_keys, sorted_ids,
-                                         ranges);
+  if ((e = launch_pdl(finalize_kernel, grid_f, 256, s, pa, num_pairs_dev, xy_depth, sorted_keys,
+                      sorted_ids, ranges))) return e;
   launch_counted();
   return cudaGetLastError();
 }

@@ -118,6 +118,15 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
 __device__ __forceinline__ void red_add_f32(float* addr, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" :: "l"(addr), "f"(v) : "memory");
 }
+// Programmatic dependent launch (a kernel launched with the programmatic stream
+// serialisation attribute may start before its predecessor on the stream ends):
+// pdl_wait() blocks until the predecessor grid has completed and its writes are
+// visible — every such kernel calls it before reading what the predecessor wrote;
+// pdl_trigger() lets the dependent grid's blocks be scheduled once every block of
+// this grid has issued it.  Both are no-ops for a kernel launched without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void red_add_u32(uint32_t* addr, uint32_t v) {
   asm volatile("red.global.add.u32 [%0], %1;" :: "l"(addr), "r"(v) : "memory");
 }
