@@ -1008,10 +1008,20 @@ def cpu_baseline(cams, scene, nviews, config="c3"):
                 "sample": f"the whole {config} step (one view fwd+bwd, {mode} form, double), repeated",
                 "seconds": out}
     secs = time_oracle(cams, scene, list(range(nviews)))
-    return {"value": round(nviews / secs, 4), "unit": "views/s", "cores": allt,
-            "kind": "oracle", "host": host_cpu(),
-            "sample": f"{nviews} of the {len(cams)} views (fwd+bwd, scatter form, double) + the shift, "
-                      f"{secs:.1f} s on {allt} OpenMP threads"}
+    out = {"value": round(nviews / secs, 4), "unit": "views/s", "cores": allt,
+           "kind": "oracle", "host": host_cpu(),
+           "sample": f"{nviews} of the {len(cams)} views (fwd+bwd, scatter form, double) + the shift, "
+                     f"{secs:.1f} s on {allt} OpenMP threads"}
+    if config != "c5":   # C5's 1M Gaussians would take about a minute on one thread
+        # and one view (+ the shift) on one thread: the oracle's serial rate
+        oracle.set_threads(1)
+        try:
+            s1 = time_oracle(cams, scene, [0])
+        finally:
+            oracle.set_threads(allt)
+        out["single_thread"] = {"value": round(1.0 / s1, 4), "unit": "views/s", "threads": 1,
+                                "sample": f"view 0 (fwd+bwd, scatter form, double) + the shift, {s1:.1f} s"}
+    return out
 
 
 def run_reference(args):
