@@ -291,6 +291,22 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth,
                   uint32_t* tile_ranges, uint32_t* num_pairs_dev,
                   int64_t* num_pairs_host, void* stream);
 
+/* dass_bin_sort_shared — dass_bin_sort (same arguments, workspace, outputs and
+ * errors, bit for bit the same results) for a view sorted while other views'
+ * kernels share the GPU, as in the multi-view step.  K is known on the
+ * device only, so dass_bin_sort launches the pair passes for the capacity, one
+ * block per 2048-key tile; here a fixed grid of 74 blocks loops over the key
+ * tiles instead: slower alone, but fewer resident blocks next to the other
+ * views' sorts and raster kernels (C3 step 11.32 → 11.29 ms against a
+ * one-block-per-SM grid, 11.44 against the capacity grid). */
+int dass_bin_sort_shared(const dass_camera* cam, int32_t n, const float* xy_depth,
+                         const uint32_t* box, const uint32_t* tile_rows,
+                         const uint32_t* tiles_touched, void* ws, size_t ws_bytes,
+                         int64_t pair_capacity,
+                         uint64_t* sorted_keys, uint32_t* sorted_ids,
+                         uint32_t* tile_ranges, uint32_t* num_pairs_dev,
+                         int64_t* num_pairs_host, void* stream);
+
 /* ---------------------------------------------------------------------------
  * dass_bin_sort_views — dass_bin_sort for V views of one timestep at once
  * (a3-a5 batched over the views of P:74; A03, A04).  All cameras share W×H

@@ -210,11 +210,12 @@ int dass_bin_sort_workspace(int32_t n, int32_t num_tiles, int64_t pair_capacity,
   return DASS_OK;
 }
 
-int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, const uint32_t* box,
-                  const uint32_t* tile_rows, const uint32_t* tiles_touched, void* ws,
-                  size_t ws_bytes, int64_t pair_capacity,
-                  uint64_t* sorted_keys, uint32_t* sorted_ids, uint32_t* tile_ranges,
-                  uint32_t* num_pairs_dev, int64_t* num_pairs_host, void* stream) {
+static int bin_sort_common(int pair_grid, const dass_camera* cam, int32_t n, const float* xy_depth,
+                           const uint32_t* box, const uint32_t* tile_rows,
+                           const uint32_t* tiles_touched, void* ws, size_t ws_bytes,
+                           int64_t pair_capacity, uint64_t* sorted_keys, uint32_t* sorted_ids,
+                           uint32_t* tile_ranges, uint32_t* num_pairs_dev,
+                           int64_t* num_pairs_host, void* stream) {
   int st = check_camera(cam);
   if (st) return st;
   // the onesweep look-back packs counts into 30 bits (binsort.cu)
@@ -234,7 +235,7 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, cons
   st = cuda_status(launch_binsort(cp, n, (const float4*)xy_depth, (const uint2*)box,
                                   (const uint4*)tile_rows, tiles_touched,
                                   ws, pair_capacity, sorted_keys, sorted_ids, (uint2*)tile_ranges,
-                                  num_pairs_dev, s),
+                                  num_pairs_dev, pair_grid, s),
                    "dass_bin_sort");
   if (st || num_pairs_host == nullptr) return st;
   uint32_t h[2];
@@ -251,6 +252,27 @@ int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, cons
     return DASS_ERR_CAPACITY;
   }
   return DASS_OK;
+}
+
+int dass_bin_sort(const dass_camera* cam, int32_t n, const float* xy_depth, const uint32_t* box,
+                  const uint32_t* tile_rows, const uint32_t* tiles_touched, void* ws,
+                  size_t ws_bytes, int64_t pair_capacity,
+                  uint64_t* sorted_keys, uint32_t* sorted_ids, uint32_t* tile_ranges,
+                  uint32_t* num_pairs_dev, int64_t* num_pairs_host, void* stream) {
+  return bin_sort_common(0, cam, n, xy_depth, box, tile_rows, tiles_touched, ws, ws_bytes,
+                         pair_capacity, sorted_keys, sorted_ids, tile_ranges, num_pairs_dev,
+                         num_pairs_host, stream);
+}
+
+int dass_bin_sort_shared(const dass_camera* cam, int32_t n, const float* xy_depth,
+                         const uint32_t* box, const uint32_t* tile_rows,
+                         const uint32_t* tiles_touched, void* ws, size_t ws_bytes,
+                         int64_t pair_capacity, uint64_t* sorted_keys, uint32_t* sorted_ids,
+                         uint32_t* tile_ranges, uint32_t* num_pairs_dev,
+                         int64_t* num_pairs_host, void* stream) {
+  return bin_sort_common(BINSORT_SHARED_GRID, cam, n, xy_depth, box, tile_rows, tiles_touched, ws,
+                         ws_bytes, pair_capacity, sorted_keys, sorted_ids, tile_ranges,
+                         num_pairs_dev, num_pairs_host, stream);
 }
 
 int dass_bin_sort_views_workspace(int32_t num_views, int32_t n, int64_t view_capacity,

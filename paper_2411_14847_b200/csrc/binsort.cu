@@ -152,97 +152,101 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
   const int warp = t >> 5;
   const uint32_t lane = lane_id();
   const int n = n_static >= 0 ? n_static : (n_dev[1] ? 0 : (int)n_dev[0]);
-  // blocks past the end (the pair passes launch for the capacity, K is on the
-  // device) leave right after their claim, before touching shared memory
-  if (t == 0) s_blk = atomicAdd(counter, 1u);
-  __syncthreads();
-  const uint32_t blk = s_blk;
-  const long long base = (long long)blk * (SORT_THREADS * IPT);
-  if (base >= n) return;
-  for (int k = t; k < (SORT_THREADS / 32) * RADIX; k += SORT_THREADS) (&s_whist[0][0])[k] = 0u;
-  __syncthreads();
+  // Each block claims key tiles in order until they run out: the pair passes launch for the
+  // capacity or on a fixed grid (K is on the device), so a block past the end leaves right after
+  // its claim, before touching shared memory.
+  for (;;) {
+    if (t == 0) s_blk = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t blk = s_blk;
+    const long long base = (long long)blk * (SORT_THREADS * IPT);
+    if (base >= n) return;
+    for (int k = t; k < (SORT_THREADS / 32) * RADIX; k += SORT_THREADS) (&s_whist[0][0])[k] = 0u;
+    __syncthreads();
 
-  KT keys[IPT];
-  uint32_t digit[IPT];
-  uint32_t rank[IPT];
-  const long long wbase = base + warp * (IPT * 32);
+    KT keys[IPT];
+    uint32_t digit[IPT];
+    uint32_t rank[IPT];
+    const long long wbase = base + warp * (IPT * 32);
 #pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    const long long idx = wbase + j * 32 + lane;
-    if (idx < n) {
-      keys[j] = in[idx];
-      digit[j] = (uint32_t)(keys[j] >> shift) & 255u;
-    } else {
-      keys[j] = 0;
-      digit[j] = 256u;  // invalid: ranks only among invalid lanes, never scattered
-    }
-  }
-  const uint32_t lt_mask = (1u << lane) - 1u;
-#pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    const uint32_t d = digit[j];
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    uint32_t pre = 0u;
-    if (d < 256u) pre = s_whist[warp][d];
-    __syncwarp();
-    if (d < 256u) {
-      rank[j] = pre + __popc(peers & lt_mask);
-      const uint32_t leader = 31u - __clz(peers);
-      if (lane == leader) s_whist[warp][d] = (uint16_t)(pre + __popc(peers));
-    }
-    __syncwarp();
-  }
-  __syncthreads();
-  // per digit: exclusive scan over warps, block count
-  uint32_t count = 0u;
-#pragma unroll
-  for (int w = 0; w < SORT_THREADS / 32; ++w) {
-    const uint32_t c = s_whist[w][t];
-    s_whist[w][t] = (uint16_t)count;
-    count += c;
-  }
-  // exclusive scan of the global histogram over digits (digit = t)
-  const uint32_t hv = hist[t];
-  uint32_t incl = hv;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if ((int)lane >= o) incl += y;
-  }
-  if (lane == 31) s_wsum[warp] = incl;
-  // decoupled look-back for digit t
-  uint32_t excl = 0u;
-  uint32_t* my = status + (size_t)blk * RADIX + t;
-  if (blk == 0) {
-    st_relaxed(my, FLAG_INC | count);
-  } else {
-    st_relaxed(my, FLAG_AGG | count);
-    long long j = (long long)blk - 1;
-    while (true) {
-      const uint32_t v = ld_relaxed(status + (size_t)j * RADIX + t);
-      const uint32_t f = v & ~VAL_MASK;
-      if (f == 0u) {  // predecessor not published yet: back off, do not burn issue slots
-        __nanosleep(SPIN_NS);
-        continue;
+    for (int j = 0; j < IPT; ++j) {
+      const long long idx = wbase + j * 32 + lane;
+      if (idx < n) {
+        keys[j] = in[idx];
+        digit[j] = (uint32_t)(keys[j] >> shift) & 255u;
+      } else {
+        keys[j] = 0;
+        digit[j] = 256u;  // invalid: ranks only among invalid lanes, never scattered
       }
-      excl += v & VAL_MASK;
-      if (f == FLAG_INC) break;
-      --j;
     }
-    st_relaxed(my, FLAG_INC | (excl + count));
-  }
-  __syncthreads();
-  uint32_t gofs = incl - hv;
-  for (int w = 0; w < warp; ++w) gofs += s_wsum[w];
-  s_gbase[t] = gofs + excl;
-  __syncthreads();
+    const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    const uint32_t d = digit[j];
-    if (d < 256u) {
-      DASS_CHECK((long long)(s_gbase[d] + s_whist[warp][d] + rank[j]) < (long long)n);
-      out[s_gbase[d] + s_whist[warp][d] + rank[j]] = keys[j];
+    for (int j = 0; j < IPT; ++j) {
+      const uint32_t d = digit[j];
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      uint32_t pre = 0u;
+      if (d < 256u) pre = s_whist[warp][d];
+      __syncwarp();
+      if (d < 256u) {
+        rank[j] = pre + __popc(peers & lt_mask);
+        const uint32_t leader = 31u - __clz(peers);
+        if (lane == leader) s_whist[warp][d] = (uint16_t)(pre + __popc(peers));
+      }
+      __syncwarp();
     }
+    __syncthreads();
+    // per digit: exclusive scan over warps, block count
+    uint32_t count = 0u;
+#pragma unroll
+    for (int w = 0; w < SORT_THREADS / 32; ++w) {
+      const uint32_t c = s_whist[w][t];
+      s_whist[w][t] = (uint16_t)count;
+      count += c;
+    }
+    // exclusive scan of the global histogram over digits (digit = t)
+    const uint32_t hv = hist[t];
+    uint32_t incl = hv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    // decoupled look-back for digit t
+    uint32_t excl = 0u;
+    uint32_t* my = status + (size_t)blk * RADIX + t;
+    if (blk == 0) {
+      st_relaxed(my, FLAG_INC | count);
+    } else {
+      st_relaxed(my, FLAG_AGG | count);
+      long long j = (long long)blk - 1;
+      while (true) {
+        const uint32_t v = ld_relaxed(status + (size_t)j * RADIX + t);
+        const uint32_t f = v & ~VAL_MASK;
+        if (f == 0u) {  // predecessor not published yet: back off, do not burn issue slots
+          __nanosleep(SPIN_NS);
+          continue;
+        }
+        excl += v & VAL_MASK;
+        if (f == FLAG_INC) break;
+        --j;
+      }
+      st_relaxed(my, FLAG_INC | (excl + count));
+    }
+    __syncthreads();
+    uint32_t gofs = incl - hv;
+    for (int w = 0; w < warp; ++w) gofs += s_wsum[w];
+    s_gbase[t] = gofs + excl;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const uint32_t d = digit[j];
+      if (d < 256u) {
+        DASS_CHECK((long long)(s_gbase[d] + s_whist[warp][d] + rank[j]) < (long long)n);
+        out[s_gbase[d] + s_whist[warp][d] + rank[j]] = keys[j];
+      }
+    }
+    __syncthreads();   // s_blk, s_whist, s_gbase are reused by the next claim
   }
 }
 
@@ -518,7 +522,7 @@ size_t binsort_workspace(int n, int num_tiles, int64_t capacity) {
 cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, const uint2* box,
                            const uint4* rows, const uint32_t* tiles, void* ws_ptr, int64_t capacity,
                            uint64_t* sorted_keys, uint32_t* sorted_ids, uint2* ranges,
-                           uint32_t* num_pairs_dev, cudaStream_t s) {
+                           uint32_t* num_pairs_dev, int pair_grid, cudaStream_t s) {
   const int num_tiles = cam.tiles_x * cam.tiles_y;
   WS w = carve(ws_ptr, n, capacity);
   cudaError_t e;
@@ -560,7 +564,11 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   launch_counted();
   uint64_t* pa = w.pkeysA;
   uint64_t* pb = w.pkeysB;
-  const int grid_cap = (int)nblk_cap;
+  // K ≤ capacity is known on the device only, so the pair passes launch for the capacity:
+  // pair_grid = 0, one block per capacity tile (most leave empty; the fastest alone);
+  // pair_grid > 0, that many blocks, each looping over key tiles — fewer resident blocks
+  // next to the other views' kernels (dass_bin_sort_shared)
+  const int grid_cap = pair_grid <= 0 || (int)nblk_cap < pair_grid ? (int)nblk_cap : pair_grid;
   for (int p = 0; p < npass; ++p) {
     if ((e = launch_pdl(onesweep_kernel<uint64_t, SORT_IPT>, grid_cap, SORT_THREADS, s, pa, pb, -1,
                         num_pairs_dev, w.hist + (4 + p) * RADIX,

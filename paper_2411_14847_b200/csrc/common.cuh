@@ -164,7 +164,9 @@ size_t binsort_workspace(int n, int num_tiles, int64_t capacity);
 cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, const uint2* box,
                            const uint4* rows, const uint32_t* tiles, void* ws, int64_t capacity,
                            uint64_t* sorted_keys, uint32_t* sorted_ids, uint2* ranges,
-                           uint32_t* num_pairs_dev, cudaStream_t s);
+                           uint32_t* num_pairs_dev, int pair_grid, cudaStream_t s);
+// dass_bin_sort_shared's pair-pass grid (blocks that loop over the key tiles)
+constexpr int BINSORT_SHARED_GRID = 74;
 size_t render_accept_workspace(int ntiles, int64_t capacity);
 cudaError_t launch_render_fwd(const CamParams& cam, const uint2* ranges, const uint32_t* ids,
                               const float4* xy_depth, const float4* conic_opa, const float4* rgb,

@@ -38,7 +38,7 @@ EXPORTS = (
     "dass_render_bwd_preprocess_views_uv", "dass_render_bwd_preprocess_views_part",
     "dass_gradstat_from_uv", "dass_timestamp",
     "dass_scan_nonfinite",
-    "dass_bin_sort_views_workspace", "dass_bin_sort_views",
+    "dass_bin_sort_views_workspace", "dass_bin_sort_views", "dass_bin_sort_shared",
 )
 
 
@@ -112,6 +112,7 @@ def lib():
         L.dass_project_views_part.argtypes = [i32, P, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P]
         L.dass_bin_sort_workspace.argtypes = [i32, i32, i64, P]
         L.dass_bin_sort.argtypes = [P, i32, P, P, P, P, P, C.c_size_t, i64, P, P, P, P, P, P]
+        L.dass_bin_sort_shared.argtypes = L.dass_bin_sort.argtypes
         L.dass_bin_sort_views_workspace.argtypes = [i32, i32, i64, P]
         L.dass_bin_sort_views.argtypes = [P, i32, i32, P, P, P, P, P, C.c_size_t, i64, P, P, P, P]
         L.dass_render_accept_workspace.argtypes = [i32, i64, P]
@@ -261,17 +262,20 @@ def dass_bin_sort_workspace(n, num_tiles, pair_capacity) -> int:
 
 
 def dass_bin_sort(cam, n, xy_depth, box, tile_rows, tiles_touched, ws, pair_capacity, sorted_keys,
-                  sorted_ids, tile_ranges, num_pairs_dev, host_mode=False, stream=None):
-    """Returns K in host mode (raises DassError(CAPACITY) on overflow), else None."""
+                  sorted_ids, tile_ranges, num_pairs_dev, host_mode=False, stream=None,
+                  shared=False):
+    """Returns K in host mode (raises DassError(CAPACITY) on overflow), else None.
+    shared=True calls dass_bin_sort_shared (a view sorted next to other views' work)."""
     c = _cam(cam)
     k = C.c_int64(-1)
-    st = lib().dass_bin_sort(C.byref(c), n, _ptr(xy_depth), _ptr(box), _ptr(tile_rows),
-                             _ptr(tiles_touched),
-                             _ptr(ws), ws.numel() * ws.element_size(), pair_capacity,
-                             _ptr(sorted_keys), _ptr(sorted_ids), _ptr(tile_ranges),
-                             _ptr(num_pairs_dev), C.byref(k) if host_mode else None,
-                             _stream(stream))
-    _check(st, "dass_bin_sort")
+    fn = lib().dass_bin_sort_shared if shared else lib().dass_bin_sort
+    st = fn(C.byref(c), n, _ptr(xy_depth), _ptr(box), _ptr(tile_rows),
+            _ptr(tiles_touched),
+            _ptr(ws), ws.numel() * ws.element_size(), pair_capacity,
+            _ptr(sorted_keys), _ptr(sorted_ids), _ptr(tile_ranges),
+            _ptr(num_pairs_dev), C.byref(k) if host_mode else None,
+            _stream(stream))
+    _check(st, "dass_bin_sort_shared" if shared else "dass_bin_sort")
     return k.value if host_mode else None
 
 

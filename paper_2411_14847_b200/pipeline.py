@@ -113,13 +113,14 @@ class Raster:
             ab = dass.dass_render_accept_workspace(self.num_tiles, capacity)
             self.accept = torch.empty(ab // 4, dtype=torch.int32, device=device)
 
-    def sort(self, cam, rec, host_mode=False, sorted_keys=None, num_pairs=None):
-        """num_pairs: where (K, overflow flag) go (default: this slot's own pair)."""
+    def sort(self, cam, rec, host_mode=False, sorted_keys=None, num_pairs=None, shared=False):
+        """num_pairs: where (K, overflow flag) go (default: this slot's own pair);
+        shared: dass_bin_sort_shared (other views' kernels run next to this sort)."""
         xy, co, rgb, box, rows, tt = rec
         return dass.dass_bin_sort(cam, self.n, xy, box, rows, tt, self.sort_ws, self.capacity,
                                   sorted_keys, self.sorted_ids, self.ranges,
                                   self.num_pairs if num_pairs is None else num_pairs,
-                                  host_mode=host_mode)
+                                  host_mode=host_mode, shared=shared)
 
     def render(self, cam, rec, bg=None, tiles=None, ranges=None, sorted_ids=None):
         """ranges/sorted_ids: a view's slices of a batched dass_bin_sort_views (else
@@ -340,6 +341,9 @@ class MultiViewPass:
             if self.stamps is not None:
                 dass.dass_timestamp(self.stamps, 4 * v + i, q)
 
+        # several views sorting at once on their own streams: the shared-GPU sort variant
+        shared = self.S > 1
+
         def part_sort(v):
             k, ras, st = slot(v)
             cam, rec = self.cams[v], records.view(v)
@@ -352,12 +356,12 @@ class MultiViewPass:
                 ss = self.sort_streams[v % len(self.sort_streams)]
                 ss.wait_stream(st)    # projected, and the slot's previous view is done
                 with torch.cuda.stream(ss):
-                    ras.sort(cam, rec, num_pairs=self.num_pairs[v])
+                    ras.sort(cam, rec, num_pairs=self.num_pairs[v], shared=shared)
                 st.wait_stream(ss)
             with torch.cuda.stream(st):
                 stamp(v, 0, st)
                 if self.sort_streams is None and not self.batch_sort:
-                    ras.sort(cam, rec, num_pairs=self.num_pairs[v])
+                    ras.sort(cam, rec, num_pairs=self.num_pairs[v], shared=shared)
 
         def part_fwd(v):
             k, ras, st = slot(v)

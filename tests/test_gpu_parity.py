@@ -589,3 +589,46 @@ def test_sort_many_tiles_bit_exact(W, H, n):
     out = run_view(cam, sc, capacity=1 << 22)
     assert out["K"] > n
     check_binsort(cam, out, gpu_projection(out["rec"]))
+
+
+@pytest.mark.parametrize("case", ["c3_view", "dense_tiles", "overflow"])
+def test_bin_sort_shared_equals_bin_sort(case):
+    """dass_bin_sort_shared (the fixed, looping pair-pass grid the multi-view step uses)
+    gives bit for bit dass_bin_sort's keys, ids, ranges and (K, overflow): a C3-size view
+    (~1.3M pairs, hundreds of key tiles per block), a dense-tile scene with tile lists past
+    4096 pairs, and a capacity overflow (graph mode: flag set, every range empty)."""
+    if case == "dense_tiles":
+        cam = synth.tiny_camera(48, 48)
+        sc = synth.random_scene(40000, cam, seed=78)
+        g = np.random.default_rng(78)
+        z = sc.pos_opa[:, 2]
+        sc.pos_opa[:, 0] = (g.uniform(-5, 5, sc.n) * z / cam.fx).astype(np.float32)
+        sc.pos_opa[:, 1] = (g.uniform(-5, 5, sc.n) * z / cam.fy).astype(np.float32)
+        sc.scale[:, :3] = (np.abs(sc.scale[:, :3]) * 0.3).astype(np.float32)
+        sc.pos_opa[:10000, 2] = 3.0
+    else:
+        cams, sc = synth.c3()
+        cam = cams[3]
+    cap = 1 << 16 if case == "overflow" else 1 << 22
+    ds = DeviceScene.from_host(sc, DEV)
+    rec = ViewRecords(1, sc.n, DEV)
+    dass.dass_project(cam, sc.sh_degree, ds.pos_opa, ds.scale, ds.rot, ds.sh, None,
+                      rec.xy_depth[0], rec.conic_opa[0], rec.rgb[0], rec.box[0], rec.rows[0], rec.tiles[0])
+    out = []
+    for shared in (False, True):
+        ras = Raster(cam.width, cam.height, sc.n, cap, DEV)
+        keys = torch.zeros(cap, dtype=torch.int64, device=DEV)
+        ras.sorted_ids.fill_(-1)
+        ras.ranges.fill_(-1)
+        ras.sort(cam, rec.view(0), sorted_keys=keys, shared=shared)
+        torch.cuda.synchronize()
+        out.append((np_(ras.num_pairs), np_(keys), np_(ras.sorted_ids), np_(ras.ranges)))
+    (na, ka, ia, ra), (nb, kb, ib, rb) = out
+    assert np.array_equal(na, nb)
+    assert np.array_equal(ra, rb)
+    if case == "overflow":
+        assert na[1] == 1 and na[0] > cap and not ra.any()
+        return
+    K = int(na[0])
+    assert na[1] == 0 and K > (100000 if case == "c3_view" else 4096)
+    assert np.array_equal(ka[:K], kb[:K]) and np.array_equal(ia[:K], ib[:K])
