@@ -341,8 +341,10 @@ class MultiViewPass:
             if self.stamps is not None:
                 dass.dass_timestamp(self.stamps, 4 * v + i, q)
 
-        # several views sorting at once on their own streams: the shared-GPU sort variant
-        shared = self.S > 1
+        # many views sorting at once on their own streams: the shared-GPU sort variant (its
+        # 74-block pair passes need the other views to fill the GPU: with the 2-3 views of an
+        # 8-GPU rank it is slower, 1.68 -> 1.77 ms per step)
+        shared = self.S >= 8
 
         def part_sort(v):
             k, ras, st = slot(v)

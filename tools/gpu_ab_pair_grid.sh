@@ -1,6 +1,7 @@
 # Pair passes on a fixed looping grid: interleaved A/B/C of tools/ab libraries built with different
 # pair grids (blocks/SM then PAIR_GRID blocks; first run: A = one block per capacity tile, B = 4/SM, C = 2/SM;
-# second: A = 2/SM, B = 1/SM, C = 3/SM; third: A = 148, B = 74, C = 104 blocks).
+# second: A = 2/SM, B = 1/SM, C = 3/SM; third: A = 148, B = 74, C = 104 blocks; fourth, with 74: A = HEAD,
+# B = finalize on 148 blocks in the shared sort, C = finalize and emission on 148).
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 TAG=${1:-pg}
 for v in B C; do
