@@ -139,7 +139,7 @@ template <typename KT = uint64_t, int IPT = SORT_IPT>
 __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     const KT* __restrict__ in, KT* __restrict__ out, int n_static,
     const uint32_t* __restrict__ n_dev, const uint32_t* __restrict__ hist, uint32_t* status,
-    uint32_t* counter, int shift) {
+    uint32_t* counter, int shift, int loop) {
   // per-warp digit counts, then per-warp exclusive offsets: ≤ 256·IPT, so 16 bits
   // (4 KB instead of 8: a smaller footprint next to the raster CTAs of other views)
   __shared__ uint16_t s_whist[SORT_THREADS / 32][RADIX];
@@ -246,6 +246,9 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
         out[s_gbase[d] + s_whist[warp][d] + rank[j]] = keys[j];
       }
     }
+    // a grid of one block per key tile stops here (a second claim per block would queue
+    // one more atomic per block on the shared counter)
+    if (!loop) return;
     __syncthreads();   // s_blk, s_whist, s_gbase are reused by the next claim
   }
 }
@@ -551,7 +554,7 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   for (int p = 0; p < 4; ++p) {
     if ((e = launch_pdl(onesweep_kernel<uint64_t, PRESORT_IPT>, nblk_n, SORT_THREADS, s, a, b, n,
                         (const uint32_t*)nullptr, w.hist + p * RADIX,
-                        w.dstatus + (size_t)p * nblk_n * RADIX, w.counters + p, 32 + 8 * p))) return e;
+                        w.dstatus + (size_t)p * nblk_n * RADIX, w.counters + p, 32 + 8 * p, 0))) return e;
     launch_counted();
     uint64_t* tmp = a; a = b; b = tmp;
   }
@@ -572,7 +575,8 @@ cudaError_t launch_binsort(const CamParams& cam, int n, const float4* xy_depth, 
   for (int p = 0; p < npass; ++p) {
     if ((e = launch_pdl(onesweep_kernel<uint64_t, SORT_IPT>, grid_cap, SORT_THREADS, s, pa, pb, -1,
                         num_pairs_dev, w.hist + (4 + p) * RADIX,
-                        w.pstatus + (size_t)p * nblk_cap * RADIX, w.counters + 5 + p, 32 + 8 * p))) return e;
+                        w.pstatus + (size_t)p * nblk_cap * RADIX, w.counters + 5 + p, 32 + 8 * p,
+                        grid_cap < (int)nblk_cap ? 1 : 0))) return e;
     launch_counted();
     uint64_t* tmp = pa; pa = pb; pb = tmp;
   }
@@ -622,7 +626,7 @@ cudaError_t launch_binsort_views(const CamParams& cam, int V, int n, const float
   for (int p = 0; p < 4; ++p) {
     onesweep_kernel<uint64_t, PRESORT_IPT><<<nblk_n, SORT_THREADS, 0, s>>>(a, b, nn, nullptr, w.hist + p * RADIX,
                                                     w.dstatus + (size_t)p * nblk_n * RADIX,
-                                                    w.counters + p, 32 + 8 * p);
+                                                    w.counters + p, 32 + 8 * p, 0);
     launch_counted();
     uint64_t* tmp = a; a = b; b = tmp;
   }
@@ -637,7 +641,7 @@ cudaError_t launch_binsort_views(const CamParams& cam, int V, int n, const float
   for (int p = 0; p < npass; ++p) {
     onesweep_kernel<uint64_t><<<(int)nblk_cap, SORT_THREADS, 0, s>>>(pa, pb, -1, kg, w.hist + (4 + p) * RADIX,
                                                            w.pstatus + (size_t)p * nblk_cap * RADIX,
-                                                           w.counters + 5 + p, 32 + 8 * p);
+                                                           w.counters + 5 + p, 32 + 8 * p, 0);
     launch_counted();
     uint64_t* tmp = pa; pa = pb; pb = tmp;
   }
