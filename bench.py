@@ -100,6 +100,8 @@ def parse():
     p.add_argument("--batch-sort", action="store_true", help="A/B: PassOptions.batch_sort")
     p.add_argument("--sort-batch-chunks", type=int, default=4, help="A/B: PassOptions.sort_batch_chunks")
     p.add_argument("--pre-chunks", type=int, default=1, help="A/B: PassOptions.pre_chunks")
+    p.add_argument("--shared-sort-min-views", type=int, default=8,
+                   help="A/B: PassOptions.shared_sort_min_views")
     p.add_argument("--proj-chunks", type=int, default=1, help="A/B: PassOptions.proj_chunks")
     p.add_argument("--no-split-preprocess", action="store_true",
                    help="A/B: PassOptions.split_preprocess=False (both preprocess parts on one stream)")
@@ -341,7 +343,8 @@ def run_ours(args):
                        sort_batch_chunks=args.sort_batch_chunks,
                        pre_chunks=args.pre_chunks, proj_chunks=args.proj_chunks,
                        split_project=not args.no_split_project,
-                       split_preprocess=not args.no_split_preprocess)
+                       split_preprocess=not args.no_split_preprocess,
+                       shared_sort_min_views=args.shared_sort_min_views)
     stepper = ShiftStep(my_cams, n, deg, args.capacity, dev, streams=args.streams,
                         tiles=plan.tiles, split=plan.split, num_split=plan.num_split,
                         shift=with_shift, options=opts)

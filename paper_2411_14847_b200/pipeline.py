@@ -183,7 +183,9 @@ class PassOptions:
       views' sorts; the sorts wait only for the keys part, the forwards for both.
     split_preprocess: the preprocess's SH-coefficient part on a side stream next to
       its geometry part (DASS_PREPROCESS_SH / _GEOMETRY).
-    stream_prio: the first half of the view streams at a higher priority."""
+    stream_prio: the first half of the view streams at a higher priority.
+    shared_sort_min_views: dass_bin_sort_shared from this many concurrent view streams on
+    (dass_bin_sort below)."""
     sort_chains: int = 0
     batch_sort: bool = False
     sort_batch_chunks: int = 4
@@ -192,6 +194,7 @@ class PassOptions:
     split_project: bool = True
     split_preprocess: bool = True
     stream_prio: bool = False
+    shared_sort_min_views: int = 8
 
 
 class MultiViewPass:
@@ -344,7 +347,7 @@ class MultiViewPass:
         # many views sorting at once on their own streams: the shared-GPU sort variant (its
         # 74-block pair passes need the other views to fill the GPU: with the 2-3 views of an
         # 8-GPU rank it is slower, 1.68 -> 1.77 ms per step)
-        shared = self.S >= 8
+        shared = self.S >= self.options.shared_sort_min_views
 
         def part_sort(v):
             k, ras, st = slot(v)
